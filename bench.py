@@ -1,0 +1,372 @@
+#!/usr/bin/env python3
+"""DHO2 steps/sec (+ Lanczos curvature-refresh ms) on B200 — BASELINE.json's metric.
+
+One "step" = one inner round of run_dho2 (trainer.cpp:233-242): C logical workers' gradients over b
+samples each, the gradient collective and the fused split update; every refresh_ese and ADMM
+w/dual update the schedule places inside the timed steps is included (a refresh every
+P * rounds_per_epoch = 10 steps on C4); epoch_end evaluation is excluded.
+
+Default workload: C4 (the north-star 100,989,962-parameter MLP 3072-3584x8-10, C=8 workers x
+b=1024, curvature batch 1024, k=32, m=80, AdamW) at N=1 — it fits one B200. Inputs are larger
+than L2 (basis 32.7 GB), so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c3|c2|c1] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DHO2 steps/sec and Lanczos curvature-refresh ms at 1/2/4/8 B200 vs host-CPU ref"
+
+CONFIGS = {
+    # SURVEY.md §8d
+    "c1": dict(sizes=[784, 256, 10], workers=1, b=128, curv=128, N=1280, k=10, m=0, base="adam", P=1),
+    "c2": dict(sizes=[784, 256, 10], workers=4, b=128, curv=128, N=5120, k=10, m=0, base="momentum", P=1),
+    "c3": dict(sizes=[3072, 2048, 2048, 10], workers=1, b=512, curv=512, N=5120, k=20, m=0, base="adamw", P=1),
+    "c4": dict(sizes=[3072] + [3584] * 8 + [10], workers=8, b=1024, curv=1024, N=81920, k=32, m=80, base="adamw",
+               P=1),
+}
+
+
+def mlp_dim(sizes):
+    return sum(sizes[t] * sizes[t + 1] + sizes[t + 1] for t in range(len(sizes) - 1))
+
+
+def hvp_flops(sizes, B):  # 2B * sum_t (5 + 3[t>0]) in_t out_t
+    return 2.0 * B * sum((5 + 3 * (t > 0)) * sizes[t] * sizes[t + 1] for t in range(len(sizes) - 1))
+
+
+def grad_flops(sizes, b):  # 2b * sum_t (2 + [t>0]) in_t out_t
+    return 2.0 * b * sum((2 + (t > 0)) * sizes[t] * sizes[t + 1] for t in range(len(sizes) - 1))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm=j.get("hbm_gbs", 6650.0), tf=j.get("bf16_tflops", 1590.0),
+                    tf_sus=j.get("bf16_tflops_sustained", 1410.0), src="measured")
+    return dict(hbm=6650.0, tf=1590.0, tf_sus=1410.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": float(rows[0][2]) if rows else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def cpu_reference_sample(cfgname, threads=None, reps=1):
+    """Times the UNMODIFIED reference (oracle/_ref/libdho2ref.so, -O2 -fopenmp) on bounded samples of the
+    workload and extrapolates one DHO2 step (gradient + split update + 1/(P*rounds) of a refresh).
+    Returns (steps_per_sec, refresh_ms, detail)."""
+    from oracle.bindings import CpuChecker, base_cfg, blobs_dataset, reference_available
+    kind = "reference" if reference_available() else "port"
+    R = CpuChecker(kind)
+    c = CONFIGS[cfgname]
+    sizes = c["sizes"]
+    n = mlp_dim(sizes)
+    T = R.max_threads()
+    Bs = 16 * T  # one 16-sample chunk per OpenMP thread (oracle.cpp:374-382)
+    X, y = blobs_dataset(Bs, sizes[0], sizes[-1], seed=7)
+    w = R.mlp_init(sizes, 1)
+    v = R.rng_normal(5, n)
+    t0 = time.perf_counter()
+    R.mlp_grad(sizes, w, X, y, sizes[-1])
+    t_grad = (time.perf_counter() - t0) / Bs
+    t0 = time.perf_counter()
+    R.mlp_hvp(sizes, w, v, X, y, sizes[-1])
+    t_hvp = (time.perf_counter() - t0) / Bs
+    del w, v
+    ns = min(n, 1 << 20)
+    m = c["m"] or R.lanczos_budget(c["k"], 0, n)
+    r = c["k"]
+    import numpy as np
+    D = np.asarray(R.rng_normal(3, ns * (m // 2 + 1))).reshape(m // 2 + 1, ns).T
+    h = R.rng_normal(4, ns)
+    t0 = time.perf_counter()
+    _project(R, D, h)
+    t_gs_mid = time.perf_counter() - t0  # one projection over m/2+1 active columns
+    V = np.asarray(R.rng_normal(6, ns * r)).reshape(r, ns).T
+    g = R.rng_normal(7, ns)[None, :]
+    t0 = time.perf_counter()
+    R.deltas_seq(base_cfg(c["base"]), np.linspace(1, 2, r), V, g, np.zeros(ns), 0.1, pi=np.zeros(ns), sigma=1e-2)
+    t_upd = (time.perf_counter() - t0) * n / ns
+    scale = n / ns
+    gs_refresh = t_gs_mid * scale * m  # sum_i (i+1) ~ m * (m/2+1)
+    refresh_s = m * t_hvp * c["curv"] + gs_refresh
+    step_s = t_grad * c["b"] * c["workers"] + t_upd
+    rounds = -(-(-(-c["N"] // c["workers"])) // c["b"])
+    per_step = step_s + refresh_s / (c["P"] * rounds)
+    sample = (f"{kind} lib, {T} OpenMP threads: grad+hvp on {Bs} samples (per-sample cost x {c['b'] * c['workers']} / "
+              f"{c['curv']}), project_out over {ns} rows x {m // 2 + 1} cols and admm_deltas({c['base']}) on {ns} rows, "
+              f"extrapolated linearly to n={n}, m={m}; refresh amortised over {c['P'] * rounds} steps")
+    return 1.0 / per_step, refresh_s * 1e3, dict(kind=kind, cores=T, sample=sample, t_grad_sample=t_grad,
+                                                 t_hvp_sample=t_hvp, t_update_step=t_upd, gs_refresh_s=gs_refresh)
+
+
+def _project(R, D, h):
+    import ctypes as C
+
+    import numpy as np
+    n, cols = D.shape
+    if R.kind == "reference":
+        lib = R.lib
+        lib.ref_project_out.argtypes = [C.c_size_t, C.c_size_t, C.POINTER(C.c_double), C.c_size_t,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        Dc = np.ascontiguousarray(D.T).reshape(-1)
+        out = np.empty(n)
+        dp = C.POINTER(C.c_double)
+        lib.ref_project_out(n, cols, Dc.ctypes.data_as(dp), cols, np.ascontiguousarray(h).ctypes.data_as(dp),
+                            out.ctypes.data_as(dp))
+        return out
+    return h - D @ (D.T @ h)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(min(os.cpu_count() or 1, 16)))
+    vals, rms = [], []
+    for s in range(args.warmup + args.steps):
+        v, rm, det = cpu_reference_sample(args.config)
+        if s >= args.warmup:
+            vals.append(v)
+            rms.append(rm)
+    value = sum(vals) / len(vals)
+    line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_json(args.config, world),
+            "refresh_ms": sum(rms) / len(rms),
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": det["cores"], "kind": det["kind"],
+                             "sample": det["sample"]},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(name, world):
+    c = CONFIGS[name]
+    return {"workload": f"{name.upper()}: MLP {'-'.join(map(str, c['sizes']))} (n={mlp_dim(c['sizes'])}), "
+                        f"C={c['workers']} workers x b={c['b']}, curvature batch {c['curv']}, k={c['k']}, "
+                        f"m={c['m'] or 'budget'}, {c['base']}, refresh every P*rounds steps",
+            "global_batch": c["workers"] * c["b"], "parallelism": f"dp{world} (rows sharded over {world} GPU)",
+            "l2": "inputs larger than L2 (no flush)" if name in ("c3", "c4") else "working set fits L2",
+            "dataset": f"blobs-{c['sizes'][0]} N={c['N']} (SURVEY §8d)"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, dist):
+    import numpy as np
+
+    import paper_2505_00982_b200 as d
+    c = CONFIGS[args.config]
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ctx = d.Context(local)
+    if world > 1:
+        nid = [d.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        ctx.comm_init(nid[0], rank, world)
+    X, y = d.blobs_dataset(c["N"], c["sizes"][0], c["sizes"][-1], seed=7)
+    mlp = d.MlpOracle(ctx, c["sizes"])
+    w0 = mlp.init_params(1)
+    cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig(c["base"]), k=c["k"], l=0, alpha=0.1, sigma=1e-2,
+                          outer_rounds=10**6, inner_epochs=c["P"], batch_size=c["b"], curvature_batch=c["curv"],
+                          seed=1, lanczos_m=c["m"])
+    data = d.Dataset(X, y, c["sizes"][-1], 7)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timed run (value)
+    tr = d.Trainer(ctx, cfg, mlp, data, w0, workers=c["workers"])
+    tr.step(args.warmup)
+    ctx.synchronize()
+    rounds = int(tr.stat("rounds_per_epoch"))
+    refreshes0, rms0 = tr.stat("refreshes"), tr.stat("refresh_ms_total")
+    ctx.set_option("ktimers_reset", 1)
+    ctx.set_option("ktimers", 1)
+    launches0 = ctx.stat("launches")
+    barrier()
+    ctx.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.mark(0)
+    for _ in range(args.steps):
+        tr.step(1)
+    ctx.mark(1)
+    ms = ctx.elapsed_ms(0, 1)
+    clocks = sampler.stop()
+    launches = ctx.stat("launches") - launches0
+    ctx.set_option("ktimers", 0)
+    kstats = ctx.kernel_stats()
+    ms = max_over_ranks(ms)
+    n_ref = tr.stat("refreshes") - refreshes0
+    refresh_ms = (tr.stat("refresh_ms_total") - rms0) / n_ref if n_ref else None
+    refresh_ms = max_over_ranks(refresh_ms) if refresh_ms is not None else None
+    tr.close()
+
+    # ---- end to end through the C ABI with the dataset in (pinned) host memory
+    e2e = None
+    if not args.no_e2e:
+        tr = d.Trainer(ctx, cfg, mlp, data, w0, workers=c["workers"], host_resident=True)
+        for _ in range(args.warmup):
+            tr.step(1)
+            tr.last_loss()
+        h0, d0 = tr.stat("h2d_bytes"), tr.stat("d2h_bytes")
+        barrier()
+        ctx.synchronize()
+        ctx.mark(2)
+        for _ in range(args.steps):
+            tr.step(1)
+            tr.last_loss()  # device -> host read of the step's result
+        ctx.mark(3)
+        ems = max_over_ranks(ctx.elapsed_ms(2, 3))
+        e2e = {"value": args.steps / (ems / 1e3), "unit": "steps/s",
+               "h2d_bytes_per_step": (tr.stat("h2d_bytes") - h0) / args.steps,
+               "d2h_bytes_per_step": (tr.stat("d2h_bytes") - d0) / args.steps,
+               "note": "dataset pinned in host memory; each step's batch (and each refresh's curvature batch) is "
+                       "gathered over PCIe by the packing kernel; per-step loss read back"}
+        tr.close()
+
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    value = args.steps / (ms / 1e3)
+    # dominant kernel -> roofline
+    kern = {}
+    for name, (kms, cnt, work) in kstats.items():
+        if cnt == 0 or kms <= 0:
+            continue
+        is_gemm = name.startswith("gemm3")
+        per = kms / cnt
+        ach = (work / cnt) / (per / 1e3) / (1e12 if is_gemm else 1e9)
+        peak = peaks["tf_sus"] if is_gemm else peaks["hbm"]
+        kern[name] = {"ms_total": round(kms, 3), "launches": int(cnt), "avg_us": round(per * 1e3, 2),
+                      "achieved": round(ach, 2), "unit": "TFLOP/s" if is_gemm else "GB/s",
+                      "frac": round(ach / peak, 4), "share_of_step": round(kms / ms, 4)}
+    dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
+    roof = None
+    if dom:
+        k = kern[dom]
+        is_gemm = dom.startswith("gemm3")
+        roof = {"kernel": dom, "bound": "tensor" if is_gemm else "hbm", "achieved": k["achieved"],
+                "peak": peaks["tf_sus"] if is_gemm else peaks["hbm"], "unit": k["unit"], "frac": k["frac"],
+                "peak_source": f"{peaks['src']} ({'bf16_tflops_sustained' if is_gemm else 'hbm_gbs'})",
+                "traffic": traffic_from_profiles(dom),
+                "work_def": ("useful split-BF16x3 GEMM flops 2*M*N*K per launch (tensor pipe issues 3x)"
+                             if is_gemm else "algorithmic bytes per launch (SURVEY §8d)")}
+        if is_gemm:
+            roof["issued_frac"] = round(3 * k["achieved"] / peaks["tf_sus"], 4)
+    line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (split-bf16x3 tensor-core GEMMs, fp64 reductions)",
+            "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
+            "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "kernels": kern,
+            "useful_tflops_per_step": (grad_flops(c["sizes"], c["b"] * c["workers"]) +
+                                       hvp_flops(c["sizes"], c["curv"]) * (c["m"] or 40) / (c["P"] * rounds)) / 1e12}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            v, rm, det = cpu_reference_sample(args.config)
+            line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": det["cores"], "kind": det["kind"],
+                                    "sample": det["sample"], "refresh_ms": rm}
+        except Exception as e:  # the baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def traffic_from_profiles(kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(kernel)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,790 @@
+// extern "C" boundary of libdho2gpu.so (include/dho2gpu.h). Every entry point converts internal
+// exceptions into a dho2g_status + thread-local message, mirroring the reference's exception
+// types (proj/include/dho2/errors.hpp:8-36).
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "internal.h"
+
+using namespace dho2g;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return DHO2G_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return DHO2G_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DHO2G_ARGUMENT;
+  }
+}
+
+void check_ctx(dho2g_ctx* c) {
+  if (!c) fail(DHO2G_ARGUMENT, "null context");
+  DHO2G_CUDA(cudaSetDevice(c->device));
+}
+
+std::vector<float> to_f32(const double* p, size_t n) {
+  std::vector<float> f(n);
+  for (size_t i = 0; i < n; ++i) f[i] = (float)p[i];
+  return f;
+}
+
+void upload(DevBuf<float>& buf, const double* p, size_t n, cudaStream_t s) {
+  buf.ensure(std::max<size_t>(n, 1));
+  if (!n) return;
+  const auto f = to_f32(p, n);
+  DHO2G_CUDA(cudaMemcpyAsync(buf.p, f.data(), n * sizeof(float), cudaMemcpyHostToDevice, s));
+  DHO2G_CUDA(cudaStreamSynchronize(s));  // host vector f goes out of scope
+}
+
+void download(const float* d, double* p, size_t n, cudaStream_t s) {
+  std::vector<float> f(n);
+  DHO2G_CUDA(cudaMemcpyAsync(f.data(), d, n * sizeof(float), cudaMemcpyDeviceToHost, s));
+  DHO2G_CUDA(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < n; ++i) p[i] = f[i];
+}
+
+// oracle.cpp:326-343
+void check_batch(const dho2g_mlp* m, size_t B, size_t ncls) {
+  if (B == 0) fail(DHO2G_ARGUMENT, "mlp oracle: empty batch");
+  const size_t out = m->sizes.back();
+  if (m->loss == 0) {
+    if (ncls == 0 || ncls != out) fail(DHO2G_ARGUMENT, "mlp oracle: softmax_ce needs n_classes == output layer size");
+  } else if (ncls > 0) {
+    if (ncls != out) fail(DHO2G_ARGUMENT, "mlp oracle: mse one-hot targets need n_classes == output layer size");
+  } else if (out != 1) {
+    fail(DHO2G_ARGUMENT, "mlp oracle: regression targets need output layer size 1");
+  }
+}
+
+uint64_t splitmix_at(uint64_t s0, uint64_t i) {
+  uint64_t z = s0 + (i + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// normal number i of Rng(s0) (rng.hpp:37-50): pair p = i/2, cos for even i, sin (spare) for odd i
+double normal_at(uint64_t s0, uint64_t i) {
+  const uint64_t p = i >> 1;
+  const double u1 = (static_cast<double>(splitmix_at(s0, 2 * p) >> 11) + 1.0) * 0x1.0p-53;
+  const double u2 = static_cast<double>(splitmix_at(s0, 2 * p + 1) >> 11) * 0x1.0p-53;
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * 3.141592653589793 * u2;
+  return (i & 1) ? radius * std::sin(angle) : radius * std::cos(angle);
+}
+}  // namespace
+
+extern "C" {
+
+const char* dho2g_last_error(void) { return g_err.c_str(); }
+
+int dho2g_ctx_create(int device, dho2g_ctx** out) {
+  return guard([&] {
+    auto c = std::make_unique<dho2g_ctx>();
+    c->device = device;
+    DHO2G_CUDA(cudaSetDevice(device));
+    DHO2G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    DHO2G_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    int major = 0, minor = 0;
+    DHO2G_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    DHO2G_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (major != 10) fail(DHO2G_CUDA, "libdho2gpu is built for sm_100a (B200); device is sm_" +
+                                          std::to_string(major) + std::to_string(minor));
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    DHO2G_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled unavailable");
+    c->encode_fn = fn;
+    *out = c.release();
+  });
+}
+
+int dho2g_ctx_destroy(dho2g_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) dho2g::nccl().CommDestroy(ctx->comm);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
+  return guard([&] {
+    check_ctx(ctx);
+    const std::string k = key ? key : "";
+    if (k == "gemm") ctx->gemm_backend = (int)value;
+    else if (k == "graphs") ctx->use_graphs = (int)value;
+    else if (k == "ktimers") {
+      ctx->kt_flush();
+      ctx->ktimers = value != 0.0;
+    } else if (k == "ktimers_reset") {
+      ctx->kt_flush();
+      ctx->kstats.clear();
+    }
+    else fail(DHO2G_ARGUMENT, "unknown option '" + k + "'");
+  });
+}
+
+int dho2g_ctx_get_stat(dho2g_ctx* ctx, const char* key, double* value) {
+  return guard([&] {
+    if (!ctx) fail(DHO2G_ARGUMENT, "null context");
+    const std::string k = key ? key : "";
+    if (k.rfind("kt.", 0) == 0) {  // kt.<kernel>.ms | .count | .work
+      ctx->kt_flush();
+      const size_t dot = k.rfind('.');
+      const std::string name = k.substr(3, dot - 3), field = k.substr(dot + 1);
+      auto it = ctx->kstats.find(name);
+      if (it == ctx->kstats.end()) *value = 0.0;
+      else *value = field == "ms" ? it->second.ms : field == "count" ? it->second.count : it->second.work;
+      return;
+    }
+    if (k == "kt_names") {  // number of timed kernels; names via dho2g_ctx_kernel_name
+      ctx->kt_flush();
+      *value = (double)ctx->kstats.size();
+      return;
+    }
+    if (k == "launches") *value = (double)g_launches;
+    else if (k == "sm_count") *value = ctx->sm_count;
+    else if (k == "world") *value = ctx->world;
+    else if (k == "rank") *value = ctx->rank;
+    else {
+      auto it = ctx->stats.find(k);
+      *value = it == ctx->stats.end() ? 0.0 : it->second;
+    }
+  });
+}
+
+int dho2g_ctx_kernel_name(dho2g_ctx* ctx, int i, char* buf, size_t len) {
+  return guard([&] {
+    ctx->kt_flush();
+    if (i < 0 || (size_t)i >= ctx->kstats.size()) fail(DHO2G_ARGUMENT, "kernel index out of range");
+    auto it = ctx->kstats.begin();
+    std::advance(it, i);
+    std::snprintf(buf, len, "%s", it->first.c_str());
+  });
+}
+
+int dho2g_timer_mark(dho2g_ctx* ctx, int id) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (id < 0 || id > 1023) fail(DHO2G_ARGUMENT, "timer id out of range");
+    while ((int)ctx->marks.size() <= id) {
+      cudaEvent_t e;
+      DHO2G_CUDA(cudaEventCreate(&e));
+      ctx->marks.push_back(e);
+    }
+    DHO2G_CUDA(cudaEventRecord(ctx->marks[id], ctx->stream));
+  });
+}
+
+int dho2g_timer_ms(dho2g_ctx* ctx, int id0, int id1, double* ms) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (id0 < 0 || id1 < 0 || id0 >= (int)ctx->marks.size() || id1 >= (int)ctx->marks.size())
+      fail(DHO2G_ARGUMENT, "timer id not marked");
+    DHO2G_CUDA(cudaEventSynchronize(ctx->marks[id1]));
+    float f = 0.f;
+    DHO2G_CUDA(cudaEventElapsedTime(&f, ctx->marks[id0], ctx->marks[id1]));
+    *ms = f;
+  });
+}
+
+int dho2g_synchronize(dho2g_ctx* ctx) {
+  return guard([&] {
+    check_ctx(ctx);
+    ctx->sync();
+  });
+}
+
+int dho2g_nccl_unique_id(void* id_out_128) {
+  return guard([&] {
+    ncclUniqueId id;
+    DHO2G_NCCLCHK(dho2g::nccl().GetUniqueId(&id));
+    std::memcpy(id_out_128, &id, sizeof(id));
+  });
+}
+
+int dho2g_comm_init(dho2g_ctx* ctx, const void* nccl_id_128, int rank, int world) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (world < 1 || rank < 0 || rank >= world) fail(DHO2G_ARGUMENT, "Shard: rank out of range");
+    ctx->rank = rank;
+    ctx->world = world;
+    if (world == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id_128, sizeof(id));
+    DHO2G_NCCLCHK(dho2g::nccl().CommInitRank(&ctx->comm, world, id, rank));
+  });
+}
+
+int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world) {
+  return guard([&] {
+    if (!ctx) fail(DHO2G_ARGUMENT, "null context");
+    *rank = ctx->rank;
+    *world = ctx->world;
+  });
+}
+
+// ------------------------------------------------------------------ host bookkeeping
+void dho2g_rng_u64(uint64_t seed, size_t n, uint64_t* out) {
+  Rng r(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+void dho2g_rng_normal(uint64_t seed, size_t n, double* out) {
+  Rng r(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+void dho2g_shuffle_iota(uint64_t seed, size_t n, uint64_t* out) { shuffle_iota(seed, n, out); }
+uint64_t dho2g_mix_seed(uint64_t seed, uint64_t salt) {  // trainer.cpp:41-46
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+int dho2g_shard(size_t n, int world, int rank, size_t* begin, size_t* end) {
+  return guard([&] { shard_range(n, world, rank, begin, end); });
+}
+int dho2g_lanczos_budget(size_t k, size_t l, size_t n, size_t* m) {
+  return guard([&] { *m = lanczos_budget(k, l, n); });
+}
+void dho2g_epoch_permutation(size_t N, uint64_t shuffle_seed, uint64_t epoch, uint64_t* out) {
+  shuffle_iota(shuffle_seed * 0x9e3779b97f4a7c15ULL + epoch + 1, N, out);
+}
+void dho2g_curvature_indices(size_t N, size_t want, uint64_t seed, uint64_t refresh, uint64_t* out) {
+  std::vector<uint64_t> all(N);
+  shuffle_iota(dho2g_mix_seed(seed, 0xc0ffee + refresh), N, all.data());
+  std::copy(all.begin(), all.begin() + std::min(want, N), out);
+}
+int dho2g_batch_indices(const uint64_t* perm, size_t N, int workers, int worker, size_t round, size_t batch,
+                        uint64_t* out) {
+  return guard([&] {
+    size_t sb, se;
+    shard_range(N, workers, worker, &sb, &se);
+    const size_t len = se - sb;
+    if (len == 0) fail(DHO2G_ARGUMENT, "train: fewer samples than workers");
+    for (size_t j = 0; j < batch; ++j) out[j] = perm[sb + (round * batch + j) % len];
+  });
+}
+void dho2g_blobs_dataset(size_t N, size_t D, size_t n_classes, uint64_t seed, double* X, double* y) {
+  const uint64_t s0 = seed * 0x2545F4914F6CDD1DULL + 0xB10B5ULL;
+  const size_t nmu = n_classes * D;
+  std::vector<double> mu(nmu);
+  for (size_t i = 0; i < nmu; ++i) mu[i] = normal_at(s0, i);
+  const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t i = t; i < N; i += nt) {
+        const size_t c = n_classes ? i % n_classes : 0;
+        for (size_t k = 0; k < D; ++k) X[i * D + k] = mu[c * D + k] + normal_at(s0, nmu + i * D + k);
+        y[i] = (double)c;
+      }
+    });
+  for (auto& x : th) x.join();
+}
+int dho2g_tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs) {
+  std::string err;
+  const int rc = tridiag_eig_host(n, diag, off, vals, vecs, &err);
+  if (rc) g_err = err;
+  return rc;
+}
+
+// ------------------------------------------------------------------ MLP plugin
+int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, int loss, dho2g_mlp** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n_sizes < 3) fail(DHO2G_ARGUMENT, "mlp oracle: need at least one hidden layer");
+    for (int i = 0; i < n_sizes; ++i)
+      if (sizes[i] == 0) fail(DHO2G_ARGUMENT, "mlp oracle: zero layer size");
+    if (act < 0 || act > 1) fail(DHO2G_ARGUMENT, "activation: expected tanh|relu");
+    if (loss < 0 || loss > 1) fail(DHO2G_ARGUMENT, "loss: expected mse|softmax_ce");
+    auto m = std::make_unique<dho2g_mlp>();
+    m->ctx = ctx;
+    m->sizes.assign(sizes, sizes + n_sizes);
+    m->act = act;
+    m->loss = loss;
+    m->L = n_sizes - 1;
+    size_t off = 0;
+    for (int t = 0; t < m->L; ++t) {
+      LayerDesc ld;
+      ld.in = (int)sizes[t];
+      ld.out = (int)sizes[t + 1];
+      ld.Pin = (int)round_up(sizes[t], 8);
+      ld.Pout = (int)round_up(sizes[t + 1], 8);
+      ld.w_off = off;
+      off += sizes[t] * sizes[t + 1];
+      ld.b_off = off;
+      off += sizes[t + 1];
+      m->layers.push_back(ld);
+    }
+    m->dim = off;
+    for (size_t s : m->sizes) m->smax = std::max(m->smax, s);
+    m->WV_hi.resize(m->L); m->WV_lo.resize(m->L); m->WVt_hi.resize(m->L); m->WVt_lo.resize(m->L);
+    for (int t = 0; t < m->L; ++t) {
+      const LayerDesc& ld = m->layers[t];
+      m->WV_hi[t].alloc((size_t)ld.out * 2 * ld.Pin);
+      m->WV_lo[t].alloc((size_t)ld.out * 2 * ld.Pin);
+      if (t > 0) {
+        m->WVt_hi[t].alloc((size_t)ld.in * 2 * ld.Pout);
+        m->WVt_lo[t].alloc((size_t)ld.in * 2 * ld.Pout);
+      }
+    }
+    *out = m.release();
+  });
+}
+
+int dho2g_mlp_destroy(dho2g_mlp* mlp) {
+  return guard([&] {
+    if (!mlp) return;
+    cudaSetDevice(mlp->ctx->device);
+    cudaStreamSynchronize(mlp->ctx->stream);
+    delete mlp;
+  });
+}
+
+size_t dho2g_mlp_dim(const dho2g_mlp* mlp) { return mlp ? mlp->dim : 0; }
+
+int dho2g_mlp_init_params(const dho2g_mlp* mlp, uint64_t seed, double* w) {  // oracle.cpp:386-394
+  return guard([&] {
+    std::fill(w, w + mlp->dim, 0.0);
+    Rng rng(seed * 0x9e3779b97f4a7c15ULL + 17);
+    for (const LayerDesc& l : mlp->layers) {
+      const double sd = 1.0 / std::sqrt(static_cast<double>(l.in));
+      for (size_t k = 0; k < (size_t)l.in * l.out; ++k) w[l.w_off + k] = sd * rng.normal();
+    }
+  });
+}
+
+static void mlp_stage(dho2g_mlp* m, const double* w, const double* X, const double* y, size_t B) {
+  cudaStream_t s = m->ctx->stream;
+  upload(m->w32, w, m->dim, s);
+  upload(m->X32, X, B * m->sizes[0], s);
+  upload(m->y32, y, B, s);
+}
+
+int dho2g_mlp_value(dho2g_mlp* m, const double* w, const double* X, const double* y, size_t B, size_t ncls,
+                    double* out) {
+  return guard([&] {
+    check_ctx(m->ctx);
+    check_batch(m, B, ncls);
+    mlp_stage(m, w, X, y, B);
+    m->red.ensure(2 * 16);
+    DHO2G_CUDA(cudaMemsetAsync(m->red.p, 0, 2 * sizeof(double), m->ctx->stream));
+    mlp_load_weights(m, m->w32.p);
+    mlp_eval_dev(m, m->w32.p, m->X32.p, m->y32.p, nullptr, B, ncls, m->red.p);
+    double h[2];
+    DHO2G_CUDA(cudaMemcpyAsync(h, m->red.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->ctx->stream));
+    DHO2G_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    *out = h[0] / (double)B;
+  });
+}
+
+int dho2g_mlp_accuracy(dho2g_mlp* m, const double* w, const double* X, const double* y, size_t B, size_t ncls,
+                       double* acc) {
+  return guard([&] {
+    check_ctx(m->ctx);
+    if (ncls == 0) {  // oracle.cpp:650: nullopt for regression
+      *acc = -1.0;
+      return;
+    }
+    check_batch(m, B, ncls);
+    mlp_stage(m, w, X, y, B);
+    m->red.ensure(2 * 16);
+    DHO2G_CUDA(cudaMemsetAsync(m->red.p, 0, 2 * sizeof(double), m->ctx->stream));
+    mlp_load_weights(m, m->w32.p);
+    mlp_eval_dev(m, m->w32.p, m->X32.p, m->y32.p, nullptr, B, ncls, m->red.p);
+    double h[2];
+    DHO2G_CUDA(cudaMemcpyAsync(h, m->red.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, m->ctx->stream));
+    DHO2G_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    *acc = h[1] / (double)B;
+  });
+}
+
+int dho2g_mlp_grad(dho2g_mlp* m, const double* w, const double* X, const double* y, size_t B, size_t ncls,
+                   double* g) {
+  return guard([&] {
+    check_ctx(m->ctx);
+    check_batch(m, B, ncls);
+    mlp_stage(m, w, X, y, B);
+    m->out32.ensure(m->dim);
+    mlp_load_weights(m, m->w32.p);
+    mlp_grad_dev(m, m->w32.p, m->X32.p, m->y32.p, nullptr, B, ncls, 1.0 / (double)B, m->out32.p);
+    download(m->out32.p, g, m->dim, m->ctx->stream);
+  });
+}
+
+int dho2g_mlp_hvp(dho2g_mlp* m, const double* w, const double* v, const double* X, const double* y, size_t B,
+                  size_t ncls, double* hv) {
+  return guard([&] {
+    check_ctx(m->ctx);
+    check_batch(m, B, ncls);
+    mlp_stage(m, w, X, y, B);
+    upload(m->v32, v, m->dim, m->ctx->stream);
+    m->out32.ensure(m->dim);
+    mlp_set_input(m, m->X32.p, m->y32.p, nullptr, B, true);
+    mlp_load_weights(m, m->w32.p);
+    mlp_hvp_dev(m, m->v32.p, nullptr, B, ncls, 1.0 / (double)B, m->out32.p);
+    download(m->out32.p, hv, m->dim, m->ctx->stream);
+  });
+}
+
+// ------------------------------------------------------------------ operators
+int dho2g_op_mlp(dho2g_ctx* ctx, dho2g_mlp* mlp, const double* w, const double* X, const double* y, size_t B,
+                 size_t ncls, dho2g_op** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    check_batch(mlp, B, ncls);
+    auto op = std::make_unique<dho2g_op>();
+    op->ctx = ctx;
+    op->kind = 0;
+    op->n = mlp->dim;
+    op->mlp = mlp;
+    upload(op->w, w, mlp->dim, ctx->stream);
+    upload(op->X, X, B * mlp->sizes[0], ctx->stream);
+    upload(op->y, y, B, ctx->stream);
+    op->wptr = op->w.p;
+    op->Xptr = op->X.p;
+    op->yptr = op->y.p;
+    op->B = B;
+    op->ncls = ncls;
+    shard_range(B, ctx->world, ctx->rank, &op->b0, &op->b1);
+    op->scale = 1.0 / (double)B;
+    if (ctx->world > 1) op->hfull.alloc(cdiv(op->n, (size_t)ctx->world) * ctx->world);
+    *out = op.release();
+  });
+}
+
+int dho2g_op_diag(dho2g_ctx* ctx, const double* spectrum, size_t n, dho2g_op** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n == 0) fail(DHO2G_ARGUMENT, "quadratic oracle: empty spectrum");
+    auto op = std::make_unique<dho2g_op>();
+    op->ctx = ctx;
+    op->kind = 1;
+    op->n = n;
+    upload(op->mat, spectrum, n, ctx->stream);
+    *out = op.release();
+  });
+}
+
+int dho2g_op_dense(dho2g_ctx* ctx, const double* mat, size_t n, dho2g_op** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n == 0) fail(DHO2G_ARGUMENT, "dense operator: empty");
+    auto op = std::make_unique<dho2g_op>();
+    op->ctx = ctx;
+    op->kind = 2;
+    op->n = n;
+    upload(op->mat, mat, n * n, ctx->stream);
+    *out = op.release();
+  });
+}
+
+int dho2g_op_host(dho2g_ctx* ctx, dho2g_host_hvp fn, void* user, size_t n, dho2g_op** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!fn || n == 0) fail(DHO2G_ARGUMENT, "host operator: null callback or empty");
+    auto op = std::make_unique<dho2g_op>();
+    op->ctx = ctx;
+    op->kind = 3;
+    op->n = n;
+    op->fn = fn;
+    op->user = user;
+    *out = op.release();
+  });
+}
+
+int dho2g_op_destroy(dho2g_op* op) {
+  return guard([&] {
+    if (!op) return;
+    if (op->mlp && op->mlp->input_owner == op) op->mlp->input_owner = nullptr;
+    cudaStreamSynchronize(op->ctx->stream);
+    delete op;
+  });
+}
+
+// ------------------------------------------------------------------ Lanczos / ESE
+int dho2g_lanczos_run(dho2g_ctx* ctx, dho2g_op* op, size_t m, uint64_t seed, const dho2g_lanczos_opts* opts,
+                      dho2g_lanczos** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!op) fail(DHO2G_ARGUMENT, "null operator");
+    if (m < 1 || m > op->n) fail(DHO2G_ARGUMENT, "lanczos_distributed: need 1 <= m <= n");
+    if (m >= (size_t)kMaxLanczos) fail(DHO2G_ARGUMENT, "lanczos: m exceeds the device limit (1023)");
+    auto lz = std::make_unique<dho2g_lanczos>();
+    if (opts) lz->opts = *opts;
+    lanczos_alloc(lz.get(), ctx, op->n, m);
+    lanczos_run_into(lz.get(), op, seed);
+    *out = lz.release();
+  });
+}
+
+int dho2g_lanczos_result(const dho2g_lanczos* lz, double* diag, double* off, size_t* iters, int* breakdown,
+                         size_t* safeguard_passes, size_t* shard_begin, size_t* shard_end) {
+  return guard([&] {
+    const int it = lz->host.iters;
+    if (diag)
+      for (int i = 0; i < it; ++i) diag[i] = lz->host.diag[i];
+    const int noff = lz->host.breakdown ? it - 1 : it;
+    if (off)
+      for (int i = 0; i < noff; ++i) off[i] = lz->host.off[i];
+    if (iters) *iters = (size_t)it;
+    if (breakdown) *breakdown = lz->host.breakdown;
+    if (safeguard_passes) *safeguard_passes = (size_t)lz->host.safeguards;
+    if (shard_begin) *shard_begin = lz->begin;
+    if (shard_end) *shard_end = lz->end;
+  });
+}
+
+int dho2g_lanczos_basis(const dho2g_lanczos* lz, double* basis_shard) {
+  return guard([&] {
+    const int it = lz->host.iters;
+    const int cols = lz->host.breakdown ? it : it + 1;
+    std::vector<float> f(lz->rows);
+    for (int j = 0; j < cols; ++j) {
+      if (lz->rows)
+        DHO2G_CUDA(cudaMemcpy(f.data(), lz->D.p + (size_t)j * lz->ldd, lz->rows * sizeof(float),
+                              cudaMemcpyDeviceToHost));
+      const double sg = lz->host.sigma[j];
+      for (size_t r = 0; r < lz->rows; ++r) basis_shard[(size_t)j * lz->rows + r] = sg * (double)f[r];
+    }
+  });
+}
+
+int dho2g_lanczos_destroy(dho2g_lanczos* lz) {
+  return guard([&] { delete lz; });
+}
+
+int dho2g_extract_ese(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    auto e = std::make_unique<dho2g_ese>();
+    extract_ese_into(ctx, lz, k, l, e.get());
+    *out = e.release();
+  });
+}
+
+size_t dho2g_ese_count(const dho2g_ese* ese) { return ese ? ese->r : 0; }
+
+int dho2g_ese_eigvals(const dho2g_ese* ese, double* vals) {
+  return guard([&] {
+    for (size_t i = 0; i < ese->r; ++i) vals[i] = ese->eigvals[i];
+  });
+}
+
+int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs) {
+  return guard([&] {
+    std::vector<float> f(ese->rows);
+    for (size_t c = 0; c < ese->r; ++c) {
+      if (ese->rows)
+        DHO2G_CUDA(cudaMemcpy(f.data(), ese->V.p + c * ese->ldv, ese->rows * sizeof(float), cudaMemcpyDeviceToHost));
+      for (size_t r = 0; r < ese->rows; ++r) vecs[c * ese->rows + r] = (double)(ese->sign[c] * f[r]);
+    }
+  });
+}
+
+int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, size_t n, size_t r, dho2g_ese** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    auto e = std::make_unique<dho2g_ese>();
+    e->ctx = ctx;
+    e->n = n;
+    e->r = r;
+    shard_range(n, ctx->world, ctx->rank, &e->begin, &e->end);
+    e->rows = e->end - e->begin;
+    e->ldv = round_up(std::max<size_t>(cdiv(n, (size_t)ctx->world), 1), kGsChunk);
+    e->eigvals.assign(eigvals, eigvals + r);
+    e->sign.assign(r, 1.f);
+    e->V.alloc(e->ldv * std::max<size_t>(r, 1));
+    e->ev_dev.alloc(std::max<size_t>(r, 1));
+    std::vector<float> col(e->rows);
+    for (size_t c = 0; c < r; ++c) {
+      for (size_t i = 0; i < e->rows; ++i) col[i] = (float)V[c * n + e->begin + i];
+      if (e->rows)
+        DHO2G_CUDA(cudaMemcpy(e->V.p + c * e->ldv, col.data(), e->rows * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    if (r) DHO2G_CUDA(cudaMemcpy(e->ev_dev.p, eigvals, r * sizeof(double), cudaMemcpyHostToDevice));
+    *out = e.release();
+  });
+}
+
+int dho2g_ese_destroy(dho2g_ese* ese) {
+  return guard([&] { delete ese; });
+}
+
+// ------------------------------------------------------------------ optimizer (rank rows of host vectors)
+int dho2g_opt_create(dho2g_ctx* ctx, const dho2g_base_cfg* cfg, size_t n, dho2g_opt** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n == 0) fail(DHO2G_ARGUMENT, "BaseOptimizer: zero dimension");
+    auto o = std::make_unique<dho2g_opt>();
+    size_t b, e;
+    shard_range(n, ctx->world, ctx->rank, &b, &e);
+    opt_alloc(o.get(), ctx, *cfg, e - b);
+    *out = o.release();
+  });
+}
+
+int dho2g_opt_destroy(dho2g_opt* opt) {
+  return guard([&] { delete opt; });
+}
+
+struct HostUpd {
+  DevBuf<float> g, pi, w, nw, bs;
+};
+
+static void run_host_update(dho2g_opt* o, const dho2g_ese* ese, const double* g, const double* pi, const double* w,
+                            double alpha, double sigma, double fl, double* newton, double* base) {
+  cudaStream_t s = o->ctx->stream;
+  const size_t rows = o->n;
+  HostUpd h;
+  upload(h.g, g, rows, s);
+  if (pi) upload(h.pi, pi, rows, s);
+  upload(h.w, w, rows, s);
+  h.nw.alloc(std::max<size_t>(rows, 1));
+  h.bs.alloc(std::max<size_t>(rows, 1));
+  UpdateArgs a{};
+  a.g = h.g.p;
+  a.pi = pi ? h.pi.p : nullptr;
+  a.w_a = nullptr;
+  a.w_decay = h.w.p;
+  a.newton_out = h.nw.p;
+  a.base_out = h.bs.p;
+  a.alpha = alpha;
+  a.sigma = sigma;
+  a.floor = fl;
+  if (ese && ese->r > 0 && ese->rows != rows) fail(DHO2G_DIMENSION, "deltas: eigenvector rows != gradient length");
+  split_update(o, (ese && ese->r > 0) ? ese : nullptr, a);
+  check_opt_flags(o);
+  if (newton) download(h.nw.p, newton, rows, s);
+  if (base) download(h.bs.p, base, rows, s);
+}
+
+int dho2g_opt_step(dho2g_opt* opt, const double* g, const double* w, double* d) {
+  return guard([&] {
+    check_ctx(opt->ctx);
+    run_host_update(opt, nullptr, g, nullptr, w, 0.0, 0.0, 1e-6, nullptr, d);
+  });
+}
+
+int dho2g_deltas(dho2g_opt* opt, const dho2g_ese* ese, const double* g, const double* pi, const double* w, double alpha,
+                 double sigma, double eigval_floor, double* newton, double* base) {
+  return guard([&] {
+    check_ctx(opt->ctx);
+    run_host_update(opt, ese, g, pi, w, alpha, sigma, eigval_floor, newton, base);
+    if (!ese || ese->r == 0)
+      if (newton) std::fill(newton, newton + opt->n, 0.0);
+  });
+}
+
+int dho2g_admm_w_update(dho2g_ctx* ctx, size_t n, double sigma, const double* w_a, const double* pi, double* w) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (sigma <= 0.0) fail(DHO2G_ARGUMENT, "admm_w_update: sigma must be positive");
+    DevBuf<float> a, p, o;
+    upload(a, w_a, n, ctx->stream);
+    upload(p, pi, n, ctx->stream);
+    o.alloc(std::max<size_t>(n, 1));
+    admm_w_update_dev(ctx->stream, n, sigma, a.p, p.p, o.p);
+    download(o.p, w, n, ctx->stream);
+  });
+}
+
+int dho2g_admm_dual_update(dho2g_ctx* ctx, size_t n, double sigma, const double* w_a, const double* w, double* pi) {
+  return guard([&] {
+    check_ctx(ctx);
+    DevBuf<float> a, b, p;
+    upload(a, w_a, n, ctx->stream);
+    upload(b, w, n, ctx->stream);
+    upload(p, pi, n, ctx->stream);
+    admm_dual_update_dev(ctx->stream, n, sigma, a.p, b.p, p.p);
+    download(p.p, pi, n, ctx->stream);
+  });
+}
+
+// ------------------------------------------------------------------ trainer
+int dho2g_trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X, const double* y,
+                         size_t N, size_t ncls, uint64_t dataset_seed, const double* w0, int workers, int host_resident,
+                         dho2g_trainer** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    *out = trainer_create(ctx, cfg, mlp, X, y, N, ncls, dataset_seed, w0, workers, host_resident);
+  });
+}
+int dho2g_trainer_destroy(dho2g_trainer* tr) {
+  return guard([&] { trainer_destroy(tr); });
+}
+int dho2g_trainer_step(dho2g_trainer* tr, size_t steps, int with_eval) {
+  return guard([&] { trainer_step(tr, steps, with_eval); });
+}
+int dho2g_trainer_run(dho2g_trainer* tr) {
+  return guard([&] { trainer_run(tr); });
+}
+int dho2g_trainer_params(dho2g_trainer* tr, double* w) {
+  return guard([&] { trainer_params(tr, w); });
+}
+size_t dho2g_trainer_rows(dho2g_trainer* tr) { return tr ? trainer_rows(tr) : 0; }
+int dho2g_trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
+                          int* refresh) {
+  return guard([&] { trainer_metrics(tr, max_rows, loss, acc, resid, epoch, refresh); });
+}
+int dho2g_trainer_last_loss(dho2g_trainer* tr, double* loss) {
+  return guard([&] { *loss = trainer_last_loss(tr); });
+}
+int dho2g_trainer_stat(dho2g_trainer* tr, const char* key, double* value) {
+  return guard([&] {
+    if (!trainer_stat(tr, key ? key : "", value)) fail(DHO2G_ARGUMENT, std::string("unknown trainer stat ") + key);
+  });
+}
+int dho2g_trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count) {
+  return guard([&] { trainer_eigvals(tr, vals, count); });
+}
+
+// ------------------------------------------------------------------ test hook
+namespace {
+__global__ void split_rows_kernel(const float* __restrict__ src, int rows, int K, int ld, bf16* __restrict__ hi,
+                                  bf16* __restrict__ lo) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)rows * ld) return;
+  const int r = (int)(i / ld), k = (int)(i % ld);
+  const float x = k < K ? src[(size_t)r * K + k] : 0.f;
+  split_bf16(x, hi[i], lo[i]);
+}
+}  // namespace
+
+int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* Cout, int backend) {
+  return guard([&] {
+    check_ctx(ctx);
+    const int ld = (int)round_up(std::max(K, 1), 8);
+    DevBuf<float> a((size_t)M * K), b((size_t)N * K), c((size_t)M * N);
+    DevBuf<bf16> ah((size_t)M * ld), al((size_t)M * ld), bh((size_t)N * ld), bl((size_t)N * ld);
+    DHO2G_CUDA(cudaMemcpy(a.p, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
+    DHO2G_CUDA(cudaMemcpy(b.p, B, sizeof(float) * N * K, cudaMemcpyHostToDevice));
+    split_rows_kernel<<<cdiv((size_t)M * ld, 256), 256, 0, ctx->stream>>>(a.p, M, K, ld, ah.p, al.p);
+    split_rows_kernel<<<cdiv((size_t)N * ld, 256), 256, 0, ctx->stream>>>(b.p, N, K, ld, bh.p, bl.p);
+    DHO2G_LAUNCH();
+    const int saved = ctx->gemm_backend;
+    ctx->gemm_backend = backend;
+    gemm3(ctx, M, N, K, ah.p, al.p, ld, bh.p, bl.p, ld, c.p, N, 1.0f);
+    ctx->gemm_backend = saved;
+    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+    DHO2G_CUDA(cudaMemcpy(Cout, c.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Shared internals of libdho2gpu.so: error plumbing, device buffers, small device helpers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dho2gpu.h"
+
+namespace dho2g {
+
+// Internal exception carrying a dho2g_status; converted at the C boundary (capi.cu).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define DHO2G_CUDA(expr)                                                                        \
+  do {                                                                                          \
+    cudaError_t e__ = (expr);                                                                   \
+    if (e__ != cudaSuccess)                                                                     \
+      ::dho2g::fail(DHO2G_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__) + " @" +    \
+                                    __FILE__ + ":" + std::to_string(__LINE__));                 \
+  } while (0)
+
+// NCCL is resolved at run time (dlopen of libnccl.so.2) so the library never pins a NCCL build:
+// inside a torch process it binds to the NCCL torch already loaded.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+const NcclApi& nccl();
+
+#define DHO2G_NCCLCHK(expr)                                                                    \
+  do {                                                                                         \
+    ncclResult_t r__ = (expr);                                                                 \
+    if (r__ != ncclSuccess)                                                                    \
+      ::dho2g::fail(DHO2G_NCCL, std::string(#expr) + ": " + ::dho2g::nccl().GetErrorString(r__)); \
+  } while (0)
+
+// Every kernel launch of the library goes through DHO2G_LAUNCH(): counts it (bench evidence of
+// device work, "gpu_launches") and surfaces launch errors.
+extern unsigned long long g_launches;
+#define DHO2G_LAUNCH()              \
+  do {                              \
+    ++::dho2g::g_launches;          \
+    DHO2G_CUDA(cudaGetLastError()); \
+  } while (0)
+
+__host__ __device__ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
+
+// RAII device allocation (cudaMalloc, zero-initialised).
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count == 0) return;
+    DHO2G_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    DHO2G_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+  }
+  void ensure(size_t count) { if (count > n) alloc(count); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+// Pinned host allocation.
+template <typename T>
+struct HostBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() { if (p) cudaFreeHost(p); }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    DHO2G_CUDA(cudaHostAlloc(&p, count * sizeof(T), cudaHostAllocPortable | cudaHostAllocMapped));
+    n = count;
+  }
+};
+
+typedef __nv_bfloat16 bf16;
+
+// ----------------------------------------------------------------------------- device helpers
+__device__ __forceinline__ void split_bf16(float x, bf16& hi, bf16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block reduction of one double per thread (fixed tree order). Result valid in
+// thread 0. `sh` needs blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += sh[i];
+  return r;
+}
+
+}  // namespace dho2g

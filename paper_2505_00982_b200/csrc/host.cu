@@ -1,0 +1,262 @@
+// Host-side bookkeeping that must be bit-exact with the reference (rng, shards, budget,
+// permutations, sample/curvature indices) and the context's collectives.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "internal.h"
+
+namespace dho2g {
+
+unsigned long long g_launches = 0;
+
+// rng.hpp:18-23 SplitMix64
+uint64_t Rng::next_u64() {
+  uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// rng.hpp:26
+double Rng::uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+// rng.hpp:29-35
+uint64_t Rng::uniform_below(uint64_t bound) {
+  const uint64_t threshold = (0 - bound) % bound;
+  for (;;) {
+    const uint64_t r = next_u64();
+    if (r >= threshold) return r % bound;
+  }
+}
+// rng.hpp:37-50
+double Rng::normal() {
+  if (have_spare) {
+    have_spare = false;
+    return spare;
+  }
+  const double u1 = (static_cast<double>(next_u64() >> 11) + 1.0) * 0x1.0p-53;
+  const double u2 = uniform();
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * 3.141592653589793 * u2;
+  spare = radius * std::sin(angle);
+  have_spare = true;
+  return radius * std::cos(angle);
+}
+
+// rng.hpp:56-62 Fisher-Yates over iota
+void shuffle_iota(uint64_t seed, size_t n, uint64_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = i;
+  Rng r(seed);
+  for (size_t i = n; i > 1; --i) {
+    const size_t j = static_cast<size_t>(r.uniform_below(i));
+    std::swap(out[i - 1], out[j]);
+  }
+}
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) fail(DHO2G_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p) fail(DHO2G_NCCL, std::string("libnccl.so.2 lacks ") + n);
+      return p;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+    a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
+// collectives.cpp:10-20
+void shard_range(size_t n, int world, int rank, size_t* begin, size_t* end) {
+  if (world < 1) fail(DHO2G_ARGUMENT, "Shard: world_size must be >= 1");
+  if (rank < 0 || rank >= world) fail(DHO2G_ARGUMENT, "Shard: rank out of range");
+  const size_t base = (n + static_cast<size_t>(world) - 1) / static_cast<size_t>(world);
+  *begin = std::min(base * static_cast<size_t>(rank), n);
+  *end = std::min(*begin + base, n);
+}
+
+// lanczos.cpp:10-16
+size_t lanczos_budget(size_t k, size_t l, size_t n) {
+  if (n < 1) fail(DHO2G_ARGUMENT, "lanczos_budget: n must be >= 1");
+  if (k + l < 1) fail(DHO2G_ARGUMENT, "lanczos_budget: k+l must be >= 1");
+  if (k + l > n) fail(DHO2G_ARGUMENT, "lanczos_budget: k+l exceeds the dimension");
+  const auto log_term = static_cast<size_t>(std::ceil(2.0 * std::log(static_cast<double>(n))));
+  return std::min(n, std::max(4 * (k + l), log_term));
+}
+
+// Host fp64 implicit-shift QL (linalg.cpp:140-226 semantics: ascending, stable order,
+// NumericError after 60 sweeps). The device path uses the single-CTA kernel in lanczos.cu.
+int tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs,
+                     std::string* err) {
+  if (n == 0) {
+    *err = "tridiag_eig: empty matrix";
+    return DHO2G_ARGUMENT;
+  }
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(diag[i]) || (i + 1 < n && !std::isfinite(off[i]))) {
+      *err = "tridiag_eig: non-finite entries";
+      return DHO2G_NUMERIC;
+    }
+  std::vector<double> d(diag, diag + n), e(n, 0.0), z(n * n, 0.0);
+  for (size_t i = 0; i + 1 < n; ++i) e[i] = off[i];
+  for (size_t i = 0; i < n; ++i) z[i * n + i] = 1.0;
+  const double eps = 2.220446049250313e-16;
+  for (size_t l = 0; l < n && n > 1; ++l) {
+    int iter = 0;
+    size_t mm;
+    for (;;) {
+      for (mm = l; mm + 1 < n; ++mm) {
+        if (std::abs(e[mm]) <= eps * (std::abs(d[mm]) + std::abs(d[mm + 1]))) break;
+      }
+      if (mm == l) break;
+      if (iter++ == 60) {
+        *err = "tridiag_eig: QL iteration did not converge";
+        return DHO2G_NUMERIC;
+      }
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = std::hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      bool under = false;
+      for (size_t ii = mm; ii-- > l;) {
+        double f = s * e[ii];
+        const double b = c * e[ii];
+        r = std::hypot(f, g);
+        e[ii + 1] = r;
+        if (r == 0.0) {
+          d[ii + 1] -= p;
+          e[mm] = 0.0;
+          under = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[ii + 1] - p;
+        r = (d[ii] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[ii + 1] = g + p;
+        g = c * r - b;
+        for (size_t k = 0; k < n; ++k) {
+          f = z[(ii + 1) * n + k];
+          z[(ii + 1) * n + k] = s * z[ii * n + k] + c * f;
+          z[ii * n + k] = c * z[ii * n + k] - s * f;
+        }
+      }
+      if (under) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  std::vector<size_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return d[a] < d[b]; });
+  for (size_t j = 0; j < n; ++j) {
+    vals[j] = d[order[j]];
+    std::copy(z.begin() + order[j] * n, z.begin() + (order[j] + 1) * n, vecs + j * n);
+  }
+  return DHO2G_OK;
+}
+
+}  // namespace dho2g
+
+// ------------------------------------------------------------------------- context collectives
+void dho2g_ctx::sync() { DHO2G_CUDA(cudaStreamSynchronize(stream)); }
+
+int dho2g_ctx::kt_begin() {
+  if (!ktimers) return -1;
+  cudaEvent_t a, b;
+  if (kpool.size() >= 2) {
+    a = kpool.back(); kpool.pop_back();
+    b = kpool.back(); kpool.pop_back();
+  } else {
+    DHO2G_CUDA(cudaEventCreate(&a));
+    DHO2G_CUDA(cudaEventCreate(&b));
+  }
+  DHO2G_CUDA(cudaEventRecord(a, stream));
+  kpend.push_back({std::string(), a, b, 0.0});
+  return (int)kpend.size() - 1;
+}
+
+void dho2g_ctx::kt_end(int slot, const char* name, double work) {
+  if (slot < 0) return;
+  KPending& p = kpend[slot];
+  p.name = name;
+  p.work = work;
+  DHO2G_CUDA(cudaEventRecord(p.b, stream));
+  if (kpend.size() > 4096) kt_flush();
+}
+
+void dho2g_ctx::kt_flush() {
+  if (kpend.empty()) return;
+  DHO2G_CUDA(cudaStreamSynchronize(stream));
+  for (auto& p : kpend) {
+    float ms = 0.f;
+    DHO2G_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    KStat& k = kstats[p.name];
+    k.ms += ms;
+    k.count += 1;
+    k.work += p.work;
+    kpool.push_back(p.a);
+    kpool.push_back(p.b);
+  }
+  kpend.clear();
+}
+
+void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count) {
+  if (world == 1) {
+    if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
+  DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream));
+  bump("nccl_calls", 1);
+  bump("nccl_bytes", double(count) * 8 * world);
+}
+
+void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count) {
+  if (world == 1) {
+    if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
+  DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream));
+  bump("nccl_calls", 1);
+  bump("nccl_bytes", double(count) * 4 * world);
+}
+
+void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count) {
+  if (world == 1) {
+    if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
+  DHO2G_NCCLCHK(dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream));
+  bump("nccl_calls", 1);
+  bump("nccl_bytes", double(count) * 4 * world);
+}
+
+namespace {
+__global__ void ordered_sum_kernel(const double* __restrict__ all, double* __restrict__ out, size_t count, int world) {
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x) {
+    double s = all[i];
+    for (int r = 1; r < world; ++r) s += all[size_t(r) * count + i];  // ascending rank (collectives.cpp:310-324)
+    out[i] = s;
+  }
+}
+}  // namespace
+
+void dho2g_ctx::allreduce_sum_f64_ordered(double* inout, size_t count) {
+  if (world == 1) return;
+  gather_f64.ensure(count * world);
+  allgather_f64(inout, gather_f64.p, count);
+  ordered_sum_kernel<<<(unsigned)std::min<size_t>(dho2g::cdiv(count, 256), 1024), 256, 0, stream>>>(
+      gather_f64.p, inout, count, world);
+  DHO2G_LAUNCH();
+}

@@ -1,0 +1,252 @@
+// Internal object layouts shared by the translation units of libdho2gpu.so.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dho2g {
+
+constexpr int kMaxLanczos = 1024;  // m <= 1023 (C5 sweep needs 512)
+constexpr int kGsChunk = 2048;     // rows per GS pass-1 chunk; shard rows are padded to this
+
+// ------------------------------------------------------------------------- host bookkeeping
+struct Rng {  // rng.hpp:14-68 (SplitMix64 + Box-Muller with spare)
+  uint64_t state;
+  double spare = 0.0;
+  bool have_spare = false;
+  explicit Rng(uint64_t s) : state(s) {}
+  uint64_t next_u64();
+  double uniform();
+  uint64_t uniform_below(uint64_t bound);
+  double normal();
+};
+void shuffle_iota(uint64_t seed, size_t n, uint64_t* out);
+void shard_range(size_t n, int world, int rank, size_t* begin, size_t* end);
+size_t lanczos_budget(size_t k, size_t l, size_t n);
+int tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs, std::string* err);
+
+}  // namespace dho2g
+
+// ------------------------------------------------------------------------- context
+struct dho2g_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  int gemm_backend = 0;  // 0 tcgen05, 1 CUDA-core reference kernel
+  int use_graphs = 0;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled
+  std::map<std::string, double> stats;
+  // Per-kernel device timers (CUDA events on this stream), enabled by option "ktimers".
+  bool ktimers = false;
+  struct KPending { std::string name; cudaEvent_t a, b; double work; };
+  std::vector<KPending> kpend;
+  std::vector<cudaEvent_t> kpool;
+  struct KStat { double ms = 0, count = 0, work = 0; };
+  std::map<std::string, KStat> kstats;
+  std::vector<cudaEvent_t> marks;  // user timer marks
+  int kt_begin();                  // returns slot or -1
+  void kt_end(int slot, const char* name, double work);
+  void kt_flush();                 // synchronize and fold pending events into kstats
+  dho2g::DevBuf<double> gather_f64;  // world * count scratch for ordered all-reduces
+  dho2g::DevBuf<double> pinned_dummy;
+
+  // Collectives (NCCL over NVLink at world > 1; identity at world == 1).
+  void allgather_f64(const double* send, double* recv, size_t count);
+  void allgather_f32(const float* send, float* recv, size_t count);
+  void reduce_scatter_f32(const float* send, float* recv, size_t count);
+  void allreduce_sum_f64_ordered(double* inout, size_t count);  // all_gather + rank-ordered sum
+  void sync();
+  void bump(const char* key, double v) { stats[key] += v; }
+};
+
+// ------------------------------------------------------------------------- MLP (oracle.hpp:113)
+struct LayerDesc {
+  int in = 0, out = 0;    // sizes[t], sizes[t+1]
+  int Pin = 0, Pout = 0;  // round_up(., 8): half-width of the hi/lo operand pairs
+  size_t w_off = 0, b_off = 0;
+};
+
+struct dho2g_mlp {
+  dho2g_ctx* ctx = nullptr;
+  std::vector<size_t> sizes;
+  std::vector<LayerDesc> layers;
+  size_t dim = 0;
+  int act = 0, loss = 0;
+  int L = 0;
+  // Weight operands per layer t: WV[t] = [V | W] rows o (out x 2Pin); WVt[t] = [V^T | W^T] rows k (in x 2Pout)
+  std::vector<dho2g::DevBuf<dho2g::bf16>> WV_hi, WV_lo, WVt_hi, WVt_lo;
+  // Batch operands per activation level j (width s_j = sizes[j], half-width P_j):
+  //  AR[j]  = [a | ra] rows b   (Bcap x 2P_j), j = 0..L-1
+  //  ART[j] = [a^T | ra^T] rows k (s_j x 2Bpcap), j = 0..L-1
+  //  DR[j]  = [d | rd] rows b   (Bcap x 2P_j), j = 1..L
+  //  DRT[j] = [rd^T | d^T] rows o (s_j x 2Bpcap), j = 1..L
+  std::vector<dho2g::DevBuf<dho2g::bf16>> AR_hi, AR_lo, ART_hi, ART_lo, DR_hi, DR_lo, DRT_hi, DRT_lo;
+  std::vector<dho2g::DevBuf<float>> a32, ra32, d32, rd32;  // fp32 B x s_j
+  dho2g::DevBuf<float> Z, RZ;                               // GEMM outputs (Bcap x max s)
+  dho2g::DevBuf<float> lab;                                 // gathered labels (Bcap)
+  dho2g::DevBuf<double> sample_loss;                        // per-sample loss (Bcap)
+  dho2g::DevBuf<int> sample_correct;
+  size_t Bcap = 0, Bpcap = 0;
+  size_t smax = 0;
+  // host-API staging
+  dho2g::DevBuf<float> w32, v32, X32, y32, out32;
+  dho2g::DevBuf<int64_t> idx;
+  dho2g::DevBuf<double> red;
+  const float* w_cur = nullptr;        // params whose W halves are loaded
+  const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
+  const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)
+  const void* input_owner = nullptr;   // operator whose curvature batch is packed at level 0
+
+  void ensure_batch(size_t B);
+};
+
+namespace dho2g {
+// MLP device operations (mlp.cu). All stream-ordered on mlp->ctx->stream.
+void mlp_load_weights(dho2g_mlp* m, const float* w);
+void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale /* device scalar or null */);
+// Pack level-0 operands from dataset rows X[idx[b]] (idx null: b itself); labels likewise.
+void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool with_r);
+void mlp_forward(dho2g_mlp* m, const float* w, size_t B, bool with_r);
+// Output delta (and R-delta); fills sample_loss/sample_correct. scale = 1/B (times 1/C).
+void mlp_output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool with_r);
+// Backward into out (flat n-vector, fully overwritten): gradient or Hv.
+void mlp_backward(dho2g_mlp* m, const float* w, size_t B, float* out, bool with_r);
+// Convenience compositions.
+void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
+                  size_t ncls, double scale, float* g);
+void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv);
+// Forward-only evaluation: adds sum of per-sample loss and correct count into acc[0], acc[1] (fp64).
+void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
+                  size_t ncls, double* acc2);
+
+void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);  // acc2 = {sum loss, sum correct} of last batch
+
+// GEMM: C[M x N] = alpha * A[M x K] * B[N x K]^T, split-BF16x3 (hi*hi + hi*lo + lo*hi), fp32 out.
+void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+           const bf16* Blo, int ldb, float* C, int ldc, float alpha);
+void gemm3_simt(cudaStream_t s, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+                const bf16* Blo, int ldb, float* C, int ldc, float alpha);
+bool gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+              const bf16* Blo, int ldb, float* C, int ldc, float alpha);
+
+// fp32 elementwise helpers (update.cu)
+void dev_copy_f64_to_f32(cudaStream_t s, const double* src, float* dst, size_t n);
+void dev_copy_f32_to_f64(cudaStream_t s, const float* src, double* dst, size_t n);
+}  // namespace dho2g
+
+// ------------------------------------------------------------------------- operators / Lanczos
+struct dho2g_op {
+  dho2g_ctx* ctx = nullptr;
+  int kind = 0;  // 0 mlp, 1 diag, 2 dense, 3 host
+  size_t n = 0;
+  dho2g_mlp* mlp = nullptr;
+  dho2g::DevBuf<float> w, X, y, mat;
+  const float* wptr = nullptr;  // params the Hessian is taken at (own copy `w` or the trainer's w_a)
+  const float* Xptr = nullptr;  // dataset rows (own copy `X` or the trainer's resident dataset)
+  const float* yptr = nullptr;
+  dho2g::DevBuf<int64_t> idx;
+  dho2g::DevBuf<float> hfull;  // full-length partial (padded to world * base)
+  size_t B = 0, ncls = 0, b0 = 0, b1 = 0;  // this rank's slice of the curvature batch
+  double scale = 1.0;
+  dho2g_host_hvp fn = nullptr;
+  void* user = nullptr;
+  std::vector<double> hv_in, hv_out;
+  dho2g::HostBuf<float> pin;
+  bool weights_loaded = false;
+  // h_shard[r] = (H (vscale * vfull))[begin + r]
+  void apply(const float* vfull, const float* vscale, float* h_shard, size_t begin, size_t rows, size_t base);
+};
+
+namespace dho2g {
+struct LzDev {  // device-resident Lanczos scalars (fixed launch sequence; no host round trips)
+  double diag[kMaxLanczos + 1];
+  double off[kMaxLanczos + 1];
+  float sigma[kMaxLanczos + 2];  // lazy column normalisation: v_j = sigma_j * D[:, j]
+  double pre, beta;
+  int iters, stopped, breakdown, safeguards, need_sg;
+};
+}  // namespace dho2g
+
+struct dho2g_lanczos {
+  dho2g_ctx* ctx = nullptr;
+  size_t n = 0, m = 0, begin = 0, end = 0, rows = 0, ldd = 0, base = 0;
+  dho2g::DevBuf<float> D;       // ldd x (m+1) column-major, raw (scale sigma_j)
+  dho2g::DevBuf<float> h;       // ldd
+  dho2g::DevBuf<float> vfull;   // world * base (all_gather target)
+  dho2g::DevBuf<dho2g::LzDev> st;
+  dho2g::DevBuf<double> part;   // per-CTA partials
+  dho2g::DevBuf<double> rankp;  // this rank's partial vector (m+2)
+  dho2g::DevBuf<double> allp;   // world x (m+2)
+  dho2g::DevBuf<unsigned> ticket;
+  dho2g::LzDev host{};          // copy after run
+  dho2g_lanczos_opts opts{1, 1e-6, 1e-10};
+  double ms = 0.0;
+};
+
+struct dho2g_ese {
+  dho2g_ctx* ctx = nullptr;
+  size_t n = 0, r = 0, rows = 0, begin = 0, end = 0, ldv = 0;
+  dho2g::DevBuf<float> V;  // ldv x r column-major (column signs in `sign`)
+  std::vector<double> eigvals;
+  std::vector<float> sign;
+  dho2g::DevBuf<double> ev_dev;
+};
+
+namespace dho2g {
+void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed);
+void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m);
+void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese);
+}  // namespace dho2g
+
+// ------------------------------------------------------------------------- optimizer / update
+struct dho2g_opt {
+  dho2g_ctx* ctx = nullptr;
+  dho2g_base_cfg cfg{};
+  size_t n = 0;  // local rows
+  size_t t = 0;
+  dho2g::DevBuf<float> m, v, s;
+  dho2g::DevBuf<double> part, rank1, rank2, all1, all2;
+  dho2g::DevBuf<unsigned> ticket;
+  dho2g::DevBuf<int> bad;  // non-finite gradient flag
+};
+
+namespace dho2g {
+struct UpdateArgs {
+  const float* g;    // rows (shard)
+  const float* pi;   // rows or null
+  float* w_a;        // rows, updated in place (null: only materialize)
+  const float* w_decay;  // rows, w read by the AdamW term (null: w_a)
+  float* newton_out; // optional materialized newton (rows)
+  float* base_out;   // optional materialized base (rows)
+  double alpha, sigma, floor;
+};
+void opt_alloc(dho2g_opt* o, dho2g_ctx* ctx, const dho2g_base_cfg& cfg, size_t rows);
+// One split update (optimizer.cpp:81-117 + BaseOptimizer::step) on this rank's rows.
+void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a);
+void admm_w_update_dev(cudaStream_t s, size_t n, double sigma, const float* w_a, const float* pi, float* w);
+void admm_dual_update_dev(cudaStream_t s, size_t n, double sigma, const float* w_a, const float* w, float* pi);
+void check_opt_flags(dho2g_opt* o);
+}  // namespace dho2g
+
+struct dho2g_trainer;
+namespace dho2g {
+dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
+                              const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
+                              int workers, int host_resident);
+void trainer_step(dho2g_trainer* tr, size_t steps, int with_eval);
+void trainer_run(dho2g_trainer* tr);
+void trainer_params(dho2g_trainer* tr, double* w);
+size_t trainer_rows(dho2g_trainer* tr);
+void trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
+                     int* refresh);
+double trainer_last_loss(dho2g_trainer* tr);
+bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v);
+void trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count);
+void trainer_destroy(dho2g_trainer* tr);
+}  // namespace dho2g

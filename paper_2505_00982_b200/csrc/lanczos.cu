@@ -1,0 +1,668 @@
+// Sharded Lanczos with full reorthogonalisation (reference: proj/src/dist_lanczos.cpp:31-119,
+// lanczos.cpp:28-70), device tridiagonal eigensolve + Ritz extraction (dist_lanczos.cpp:121-158,
+// linalg.cpp:140-226, lanczos.cpp:72-94).
+//
+// Per iteration i on this rank's basis rows (D column-major, lazily normalised: v_j = sigma_j D_j):
+//   all_gather(D_i)  ->  h = H v_i (operator)  ->
+//   pass 1: r_j = D_j^T h (j <= i), hh = ||h||^2           one read of D[:, 0..i] + h
+//   [all_gather of the (i+2) fp64 partials, rank-ordered sum]
+//   pass 2: h' = h - sum_j D_j sigma_j^2 r_j, ||h'||^2      one read of D[:, 0..i] + h, one write
+//   [all_gather of ||h'||^2 partials] -> decide (safeguard / breakdown / beta) on device
+// The launch sequence is fixed (safeguard passes and post-breakdown iterations are predicated on
+// device flags), so the whole refresh needs no host round trip.
+#include <cmath>
+
+#include "internal.h"
+
+using namespace dho2g;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSub = 512;  // rows per warp work item (32 lanes x 4 float4)
+
+// ------------------------------------------------------------------ start vector
+// seeded_unit_gaussian (lanczos.cpp:18-26): Rng(seed*phi + 0x1234567).fill_normal, computed
+// counter-wise (SplitMix64 output i = mix(state0 + (i+1) phi); Box-Muller pairs (2p, 2p+1)).
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t i) {
+  uint64_t z = s0 + (i + 1) * 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void gauss_kernel(uint64_t s0, size_t begin, size_t rows, float* __restrict__ out, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double ss = 0.0;
+  for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < rows; r += (size_t)gridDim.x * blockDim.x) {
+    const size_t i = begin + r;
+    const size_t p = i >> 1;
+    const double u1 = ((double)(splitmix_at(s0, 2 * p) >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = (double)(splitmix_at(s0, 2 * p + 1) >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.141592653589793 * u2;
+    const double x = (i & 1) ? radius * sin(angle) : radius * cos(angle);
+    out[r] = (float)x;
+    ss += x * x;
+  }
+  const double t = block_sum(ss, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void gauss_norm_kernel(const double* __restrict__ part, int nb, double* __restrict__ rankp) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    rankp[0] = s;
+  }
+}
+
+__global__ void lz_init_kernel(LzDev* st, const double* __restrict__ allp, int world, int stride) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += allp[(size_t)r * stride];
+  st->sigma[0] = (float)(1.0 / sqrt(s));
+  st->iters = 0;
+  st->stopped = 0;
+  st->breakdown = 0;
+  st->safeguards = 0;
+  st->need_sg = 0;
+  st->pre = 0.0;
+  st->beta = 0.0;
+}
+
+// ------------------------------------------------------------------ GS pass 1: dots
+// rankp[j] = D_j^T h (j < active), rankp[active] = h^T h, fp64, deterministic order.
+__global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restrict__ D, size_t ldd,
+                                                            const float* __restrict__ h, int active, int nchunks,
+                                                            int stride, double* __restrict__ part,
+                                                            double* __restrict__ rankp, unsigned* ticket,
+                                                            const LzDev* st, int safeguard_pass) {
+  if (st->stopped || (safeguard_pass && !st->need_sg)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* hs = reinterpret_cast<float*>(smem);
+  double* acc = reinterpret_cast<double*>(smem + kGsChunk * sizeof(float));  // [kWarps][active+1]
+  __shared__ bool is_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = active + 1;
+  for (int e = threadIdx.x; e < kWarps * nj; e += kThreads) acc[e] = 0.0;
+  const int items = nj * (kGsChunk / kSub);
+  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const size_t r0 = (size_t)c * kGsChunk;
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGsChunk / 4; e += kThreads)
+      reinterpret_cast<float4*>(hs)[e] = reinterpret_cast<const float4*>(h + r0)[e];
+    __syncthreads();
+    for (int it = warp; it < items; it += kWarps) {
+      const int j = it / (kGsChunk / kSub), q = it % (kGsChunk / kSub);
+      const int rb = q * kSub + lane * 4;
+      double s = 0.0;
+      if (j < active) {
+        const float* col = D + (size_t)j * ldd + r0;
+        float4 x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + rb + k * 128));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 y = *reinterpret_cast<const float4*>(hs + rb + k * 128);
+          s += (double)x[k].x * y.x + (double)x[k].y * y.y + (double)x[k].z * y.z + (double)x[k].w * y.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 y = *reinterpret_cast<const float4*>(hs + rb + k * 128);
+          s += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
+        }
+      }
+      s = warp_sum(s);
+      if (lane == 0) acc[warp * nj + j] += s;
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nj; j += kThreads) {
+    double t = 0.0;
+    for (int w = 0; w < kWarps; ++w) t += acc[w * nj + j];
+    part[(size_t)blockIdx.x * stride + j] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int j = threadIdx.x; j < nj; j += kThreads) {
+    double t = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * stride + j];
+    rankp[j] = t;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// ------------------------------------------------------------------ GS pass 2: projection
+// dst = hsrc - sum_j D_j e_j with e_j = sigma_j^2 r_j (r_j rank-ordered sums of pass-1 partials);
+// rankb[0] = ||dst||^2 for this rank. First pass also records alpha_i = diag[i] and pre.
+__global__ void __launch_bounds__(kThreads) gs_pass2_kernel(const float* __restrict__ D, size_t ldd,
+                                                            const float* hsrc, float* dst, int active, size_t ngroups,
+                                                            const double* __restrict__ allp, int world, int stride,
+                                                            double* __restrict__ part, double* __restrict__ rankb,
+                                                            unsigned* ticket, LzDev* st, int it, int safeguard_pass) {
+  if (st->stopped || (safeguard_pass && !st->need_sg)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* e = reinterpret_cast<double*>(smem);
+  __shared__ double red[kWarps];
+  __shared__ bool is_last;
+  for (int j = threadIdx.x; j <= active; j += kThreads) {
+    double r = 0.0;
+    for (int w = 0; w < world; ++w) r += allp[(size_t)w * stride + j];
+    if (j < active) {
+      const double sg = (double)st->sigma[j];
+      e[j] = sg * sg * r;
+      if (!safeguard_pass && j == it && blockIdx.x == 0) st->diag[it] = sg * r;  // alpha = v_i^T h
+    } else if (!safeguard_pass && blockIdx.x == 0) {
+      st->pre = sqrt(r);
+    }
+  }
+  __syncthreads();
+  double ss = 0.0;
+  for (size_t g = blockIdx.x * (size_t)kThreads + threadIdx.x; g < ngroups; g += (size_t)gridDim.x * kThreads) {
+    const float4 h4 = reinterpret_cast<const float4*>(hsrc)[g];
+    double a0 = h4.x, a1 = h4.y, a2 = h4.z, a3 = h4.w;
+    int j = 0;
+    for (; j + 4 <= active; j += 4) {
+      float4 d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const float4*>(D + (size_t)(j + u) * ldd) + g);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double c = e[j + u];
+        a0 -= (double)d[u].x * c;
+        a1 -= (double)d[u].y * c;
+        a2 -= (double)d[u].z * c;
+        a3 -= (double)d[u].w * c;
+      }
+    }
+    for (; j < active; ++j) {
+      const float4 d = __ldg(reinterpret_cast<const float4*>(D + (size_t)j * ldd) + g);
+      const double c = e[j];
+      a0 -= (double)d.x * c;
+      a1 -= (double)d.y * c;
+      a2 -= (double)d.z * c;
+      a3 -= (double)d.w * c;
+    }
+    const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+    reinterpret_cast<float4*>(dst)[g] = o;
+    ss += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+  }
+  const double t = block_sum(ss, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last || threadIdx.x != 0) return;
+  __threadfence();
+  double s = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b];
+  rankb[0] = s;
+  *ticket = 0u;
+}
+
+// ------------------------------------------------------------------ decide (dist_lanczos.cpp:91-111)
+__global__ void lz_decide_kernel(LzDev* st, const double* __restrict__ allb, int world, int stride, int it,
+                                 int safeguard_pass, int safeguard_on, double ratio, double rtol) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->stopped || (safeguard_pass && !st->need_sg)) return;
+  double b2 = 0.0;
+  for (int w = 0; w < world; ++w) b2 += allb[(size_t)w * stride];
+  const double beta = sqrt(b2);
+  const double pre = st->pre;
+  st->beta = beta;
+  if (!safeguard_pass && safeguard_on && beta > rtol * pre && beta < ratio * pre) {
+    st->need_sg = 1;
+    st->safeguards += 1;
+    return;
+  }
+  st->need_sg = 0;
+  if (beta <= rtol * pre) {  // invariant subspace: truncate (:99-108)
+    st->breakdown = 1;
+    st->stopped = 1;
+    st->iters = it + 1;
+    return;
+  }
+  st->off[it] = beta;
+  st->sigma[it + 1] = (float)(1.0 / beta);
+  st->iters = it + 1;
+}
+
+// ------------------------------------------------------------------ operators
+__global__ void diag_apply_kernel(const float* __restrict__ spec, const float* __restrict__ v, const float* vscale,
+                                  float* __restrict__ h, size_t rows) {
+  const float sc = vscale ? *vscale : 1.f;
+  for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < rows; r += (size_t)gridDim.x * blockDim.x)
+    h[r] = (float)((double)spec[r] * (double)(sc * v[r]));
+}
+
+__global__ void dense_apply_kernel(const float* __restrict__ H, size_t n, const float* __restrict__ v,
+                                   const float* vscale, float* __restrict__ h, size_t begin, size_t rows) {
+  const float sc = vscale ? *vscale : 1.f;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if ((size_t)warp >= rows) return;
+  const float* col = H + (begin + warp) * n;  // symmetric: row i == column i
+  double s = 0.0;
+  for (size_t j = lane; j < n; j += 32) s += (double)col[j] * (double)(sc * v[j]);
+  s = warp_sum(s);
+  if (lane == 0) h[warp] = (float)s;
+}
+
+// ------------------------------------------------------------------ tridiagonal eigensolve
+// Single CTA, fp64 implicit-shift QL (linalg.cpp:140-226). Thread 0 runs the scalar recurrence
+// of each sweep and records its Givens rotations; every thread then applies the sweep's
+// rotations, in the reference's order, to its rows of Z (global, column-major n x n).
+// Then stable ascending order (:199-212), extreme selection (lanczos.cpp:72-80) and
+// U'[j][c] = sigma_j * Z[j, idx_c] (folds the lazy basis normalisation into the Ritz GEMM).
+__global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* __restrict__ Z,
+                            float* __restrict__ Usel, double* __restrict__ evsel, double* __restrict__ evall,
+                            int* __restrict__ status) {
+  extern __shared__ double sh[];
+  double* d = sh;
+  double* e = d + n;
+  double* cs = e + n;
+  double* sn = cs + n;
+  int* order = reinterpret_cast<int*>(sn + n);
+  __shared__ int s_mm, s_cnt, s_fail;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += blockDim.x) {
+    d[i] = st->diag[i];
+    e[i] = (i + 1 < n) ? st->off[i] : 0.0;
+  }
+  for (size_t q = tid; q < (size_t)n * n; q += blockDim.x) Z[q] = ((q / n) == (q % n)) ? 1.0 : 0.0;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  const double eps = 2.220446049250313e-16;
+  for (int l = 0; l < n && n > 1; ++l) {
+    int iter = 0;
+    for (;;) {
+      if (tid == 0) {
+        int mm;
+        for (mm = l; mm + 1 < n; ++mm)
+          if (fabs(e[mm]) <= eps * (fabs(d[mm]) + fabs(d[mm + 1]))) break;
+        s_mm = mm;
+        s_cnt = 0;
+        if (mm != l) {
+          if (iter++ == 60) {
+            s_fail = 1;
+          } else {
+            double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+            double r = hypot(g, 1.0);
+            g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+            double s = 1.0, c = 1.0, p = 0.0;
+            bool under = false;
+            int cnt = 0;
+            for (int ii = mm - 1; ii >= l; --ii) {
+              const double f = s * e[ii];
+              const double b = c * e[ii];
+              r = hypot(f, g);
+              e[ii + 1] = r;
+              if (r == 0.0) {
+                d[ii + 1] -= p;
+                e[mm] = 0.0;
+                under = true;
+                break;
+              }
+              s = f / r;
+              c = g / r;
+              g = d[ii + 1] - p;
+              r = (d[ii] - g) * s + 2.0 * c * b;
+              p = s * r;
+              d[ii + 1] = g + p;
+              g = c * r - b;
+              cs[cnt] = c;
+              sn[cnt] = s;
+              ++cnt;
+            }
+            s_cnt = cnt;
+            if (!under) {
+              d[l] -= p;
+              e[l] = g;
+              e[mm] = 0.0;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const int mm = s_mm, cnt = s_cnt, failed = s_fail;
+      __syncthreads();  // everyone has read the sweep descriptor before thread 0 rewrites it
+      if (failed) {
+        if (tid == 0) *status = 1;
+        return;
+      }
+      if (mm == l) break;
+      for (int k = tid; k < n; k += blockDim.x) {
+        for (int q = 0; q < cnt; ++q) {
+          const int ii = mm - 1 - q;
+          const double c = cs[q], s = sn[q];
+          const double f = Z[(size_t)(ii + 1) * n + k];
+          const double z0 = Z[(size_t)ii * n + k];
+          Z[(size_t)(ii + 1) * n + k] = s * z0 + c * f;
+          Z[(size_t)ii * n + k] = c * z0 - s * f;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // stable ascending order
+  for (int i = tid; i < n; i += blockDim.x) {
+    int rank = 0;
+    const double di = d[i];
+    for (int j = 0; j < n; ++j) rank += (d[j] < di) || (d[j] == di && j < i);
+    order[rank] = i;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += blockDim.x) evall[i] = d[order[i]];
+  const int r = keff + leff;
+  for (int c = 0; c < r; ++c) {
+    const int idx = c < keff ? order[n - 1 - c] : order[c - keff];
+    if (tid == 0) evsel[c] = d[idx];
+    for (int j = tid; j < n; j += blockDim.x)
+      Usel[(size_t)j * r + c] = (float)((double)st->sigma[j] * Z[(size_t)idx * n + j]);
+  }
+  if (tid == 0) *status = 0;
+}
+
+// ------------------------------------------------------------------ Ritz vectors
+// V[:, c0:c0+RC] = D[:, 0:me] U'[:, c0:c0+RC]  (bandwidth-bound tall-skinny GEMM)
+constexpr int RC = 32;
+__global__ void __launch_bounds__(256) ritz_kernel(const float* __restrict__ D, size_t ldd, int me,
+                                                   const float* __restrict__ Usel, int r, int c0,
+                                                   float* __restrict__ V, size_t ldv, size_t rows) {
+  extern __shared__ __align__(16) float us[];  // me x RC
+  const int nc = min(RC, r - c0);
+  for (int q = threadIdx.x; q < me * RC; q += blockDim.x) {
+    const int j = q / RC, c = q % RC;
+    us[q] = c < nc ? Usel[(size_t)j * r + c0 + c] : 0.f;
+  }
+  __syncthreads();
+  for (size_t row = blockIdx.x * (size_t)blockDim.x + threadIdx.x; row < rows; row += (size_t)gridDim.x * blockDim.x) {
+    float acc[RC];
+#pragma unroll
+    for (int c = 0; c < RC; ++c) acc[c] = 0.f;
+    for (int j = 0; j < me; ++j) {
+      const float x = __ldg(D + (size_t)j * ldd + row);
+      const float4* u4 = reinterpret_cast<const float4*>(us + j * RC);
+#pragma unroll
+      for (int q = 0; q < RC / 4; ++q) {
+        const float4 u = u4[q];
+        acc[4 * q] = fmaf(x, u.x, acc[4 * q]);
+        acc[4 * q + 1] = fmaf(x, u.y, acc[4 * q + 1]);
+        acc[4 * q + 2] = fmaf(x, u.z, acc[4 * q + 2]);
+        acc[4 * q + 3] = fmaf(x, u.w, acc[4 * q + 3]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < RC; ++c)
+      if (c < nc) V[(size_t)(c0 + c) * ldv + row] = acc[c];
+  }
+}
+
+// per-column argmax |x| with the lowest index on ties (lanczos.cpp:82-94)
+__global__ void col_argmax_kernel(const float* __restrict__ V, size_t ldv, size_t rows, size_t begin,
+                                  double* __restrict__ out /* r x 3: maxabs, global index, value */) {
+  const int c = blockIdx.x;
+  const float* col = V + (size_t)c * ldv;
+  float best = -1.f;
+  size_t bi = 0;
+  float bv = 0.f;
+  for (size_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    const float a = fabsf(col[r]);
+    if (a > best) {
+      best = a;
+      bi = r;
+      bv = col[r];
+    }
+  }
+  __shared__ float sb[1024];
+  __shared__ size_t si[1024];
+  __shared__ float sv[1024];
+  sb[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  sv[threadIdx.x] = bv;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const float ob = sb[threadIdx.x + s];
+      const size_t oi = si[threadIdx.x + s];
+      if (ob > sb[threadIdx.x] || (ob == sb[threadIdx.x] && oi < si[threadIdx.x])) {
+        sb[threadIdx.x] = ob;
+        si[threadIdx.x] = oi;
+        sv[threadIdx.x] = sv[threadIdx.x + s];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[3 * c] = sb[0];
+    out[3 * c + 1] = (double)(begin + si[0]);
+    out[3 * c + 2] = sv[0];
+  }
+}
+
+int grid_for(dho2g_ctx* ctx, size_t work, int threads, int per_sm = 4) {
+  const size_t want = cdiv(work, threads);
+  const size_t cap = (size_t)ctx->sm_count * per_sm;
+  return (int)std::max<size_t>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ dho2g_op::apply
+void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, size_t begin, size_t rows, size_t base) {
+  cudaStream_t st = ctx->stream;
+  if (kind == 0) {
+    dho2g_mlp* m = mlp;
+    if (m->w_cur != wptr || !weights_loaded || m->input_owner != this) {
+      if (idx.p) mlp_set_input(m, Xptr, yptr, idx.p + b0, b1 - b0, true);
+      else mlp_set_input(m, Xptr + b0 * m->sizes[0], yptr + b0, nullptr, b1 - b0, true);
+      mlp_load_weights(m, wptr);
+      m->input_owner = this;
+      weights_loaded = true;
+    }
+    float* out = ctx->world == 1 ? h_shard : hfull.p;
+    if (b1 > b0) {
+      mlp_hvp_dev(m, vfull, vscale, b1 - b0, ncls, scale, out);
+    } else {
+      DHO2G_CUDA(cudaMemsetAsync(out, 0, n * sizeof(float), st));
+    }
+    if (ctx->world > 1) ctx->reduce_scatter_f32(hfull.p, h_shard, base);
+    return;
+  }
+  if (kind == 1) {
+    diag_apply_kernel<<<grid_for(ctx, rows, 256), 256, 0, st>>>(mat.p + begin, vfull + begin, vscale, h_shard, rows);
+    DHO2G_LAUNCH();
+    return;
+  }
+  if (kind == 2) {
+    dense_apply_kernel<<<cdiv(rows * 32, 256), 256, 0, st>>>(mat.p, n, vfull, vscale, h_shard, begin, rows);
+    DHO2G_LAUNCH();
+    return;
+  }
+  // host callback (tests / reference HvpFn adapters)
+  pin.ensure(n + 1);
+  DHO2G_CUDA(cudaMemcpyAsync(pin.p, vfull, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (vscale) DHO2G_CUDA(cudaMemcpyAsync(pin.p + n, vscale, sizeof(float), cudaMemcpyDeviceToHost, st));
+  DHO2G_CUDA(cudaStreamSynchronize(st));
+  const double sc = vscale ? pin.p[n] : 1.0;
+  hv_in.resize(n);
+  hv_out.assign(n, 0.0);
+  for (size_t i = 0; i < n; ++i) hv_in[i] = sc * (double)pin.p[i];
+  fn(user, hv_in.data(), hv_out.data(), n);
+  for (size_t r = 0; r < rows; ++r) pin.p[r] = (float)hv_out[begin + r];
+  DHO2G_CUDA(cudaMemcpyAsync(h_shard, pin.p, rows * sizeof(float), cudaMemcpyHostToDevice, st));
+  DHO2G_CUDA(cudaStreamSynchronize(st));
+}
+
+namespace dho2g {
+
+void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
+  lz->ctx = ctx;
+  lz->n = n;
+  lz->m = m;
+  shard_range(n, ctx->world, ctx->rank, &lz->begin, &lz->end);
+  lz->rows = lz->end - lz->begin;
+  lz->base = cdiv(n, (size_t)ctx->world);
+  lz->ldd = round_up(std::max<size_t>(lz->base, 1), kGsChunk);
+  lz->D.alloc(lz->ldd * (m + 1));
+  lz->h.alloc(lz->ldd);
+  if (ctx->world > 1) lz->vfull.alloc(lz->base * ctx->world);
+  lz->st.alloc(1);
+  const int g1 = (int)std::min<size_t>(cdiv(lz->ldd, kGsChunk), (size_t)ctx->sm_count * 4);
+  const int g2 = (int)std::min<size_t>(cdiv(lz->ldd / 4, kThreads), (size_t)ctx->sm_count * 4);
+  lz->part.alloc((size_t)std::max(g1, g2) * (m + 2) + 8);
+  lz->rankp.alloc(m + 2);
+  lz->allp.alloc((m + 2) * ctx->world);
+  lz->ticket.alloc(2);
+}
+
+void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
+  dho2g_ctx* ctx = lz->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t m = lz->m;
+  const int world = ctx->world;
+  const int stride = (int)(m + 2);
+  cudaEvent_t e0, e1;
+  DHO2G_CUDA(cudaEventCreate(&e0));
+  DHO2G_CUDA(cudaEventCreate(&e1));
+  DHO2G_CUDA(cudaEventRecord(e0, st));
+
+  // v1 (lanczos.cpp:18-26) into column 0, raw; sigma_0 = 1/||v1||
+  {
+    const int gb = grid_for(ctx, lz->rows, 256);
+    gauss_kernel<<<gb, 256, 0, st>>>(seed * 0x9e3779b97f4a7c15ULL + 0x1234567ULL, lz->begin, lz->rows, lz->D.p,
+                                     lz->part.p);
+    gauss_norm_kernel<<<1, 32, 0, st>>>(lz->part.p, gb, lz->rankp.p);
+    DHO2G_LAUNCH();
+    ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);
+    lz_init_kernel<<<1, 32, 0, st>>>(lz->st.p, lz->allp.p, world, 1);
+    DHO2G_LAUNCH();
+  }
+
+  const int nchunks = (int)(lz->ldd / kGsChunk);
+  const int g1 = std::min(nchunks, ctx->sm_count * 4);
+  const size_t ngroups = lz->ldd / 4;
+  const int g2 = (int)std::min<size_t>(cdiv(ngroups, kThreads), (size_t)ctx->sm_count * 4);
+  const double* allp = world > 1 ? lz->allp.p : lz->rankp.p;
+  const double* allb = world > 1 ? lz->allp.p : lz->rankp.p;
+
+  for (size_t i = 0; i < m; ++i) {
+    const int active = (int)i + 1;
+    float* Di = lz->D.p + i * lz->ldd;
+    float* Dn = lz->D.p + (i + 1) * lz->ldd;
+    const float* vfull = Di;
+    if (world > 1) {
+      ctx->allgather_f32(Di, lz->vfull.p, lz->base);
+      vfull = lz->vfull.p;
+    }
+    op->apply(vfull, &lz->st.p->sigma[i], lz->h.p, lz->begin, lz->rows, lz->base);
+    const size_t smem1 = kGsChunk * sizeof(float) + (size_t)kWarps * (active + 1) * sizeof(double);
+    const size_t smem2 = (size_t)(active + 1) * sizeof(double);
+    for (int pass = 0; pass < (lz->opts.reorth_safeguard ? 2 : 1); ++pass) {
+      const float* hsrc = pass == 0 ? lz->h.p : Dn;
+      // algorithmic bytes: active columns of D + h (pass 1); + h' write (pass 2)
+      const double gsb = 4.0 * (double)lz->rows * (double)(active + 1);
+      int ks = pass == 0 ? ctx->kt_begin() : -1;
+      gs_pass1_kernel<<<g1, kThreads, smem1, st>>>(lz->D.p, lz->ldd, hsrc, active, nchunks, stride, lz->part.p,
+                                                    lz->rankp.p, lz->ticket.p, lz->st.p, pass);
+      DHO2G_LAUNCH();
+      ctx->kt_end(ks, "gs_pass1", gsb);
+      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, stride);
+      ks = pass == 0 ? ctx->kt_begin() : -1;
+      gs_pass2_kernel<<<g2, kThreads, smem2, st>>>(lz->D.p, lz->ldd, hsrc, Dn, active, ngroups, allp, world, stride,
+                                                    lz->part.p, lz->rankp.p, lz->ticket.p + 1, lz->st.p, (int)i, pass);
+      DHO2G_LAUNCH();
+      ctx->kt_end(ks, "gs_pass2", gsb + 4.0 * (double)lz->rows);
+      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);
+      lz_decide_kernel<<<1, 32, 0, st>>>(lz->st.p, allb, world, world > 1 ? 1 : 1, (int)i, pass,
+                                         lz->opts.reorth_safeguard, lz->opts.safeguard_ratio, lz->opts.breakdown_rtol);
+      DHO2G_LAUNCH();
+    }
+  }
+  DHO2G_CUDA(cudaEventRecord(e1, st));
+  DHO2G_CUDA(cudaMemcpyAsync(&lz->host, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, st));
+  DHO2G_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  DHO2G_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  lz->ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (lz->host.stopped == 0) lz->host.iters = (int)m;
+  ctx->bump("lanczos_runs", 1);
+  ctx->bump("lanczos_ms", ms);
+}
+
+void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese) {
+  cudaStream_t st = ctx->stream;
+  const int me = lz->host.iters;
+  ese->ctx = ctx;
+  ese->n = lz->n;
+  ese->rows = lz->rows;
+  ese->begin = lz->begin;
+  ese->end = lz->end;
+  ese->ldv = lz->ldd;
+  if (k + l == 0) {
+    ese->r = 0;
+    return;
+  }
+  if (me < 1) fail(DHO2G_ARGUMENT, "extract_ese_distributed: empty Lanczos state");
+  if (k + l > (size_t)me) fail(DHO2G_ARGUMENT, "extract_ese_distributed: k+l exceeds the filled block");
+  const int r = (int)(k + l);
+  ese->r = r;
+  DevBuf<double> Z((size_t)me * me);
+  DevBuf<float> U((size_t)me * r);
+  ese->ev_dev.alloc(r);
+  DevBuf<double> evall(me);
+  DevBuf<int> status(1);
+  const size_t smem = (size_t)me * 4 * sizeof(double) + (size_t)me * sizeof(int);
+  if (smem > 48 * 1024)
+    DHO2G_CUDA(cudaFuncSetAttribute(tql2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int threads = (int)std::min<size_t>(1024, round_up((size_t)me, 32));
+  tql2_kernel<<<1, threads, smem, st>>>(lz->st.p, me, (int)k, (int)l, Z.p, U.p, ese->ev_dev.p, evall.p, status.p);
+  DHO2G_LAUNCH();
+  ese->V.alloc(ese->ldv * r);
+  for (int c0 = 0; c0 < r; c0 += RC) {
+    const size_t sm = (size_t)me * RC * sizeof(float);
+    if (sm > 48 * 1024)
+      DHO2G_CUDA(cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ritz_kernel<<<grid_for(ctx, lz->rows, 256, 8), 256, sm, st>>>(lz->D.p, lz->ldd, me, U.p, r, c0, ese->V.p, ese->ldv,
+                                                                  lz->rows);
+    DHO2G_LAUNCH();
+  }
+  DevBuf<double> am((size_t)3 * r);
+  DevBuf<double> amall((size_t)3 * r * ctx->world);
+  col_argmax_kernel<<<r, 1024, 0, st>>>(ese->V.p, ese->ldv, lz->rows, lz->begin, am.p);
+  DHO2G_LAUNCH();
+  ctx->allgather_f64(am.p, amall.p, (size_t)3 * r);
+  std::vector<double> h_am((size_t)3 * r * ctx->world);
+  int h_status = 0;
+  ese->eigvals.resize(r);
+  DHO2G_CUDA(cudaMemcpyAsync(h_am.data(), amall.p, h_am.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  DHO2G_CUDA(cudaMemcpyAsync(ese->eigvals.data(), ese->ev_dev.p, r * sizeof(double), cudaMemcpyDeviceToHost, st));
+  DHO2G_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DHO2G_CUDA(cudaStreamSynchronize(st));
+  if (h_status) fail(DHO2G_NUMERIC, "tridiag_eig: QL iteration did not converge");
+  ese->sign.assign(r, 1.f);
+  for (int c = 0; c < r; ++c) {
+    double best = -1.0, bidx = 0.0, bval = 0.0;
+    for (int w = 0; w < ctx->world; ++w) {
+      const double* p = h_am.data() + (size_t)w * 3 * r + 3 * c;
+      if (p[0] > best || (p[0] == best && p[1] < bidx)) {
+        best = p[0];
+        bidx = p[1];
+        bval = p[2];
+      }
+    }
+    ese->sign[c] = bval < 0.0 ? -1.f : 1.f;
+  }
+}
+
+}  // namespace dho2g

@@ -1,0 +1,466 @@
+// Device MLP oracle (reference: proj/src/oracle.cpp:288-687) — forward, backward and the
+// Pearlmutter R-op as batched split-BF16x3 GEMMs plus fused tile epilogues.
+//
+// Layout (reference oracle.cpp:304-324): flat params, per layer W (out x in, row-major) then b.
+// Per layer t with in = s_t, out = s_{t+1} the contractions are (B = batch):
+//   forward    Z  = A W^T            RZ = [A | RA] [V | W]^T         (K = in, 2 in)
+//   backward   U  = D W              RU = [D | RD] [V^T | W^T]^T     (K = out, 2 out)
+//   weight     hvW = [RD^T | D^T] [A^T | RA^T]^T                     (K = 2B)
+// with every operand stored K-major as (hi, lo) bf16 pairs so all GEMMs are "TN" for tcgen05.
+#include <cmath>
+
+#include "internal.h"
+
+using namespace dho2g;
+
+void dho2g_mlp::ensure_batch(size_t B) {
+  if (B <= Bcap) return;
+  const size_t nB = round_up(B, 128);
+  const size_t nBp = round_up(nB, 8);
+  const int Ls = L;
+  AR_hi.resize(Ls); AR_lo.resize(Ls); ART_hi.resize(Ls); ART_lo.resize(Ls);
+  DR_hi.resize(Ls + 1); DR_lo.resize(Ls + 1); DRT_hi.resize(Ls + 1); DRT_lo.resize(Ls + 1);
+  a32.resize(Ls + 1); ra32.resize(Ls + 1); d32.resize(Ls + 1); rd32.resize(Ls + 1);
+  for (int j = 0; j <= Ls; ++j) {
+    const size_t s = sizes[j], P = round_up(s, 8);
+    if (j < Ls) {
+      AR_hi[j].alloc(nB * 2 * P); AR_lo[j].alloc(nB * 2 * P);
+      ART_hi[j].alloc(s * 2 * nBp); ART_lo[j].alloc(s * 2 * nBp);
+    }
+    if (j >= 1) {
+      DR_hi[j].alloc(nB * 2 * P); DR_lo[j].alloc(nB * 2 * P);
+      DRT_hi[j].alloc(s * 2 * nBp); DRT_lo[j].alloc(s * 2 * nBp);
+      a32[j].alloc(nB * s); ra32[j].alloc(nB * s); d32[j].alloc(nB * s); rd32[j].alloc(nB * s);
+    }
+  }
+  Z.alloc(nB * smax);
+  RZ.alloc(nB * smax);
+  lab.alloc(nB);
+  sample_loss.alloc(nB);
+  sample_correct.alloc(nB);
+  Bcap = nB;
+  Bpcap = nBp;
+}
+
+namespace {
+
+constexpr int TILE = 32;
+
+// ------------------------------------------------------------------ weight operand packing
+// WV[t][o][h*Pin + k] = p(o,k) (k < in, zero-padded to Pin); WVt[t][k][h*Pout + o] likewise.
+__global__ void pack_weights_kernel(const float* __restrict__ p, const float* __restrict__ pscale, int in, int out,
+                                    int Pin, int Pout, int half, bf16* __restrict__ WVh, bf16* __restrict__ WVl,
+                                    bf16* __restrict__ WVth, bf16* __restrict__ WVtl) {
+  __shared__ float sh[TILE][TILE + 1];
+  const int k0 = blockIdx.x * TILE, o0 = blockIdx.y * TILE;
+  const float sc = pscale ? *pscale : 1.0f;
+  for (int i = threadIdx.y; i < TILE; i += blockDim.y) {
+    const int o = o0 + i, k = k0 + threadIdx.x;
+    float x = 0.f;
+    if (o < out && k < in) x = p[(size_t)o * in + k] * sc;
+    sh[i][threadIdx.x] = x;
+    if (o < out && k < Pin) {
+      bf16 h, l;
+      split_bf16(x, h, l);
+      const size_t idx = (size_t)o * (2 * Pin) + (size_t)half * Pin + k;
+      WVh[idx] = h;
+      WVl[idx] = l;
+    }
+  }
+  if (!WVth) return;
+  __syncthreads();
+  for (int i = threadIdx.y; i < TILE; i += blockDim.y) {
+    const int k = k0 + i, o = o0 + threadIdx.x;
+    if (k < in && o < Pout) {
+      const float x = sh[threadIdx.x][i];
+      bf16 h, l;
+      split_bf16(x, h, l);
+      const size_t idx = (size_t)k * (2 * Pout) + (size_t)half * Pout + o;
+      WVth[idx] = h;
+      WVtl[idx] = l;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ activation tile epilogues
+enum Mode { M_INPUT = 0, M_FWD = 1, M_FWD_OUT = 2, M_BWD = 3, M_DPACK = 4 };
+
+struct TileArgs {
+  int B, s, P, Bp, ldT;  // batch, width, half width, padded batch, transposed row stride
+  bool with_r, relu;
+  // sources
+  const float* X; const int64_t* idx; int ldX;  // M_INPUT
+  const float* Zs; const float* RZs;             // GEMM outputs (B x s)
+  const float* bias; const float* vbias; const float* vscale;
+  const float* a_in; const float* ra_in;         // M_BWD: level activations
+  const float* d_in; const float* rd_in;         // M_DPACK
+  // fp32 outputs (B x s)
+  float* o0; float* o1;
+  // packed outputs
+  bf16 *Rh, *Rl;   // row-major pairs (B x 2P): x0 -> half 0, x1 -> half 1
+  bf16 *Th, *Tl;   // transposed pairs (s x ldT): x0 -> half t0, x1 -> half t1
+  int t0, t1;
+};
+
+template <int MODE>
+__global__ void tile_epilogue_kernel(TileArgs a) {
+  __shared__ float s0[TILE][TILE + 1], s1[TILE][TILE + 1];
+  const int k0 = blockIdx.x * TILE, b0 = blockIdx.y * TILE;
+  const float vsc = (a.vscale && a.with_r) ? *a.vscale : 1.0f;
+  for (int i = threadIdx.y; i < TILE; i += blockDim.y) {
+    const int b = b0 + i, k = k0 + threadIdx.x;
+    float x0 = 0.f, x1 = 0.f;
+    const bool valid = b < a.B && k < a.s;
+    if (valid) {
+      const size_t e = (size_t)b * a.s + k;
+      if (MODE == M_INPUT) {
+        const int64_t row = a.idx ? a.idx[b] : b;
+        x0 = a.X[(size_t)row * a.ldX + k];
+      } else if (MODE == M_FWD || MODE == M_FWD_OUT) {
+        const float z = a.Zs[e] + a.bias[k];
+        if (MODE == M_FWD_OUT) {
+          x0 = z;
+          if (a.with_r) x1 = a.RZs[e] + vsc * a.vbias[k];
+        } else {
+          // oracle.cpp:559-563: a = act(z); ra = act'(a) * rz
+          const float av = a.relu ? fmaxf(z, 0.f) : tanhf(z);
+          x0 = av;
+          if (a.with_r) {
+            const float ap = a.relu ? (av > 0.f ? 1.f : 0.f) : 1.f - av * av;
+            x1 = ap * (a.RZs[e] + vsc * a.vbias[k]);
+          }
+        }
+        a.o0[e] = x0;
+        if (a.with_r) a.o1[e] = x1;
+      } else if (MODE == M_BWD) {
+        // oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh only)
+        const float u = a.Zs[e];
+        const float av = a.a_in[e];
+        const float ap = a.relu ? (av > 0.f ? 1.f : 0.f) : 1.f - av * av;
+        x0 = u * ap;
+        if (a.with_r) {
+          float rap = 0.f;
+          if (!a.relu && ap != 0.f) rap = -2.f * av * a.ra_in[e];
+          x1 = a.RZs[e] * ap + u * rap;
+        }
+        a.o0[e] = x0;
+        if (a.with_r) a.o1[e] = x1;
+      } else {  // M_DPACK
+        x0 = a.d_in[e];
+        if (a.with_r) x1 = a.rd_in[e];
+      }
+    }
+    if (MODE == M_FWD_OUT) continue;
+    s0[i][threadIdx.x] = x0;
+    s1[i][threadIdx.x] = x1;
+    if (b < a.B && k < a.P && a.Rh) {
+      bf16 h, l;
+      const size_t r = (size_t)b * (2 * a.P) + k;
+      split_bf16(x0, h, l);
+      a.Rh[r] = h;
+      a.Rl[r] = l;
+      if (a.with_r) {
+        split_bf16(x1, h, l);
+        a.Rh[r + a.P] = h;
+        a.Rl[r + a.P] = l;
+      }
+    }
+  }
+  if (MODE == M_FWD_OUT || !a.Th) return;
+  __syncthreads();
+  for (int i = threadIdx.y; i < TILE; i += blockDim.y) {
+    const int k = k0 + i, b = b0 + threadIdx.x;
+    if (k < a.s && b < a.Bp) {
+      const size_t r = (size_t)k * a.ldT + b;
+      bf16 h, l;
+      if (a.t0 >= 0) {
+        split_bf16(s0[threadIdx.x][i], h, l);
+        a.Th[r + (size_t)a.t0 * a.Bp] = h;
+        a.Tl[r + (size_t)a.t0 * a.Bp] = l;
+      }
+      if (a.with_r && a.t1 >= 0) {
+        split_bf16(s1[threadIdx.x][i], h, l);
+        a.Th[r + (size_t)a.t1 * a.Bp] = h;
+        a.Tl[r + (size_t)a.t1 * a.Bp] = l;
+      }
+    }
+  }
+}
+
+template <int MODE>
+void launch_tile(cudaStream_t st, const TileArgs& a) {
+  dim3 grid(cdiv(std::max(a.P, a.s), TILE), cdiv(std::max(a.Bp, a.B), TILE));
+  tile_epilogue_kernel<MODE><<<grid, dim3(TILE, 8), 0, st>>>(a);
+  DHO2G_LAUNCH();
+}
+
+// ------------------------------------------------------------------ output layer delta
+// oracle.cpp:476-495 (delta) and :572-599 (R-delta); also per-sample loss / correctness.
+__global__ void output_delta_kernel(int B, int O, int mse, int ncls, int with_r, double scale,
+                                    const float* __restrict__ z, const float* __restrict__ rz,
+                                    const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
+                                    double* __restrict__ loss, int* __restrict__ correct) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float* o = z + (size_t)b * O;
+  const float* ro = with_r ? rz + (size_t)b * O : nullptr;
+  float* dd = d + (size_t)b * O;
+  float* rdd = with_r ? rd + (size_t)b * O : nullptr;
+  const float y = lab[b];
+  int best = 0;
+  for (int j = 1; j < O; ++j)
+    if (o[j] > o[best]) best = j;
+  correct[b] = (ncls > 0 && best == (int)y) ? 1 : 0;
+  if (!mse) {
+    const int lbl = (int)y;
+    const float mx = o[best];
+    double den = 0.0;
+    for (int j = 0; j < O; ++j) den += exp((double)o[j] - (double)mx);
+    double sdot = 0.0;
+    for (int j = 0; j < O; ++j) {
+      const double soft = exp((double)o[j] - (double)mx) / den;
+      dd[j] = (float)((soft - (j == lbl ? 1.0 : 0.0)) * scale);
+      if (with_r) sdot += soft * ro[j];
+    }
+    if (with_r)
+      for (int j = 0; j < O; ++j) {
+        const double soft = exp((double)o[j] - (double)mx) / den;
+        rdd[j] = (float)(soft * (ro[j] - sdot) * scale);
+      }
+    loss[b] = (double)mx + log(den) - (double)o[lbl];
+  } else {
+    double acc = 0.0;
+    for (int j = 0; j < O; ++j) {
+      const float t = ncls > 0 ? (j == (int)y ? 1.f : 0.f) : (j == 0 ? y : 0.f);
+      const float df = o[j] - t;
+      dd[j] = (float)(df * scale);
+      if (with_r) rdd[j] = (float)(ro[j] * scale);
+      acc += 0.5 * (double)df * (double)df;
+    }
+    loss[b] = acc;
+  }
+}
+
+// label gather
+__global__ void gather_labels_kernel(int B, const float* __restrict__ y, const int64_t* __restrict__ idx,
+                                     float* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) out[b] = y[idx ? idx[b] : b];
+}
+
+// bias gradient: out[o] = sum_b src[b, o] (fp64 accumulation, fixed order over fixed chunks)
+constexpr int kBiasChunks = 32;
+__global__ void bias_partial_kernel(int B, int O, const float* __restrict__ src, double* __restrict__ part) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= O) return;
+  const int c = blockIdx.y;
+  const int per = (B + kBiasChunks - 1) / kBiasChunks;
+  const int b0 = c * per, b1 = min(B, b0 + per);
+  double s = 0.0;
+  for (int b = b0; b < b1; ++b) s += src[(size_t)b * O + o];
+  part[(size_t)c * O + o] = s;
+}
+__global__ void bias_final_kernel(int O, const double* __restrict__ part, float* __restrict__ out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= O) return;
+  double s = 0.0;
+  for (int c = 0; c < kBiasChunks; ++c) s += part[(size_t)c * O + o];
+  out[o] = (float)s;
+}
+
+// deterministic single-CTA sum of per-sample loss / correct into acc2[0], acc2[1] (+=)
+__global__ void eval_reduce_kernel(int B, const double* __restrict__ loss, const int* __restrict__ correct,
+                                   double* __restrict__ acc2) {
+  __shared__ double sh[32];
+  double l = 0.0, c = 0.0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    l += loss[b];
+    c += correct[b];
+  }
+  const double L = block_sum(l, sh);
+  const double Cc = block_sum(c, sh);
+  if (threadIdx.x == 0) {
+    acc2[0] += L;
+    acc2[1] += Cc;
+  }
+}
+
+}  // namespace
+
+namespace dho2g {
+
+void mlp_load_weights(dho2g_mlp* m, const float* w) {
+  cudaStream_t st = m->ctx->stream;
+  m->w_cur = w;
+  for (int t = 0; t < m->L; ++t) {
+    const LayerDesc& ld = m->layers[t];
+    dim3 grid(cdiv(std::max(ld.Pin, ld.in), TILE), cdiv(std::max(ld.Pout, ld.out), TILE));
+    pack_weights_kernel<<<grid, dim3(TILE, 8), 0, st>>>(
+        w + ld.w_off, nullptr, ld.in, ld.out, ld.Pin, ld.Pout, 1, m->WV_hi[t].p, m->WV_lo[t].p,
+        t > 0 ? m->WVt_hi[t].p : nullptr, t > 0 ? m->WVt_lo[t].p : nullptr);
+    DHO2G_LAUNCH();
+  }
+}
+
+void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale) {
+  cudaStream_t st = m->ctx->stream;
+  for (int t = 0; t < m->L; ++t) {
+    const LayerDesc& ld = m->layers[t];
+    dim3 grid(cdiv(std::max(ld.Pin, ld.in), TILE), cdiv(std::max(ld.Pout, ld.out), TILE));
+    pack_weights_kernel<<<grid, dim3(TILE, 8), 0, st>>>(
+        v + ld.w_off, vscale, ld.in, ld.out, ld.Pin, ld.Pout, 0, m->WV_hi[t].p, m->WV_lo[t].p,
+        t > 0 ? m->WVt_hi[t].p : nullptr, t > 0 ? m->WVt_lo[t].p : nullptr);
+    DHO2G_LAUNCH();
+  }
+}
+
+void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool /*with_r*/) {
+  m->ensure_batch(B);
+  m->input_owner = nullptr;
+  cudaStream_t st = m->ctx->stream;
+  TileArgs a{};
+  const int s0 = (int)m->sizes[0];
+  a.B = (int)B; a.s = s0; a.P = (int)round_up(s0, 8); a.Bp = (int)round_up(B, 8); a.ldT = (int)(2 * m->Bpcap);
+  a.with_r = false;
+  a.X = X; a.idx = idx; a.ldX = s0;
+  a.Rh = m->AR_hi[0].p; a.Rl = m->AR_lo[0].p; a.Th = m->ART_hi[0].p; a.Tl = m->ART_lo[0].p;
+  a.t0 = 0; a.t1 = -1;
+  launch_tile<M_INPUT>(st, a);
+  gather_labels_kernel<<<cdiv(B, 256), 256, 0, st>>>((int)B, y, idx, m->lab.p);
+  DHO2G_LAUNCH();
+}
+
+void mlp_forward(dho2g_mlp* m, const float* w, size_t B, bool with_r) {
+  dho2g_ctx* ctx = m->ctx;
+  const int Bp = (int)round_up(B, 8);
+  for (int t = 0; t < m->L; ++t) {
+    const LayerDesc& ld = m->layers[t];
+    const bool last = t + 1 == m->L;
+    const int lda = 2 * ld.Pin;
+    // Z = A W^T
+    gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
+          m->WV_lo[t].p + ld.Pin, lda, m->Z.p, ld.out, 1.0f);
+    if (with_r) {
+      // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
+      const int K = t == 0 ? ld.in : 2 * ld.Pin;
+      gemm3(ctx, (int)B, ld.out, K, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p, m->WV_lo[t].p, lda, m->RZ.p,
+            ld.out, 1.0f);
+    }
+    TileArgs a{};
+    a.B = (int)B; a.s = ld.out; a.P = ld.Pout; a.Bp = Bp; a.ldT = (int)(2 * m->Bpcap);
+    a.with_r = with_r; a.relu = m->act == 1;
+    a.Zs = m->Z.p; a.RZs = m->RZ.p; a.bias = w + ld.b_off; a.vbias = m->v_bias_ptr ? m->v_bias_ptr + ld.b_off : nullptr;
+    a.vscale = m->v_scale_ptr;
+    a.o0 = m->a32[t + 1].p; a.o1 = m->ra32[t + 1].p;
+    if (last) {
+      launch_tile<M_FWD_OUT>(ctx->stream, a);
+    } else {
+      a.Rh = m->AR_hi[t + 1].p; a.Rl = m->AR_lo[t + 1].p; a.Th = m->ART_hi[t + 1].p; a.Tl = m->ART_lo[t + 1].p;
+      a.t0 = 0; a.t1 = 1;
+      launch_tile<M_FWD>(ctx->stream, a);
+    }
+  }
+}
+
+void mlp_output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool with_r) {
+  cudaStream_t st = m->ctx->stream;
+  const int L = m->L;
+  const int O = (int)m->sizes[L];
+  output_delta_kernel<<<cdiv(B, 128), 128, 0, st>>>((int)B, O, m->loss, (int)ncls, with_r ? 1 : 0, scale,
+                                                     m->a32[L].p, m->ra32[L].p, m->lab.p, m->d32[L].p, m->rd32[L].p,
+                                                     m->sample_loss.p, m->sample_correct.p);
+  DHO2G_LAUNCH();
+}
+
+static void pack_delta_level(dho2g_mlp* m, int j, size_t B, bool with_r, int mode, const float* U, const float* RU) {
+  TileArgs a{};
+  const int s = (int)m->sizes[j];
+  a.B = (int)B; a.s = s; a.P = (int)round_up(s, 8); a.Bp = (int)round_up(B, 8); a.ldT = (int)(2 * m->Bpcap);
+  a.with_r = with_r; a.relu = m->act == 1;
+  a.Rh = m->DR_hi[j].p; a.Rl = m->DR_lo[j].p; a.Th = m->DRT_hi[j].p; a.Tl = m->DRT_lo[j].p;
+  // transposed pair is [rd^T | d^T]: d -> half 1, rd -> half 0
+  a.t0 = 1; a.t1 = 0;
+  if (mode == M_DPACK) {
+    a.d_in = m->d32[j].p; a.rd_in = m->rd32[j].p;
+    launch_tile<M_DPACK>(m->ctx->stream, a);
+  } else {
+    a.Zs = U; a.RZs = RU; a.a_in = m->a32[j].p; a.ra_in = m->ra32[j].p;
+    a.o0 = m->d32[j].p; a.o1 = m->rd32[j].p;
+    launch_tile<M_BWD>(m->ctx->stream, a);
+  }
+}
+
+static void bias_sum(dho2g_mlp* m, int B, int O, const float* src, float* out) {
+  m->red.ensure((size_t)kBiasChunks * m->smax);
+  cudaStream_t st = m->ctx->stream;
+  bias_partial_kernel<<<dim3(cdiv(O, 128), kBiasChunks), 128, 0, st>>>(B, O, src, m->red.p);
+  bias_final_kernel<<<cdiv(O, 128), 128, 0, st>>>(O, m->red.p, out);
+  DHO2G_LAUNCH();
+}
+
+void mlp_backward(dho2g_mlp* m, const float* /*w*/, size_t B, float* out, bool with_r) {
+  dho2g_ctx* ctx = m->ctx;
+  const int L = m->L;
+  const int Bp = (int)round_up(B, 8);
+  const int ldT = (int)(2 * m->Bpcap);
+  pack_delta_level(m, L, B, with_r, M_DPACK, nullptr, nullptr);
+  for (int t = L - 1; t >= 0; --t) {
+    const LayerDesc& ld = m->layers[t];
+    const int j = t + 1;
+    // weight block: hvW = [RD^T | D^T] [A^T | RA^T]^T; grad: D^T A
+    if (with_r) {
+      const int K = t == 0 ? Bp : 2 * Bp;
+      gemm3(ctx, ld.out, ld.in, K, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p, m->ART_lo[t].p, ldT,
+            out + ld.w_off, ld.in, 1.0f);
+    } else {
+      gemm3(ctx, ld.out, ld.in, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p, m->ART_lo[t].p,
+            ldT, out + ld.w_off, ld.in, 1.0f);
+    }
+    bias_sum(m, (int)B, ld.out, with_r ? m->rd32[j].p : m->d32[j].p, out + ld.b_off);
+    if (t > 0) {
+      const int lda = 2 * ld.Pout;
+      // U = D W ; RU = [D | RD] [V^T | W^T]^T
+      gemm3(ctx, (int)B, ld.in, ld.out, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p + ld.Pout,
+            m->WVt_lo[t].p + ld.Pout, lda, m->Z.p, ld.in, 1.0f);
+      if (with_r)
+        gemm3(ctx, (int)B, ld.in, 2 * ld.Pout, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p, m->WVt_lo[t].p, lda,
+              m->RZ.p, ld.in, 1.0f);
+      pack_delta_level(m, t, B, with_r, M_BWD, m->Z.p, m->RZ.p);
+    }
+  }
+}
+
+void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
+                  size_t ncls, double scale, float* g) {
+  mlp_set_input(m, X, y, idx, B, false);
+  mlp_forward(m, w, B, false);
+  mlp_output_delta(m, B, ncls, scale, false);
+  mlp_backward(m, w, B, g, false);
+}
+
+void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv) {
+  // input and weights must already be loaded (mlp_set_input / mlp_load_weights)
+  m->v_bias_ptr = v;
+  m->v_scale_ptr = vscale;
+  mlp_load_direction(m, v, vscale);
+  mlp_forward(m, m->w_cur, B, true);
+  mlp_output_delta(m, B, ncls, scale, true);
+  mlp_backward(m, m->w_cur, B, hv, true);
+}
+
+void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
+                  size_t ncls, double* acc2) {
+  mlp_set_input(m, X, y, idx, B, false);
+  mlp_forward(m, w, B, false);
+  mlp_output_delta(m, B, ncls, 1.0, false);
+  eval_reduce_kernel<<<1, 1024, 0, m->ctx->stream>>>((int)B, m->sample_loss.p, m->sample_correct.p, acc2);
+  DHO2G_LAUNCH();
+}
+
+void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2) {
+  DHO2G_CUDA(cudaMemsetAsync(acc2, 0, 2 * sizeof(double), m->ctx->stream));
+  eval_reduce_kernel<<<1, 1024, 0, m->ctx->stream>>>((int)B, m->sample_loss.p, m->sample_correct.p, acc2);
+  DHO2G_LAUNCH();
+}
+
+}  // namespace dho2g

@@ -1,0 +1,454 @@
+// Device DHO2 / FOSI / first-order loops (reference: proj/src/trainer.cpp:51-298).
+//
+// One trainer per GPU (rank). Parameters w_a are replicated (the MLP needs all of them);
+// gradient, ADMM primal w, multiplier pi, optimizer moments, Lanczos basis and V_hat are
+// row-sharded with Shard::for_rank(n, G, g) semantics. Per step: the rank's logical workers'
+// gradient (batched into one GEMM pass) -> reduce_scatter -> fused split update on the shard ->
+// all_gather(w_a). Per refresh: curvature batch split over ranks -> sharded Lanczos ->
+// replicated eigensolve -> sharded Ritz vectors.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+using namespace dho2g;
+
+struct MetricsRowH {
+  int64_t outer = -1, inner = -1, epoch = 0;
+  double loss = 0, acc = NAN, resid = NAN;
+  int refresh = 0;
+};
+
+struct dho2g_trainer {
+  dho2g_ctx* ctx = nullptr;
+  dho2g_train_cfg cfg{};
+  dho2g_mlp* mlp = nullptr;
+  size_t N = 0, D = 0, ncls = 0, n = 0;
+  uint64_t dataset_seed = 0;
+  int C = 1;
+  int host_resident = 0;
+  // dataset
+  DevBuf<float> Xd, yd;
+  HostBuf<float> Xh, yh;
+  const float* Xptr = nullptr;
+  const float* yptr = nullptr;
+  // sharding
+  size_t base = 0, begin = 0, end = 0, rows = 0;
+  int c0 = 0, c1 = 1;  // logical workers on this rank
+  // parameters / state
+  DevBuf<float> w_a_full, g_full, w_a_sh, g_sh, w_sh, pi_sh;
+  float* w_a_shard = nullptr;
+  float* g_shard = nullptr;
+  dho2g_opt opt;
+  dho2g_op op;
+  dho2g_lanczos lz;
+  dho2g_ese ese;
+  bool have_ese = false;
+  // schedule (trainer.cpp:211-249)
+  size_t rounds = 0, k_outer = 0, l_inner = 0, r = 0, iter = 0, epoch_fo = 0;
+  bool outer_started = false;
+  std::vector<uint64_t> perm;
+  int64_t perm_epoch = -1;
+  size_t refreshes = 0, safeguards = 0, steps = 0;
+  double refresh_ms_last = 0, refresh_ms_total = 0;
+  bool refreshed_this_epoch = false;
+  bool done = false;
+  // staging
+  static constexpr int kSlots = 4;
+  HostBuf<int64_t> idx_pin[kSlots];
+  cudaEvent_t idx_ev[kSlots] = {};
+  int slot = 0;
+  DevBuf<int64_t> idx_dev;
+  DevBuf<double> acc2, stepacc;
+  std::vector<MetricsRowH> metrics;
+  size_t B_local = 0;
+  double h2d_bytes = 0, d2h_bytes = 0;
+  std::vector<double> last_eigvals;
+
+  ~dho2g_trainer() {
+    for (auto& e : idx_ev)
+      if (e) cudaEventDestroy(e);
+  }
+
+  const int64_t* upload_indices(const std::vector<int64_t>& idx) {
+    const int s = slot;
+    slot = (slot + 1) % kSlots;
+    if (idx_ev[s]) DHO2G_CUDA(cudaEventSynchronize(idx_ev[s]));
+    idx_pin[s].ensure(idx.size());
+    std::memcpy(idx_pin[s].p, idx.data(), idx.size() * sizeof(int64_t));
+    const size_t off = (size_t)s * idx_stride;
+    DHO2G_CUDA(cudaMemcpyAsync(idx_dev.p + off, idx_pin[s].p, idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    if (!idx_ev[s]) DHO2G_CUDA(cudaEventCreateWithFlags(&idx_ev[s], cudaEventDisableTiming));
+    DHO2G_CUDA(cudaEventRecord(idx_ev[s], ctx->stream));
+    h2d_bytes += (double)idx.size() * sizeof(int64_t);
+    return idx_dev.p + off;
+  }
+  size_t idx_stride = 0;
+
+  void ensure_perm(int64_t epoch) {
+    if (perm_epoch == epoch) return;
+    perm.resize(N);
+    dho2g_epoch_permutation(N, dataset_seed, (uint64_t)epoch, perm.data());  // oracle.cpp:56-62
+    perm_epoch = epoch;
+  }
+
+  // mean_gradient (trainer.cpp:92-103): this rank's workers' samples batched into one pass;
+  // reduce_scatter sums over ranks; the 1/(b C) mean is folded into the output delta.
+  void mean_gradient(size_t round) {
+    const size_t b = cfg.batch_size;
+    std::vector<int64_t> idx;
+    idx.reserve((size_t)(c1 - c0) * b);
+    for (int c = c0; c < c1; ++c) {
+      size_t sb, se;
+      shard_range(N, C, c, &sb, &se);
+      const size_t len = se - sb;
+      for (size_t j = 0; j < b; ++j) idx.push_back((int64_t)perm[sb + (round * b + j) % len]);
+    }
+    B_local = idx.size();
+    const double scale = (1.0 / (double)b) * (1.0 / (double)C);
+    if (B_local > 0) {
+      const int64_t* di = upload_indices(idx);
+      mlp_load_weights(mlp, w_a_full.p);
+      mlp_grad_dev(mlp, w_a_full.p, Xptr, yptr, di, B_local, ncls, scale, g_full.p);
+      mlp_loss_sum(mlp, B_local, stepacc.p);
+      if (host_resident) h2d_bytes += (double)B_local * (D + 1) * sizeof(float);
+    } else {
+      DHO2G_CUDA(cudaMemsetAsync(g_full.p, 0, n * sizeof(float), ctx->stream));
+    }
+    if (ctx->world > 1) ctx->reduce_scatter_f32(g_full.p, g_shard, base);
+  }
+
+  // refresh_ese (trainer.cpp:105-135)
+  void refresh() {
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t want = std::min<size_t>(cfg.curvature_batch, N);
+    std::vector<uint64_t> all(N);
+    dho2g_curvature_indices(N, want, cfg.seed, refreshes, all.data());
+    std::vector<int64_t> cidx(all.begin(), all.begin() + want);
+    op.idx.ensure(want);
+    DHO2G_CUDA(cudaMemcpyAsync(op.idx.p, cidx.data(), want * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    if (host_resident) h2d_bytes += (double)want * (D + 1) * sizeof(float) + want * sizeof(int64_t);
+    op.B = want;
+    shard_range(want, ctx->world, ctx->rank, &op.b0, &op.b1);  // HVP batch split across ranks
+    op.scale = 1.0 / (double)want;
+    op.weights_loaded = false;  // w_a changed since the last refresh
+    const size_t m = cfg.lanczos_m ? cfg.lanczos_m : lanczos_budget(cfg.k, cfg.l, n);
+    if (m < 1 || m > n) fail(DHO2G_ARGUMENT, "lanczos_distributed: need 1 <= m <= n");
+    if (m > (size_t)kMaxLanczos - 1) fail(DHO2G_ARGUMENT, "lanczos: m exceeds the device limit");
+    if (lz.m != m) lanczos_alloc(&lz, ctx, n, m);
+    lanczos_run_into(&lz, &op, dho2g_mix_seed(cfg.seed, 0xbeef + refreshes));
+    const size_t iters = (size_t)lz.host.iters;
+    const size_t keff = std::min(cfg.k, iters);
+    const size_t leff = std::min(cfg.l, iters - keff);
+    extract_ese_into(ctx, &lz, keff, leff, &ese);
+    have_ese = ese.r > 0;
+    last_eigvals = ese.eigvals;
+    safeguards += (size_t)lz.host.safeguards;
+    ++refreshes;
+    refresh_ms_last = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    refresh_ms_total += refresh_ms_last;
+    refreshed_this_epoch = true;
+  }
+
+  void allgather_params() {
+    if (ctx->world > 1) ctx->allgather_f32(w_a_shard, w_a_full.p, base);
+  }
+
+  void update(bool use_pi, double sigma_eff) {
+    UpdateArgs a{};
+    a.g = g_shard;
+    a.pi = use_pi ? pi_sh.p : nullptr;
+    a.w_a = w_a_shard;
+    a.alpha = cfg.alpha;
+    a.sigma = sigma_eff;
+    a.floor = cfg.eigval_floor;
+    split_update(&opt, have_ese ? &ese : nullptr, a);
+    allgather_params();
+  }
+
+  // epoch_end (trainer.cpp:150-172)
+  void epoch_end(int64_t outer, int64_t inner, int64_t epoch, bool refreshed, bool with_resid) {
+    size_t sb, se;
+    shard_range(N, ctx->world, ctx->rank, &sb, &se);
+    DHO2G_CUDA(cudaMemsetAsync(acc2.p, 0, 4 * sizeof(double), ctx->stream));
+    mlp_load_weights(mlp, w_a_full.p);
+    const size_t chunk = std::max<size_t>(mlp->Bcap, 1024);
+    for (size_t s0 = sb; s0 < se; s0 += chunk) {
+      const size_t cnt = std::min(chunk, se - s0);
+      if (host_resident) h2d_bytes += (double)cnt * (D + 1) * sizeof(float);
+      mlp_eval_dev(mlp, w_a_full.p, Xptr + s0 * D, yptr + s0, nullptr, cnt, ncls, acc2.p);
+    }
+    if (with_resid) residual_partial(acc2.p + 2);
+    ctx->allreduce_sum_f64_ordered(acc2.p, 3);
+    double h[3];
+    DHO2G_CUDA(cudaMemcpyAsync(h, acc2.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+    d2h_bytes += 3 * sizeof(double);
+    MetricsRowH row;
+    row.outer = outer;
+    row.inner = inner;
+    row.epoch = epoch;
+    row.loss = h[0] / (double)N;
+    if (!std::isfinite(row.loss))
+      fail(DHO2G_DIVERGED, "non-finite loss at epoch " + std::to_string(epoch) + " (trainer " +
+                               (cfg.trainer == 2 ? "dho2" : cfg.trainer == 1 ? "fosi" : "sgd") + ")");
+    row.acc = ncls > 0 ? h[1] / (double)N : NAN;
+    row.resid = with_resid ? std::sqrt(h[2]) : NAN;
+    row.refresh = refreshed ? 1 : 0;
+    metrics.push_back(row);
+    check_opt_flags(&opt);
+  }
+
+  void residual_partial(double* out);
+
+  void step_one(bool with_eval) {
+    const bool curvature = cfg.k + cfg.l > 0;
+    if (cfg.trainer == 2) {  // run_dho2 (trainer.cpp:211-249)
+      const bool red = cfg.sigma_zero_reduction != 0;
+      const double sigma_state = red ? 1.0 : cfg.sigma;
+      const double sigma_eff = red ? 0.0 : cfg.sigma;
+      if (k_outer >= cfg.outer_rounds) {
+        done = true;
+        return;
+      }
+      if (r == 0 && l_inner == 0) {
+        have_ese = false;
+        if (curvature) refresh();
+        if (red) DHO2G_CUDA(cudaMemcpyAsync(w_sh.p, w_a_shard, rows * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+        else admm_w_update_dev(ctx->stream, rows, sigma_state, w_a_shard, pi_sh.p, w_sh.p);
+        DHO2G_CUDA(cudaMemcpyAsync(w_a_shard, w_sh.p, rows * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+        allgather_params();
+      }
+      const int64_t epoch = (int64_t)(k_outer * cfg.inner_epochs + l_inner);
+      ensure_perm(epoch);
+      mean_gradient(r);
+      update(!red, sigma_eff);
+      ++r;
+      ++steps;
+      if (r == rounds) {
+        if (with_eval) epoch_end((int64_t)k_outer, (int64_t)l_inner, epoch, l_inner == 0 && curvature, true);
+        r = 0;
+        ++l_inner;
+        if (l_inner == cfg.inner_epochs) {
+          if (!red) admm_dual_update_dev(ctx->stream, rows, sigma_state, w_a_shard, w_sh.p, pi_sh.p);
+          l_inner = 0;
+          ++k_outer;
+          if (k_outer >= cfg.outer_rounds) done = true;
+        }
+      }
+    } else {  // run_fosi (:187-209) / run_first_order (:174-185)
+      if (epoch_fo >= cfg.epochs) {
+        done = true;
+        return;
+      }
+      if (r == 0) refreshed_this_epoch = false;
+      ensure_perm((int64_t)epoch_fo);
+      if (cfg.trainer == 1 && curvature) {
+        const size_t interval = cfg.refresh_interval > 0 ? cfg.refresh_interval : rounds;
+        if (iter % interval == 0) refresh();
+      }
+      mean_gradient(r);
+      update(false, 0.0);
+      ++r;
+      ++iter;
+      ++steps;
+      if (r == rounds) {
+        if (with_eval) epoch_end(-1, -1, (int64_t)epoch_fo, refreshed_this_epoch, false);
+        r = 0;
+        ++epoch_fo;
+        if (epoch_fo >= cfg.epochs) done = true;
+      }
+    }
+  }
+};
+
+namespace {
+__global__ void resid_kernel(size_t n, const float* __restrict__ a, const float* __restrict__ b, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double d = (double)a[i] - (double)b[i];
+    s += d * d;
+  }
+  const double t = block_sum(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+__global__ void sum_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    *out = s;
+  }
+}
+}  // namespace
+
+void dho2g_trainer::residual_partial(double* out) {
+  const int nb = (int)std::max<size_t>(1, std::min<size_t>(cdiv(rows, 256), 296));
+  DevBuf<double> part(nb);
+  resid_kernel<<<nb, 256, 0, ctx->stream>>>(rows, w_a_shard, w_sh.p, part.p);
+  sum_kernel<<<1, 32, 0, ctx->stream>>>(part.p, nb, out);
+  DHO2G_LAUNCH();
+  DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+namespace dho2g {
+
+dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
+                              const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
+                              int workers, int host_resident) {
+  if (cfg->batch_size == 0) fail(DHO2G_ARGUMENT, "train: batch_size must be >= 1");
+  if (workers < 1) fail(DHO2G_ARGUMENT, "run_workers: world_size must be >= 1");
+  if (N < (size_t)workers) fail(DHO2G_ARGUMENT, "train: fewer samples than workers");
+  if (cfg->trainer == 2 && !cfg->sigma_zero_reduction && cfg->sigma <= 0.0)
+    fail(DHO2G_ARGUMENT, "dho2: sigma must be positive");
+  auto t = std::make_unique<dho2g_trainer>();
+  t->ctx = ctx;
+  t->cfg = *cfg;
+  t->mlp = mlp;
+  t->N = N;
+  t->D = mlp->sizes[0];
+  t->ncls = ncls;
+  t->n = mlp->dim;
+  t->dataset_seed = dataset_seed;
+  t->C = workers;
+  t->host_resident = host_resident;
+  const size_t n = t->n;
+  cudaStream_t st = ctx->stream;
+  // dataset: fp32 copy, device resident (or pinned + mapped host memory in end-to-end mode)
+  std::vector<float> Xf(N * t->D), yf(N);
+  for (size_t i = 0; i < N * t->D; ++i) Xf[i] = (float)X[i];
+  for (size_t i = 0; i < N; ++i) yf[i] = (float)y[i];
+  if (host_resident) {
+    t->Xh.ensure(Xf.size());
+    t->yh.ensure(yf.size());
+    std::memcpy(t->Xh.p, Xf.data(), Xf.size() * sizeof(float));
+    std::memcpy(t->yh.p, yf.data(), yf.size() * sizeof(float));
+    float *dx = nullptr, *dy = nullptr;
+    DHO2G_CUDA(cudaHostGetDevicePointer((void**)&dx, t->Xh.p, 0));
+    DHO2G_CUDA(cudaHostGetDevicePointer((void**)&dy, t->yh.p, 0));
+    t->Xptr = dx;
+    t->yptr = dy;
+  } else {
+    t->Xd.alloc(Xf.size());
+    t->yd.alloc(yf.size());
+    DHO2G_CUDA(cudaMemcpy(t->Xd.p, Xf.data(), Xf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    DHO2G_CUDA(cudaMemcpy(t->yd.p, yf.data(), yf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    t->Xptr = t->Xd.p;
+    t->yptr = t->yd.p;
+  }
+  // sharding over GPUs
+  t->base = cdiv(n, (size_t)ctx->world);
+  shard_range(n, ctx->world, ctx->rank, &t->begin, &t->end);
+  t->rows = t->end - t->begin;
+  {
+    size_t a, b;
+    shard_range((size_t)workers, ctx->world, ctx->rank, &a, &b);
+    t->c0 = (int)a;
+    t->c1 = (int)b;
+  }
+  size_t sb, se;
+  shard_range(N, workers, 0, &sb, &se);
+  t->rounds = (se - sb + cfg->batch_size - 1) / cfg->batch_size;  // trainer.cpp:66-69
+  const size_t full = t->base * ctx->world;
+  t->w_a_full.alloc(full);
+  t->g_full.alloc(full);
+  std::vector<float> w0f(n);
+  for (size_t i = 0; i < n; ++i) w0f[i] = (float)w0[i];
+  DHO2G_CUDA(cudaMemcpy(t->w_a_full.p, w0f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  if (ctx->world == 1) {
+    t->w_a_shard = t->w_a_full.p;
+    t->g_shard = t->g_full.p;
+  } else {
+    t->w_a_sh.alloc(std::max<size_t>(t->base, 1));
+    t->g_sh.alloc(std::max<size_t>(t->base, 1));
+    t->w_a_shard = t->w_a_sh.p;
+    t->g_shard = t->g_sh.p;
+    if (t->rows)
+      DHO2G_CUDA(cudaMemcpy(t->w_a_shard, t->w_a_full.p + t->begin, t->rows * sizeof(float), cudaMemcpyDeviceToDevice));
+  }
+  t->w_sh.alloc(std::max<size_t>(t->base, 1));
+  t->pi_sh.alloc(std::max<size_t>(t->base, 1));
+  if (t->rows)
+    DHO2G_CUDA(cudaMemcpy(t->w_sh.p, t->w_a_shard, t->rows * sizeof(float), cudaMemcpyDeviceToDevice));  // make_admm_state
+  opt_alloc(&t->opt, ctx, cfg->base, t->rows);
+  // curvature operator bound to (w_a, curvature batch) like the trainer.cpp:116 lambda
+  t->op.ctx = ctx;
+  t->op.kind = 0;
+  t->op.n = n;
+  t->op.mlp = mlp;
+  t->op.ncls = ncls;
+  t->op.wptr = t->w_a_full.p;
+  t->op.Xptr = t->Xptr;
+  t->op.yptr = t->yptr;
+  if (ctx->world > 1) t->op.hfull.alloc(full);
+  t->idx_stride = round_up((size_t)(t->c1 - t->c0) * cfg->batch_size + 1, 64);
+  t->idx_dev.alloc(t->idx_stride * dho2g_trainer::kSlots);
+  t->acc2.alloc(4);
+  t->stepacc.alloc(2);
+  DHO2G_CUDA(cudaStreamSynchronize(st));
+  return t.release();
+}
+
+}  // namespace dho2g
+
+namespace dho2g {
+void trainer_step(dho2g_trainer* tr, size_t steps, int with_eval) {
+  for (size_t s = 0; s < steps && !tr->done; ++s) tr->step_one(with_eval != 0);
+}
+void trainer_run(dho2g_trainer* tr) {
+  while (!tr->done) tr->step_one(true);
+  tr->ctx->sync();
+  check_opt_flags(&tr->opt);
+}
+void trainer_params(dho2g_trainer* tr, double* w) {
+  std::vector<float> f(tr->n);
+  DHO2G_CUDA(cudaMemcpyAsync(f.data(), tr->w_a_full.p, tr->n * sizeof(float), cudaMemcpyDeviceToHost, tr->ctx->stream));
+  DHO2G_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  for (size_t i = 0; i < tr->n; ++i) w[i] = f[i];
+}
+size_t trainer_rows(dho2g_trainer* tr) { return tr->metrics.size(); }
+void trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
+                     int* refresh) {
+  for (size_t i = 0; i < tr->metrics.size() && i < max_rows; ++i) {
+    const auto& m = tr->metrics[i];
+    if (loss) loss[i] = m.loss;
+    if (acc) acc[i] = m.acc;
+    if (resid) resid[i] = m.resid;
+    if (epoch) epoch[i] = m.epoch;
+    if (refresh) refresh[i] = m.refresh;
+  }
+}
+double trainer_last_loss(dho2g_trainer* tr) {
+  double h[2] = {0, 0};
+  DHO2G_CUDA(cudaMemcpyAsync(h, tr->stepacc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, tr->ctx->stream));
+  DHO2G_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  tr->d2h_bytes += 2 * sizeof(double);
+  return tr->B_local ? h[0] / (double)tr->B_local : 0.0;
+}
+bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v) {
+  if (key == "refreshes") *v = (double)tr->refreshes;
+  else if (key == "safeguard_passes") *v = (double)tr->safeguards;
+  else if (key == "steps") *v = (double)tr->steps;
+  else if (key == "refresh_ms_last") *v = tr->refresh_ms_last;
+  else if (key == "refresh_ms_total") *v = tr->refresh_ms_total;
+  else if (key == "lanczos_ms_last") *v = tr->lz.ms;
+  else if (key == "h2d_bytes") *v = tr->h2d_bytes;
+  else if (key == "d2h_bytes") *v = tr->d2h_bytes;
+  else if (key == "rounds_per_epoch") *v = (double)tr->rounds;
+  else if (key == "batch_local") *v = (double)tr->B_local;
+  else if (key == "done") *v = tr->done ? 1.0 : 0.0;
+  else if (key == "lanczos_m") *v = (double)tr->lz.m;
+  else if (key == "lanczos_iters") *v = (double)tr->lz.host.iters;
+  else if (key == "ese_count") *v = (double)(tr->have_ese ? tr->ese.r : 0);
+  else return false;
+  return true;
+}
+void trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count) {
+  *count = tr->last_eigvals.size();
+  if (vals)
+    for (size_t i = 0; i < tr->last_eigvals.size(); ++i) vals[i] = tr->last_eigvals[i];
+}
+void trainer_destroy(dho2g_trainer* tr) { delete tr; }
+}  // namespace dho2g

@@ -1,0 +1,264 @@
+"""GPU parity of the individual sm_100a kernels against the CPU checker (oracle/) and exact fp64.
+
+Tolerances: the device path is fp32 with split-BF16x3 tensor-core GEMMs and fp64
+reductions, the checker is fp64. Each bound is written next to its assertion."""
+import numpy as np
+import pytest
+
+import paper_2505_00982_b200 as d
+from paper_2505_00982_b200.api import test_gemm as run_gemm
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+# ------------------------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (37, 10, 20), (130, 250, 200), (256, 384, 1000), (8, 3584, 7168),
+                                   (1024, 256, 784), (300, 129, 65)])
+def test_gemm3_tcgen05_vs_exact(ctx, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    exact = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
+    tc = run_gemm(ctx, A, B, 0)
+    st = run_gemm(ctx, A, B, 1)
+    # split-BF16x3 drops lo*lo (2^-16 relative per product) -> bound 2e-5 of sum |a||b|
+    assert np.max(np.abs(tc - exact) / scale) < 2e-5
+    assert np.max(np.abs(st - exact) / scale) < 2e-5
+    # the tensor-core and CUDA-core paths compute the same split products
+    assert np.max(np.abs(tc - st) / scale) < 2e-6
+
+
+# ------------------------------------------------------------------------------------ MLP oracle
+CASES = [([20, 16, 12, 5], 37, "tanh", "softmax_ce", 5), ([20, 16, 12, 5], 37, "relu", "softmax_ce", 5),
+         ([20, 16, 12, 5], 37, "tanh", "mse", 5), ([13, 24, 1], 19, "tanh", "mse", 0),
+         ([784, 256, 10], 128, "tanh", "softmax_ce", 10), ([64, 96, 96, 96, 10], 200, "tanh", "softmax_ce", 10)]
+
+
+@pytest.mark.parametrize("sizes,B,act,loss,ncls", CASES)
+def test_mlp_oracle_vs_checker(ctx, port, sizes, B, act, loss, ncls):
+    from oracle.bindings import blobs_dataset
+    X, y = blobs_dataset(B, sizes[0], max(ncls, 1), seed=11)
+    if ncls == 0:
+        y = np.sin(np.arange(B) * 0.37)
+    mlp = d.MlpOracle(ctx, sizes, act, loss)
+    w = mlp.init_params(3)
+    assert (w == port.mlp_init(sizes, 3)).all()  # oracle.cpp:386-394 bitwise on the host
+    w = w + 0.05 * port.rng_normal(5, len(w))
+    v = port.rng_normal(6, len(w))
+    batch = d.Batch(X, y, ncls)
+    a, lo = {"tanh": 0, "relu": 1}[act], {"softmax_ce": 0, "mse": 1}[loss]
+    hv_ref = port.mlp_hvp(sizes, w, v, X, y, ncls, a, lo)
+    g_ref = port.mlp_grad(sizes, w, X, y, ncls, a, lo)
+    hv = mlp.hvp(w, v, batch)
+    g = mlp.grad(w, batch)
+    # fp32 + split-BF16x3: relative L2 <= 1e-4 (survey probe: ~4e-6)
+    assert rel_l2(hv, hv_ref) < 1e-4
+    assert rel_l2(g, g_ref) < 1e-4
+    assert abs(mlp.value(w, batch) - port.mlp_value(sizes, w, X, y, ncls, a, lo)) <= 1e-5 * max(
+        1.0, abs(port.mlp_value(sizes, w, X, y, ncls, a, lo)))
+    if ncls:
+        assert abs(mlp.accuracy(w, batch) - port.mlp_accuracy(sizes, w, X, y, ncls, a, lo)) <= 1.5 / B
+    else:
+        assert mlp.accuracy(w, batch) is None
+
+
+def test_mlp_hvp_linear_symmetric(ctx, port):  # test_oracle.cpp:107-132
+    from oracle.bindings import blobs_dataset
+    sizes = [30, 24, 6]
+    X, y = blobs_dataset(64, 30, 6, seed=2)
+    mlp = d.MlpOracle(ctx, sizes)
+    w = mlp.init_params(7)
+    u, v = port.rng_normal(71, len(w)), port.rng_normal(72, len(w))
+    b = d.Batch(X, y, 6)
+    hu, hv, hc = mlp.hvp(w, u, b), mlp.hvp(w, v, b), mlp.hvp(w, 0.7 * u - 1.3 * v, b)
+    assert rel_l2(hc, 0.7 * hu - 1.3 * hv) < 1e-5
+    assert abs(u @ hv - v @ hu) <= 1e-4 * max(1.0, abs(u @ hv))
+
+
+def test_mlp_argument_errors(ctx):
+    with pytest.raises(d.ArgumentError):
+        d.MlpOracle(ctx, [2, 2])
+    mlp = d.MlpOracle(ctx, [3, 4, 2])
+    with pytest.raises(d.ArgumentError):
+        mlp.value(np.zeros(mlp.dim()), d.Batch(np.zeros((4, 3)), np.zeros(4), 5))  # n_classes != outputs
+    with pytest.raises(d.DimensionError):
+        mlp.grad(np.zeros(3), d.Batch(np.zeros((4, 3)), np.zeros(4), 2))
+
+
+def test_gemm_backends_agree_on_hvp(ctx, port):
+    from oracle.bindings import blobs_dataset
+    sizes = [784, 256, 10]
+    X, y = blobs_dataset(128, 784, 10, seed=1)
+    mlp = d.MlpOracle(ctx, sizes)
+    w = mlp.init_params(1)
+    v = port.rng_normal(9, len(w))
+    b = d.Batch(X, y, 10)
+    ctx.set_option("gemm", 1)
+    try:
+        h1 = mlp.hvp(w, v, b)
+    finally:
+        ctx.set_option("gemm", 0)
+    h0 = mlp.hvp(w, v, b)
+    assert rel_l2(h0, h1) < 2e-6
+
+
+# ------------------------------------------------------------------------------------ Lanczos
+def random_symmetric(port, n, seed):  # test_support.hpp:65-72
+    a = port.rng_normal(seed, n * n).reshape(n, n)
+    return 0.5 * (a + a.T)
+
+
+def run_lanczos(ctx, op, n, m, seed, k=0, l=0):
+    st = d.lanczos_distributed(ctx, m, op, n, seed)
+    ese = d.extract_ese_distributed(ctx, st, min(k, st.iterations), min(l, st.iterations - min(k, st.iterations)))
+    return st, ese
+
+
+def test_lanczos_dense_matches_checker(ctx, port):
+    H = random_symmetric(port, 50, 123)
+    st, ese = run_lanczos(ctx, d.dense_operator(ctx, H), 50, 20, 9, k=3, l=2)
+    ref = port.lanczos(dict(kind=0, n=50, mat=H), 20, 9, k=3, l=2)
+    hn = np.max(np.abs(np.linalg.eigvalsh(H)))
+    assert st.iterations == ref["iterations"] == 20 and not st.breakdown
+    # B entries within 1e-5 of ||H|| (fp32 basis, fp64 reductions)
+    assert np.max(np.abs(st.tridiag.diag - ref["diag"])) <= 1e-5 * hn
+    assert np.max(np.abs(st.tridiag.offdiag - ref["off"])) <= 1e-5 * hn
+    assert np.max(np.abs(ese.eigvals - ref["eigvals"])) <= 1e-5 * hn
+    D = st.basis_shard[:, :20]
+    assert np.max(np.abs(D.T @ D - np.eye(20))) <= 1e-5  # test_lanczos.cpp:47-61 (fp32: 1e-5)
+    T = np.diag(st.tridiag.diag) + np.diag(st.tridiag.offdiag[:19], 1) + np.diag(st.tridiag.offdiag[:19], -1)
+    assert np.linalg.norm(D.T @ H @ D - T) <= 1e-4 * hn
+    V = ese.eigvecs_shard(50)
+    Vr = ref["eigvecs"]
+    assert np.max(np.abs(V - Vr)) <= 1e-4  # same sign convention (lanczos.cpp:82-94)
+
+
+def test_lanczos_identity_breakdown(ctx):  # test_lanczos.cpp:22-33
+    st, ese = run_lanczos(ctx, d.dense_operator(ctx, np.eye(6)), 6, 4, 11, k=1)
+    assert st.breakdown and st.iterations == 1 and st.tridiag.dim() == 1
+    assert abs(st.tridiag.diag[0] - 1.0) < 1e-6 and abs(ese.eigvals[0] - 1.0) < 1e-6
+
+
+def test_lanczos_rank2_breakdown_matches(ctx, port):  # test_dist_lanczos.cpp:193-203
+    H = np.zeros((12, 12))
+    H[0, 0], H[1, 1] = 3.0, 1.0
+    st, _ = run_lanczos(ctx, d.dense_operator(ctx, H), 12, 6, 13, k=1)
+    ref = port.lanczos(dict(kind=0, n=12, mat=H), 6, 13, k=1)
+    assert st.breakdown and st.iterations == ref["iterations"] < 6
+
+
+def test_lanczos_diagonal_spectrum_exact(ctx):  # test_lanczos.cpp:35-45
+    st, ese = run_lanczos(ctx, d.diagonal_operator(ctx, np.arange(1.0, 7.0)), 6, 6, 5, k=6)
+    assert st.iterations == 6
+    assert np.max(np.abs(np.sort(ese.eigvals) - np.arange(1.0, 7.0))) <= 1e-5
+
+
+def test_extract_known_diagonal_signs(ctx):  # test_lanczos.cpp:95-111
+    st, ese = run_lanczos(ctx, d.dense_operator(ctx, np.diag([10.0, 5.0, 1.0, 0.1])), 4, 4, 2, k=1, l=1)
+    assert abs(ese.eigvals[0] - 10.0) <= 1e-5 and abs(ese.eigvals[1] - 0.1) <= 1e-5
+    V = ese.eigvecs_shard(4)
+    assert V[0, 0] >= 1 - 1e-5 and V[3, 1] >= 1 - 1e-5
+
+
+def test_lanczos_rejects_bad_m(ctx):
+    op = d.diagonal_operator(ctx, np.arange(1.0, 5.0))
+    with pytest.raises(d.ArgumentError):
+        d.lanczos_distributed(ctx, 5, op, 4, 1)
+    st = d.lanczos_distributed(ctx, 4, op, 4, 1)
+    with pytest.raises(d.ArgumentError):
+        d.extract_ese_distributed(ctx, st, 3, 2)
+
+
+def test_lanczos_host_operator(ctx, port):
+    H = random_symmetric(port, 40, 5)
+    st, ese = run_lanczos(ctx, d.host_operator(ctx, lambda v: H @ v, 40), 40, 12, 21, k=2, l=1)
+    ref = port.lanczos(dict(kind=0, n=40, mat=H), 12, 21, k=2, l=1)
+    assert np.max(np.abs(ese.eigvals - ref["eigvals"])) <= 1e-5 * np.max(np.abs(ref["eigvals"]))
+
+
+def test_lanczos_large_diagonal(ctx, port):
+    """GS passes at scale (many CTAs, chunked rows): n = 2^18, m = 40, spectrum 1 + (i mod 1000)."""
+    n, m = 1 << 18, 40
+    spec = 1.0 + (np.arange(n) % 1000)
+    spec[:3] = [5000.0, 3000.0, 2000.0]
+    st, ese = run_lanczos(ctx, d.diagonal_operator(ctx, spec), n, m, 99, k=4, l=2)
+    ref = port.lanczos(dict(kind=1, n=n, mat=spec), m, 99, k=4, l=2, want_basis=False)
+    assert np.max(np.abs(ese.eigvals - ref["eigvals"]) / np.abs(ref["eigvals"])) <= 1e-4
+    assert np.max(np.abs(st.tridiag.diag - ref["diag"]) / np.max(spec)) <= 1e-5
+    V, Vr = ese.eigvecs_shard(n), ref["eigvecs"]
+    proj = 2 * V.shape[1] - 2 * np.linalg.norm(V.T @ Vr) ** 2
+    assert proj <= 1e-8  # ||V V^T - Vr Vr^T||_F^2 (sign-invariant)
+
+
+def test_refresh_mlp_c1_eigenvalues(ctx, port):
+    """SURVEY §8d per-refresh parity on identical inputs: C1 model 784-256-10, B=128, m=40, k=10."""
+    from oracle.bindings import blobs_dataset
+    sizes = [784, 256, 10]
+    X, y = blobs_dataset(128, 784, 10, seed=7)
+    mlp = d.MlpOracle(ctx, sizes)
+    w = mlp.init_params(1)
+    op = d.mlp_hvp_operator(ctx, mlp, w, d.Batch(X, y, 10))
+    st, ese = run_lanczos(ctx, op, mlp.dim(), 40, 4242, k=10)
+    ref = port.lanczos(dict(kind=2, n=mlp.dim(), sizes=sizes, w=w, X=X, y=y, ncls=10), 40, 4242, k=10,
+                       want_basis=False)
+    rel = np.abs(ese.eigvals - ref["eigvals"]) / np.abs(ref["eigvals"])
+    assert rel.max() <= 1e-4, rel  # north-star bound: eigenvalues within 1e-4 relative
+    assert st.iterations == ref["iterations"]
+
+
+# ------------------------------------------------------------------------------------ update
+@pytest.mark.parametrize("kind", ["sgd", "momentum", "adam", "adamw"])
+@pytest.mark.parametrize("admm", [False, True])
+def test_deltas_vs_checker(ctx, port, kind, admm):
+    from oracle.bindings import base_cfg
+    n, r, T = 20000, 8, 4
+    V = np.linalg.qr(port.rng_normal(1, n * r).reshape(n, r))[0]
+    ev = np.array([50.0, 20.0, 7.0, 3.0, 1e-9, -1e-13, -2.0, 0.5])
+    g = port.rng_normal(2, T * n).reshape(T, n)
+    pi = port.rng_normal(3, n) if admm else None
+    w = port.rng_normal(4, n)
+    sigma = 0.05 if admm else 0.0
+    cfg = d.BaseConfig(kind, lr=1e-2)
+    opt = d.BaseOptimizer(ctx, cfg, n)
+    ese = d.EseResult.from_host(ctx, ev, V)
+    nw_ref, bs_ref, _ = port.deltas_seq(base_cfg(kind, lr=1e-2), ev, V, g, w, 0.3, pi=pi, sigma=sigma)
+    for t in range(T):
+        dl = d.admm_deltas(g[t], pi, ese, opt, w, 0.3, sigma) if admm else d.fosi_deltas(g[t], ese, opt, w, 0.3)
+        # update pass fed identical g, pi, w, V: per-element within 2e-6 of the vector's max (fp32)
+        assert np.max(np.abs(dl.newton - nw_ref[t])) <= 2e-6 * np.max(np.abs(nw_ref[t]))
+        assert np.max(np.abs(dl.base - bs_ref[t])) <= 2e-6 * np.max(np.abs(bs_ref[t]))
+
+
+def test_deltas_known_answers(ctx):  # test_optimizer.cpp:78-199
+    V = np.array([[1.0], [0.0]])
+    ese = d.EseResult.from_host(ctx, [4.0], V)
+    zero = d.BaseOptimizer(ctx, d.BaseConfig("sgd", lr=0.0), 2)
+    dl = d.fosi_deltas([4.0, 1.0], ese, zero, [0.0, 0.0], 1.0)
+    assert abs(dl.newton[0] + 1.0) < 1e-6 and dl.newton[1] == 0.0 and np.abs(dl.base).max() == 0.0
+    dl = d.admm_deltas([4.0, 1.0], [0.0, 0.0], ese, zero, [0.0, 0.0], 1.0, 1.0)
+    assert abs(dl.newton[0] + 0.8) < 1e-6
+    adam = d.BaseOptimizer(ctx, d.BaseConfig("adam", lr=1e-3), 3)
+    g = np.array([0.5, -2.0, 3.0])
+    assert np.allclose(adam.step(g, np.zeros(3)), -1e-3 * g / (np.abs(g) + 1e-8), rtol=1e-6)
+    with pytest.raises(d.NumericError):
+        d.BaseOptimizer(ctx, d.BaseConfig("adam"), 2).step([1.0, np.inf], [0.0, 0.0])
+
+
+def test_admm_round(ctx, port):
+    n = 1000
+    w_a, pi, w_a2 = port.rng_normal(1, n), port.rng_normal(2, n), port.rng_normal(3, n)
+    st = d.make_admm_state(w_a, 0.7)
+    st.pi = pi
+    d.admm_w_update(ctx, st)
+    w_ref, pi_ref = port.admm_round(0.7, w_a, pi, w_a2)
+    assert np.max(np.abs(st.w - w_ref)) <= 1e-6 * np.max(np.abs(w_ref))
+    st.w_a = w_a2
+    d.admm_dual_update(ctx, st)
+    assert np.max(np.abs(st.pi - pi_ref)) <= 1e-5 * np.max(np.abs(pi_ref))
+    with pytest.raises(d.ArgumentError):
+        d.make_admm_state(w_a, 0.0)
