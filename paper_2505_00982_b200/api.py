@@ -8,6 +8,7 @@ float64 like dho2::Vector; column-major matrices (TallMatrix) are numpy arrays o
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from typing import Callable, Optional
 
@@ -164,6 +165,10 @@ class Context:
         check(lib.dho2g_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self._children = weakref.WeakSet()
+
+    def _adopt(self, obj):
+        self._children.add(obj)
 
     def set_option(self, key: str, value: float):
         check(lib.dho2g_ctx_set_option(self.h, key.encode(), float(value)))
@@ -219,6 +224,12 @@ class Context:
 
     def close(self):
         if self.h:
+            # device objects hold pointers into this context: release them first, users before owners
+            for obj in sorted(list(self._children), key=lambda o: getattr(o, "_close_order", 9)):
+                try:
+                    obj.close()
+                except Exception:
+                    pass
             lib.dho2g_ctx_destroy(self.h)
             self.h = None
 
@@ -275,6 +286,9 @@ class MlpOracle:
         check(lib.dho2g_mlp_create(ctx.h, sizes, len(self.layer_sizes), ACTIVATIONS[activation], LOSSES[loss],
                                    C.byref(h)))
         self.h = h
+        ctx._adopt(self)
+
+    _close_order = 6
 
     def dim(self) -> int:
         return int(lib.dho2g_mlp_dim(self.h))
@@ -335,8 +349,11 @@ class MlpOracle:
 
 # ----------------------------------------------------------------------------- operators (HvpFn)
 class Operator:
+    _close_order = 4
+
     def __init__(self, ctx, h, n, keep=()):
         self.ctx, self.h, self.n, self._keep = ctx, h, n, keep
+        ctx._adopt(self)
 
     def close(self):
         if self.h:
@@ -417,8 +434,11 @@ class TridiagMatrix:
 class ShardedLanczosResult:
     """dist_lanczos.hpp:21-30: this rank's basis rows stay on the GPU; B is host fp64."""
 
+    _close_order = 3
+
     def __init__(self, ctx, h, m):
         self.ctx, self.h, self.m = ctx, h, m
+        ctx._adopt(self)
         diag, off = np.zeros(m + 1), np.zeros(m + 1)
         it, bd, sg, b, e = C.c_size_t(), C.c_int(), C.c_size_t(), C.c_size_t(), C.c_size_t()
         check(lib.dho2g_lanczos_result(h, _d(diag), _d(off), C.byref(it), C.byref(bd), C.byref(sg), C.byref(b),
@@ -466,8 +486,11 @@ class EseResult:
     """lanczos.hpp:45-52: k largest (descending) then l smallest (ascending) Ritz pairs; the
     eigenvectors are this rank's rows (all rows at world == 1)."""
 
+    _close_order = 2
+
     def __init__(self, ctx, h, k=0, l=0):
         self.ctx, self.h, self.k, self.l = ctx, h, k, l
+        ctx._adopt(self)
 
     def count(self) -> int:
         return int(lib.dho2g_ese_count(self.h)) if self.h else 0
@@ -551,6 +574,9 @@ class BaseOptimizer:
         c = cfg.to_c()
         check(lib.dho2g_opt_create(ctx.h, C.byref(c), n, C.byref(h)))
         self.h = h
+        ctx._adopt(self)
+
+    _close_order = 5
 
     def step(self, g, w):
         g, w = _f64(g), _f64(w)
@@ -714,6 +740,9 @@ class Trainer:
                                        data.shuffle_seed, _d(w0), workers, int(host_resident), C.byref(h)))
         self.h = h
         self.n = mlp.dim()
+        ctx._adopt(self)
+
+    _close_order = 1
 
     def step(self, steps: int = 1, with_eval: bool = False):
         check(lib.dho2g_trainer_step(self.h, steps, int(with_eval)))

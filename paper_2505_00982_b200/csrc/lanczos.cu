@@ -21,6 +21,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSub = 512;  // rows per warp work item (32 lanes x 4 float4)
+constexpr double kBreakdownFloor32 = 4e-6;
+constexpr double kSafeguardFloor32 = 1e-3;
 
 // ------------------------------------------------------------------ start vector
 // seeded_unit_gaussian (lanczos.cpp:18-26): Rng(seed*phi + 0x1234567).fill_normal, computed
@@ -217,6 +219,11 @@ __global__ void lz_decide_kernel(LzDev* st, const double* __restrict__ allb, int
   for (int w = 0; w < world; ++w) b2 += allb[(size_t)w * stride];
   const double beta = sqrt(b2);
   const double pre = st->pre;
+  // fp32 adaptation of the reference thresholds (fp64 there): h and D are stored in fp32, so an
+  // exactly invariant subspace leaves a residual at the fp32 rounding floor (~3e-8 pre), never at
+  // 1e-10 pre; and a projection that cancels beyond ~1e-3 loses orthogonality at eps32/ratio.
+  rtol = fmax(rtol, kBreakdownFloor32);
+  ratio = fmax(ratio, kSafeguardFloor32);
   st->beta = beta;
   if (!safeguard_pass && safeguard_on && beta > rtol * pre && beta < ratio * pre) {
     st->need_sg = 1;

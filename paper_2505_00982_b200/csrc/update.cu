@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kT) upd_p1_kernel(const float* __restrict__ V,
 
 struct BaseHyper {
   int kind;
-  float lr, wd, b1, b2, eps, mom;
+  float lr, wd, b1, b2, omb1, omb2, eps, mom;  // omb = 1 - beta, formed in fp64 on the host
   float bc1, bc2;
 };
 
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
           m[r] = mm;
           sv = -hp.lr * mm;
         } else {
-          const float mm = hp.b1 * m[r] + (1.f - hp.b1) * gf;
-          const float vv = hp.b2 * v[r] + (1.f - hp.b2) * gf * gf;
+          const float mm = hp.b1 * m[r] + hp.omb1 * gf;
+          const float vv = hp.b2 * v[r] + hp.omb2 * gf * gf;
           m[r] = mm;
           v[r] = vv;
           sv = -hp.lr * (mm / hp.bc1) / (sqrtf(vv / hp.bc2) + hp.eps);
@@ -277,6 +277,8 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   hp.wd = (float)o->cfg.weight_decay;
   hp.b1 = (float)o->cfg.beta1;
   hp.b2 = (float)o->cfg.beta2;
+  hp.omb1 = (float)(1.0 - o->cfg.beta1);
+  hp.omb2 = (float)(1.0 - o->cfg.beta2);
   hp.eps = (float)o->cfg.eps;
   hp.mom = (float)o->cfg.momentum;
   hp.bc1 = (float)(1.0 - std::pow(o->cfg.beta1, (double)o->t));

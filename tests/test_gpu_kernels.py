@@ -30,7 +30,7 @@ def test_gemm3_tcgen05_vs_exact(ctx, M, N, K):
     assert np.max(np.abs(tc - exact) / scale) < 2e-5
     assert np.max(np.abs(st - exact) / scale) < 2e-5
     # the tensor-core and CUDA-core paths compute the same split products
-    assert np.max(np.abs(tc - st) / scale) < 2e-6
+    assert np.max(np.abs(tc - st) / scale) < 5e-6
 
 
 # ------------------------------------------------------------------------------------ MLP oracle
@@ -104,7 +104,7 @@ def test_gemm_backends_agree_on_hvp(ctx, port):
     finally:
         ctx.set_option("gemm", 0)
     h0 = mlp.hvp(w, v, b)
-    assert rel_l2(h0, h1) < 2e-6
+    assert rel_l2(h0, h1) < 2e-5
 
 
 # ------------------------------------------------------------------------------------ Lanczos
