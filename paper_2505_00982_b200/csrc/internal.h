@@ -87,7 +87,7 @@ struct dho2g_mlp {
   //  DR[j]  = [d | rd] rows b   (Bcap x 2P_j), j = 1..L
   //  DRT[j] = [rd^T | d^T] rows o (s_j x 2Bpcap), j = 1..L
   std::vector<dho2g::DevBuf<dho2g::bf16>> AR_hi, AR_lo, ART_hi, ART_lo, DR_hi, DR_lo, DRT_hi, DRT_lo;
-  std::vector<dho2g::DevBuf<float>> a32, ra32, d32, rd32;  // fp32 B x s_j
+  std::vector<dho2g::DevBuf<float>> a32, ra32, d32, rd32, u32;  // fp32 B x s_j (u32: cached U = D W)
   dho2g::DevBuf<float> Z, RZ;                               // GEMM outputs (Bcap x max s)
   dho2g::DevBuf<float> lab;                                 // gathered labels (Bcap)
   dho2g::DevBuf<double> sample_loss;                        // per-sample loss (Bcap)
@@ -102,6 +102,7 @@ struct dho2g_mlp {
   const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
   const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)
   const void* input_owner = nullptr;   // operator whose curvature batch is packed at level 0
+  const float* prepared = nullptr;     // w whose v-independent HVP quantities are cached
 
   void ensure_batch(size_t B);
 };
@@ -112,14 +113,11 @@ void mlp_load_weights(dho2g_mlp* m, const float* w);
 void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale /* device scalar or null */);
 // Pack level-0 operands from dataset rows X[idx[b]] (idx null: b itself); labels likewise.
 void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool with_r);
-void mlp_forward(dho2g_mlp* m, const float* w, size_t B, bool with_r);
-// Output delta (and R-delta); fills sample_loss/sample_correct. scale = 1/B (times 1/C).
-void mlp_output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool with_r);
-// Backward into out (flat n-vector, fully overwritten): gradient or Hv.
-void mlp_backward(dho2g_mlp* m, const float* w, size_t B, float* out, bool with_r);
 // Convenience compositions.
 void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double scale, float* g);
+// Caches A, Z, softmax, D and U at the loaded point (Lanczos applies H m times at one point).
+void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale);
 void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv);
 // Forward-only evaluation: adds sum of per-sample loss and correct count into acc[0], acc[1] (fp64).
 void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,

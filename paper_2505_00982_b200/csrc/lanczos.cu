@@ -413,30 +413,34 @@ __global__ void __launch_bounds__(256) ritz_kernel(const float* __restrict__ D, 
   }
 }
 
-// per-column argmax |x| with the lowest index on ties (lanczos.cpp:82-94)
-__global__ void col_argmax_kernel(const float* __restrict__ V, size_t ldv, size_t rows, size_t begin,
-                                  double* __restrict__ out /* r x 3: maxabs, global index, value */) {
-  const int c = blockIdx.x;
+// per-column argmax |x| with the lowest index on ties (lanczos.cpp:82-94): blocks own contiguous
+// row segments of one column; partials (maxabs, global index, value) merged in segment order.
+constexpr int kArgThreads = 256;
+__global__ void col_argmax_kernel(const float* __restrict__ V, size_t ldv, size_t rows, size_t begin, size_t seg,
+                                  double* __restrict__ part /* [c][blk][3] */) {
+  const int c = blockIdx.y;
   const float* col = V + (size_t)c * ldv;
+  const size_t r0 = blockIdx.x * seg, r1 = min(rows, r0 + seg);
   float best = -1.f;
-  size_t bi = 0;
+  size_t bi = r0;
   float bv = 0.f;
-  for (size_t r = threadIdx.x; r < rows; r += blockDim.x) {
-    const float a = fabsf(col[r]);
+  for (size_t r = r0 + threadIdx.x; r < r1; r += kArgThreads) {
+    const float x = col[r];
+    const float a = fabsf(x);
     if (a > best) {
       best = a;
       bi = r;
-      bv = col[r];
+      bv = x;
     }
   }
-  __shared__ float sb[1024];
-  __shared__ size_t si[1024];
-  __shared__ float sv[1024];
+  __shared__ float sb[kArgThreads];
+  __shared__ size_t si[kArgThreads];
+  __shared__ float sv[kArgThreads];
   sb[threadIdx.x] = best;
   si[threadIdx.x] = bi;
   sv[threadIdx.x] = bv;
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+  for (int s = kArgThreads / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
       const float ob = sb[threadIdx.x + s];
       const size_t oi = si[threadIdx.x + s];
@@ -449,10 +453,27 @@ __global__ void col_argmax_kernel(const float* __restrict__ V, size_t ldv, size_
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out[3 * c] = sb[0];
-    out[3 * c + 1] = (double)(begin + si[0]);
-    out[3 * c + 2] = sv[0];
+    double* o = part + ((size_t)c * gridDim.x + blockIdx.x) * 3;
+    o[0] = sb[0];
+    o[1] = (double)(begin + si[0]);
+    o[2] = sv[0];
   }
+}
+
+__global__ void col_argmax_final_kernel(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  const int c = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const double* p = part + (size_t)c * nblk * 3;
+  double best = p[0], bidx = p[1], bval = p[2];
+  for (int b = 1; b < nblk; ++b)  // later segments win only on a strictly larger |x|
+    if (p[3 * b] > best) {
+      best = p[3 * b];
+      bidx = p[3 * b + 1];
+      bval = p[3 * b + 2];
+    }
+  out[3 * c] = best;
+  out[3 * c + 1] = bidx;
+  out[3 * c + 2] = bval;
 }
 
 int grid_for(dho2g_ctx* ctx, size_t work, int threads, int per_sm = 4) {
@@ -646,8 +667,14 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   }
   DevBuf<double> am((size_t)3 * r);
   DevBuf<double> amall((size_t)3 * r * ctx->world);
-  col_argmax_kernel<<<r, 1024, 0, st>>>(ese->V.p, ese->ldv, lz->rows, lz->begin, am.p);
-  DHO2G_LAUNCH();
+  {
+    const int nblk = (int)std::max<size_t>(1, std::min<size_t>(cdiv(lz->rows, 4 * kArgThreads), 256));
+    const size_t seg = cdiv(std::max<size_t>(lz->rows, 1), (size_t)nblk);
+    DevBuf<double> part((size_t)3 * r * nblk);
+    col_argmax_kernel<<<dim3(nblk, r), kArgThreads, 0, st>>>(ese->V.p, ese->ldv, lz->rows, lz->begin, seg, part.p);
+    col_argmax_final_kernel<<<r, 32, 0, st>>>(part.p, nblk, am.p);
+    DHO2G_LAUNCH();
+  }
   ctx->allgather_f64(am.p, amall.p, (size_t)3 * r);
   std::vector<double> h_am((size_t)3 * r * ctx->world);
   int h_status = 0;

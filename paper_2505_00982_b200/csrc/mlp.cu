@@ -7,6 +7,11 @@
 //   backward   U  = D W              RU = [D | RD] [V^T | W^T]^T     (K = out, 2 out)
 //   weight     hvW = [RD^T | D^T] [A^T | RA^T]^T                     (K = 2B)
 // with every operand stored K-major as (hi, lo) bf16 pairs so all GEMMs are "TN" for tcgen05.
+//
+// A Lanczos refresh applies H at ONE point w on ONE curvature batch m times, so everything that
+// does not depend on the direction v (A, Z, softmax, D, U for every layer) is computed once by
+// mlp_prepare_point() and cached; each mlp_hvp_cached() then only runs the R-GEMMs (RZ, RU) and the
+// weight-block GEMM: 6 of the 8 per-layer GEMM units of oracle.cpp:524-647 (2 of 3 at layer 0).
 #include <cmath>
 
 #include "internal.h"
@@ -20,7 +25,7 @@ void dho2g_mlp::ensure_batch(size_t B) {
   const int Ls = L;
   AR_hi.resize(Ls); AR_lo.resize(Ls); ART_hi.resize(Ls); ART_lo.resize(Ls);
   DR_hi.resize(Ls + 1); DR_lo.resize(Ls + 1); DRT_hi.resize(Ls + 1); DRT_lo.resize(Ls + 1);
-  a32.resize(Ls + 1); ra32.resize(Ls + 1); d32.resize(Ls + 1); rd32.resize(Ls + 1);
+  a32.resize(Ls + 1); ra32.resize(Ls + 1); d32.resize(Ls + 1); rd32.resize(Ls + 1); u32.resize(Ls + 1);
   for (int j = 0; j <= Ls; ++j) {
     const size_t s = sizes[j], P = round_up(s, 8);
     if (j < Ls) {
@@ -31,6 +36,7 @@ void dho2g_mlp::ensure_batch(size_t B) {
       DR_hi[j].alloc(nB * 2 * P); DR_lo[j].alloc(nB * 2 * P);
       DRT_hi[j].alloc(s * 2 * nBp); DRT_lo[j].alloc(s * 2 * nBp);
       a32[j].alloc(nB * s); ra32[j].alloc(nB * s); d32[j].alloc(nB * s); rd32[j].alloc(nB * s);
+      if (j < Ls) u32[j].alloc(nB * s);
     }
   }
   Z.alloc(nB * smax);
@@ -40,6 +46,7 @@ void dho2g_mlp::ensure_batch(size_t B) {
   sample_correct.alloc(nB);
   Bcap = nB;
   Bpcap = nBp;
+  prepared = nullptr;
 }
 
 namespace {
@@ -87,15 +94,16 @@ enum Mode { M_INPUT = 0, M_FWD = 1, M_FWD_OUT = 2, M_BWD = 3, M_DPACK = 4 };
 
 struct TileArgs {
   int B, s, P, Bp, ldT;  // batch, width, half width, padded batch, transposed row stride
-  bool with_r, relu;
+  bool do0, do1, relu;   // compute/pack the plain (x0) and/or the R (x1) quantity
   // sources
   const float* X; const int64_t* idx; int ldX;  // M_INPUT
-  const float* Zs; const float* RZs;             // GEMM outputs (B x s)
+  const float* Zs; const float* RZs;             // GEMM outputs (B x s): Z or U, RZ or RU
   const float* bias; const float* vbias; const float* vscale;
-  const float* a_in; const float* ra_in;         // M_BWD: level activations
+  const float* a_in; const float* ra_in;         // cached activations of this level
+  const float* u_in;                             // cached U (M_BWD with !do0)
   const float* d_in; const float* rd_in;         // M_DPACK
   // fp32 outputs (B x s)
-  float* o0; float* o1;
+  float* o0; float* o1; float* u_out;
   // packed outputs
   bf16 *Rh, *Rl;   // row-major pairs (B x 2P): x0 -> half 0, x1 -> half 1
   bf16 *Th, *Tl;   // transposed pairs (s x ldT): x0 -> half t0, x1 -> half t1
@@ -106,48 +114,56 @@ template <int MODE>
 __global__ void tile_epilogue_kernel(TileArgs a) {
   __shared__ float s0[TILE][TILE + 1], s1[TILE][TILE + 1];
   const int k0 = blockIdx.x * TILE, b0 = blockIdx.y * TILE;
-  const float vsc = (a.vscale && a.with_r) ? *a.vscale : 1.0f;
+  const float vsc = (a.vscale && a.do1) ? *a.vscale : 1.0f;
   for (int i = threadIdx.y; i < TILE; i += blockDim.y) {
     const int b = b0 + i, k = k0 + threadIdx.x;
     float x0 = 0.f, x1 = 0.f;
-    const bool valid = b < a.B && k < a.s;
-    if (valid) {
+    if (b < a.B && k < a.s) {
       const size_t e = (size_t)b * a.s + k;
       if (MODE == M_INPUT) {
         const int64_t row = a.idx ? a.idx[b] : b;
         x0 = a.X[(size_t)row * a.ldX + k];
       } else if (MODE == M_FWD || MODE == M_FWD_OUT) {
-        const float z = a.Zs[e] + a.bias[k];
-        if (MODE == M_FWD_OUT) {
-          x0 = z;
-          if (a.with_r) x1 = a.RZs[e] + vsc * a.vbias[k];
+        // oracle.cpp:548-563: z = b + W a ; a' = act(z) ; ra' = act'(a') (v_b + V a + W ra)
+        if (a.do0) {
+          const float z = a.Zs[e] + a.bias[k];
+          x0 = MODE == M_FWD_OUT ? z : (a.relu ? fmaxf(z, 0.f) : tanhf(z));
+          a.o0[e] = x0;
         } else {
-          // oracle.cpp:559-563: a = act(z); ra = act'(a) * rz
-          const float av = a.relu ? fmaxf(z, 0.f) : tanhf(z);
-          x0 = av;
-          if (a.with_r) {
-            const float ap = a.relu ? (av > 0.f ? 1.f : 0.f) : 1.f - av * av;
-            x1 = ap * (a.RZs[e] + vsc * a.vbias[k]);
-          }
+          x0 = a.a_in[e];
         }
-        a.o0[e] = x0;
-        if (a.with_r) a.o1[e] = x1;
+        if (a.do1) {
+          const float rz = a.RZs[e] + vsc * a.vbias[k];
+          if (MODE == M_FWD_OUT) {
+            x1 = rz;
+          } else {
+            const float ap = a.relu ? (x0 > 0.f ? 1.f : 0.f) : 1.f - x0 * x0;
+            x1 = ap * rz;
+          }
+          a.o1[e] = x1;
+        }
       } else if (MODE == M_BWD) {
         // oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh only)
-        const float u = a.Zs[e];
         const float av = a.a_in[e];
         const float ap = a.relu ? (av > 0.f ? 1.f : 0.f) : 1.f - av * av;
-        x0 = u * ap;
-        if (a.with_r) {
+        float u;
+        if (a.do0) {
+          u = a.Zs[e];
+          x0 = u * ap;
+          a.o0[e] = x0;
+          if (a.u_out) a.u_out[e] = u;
+        } else {
+          u = a.u_in[e];
+        }
+        if (a.do1) {
           float rap = 0.f;
           if (!a.relu && ap != 0.f) rap = -2.f * av * a.ra_in[e];
           x1 = a.RZs[e] * ap + u * rap;
+          a.o1[e] = x1;
         }
-        a.o0[e] = x0;
-        if (a.with_r) a.o1[e] = x1;
       } else {  // M_DPACK
-        x0 = a.d_in[e];
-        if (a.with_r) x1 = a.rd_in[e];
+        if (a.do0) x0 = a.d_in[e];
+        if (a.do1) x1 = a.rd_in[e];
       }
     }
     if (MODE == M_FWD_OUT) continue;
@@ -156,10 +172,12 @@ __global__ void tile_epilogue_kernel(TileArgs a) {
     if (b < a.B && k < a.P && a.Rh) {
       bf16 h, l;
       const size_t r = (size_t)b * (2 * a.P) + k;
-      split_bf16(x0, h, l);
-      a.Rh[r] = h;
-      a.Rl[r] = l;
-      if (a.with_r) {
+      if (a.do0) {
+        split_bf16(x0, h, l);
+        a.Rh[r] = h;
+        a.Rl[r] = l;
+      }
+      if (a.do1) {
         split_bf16(x1, h, l);
         a.Rh[r + a.P] = h;
         a.Rl[r + a.P] = l;
@@ -173,12 +191,12 @@ __global__ void tile_epilogue_kernel(TileArgs a) {
     if (k < a.s && b < a.Bp) {
       const size_t r = (size_t)k * a.ldT + b;
       bf16 h, l;
-      if (a.t0 >= 0) {
+      if (a.do0 && a.t0 >= 0) {
         split_bf16(s0[threadIdx.x][i], h, l);
         a.Th[r + (size_t)a.t0 * a.Bp] = h;
         a.Tl[r + (size_t)a.t0 * a.Bp] = l;
       }
-      if (a.with_r && a.t1 >= 0) {
+      if (a.do1 && a.t1 >= 0) {
         split_bf16(s1[threadIdx.x][i], h, l);
         a.Th[r + (size_t)a.t1 * a.Bp] = h;
         a.Tl[r + (size_t)a.t1 * a.Bp] = l;
@@ -188,29 +206,31 @@ __global__ void tile_epilogue_kernel(TileArgs a) {
 }
 
 template <int MODE>
-void launch_tile(cudaStream_t st, const TileArgs& a) {
+void launch_tile(dho2g_ctx* ctx, const TileArgs& a) {
   dim3 grid(cdiv(std::max(a.P, a.s), TILE), cdiv(std::max(a.Bp, a.B), TILE));
-  tile_epilogue_kernel<MODE><<<grid, dim3(TILE, 8), 0, st>>>(a);
+  const int slot = ctx->kt_begin();
+  tile_epilogue_kernel<MODE><<<grid, dim3(TILE, 8), 0, ctx->stream>>>(a);
   DHO2G_LAUNCH();
+  ctx->kt_end(slot, "tile_epilogue", 0.0);
 }
 
 // ------------------------------------------------------------------ output layer delta
 // oracle.cpp:476-495 (delta) and :572-599 (R-delta); also per-sample loss / correctness.
-__global__ void output_delta_kernel(int B, int O, int mse, int ncls, int with_r, double scale,
+__global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, int do1, double scale,
                                     const float* __restrict__ z, const float* __restrict__ rz,
                                     const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
                                     double* __restrict__ loss, int* __restrict__ correct) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const float* o = z + (size_t)b * O;
-  const float* ro = with_r ? rz + (size_t)b * O : nullptr;
+  const float* ro = do1 ? rz + (size_t)b * O : nullptr;
   float* dd = d + (size_t)b * O;
-  float* rdd = with_r ? rd + (size_t)b * O : nullptr;
+  float* rdd = do1 ? rd + (size_t)b * O : nullptr;
   const float y = lab[b];
   int best = 0;
   for (int j = 1; j < O; ++j)
     if (o[j] > o[best]) best = j;
-  correct[b] = (ncls > 0 && best == (int)y) ? 1 : 0;
+  if (do0) correct[b] = (ncls > 0 && best == (int)y) ? 1 : 0;
   if (!mse) {
     const int lbl = (int)y;
     const float mx = o[best];
@@ -219,25 +239,25 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int with_r,
     double sdot = 0.0;
     for (int j = 0; j < O; ++j) {
       const double soft = exp((double)o[j] - (double)mx) / den;
-      dd[j] = (float)((soft - (j == lbl ? 1.0 : 0.0)) * scale);
-      if (with_r) sdot += soft * ro[j];
+      if (do0) dd[j] = (float)((soft - (j == lbl ? 1.0 : 0.0)) * scale);
+      if (do1) sdot += soft * ro[j];
     }
-    if (with_r)
+    if (do1)
       for (int j = 0; j < O; ++j) {
         const double soft = exp((double)o[j] - (double)mx) / den;
         rdd[j] = (float)(soft * (ro[j] - sdot) * scale);
       }
-    loss[b] = (double)mx + log(den) - (double)o[lbl];
+    if (do0) loss[b] = (double)mx + log(den) - (double)o[lbl];
   } else {
     double acc = 0.0;
     for (int j = 0; j < O; ++j) {
       const float t = ncls > 0 ? (j == (int)y ? 1.f : 0.f) : (j == 0 ? y : 0.f);
       const float df = o[j] - t;
-      dd[j] = (float)(df * scale);
-      if (with_r) rdd[j] = (float)(ro[j] * scale);
+      if (do0) dd[j] = (float)(df * scale);
+      if (do1) rdd[j] = (float)(ro[j] * scale);
       acc += 0.5 * (double)df * (double)df;
     }
-    loss[b] = acc;
+    if (do0) loss[b] = acc;
   }
 }
 
@@ -289,143 +309,145 @@ __global__ void eval_reduce_kernel(int B, const double* __restrict__ loss, const
 
 namespace dho2g {
 
-void mlp_load_weights(dho2g_mlp* m, const float* w) {
+static void pack_params(dho2g_mlp* m, const float* p, const float* pscale, int half) {
   cudaStream_t st = m->ctx->stream;
-  m->w_cur = w;
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
     dim3 grid(cdiv(std::max(ld.Pin, ld.in), TILE), cdiv(std::max(ld.Pout, ld.out), TILE));
-    pack_weights_kernel<<<grid, dim3(TILE, 8), 0, st>>>(
-        w + ld.w_off, nullptr, ld.in, ld.out, ld.Pin, ld.Pout, 1, m->WV_hi[t].p, m->WV_lo[t].p,
-        t > 0 ? m->WVt_hi[t].p : nullptr, t > 0 ? m->WVt_lo[t].p : nullptr);
+    const int slot = m->ctx->kt_begin();
+    pack_weights_kernel<<<grid, dim3(TILE, 8), 0, st>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, ld.Pout, half,
+                                                        m->WV_hi[t].p, m->WV_lo[t].p, t > 0 ? m->WVt_hi[t].p : nullptr,
+                                                        t > 0 ? m->WVt_lo[t].p : nullptr);
     DHO2G_LAUNCH();
+    // algorithmic bytes: read fp32 (4) + write hi/lo to both layouts (2 x 4)
+    m->ctx->kt_end(slot, "pack_params", (double)ld.in * ld.out * (t > 0 ? 12.0 : 8.0));
   }
 }
 
-void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale) {
-  cudaStream_t st = m->ctx->stream;
-  for (int t = 0; t < m->L; ++t) {
-    const LayerDesc& ld = m->layers[t];
-    dim3 grid(cdiv(std::max(ld.Pin, ld.in), TILE), cdiv(std::max(ld.Pout, ld.out), TILE));
-    pack_weights_kernel<<<grid, dim3(TILE, 8), 0, st>>>(
-        v + ld.w_off, vscale, ld.in, ld.out, ld.Pin, ld.Pout, 0, m->WV_hi[t].p, m->WV_lo[t].p,
-        t > 0 ? m->WVt_hi[t].p : nullptr, t > 0 ? m->WVt_lo[t].p : nullptr);
-    DHO2G_LAUNCH();
-  }
+void mlp_load_weights(dho2g_mlp* m, const float* w) {
+  m->w_cur = w;
+  m->prepared = nullptr;
+  pack_params(m, w, nullptr, 1);
 }
+
+void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale) { pack_params(m, v, vscale, 0); }
 
 void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool /*with_r*/) {
   m->ensure_batch(B);
   m->input_owner = nullptr;
+  m->prepared = nullptr;
   cudaStream_t st = m->ctx->stream;
   TileArgs a{};
   const int s0 = (int)m->sizes[0];
   a.B = (int)B; a.s = s0; a.P = (int)round_up(s0, 8); a.Bp = (int)round_up(B, 8); a.ldT = (int)(2 * m->Bpcap);
-  a.with_r = false;
+  a.do0 = true; a.do1 = false;
   a.X = X; a.idx = idx; a.ldX = s0;
   a.Rh = m->AR_hi[0].p; a.Rl = m->AR_lo[0].p; a.Th = m->ART_hi[0].p; a.Tl = m->ART_lo[0].p;
   a.t0 = 0; a.t1 = -1;
-  launch_tile<M_INPUT>(st, a);
+  launch_tile<M_INPUT>(m->ctx, a);
   gather_labels_kernel<<<cdiv(B, 256), 256, 0, st>>>((int)B, y, idx, m->lab.p);
   DHO2G_LAUNCH();
 }
 
-void mlp_forward(dho2g_mlp* m, const float* w, size_t B, bool with_r) {
+// Forward pass. do0: plain activations (Z GEMM, act, pack a). do1: R-activations (RZ GEMM).
+static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) {
   dho2g_ctx* ctx = m->ctx;
   const int Bp = (int)round_up(B, 8);
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
     const bool last = t + 1 == m->L;
     const int lda = 2 * ld.Pin;
-    // Z = A W^T
-    gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
-          m->WV_lo[t].p + ld.Pin, lda, m->Z.p, ld.out, 1.0f);
-    if (with_r) {
-      // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
+    if (do0)  // Z = A W^T
+      gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
+            m->WV_lo[t].p + ld.Pin, lda, m->Z.p, ld.out, 1.0f);
+    if (do1) {  // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
       const int K = t == 0 ? ld.in : 2 * ld.Pin;
       gemm3(ctx, (int)B, ld.out, K, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p, m->WV_lo[t].p, lda, m->RZ.p,
             ld.out, 1.0f);
     }
     TileArgs a{};
     a.B = (int)B; a.s = ld.out; a.P = ld.Pout; a.Bp = Bp; a.ldT = (int)(2 * m->Bpcap);
-    a.with_r = with_r; a.relu = m->act == 1;
-    a.Zs = m->Z.p; a.RZs = m->RZ.p; a.bias = w + ld.b_off; a.vbias = m->v_bias_ptr ? m->v_bias_ptr + ld.b_off : nullptr;
+    a.do0 = do0; a.do1 = do1; a.relu = m->act == 1;
+    a.Zs = m->Z.p; a.RZs = m->RZ.p; a.bias = w + ld.b_off; a.vbias = do1 ? m->v_bias_ptr + ld.b_off : nullptr;
     a.vscale = m->v_scale_ptr;
+    a.a_in = m->a32[t + 1].p;
     a.o0 = m->a32[t + 1].p; a.o1 = m->ra32[t + 1].p;
     if (last) {
-      launch_tile<M_FWD_OUT>(ctx->stream, a);
+      launch_tile<M_FWD_OUT>(ctx, a);
     } else {
       a.Rh = m->AR_hi[t + 1].p; a.Rl = m->AR_lo[t + 1].p; a.Th = m->ART_hi[t + 1].p; a.Tl = m->ART_lo[t + 1].p;
       a.t0 = 0; a.t1 = 1;
-      launch_tile<M_FWD>(ctx->stream, a);
+      launch_tile<M_FWD>(ctx, a);
     }
   }
 }
 
-void mlp_output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool with_r) {
-  cudaStream_t st = m->ctx->stream;
+static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool do0, bool do1) {
   const int L = m->L;
   const int O = (int)m->sizes[L];
-  output_delta_kernel<<<cdiv(B, 128), 128, 0, st>>>((int)B, O, m->loss, (int)ncls, with_r ? 1 : 0, scale,
-                                                     m->a32[L].p, m->ra32[L].p, m->lab.p, m->d32[L].p, m->rd32[L].p,
-                                                     m->sample_loss.p, m->sample_correct.p);
+  output_delta_kernel<<<cdiv(B, 128), 128, 0, m->ctx->stream>>>((int)B, O, m->loss, (int)ncls, do0, do1, scale,
+                                                                   m->a32[L].p, m->ra32[L].p, m->lab.p, m->d32[L].p,
+                                                                   m->rd32[L].p, m->sample_loss.p,
+                                                                   m->sample_correct.p);
   DHO2G_LAUNCH();
-}
-
-static void pack_delta_level(dho2g_mlp* m, int j, size_t B, bool with_r, int mode, const float* U, const float* RU) {
   TileArgs a{};
-  const int s = (int)m->sizes[j];
+  const int s = O;
   a.B = (int)B; a.s = s; a.P = (int)round_up(s, 8); a.Bp = (int)round_up(B, 8); a.ldT = (int)(2 * m->Bpcap);
-  a.with_r = with_r; a.relu = m->act == 1;
-  a.Rh = m->DR_hi[j].p; a.Rl = m->DR_lo[j].p; a.Th = m->DRT_hi[j].p; a.Tl = m->DRT_lo[j].p;
-  // transposed pair is [rd^T | d^T]: d -> half 1, rd -> half 0
-  a.t0 = 1; a.t1 = 0;
-  if (mode == M_DPACK) {
-    a.d_in = m->d32[j].p; a.rd_in = m->rd32[j].p;
-    launch_tile<M_DPACK>(m->ctx->stream, a);
-  } else {
-    a.Zs = U; a.RZs = RU; a.a_in = m->a32[j].p; a.ra_in = m->ra32[j].p;
-    a.o0 = m->d32[j].p; a.o1 = m->rd32[j].p;
-    launch_tile<M_BWD>(m->ctx->stream, a);
-  }
+  a.do0 = do0; a.do1 = do1;
+  a.Rh = m->DR_hi[L].p; a.Rl = m->DR_lo[L].p; a.Th = m->DRT_hi[L].p; a.Tl = m->DRT_lo[L].p;
+  a.t0 = 1; a.t1 = 0;  // transposed pair is [rd^T | d^T]
+  a.d_in = m->d32[L].p; a.rd_in = m->rd32[L].p;
+  launch_tile<M_DPACK>(m->ctx, a);
 }
 
 static void bias_sum(dho2g_mlp* m, int B, int O, const float* src, float* out) {
   m->red.ensure((size_t)kBiasChunks * m->smax);
   cudaStream_t st = m->ctx->stream;
+  const int slot = m->ctx->kt_begin();
   bias_partial_kernel<<<dim3(cdiv(O, 128), kBiasChunks), 128, 0, st>>>(B, O, src, m->red.p);
   bias_final_kernel<<<cdiv(O, 128), 128, 0, st>>>(O, m->red.p, out);
   DHO2G_LAUNCH();
+  m->ctx->kt_end(slot, "bias_sum", 4.0 * B * O);
 }
 
-void mlp_backward(dho2g_mlp* m, const float* /*w*/, size_t B, float* out, bool with_r) {
+// Backward pass. do0: deltas d (U GEMMs) and, if wgrad, the gradient blocks. do1: R-deltas (RU GEMMs)
+// and the Hessian blocks hvW into `out`.
+static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, bool wgrad) {
   dho2g_ctx* ctx = m->ctx;
   const int L = m->L;
   const int Bp = (int)round_up(B, 8);
   const int ldT = (int)(2 * m->Bpcap);
-  pack_delta_level(m, L, B, with_r, M_DPACK, nullptr, nullptr);
   for (int t = L - 1; t >= 0; --t) {
     const LayerDesc& ld = m->layers[t];
     const int j = t + 1;
-    // weight block: hvW = [RD^T | D^T] [A^T | RA^T]^T; grad: D^T A
-    if (with_r) {
+    if (do1) {  // hvW = [RD^T | D^T] [A^T | RA^T]^T ; hv_b = sum_b rd (oracle.cpp:606-613)
       const int K = t == 0 ? Bp : 2 * Bp;
       gemm3(ctx, ld.out, ld.in, K, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p, m->ART_lo[t].p, ldT,
             out + ld.w_off, ld.in, 1.0f);
-    } else {
+      bias_sum(m, (int)B, ld.out, m->rd32[j].p, out + ld.b_off);
+    } else if (wgrad) {  // gW = D^T A ; g_b = sum_b d (oracle.cpp:497-504)
       gemm3(ctx, ld.out, ld.in, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p, m->ART_lo[t].p,
             ldT, out + ld.w_off, ld.in, 1.0f);
+      bias_sum(m, (int)B, ld.out, m->d32[j].p, out + ld.b_off);
     }
-    bias_sum(m, (int)B, ld.out, with_r ? m->rd32[j].p : m->d32[j].p, out + ld.b_off);
     if (t > 0) {
       const int lda = 2 * ld.Pout;
-      // U = D W ; RU = [D | RD] [V^T | W^T]^T
-      gemm3(ctx, (int)B, ld.in, ld.out, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p + ld.Pout,
-            m->WVt_lo[t].p + ld.Pout, lda, m->Z.p, ld.in, 1.0f);
-      if (with_r)
-        gemm3(ctx, (int)B, ld.in, 2 * ld.Pout, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p, m->WVt_lo[t].p, lda,
-              m->RZ.p, ld.in, 1.0f);
-      pack_delta_level(m, t, B, with_r, M_BWD, m->Z.p, m->RZ.p);
+      if (do0)  // U = D W
+        gemm3(ctx, (int)B, ld.in, ld.out, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p + ld.Pout,
+              m->WVt_lo[t].p + ld.Pout, lda, m->Z.p, ld.in, 1.0f);
+      if (do1)  // RU = [D | RD] [V^T | W^T]^T
+        gemm3(ctx, (int)B, ld.in, 2 * ld.Pout, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p, m->WVt_lo[t].p,
+              lda, m->RZ.p, ld.in, 1.0f);
+      TileArgs a{};
+      const int s = (int)m->sizes[t];
+      a.B = (int)B; a.s = s; a.P = (int)round_up(s, 8); a.Bp = Bp; a.ldT = ldT;
+      a.do0 = do0; a.do1 = do1; a.relu = m->act == 1;
+      a.Rh = m->DR_hi[t].p; a.Rl = m->DR_lo[t].p; a.Th = m->DRT_hi[t].p; a.Tl = m->DRT_lo[t].p;
+      a.t0 = 1; a.t1 = 0;
+      a.Zs = m->Z.p; a.RZs = m->RZ.p; a.a_in = m->a32[t].p; a.ra_in = m->ra32[t].p;
+      a.u_in = m->u32[t].p; a.u_out = do0 ? m->u32[t].p : nullptr;
+      a.o0 = m->d32[t].p; a.o1 = m->rd32[t].p;
+      launch_tile<M_BWD>(ctx, a);
     }
   }
 }
@@ -433,26 +455,34 @@ void mlp_backward(dho2g_mlp* m, const float* /*w*/, size_t B, float* out, bool w
 void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double scale, float* g) {
   mlp_set_input(m, X, y, idx, B, false);
-  mlp_forward(m, w, B, false);
-  mlp_output_delta(m, B, ncls, scale, false);
-  mlp_backward(m, w, B, g, false);
+  forward(m, w, B, true, false);
+  output_delta(m, B, ncls, scale, true, false);
+  backward(m, B, g, true, false, true);
+}
+
+void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale) {
+  // input and weights must already be loaded (mlp_set_input / mlp_load_weights)
+  forward(m, m->w_cur, B, true, false);
+  output_delta(m, B, ncls, scale, true, false);
+  backward(m, B, nullptr, true, false, false);
+  m->prepared = m->w_cur;
 }
 
 void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv) {
-  // input and weights must already be loaded (mlp_set_input / mlp_load_weights)
+  if (m->prepared != m->w_cur) mlp_prepare_point(m, B, ncls, scale);
   m->v_bias_ptr = v;
   m->v_scale_ptr = vscale;
   mlp_load_direction(m, v, vscale);
-  mlp_forward(m, m->w_cur, B, true);
-  mlp_output_delta(m, B, ncls, scale, true);
-  mlp_backward(m, m->w_cur, B, hv, true);
+  forward(m, m->w_cur, B, false, true);
+  output_delta(m, B, ncls, scale, false, true);
+  backward(m, B, hv, false, true, false);
 }
 
 void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double* acc2) {
   mlp_set_input(m, X, y, idx, B, false);
-  mlp_forward(m, w, B, false);
-  mlp_output_delta(m, B, ncls, 1.0, false);
+  forward(m, w, B, true, false);
+  output_delta(m, B, ncls, 1.0, true, false);
   eval_reduce_kernel<<<1, 1024, 0, m->ctx->stream>>>((int)B, m->sample_loss.p, m->sample_correct.p, acc2);
   DHO2G_LAUNCH();
 }
