@@ -4,6 +4,10 @@
 //   P2  g2 = g~ - V c ; s = base_step(g2) ; sc = V^T s       reads V, g, pi, moments(, w); writes moments, s
 //   P3  w_a += (s - V sc) + (-alpha V (c / den))             reads V, s, w_a; writes w_a
 // with the r-length reductions (c, sc) as fp64 partials + all_gather + rank-ordered sums.
+//
+// Access pattern follows the Gram-Schmidt passes (lanczos.cu): row chunks of 2048 staged through
+// shared memory; "dot" work is split into (column, 512-row block) items so every warp streams
+// 2 KB contiguous per column; "axpy" work keeps 4 rows per thread with float4 loads.
 #include <cmath>
 
 #include "internal.h"
@@ -14,7 +18,9 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kW = kT / 32;
-constexpr int kCh = 1024;  // rows staged per chunk
+constexpr int kCh = 2048;            // rows staged per chunk
+constexpr int kSubRows = 512;        // rows per warp dot item (32 lanes x 4 float4)
+constexpr int kItemsPerChunk = kCh / kSubRows;
 
 __device__ __forceinline__ double floored_den(double a, double fl, double sigma) {  // optimizer.cpp:75-79, :94-98
   double f;
@@ -28,13 +34,31 @@ __device__ __forceinline__ double floored_den(double a, double fl, double sigma)
   return den;
 }
 
-// grid-level deterministic reduction helper: per-CTA partial rows -> rank partial via ticket
-__device__ void finish_partials(const double* acc_w /* [kW][nj] */, int nj, double* part, double* rankp,
-                                unsigned* ticket) {
+__device__ __forceinline__ float4 ld4(const float* p, size_t r, size_t rows) {
+  if (r + 3 < rows) return *reinterpret_cast<const float4*>(p + r);
+  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (r < rows) x.x = p[r];
+  if (r + 1 < rows) x.y = p[r + 1];
+  if (r + 2 < rows) x.z = p[r + 2];
+  return x;
+}
+__device__ __forceinline__ void st4(float* p, size_t r, size_t rows, float4 x) {
+  if (r + 3 < rows) {
+    *reinterpret_cast<float4*>(p + r) = x;
+    return;
+  }
+  if (r < rows) p[r] = x.x;
+  if (r + 1 < rows) p[r + 1] = x.y;
+  if (r + 2 < rows) p[r + 2] = x.z;
+}
+
+// acc[w][j] -> CTA partials -> (last CTA, fixed order) rank partial
+__device__ void finish_partials(const double* acc, int nj, double* part, double* rankp, unsigned* ticket) {
   __shared__ bool is_last;
+  __syncthreads();
   for (int j = threadIdx.x; j < nj; j += kT) {
     double t = 0.0;
-    for (int w = 0; w < kW; ++w) t += acc_w[w * nj + j];
+    for (int w = 0; w < kW; ++w) t += acc[w * nj + j];
     part[(size_t)blockIdx.x * nj + j] = t;
   }
   __threadfence();
@@ -51,17 +75,24 @@ __device__ void finish_partials(const double* acc_w /* [kW][nj] */, int nj, doub
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// chunk-staged dots: acc[w][j] += V_j[chunk] . x[chunk] for x staged in smem
+// acc[w][j] += V_j[r0 : r0 + kCh] . xs (xs staged in smem); V is padded to whole chunks
 __device__ __forceinline__ void chunk_dots(const float* __restrict__ V, size_t ldv, size_t r0, int R,
                                            const float* xs, double* acc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int items = R * (kCh / 128);
+  const int items = R * kItemsPerChunk;
   for (int it = warp; it < items; it += kW) {
-    const int j = it / (kCh / 128), q = it % (kCh / 128);
-    const int rb = q * 128 + lane * 4;
-    const float4 x = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r0 + rb));
-    const float4 y = *reinterpret_cast<const float4*>(xs + rb);
-    double s = (double)x.x * y.x + (double)x.y * y.y + (double)x.z * y.z + (double)x.w * y.w;
+    const int j = it / kItemsPerChunk, q = it % kItemsPerChunk;
+    const int rb = q * kSubRows + lane * 4;
+    const float* col = V + (size_t)j * ldv + r0;
+    float4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + rb + k * 128));
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 y = *reinterpret_cast<const float4*>(xs + rb + k * 128);
+      s += (double)x[k].x * y.x + (double)x[k].y * y.y + (double)x[k].z * y.z + (double)x[k].w * y.w;
+    }
     s = warp_sum(s);
     if (lane == 0) acc[warp * R + j] += s;
   }
@@ -79,14 +110,17 @@ __global__ void __launch_bounds__(kT) upd_p1_kernel(const float* __restrict__ V,
   for (size_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const size_t r0 = c * kCh;
     __syncthreads();
-    for (int e = threadIdx.x; e < kCh; e += kT) {
-      const size_t r = r0 + e;
-      xs[e] = r < rows ? g[r] + (pi ? pi[r] : 0.f) : 0.f;
+    for (int e = threadIdx.x; e < kCh / 4; e += kT) {
+      float4 x = ld4(g, r0 + 4 * e, rows);
+      if (pi) {
+        const float4 p = ld4(pi, r0 + 4 * e, rows);
+        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+      }
+      reinterpret_cast<float4*>(xs)[e] = x;
     }
     __syncthreads();
     chunk_dots(V, ldv, r0, R, xs, acc);
   }
-  __syncthreads();
   finish_partials(acc, R, part, rankp, ticket);
 }
 
@@ -96,7 +130,21 @@ struct BaseHyper {
   float bc1, bc2;
 };
 
-// ---- P2: g2, base step (moments), s, and sc = V^T s
+__device__ __forceinline__ float base_step(const BaseHyper& hp, float gf, float& m, float& v, float w) {
+  // BaseOptimizer::step (optimizer.cpp:37-71)
+  if (hp.kind == 0) return -hp.lr * gf;
+  if (hp.kind == 1) {
+    m = hp.mom * m + gf;
+    return -hp.lr * m;
+  }
+  m = hp.b1 * m + hp.omb1 * gf;
+  v = hp.b2 * v + hp.omb2 * gf * gf;
+  float s = -hp.lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
+  if (hp.kind == 3) s -= hp.lr * hp.wd * w;
+  return s;
+}
+
+// ---- P2: g2 = g~ - V c, base step (moments), s, and sc = V^T s
 __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V, size_t ldv, int R, size_t rows,
                                                     const float* __restrict__ g, const float* __restrict__ pi,
                                                     const float* __restrict__ w, const double* __restrict__ all1,
@@ -113,43 +161,57 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
     c[j] = t;
   }
   for (int e = threadIdx.x; e < kW * R; e += kT) acc[e] = 0.0;
+  const bool need_m = hp.kind != 0, need_v = hp.kind >= 2, need_w = hp.kind == 3;
   const size_t nch = cdiv(rows, kCh);
   int local_bad = 0;
   for (size_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
     const size_t r0 = ch * kCh;
     __syncthreads();
-    for (int e = threadIdx.x; e < kCh; e += kT) {
-      const size_t r = r0 + e;
-      float sv = 0.f;
-      if (r < rows) {
-        double g2 = (double)g[r] + (pi ? (double)pi[r] : 0.0);
-        for (int j = 0; j < R; ++j) g2 -= (double)__ldg(V + (size_t)j * ldv + r) * c[j];
-        const float gf = (float)g2;
-        if (!isfinite(gf)) local_bad = 1;
-        // BaseOptimizer::step (optimizer.cpp:37-71)
-        if (hp.kind == 0) {
-          sv = -hp.lr * gf;
-        } else if (hp.kind == 1) {
-          const float mm = hp.mom * m[r] + gf;
-          m[r] = mm;
-          sv = -hp.lr * mm;
-        } else {
-          const float mm = hp.b1 * m[r] + hp.omb1 * gf;
-          const float vv = hp.b2 * v[r] + hp.omb2 * gf * gf;
-          m[r] = mm;
-          v[r] = vv;
-          sv = -hp.lr * (mm / hp.bc1) / (sqrtf(vv / hp.bc2) + hp.eps);
-          if (hp.kind == 3) sv -= hp.lr * hp.wd * w[r];
-        }
-        s_out[r] = sv;
+    for (int e = threadIdx.x; e < kCh / 4; e += kT) {
+      const size_t r = r0 + 4 * (size_t)e;
+      float4 x = ld4(g, r, rows);
+      if (pi) {
+        const float4 p = ld4(pi, r, rows);
+        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
       }
-      xs[e] = sv;
+      double g0 = x.x, g1 = x.y, g2 = x.z, g3 = x.w;
+      int j = 0;
+      for (; j + 4 <= R; j += 4) {
+        float4 d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const float4*>(V + (size_t)(j + u) * ldv + r));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double cj = c[j + u];
+          g0 -= (double)d[u].x * cj; g1 -= (double)d[u].y * cj; g2 -= (double)d[u].z * cj; g3 -= (double)d[u].w * cj;
+        }
+      }
+      for (; j < R; ++j) {
+        const float4 d = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
+        const double cj = c[j];
+        g0 -= (double)d.x * cj; g1 -= (double)d.y * cj; g2 -= (double)d.z * cj; g3 -= (double)d.w * cj;
+      }
+      const float4 gm = make_float4((float)g0, (float)g1, (float)g2, (float)g3);
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < rows) {
+        if (!isfinite(gm.x) || !isfinite(gm.y) || !isfinite(gm.z) || !isfinite(gm.w)) local_bad = 1;
+        float4 mm = need_m ? ld4(m, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 vm = need_v ? ld4(v, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 ww = need_w ? ld4(w, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+        s.x = base_step(hp, gm.x, mm.x, vm.x, ww.x);
+        s.y = r + 1 < rows ? base_step(hp, gm.y, mm.y, vm.y, ww.y) : 0.f;
+        s.z = r + 2 < rows ? base_step(hp, gm.z, mm.z, vm.z, ww.z) : 0.f;
+        s.w = r + 3 < rows ? base_step(hp, gm.w, mm.w, vm.w, ww.w) : 0.f;
+        if (need_m) st4(m, r, rows, mm);
+        if (need_v) st4(v, r, rows, vm);
+        st4(s_out, r, rows, s);
+      }
+      reinterpret_cast<float4*>(xs)[e] = s;
     }
     __syncthreads();
     if (R > 0) chunk_dots(V, ldv, r0, R, xs, acc);
   }
   if (local_bad) atomicOr(bad, 1);
-  __syncthreads();
   if (R > 0) finish_partials(acc, R, part, rankp, ticket);
 }
 
@@ -173,211 +235,28 @@ __global__ void __launch_bounds__(kT) upd_p3_kernel(const float* __restrict__ V,
     nb[j] = alpha * (c / floored_den(eigvals[j], fl, sigma));
   }
   __syncthreads();
-  for (size_t r = blockIdx.x * (size_t)kT + threadIdx.x; r < rows; r += (size_t)gridDim.x * kT) {
-    double base = s[r], newton = 0.0;
-    for (int j = 0; j < R; ++j) {
-      const double x = __ldg(V + (size_t)j * ldv + r);
-      base -= x * sc[j];
-      newton -= x * nb[j];
-    }
-    const float bf = (float)base, nf = (float)newton;
-    if (newton_out) newton_out[r] = nf;
-    if (base_out) base_out[r] = bf;
-    if (w_a) {
-      float wv = w_a[r] + bf;  // trainer.cpp:240-241 order: base, then newton
-      if (R > 0) wv += nf;
-      w_a[r] = wv;
-    }
-  }
-}
-
-// ---- vectorised variants (R <= 32, 16-byte aligned vectors): 4 rows per thread, float4 loads,
-// per-thread fp64 column accumulators, block reduction in fixed order.
-constexpr int kRT = 32;
-
-__device__ __forceinline__ float4 ld4(const float* p, size_t r, size_t rows) {
-  if (r + 3 < rows) return *reinterpret_cast<const float4*>(p + r);
-  float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (r < rows) x.x = p[r];
-  if (r + 1 < rows) x.y = p[r + 1];
-  if (r + 2 < rows) x.z = p[r + 2];
-  return x;
-}
-__device__ __forceinline__ void st4(float* p, size_t r, size_t rows, float4 x) {
-  if (r + 3 < rows) {
-    *reinterpret_cast<float4*>(p + r) = x;
-    return;
-  }
-  if (r < rows) p[r] = x.x;
-  if (r + 1 < rows) p[r + 1] = x.y;
-  if (r + 2 < rows) p[r + 2] = x.z;
-}
-
-// acc[j] (per thread) -> deterministic block sums -> part[blockIdx][j] -> ticket -> rankp[j]
-__device__ void block_finish(double (&acc)[kRT], int R, double* part, double* rankp, unsigned* ticket) {
-  __shared__ double red[kW][kRT];
-  __shared__ bool is_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < kRT; ++j) {
-    if (j < R) {
-      const double s = warp_sum(acc[j]);
-      if (lane == 0) red[warp][j] = s;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < R) {
-    double t = 0.0;
-    for (int w = 0; w < kW; ++w) t += red[w][threadIdx.x];
-    part[(size_t)blockIdx.x * R + threadIdx.x] = t;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  if (threadIdx.x < R) {
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * R + threadIdx.x];
-    rankp[threadIdx.x] = t;
-  }
-  if (threadIdx.x == 0) *ticket = 0u;
-}
-
-__global__ void __launch_bounds__(kT) upd_p1_v4(const float* __restrict__ V, size_t ldv, int R, size_t rows,
-                                                const float* __restrict__ g, const float* __restrict__ pi,
-                                                double* part, double* rankp, unsigned* ticket) {
-  double acc[kRT];
-#pragma unroll
-  for (int j = 0; j < kRT; ++j) acc[j] = 0.0;
-  const size_t ng = cdiv(rows, 4);
-  for (size_t q = blockIdx.x * (size_t)kT + threadIdx.x; q < ng; q += (size_t)gridDim.x * kT) {
-    const size_t r = 4 * q;
-    float4 x = ld4(g, r, rows);
-    if (pi) {
-      const float4 p = ld4(pi, r, rows);
-      x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
-    }
-#pragma unroll
-    for (int j = 0; j < kRT; ++j) {
-      if (j < R) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
-        acc[j] += (double)v.x * x.x + (double)v.y * x.y + (double)v.z * x.z + (double)v.w * x.w;
-      }
-    }
-  }
-  block_finish(acc, R, part, rankp, ticket);
-}
-
-__device__ __forceinline__ float base_step(const BaseHyper& hp, float gf, float& m, float& v, float w) {
-  if (hp.kind == 0) return -hp.lr * gf;
-  if (hp.kind == 1) {
-    m = hp.mom * m + gf;
-    return -hp.lr * m;
-  }
-  m = hp.b1 * m + hp.omb1 * gf;
-  v = hp.b2 * v + hp.omb2 * gf * gf;
-  float s = -hp.lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
-  if (hp.kind == 3) s -= hp.lr * hp.wd * w;
-  return s;
-}
-
-__global__ void __launch_bounds__(kT) upd_p2_v4(const float* __restrict__ V, size_t ldv, int R, size_t rows,
-                                                const float* __restrict__ g, const float* __restrict__ pi,
-                                                const float* __restrict__ w, const double* __restrict__ all1,
-                                                int world, BaseHyper hp, float* __restrict__ m,
-                                                float* __restrict__ v, float* __restrict__ s_out, double* part,
-                                                double* rankp, unsigned* ticket, int* bad) {
-  __shared__ double c[kRT];
-  if (threadIdx.x < R) {
-    double t = 0.0;
-    for (int r = 0; r < world; ++r) t += all1[(size_t)r * R + threadIdx.x];
-    c[threadIdx.x] = t;
-  }
-  __syncthreads();
-  double acc[kRT];
-#pragma unroll
-  for (int j = 0; j < kRT; ++j) acc[j] = 0.0;
-  int local_bad = 0;
-  const size_t ng = cdiv(rows, 4);
-  const bool need_m = hp.kind != 0, need_v = hp.kind >= 2, need_w = hp.kind == 3;
-  for (size_t q = blockIdx.x * (size_t)kT + threadIdx.x; q < ng; q += (size_t)gridDim.x * kT) {
-    const size_t r = 4 * q;
-    float4 x = ld4(g, r, rows);
-    if (pi) {
-      const float4 p = ld4(pi, r, rows);
-      x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
-    }
-    double g0 = x.x, g1 = x.y, g2 = x.z, g3 = x.w;
-#pragma unroll
-    for (int j = 0; j < kRT; ++j) {
-      if (j < R) {
-        const float4 vv = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
-        const double cj = c[j];
-        g0 -= (double)vv.x * cj; g1 -= (double)vv.y * cj; g2 -= (double)vv.z * cj; g3 -= (double)vv.w * cj;
-      }
-    }
-    float4 gm = make_float4((float)g0, (float)g1, (float)g2, (float)g3);
-    if (!isfinite(gm.x) || !isfinite(gm.y) || !isfinite(gm.z) || !isfinite(gm.w)) local_bad = 1;
-    float4 mm = need_m ? ld4(m, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 vm = need_v ? ld4(v, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 ww = need_w ? ld4(w, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 s;
-    s.x = base_step(hp, gm.x, mm.x, vm.x, ww.x);
-    s.y = base_step(hp, gm.y, mm.y, vm.y, ww.y);
-    s.z = base_step(hp, gm.z, mm.z, vm.z, ww.z);
-    s.w = base_step(hp, gm.w, mm.w, vm.w, ww.w);
-    if (r + 3 >= rows) {  // tail rows beyond `rows` contribute nothing
-      if (r + 1 >= rows) s.y = 0.f;
-      if (r + 2 >= rows) s.z = 0.f;
-      s.w = 0.f;
-    }
-    if (need_m) st4(m, r, rows, mm);
-    if (need_v) st4(v, r, rows, vm);
-    st4(s_out, r, rows, s);
-#pragma unroll
-    for (int j = 0; j < kRT; ++j) {
-      if (j < R) {
-        const float4 vv = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
-        acc[j] += (double)vv.x * s.x + (double)vv.y * s.y + (double)vv.z * s.z + (double)vv.w * s.w;
-      }
-    }
-  }
-  if (local_bad) atomicOr(bad, 1);
-  if (R > 0) block_finish(acc, R, part, rankp, ticket);
-}
-
-__global__ void __launch_bounds__(kT) upd_p3_v4(const float* __restrict__ V, size_t ldv, int R, size_t rows,
-                                                const float* __restrict__ s, const double* __restrict__ all1,
-                                                const double* __restrict__ all2, int world,
-                                                const double* __restrict__ eigvals, double alpha, double sigma,
-                                                double fl, float* __restrict__ w_a, float* __restrict__ newton_out,
-                                                float* __restrict__ base_out) {
-  __shared__ double sc[kRT], nb[kRT];
-  if (threadIdx.x < R) {
-    double c = 0.0, t = 0.0;
-    for (int r = 0; r < world; ++r) {
-      c += all1[(size_t)r * R + threadIdx.x];
-      t += all2[(size_t)r * R + threadIdx.x];
-    }
-    sc[threadIdx.x] = t;
-    nb[threadIdx.x] = alpha * (c / floored_den(eigvals[threadIdx.x], fl, sigma));
-  }
-  __syncthreads();
   const size_t ng = cdiv(rows, 4);
   for (size_t q = blockIdx.x * (size_t)kT + threadIdx.x; q < ng; q += (size_t)gridDim.x * kT) {
     const size_t r = 4 * q;
     const float4 s4 = ld4(s, r, rows);
     double b0 = s4.x, b1 = s4.y, b2 = s4.z, b3 = s4.w, n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+    int j = 0;
+    for (; j + 4 <= R; j += 4) {
+      float4 d[4];
 #pragma unroll
-    for (int j = 0; j < kRT; ++j) {
-      if (j < R) {
-        const float4 vv = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
-        const double a = sc[j], b = nb[j];
-        b0 -= (double)vv.x * a; b1 -= (double)vv.y * a; b2 -= (double)vv.z * a; b3 -= (double)vv.w * a;
-        n0 -= (double)vv.x * b; n1 -= (double)vv.y * b; n2 -= (double)vv.z * b; n3 -= (double)vv.w * b;
+      for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const float4*>(V + (size_t)(j + u) * ldv + r));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double a = sc[j + u], b = nb[j + u];
+        b0 -= (double)d[u].x * a; b1 -= (double)d[u].y * a; b2 -= (double)d[u].z * a; b3 -= (double)d[u].w * a;
+        n0 -= (double)d[u].x * b; n1 -= (double)d[u].y * b; n2 -= (double)d[u].z * b; n3 -= (double)d[u].w * b;
       }
+    }
+    for (; j < R; ++j) {
+      const float4 d = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
+      const double a = sc[j], b = nb[j];
+      b0 -= (double)d.x * a; b1 -= (double)d.y * a; b2 -= (double)d.z * a; b3 -= (double)d.w * a;
+      n0 -= (double)d.x * b; n1 -= (double)d.y * b; n2 -= (double)d.z * b; n3 -= (double)d.w * b;
     }
     const float4 bf = make_float4((float)b0, (float)b1, (float)b2, (float)b3);
     const float4 nf = make_float4((float)n0, (float)n1, (float)n2, (float)n3);
@@ -385,7 +264,7 @@ __global__ void __launch_bounds__(kT) upd_p3_v4(const float* __restrict__ V, siz
     if (base_out) st4(base_out, r, rows, bf);
     if (w_a) {
       float4 wv = ld4(w_a, r, rows);
-      wv.x += bf.x; wv.y += bf.y; wv.z += bf.z; wv.w += bf.w;  // trainer.cpp:240-241 order
+      wv.x += bf.x; wv.y += bf.y; wv.z += bf.z; wv.w += bf.w;  // trainer.cpp:240-241 order: base, then newton
       if (R > 0) {
         wv.x += nf.x; wv.y += nf.y; wv.z += nf.z; wv.w += nf.w;
       }
@@ -414,6 +293,22 @@ __global__ void f32_to_f64_kernel(const float* __restrict__ s, double* __restric
 }
 
 int grid_ew(size_t n) { return (int)std::max<size_t>(1, std::min<size_t>(cdiv(n, 256), 148 * 8)); }
+
+BaseHyper make_hyper(const dho2g_base_cfg& cfg, size_t t) {
+  BaseHyper hp;
+  hp.kind = cfg.kind;
+  hp.lr = (float)cfg.lr;
+  hp.wd = (float)cfg.weight_decay;
+  hp.b1 = (float)cfg.beta1;
+  hp.b2 = (float)cfg.beta2;
+  hp.omb1 = (float)(1.0 - cfg.beta1);
+  hp.omb2 = (float)(1.0 - cfg.beta2);
+  hp.eps = (float)cfg.eps;
+  hp.mom = (float)cfg.momentum;
+  hp.bc1 = (float)(1.0 - std::pow(cfg.beta1, (double)t));  // optimizer.cpp:54-55
+  hp.bc2 = (float)(1.0 - std::pow(cfg.beta2, (double)t));
+  return hp;
+}
 
 }  // namespace
 
@@ -445,22 +340,6 @@ void opt_alloc(dho2g_opt* o, dho2g_ctx* ctx, const dho2g_base_cfg& cfg, size_t r
   o->bad.alloc(1);
 }
 
-static BaseHyper make_hyper(const dho2g_base_cfg& cfg, size_t t) {
-  BaseHyper hp;
-  hp.kind = cfg.kind;
-  hp.lr = (float)cfg.lr;
-  hp.wd = (float)cfg.weight_decay;
-  hp.b1 = (float)cfg.beta1;
-  hp.b2 = (float)cfg.beta2;
-  hp.omb1 = (float)(1.0 - cfg.beta1);
-  hp.omb2 = (float)(1.0 - cfg.beta2);
-  hp.eps = (float)cfg.eps;
-  hp.mom = (float)cfg.momentum;
-  hp.bc1 = (float)(1.0 - std::pow(cfg.beta1, (double)t));  // optimizer.cpp:54-55
-  hp.bc2 = (float)(1.0 - std::pow(cfg.beta2, (double)t));
-  return hp;
-}
-
 void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   dho2g_ctx* ctx = o->ctx;
   cudaStream_t st = ctx->stream;
@@ -469,6 +348,10 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const size_t ldv = R ? ese->ldv : 0;
   const float* V = R ? ese->V.p : nullptr;
   const int world = ctx->world;
+  if (R > 0 && ldv < round_up(std::max<size_t>(rows, 1), kCh)) fail(DHO2G_DIMENSION, "deltas: V_hat not chunk padded");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(a.g) || !al16(a.pi) || !al16(a.w_a) || !al16(a.w_decay) || !al16(a.newton_out) || !al16(a.base_out))
+    fail(DHO2G_ARGUMENT, "split_update: vectors must be 16-byte aligned");
   const int gp = (int)std::max<size_t>(1, std::min<size_t>(cdiv(rows, kCh), (size_t)ctx->sm_count * 4));
   const int R1 = std::max(R, 1);
   o->part.ensure((size_t)gp * R1 + 8);
@@ -478,37 +361,8 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   o->all2.ensure((size_t)R1 * world);
   const double* all1 = world > 1 ? o->all1.p : o->rank1.p;
   const double* all2 = world > 1 ? o->all2.p : o->rank2.p;
-  const double rb = 4.0 * (double)rows;
+  const double rb = 4.0 * (double)rows;  // algorithmic bytes per row-vector pass
   const bool adam = o->cfg.kind >= 2;
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  const bool v4 = R <= kRT && al16(a.g) && al16(a.pi) && al16(a.w_a) && al16(a.w_decay) && al16(a.newton_out) &&
-                  al16(a.base_out) && al16(o->m.p) && al16(o->v.p) && al16(o->s.p) && (ldv % 4 == 0);
-  if (v4) {
-    const int gv = (int)std::max<size_t>(1, std::min<size_t>(cdiv(cdiv(rows, 4), kT), (size_t)ctx->sm_count * 4));
-    o->part.ensure((size_t)gv * R1 + 8);
-    if (R > 0) {
-      const int k1 = ctx->kt_begin();
-      upd_p1_v4<<<gv, kT, 0, st>>>(V, ldv, R, rows, a.g, a.pi, o->part.p, o->rank1.p, o->ticket.p);
-      DHO2G_LAUNCH();
-      ctx->kt_end(k1, "upd_p1", rb * (R + 1 + (a.pi ? 1 : 0)));
-      if (world > 1) ctx->allgather_f64(o->rank1.p, o->all1.p, R);
-    }
-    ++o->t;
-    const BaseHyper hp = make_hyper(o->cfg, o->t);
-    const int k2 = ctx->kt_begin();
-    upd_p2_v4<<<gv, kT, 0, st>>>(V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p,
-                                 o->v.p, o->s.p, o->part.p, o->rank2.p, o->ticket.p + 1, o->bad.p);
-    DHO2G_LAUNCH();
-    ctx->kt_end(k2, "upd_p2", rb * (R + 2 + (a.pi ? 1 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
-                                    (o->cfg.kind == 3 ? 1 : 0)));
-    if (R > 0 && world > 1) ctx->allgather_f64(o->rank2.p, o->all2.p, R);
-    const int k3 = ctx->kt_begin();
-    upd_p3_v4<<<gv, kT, 0, st>>>(V, ldv, R, rows, o->s.p, all1, all2, world, R ? ese->ev_dev.p : nullptr, a.alpha,
-                                 a.sigma, a.floor, a.w_a, a.newton_out, a.base_out);
-    DHO2G_LAUNCH();
-    ctx->kt_end(k3, "upd_p3", rb * (R + 1 + (a.w_a ? 2 : 0) + (a.newton_out ? 1 : 0) + (a.base_out ? 1 : 0)));
-    return;
-  }
   if (R > 0) {
     const int k1 = ctx->kt_begin();
     upd_p1_kernel<<<gp, kT, kCh * sizeof(float) + (size_t)kW * R * sizeof(double), st>>>(V, ldv, R, rows, a.g, a.pi,
@@ -522,13 +376,13 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const BaseHyper hp = make_hyper(o->cfg, o->t);
   const int k2 = ctx->kt_begin();
   upd_p2_kernel<<<gp, kT, kCh * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double), st>>>(
-      V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p, o->v.p, o->s.p, o->part.p, o->rank2.p,
-      o->ticket.p + 1, o->bad.p);
+      V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p, o->v.p, o->s.p, o->part.p,
+      o->rank2.p, o->ticket.p + 1, o->bad.p);
   DHO2G_LAUNCH();
   ctx->kt_end(k2, "upd_p2", rb * (R + 2 + (a.pi ? 1 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
                                   (o->cfg.kind == 3 ? 1 : 0)));
   if (R > 0 && world > 1) ctx->allgather_f64(o->rank2.p, o->all2.p, R);
-  const int g3 = (int)std::max<size_t>(1, std::min<size_t>(cdiv(rows, kT), (size_t)ctx->sm_count * 8));
+  const int g3 = (int)std::max<size_t>(1, std::min<size_t>(cdiv(cdiv(rows, 4), kT), (size_t)ctx->sm_count * 4));
   const int k3 = ctx->kt_begin();
   upd_p3_kernel<<<g3, kT, (size_t)2 * R1 * sizeof(double), st>>>(V, ldv, R, rows, o->s.p, all1, all2, world,
                                                                   R ? ese->ev_dev.p : nullptr, a.alpha, a.sigma,
