@@ -290,9 +290,16 @@ def run_ours(args, rank, world, dist):
     peaks = load_peaks()
     value = args.steps / (ms / 1e3)
     # dominant kernel -> roofline
-    kern = {}
+    kern, phases = {}, {}
     for name, (kms, cnt, work) in kstats.items():
         if cnt == 0 or kms <= 0:
+            continue
+        if name.startswith("phase."):
+            phases[name[6:]] = {"ms_total": round(kms, 3), "count": int(cnt), "share_of_step": round(kms / ms, 4)}
+            continue
+        if name in ("tile_epilogue", "extract_ese"):
+            kern[name] = {"ms_total": round(kms, 3), "launches": int(cnt), "avg_us": round(kms / cnt * 1e3, 2),
+                          "share_of_step": round(kms / ms, 4)}
             continue
         is_gemm = name.startswith("gemm3")
         per = kms / cnt
@@ -301,7 +308,8 @@ def run_ours(args, rank, world, dist):
         kern[name] = {"ms_total": round(kms, 3), "launches": int(cnt), "avg_us": round(per * 1e3, 2),
                       "achieved": round(ach, 2), "unit": "TFLOP/s" if is_gemm else "GB/s",
                       "frac": round(ach / peak, 4), "share_of_step": round(kms / ms, 4)}
-    dom = max(kern, key=lambda k: kern[k]["ms_total"]) if kern else None
+    cands = [k for k in kern if "achieved" in kern[k]]
+    dom = max(cands, key=lambda k: kern[k]["ms_total"]) if cands else None
     roof = None
     if dom:
         k = kern[dom]
@@ -320,6 +328,7 @@ def run_ours(args, rank, world, dist):
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "kernels": kern,
+            "phases": phases,
             "useful_tflops_per_step": (grad_flops(c["sizes"], c["b"] * c["workers"]) +
                                        hvp_flops(c["sizes"], c["curv"]) * (c["m"] or 40) / (c["P"] * rounds)) / 1e12}
     if world == 1 and not args.no_cpu_baseline:

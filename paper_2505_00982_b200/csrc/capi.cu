@@ -128,6 +128,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     check_ctx(ctx);
     const std::string k = key ? key : "";
     if (k == "gemm") ctx->gemm_backend = (int)value;
+    else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
     else if (k == "ktimers") {
       ctx->kt_flush();
@@ -780,7 +781,7 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
     DHO2G_LAUNCH();
     const int saved = ctx->gemm_backend;
     ctx->gemm_backend = backend;
-    gemm3(ctx, M, N, K, ah.p, al.p, ld, bh.p, bl.p, ld, c.p, N, 1.0f);
+    gemm3_store(ctx, M, N, K, ah.p, al.p, ld, bh.p, bl.p, ld, c.p, N, 1.0f);
     ctx->gemm_backend = saved;
     DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
     DHO2G_CUDA(cudaMemcpy(Cout, c.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));

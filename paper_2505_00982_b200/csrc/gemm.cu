@@ -1,19 +1,129 @@
 // Split-BF16x3 GEMMs for the MLP contractions (HVP forward/R-forward, backward/R-backward,
 // weight-gradient accumulation; SURVEY.md §2 kernel table):
 //
-//     C[M x N] = alpha * (Ah*Bh^T + Ah*Bl^T + Al*Bh^T),   A: M x K, B: N x K, both K-major.
+//     acc[M x N] = Ah*Bh^T + Ah*Bl^T + Al*Bh^T,   A: M x K, B: N x K, both K-major (bf16 hi/lo)
 //
-// gemm3_tc   : sm_100a tcgen05.mma (kind::f16, BF16 in, FP32 accumulate in TMEM), operands
-//              staged by TMA (SWIZZLE_128B) through a multi-stage mbarrier pipeline; one
-//              elected thread issues MMAs, 4 epilogue warps drain TMEM with tcgen05.ld.
-// gemm3_simt : CUDA-core reference kernel with identical split arithmetic (fp32 FMA); used as
-//              the in-device cross-check of the tensor-core path and selectable via
-//              dho2g_ctx_set_option("gemm", 1).
+// followed by a fused epilogue (Epi, internal.h): plain fp32 store (with the bias-column redirect
+// used by the weight-gradient GEMMs) or the MLP layer epilogues — bias + tanh/relu (+ R-term),
+// back-propagated delta (+ R-delta) — writing fp32 activations and the next GEMMs' bf16 hi/lo
+// operands in both row-major and transposed layouts.
+//
+// gemm3_tc   : sm_100a persistent kernel. One CTA per SM walks a static work list of
+//              (split, tile) units; a TMA producer warp streams A/B (hi, lo) tiles through a
+//              3-stage mbarrier ring (SWIZZLE_128B); one elected thread issues tcgen05.mma
+//              (kind::f16, M=128, N=128, FP32 accumulate) into one of two TMEM accumulators;
+//              4 epilogue warps drain the other accumulator with tcgen05.ld (epilogue of unit
+//              i overlaps the MMAs of unit i+1). Small-M GEMMs (the HVP at B=1024) are split
+//              along K; the split partials are combined in a fixed order through a global
+//              workspace + release/acquire flags, so results are deterministic.
+// gemm3_simt : CUDA-core reference kernel with identical split arithmetic (fp32 FMA) + the same
+//              epilogue device function, selectable via dho2g_ctx_set_option("gemm", 1).
 #include <cudaTypedefs.h>
 
 #include "internal.h"
 
 namespace dho2g {
+
+// =============================================================================== epilogue
+__device__ __forceinline__ float act_prime(bool relu, float a) { return relu ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a; }
+
+// Applies the epilogue to 16 consecutive columns [col0, col0+16) of one output row.
+__device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16]) {
+  if (e.mode == EPI_STORE) {
+    if (row >= e.M) return;
+    float* crow = e.C + (size_t)row * e.ldc;
+    const bool fast = col0 + 16 <= e.N - (e.bias_out ? 1 : 0) && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0);
+    if (fast) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(crow + col0 + j) =
+            make_float4(e.alpha * acc[j], e.alpha * acc[j + 1], e.alpha * acc[j + 2], e.alpha * acc[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = col0 + j;
+        if (col >= e.N) break;
+        const float v = e.alpha * acc[j];
+        if (e.bias_out && col == e.N - 1) e.bias_out[row] = v;
+        else crow[col] = v;
+      }
+    }
+    return;
+  }
+  const bool live = row < e.M;
+  const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
+  float x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = col0 + j;
+    float v = 0.f;
+    if (live && col < e.N) {
+      const size_t ei = (size_t)row * e.N + col;
+      if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
+        // oracle.cpp:548-563: a = act(z), z = W a + b ; ra = act'(a) (V a + W ra + v_b)
+        if (e.do0) {
+          const float z = acc[j] + e.bias[col];
+          v = e.mode == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
+          e.f0[ei] = v;
+        } else {
+          const float rz = acc[j] + vsc * e.vbias[col];
+          v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, e.a_in[ei]) * rz;
+          e.f1[ei] = v;
+        }
+      } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
+        const float a = e.a_in[ei];
+        const float ap = act_prime(e.relu, a);
+        if (e.do0) {
+          v = acc[j] * ap;
+          e.f0[ei] = v;
+          e.u_out[ei] = acc[j];
+        } else {
+          const float rap = (!e.relu && ap != 0.f) ? -2.f * a * e.ra_in[ei] : 0.f;
+          v = acc[j] * ap + e.u_in[ei] * rap;
+          e.f1[ei] = v;
+        }
+      }
+    }
+    x[j] = v;
+  }
+  if (live && e.Rh) {  // row-major (hi, lo) pair, half hR
+    const size_t base = (size_t)row * (2 * e.P) + (size_t)e.hR * e.P + col0;
+    if (col0 + 16 <= e.N) {
+      __align__(16) bf16 h[16], l[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) split_bf16(x[j], h[j], l[j]);
+      *reinterpret_cast<uint4*>(e.Rh + base) = *reinterpret_cast<const uint4*>(h);
+      *reinterpret_cast<uint4*>(e.Rh + base + 8) = *reinterpret_cast<const uint4*>(h + 8);
+      *reinterpret_cast<uint4*>(e.Rl + base) = *reinterpret_cast<const uint4*>(l);
+      *reinterpret_cast<uint4*>(e.Rl + base + 8) = *reinterpret_cast<const uint4*>(l + 8);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (col0 + j < e.N) split_bf16(x[j], e.Rh[base + j], e.Rl[base + j]);
+    }
+  }
+  if (e.Th && row < e.Bp) {  // transposed (hi, lo) pair, half hT; pad rows [M, Bp) get zeros
+    const size_t base = (size_t)e.hT * e.Bp + row;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int col = col0 + j;
+      if (col < e.N) split_bf16(x[j], e.Th[(size_t)col * e.ldT + base], e.Tl[(size_t)col * e.ldT + base]);
+    }
+  }
+}
+
+namespace {
+// standalone epilogue over an fp32 accumulator matrix (CUDA-core backend)
+__global__ void epi_kernel(Epi e, const float* __restrict__ acc, int ldacc, int rows_pad) {
+  const int row = blockIdx.y * blockDim.y + threadIdx.y;
+  const int col0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
+  if (row >= rows_pad || col0 >= e.N) return;
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = (row < e.M && col0 + j < e.N) ? acc[(size_t)row * ldacc + col0 + j] : 0.f;
+  epi_apply16(e, row, col0, v);
+}
+}  // namespace
 
 // =============================================================================== CUDA-core path
 namespace {
@@ -22,7 +132,7 @@ constexpr int ST_BM = 64, ST_BN = 64, ST_BK = 16;
 __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, const bf16* __restrict__ Ahi,
                                                          const bf16* __restrict__ Alo, int lda,
                                                          const bf16* __restrict__ Bhi, const bf16* __restrict__ Blo,
-                                                         int ldb, float* __restrict__ C, int ldc, float alpha) {
+                                                         int ldb, float* __restrict__ C, int ldc) {
   __shared__ float sAh[ST_BK][ST_BM + 4], sAl[ST_BK][ST_BM + 4], sBh[ST_BK][ST_BN + 4], sBl[ST_BK][ST_BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * ST_BM, n0 = blockIdx.x * ST_BN;
@@ -76,16 +186,23 @@ __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, co
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int gn = n0 + tx * 4 + j;
-      if (gn < N) C[(size_t)gm * ldc + gn] = alpha * acc[i][j];
+      if (gn < N) C[(size_t)gm * ldc + gn] = acc[i][j];
     }
   }
 }
 }  // namespace
 
-void gemm3_simt(cudaStream_t s, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-                const bf16* Blo, int ldb, float* C, int ldc, float alpha) {
+void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+                const bf16* Blo, int ldb, const Epi& e) {
+  ctx->simt_ws.ensure((size_t)M * N + 16);
+  float* acc = ctx->simt_ws.p;
   dim3 grid(cdiv(N, ST_BN), cdiv(M, ST_BM));
-  gemm3_simt_kernel<<<grid, 256, 0, s>>>(M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, C, ldc, alpha);
+  gemm3_simt_kernel<<<grid, 256, 0, ctx->stream>>>(M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, acc, N);
+  DHO2G_LAUNCH();
+  const int rows_pad = e.mode == EPI_STORE ? M : std::max(M, e.Bp);
+  dim3 eb(8, 16);
+  dim3 eg(cdiv(cdiv(N, 16), 8), cdiv(rows_pad, 16));
+  epi_kernel<<<eg, eb, 0, ctx->stream>>>(e, acc, N, rows_pad);
   DHO2G_LAUNCH();
 }
 
@@ -93,8 +210,19 @@ void gemm3_simt(cudaStream_t s, int M, int N, int K, const bf16* Ahi, const bf16
 namespace tc {
 
 constexpr int BM = 128;  // UMMA_M (cta_group::1): TMEM lane i <-> output row i
+constexpr int BN = 128;  // UMMA_N
 constexpr int BK = 64;   // one 128-byte swizzle row of bf16
 constexpr int UK = 16;   // K per tcgen05.mma kind::f16
+constexpr int STAGES = 3;
+constexpr int ACC = 2;   // TMEM accumulator buffers
+constexpr uint32_t A_BYTES = BM * BK * 2;
+constexpr uint32_t B_BYTES = BN * BK * 2;
+constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t TMEM_COLS = ACC * BN;
+// instruction descriptor, kind::f16: D=F32 [4,6), A=BF16 [7,10), B=BF16 [10,13), K-major both,
+// N>>3 [17,23), M>>4 [24,29)
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -104,6 +232,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
@@ -139,55 +270,64 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN, int STAGES>
-struct Cfg {
-  static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = BN * BK * 2;
-  static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
-  // instruction descriptor, kind::f16: D=F32 [4,6), A=BF16 [7,10), B=BF16 [10,13), K-major both,
-  // N>>3 [17,23), M>>4 [24,29)
-  static constexpr uint32_t IDESC =
-      (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+struct Sched {
+  int mt, nt, tiles, splits, units, nkb;  // nkb: k-blocks total
+  __device__ __forceinline__ void unit(int u, int& m0, int& n0, int& split, int& tile, int& kb0, int& kb1) const {
+    split = u / tiles;
+    tile = u - split * tiles;
+    m0 = (tile / nt) * BM;  // row-major tile order: consecutive CTAs share the A rows
+    n0 = (tile % nt) * BN;
+    kb0 = (int)((long long)nkb * split / splits);
+    kb1 = (int)((long long)nkb * (split + 1) / splits);
+  }
 };
 
-template <int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     gemm3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
-                    float* __restrict__ C, int ldc, int M, int N, int K, float alpha) {
-  using CF = Cfg<BN, STAGES>;
+                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Sched sc,
+                    const __grid_constant__ Epi e, float* __restrict__ ws, unsigned* __restrict__ flags,
+                    unsigned epoch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* tfull = empty + STAGES;  // [ACC]
+  uint64_t* tempty = tfull + ACC;    // [ACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nk = (K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -195,14 +335,20 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+#pragma unroll
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAl)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBl)) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(CF::TMEM_COLS));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   fence_before();
@@ -211,64 +357,100 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* st = smem + s * CF::STAGE_BYTES;
-      mbar_expect_tx(&full[s], CF::STAGE_BYTES);
-      tma_load_2d(st, &mAh, kb * BK, m0, &full[s]);
-      tma_load_2d(st + CF::A_BYTES, &mAl, kb * BK, m0, &full[s]);
-      tma_load_2d(st + 2 * CF::A_BYTES, &mBh, kb * BK, n0, &full[s]);
-      tma_load_2d(st + 2 * CF::A_BYTES + CF::B_BYTES, &mBl, kb * BK, n0, &full[s]);
+    // ---------------- TMA producer: continuous ring over all k-blocks of this CTA's units
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < sc.units; u += gridDim.x) {
+      int m0, n0, split, tile, kb0, kb1;
+      sc.unit(u, m0, n0, split, tile, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(st, &mAh, kb * BK, m0, &full[s]);
+        tma_load_2d(st + A_BYTES, &mAl, kb * BK, m0, &full[s]);
+        tma_load_2d(st + 2 * A_BYTES, &mBh, kb * BK, n0, &full[s]);
+        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mBl, kb * BK, n0, &full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
+    // ---------------- MMA issuer (single thread), accumulator double-buffered in TMEM
+    uint32_t it = 0, uc = 0;
+    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
+      int m0, n0, split, tile, kb0, kb1;
+      sc.unit(u, m0, n0, split, tile, kb0, kb1);
+      const uint32_t ab = uc % ACC;
+      mbar_wait(&tempty[ab], ((uc / ACC) & 1) ^ 1);  // epilogue drained this buffer
       fence_after();
-      const uint32_t base = smem_u32(smem + s * CF::STAGE_BYTES);
+      const uint32_t acc_addr = tmem + ab * BN;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        fence_after();
+        const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < BK / UK; ++kk) {
-        const uint64_t dAh = sw128_desc(base + kk * 32);
-        const uint64_t dAl = sw128_desc(base + CF::A_BYTES + kk * 32);
-        const uint64_t dBh = sw128_desc(base + 2 * CF::A_BYTES + kk * 32);
-        const uint64_t dBl = sw128_desc(base + 2 * CF::A_BYTES + CF::B_BYTES + kk * 32);
-        mma_bf16(tmem, dAh, dBh, CF::IDESC, (kb | kk) != 0);
-        mma_bf16(tmem, dAh, dBl, CF::IDESC, 1u);
-        mma_bf16(tmem, dAl, dBh, CF::IDESC, 1u);
-      }
-      mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
-    }
-    mma_commit(accf);  // accumulator complete
-  } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> global (row = TMEM lane)
-    mbar_wait(accf, 0);
-    fence_after();
-    const int ew = warp - 4;
-    const int row = m0 + ew * 32 + lane;
-    float* crow = C + (size_t)row * ldc;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)c0, r);
-      if (row < M) {
-        const int col = n0 + c0;
-        if (col + 16 <= N && ((reinterpret_cast<uintptr_t>(crow + col) & 15) == 0)) {
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            float4 v = make_float4(alpha * __uint_as_float(r[j]), alpha * __uint_as_float(r[j + 1]),
-                                   alpha * __uint_as_float(r[j + 2]), alpha * __uint_as_float(r[j + 3]));
-            *reinterpret_cast<float4*>(crow + col + j) = v;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (col + j < N) crow[col + j] = alpha * __uint_as_float(r[j]);
+        for (int kk = 0; kk < BK / UK; ++kk) {
+          const uint64_t dAh = sw128_desc(base + kk * 32);
+          const uint64_t dAl = sw128_desc(base + A_BYTES + kk * 32);
+          const uint64_t dBh = sw128_desc(base + 2 * A_BYTES + kk * 32);
+          const uint64_t dBl = sw128_desc(base + 2 * A_BYTES + B_BYTES + kk * 32);
+          mma_bf16(acc_addr, dAh, dBh, (kb > kb0 || kk > 0) ? 1u : 0u);
+          mma_bf16(acc_addr, dAh, dBl, 1u);
+          mma_bf16(acc_addr, dAl, dBh, 1u);
         }
+        mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+      }
+      mma_commit(&tfull[ab]);  // accumulator ready for the epilogue
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps: TMEM -> registers -> (split-K combine) -> fused epilogue
+    const int ew = warp - 4;
+    uint32_t uc = 0;
+    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
+      int m0, n0, split, tile, kb0, kb1;
+      sc.unit(u, m0, n0, split, tile, kb0, kb1);
+      const uint32_t ab = uc % ACC;
+      mbar_wait(&tfull[ab], (uc / ACC) & 1);
+      fence_after();
+      const int r_local = ew * 32 + lane;
+      const int row = m0 + r_local;
+      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
+      float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)r_local * BN : nullptr;
+      const bool last = split == sc.splits - 1;
+      if (split > 0) {  // wait for the previous split of this tile (fixed combine order)
+        if (threadIdx.x == 128) {
+          const unsigned want = epoch * 16u + (unsigned)split;
+          while (ld_acquire(flags + tile) != want) __nanosleep(64);
+        }
+        epi_bar();
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + (uint32_t)c0, v);
+        if (split > 0) {
+          const float4* p = reinterpret_cast<const float4*>(wtile + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 t = __ldcg(p + q);
+            v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
+          }
+        }
+        if (last) {
+          epi_apply16(e, row, n0 + c0, v);
+        } else {
+          float4* p = reinterpret_cast<float4*>(wtile + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) __stcg(p + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (!last) {  // publish this split's partial
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) st_release(flags + tile, epoch * 16u + (unsigned)(split + 1));
       }
     }
   }
@@ -276,7 +458,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -296,52 +478,93 @@ CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t 
   return m;
 }
 
-template <int BN, int STAGES>
-void launch(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-            const bf16* Blo, int ldb, float* C, int ldc, float alpha) {
-  using CF = Cfg<BN, STAGES>;
+// split-K factor that best fills the persistent grid (work quantization), >= 8 k-blocks per split
+int pick_splits(int tiles, int nkb, int sms) {
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 4; ++s) {
+    if (s > 1 && nkb / s < 8) break;
+    const int units = tiles * s;
+    const int waves = (units + sms - 1) / sms;
+    const double eff = (double)units / ((double)waves * sms) * (1.0 - 0.02 * (s - 1));  // combine cost
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+}  // namespace tc
+
+void gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+              const bf16* Blo, int ldb, const Epi& e) {
+  using namespace tc;
+  if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(Ahi) & 15) || (reinterpret_cast<uintptr_t>(Alo) & 15) ||
+      (reinterpret_cast<uintptr_t>(Bhi) & 15) || (reinterpret_cast<uintptr_t>(Blo) & 15))
+    fail(DHO2G_ARGUMENT, "gemm3_tc: operands must be 16-byte aligned with ld % 8 == 0");
   static bool attr_set = false;
   if (!attr_set) {
-    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)CF::SMEM));
+    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
+  }
+  Sched sc;
+  sc.mt = (int)cdiv(M, BM);
+  sc.nt = (int)cdiv(N, BN);
+  sc.tiles = sc.mt * sc.nt;
+  sc.nkb = (int)cdiv(K, BK);
+  sc.splits = ctx->gemm_splits > 0 ? std::min(ctx->gemm_splits, std::max(1, sc.nkb))
+                                   : pick_splits(sc.tiles, sc.nkb, ctx->sm_count);
+  sc.units = sc.tiles * sc.splits;
+  float* ws = nullptr;
+  unsigned* flags = nullptr;
+  unsigned epoch = 0;
+  if (sc.splits > 1) {
+    ctx->gemm_ws.ensure((size_t)sc.tiles * BM * BN);
+    ctx->gemm_flags.ensure((size_t)sc.tiles);
+    ws = ctx->gemm_ws.p;
+    flags = ctx->gemm_flags.p;
+    epoch = ++ctx->gemm_epoch;
+    if (epoch >= (1u << 27)) {  // flag encoding epoch * 16 + split: recycle
+      DHO2G_CUDA(cudaMemsetAsync(flags, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
+      ctx->gemm_epoch = epoch = 1;
+    }
   }
   const CUtensorMap mAh = make_map(ctx->encode_fn, Ahi, K, M, lda, BM);
   const CUtensorMap mAl = make_map(ctx->encode_fn, Alo, K, M, lda, BM);
   const CUtensorMap mBh = make_map(ctx->encode_fn, Bhi, K, N, ldb, BN);
   const CUtensorMap mBl = make_map(ctx->encode_fn, Blo, K, N, ldb, BN);
-  dim3 grid(cdiv(N, BN), cdiv(M, BM));
-  gemm3_tc_kernel<BN, STAGES><<<grid, 256, CF::SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, C, ldc, M, N, K, alpha);
+  const int grid = std::min(sc.units, ctx->sm_count);
+  gemm3_tc_kernel<<<grid, 256, SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, sc, e, ws, flags, epoch);
   DHO2G_LAUNCH();
 }
 
-}  // namespace tc
-
-bool gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-              const bf16* Blo, int ldb, float* C, int ldc, float alpha) {
-  if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(Ahi) & 15) || (reinterpret_cast<uintptr_t>(Alo) & 15) ||
-      (reinterpret_cast<uintptr_t>(Bhi) & 15) || (reinterpret_cast<uintptr_t>(Blo) & 15))
-    fail(DHO2G_ARGUMENT, "gemm3_tc: operands must be 16-byte aligned with ld % 8 == 0");
-  tc::launch<128, 3>(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, C, ldc, alpha);
-  return true;
-}
-
 void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-           const bf16* Blo, int ldb, float* C, int ldc, float alpha) {
+           const bf16* Blo, int ldb, const Epi& e) {
   if (M <= 0 || N <= 0) return;
-  if (K <= 0) {
-    DHO2G_CUDA(cudaMemset2DAsync(C, (size_t)ldc * sizeof(float), 0, (size_t)N * sizeof(float), M, ctx->stream));
-    return;
-  }
+  if (K <= 0) fail(DHO2G_ARGUMENT, "gemm3: empty reduction dimension");
   ctx->bump("gemm_calls", 1);
   ctx->bump("gemm_flops_issued", 3.0 * 2.0 * double(M) * double(N) * double(K));
   const int slot = ctx->kt_begin();
   if (ctx->gemm_backend == 1)
-    gemm3_simt(ctx->stream, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, C, ldc, alpha);
+    gemm3_simt(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
   else
-    gemm3_tc(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, C, ldc, alpha);
+    gemm3_tc(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
   ctx->kt_end(slot, ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05", 2.0 * double(M) * double(N) * double(K));
+}
+
+void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+                 const bf16* Blo, int ldb, float* C, int ldc, float alpha, float* bias_out) {
+  Epi e{};
+  e.mode = EPI_STORE;
+  e.M = M;
+  e.N = N;
+  e.C = C;
+  e.ldc = ldc;
+  e.alpha = alpha;
+  e.bias_out = bias_out;
+  gemm3(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
 }
 
 }  // namespace dho2g

@@ -37,6 +37,10 @@ struct dho2g_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   int gemm_backend = 0;  // 0 tcgen05, 1 CUDA-core reference kernel
+  int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs
+  dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
+  dho2g::DevBuf<unsigned> gemm_flags;
+  unsigned gemm_epoch = 0;
   int use_graphs = 0;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -103,6 +107,7 @@ struct dho2g_mlp {
   const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)
   const void* input_owner = nullptr;   // operator whose curvature batch is packed at level 0
   const float* prepared = nullptr;     // w whose v-independent HVP quantities are cached
+  size_t ones_B = 0;                   // batch size the ones rows of ART were written for
 
   void ensure_batch(size_t B);
 };
@@ -125,13 +130,46 @@ void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, 
 
 void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);  // acc2 = {sum loss, sum correct} of last batch
 
-// GEMM: C[M x N] = alpha * A[M x K] * B[N x K]^T, split-BF16x3 (hi*hi + hi*lo + lo*hi), fp32 out.
+// GEMM epilogues (gemm.cu). One accumulator element (row, col) of a GEMM tile is turned into:
+//  EPI_STORE   C[row*ldc + col] = alpha*acc (column N-1 -> bias_out[row] when bias_out != null)
+//  EPI_FWD     hidden layer: do0: a = act(acc + bias) ; do1: ra = act'(a_in) (acc + vscale*vbias)
+//  EPI_FWD_OUT output layer: do0: z = acc + bias ; do1: rz = acc + vscale*vbias   (fp32 only)
+//  EPI_BWD     do0: d = acc act'(a_in), u_out = acc ; do1: rd = acc act'(a_in) + u_in (-2 a_in ra_in)
+// writing the fp32 value (f0 / f1, B x N) and its bf16 (hi, lo) split into the row-major pair
+// buffer (R, half hR) and the transposed pair buffer (T, half hT; rows [M, Bp) get zeros).
+enum EpiMode { EPI_STORE = 0, EPI_FWD = 1, EPI_FWD_OUT = 2, EPI_BWD = 3 };
+struct Epi {
+  int mode, M, N;
+  float alpha;
+  float* C;
+  int ldc;
+  float* bias_out;
+  int do0, do1, relu;
+  const float* bias;
+  const float* vbias;
+  const float* vscale;
+  const float* a_in;
+  const float* ra_in;
+  const float* u_in;
+  float* f0;
+  float* f1;
+  float* u_out;
+  bf16* Rh;
+  bf16* Rl;
+  int P, hR;
+  bf16* Th;
+  bf16* Tl;
+  int ldT, Bp, hT;
+};
+// acc = A[M x K] B[N x K]^T in split-BF16x3 (hi*hi + hi*lo + lo*hi), then the epilogue.
 void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-           const bf16* Blo, int ldb, float* C, int ldc, float alpha);
-void gemm3_simt(cudaStream_t s, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-                const bf16* Blo, int ldb, float* C, int ldc, float alpha);
-bool gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-              const bf16* Blo, int ldb, float* C, int ldc, float alpha);
+           const bf16* Blo, int ldb, const Epi& e);
+void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+                 const bf16* Blo, int ldb, float* C, int ldc, float alpha, float* bias_out = nullptr);
+void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+                const bf16* Blo, int ldb, const Epi& e);
+void gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+              const bf16* Blo, int ldb, const Epi& e);
 
 // fp32 elementwise helpers (update.cu)
 void dev_copy_f64_to_f32(cudaStream_t s, const double* src, float* dst, size_t n);
@@ -184,6 +222,9 @@ struct dho2g_lanczos {
   dho2g::DevBuf<unsigned> ticket;
   dho2g::LzDev host{};          // copy after run
   dho2g_lanczos_opts opts{1, 1e-6, 1e-10};
+  dho2g::DevBuf<double> xZ, xev, xam, xamall, xpart;  // extract_ese scratch
+  dho2g::DevBuf<float> xU;
+  dho2g::DevBuf<int> xstatus;
   double ms = 0.0;
 };
 

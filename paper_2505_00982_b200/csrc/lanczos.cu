@@ -645,18 +645,24 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   if (k + l > (size_t)me) fail(DHO2G_ARGUMENT, "extract_ese_distributed: k+l exceeds the filled block");
   const int r = (int)(k + l);
   ese->r = r;
-  DevBuf<double> Z((size_t)me * me);
-  DevBuf<float> U((size_t)me * r);
-  ese->ev_dev.alloc(r);
-  DevBuf<double> evall(me);
-  DevBuf<int> status(1);
+  // scratch persists in the Lanczos state (no allocation, hence no implicit device sync, per refresh)
+  DevBuf<double>& Z = lz->xZ;
+  DevBuf<float>& U = lz->xU;
+  DevBuf<double>& evall = lz->xev;
+  DevBuf<int>& status = lz->xstatus;
+  Z.ensure((size_t)me * me);
+  U.ensure((size_t)me * r);
+  evall.ensure(me);
+  status.ensure(1);
+  ese->ev_dev.ensure(r);
   const size_t smem = (size_t)me * 4 * sizeof(double) + (size_t)me * sizeof(int);
   if (smem > 48 * 1024)
     DHO2G_CUDA(cudaFuncSetAttribute(tql2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int threads = (int)std::min<size_t>(1024, round_up((size_t)me, 32));
+  const int kx = ctx->kt_begin();
   tql2_kernel<<<1, threads, smem, st>>>(lz->st.p, me, (int)k, (int)l, Z.p, U.p, ese->ev_dev.p, evall.p, status.p);
   DHO2G_LAUNCH();
-  ese->V.alloc(ese->ldv * r);
+  ese->V.ensure(ese->ldv * r);  // padded rows stay zero (Ritz writes rows < rows only)
   for (int c0 = 0; c0 < r; c0 += RC) {
     const size_t sm = (size_t)me * RC * sizeof(float);
     if (sm > 48 * 1024)
@@ -665,16 +671,21 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
                                                                   lz->rows);
     DHO2G_LAUNCH();
   }
-  DevBuf<double> am((size_t)3 * r);
-  DevBuf<double> amall((size_t)3 * r * ctx->world);
+  DevBuf<double>& am = lz->xam;
+  DevBuf<double>& amall = lz->xamall;
+  am.ensure((size_t)3 * r);
+  amall.ensure((size_t)3 * r * ctx->world);
   {
     const int nblk = (int)std::max<size_t>(1, std::min<size_t>(cdiv(lz->rows, 4 * kArgThreads), 256));
     const size_t seg = cdiv(std::max<size_t>(lz->rows, 1), (size_t)nblk);
-    DevBuf<double> part((size_t)3 * r * nblk);
+    DevBuf<double>& part = lz->xpart;
+    part.ensure((size_t)3 * r * nblk);
     col_argmax_kernel<<<dim3(nblk, r), kArgThreads, 0, st>>>(ese->V.p, ese->ldv, lz->rows, lz->begin, seg, part.p);
     col_argmax_final_kernel<<<r, 32, 0, st>>>(part.p, nblk, am.p);
     DHO2G_LAUNCH();
   }
+  // tql2 + Ritz (reads D[:, :m_eff], writes V_hat) + argmax (reads V_hat): algorithmic bytes
+  ctx->kt_end(kx, "extract_ese", 4.0 * (double)lz->rows * (double)(me + 2 * r));
   ctx->allgather_f64(am.p, amall.p, (size_t)3 * r);
   std::vector<double> h_am((size_t)3 * r * ctx->world);
   int h_status = 0;

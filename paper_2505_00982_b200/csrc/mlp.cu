@@ -30,7 +30,7 @@ void dho2g_mlp::ensure_batch(size_t B) {
     const size_t s = sizes[j], P = round_up(s, 8);
     if (j < Ls) {
       AR_hi[j].alloc(nB * 2 * P); AR_lo[j].alloc(nB * 2 * P);
-      ART_hi[j].alloc(s * 2 * nBp); ART_lo[j].alloc(s * 2 * nBp);
+      ART_hi[j].alloc((s + 1) * 2 * nBp); ART_lo[j].alloc((s + 1) * 2 * nBp);  // + ones row (bias grads)
     }
     if (j >= 1) {
       DR_hi[j].alloc(nB * 2 * P); DR_lo[j].alloc(nB * 2 * P);
@@ -47,6 +47,7 @@ void dho2g_mlp::ensure_batch(size_t B) {
   Bcap = nB;
   Bpcap = nBp;
   prepared = nullptr;
+  ones_B = 0;
 }
 
 namespace {
@@ -261,31 +262,18 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, in
   }
 }
 
+__global__ void ones_row_kernel(bf16* __restrict__ hi, bf16* __restrict__ lo, int len, int B) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  hi[i] = __float2bfloat16_rn(i < B ? 1.f : 0.f);
+  lo[i] = __float2bfloat16_rn(0.f);
+}
+
 // label gather
 __global__ void gather_labels_kernel(int B, const float* __restrict__ y, const int64_t* __restrict__ idx,
                                      float* __restrict__ out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) out[b] = y[idx ? idx[b] : b];
-}
-
-// bias gradient: out[o] = sum_b src[b, o] (fp64 accumulation, fixed order over fixed chunks)
-constexpr int kBiasChunks = 32;
-__global__ void bias_partial_kernel(int B, int O, const float* __restrict__ src, double* __restrict__ part) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= O) return;
-  const int c = blockIdx.y;
-  const int per = (B + kBiasChunks - 1) / kBiasChunks;
-  const int b0 = c * per, b1 = min(B, b0 + per);
-  double s = 0.0;
-  for (int b = b0; b < b1; ++b) s += src[(size_t)b * O + o];
-  part[(size_t)c * O + o] = s;
-}
-__global__ void bias_final_kernel(int O, const double* __restrict__ part, float* __restrict__ out) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= O) return;
-  double s = 0.0;
-  for (int c = 0; c < kBiasChunks; ++c) s += part[(size_t)c * O + o];
-  out[o] = (float)s;
 }
 
 // deterministic single-CTA sum of per-sample loss / correct into acc2[0], acc2[1] (+=)
@@ -345,11 +333,20 @@ void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* 
   a.Rh = m->AR_hi[0].p; a.Rl = m->AR_lo[0].p; a.Th = m->ART_hi[0].p; a.Tl = m->ART_lo[0].p;
   a.t0 = 0; a.t1 = -1;
   launch_tile<M_INPUT>(m->ctx, a);
+  if (m->ones_B != B) {  // ones row of every transposed activation buffer: [1 (B) 0 (Bp-B) | 0 (Bp)]
+    for (int j = 0; j < m->L; ++j)
+      ones_row_kernel<<<cdiv(2 * m->Bpcap, 256), 256, 0, st>>>(m->ART_hi[j].p + m->sizes[j] * 2 * m->Bpcap,
+                                                              m->ART_lo[j].p + m->sizes[j] * 2 * m->Bpcap,
+                                                              (int)(2 * m->Bpcap), (int)B);
+    DHO2G_LAUNCH();
+    m->ones_B = B;
+  }
   gather_labels_kernel<<<cdiv(B, 256), 256, 0, st>>>((int)B, y, idx, m->lab.p);
   DHO2G_LAUNCH();
 }
 
-// Forward pass. do0: plain activations (Z GEMM, act, pack a). do1: R-activations (RZ GEMM).
+// Forward pass. do0: plain activations (Z GEMM + fused bias/act epilogue). do1: R-activations
+// (RZ GEMM + fused R-epilogue over the cached activations).
 static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) {
   dho2g_ctx* ctx = m->ctx;
   const int Bp = (int)round_up(B, 8);
@@ -357,27 +354,32 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
     const LayerDesc& ld = m->layers[t];
     const bool last = t + 1 == m->L;
     const int lda = 2 * ld.Pin;
-    if (do0)  // Z = A W^T
-      gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
-            m->WV_lo[t].p + ld.Pin, lda, m->Z.p, ld.out, 1.0f);
-    if (do1) {  // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
-      const int K = t == 0 ? ld.in : 2 * ld.Pin;
-      gemm3(ctx, (int)B, ld.out, K, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p, m->WV_lo[t].p, lda, m->RZ.p,
-            ld.out, 1.0f);
-    }
-    TileArgs a{};
-    a.B = (int)B; a.s = ld.out; a.P = ld.Pout; a.Bp = Bp; a.ldT = (int)(2 * m->Bpcap);
-    a.do0 = do0; a.do1 = do1; a.relu = m->act == 1;
-    a.Zs = m->Z.p; a.RZs = m->RZ.p; a.bias = w + ld.b_off; a.vbias = do1 ? m->v_bias_ptr + ld.b_off : nullptr;
-    a.vscale = m->v_scale_ptr;
-    a.a_in = m->a32[t + 1].p;
-    a.o0 = m->a32[t + 1].p; a.o1 = m->ra32[t + 1].p;
-    if (last) {
-      launch_tile<M_FWD_OUT>(ctx, a);
-    } else {
-      a.Rh = m->AR_hi[t + 1].p; a.Rl = m->AR_lo[t + 1].p; a.Th = m->ART_hi[t + 1].p; a.Tl = m->ART_lo[t + 1].p;
-      a.t0 = 0; a.t1 = 1;
-      launch_tile<M_FWD>(ctx, a);
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool r = pass == 1;
+      if ((r && !do1) || (!r && !do0)) continue;
+      Epi e{};
+      e.mode = last ? EPI_FWD_OUT : EPI_FWD;
+      e.M = (int)B;
+      e.N = ld.out;
+      e.do0 = !r;
+      e.do1 = r;
+      e.relu = m->act == 1;
+      e.bias = w + ld.b_off;
+      e.vbias = r ? m->v_bias_ptr + ld.b_off : nullptr;
+      e.vscale = m->v_scale_ptr;
+      e.a_in = m->a32[t + 1].p;
+      e.f0 = m->a32[t + 1].p;
+      e.f1 = m->ra32[t + 1].p;
+      if (!last) {
+        e.Rh = m->AR_hi[t + 1].p; e.Rl = m->AR_lo[t + 1].p; e.P = ld.Pout; e.hR = r ? 1 : 0;
+        e.Th = m->ART_hi[t + 1].p; e.Tl = m->ART_lo[t + 1].p; e.ldT = (int)(2 * m->Bpcap); e.Bp = Bp; e.hT = r ? 1 : 0;
+      }
+      if (!r)  // Z = A W^T
+        gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
+              m->WV_lo[t].p + ld.Pin, lda, e);
+      else  // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
+        gemm3(ctx, (int)B, ld.out, t == 0 ? ld.in : 2 * ld.Pin, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p,
+              m->WV_lo[t].p, lda, e);
     }
   }
 }
@@ -400,18 +402,10 @@ static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool
   launch_tile<M_DPACK>(m->ctx, a);
 }
 
-static void bias_sum(dho2g_mlp* m, int B, int O, const float* src, float* out) {
-  m->red.ensure((size_t)kBiasChunks * m->smax);
-  cudaStream_t st = m->ctx->stream;
-  const int slot = m->ctx->kt_begin();
-  bias_partial_kernel<<<dim3(cdiv(O, 128), kBiasChunks), 128, 0, st>>>(B, O, src, m->red.p);
-  bias_final_kernel<<<cdiv(O, 128), 128, 0, st>>>(O, m->red.p, out);
-  DHO2G_LAUNCH();
-  m->ctx->kt_end(slot, "bias_sum", 4.0 * B * O);
-}
-
-// Backward pass. do0: deltas d (U GEMMs) and, if wgrad, the gradient blocks. do1: R-deltas (RU GEMMs)
-// and the Hessian blocks hvW into `out`.
+// Backward pass. do0: deltas d (U GEMMs + fused act' epilogue) and, if wgrad, the gradient blocks.
+// do1: R-deltas (RU GEMMs + fused R-epilogue) and the Hessian blocks into `out`. The weight-block
+// GEMMs take the bias column from the ones row appended to the transposed activations
+// (N = in + 1: column `in` = sum_b rd (or d), routed to out[b_off + o]).
 static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, bool wgrad) {
   dho2g_ctx* ctx = m->ctx;
   const int L = m->L;
@@ -420,34 +414,38 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   for (int t = L - 1; t >= 0; --t) {
     const LayerDesc& ld = m->layers[t];
     const int j = t + 1;
-    if (do1) {  // hvW = [RD^T | D^T] [A^T | RA^T]^T ; hv_b = sum_b rd (oracle.cpp:606-613)
-      const int K = t == 0 ? Bp : 2 * Bp;
-      gemm3(ctx, ld.out, ld.in, K, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p, m->ART_lo[t].p, ldT,
-            out + ld.w_off, ld.in, 1.0f);
-      bias_sum(m, (int)B, ld.out, m->rd32[j].p, out + ld.b_off);
-    } else if (wgrad) {  // gW = D^T A ; g_b = sum_b d (oracle.cpp:497-504)
-      gemm3(ctx, ld.out, ld.in, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p, m->ART_lo[t].p,
-            ldT, out + ld.w_off, ld.in, 1.0f);
-      bias_sum(m, (int)B, ld.out, m->d32[j].p, out + ld.b_off);
-    }
-    if (t > 0) {
-      const int lda = 2 * ld.Pout;
-      if (do0)  // U = D W
+    if (do1)  // hvW = [RD^T | D^T] [A^T | RA^T]^T ; hv_b = sum_b rd (oracle.cpp:606-613)
+      gemm3_store(ctx, ld.out, ld.in + 1, t == 0 ? Bp : 2 * Bp, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p,
+                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f, out + ld.b_off);
+    else if (wgrad)  // gW = D^T A ; g_b = sum_b d (oracle.cpp:497-504)
+      gemm3_store(ctx, ld.out, ld.in + 1, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p,
+                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f, out + ld.b_off);
+    if (t == 0) continue;
+    const int lda = 2 * ld.Pout;
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool r = pass == 1;
+      if ((r && !do1) || (!r && !do0)) continue;
+      Epi e{};
+      e.mode = EPI_BWD;
+      e.M = (int)B;
+      e.N = ld.in;
+      e.do0 = !r;
+      e.do1 = r;
+      e.relu = m->act == 1;
+      e.a_in = m->a32[t].p;
+      e.ra_in = m->ra32[t].p;
+      e.u_in = m->u32[t].p;
+      e.u_out = m->u32[t].p;
+      e.f0 = m->d32[t].p;
+      e.f1 = m->rd32[t].p;
+      e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Pin; e.hR = r ? 1 : 0;
+      e.Th = m->DRT_hi[t].p; e.Tl = m->DRT_lo[t].p; e.ldT = ldT; e.Bp = Bp; e.hT = r ? 0 : 1;  // [rd^T | d^T]
+      if (!r)  // U = D W
         gemm3(ctx, (int)B, ld.in, ld.out, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p + ld.Pout,
-              m->WVt_lo[t].p + ld.Pout, lda, m->Z.p, ld.in, 1.0f);
-      if (do1)  // RU = [D | RD] [V^T | W^T]^T
-        gemm3(ctx, (int)B, ld.in, 2 * ld.Pout, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p, m->WVt_lo[t].p,
-              lda, m->RZ.p, ld.in, 1.0f);
-      TileArgs a{};
-      const int s = (int)m->sizes[t];
-      a.B = (int)B; a.s = s; a.P = (int)round_up(s, 8); a.Bp = Bp; a.ldT = ldT;
-      a.do0 = do0; a.do1 = do1; a.relu = m->act == 1;
-      a.Rh = m->DR_hi[t].p; a.Rl = m->DR_lo[t].p; a.Th = m->DRT_hi[t].p; a.Tl = m->DRT_lo[t].p;
-      a.t0 = 1; a.t1 = 0;
-      a.Zs = m->Z.p; a.RZs = m->RZ.p; a.a_in = m->a32[t].p; a.ra_in = m->ra32[t].p;
-      a.u_in = m->u32[t].p; a.u_out = do0 ? m->u32[t].p : nullptr;
-      a.o0 = m->d32[t].p; a.o1 = m->rd32[t].p;
-      launch_tile<M_BWD>(ctx, a);
+              m->WVt_lo[t].p + ld.Pout, lda, e);
+      else  // RU = [D | RD] [V^T | W^T]^T
+        gemm3(ctx, (int)B, ld.in, 2 * ld.Pout, m->DR_hi[j].p, m->DR_lo[j].p, lda, m->WVt_hi[t].p, m->WVt_lo[t].p, lda,
+              e);
     }
   }
 }

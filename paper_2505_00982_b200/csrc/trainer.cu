@@ -108,6 +108,7 @@ struct dho2g_trainer {
     }
     B_local = idx.size();
     const double scale = (1.0 / (double)b) * (1.0 / (double)C);
+    const int ph = ctx->kt_begin();
     if (B_local > 0) {
       const int64_t* di = upload_indices(idx);
       mlp_load_weights(mlp, w_a_full.p);
@@ -118,11 +119,13 @@ struct dho2g_trainer {
       DHO2G_CUDA(cudaMemsetAsync(g_full.p, 0, n * sizeof(float), ctx->stream));
     }
     if (ctx->world > 1) ctx->reduce_scatter_f32(g_full.p, g_shard, base);
+    ctx->kt_end(ph, "phase.grad", 0.0);
   }
 
   // refresh_ese (trainer.cpp:105-135)
   void refresh() {
     const auto t0 = std::chrono::steady_clock::now();
+    const int ph = ctx->kt_begin();
     const size_t want = std::min<size_t>(cfg.curvature_batch, N);
     std::vector<uint64_t> all(N);
     dho2g_curvature_indices(N, want, cfg.seed, refreshes, all.data());
@@ -144,6 +147,7 @@ struct dho2g_trainer {
     const size_t leff = std::min(cfg.l, iters - keff);
     extract_ese_into(ctx, &lz, keff, leff, &ese);
     have_ese = ese.r > 0;
+    ctx->kt_end(ph, "phase.refresh", 0.0);
     last_eigvals = ese.eigvals;
     safeguards += (size_t)lz.host.safeguards;
     ++refreshes;
@@ -164,8 +168,10 @@ struct dho2g_trainer {
     a.alpha = cfg.alpha;
     a.sigma = sigma_eff;
     a.floor = cfg.eigval_floor;
+    const int ph = ctx->kt_begin();
     split_update(&opt, have_ese ? &ese : nullptr, a);
     allgather_params();
+    ctx->kt_end(ph, "phase.update", 0.0);
   }
 
   // epoch_end (trainer.cpp:150-172)

@@ -33,6 +33,24 @@ def test_gemm3_tcgen05_vs_exact(ctx, M, N, K):
     assert np.max(np.abs(tc - st) / scale) < 5e-6
 
 
+@pytest.mark.parametrize("splits", [1, 2, 3, 4])
+def test_gemm3_split_k_deterministic(ctx, splits):
+    """Persistent tcgen05 GEMM with split-K: fixed-order combine -> bitwise repeatable, exact to 2e-5."""
+    rng = np.random.default_rng(splits)
+    A = rng.standard_normal((1024, 2048)).astype(np.float32)
+    B = rng.standard_normal((640, 2048)).astype(np.float32)
+    exact = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
+    ctx.set_option("gemm_splits", splits)
+    try:
+        c1 = run_gemm(ctx, A, B, 0)
+        c2 = run_gemm(ctx, A, B, 0)
+    finally:
+        ctx.set_option("gemm_splits", 0)
+    assert (c1 == c2).all()
+    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
+
+
 # ------------------------------------------------------------------------------------ MLP oracle
 CASES = [([20, 16, 12, 5], 37, "tanh", "softmax_ce", 5), ([20, 16, 12, 5], 37, "relu", "softmax_ce", 5),
          ([20, 16, 12, 5], 37, "tanh", "mse", 5), ([13, 24, 1], 19, "tanh", "mse", 0),
