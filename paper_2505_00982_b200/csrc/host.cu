@@ -183,15 +183,19 @@ int dho2g_ctx::kt_begin() {
     DHO2G_CUDA(cudaEventCreate(&b));
   }
   DHO2G_CUDA(cudaEventRecord(a, stream));
-  kpend.push_back({std::string(), a, b, 0.0});
-  return (int)kpend.size() - 1;
+  const int id = knext++;
+  kpend[id] = {std::string(), a, b, 0.0, false};
+  return id;
 }
 
 void dho2g_ctx::kt_end(int slot, const char* name, double work) {
   if (slot < 0) return;
-  KPending& p = kpend[slot];
+  auto it = kpend.find(slot);
+  if (it == kpend.end()) return;
+  KPending& p = it->second;
   p.name = name;
   p.work = work;
+  p.ended = true;
   DHO2G_CUDA(cudaEventRecord(p.b, stream));
   if (kpend.size() > 4096) kt_flush();
 }
@@ -199,7 +203,12 @@ void dho2g_ctx::kt_end(int slot, const char* name, double work) {
 void dho2g_ctx::kt_flush() {
   if (kpend.empty()) return;
   DHO2G_CUDA(cudaStreamSynchronize(stream));
-  for (auto& p : kpend) {
+  for (auto it = kpend.begin(); it != kpend.end();) {
+    KPending& p = it->second;
+    if (!p.ended) {  // still open (an enclosing phase timer): keep
+      ++it;
+      continue;
+    }
     float ms = 0.f;
     DHO2G_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     KStat& k = kstats[p.name];
@@ -208,8 +217,8 @@ void dho2g_ctx::kt_flush() {
     k.work += p.work;
     kpool.push_back(p.a);
     kpool.push_back(p.b);
+    it = kpend.erase(it);
   }
-  kpend.clear();
 }
 
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count) {

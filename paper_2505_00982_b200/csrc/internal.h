@@ -48,8 +48,9 @@ struct dho2g_ctx {
   std::map<std::string, double> stats;
   // Per-kernel device timers (CUDA events on this stream), enabled by option "ktimers".
   bool ktimers = false;
-  struct KPending { std::string name; cudaEvent_t a, b; double work; };
-  std::vector<KPending> kpend;
+  struct KPending { std::string name; cudaEvent_t a, b; double work; bool ended; };
+  std::map<int, KPending> kpend;  // open (nested) and ended timers, by id
+  int knext = 0;
   std::vector<cudaEvent_t> kpool;
   struct KStat { double ms = 0, count = 0, work = 0; };
   std::map<std::string, KStat> kstats;
