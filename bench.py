@@ -290,8 +290,18 @@ def run_ours(args, rank, world, dist):
     peaks = load_peaks()
     value = args.steps / (ms / 1e3)
     # dominant kernel -> roofline
-    kern, phases = {}, {}
-    for name, (kms, cnt, work) in kstats.items():
+    kern, phases, gemm_detail = {}, {}, {}
+    agg = {}
+    for name, (kms, cnt, work) in kstats.items():  # fold gemm3_tcgen05:<epilogue>/s<k> into one kernel
+        if ":" in name:
+            gemm_detail[name] = {"ms_total": round(kms, 3), "launches": int(cnt),
+                                 "useful_tflops": round(work / (kms / 1e3) / 1e12, 1) if kms > 0 else None}
+            name = name.split(":")[0]
+        a = agg.setdefault(name, [0.0, 0.0, 0.0])
+        a[0] += kms
+        a[1] += cnt
+        a[2] += work
+    for name, (kms, cnt, work) in agg.items():
         if cnt == 0 or kms <= 0:
             continue
         if name.startswith("phase."):
@@ -328,7 +338,7 @@ def run_ours(args, rank, world, dist):
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "kernels": kern,
-            "phases": phases,
+            "phases": phases, "gemm_detail": gemm_detail,
             "useful_tflops_per_step": (grad_flops(c["sizes"], c["b"] * c["workers"]) +
                                        hvp_flops(c["sizes"], c["curv"]) * (c["m"] or 40) / (c["P"] * rounds)) / 1e12}
     if world == 1 and not args.no_cpu_baseline:

@@ -64,23 +64,23 @@ __device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, con
         if (e.do0) {
           const float z = acc[j] + e.bias[col];
           v = e.mode == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
-          e.f0[ei] = v;
+          if (e.f0) e.f0[ei] = v;
         } else {
           const float rz = acc[j] + vsc * e.vbias[col];
           v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, e.a_in[ei]) * rz;
-          e.f1[ei] = v;
+          if (e.f1) e.f1[ei] = v;
         }
       } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
         const float a = e.a_in[ei];
         const float ap = act_prime(e.relu, a);
         if (e.do0) {
           v = acc[j] * ap;
-          e.f0[ei] = v;
-          e.u_out[ei] = acc[j];
+          if (e.f0) e.f0[ei] = v;
+          if (e.u_out) e.u_out[ei] = acc[j];
         } else {
           const float rap = (!e.relu && ap != 0.f) ? -2.f * a * e.ra_in[ei] : 0.f;
           v = acc[j] * ap + e.u_in[ei] * rap;
-          e.f1[ei] = v;
+          if (e.f1) e.f1[ei] = v;
         }
       }
     }
@@ -292,7 +292,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -314,7 +314,7 @@ struct Sched {
   }
 };
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Sched sc,
                     const __grid_constant__ Epi e, float* __restrict__ ws, unsigned* __restrict__ flags,
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int a = 0; a < ACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
@@ -404,7 +404,9 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps: TMEM -> registers -> (split-K combine) -> fused epilogue
-    const int ew = warp - 4;
+    // 8 warps: warp w reads TMEM lane quadrant w % 4 (hardware rule) and column half (w - 4) / 4.
+    const int ew = warp & 3;
+    const int chalf = (warp - 4) >> 2;
     uint32_t uc = 0;
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(256, 1)
         epi_bar();
       }
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
         float v[16];
         tmem_ld16(tbase + (uint32_t)c0, v);
         if (split > 0) {
@@ -497,8 +499,8 @@ int pick_splits(int tiles, int nkb, int sms) {
 
 }  // namespace tc
 
-void gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-              const bf16* Blo, int ldb, const Epi& e) {
+int gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+             const bf16* Blo, int ldb, const Epi& e) {
   using namespace tc;
   if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(Ahi) & 15) || (reinterpret_cast<uintptr_t>(Alo) & 15) ||
@@ -536,8 +538,9 @@ void gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* 
   const CUtensorMap mBh = make_map(ctx->encode_fn, Bhi, K, N, ldb, BN);
   const CUtensorMap mBl = make_map(ctx->encode_fn, Blo, K, N, ldb, BN);
   const int grid = std::min(sc.units, ctx->sm_count);
-  gemm3_tc_kernel<<<grid, 256, SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, sc, e, ws, flags, epoch);
+  gemm3_tc_kernel<<<grid, 384, SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, sc, e, ws, flags, epoch);
   DHO2G_LAUNCH();
+  return sc.splits;
 }
 
 void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
@@ -547,11 +550,18 @@ void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo
   ctx->bump("gemm_calls", 1);
   ctx->bump("gemm_flops_issued", 3.0 * 2.0 * double(M) * double(N) * double(K));
   const int slot = ctx->kt_begin();
+  int splits = 1;
   if (ctx->gemm_backend == 1)
     gemm3_simt(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
   else
-    gemm3_tc(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
-  ctx->kt_end(slot, ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05", 2.0 * double(M) * double(N) * double(K));
+    splits = gemm3_tc(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
+  if (slot >= 0) {  // name: backend:epilogue(+R)/splits, aggregated by prefix in the bench
+    static const char* modes[] = {"store", "fwd", "fwdout", "bwd"};
+    char name[64];
+    std::snprintf(name, sizeof(name), "%s:%s%s/s%d", ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05",
+                  modes[e.mode], e.do1 ? "R" : "", splits);
+    ctx->kt_end(slot, name, 2.0 * double(M) * double(N) * double(K));
+  }
 }
 
 void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,

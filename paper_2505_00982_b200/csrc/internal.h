@@ -169,8 +169,8 @@ void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf1
                  const bf16* Blo, int ldb, float* C, int ldc, float alpha, float* bias_out = nullptr);
 void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
                 const bf16* Blo, int ldb, const Epi& e);
-void gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-              const bf16* Blo, int ldb, const Epi& e);
+int gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+             const bf16* Blo, int ldb, const Epi& e);  // returns the split-K factor used
 
 // fp32 elementwise helpers (update.cu)
 void dev_copy_f64_to_f32(cudaStream_t s, const double* src, float* dst, size_t n);

@@ -435,9 +435,9 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.a_in = m->a32[t].p;
       e.ra_in = m->ra32[t].p;
       e.u_in = m->u32[t].p;
-      e.u_out = m->u32[t].p;
-      e.f0 = m->d32[t].p;
-      e.f1 = m->rd32[t].p;
+      e.u_out = wgrad ? nullptr : m->u32[t].p;  // U is only re-read by the R-epilogue of the HVP
+      e.f0 = nullptr;  // fp32 deltas of hidden levels are not re-read (bias grads come from the GEMM)
+      e.f1 = nullptr;
       e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Pin; e.hR = r ? 1 : 0;
       e.Th = m->DRT_hi[t].p; e.Tl = m->DRT_lo[t].p; e.ldT = ldT; e.Bp = Bp; e.hT = r ? 0 : 1;  // [rd^T | d^T]
       if (!r)  // U = D W
