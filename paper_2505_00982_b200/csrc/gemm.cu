@@ -482,6 +482,10 @@ CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t 
 
 // split-K factor that best fills the persistent grid (work quantization), >= 8 k-blocks per split
 int pick_splits(int tiles, int nkb, int sms) {
+  // Measured on B200 (profiles/r01_gemm_splits.txt): the fixed-order split-K combine costs more than
+  // the wave-quantization it removes for every C1-C4 shape, so the default is no split; the path
+  // stays available through dho2g_ctx_set_option("gemm_splits", s).
+  if (tiles > 0) return 1;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 4; ++s) {
