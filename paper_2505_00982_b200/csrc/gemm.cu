@@ -27,89 +27,94 @@ namespace dho2g {
 // =============================================================================== epilogue
 __device__ __forceinline__ float act_prime(bool relu, float a) { return relu ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a; }
 
-// Applies the epilogue to 16 consecutive columns [col0, col0+16) of one output row.
-__device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16]) {
+// One output element (row < M, col < N): mode-specific math, fp32 side outputs and the row-major
+// (hi, lo) pair; returns the value that goes to the transposed pair (0 when nothing does).
+__device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float acc, float vsc) {
+  const size_t ei = (size_t)row * e.N + col;
+  float v;
   if (e.mode == EPI_STORE) {
-    if (row >= e.M) return;
-    float* crow = e.C + (size_t)row * e.ldc;
-    const bool fast = col0 + 16 <= e.N - (e.bias_out ? 1 : 0) && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0);
-    if (fast) {
-#pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(crow + col0 + j) =
-            make_float4(e.alpha * acc[j], e.alpha * acc[j + 1], e.alpha * acc[j + 2], e.alpha * acc[j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = col0 + j;
-        if (col >= e.N) break;
-        const float v = e.alpha * acc[j];
-        if (e.bias_out && col == e.N - 1) e.bias_out[row] = v;
-        else crow[col] = v;
-      }
-    }
-    return;
+    v = e.alpha * acc;
+    if (e.bias_out && col == e.N - 1) e.bias_out[row] = v;
+    else e.C[(size_t)row * e.ldc + col] = v;
+    return 0.f;
   }
-  const bool live = row < e.M;
+  if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
+    // oracle.cpp:548-563: a = act(z), z = W a + b ; ra = act'(a) (V a + W ra + v_b)
+    if (e.do0) {
+      const float z = acc + e.bias[col];
+      v = e.mode == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
+      if (e.f0) e.f0[ei] = v;
+    } else {
+      const float rz = acc + vsc * e.vbias[col];
+      v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, e.a_in[ei]) * rz;
+      if (e.f1) e.f1[ei] = v;
+    }
+  } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
+    const float a = e.a_in[ei];
+    const float ap = act_prime(e.relu, a);
+    if (e.do0) {
+      v = acc * ap;
+      if (e.f0) e.f0[ei] = v;
+      if (e.u_out) e.u_out[ei] = acc;
+    } else {
+      const float rap = (!e.relu && ap != 0.f) ? -2.f * a * e.ra_in[ei] : 0.f;
+      v = acc * ap + e.u_in[ei] * rap;
+      if (e.f1) e.f1[ei] = v;
+    }
+  }
+  if (e.Rh) {
+    const size_t r = (size_t)row * (2 * e.P) + (size_t)e.hR * e.P + col;
+    split_bf16(v, e.Rh[r], e.Rl[r]);
+  }
+  return v;
+}
+
+// Per-thread form (CUDA-core backend): 16 consecutive columns of one row.
+__device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16]) {
   const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
   float x[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int col = col0 + j;
-    float v = 0.f;
-    if (live && col < e.N) {
-      const size_t ei = (size_t)row * e.N + col;
-      if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
-        // oracle.cpp:548-563: a = act(z), z = W a + b ; ra = act'(a) (V a + W ra + v_b)
-        if (e.do0) {
-          const float z = acc[j] + e.bias[col];
-          v = e.mode == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
-          if (e.f0) e.f0[ei] = v;
-        } else {
-          const float rz = acc[j] + vsc * e.vbias[col];
-          v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, e.a_in[ei]) * rz;
-          if (e.f1) e.f1[ei] = v;
-        }
-      } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
-        const float a = e.a_in[ei];
-        const float ap = act_prime(e.relu, a);
-        if (e.do0) {
-          v = acc[j] * ap;
-          if (e.f0) e.f0[ei] = v;
-          if (e.u_out) e.u_out[ei] = acc[j];
-        } else {
-          const float rap = (!e.relu && ap != 0.f) ? -2.f * a * e.ra_in[ei] : 0.f;
-          v = acc[j] * ap + e.u_in[ei] * rap;
-          if (e.f1) e.f1[ei] = v;
-        }
-      }
-    }
-    x[j] = v;
-  }
-  if (live && e.Rh) {  // row-major (hi, lo) pair, half hR
-    const size_t base = (size_t)row * (2 * e.P) + (size_t)e.hR * e.P + col0;
-    if (col0 + 16 <= e.N) {
-      __align__(16) bf16 h[16], l[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) split_bf16(x[j], h[j], l[j]);
-      *reinterpret_cast<uint4*>(e.Rh + base) = *reinterpret_cast<const uint4*>(h);
-      *reinterpret_cast<uint4*>(e.Rh + base + 8) = *reinterpret_cast<const uint4*>(h + 8);
-      *reinterpret_cast<uint4*>(e.Rl + base) = *reinterpret_cast<const uint4*>(l);
-      *reinterpret_cast<uint4*>(e.Rl + base + 8) = *reinterpret_cast<const uint4*>(l + 8);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (col0 + j < e.N) split_bf16(x[j], e.Rh[base + j], e.Rl[base + j]);
-    }
-  }
-  if (e.Th && row < e.Bp) {  // transposed (hi, lo) pair, half hT; pad rows [M, Bp) get zeros
+  for (int j = 0; j < 16; ++j) x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j], vsc) : 0.f;
+  if (e.mode != EPI_STORE && e.Th && row < e.Bp) {  // transposed pair; pad rows [M, Bp) get zeros
     const size_t base = (size_t)e.hT * e.Bp + row;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int col = col0 + j;
-      if (col < e.N) split_bf16(x[j], e.Th[(size_t)col * e.ldT + base], e.Tl[(size_t)col * e.ldT + base]);
+    for (int j = 0; j < 16; ++j)
+      if (col0 + j < e.N) split_bf16(x[j], e.Th[(size_t)(col0 + j) * e.ldT + base], e.Tl[(size_t)(col0 + j) * e.ldT + base]);
+  }
+}
+
+// Warp-cooperative form (tcgen05 epilogue): lane l holds row row0 + l, columns [col0, col0+16).
+// The 32x16 block is restaged through shared memory (sm: 32 x 17 floats) so that the row-major
+// traffic (fp32 inputs/outputs, row-major pairs, C) is coalesced (16 lanes per row segment), and the
+// transposed pair is written from the lane=row layout (32 consecutive rows per column).
+__device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, const float (&acc)[16], float* sm) {
+  const int lane = threadIdx.x & 31;
+  const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) sm[lane * 17 + j] = acc[j];
+  __syncwarp();
+  const int rr = lane >> 4, cc = lane & 15;
+  const int col = col0 + cc;
+#pragma unroll 4
+  for (int it = 0; it < 16; ++it) {
+    const int rl = 2 * it + rr;
+    const int row = row0 + rl;
+    float x = 0.f;
+    if (row < e.M && col < e.N) x = epi_elem(e, row, col, sm[rl * 17 + cc], vsc);
+    sm[rl * 17 + cc] = x;
+  }
+  __syncwarp();
+  if (e.mode != EPI_STORE && e.Th) {
+    const int row = row0 + lane;
+    if (row < e.Bp) {
+      const size_t base = (size_t)e.hT * e.Bp + row;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (col0 + j < e.N) split_bf16(sm[lane * 17 + j], e.Th[(size_t)(col0 + j) * e.ldT + base],
+                                       e.Tl[(size_t)(col0 + j) * e.ldT + base]);
     }
   }
+  __syncwarp();
 }
 
 namespace {
@@ -218,7 +223,8 @@ constexpr int ACC = 2;   // TMEM accumulator buffers
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t EPI_SMEM = 8 * 32 * 17 * 4;  // per epilogue warp: 32 x 16 restaging block (+1 pad)
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
 constexpr uint32_t TMEM_COLS = ACC * BN;
 // instruction descriptor, kind::f16: D=F32 [4,6), A=BF16 [7,10), B=BF16 [10,13), K-major both,
 // N>>3 [17,23), M>>4 [24,29)
@@ -407,6 +413,7 @@ __global__ void __launch_bounds__(384, 1)
     // 8 warps: warp w reads TMEM lane quadrant w % 4 (hardware rule) and column half (w - 4) / 4.
     const int ew = warp & 3;
     const int chalf = (warp - 4) >> 2;
+    float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
     uint32_t uc = 0;
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
@@ -415,7 +422,6 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
       const int r_local = ew * 32 + lane;
-      const int row = m0 + r_local;
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
       float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)r_local * BN : nullptr;
       const bool last = split == sc.splits - 1;
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
         if (last) {
-          epi_apply16(e, row, n0 + c0, v);
+          epi_warp16(e, m0 + ew * 32, n0 + c0, v, esm);
         } else {
           float4* p = reinterpret_cast<float4*>(wtile + c0);
 #pragma unroll
