@@ -83,7 +83,10 @@ struct DevBuf {
     n = count;
     if (count == 0) return;
     DHO2G_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    // cudaMemset runs on the legacy stream, which does not order with the library's non-blocking
+    // stream: complete it before any kernel can touch the buffer.
     DHO2G_CUDA(cudaMemset(p, 0, count * sizeof(T)));
+    DHO2G_CUDA(cudaStreamSynchronize(0));
   }
   void ensure(size_t count) { if (count > n) alloc(count); }
   void release() {

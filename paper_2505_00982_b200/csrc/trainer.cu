@@ -372,12 +372,12 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
     t->w_a_shard = t->w_a_sh.p;
     t->g_shard = t->g_sh.p;
     if (t->rows)
-      DHO2G_CUDA(cudaMemcpy(t->w_a_shard, t->w_a_full.p + t->begin, t->rows * sizeof(float), cudaMemcpyDeviceToDevice));
+      DHO2G_CUDA(cudaMemcpyAsync(t->w_a_shard, t->w_a_full.p + t->begin, t->rows * sizeof(float), cudaMemcpyDeviceToDevice, st));
   }
   t->w_sh.alloc(std::max<size_t>(t->base, 1));
   t->pi_sh.alloc(std::max<size_t>(t->base, 1));
   if (t->rows)
-    DHO2G_CUDA(cudaMemcpy(t->w_sh.p, t->w_a_shard, t->rows * sizeof(float), cudaMemcpyDeviceToDevice));  // make_admm_state
+    DHO2G_CUDA(cudaMemcpyAsync(t->w_sh.p, t->w_a_shard, t->rows * sizeof(float), cudaMemcpyDeviceToDevice, st));  // make_admm_state
   opt_alloc(&t->opt, ctx, cfg->base, t->rows);
   // curvature operator bound to (w_a, curvature batch) like the trainer.cpp:116 lambda
   t->op.ctx = ctx;
