@@ -423,7 +423,11 @@ __global__ void __launch_bounds__(384, 1)
       fence_after();
       const int r_local = ew * 32 + lane;
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
-      float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)r_local * BN : nullptr;
+      // split-K partial, private layout [warp slot][chunk][q][lane][4] so every float4 access of a
+      // warp is one contiguous 512 B segment
+      float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)(ew + 4 * chalf) * (32 * BN / 2) + (size_t)lane * 4
+                        : nullptr;
+      (void)r_local;
       const bool last = split == sc.splits - 1;
       if (split > 0) {  // wait for the previous split of this tile (fixed combine order)
         if (threadIdx.x == 128) {
@@ -437,19 +441,20 @@ __global__ void __launch_bounds__(384, 1)
         float v[16];
         tmem_ld16(tbase + (uint32_t)c0, v);
         if (split > 0) {
-          const float4* p = reinterpret_cast<const float4*>(wtile + c0);
+          const float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 t = __ldcg(p + q);
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(p + q * 128));
             v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
           }
         }
         if (last) {
           epi_warp16(e, m0 + ew * 32, n0 + c0, v, esm);
         } else {
-          float4* p = reinterpret_cast<float4*>(wtile + c0);
+          float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) __stcg(p + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+          for (int q = 0; q < 4; ++q)
+            __stcg(reinterpret_cast<float4*>(p + q * 128), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
       }
       fence_before();

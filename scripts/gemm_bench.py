@@ -24,6 +24,9 @@ SHAPES = [  # (M, N, K, what)
 
 def main():
     ctx = d.Context(0)
+    splits = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    ctx.set_option("gemm_splits", splits)
+    print("gemm_splits", splits)
     rng = np.random.default_rng(0)
     for M, N, K, what in SHAPES:
         A = rng.standard_normal((M, K)).astype(np.float32)
