@@ -493,17 +493,20 @@ CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t 
 
 // split-K factor that best fills the persistent grid (work quantization), >= 8 k-blocks per split
 int pick_splits(int tiles, int nkb, int sms) {
-  // Measured on B200 (profiles/r01_gemm_splits.txt): the fixed-order split-K combine costs more than
-  // the wave-quantization it removes for every C1-C4 shape, so the default is no split; the path
-  // stays available through dho2g_ctx_set_option("gemm_splits", s).
-  if (tiles > 0) return 1;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 4; ++s) {
-    if (s > 1 && nkb / s < 8) break;
+  // Split only when whole-tile scheduling leaves the persistent grid badly quantised (the HVP GEMMs at
+  // M = B = 1024: 224 tiles on 148 SMs); each extra split costs ~5% (partial write + read).
+  // Measured on B200: profiles/r01_gemm_splits.txt.
+  auto eff_of = [&](int s) {
     const int units = tiles * s;
     const int waves = (units + sms - 1) / sms;
-    const double eff = (double)units / ((double)waves * sms) * (1.0 - 0.02 * (s - 1));  // combine cost
+    return (double)units / ((double)waves * sms) - 0.05 * (s - 1);
+  };
+  if (eff_of(1) >= 0.85) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 3; ++s) {
+    if (s > 1 && nkb / s < 8) break;
+    const double eff = eff_of(s);
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = s;
