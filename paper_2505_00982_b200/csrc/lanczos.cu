@@ -166,35 +166,56 @@ __global__ void __launch_bounds__(kThreads) gs_pass2_kernel(const float* __restr
     }
   }
   __syncthreads();
+  // Each warp owns super-groups of 128 float4 groups (512 rows): per basis column it streams one
+  // contiguous 2 KB segment (lane l reads groups l, l+32, l+64, l+96), like pass 1's work items.
   double ss = 0.0;
-  for (size_t g = blockIdx.x * (size_t)kThreads + threadIdx.x; g < ngroups; g += (size_t)gridDim.x * kThreads) {
-    const float4 h4 = reinterpret_cast<const float4*>(hsrc)[g];
-    double a0 = h4.x, a1 = h4.y, a2 = h4.z, a3 = h4.w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t nsg = ngroups / 128;
+  for (size_t sgi = (size_t)blockIdx.x * kWarps + warp; sgi < nsg; sgi += (size_t)gridDim.x * kWarps) {
+    const size_t g0 = sgi * 128 + lane;
+    double a[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 h4 = reinterpret_cast<const float4*>(hsrc)[g0 + 32 * q];
+      a[q][0] = h4.x; a[q][1] = h4.y; a[q][2] = h4.z; a[q][3] = h4.w;
+    }
     int j = 0;
-    for (; j + 4 <= active; j += 4) {
-      float4 d[4];
+    for (; j + 2 <= active; j += 2) {
+      float4 d[2][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) d[u] = __ldg(reinterpret_cast<const float4*>(D + (size_t)(j + u) * ldd) + g);
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+        for (int q = 0; q < 4; ++q)
+          d[u][q] = __ldg(reinterpret_cast<const float4*>(D + (size_t)(j + u) * ldd) + g0 + 32 * q);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
         const double c = e[j + u];
-        a0 -= (double)d[u].x * c;
-        a1 -= (double)d[u].y * c;
-        a2 -= (double)d[u].z * c;
-        a3 -= (double)d[u].w * c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q][0] -= (double)d[u][q].x * c;
+          a[q][1] -= (double)d[u][q].y * c;
+          a[q][2] -= (double)d[u][q].z * c;
+          a[q][3] -= (double)d[u][q].w * c;
+        }
       }
     }
     for (; j < active; ++j) {
-      const float4 d = __ldg(reinterpret_cast<const float4*>(D + (size_t)j * ldd) + g);
       const double c = e[j];
-      a0 -= (double)d.x * c;
-      a1 -= (double)d.y * c;
-      a2 -= (double)d.z * c;
-      a3 -= (double)d.w * c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 dd = __ldg(reinterpret_cast<const float4*>(D + (size_t)j * ldd) + g0 + 32 * q);
+        a[q][0] -= (double)dd.x * c;
+        a[q][1] -= (double)dd.y * c;
+        a[q][2] -= (double)dd.z * c;
+        a[q][3] -= (double)dd.w * c;
+      }
     }
-    const float4 o = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-    reinterpret_cast<float4*>(dst)[g] = o;
-    ss += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 o = make_float4((float)a[q][0], (float)a[q][1], (float)a[q][2], (float)a[q][3]);
+      reinterpret_cast<float4*>(dst)[g0 + 32 * q] = o;
+      ss += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+    }
   }
   const double t = block_sum(ss, red);
   if (threadIdx.x == 0) part[blockIdx.x] = t;
@@ -578,7 +599,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   const int nchunks = (int)(lz->ldd / kGsChunk);
   const int g1 = std::min(nchunks, ctx->sm_count * 4);
   const size_t ngroups = lz->ldd / 4;
-  const int g2 = (int)std::min<size_t>(cdiv(ngroups, kThreads), (size_t)ctx->sm_count * 4);
+  const int g2 = (int)std::min<size_t>(cdiv(ngroups / 128, kWarps), (size_t)ctx->sm_count * 4);
   const double* allp = world > 1 ? lz->allp.p : lz->rankp.p;
   const double* allb = world > 1 ? lz->allp.p : lz->rankp.p;
 
