@@ -83,43 +83,41 @@ __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restr
                                                             const LzDev* st, int safeguard_pass) {
   if (st->stopped || (safeguard_pass && !st->need_sg)) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  float* hs = reinterpret_cast<float*>(smem);
-  double* acc = reinterpret_cast<double*>(smem + kGsChunk * sizeof(float));  // [kWarps][active+1]
+  double* acc = reinterpret_cast<double*>(smem);  // [kWarps][active+1]
   __shared__ bool is_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nj = active + 1;
   for (int e = threadIdx.x; e < kWarps * nj; e += kThreads) acc[e] = 0.0;
+  __syncthreads();
+  // Work items (chunk of this CTA, column j <= active, 512-row quarter q) are walked by the warps
+  // independently (no block barrier per chunk); h is read through L1 (reused by the nj items of a
+  // chunk). 4-term products in fp32, everything above in fp64.
   const int items = nj * (kGsChunk / kSub);
-  for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const size_t r0 = (size_t)c * kGsChunk;
-    __syncthreads();
-    for (int e = threadIdx.x; e < kGsChunk / 4; e += kThreads)
-      reinterpret_cast<float4*>(hs)[e] = reinterpret_cast<const float4*>(h + r0)[e];
-    __syncthreads();
-    for (int it = warp; it < items; it += kWarps) {
-      const int j = it / (kGsChunk / kSub), q = it % (kGsChunk / kSub);
-      const int rb = q * kSub + lane * 4;
-      double s = 0.0;
-      if (j < active) {
-        const float* col = D + (size_t)j * ldd + r0;
-        float4 x[4];
+  const int my_chunks = blockIdx.x < nchunks ? (nchunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const long long total = (long long)my_chunks * items;
+  for (long long idx = warp; idx < total; idx += kWarps) {
+    const int cl = (int)(idx / items), it = (int)(idx % items);
+    const size_t r0 = ((size_t)blockIdx.x + (size_t)cl * gridDim.x) * kGsChunk;
+    const int j = it / (kGsChunk / kSub), q = it % (kGsChunk / kSub);
+    const int rb = q * kSub + lane * 4;
+    const float* hc = h + r0 + rb;
+    float4 y[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + rb + k * 128));
+    for (int k = 0; k < 4; ++k) y[k] = __ldg(reinterpret_cast<const float4*>(hc + k * 128));
+    double s = 0.0;
+    if (j < active) {
+      const float* col = D + (size_t)j * ldd + r0 + rb;
+      float4 x[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 y = *reinterpret_cast<const float4*>(hs + rb + k * 128);
-          s += (double)x[k].x * y.x + (double)x[k].y * y.y + (double)x[k].z * y.z + (double)x[k].w * y.w;
-        }
-      } else {
+      for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + k * 128));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 y = *reinterpret_cast<const float4*>(hs + rb + k * 128);
-          s += (double)y.x * y.x + (double)y.y * y.y + (double)y.z * y.z + (double)y.w * y.w;
-        }
-      }
-      s = warp_sum(s);
-      if (lane == 0) acc[warp * nj + j] += s;
+      for (int k = 0; k < 4; ++k) s += (double)(x[k].x * y[k].x + x[k].y * y[k].y + x[k].z * y[k].z + x[k].w * y[k].w);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += (double)(y[k].x * y[k].x + y[k].y * y[k].y + y[k].z * y[k].z + y[k].w * y[k].w);
     }
+    s = warp_sum(s);
+    if (lane == 0) acc[warp * nj + j] += s;
   }
   __syncthreads();
   for (int j = threadIdx.x; j < nj; j += kThreads) {
@@ -613,7 +611,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
       vfull = lz->vfull.p;
     }
     op->apply(vfull, &lz->st.p->sigma[i], lz->h.p, lz->begin, lz->rows, lz->base);
-    const size_t smem1 = kGsChunk * sizeof(float) + (size_t)kWarps * (active + 1) * sizeof(double);
+    const size_t smem1 = (size_t)kWarps * (active + 1) * sizeof(double);
     const size_t smem2 = (size_t)(active + 1) * sizeof(double);
     for (int pass = 0; pass < (lz->opts.reorth_safeguard ? 2 : 1); ++pass) {
       const float* hsrc = pass == 0 ? lz->h.p : Dn;
