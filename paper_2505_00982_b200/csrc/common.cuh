@@ -117,6 +117,17 @@ struct HostBuf {
 
 typedef __nv_bfloat16 bf16;
 
+// Grid for a grid-stride (persistent-style) kernel: exactly one wave of resident CTAs, capped by
+// the work. A second partial wave of such a kernel idles most SMs for a whole CTA lifetime.
+template <typename Kernel>
+inline int one_wave_grid(Kernel kernel, int threads, size_t smem, int sm_count, size_t work_blocks) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const size_t cap = (size_t)per_sm * (size_t)sm_count;
+  return (int)(work_blocks < 1 ? 1 : (work_blocks < cap ? work_blocks : cap));
+}
+
 // ----------------------------------------------------------------------------- device helpers
 __device__ __forceinline__ void split_bf16(float x, bf16& hi, bf16& lo) {
   hi = __float2bfloat16_rn(x);

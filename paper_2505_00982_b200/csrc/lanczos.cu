@@ -22,6 +22,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSub = 512;  // rows per warp work item (32 lanes x 4 float4)
 constexpr double kBreakdownFloor32 = 4e-6;
+constexpr int kP2Unroll = 4;  // basis columns in flight per pass-2 thread (x 4 float4)
 constexpr double kSafeguardFloor32 = 1e-3;
 
 // ------------------------------------------------------------------ start vector
@@ -178,15 +179,15 @@ __global__ void __launch_bounds__(kThreads) gs_pass2_kernel(const float* __restr
       a[q][0] = h4.x; a[q][1] = h4.y; a[q][2] = h4.z; a[q][3] = h4.w;
     }
     int j = 0;
-    for (; j + 2 <= active; j += 2) {
-      float4 d[2][4];
+    for (; j + kP2Unroll <= active; j += kP2Unroll) {
+      float4 d[kP2Unroll][4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < kP2Unroll; ++u)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           d[u][q] = __ldg(reinterpret_cast<const float4*>(D + (size_t)(j + u) * ldd) + g0 + 32 * q);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kP2Unroll; ++u) {
         const double c = e[j + u];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -563,8 +564,8 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   lz->h.alloc(lz->ldd);
   if (ctx->world > 1) lz->vfull.alloc(lz->base * ctx->world);
   lz->st.alloc(1);
-  const int g1 = (int)std::min<size_t>(cdiv(lz->ldd, kGsChunk), (size_t)ctx->sm_count * 4);
-  const int g2 = (int)std::min<size_t>(cdiv(lz->ldd / 4, kThreads), (size_t)ctx->sm_count * 4);
+  const int g1 = ctx->sm_count * 8;  // upper bound of the one-wave grids (256-thread CTAs, <= 8 per SM)
+  const int g2 = ctx->sm_count * 8;
   lz->part.alloc((size_t)std::max(g1, g2) * (m + 2) + 8);
   lz->rankp.alloc(m + 2);
   lz->allp.alloc((m + 2) * ctx->world);
@@ -595,9 +596,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   }
 
   const int nchunks = (int)(lz->ldd / kGsChunk);
-  const int g1 = std::min(nchunks, ctx->sm_count * 4);
   const size_t ngroups = lz->ldd / 4;
-  const int g2 = (int)std::min<size_t>(cdiv(ngroups / 128, kWarps), (size_t)ctx->sm_count * 4);
   const double* allp = world > 1 ? lz->allp.p : lz->rankp.p;
   const double* allb = world > 1 ? lz->allp.p : lz->rankp.p;
 
@@ -613,6 +612,8 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
     op->apply(vfull, &lz->st.p->sigma[i], lz->h.p, lz->begin, lz->rows, lz->base);
     const size_t smem1 = (size_t)kWarps * (active + 1) * sizeof(double);
     const size_t smem2 = (size_t)(active + 1) * sizeof(double);
+    const int g1 = one_wave_grid(gs_pass1_kernel, kThreads, smem1, ctx->sm_count, (size_t)nchunks);
+    const int g2 = one_wave_grid(gs_pass2_kernel, kThreads, smem2, ctx->sm_count, cdiv(ngroups / 128, kWarps));
     for (int pass = 0; pass < (lz->opts.reorth_safeguard ? 2 : 1); ++pass) {
       const float* hsrc = pass == 0 ? lz->h.p : Dn;
       // algorithmic bytes: active columns of D + h (pass 1); + h' write (pass 2)

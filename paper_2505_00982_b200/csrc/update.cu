@@ -91,7 +91,7 @@ __device__ __forceinline__ void chunk_dots(const float* __restrict__ V, size_t l
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float4 y = *reinterpret_cast<const float4*>(xs + rb + k * 128);
-      s += (double)x[k].x * y.x + (double)x[k].y * y.y + (double)x[k].z * y.z + (double)x[k].w * y.w;
+      s += (double)(x[k].x * y.x + x[k].y * y.y + x[k].z * y.z + x[k].w * y.w);  // fp32 4-term, fp64 above
     }
     s = warp_sum(s);
     if (lane == 0) acc[warp * R + j] += s;
@@ -352,7 +352,10 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(a.g) || !al16(a.pi) || !al16(a.w_a) || !al16(a.w_decay) || !al16(a.newton_out) || !al16(a.base_out))
     fail(DHO2G_ARGUMENT, "split_update: vectors must be 16-byte aligned");
-  const int gp = (int)std::max<size_t>(1, std::min<size_t>(cdiv(rows, kCh), (size_t)ctx->sm_count * 4));
+  const size_t smem_p1 = kCh * sizeof(float) + (size_t)kW * R * sizeof(double);
+  const size_t smem_p2 = kCh * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double);
+  const int gp = std::min(one_wave_grid(upd_p1_kernel, kT, smem_p1, ctx->sm_count, cdiv(rows, kCh)),
+                          one_wave_grid(upd_p2_kernel, kT, smem_p2, ctx->sm_count, cdiv(rows, kCh)));
   const int R1 = std::max(R, 1);
   o->part.ensure((size_t)gp * R1 + 8);
   o->rank1.ensure(R1);
@@ -365,7 +368,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const bool adam = o->cfg.kind >= 2;
   if (R > 0) {
     const int k1 = ctx->kt_begin();
-    upd_p1_kernel<<<gp, kT, kCh * sizeof(float) + (size_t)kW * R * sizeof(double), st>>>(V, ldv, R, rows, a.g, a.pi,
+    upd_p1_kernel<<<gp, kT, smem_p1, st>>>(V, ldv, R, rows, a.g, a.pi,
                                                                                          o->part.p, o->rank1.p,
                                                                                          o->ticket.p);
     DHO2G_LAUNCH();
@@ -375,14 +378,14 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   ++o->t;
   const BaseHyper hp = make_hyper(o->cfg, o->t);
   const int k2 = ctx->kt_begin();
-  upd_p2_kernel<<<gp, kT, kCh * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double), st>>>(
+  upd_p2_kernel<<<gp, kT, smem_p2, st>>>(
       V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p, o->v.p, o->s.p, o->part.p,
       o->rank2.p, o->ticket.p + 1, o->bad.p);
   DHO2G_LAUNCH();
   ctx->kt_end(k2, "upd_p2", rb * (R + 2 + (a.pi ? 1 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
                                   (o->cfg.kind == 3 ? 1 : 0)));
   if (R > 0 && world > 1) ctx->allgather_f64(o->rank2.p, o->all2.p, R);
-  const int g3 = (int)std::max<size_t>(1, std::min<size_t>(cdiv(cdiv(rows, 4), kT), (size_t)ctx->sm_count * 4));
+  const int g3 = one_wave_grid(upd_p3_kernel, kT, (size_t)2 * R1 * sizeof(double), ctx->sm_count, cdiv(cdiv(rows, 4), kT));
   const int k3 = ctx->kt_begin();
   upd_p3_kernel<<<g3, kT, (size_t)2 * R1 * sizeof(double), st>>>(V, ldv, R, rows, o->s.p, all1, all2, world,
                                                                   R ? ese->ev_dev.p : nullptr, a.alpha, a.sigma,
