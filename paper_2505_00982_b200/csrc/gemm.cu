@@ -27,9 +27,35 @@ namespace dho2g {
 // =============================================================================== epilogue
 __device__ __forceinline__ float act_prime(bool relu, float a) { return relu ? (a > 0.f ? 1.f : 0.f) : 1.f - a * a; }
 
+// Inputs an element's epilogue reads besides the accumulator (split from the math so the
+// warp-cooperative form can issue all of a block's loads before the first use).
+struct EpiIn {
+  float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+};
+__device__ __forceinline__ EpiIn epi_load(const Epi& e, int row, int col) {
+  EpiIn in;
+  const size_t ei = (size_t)row * e.N + col;
+  if (e.mode == EPI_STORE) return in;
+  if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
+    if (e.do0) {
+      in.p0 = __ldg(e.bias + col);
+    } else {
+      in.p0 = __ldg(e.vbias + col);
+      if (e.mode == EPI_FWD) in.p1 = __ldg(e.a_in + ei);
+    }
+  } else {
+    in.p1 = __ldg(e.a_in + ei);
+    if (e.do1) {
+      in.p0 = __ldg(e.u_in + ei);
+      if (!e.relu) in.p2 = __ldg(e.ra_in + ei);
+    }
+  }
+  return in;
+}
+
 // One output element (row < M, col < N): mode-specific math, fp32 side outputs and the row-major
 // (hi, lo) pair; returns the value that goes to the transposed pair (0 when nothing does).
-__device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float acc, float vsc) {
+__device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float acc, float vsc, const EpiIn& in) {
   const size_t ei = (size_t)row * e.N + col;
   float v;
   if (e.mode == EPI_STORE) {
@@ -41,24 +67,24 @@ __device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float 
   if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
     // oracle.cpp:548-563: a = act(z), z = W a + b ; ra = act'(a) (V a + W ra + v_b)
     if (e.do0) {
-      const float z = acc + e.bias[col];
+      const float z = acc + in.p0;
       v = e.mode == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
       if (e.f0) e.f0[ei] = v;
     } else {
-      const float rz = acc + vsc * e.vbias[col];
-      v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, e.a_in[ei]) * rz;
+      const float rz = acc + vsc * in.p0;
+      v = e.mode == EPI_FWD_OUT ? rz : act_prime(e.relu, in.p1) * rz;
       if (e.f1) e.f1[ei] = v;
     }
   } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
-    const float a = e.a_in[ei];
+    const float a = in.p1;
     const float ap = act_prime(e.relu, a);
     if (e.do0) {
       v = acc * ap;
       if (e.f0) e.f0[ei] = v;
       if (e.u_out) e.u_out[ei] = acc;
     } else {
-      const float rap = (!e.relu && ap != 0.f) ? -2.f * a * e.ra_in[ei] : 0.f;
-      v = acc * ap + e.u_in[ei] * rap;
+      const float rap = (!e.relu && ap != 0.f) ? -2.f * a * in.p2 : 0.f;
+      v = acc * ap + in.p0 * rap;
       if (e.f1) e.f1[ei] = v;
     }
   }
@@ -74,7 +100,8 @@ __device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, con
   const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
   float x[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j], vsc) : 0.f;
+  for (int j = 0; j < 16; ++j)
+    x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j], vsc, epi_load(e, row, col0 + j)) : 0.f;
   if (e.mode != EPI_STORE && e.Th && row < e.Bp) {  // transposed pair; pad rows [M, Bp) get zeros
     const size_t base = (size_t)e.hT * e.Bp + row;
 #pragma unroll
@@ -95,12 +122,19 @@ __device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, con
   __syncwarp();
   const int rr = lane >> 4, cc = lane & 15;
   const int col = col0 + cc;
-#pragma unroll 4
+  // all loads of the 32x16 block first (one memory latency per block, not one per row pair)
+  EpiIn in[16];
+#pragma unroll
+  for (int it = 0; it < 16; ++it) {
+    const int row = row0 + 2 * it + rr;
+    if (row < e.M && col < e.N) in[it] = epi_load(e, row, col);
+  }
+#pragma unroll
   for (int it = 0; it < 16; ++it) {
     const int rl = 2 * it + rr;
     const int row = row0 + rl;
     float x = 0.f;
-    if (row < e.M && col < e.N) x = epi_elem(e, row, col, sm[rl * 17 + cc], vsc);
+    if (row < e.M && col < e.N) x = epi_elem(e, row, col, sm[rl * 17 + cc], vsc, in[it]);
     sm[rl * 17 + cc] = x;
   }
   __syncwarp();
