@@ -195,6 +195,11 @@ int dho2g_trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count);
 /* ---- test hook: one split-BF16x3 GEMM C = A B^T over host fp32 (A: M x K, B: N x K, row-major).
  * backend 0 = tcgen05 kernel, 1 = CUDA-core reference kernel. ------------------------------- */
 int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* C, int backend);
+/* Two-segment form C = A0 B0^T + A1 B1^T (A0: M x K0, A1: M x K1, B0: N x K0, B1: N x K1; K1 = 0: one
+ * segment) with each operand stored K-major (a_mn / b_mn = 0) or MN-major (1), the layouts the MLP's
+ * concatenated contractions use. */
+int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const float* A0, const float* A1,
+                        const float* B0, const float* B1, float* C, int backend, int a_mn, int b_mn);
 
 #ifdef __cplusplus
 }

@@ -112,6 +112,8 @@ _SIGS = {
     "dho2g_trainer_eigvals": ([vp, dp, sp], C.c_int),
     "dho2g_test_gemm": ([vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float),
                          C.POINTER(C.c_float), C.c_int], C.c_int),
+    "dho2g_test_gemm_seg": ([vp, C.c_int, C.c_int, C.c_int, C.c_int] + [C.POINTER(C.c_float)] * 5 +
+                            [C.c_int, C.c_int, C.c_int], C.c_int),
 }
 
 for _name, (_args, _res) in _SIGS.items():

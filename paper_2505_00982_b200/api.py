@@ -253,6 +253,27 @@ def test_gemm(ctx: "Context", A, B, backend: int = 0):
     return Cm
 
 
+def test_gemm_seg(ctx: "Context", A0, B0, A1=None, B1=None, backend: int = 0, a_mn: int = 0, b_mn: int = 0):
+    """Two-segment GEMM C = A0 B0^T + A1 B1^T with K-major (0) or MN-major (1) operand storage (test hook)."""
+    A0 = np.ascontiguousarray(A0, np.float32)
+    B0 = np.ascontiguousarray(B0, np.float32)
+    M, K0 = A0.shape
+    N = B0.shape[0]
+    if A1 is None:
+        A1 = np.zeros((M, 0), np.float32)
+        B1 = np.zeros((N, 0), np.float32)
+    A1 = np.ascontiguousarray(A1, np.float32)
+    B1 = np.ascontiguousarray(B1, np.float32)
+    K1 = A1.shape[1]
+    Cm = np.empty((M, N), np.float32)
+    fp = C.POINTER(C.c_float)
+    one = np.zeros(1, np.float32)
+    ptr = lambda x: (x if x.size else one).ctypes.data_as(fp)  # noqa: E731
+    check(lib.dho2g_test_gemm_seg(ctx.h, M, N, K0, K1, ptr(A0), ptr(A1), ptr(B0), ptr(B1), Cm.ctypes.data_as(fp),
+                                  backend, a_mn, b_mn))
+    return Cm
+
+
 # ----------------------------------------------------------------------------- oracle.hpp
 @dataclass
 class Batch:

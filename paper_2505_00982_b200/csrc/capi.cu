@@ -129,6 +129,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     const std::string k = key ? key : "";
     if (k == "gemm") ctx->gemm_backend = (int)value;
     else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
+    else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
     else if (k == "ktimers") {
       ctx->kt_flush();
@@ -556,6 +557,7 @@ int dho2g_lanczos_basis(const dho2g_lanczos* lz, double* basis_shard) {
   return guard([&] {
     const int it = lz->host.iters;
     const int cols = lz->host.breakdown ? it : it + 1;
+    DHO2G_CUDA(cudaStreamSynchronize(lz->ctx->stream));  // legacy-stream copies below do not order with it
     std::vector<float> f(lz->rows);
     for (int j = 0; j < cols; ++j) {
       if (lz->rows)
@@ -590,6 +592,7 @@ int dho2g_ese_eigvals(const dho2g_ese* ese, double* vals) {
 
 int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs) {
   return guard([&] {
+    if (ese->ctx) DHO2G_CUDA(cudaStreamSynchronize(ese->ctx->stream));
     std::vector<float> f(ese->rows);
     for (size_t c = 0; c < ese->r; ++c) {
       if (ese->rows)
@@ -617,9 +620,11 @@ int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, 
     for (size_t c = 0; c < r; ++c) {
       for (size_t i = 0; i < e->rows; ++i) col[i] = (float)V[c * n + e->begin + i];
       if (e->rows)
-        DHO2G_CUDA(cudaMemcpy(e->V.p + c * e->ldv, col.data(), e->rows * sizeof(float), cudaMemcpyHostToDevice));
+        DHO2G_CUDA(cudaMemcpyAsync(e->V.p + c * e->ldv, col.data(), e->rows * sizeof(float), cudaMemcpyHostToDevice,
+                                   ctx->stream));  // stream-ordered before any use (pageable source staged)
     }
-    if (r) DHO2G_CUDA(cudaMemcpy(e->ev_dev.p, eigvals, r * sizeof(double), cudaMemcpyHostToDevice));
+    if (r) DHO2G_CUDA(cudaMemcpyAsync(e->ev_dev.p, eigvals, r * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = e.release();
   });
 }
@@ -774,14 +779,93 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
     const int ld = (int)round_up(std::max(K, 1), 8);
     DevBuf<float> a((size_t)M * K), b((size_t)N * K), c((size_t)M * N);
     DevBuf<bf16> ah((size_t)M * ld), al((size_t)M * ld), bh((size_t)N * ld), bl((size_t)N * ld);
-    DHO2G_CUDA(cudaMemcpy(a.p, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
-    DHO2G_CUDA(cudaMemcpy(b.p, B, sizeof(float) * N * K, cudaMemcpyHostToDevice));
+    DHO2G_CUDA(cudaMemcpyAsync(a.p, A, sizeof(float) * M * K, cudaMemcpyHostToDevice, ctx->stream));
+    DHO2G_CUDA(cudaMemcpyAsync(b.p, B, sizeof(float) * N * K, cudaMemcpyHostToDevice, ctx->stream));
     split_rows_kernel<<<cdiv((size_t)M * ld, 256), 256, 0, ctx->stream>>>(a.p, M, K, ld, ah.p, al.p);
     split_rows_kernel<<<cdiv((size_t)N * ld, 256), 256, 0, ctx->stream>>>(b.p, N, K, ld, bh.p, bl.p);
     DHO2G_LAUNCH();
     const int saved = ctx->gemm_backend;
     ctx->gemm_backend = backend;
     gemm3_store(ctx, M, N, K, ah.p, al.p, ld, bh.p, bl.p, ld, c.p, N, 1.0f);
+    ctx->gemm_backend = saved;
+    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+    DHO2G_CUDA(cudaMemcpy(Cout, c.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+  });
+}
+
+// Physical operand for the segmented test: X0 (MN x K0), X1 (MN x K1) row-major logical.
+static GOp test_operand(dho2g_ctx* ctx, int MN, int K0, int K1, int kseg, const float* X0, const float* X1, int mn_major,
+                        DevBuf<bf16>& hi, DevBuf<bf16>& lo) {
+  std::vector<float> h;
+  GOp g{};
+  g.mn_major = mn_major;
+  if (!mn_major) {  // rows mn: [X0 | 0 .. kseg | X1 | 0]
+    const int w = (int)round_up((size_t)(kseg + std::max(K1, 1)), 8);
+    h.assign((size_t)MN * w, 0.f);
+    for (int r = 0; r < MN; ++r) {
+      for (int k = 0; k < K0; ++k) h[(size_t)r * w + k] = X0[(size_t)r * K0 + k];
+      for (int k = 0; k < K1; ++k) h[(size_t)r * w + kseg + k] = X1[(size_t)r * K1 + k];
+    }
+    g.ld = w;
+    g.inner = w;
+    g.outer = MN;
+    g.off_in[0] = 0;
+    g.off_in[1] = kseg;
+  } else {  // rows k: [X0^T | X1^T], halves of MNp
+    const int MNp = (int)round_up((size_t)MN, 8), rows = std::max(K0, K1);
+    const int w = 2 * MNp;
+    h.assign((size_t)rows * w, 0.f);
+    for (int r = 0; r < MN; ++r) {
+      for (int k = 0; k < K0; ++k) h[(size_t)k * w + r] = X0[(size_t)r * K0 + k];
+      for (int k = 0; k < K1; ++k) h[(size_t)k * w + MNp + r] = X1[(size_t)r * K1 + k];
+    }
+    g.ld = w;
+    g.inner = w;
+    g.outer = rows;
+    g.off_in[0] = 0;
+    g.off_in[1] = MNp;
+  }
+  DevBuf<float> f(h.size());
+  hi.alloc(h.size());
+  lo.alloc(h.size());
+  // stream-ordered upload: a pageable cudaMemcpy may return before its DMA lands, and the split
+  // kernel runs on the library's (non-blocking) stream
+  DHO2G_CUDA(cudaMemcpyAsync(f.p, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+  const int rows = (int)(h.size() / g.ld);
+  split_rows_kernel<<<cdiv(h.size(), 256), 256, 0, ctx->stream>>>(f.p, rows, g.ld, g.ld, hi.p, lo.p);
+  DHO2G_LAUNCH();
+  DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+  g.hi = hi.p;
+  g.lo = lo.p;
+  return g;
+}
+
+int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const float* A0, const float* A1,
+                        const float* B0, const float* B1, float* Cout, int backend, int a_mn, int b_mn) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (M <= 0 || N <= 0 || K0 <= 0 || K1 < 0) fail(DHO2G_ARGUMENT, "test_gemm_seg: bad shape");
+    const int kseg = K1 > 0 ? (int)round_up((size_t)K0, 64) : K0;
+    const int K = K1 > 0 ? kseg + K1 : K0;
+    DevBuf<bf16> ah, al, bh, bl;
+    const GOp A = test_operand(ctx, M, K0, K1, kseg, A0, A1, a_mn, ah, al);
+    const GOp B = test_operand(ctx, N, K0, K1, kseg, B0, B1, b_mn, bh, bl);
+    DevBuf<float> c((size_t)M * N);
+    Epi e{};
+    e.mode = EPI_STORE;
+    e.M = M;
+    e.N = N;
+    e.C = c.p;
+    e.ldc = N;
+    e.alpha = 1.0f;
+    const int saved = ctx->gemm_backend;
+    ctx->gemm_backend = backend;
+    try {
+      gemm3x(ctx, M, N, K, K1 > 0 ? kseg : K, A, B, e);
+    } catch (...) {
+      ctx->gemm_backend = saved;
+      throw;
+    }
     ctx->gemm_backend = saved;
     DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
     DHO2G_CUDA(cudaMemcpy(Cout, c.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));

@@ -164,14 +164,47 @@ __global__ void epi_kernel(Epi e, const float* __restrict__ acc, int ldacc, int 
 }
 }  // namespace
 
+// =============================================================================== operand windows
+__host__ __device__ __forceinline__ void gop_coord(const GOp& op, int mn, int k, int kseg, int& in, int& out) {
+  const int seg = k >= kseg ? 1 : 0;
+  const int kk = k - (seg ? kseg : 0);
+  if (op.mn_major) {
+    in = mn + op.off_in[seg];
+    out = kk + op.off_out[seg];
+  } else {
+    in = kk + op.off_in[seg];
+    out = mn + op.off_out[seg];
+  }
+}
+
+GOp gop_k(const bf16* hi, const bf16* lo, int ld, int K, int rows) {
+  GOp g{};
+  g.hi = hi;
+  g.lo = lo;
+  g.ld = ld;
+  g.mn_major = 0;
+  g.inner = K;
+  g.outer = rows;
+  return g;
+}
+
 // =============================================================================== CUDA-core path
 namespace {
 constexpr int ST_BM = 64, ST_BN = 64, ST_BK = 16;
 
-__global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, const bf16* __restrict__ Ahi,
-                                                         const bf16* __restrict__ Alo, int lda,
-                                                         const bf16* __restrict__ Bhi, const bf16* __restrict__ Blo,
-                                                         int ldb, float* __restrict__ C, int ldc) {
+__device__ __forceinline__ void gop_load(const GOp& op, int mn, int MN, int k, int K, int kseg, float& h, float& l) {
+  h = l = 0.f;
+  if (mn >= MN || k >= K) return;
+  int in, out;
+  gop_coord(op, mn, k, kseg, in, out);
+  if (in < 0 || in >= op.inner || out < 0 || out >= op.outer) return;
+  const size_t i = (size_t)out * op.ld + in;
+  h = __bfloat162float(op.hi[i]);
+  l = __bfloat162float(op.lo[i]);
+}
+
+__global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, int kseg, const GOp A, const GOp B,
+                                                         float* __restrict__ C, int ldc) {
   __shared__ float sAh[ST_BK][ST_BM + 4], sAl[ST_BK][ST_BM + 4], sBh[ST_BK][ST_BN + 4], sBl[ST_BK][ST_BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const int m0 = blockIdx.y * ST_BM, n0 = blockIdx.x * ST_BN;
@@ -179,22 +212,8 @@ __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, co
   for (int k0 = 0; k0 < K; k0 += ST_BK) {
     for (int e = threadIdx.x; e < ST_BM * ST_BK; e += 256) {
       const int r = e / ST_BK, kk = e % ST_BK;
-      const int gm = m0 + r, gk = k0 + kk;
-      float ah = 0.f, al = 0.f;
-      if (gm < M && gk < K) {
-        ah = __bfloat162float(Ahi[(size_t)gm * lda + gk]);
-        al = __bfloat162float(Alo[(size_t)gm * lda + gk]);
-      }
-      sAh[kk][r] = ah;
-      sAl[kk][r] = al;
-      const int gn = n0 + r;
-      float bh = 0.f, bl = 0.f;
-      if (gn < N && gk < K) {
-        bh = __bfloat162float(Bhi[(size_t)gn * ldb + gk]);
-        bl = __bfloat162float(Blo[(size_t)gn * ldb + gk]);
-      }
-      sBh[kk][r] = bh;
-      sBl[kk][r] = bl;
+      gop_load(A, m0 + r, M, k0 + kk, K, kseg, sAh[kk][r], sAl[kk][r]);
+      gop_load(B, n0 + r, N, k0 + kk, K, kseg, sBh[kk][r], sBl[kk][r]);
     }
     __syncthreads();
 #pragma unroll
@@ -231,12 +250,11 @@ __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, co
 }
 }  // namespace
 
-void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-                const bf16* Blo, int ldb, const Epi& e) {
+static void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   ctx->simt_ws.ensure((size_t)M * N + 16);
   float* acc = ctx->simt_ws.p;
   dim3 grid(cdiv(N, ST_BN), cdiv(M, ST_BM));
-  gemm3_simt_kernel<<<grid, 256, 0, ctx->stream>>>(M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, acc, N);
+  gemm3_simt_kernel<<<grid, 256, 0, ctx->stream>>>(M, N, K, kseg, A, B, acc, N);
   DHO2G_LAUNCH();
   const int rows_pad = e.mode == EPI_STORE ? M : std::max(M, e.Bp);
   dim3 eb(8, 16);
@@ -245,24 +263,32 @@ void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16
   DHO2G_LAUNCH();
 }
 
-// =============================================================================== tcgen05 path
+// =============================================================================== tcgen05 common
 namespace tc {
 
-constexpr int BM = 128;  // UMMA_M (cta_group::1): TMEM lane i <-> output row i
-constexpr int BN = 128;  // UMMA_N
-constexpr int BK = 64;   // one 128-byte swizzle row of bf16
+constexpr int BK = 64;   // one 128-byte swizzle row of bf16 (K-major) / 64 K-rows per stage (MN-major)
 constexpr int UK = 16;   // K per tcgen05.mma kind::f16
-constexpr int STAGES = 3;
 constexpr int ACC = 2;   // TMEM accumulator buffers
-constexpr uint32_t A_BYTES = BM * BK * 2;
-constexpr uint32_t B_BYTES = BN * BK * 2;
-constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr uint32_t OP_BYTES = 128 * BK * 2;      // one 128-row (hi or lo) operand tile
 constexpr uint32_t EPI_SMEM = 8 * 32 * 17 * 4;  // per epilogue warp: 32 x 16 restaging block (+1 pad)
-constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
-constexpr uint32_t TMEM_COLS = ACC * BN;
-// instruction descriptor, kind::f16: D=F32 [4,6), A=BF16 [7,10), B=BF16 [10,13), K-major both,
+// instruction descriptor, kind::f16: D=F32 [4,6), A=BF16 [7,10), B=BF16 [10,13), A/B major [15], [16],
 // N>>3 [17,23), M>>4 [24,29)
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn, bool bmn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((amn ? 1u : 0u) << 15) | ((bmn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+struct OpOff {  // per-segment coordinate offsets of one operand (GOp minus pointers / extents)
+  int off_in[2], off_out[2];
+};
+inline OpOff op_off(const GOp& g) {
+  OpOff o;
+  for (int s = 0; s < 2; ++s) {
+    o.off_in[s] = g.off_in[s];
+    o.off_out[s] = g.off_out[s];
+  }
+  return o;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -288,39 +314,57 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// 2D TMA load; PAIR: cta_group::2 form whose completion is signalled on the leader CTA's barrier
+template <bool PAIR>
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
+  if (PAIR)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, K-major SWIZZLE_128B canonical layout (8 rows x 128 B atoms):
-// start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major: 1), SBO>>4 [32,46) = 1024 B,
-// version [46,48) = 1 (sm_100), layout [61,64) = 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// UMMA shared-memory descriptors (SWIZZLE_128B; version 1 @46, layout 2 @61):
+//  K-major : 8-row x 128 B atoms stacked along M/N: LBO unused (1), SBO = 1024 B; K step = +32 B.
+//  MN-major: 64-element x 8-K-row atoms; LBO = 8 KB (next 64 M/N, one TMA box of 64 K-rows),
+//            SBO = 1024 B (next 8 K-rows); K step of 16 = +2 KB.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)(lbo >> 4) << 16;
+  d |= (uint64_t)(sbo >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
 }
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t tile_base, int kk) {
+  return MN ? sw128_desc(tile_base + kk * 2048, 8192, 1024) : sw128_desc(tile_base + kk * 32, 16, 1024);
+}
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+// Stage one 128-row (M or N) x 64-K operand tile (hi or lo) into smem through its map.
+template <bool MN, bool PAIR>
+__device__ __forceinline__ void load_op(uint8_t* dst, const CUtensorMap* map, const OpOff& o, int mn0, int kb,
+                                        int kseg, uint64_t* bar) {
+  const int k = kb * BK;
+  const int seg = k >= kseg ? 1 : 0;
+  const int kk = k - (seg ? kseg : 0);
+  if (MN) {  // two 64(MN) x 64(K) boxes
+    tma_load_2d<PAIR>(dst, map, mn0 + o.off_in[seg], kk + o.off_out[seg], bar);
+    tma_load_2d<PAIR>(dst + 8192, map, mn0 + 64 + o.off_in[seg], kk + o.off_out[seg], bar);
+  } else {  // one 64(K) x 128(MN) box
+    tma_load_2d<PAIR>(dst, map, kk + o.off_in[seg], mn0 + o.off_out[seg], bar);
+  }
 }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -342,8 +386,52 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                     uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * sizeof(bf16)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn);
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(DHO2G_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" + std::to_string(inner) +
+                         " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld));
+  return m;
+}
+// hi / lo maps of one operand: K-major boxes 64(K) x 128 rows, MN-major boxes 64(MN) x 64(K)
+void op_maps(void* encode_fn, const GOp& g, CUtensorMap& mh, CUtensorMap& ml) {
+  const uint32_t bi = 64, bo = g.mn_major ? 64 : 128;
+  mh = make_map(encode_fn, g.hi, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
+  ml = make_map(encode_fn, g.lo, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
+}
+void check_op(const GOp& g, const char* what) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if ((g.ld % 8) || !al16(g.hi) || !al16(g.lo))
+    fail(DHO2G_ARGUMENT, std::string("gemm3: operand ") + what + " must be 16-byte aligned with ld % 8 == 0");
+  if (g.inner <= 0 || g.outer <= 0) fail(DHO2G_ARGUMENT, std::string("gemm3: empty operand window ") + what);
+}
+
+}  // namespace tc
+
+// =============================================================================== single-CTA kernel
+// One CTA per SM walks a static work list of (split, tile) units (128 x 128 tiles). A TMA producer
+// warp streams A/B (hi, lo) tiles through a 3-stage mbarrier ring; one elected thread issues
+// tcgen05.mma (M = 128, N = 128) into one of two TMEM accumulators; 8 epilogue warps drain the other
+// (epilogue of unit i overlaps the MMAs of unit i+1). Small-M GEMMs are split along K; split
+// partials are combined in a fixed order through a global workspace + release/acquire flags.
+namespace tc1 {
+using namespace tc;
+constexpr int BM = 128, BN = 128, STAGES = 3;
+constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
+constexpr uint32_t TMEM_COLS = ACC * BN;
+
 struct Sched {
-  int mt, nt, tiles, splits, units, nkb;  // nkb: k-blocks total
+  int mt, nt, tiles, splits, units, nkb, kseg;  // nkb: k-blocks total
   __device__ __forceinline__ void unit(int u, int& m0, int& n0, int& split, int& tile, int& kb0, int& kb1) const {
     split = u / tiles;
     tile = u - split * tiles;
@@ -354,11 +442,12 @@ struct Sched {
   }
 };
 
+template <bool AMN, bool BMN>
 __global__ void __launch_bounds__(384, 1)
     gemm3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Sched sc,
-                    const __grid_constant__ Epi e, float* __restrict__ ws, unsigned* __restrict__ flags,
-                    unsigned epoch) {
+                    OpOff oa, OpOff ob, const __grid_constant__ Epi e, float* __restrict__ ws,
+                    unsigned* __restrict__ flags, unsigned epoch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -407,14 +496,15 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(st, &mAh, kb * BK, m0, &full[s]);
-        tma_load_2d(st + A_BYTES, &mAl, kb * BK, m0, &full[s]);
-        tma_load_2d(st + 2 * A_BYTES, &mBh, kb * BK, n0, &full[s]);
-        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &mBl, kb * BK, n0, &full[s]);
+        load_op<AMN, false>(st, &mAh, oa, m0, kb, sc.kseg, &full[s]);
+        load_op<AMN, false>(st + OP_BYTES, &mAl, oa, m0, kb, sc.kseg, &full[s]);
+        load_op<BMN, false>(st + 2 * OP_BYTES, &mBh, ob, n0, kb, sc.kseg, &full[s]);
+        load_op<BMN, false>(st + 3 * OP_BYTES, &mBl, ob, n0, kb, sc.kseg, &full[s]);
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread), accumulator double-buffered in TMEM
+    constexpr uint32_t ID = idesc(BM, BN, AMN, BMN);
     uint32_t it = 0, uc = 0;
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
@@ -430,17 +520,28 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
-          const uint64_t dAh = sw128_desc(base + kk * 32);
-          const uint64_t dAl = sw128_desc(base + A_BYTES + kk * 32);
-          const uint64_t dBh = sw128_desc(base + 2 * A_BYTES + kk * 32);
-          const uint64_t dBl = sw128_desc(base + 2 * A_BYTES + B_BYTES + kk * 32);
-          mma_bf16(acc_addr, dAh, dBh, (kb > kb0 || kk > 0) ? 1u : 0u);
-          mma_bf16(acc_addr, dAh, dBl, 1u);
-          mma_bf16(acc_addr, dAl, dBh, 1u);
+          const uint64_t dAh = op_desc<AMN>(base, kk);
+          const uint64_t dAl = op_desc<AMN>(base + OP_BYTES, kk);
+          const uint64_t dBh = op_desc<BMN>(base + 2 * OP_BYTES, kk);
+          const uint64_t dBl = op_desc<BMN>(base + 3 * OP_BYTES, kk);
+          const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
+              "l"(dAh), "l"(dBh), "r"(ID), "r"(first));
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(acc_addr), "l"(dAh), "l"(dBl),
+                       "r"(ID));
+          asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(acc_addr), "l"(dAl), "l"(dBh),
+                       "r"(ID));
         }
-        mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        // frees the stage once these MMAs have read it
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[s]))
+                     : "memory");
       }
-      mma_commit(&tfull[ab]);  // accumulator ready for the epilogue
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&tfull[ab]))
+                   : "memory");  // accumulator ready for the epilogue
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps: TMEM -> registers -> (split-K combine) -> fused epilogue
@@ -455,13 +556,11 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
-      const int r_local = ew * 32 + lane;
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
       // split-K partial, private layout [warp slot][chunk][q][lane][4] so every float4 access of a
       // warp is one contiguous 512 B segment
       float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)(ew + 4 * chalf) * (32 * BN / 2) + (size_t)lane * 4
                         : nullptr;
-      (void)r_local;
       const bool last = split == sc.splits - 1;
       if (split > 0) {  // wait for the previous split of this tile (fixed combine order)
         if (threadIdx.x == 128) {
@@ -509,22 +608,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_outer) {
-  CUtensorMap m;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * sizeof(bf16)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn);
-  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    fail(DHO2G_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" + std::to_string(inner) +
-                         " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld));
-  return m;
-}
-
 // split-K factor that best fills the persistent grid (work quantization), >= 8 k-blocks per split
 int pick_splits(int tiles, int nkb, int sms) {
   // Split only when whole-tile scheduling leaves the persistent grid badly quantised (the HVP GEMMs at
@@ -549,25 +632,27 @@ int pick_splits(int tiles, int nkb, int sms) {
   return best;
 }
 
-}  // namespace tc
-
-int gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-             const bf16* Blo, int ldb, const Epi& e) {
-  using namespace tc;
-  if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  if ((lda % 8) || (ldb % 8) || (reinterpret_cast<uintptr_t>(Ahi) & 15) || (reinterpret_cast<uintptr_t>(Alo) & 15) ||
-      (reinterpret_cast<uintptr_t>(Bhi) & 15) || (reinterpret_cast<uintptr_t>(Blo) & 15))
-    fail(DHO2G_ARGUMENT, "gemm3_tc: operands must be 16-byte aligned with ld % 8 == 0");
+template <bool AMN, bool BMN>
+void launch(dho2g_ctx* ctx, const CUtensorMap* maps, const Sched& sc, const OpOff& oa, const OpOff& ob, const Epi& e,
+            float* ws, unsigned* flags, unsigned epoch) {
   static bool attr_set = false;
   if (!attr_set) {
-    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
+  const int grid = std::min(sc.units, ctx->sm_count);
+  gemm3_tc_kernel<AMN, BMN><<<grid, 384, SMEM, ctx->stream>>>(maps[0], maps[1], maps[2], maps[3], sc, oa, ob, e, ws,
+                                                              flags, epoch);
+  DHO2G_LAUNCH();
+}
+
+int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   Sched sc;
   sc.mt = (int)cdiv(M, BM);
   sc.nt = (int)cdiv(N, BN);
   sc.tiles = sc.mt * sc.nt;
   sc.nkb = (int)cdiv(K, BK);
+  sc.kseg = kseg;
   sc.splits = ctx->gemm_splits > 0 ? std::min(ctx->gemm_splits, std::max(1, sc.nkb))
                                    : pick_splits(sc.tiles, sc.nkb, ctx->sm_count);
   sc.units = sc.tiles * sc.splits;
@@ -585,35 +670,377 @@ int gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* A
       ctx->gemm_epoch = epoch = 1;
     }
   }
-  const CUtensorMap mAh = make_map(ctx->encode_fn, Ahi, K, M, lda, BM);
-  const CUtensorMap mAl = make_map(ctx->encode_fn, Alo, K, M, lda, BM);
-  const CUtensorMap mBh = make_map(ctx->encode_fn, Bhi, K, N, ldb, BN);
-  const CUtensorMap mBl = make_map(ctx->encode_fn, Blo, K, N, ldb, BN);
-  const int grid = std::min(sc.units, ctx->sm_count);
-  gemm3_tc_kernel<<<grid, 384, SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, sc, e, ws, flags, epoch);
-  DHO2G_LAUNCH();
+  CUtensorMap maps[4];
+  op_maps(ctx->encode_fn, A, maps[0], maps[1]);
+  op_maps(ctx->encode_fn, B, maps[2], maps[3]);
+  const OpOff oa = op_off(A), ob = op_off(B);
+  if (A.mn_major && B.mn_major) launch<true, true>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else if (A.mn_major) launch<true, false>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else if (B.mn_major) launch<false, true>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else launch<false, false>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
   return sc.splits;
 }
 
-void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-           const bf16* Blo, int ldb, const Epi& e) {
+}  // namespace tc1
+
+// =============================================================================== CTA-pair kernel
+// cta_group::2: a cluster of two CTAs (one TPC) computes a 256 x Nt pair tile (Nt <= 256). CTA r
+// stages rows [m0 + 128 r, +128) of A and rows [n0 + r Nt/2, +Nt/2) of B; the leader (rank 0)
+// issues tcgen05.mma.cta_group::2 (M = 256, N = Nt) over both CTAs' shared memory, each CTA's TMEM
+// receiving its 128 output rows. Per SM this halves the shared-memory operand reads and the L2->SM
+// operand traffic per flop relative to the single-CTA 128 x 128 kernel.
+//
+// Work is distributed stream-K: the (tile, k-block) iteration space is cut into `workers` equal
+// contiguous ranges, one per pair. A range starting inside a tile begins with a non-head segment,
+// whose fp32 partial goes to the pair's workspace slot (flag = ready); the head segment's owner
+// (which processes it last) adds the later segments' partials in segment order and runs the fused
+// epilogue. The combine order is fixed by the schedule, so results are deterministic.
+namespace tc2 {
+using namespace tc;
+
+constexpr int BM = 128;   // output rows per CTA (pair tile 256)
+constexpr int BNT = 256;  // pair tile columns (UMMA_N, max)
+constexpr int STAGES = 3;
+constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;  // A hi/lo (128 rows) + B hi/lo (128 = BNT/2 rows)
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
+constexpr uint32_t TMEM_COLS = ACC * BNT;  // 512: the whole TMEM of the SM
+constexpr uint32_t PART_FLOATS = BM * BNT;  // one CTA's partial tile
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t* bar) {  // arrive on this offset's barrier in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+struct Work {
+  int nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
+  long long total;                        // tiles * nkb
+  __device__ __forceinline__ long long begin(int w) const { return total * w / workers; }
+};
+struct Seg {
+  int tile, k0, k1;
+};
+__device__ __forceinline__ bool next_seg(const Work& wk, long long& a, long long end, Seg& s) {
+  if (a >= end) return false;
+  s.tile = (int)(a / wk.nkb);
+  s.k0 = (int)(a - (long long)s.tile * wk.nkb);
+  s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
+  a += s.k1 - s.k0;
+  return true;
+}
+__device__ __forceinline__ int tile_cols(const Work& wk, int n0) {  // MMA N of a tile (<= 256)
+  const int c = wk.N - n0;
+  return c >= BNT ? BNT : ((c + wk.nround - 1) / wk.nround) * wk.nround;
+}
+
+template <bool AMN, bool BMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    gemm3_tc2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Work wk,
+                     OpOff oa, OpOff ob, const __grid_constant__ Epi e, float* __restrict__ ws,
+                     unsigned* __restrict__ flags, unsigned ready) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int worker = blockIdx.x >> 1;
+  const long long wbeg = wk.begin(worker), wend = wk.begin(worker + 1);
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+#pragma unroll
+    for (int a = 0; a < ACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (leader copy is the one used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mAl)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBl)) : "memory");
+  }
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs): this CTA's halves of A and B into its ring
+    uint32_t it = 0;
+    long long a = wbeg;
+    Seg sg;
+    while (next_seg(wk, a, wend, sg)) {
+      const int m0 = (sg.tile / wk.nt) * 256 + (int)rank * BM, n0 = (sg.tile % wk.nt) * BNT;
+      const int nb = n0 + (int)rank * (tile_cols(wk, n0) / 2);
+      for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+        load_op<AMN, true>(st, &mAh, oa, m0, kb, wk.kseg, &full[s]);
+        load_op<AMN, true>(st + OP_BYTES, &mAl, oa, m0, kb, wk.kseg, &full[s]);
+        load_op<BMN, true>(st + 2 * OP_BYTES, &mBh, ob, nb, kb, wk.kseg, &full[s]);
+        load_op<BMN, true>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader CTA only)
+    uint32_t it = 0, uc = 0;
+    long long a = wbeg;
+    Seg sg;
+    while (next_seg(wk, a, wend, sg)) {
+      const int n0 = (sg.tile % wk.nt) * BNT;
+      const uint32_t ID = idesc(256, tile_cols(wk, n0), AMN, BMN);
+      const uint32_t ab = uc % ACC;
+      mbar_wait_cluster(&tempty[ab], ((uc / ACC) & 1) ^ 1);
+      fence_after();
+      const uint32_t acc_addr = tmem + ab * BNT;
+      for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        fence_after();
+        const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / UK; ++kk) {
+          const uint64_t dAh = op_desc<AMN>(base, kk);
+          const uint64_t dAl = op_desc<AMN>(base + OP_BYTES, kk);
+          const uint64_t dBh = op_desc<BMN>(base + 2 * OP_BYTES, kk);
+          const uint64_t dBl = op_desc<BMN>(base + 3 * OP_BYTES, kk);
+          const uint32_t first = (kb > sg.k0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
+              "l"(dAh), "l"(dBh), "r"(ID), "r"(first));
+          asm volatile("tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(acc_addr), "l"(dAh), "l"(dBl),
+                       "r"(ID));
+          asm volatile("tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 1;" ::"r"(acc_addr), "l"(dAl), "l"(dBh),
+                       "r"(ID));
+        }
+        commit2(&empty[s]);
+      }
+      commit2(&tfull[ab]);
+      ++uc;
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps (both CTAs): 8 warps = 4 TMEM lane quadrants x 2 column halves
+    const int ew = warp & 3;
+    const int chalf = (warp - 4) >> 2;
+    float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
+    const size_t slot_off = (size_t)(ew + 4 * chalf) * (32 * BNT / 2) + (size_t)lane * 4;
+    uint32_t uc = 0;
+    long long a = wbeg;
+    Seg sg;
+    while (next_seg(wk, a, wend, sg)) {
+      const int m0 = (sg.tile / wk.nt) * 256 + (int)rank * BM, n0 = (sg.tile % wk.nt) * BNT;
+      const int ncols = tile_cols(wk, n0);
+      const uint32_t ab = uc % ACC;
+      mbar_wait(&tfull[ab], (uc / ACC) & 1);
+      fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BNT;
+      if (sg.k0 != 0) {
+        // non-head segment (first of this worker): publish the raw partial
+        float* p = ws + (size_t)(worker * 2 + rank) * PART_FLOATS + slot_off;
+#pragma unroll 1
+        for (int c0 = chalf * (BNT / 2); c0 < (chalf + 1) * (BNT / 2); c0 += 16) {
+          if (c0 >= ncols) break;
+          float v[16];
+          tmem_ld16(tbase + (uint32_t)c0, v);
+          float* q = p + (size_t)((c0 - chalf * (BNT / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            __stcg(reinterpret_cast<float4*>(q + j * 128), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&tempty[ab]);
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) st_release(flags + worker * 2 + rank, ready);
+      } else {
+        // head segment: later segments of this tile are the first segments of workers worker+1, ...
+        const long long tile_end = (long long)(sg.tile + 1) * wk.nkb;
+        int wlast = worker;
+        if (sg.k1 < wk.nkb) {
+          while (wlast + 1 < wk.workers && wk.begin(wlast + 1) < tile_end) ++wlast;
+          if (threadIdx.x == 128)
+            for (int w2 = worker + 1; w2 <= wlast; ++w2)
+              while (ld_acquire(flags + w2 * 2 + rank) != ready) __nanosleep(64);
+          epi_bar();
+        }
+#pragma unroll 1
+        for (int c0 = chalf * (BNT / 2); c0 < (chalf + 1) * (BNT / 2); c0 += 16) {
+          if (c0 >= ncols) break;
+          float v[16];
+          tmem_ld16(tbase + (uint32_t)c0, v);
+          for (int w2 = worker + 1; w2 <= wlast; ++w2) {
+            const float* q = ws + (size_t)(w2 * 2 + rank) * PART_FLOATS + slot_off +
+                             (size_t)((c0 - chalf * (BNT / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
+              v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+            }
+          }
+          epi_warp16(e, m0 + ew * 32, n0 + c0, v, esm);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&tempty[ab]);
+      }
+      ++uc;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+template <bool AMN, bool BMN>
+int max_pairs(dho2g_ctx* ctx) {
+  static int pairs = 0;
+  if (pairs > 0) return pairs;
+  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * (ctx->sm_count / 2));
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN>, &cfg));
+  if (clusters < 1) fail(DHO2G_CUDA, "gemm3_tc2: no CTA pair can be resident");
+  pairs = clusters;
+  return pairs;
+}
+
+template <bool AMN, bool BMN>
+int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
+  const int pairs = max_pairs<AMN, BMN>(ctx);
+  // every worker gets >= 4 k-blocks (a segment shorter than that is mostly fixup traffic)
+  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, wk.total / 4));
+  ctx->gemm_ws.ensure((size_t)wk.workers * 2 * PART_FLOATS);
+  ctx->gemm_flags.ensure((size_t)wk.workers * 2 + 16);
+  unsigned epoch = ++ctx->gemm_epoch;
+  if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
+    DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
+    ctx->gemm_epoch = epoch = 1;
+  }
+  gemm3_tc2_kernel<AMN, BMN><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
+      maps[0], maps[1], maps[2], maps[3], wk, oa, ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u);
+  DHO2G_LAUNCH();
+  return wk.workers;
+}
+
+int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
+  Work wk;
+  const int mt = (int)cdiv(M, 256);
+  wk.nt = (int)cdiv(N, BNT);
+  wk.nkb = (int)cdiv(K, BK);
+  wk.N = N;
+  wk.kseg = kseg;
+  wk.nround = B.mn_major ? 128 : 16;
+  wk.total = (long long)mt * wk.nt * wk.nkb;
+  wk.workers = 1;
+  CUtensorMap maps[4];
+  op_maps(ctx->encode_fn, A, maps[0], maps[1]);
+  op_maps(ctx->encode_fn, B, maps[2], maps[3]);
+  const OpOff oa = op_off(A), ob = op_off(B);
+  if (A.mn_major && B.mn_major) return launch<true, true>(ctx, maps, wk, oa, ob, e);
+  if (A.mn_major) return launch<true, false>(ctx, maps, wk, oa, ob, e);
+  if (B.mn_major) return launch<false, true>(ctx, maps, wk, oa, ob, e);
+  return launch<false, false>(ctx, maps, wk, oa, ob, e);
+}
+
+}  // namespace tc2
+
+// =============================================================================== dispatch
+void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   if (M <= 0 || N <= 0) return;
   if (K <= 0) fail(DHO2G_ARGUMENT, "gemm3: empty reduction dimension");
+  if (kseg < K && (kseg <= 0 || kseg % tc::BK)) fail(DHO2G_ARGUMENT, "gemm3: K segment boundary must be a multiple of 64");
+  tc::check_op(A, "A");
+  tc::check_op(B, "B");
   ctx->bump("gemm_calls", 1);
   ctx->bump("gemm_flops_issued", 3.0 * 2.0 * double(M) * double(N) * double(K));
   const int slot = ctx->kt_begin();
   int splits = 1;
-  if (ctx->gemm_backend == 1)
-    gemm3_simt(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
-  else
-    splits = gemm3_tc(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
-  if (slot >= 0) {  // name: backend:epilogue(+R)/splits, aggregated by prefix in the bench
+  bool pair = false;
+  if (ctx->gemm_backend == 1) {
+    gemm3_simt(ctx, M, N, K, kseg, A, B, e);
+  } else {
+    if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    // CTA pairs (256-row tiles) unless the GEMM is too short in M to fill them
+    pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 128);
+    splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e) : tc1::run(ctx, M, N, K, kseg, A, B, e);
+  }
+  if (slot >= 0) {  // name: backend:epilogue(+R)[operand majors]/(splits | pair), aggregated by prefix in the bench
     static const char* modes[] = {"store", "fwd", "fwdout", "bwd"};
-    char name[64];
-    std::snprintf(name, sizeof(name), "%s:%s%s/s%d", ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05",
-                  modes[e.mode], e.do1 ? "R" : "", splits);
+    char lay[8] = "";
+    if (A.mn_major || B.mn_major) std::snprintf(lay, sizeof(lay), "[%c%c]", A.mn_major ? 'm' : 'k', B.mn_major ? 'm' : 'k');
+    char name[80];
+    if (pair)
+      std::snprintf(name, sizeof(name), "gemm3_tcgen05:%s%s%s/pair", modes[e.mode], e.do1 ? "R" : "", lay);
+    else
+      std::snprintf(name, sizeof(name), "%s:%s%s%s/s%d", ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05",
+                    modes[e.mode], e.do1 ? "R" : "", lay, splits);
     ctx->kt_end(slot, name, 2.0 * double(M) * double(N) * double(K));
   }
+}
+
+void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
+           const bf16* Blo, int ldb, const Epi& e) {
+  gemm3x(ctx, M, N, K, K, gop_k(Ahi, Alo, lda, K, M), gop_k(Bhi, Blo, ldb, K, N), e);
 }
 
 void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,

@@ -37,7 +37,9 @@ struct dho2g_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   int gemm_backend = 0;  // 0 tcgen05, 1 CUDA-core reference kernel
-  int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs
+  int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
+  int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
+  int gemm_pairs = 0;    // co-resident CTA pairs of the pair kernel (queried once)
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
@@ -162,15 +164,29 @@ struct Epi {
   bf16* Tl;
   int ldT, Bp, hT;
 };
+// One GEMM operand: a (hi, lo) bf16 pair buffer read through a TMA-style window. K-major: rows are
+// the M (or N) index, K contiguous; MN-major: rows are the K index, M (or N) contiguous. The K range
+// may be two segments, [0, kseg) and [kseg, K), read at different offsets of the same buffer (the
+// MLP's [x | rx] concatenations). Logical element (mn, k): seg = k >= kseg, kk = k - seg * kseg;
+//   K-major : inner = kk + off_in[seg], outer = mn + off_out[seg]
+//   MN-major: inner = mn + off_in[seg], outer = kk + off_out[seg]
+// and address outer * ld + inner; coordinates outside [0, inner) x [0, outer) read as zero.
+struct GOp {
+  const bf16* hi;
+  const bf16* lo;
+  int ld;
+  int mn_major;
+  int inner, outer;
+  int off_in[2], off_out[2];
+};
+GOp gop_k(const bf16* hi, const bf16* lo, int ld, int K, int rows);  // plain K-major, one segment
 // acc = A[M x K] B[N x K]^T in split-BF16x3 (hi*hi + hi*lo + lo*hi), then the epilogue.
+// kseg: segment boundary (a multiple of 64) or >= K for a single segment.
+void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e);
 void gemm3(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-           const bf16* Blo, int ldb, const Epi& e);
+           const bf16* Blo, int ldb, const Epi& e);  // both K-major
 void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
                  const bf16* Blo, int ldb, float* C, int ldc, float alpha, float* bias_out = nullptr);
-void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-                const bf16* Blo, int ldb, const Epi& e);
-int gemm3_tc(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf16* Alo, int lda, const bf16* Bhi,
-             const bf16* Blo, int ldb, const Epi& e);  // returns the split-K factor used
 
 // fp32 elementwise helpers (update.cu)
 void dev_copy_f64_to_f32(cudaStream_t s, const double* src, float* dst, size_t n);

@@ -415,7 +415,26 @@ __global__ void __launch_bounds__(256) ritz_kernel(const float* __restrict__ D, 
     float acc[RC];
 #pragma unroll
     for (int c = 0; c < RC; ++c) acc[c] = 0.f;
-    for (int j = 0; j < me; ++j) {
+    // basis columns in groups of 8: all 8 loads in flight before the FMAs (one latency per group)
+    int j = 0;
+    for (; j + 8 <= me; j += 8) {
+      float x[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) x[t] = __ldg(D + (size_t)(j + t) * ldd + row);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float4* u4 = reinterpret_cast<const float4*>(us + (j + t) * RC);
+#pragma unroll
+        for (int q = 0; q < RC / 4; ++q) {
+          const float4 u = u4[q];
+          acc[4 * q] = fmaf(x[t], u.x, acc[4 * q]);
+          acc[4 * q + 1] = fmaf(x[t], u.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = fmaf(x[t], u.z, acc[4 * q + 2]);
+          acc[4 * q + 3] = fmaf(x[t], u.w, acc[4 * q + 3]);
+        }
+      }
+    }
+    for (; j < me; ++j) {
       const float x = __ldg(D + (size_t)j * ldd + row);
       const float4* u4 = reinterpret_cast<const float4*>(us + j * RC);
 #pragma unroll
@@ -680,9 +699,12 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
     DHO2G_CUDA(cudaFuncSetAttribute(tql2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int threads = (int)std::min<size_t>(1024, round_up((size_t)me, 32));
   const int kx = ctx->kt_begin();
+  const int kq = ctx->kt_begin();
   tql2_kernel<<<1, threads, smem, st>>>(lz->st.p, me, (int)k, (int)l, Z.p, U.p, ese->ev_dev.p, evall.p, status.p);
   DHO2G_LAUNCH();
+  ctx->kt_end(kq, "extract.tql2", 0.0);
   ese->V.ensure(ese->ldv * r);  // padded rows stay zero (Ritz writes rows < rows only)
+  const int kr = ctx->kt_begin();
   for (int c0 = 0; c0 < r; c0 += RC) {
     const size_t sm = (size_t)me * RC * sizeof(float);
     if (sm > 48 * 1024)
@@ -691,6 +713,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
                                                                   lz->rows);
     DHO2G_LAUNCH();
   }
+  ctx->kt_end(kr, "extract.ritz", 4.0 * (double)lz->rows * (double)(me + r));
   DevBuf<double>& am = lz->xam;
   DevBuf<double>& amall = lz->xamall;
   am.ensure((size_t)3 * r);
@@ -700,9 +723,11 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
     const size_t seg = cdiv(std::max<size_t>(lz->rows, 1), (size_t)nblk);
     DevBuf<double>& part = lz->xpart;
     part.ensure((size_t)3 * r * nblk);
+    const int ka = ctx->kt_begin();
     col_argmax_kernel<<<dim3(nblk, r), kArgThreads, 0, st>>>(ese->V.p, ese->ldv, lz->rows, lz->begin, seg, part.p);
     col_argmax_final_kernel<<<r, 32, 0, st>>>(part.p, nblk, am.p);
     DHO2G_LAUNCH();
+    ctx->kt_end(ka, "extract.argmax", 4.0 * (double)lz->rows * (double)r);
   }
   // tql2 + Ritz (reads D[:, :m_eff], writes V_hat) + argmax (reads V_hat): algorithmic bytes
   ctx->kt_end(kx, "extract_ese", 4.0 * (double)lz->rows * (double)(me + 2 * r));

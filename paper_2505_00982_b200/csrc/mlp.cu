@@ -269,6 +269,30 @@ __global__ void ones_row_kernel(bf16* __restrict__ hi, bf16* __restrict__ lo, in
   lo[i] = __float2bfloat16_rn(0.f);
 }
 
+// Bias gradient as a row sum of the weight GEMM's A operand pair: out[o] = alpha * sum_k (hi + lo)[o][k]
+// over k < K (K % 8 == 0, rows 16-byte aligned). One warp per row, fp64 accumulation, fixed order.
+__global__ void rowsum_pairs_kernel(const bf16* __restrict__ hi, const bf16* __restrict__ lo, int ld, int rows, int K,
+                                    float alpha, float* __restrict__ out) {
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (o >= rows) return;
+  const uint4* ph = reinterpret_cast<const uint4*>(hi + (size_t)o * ld);
+  const uint4* pl = reinterpret_cast<const uint4*>(lo + (size_t)o * ld);
+  double acc = 0.0;
+#pragma unroll 4
+  for (int i = lane; i < K / 8; i += 32) {
+    const uint4 a = __ldg(ph + i), b = __ldg(pl + i);
+    const bf16* ha = reinterpret_cast<const bf16*>(&a);
+    const bf16* hb = reinterpret_cast<const bf16*>(&b);
+    float f = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f += __bfloat162float(ha[j]) + __bfloat162float(hb[j]);
+    acc += (double)f;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[o] = (float)(alpha * acc);
+}
+
 // label gather
 __global__ void gather_labels_kernel(int B, const float* __restrict__ y, const int64_t* __restrict__ idx,
                                      float* __restrict__ out) {
@@ -406,6 +430,13 @@ static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool
 // do1: R-deltas (RU GEMMs + fused R-epilogue) and the Hessian blocks into `out`. The weight-block
 // GEMMs take the bias column from the ones row appended to the transposed activations
 // (N = in + 1: column `in` = sum_b rd (or d), routed to out[b_off + o]).
+static void bias_rowsum(dho2g_ctx* ctx, const bf16* hi, const bf16* lo, int ld, int rows, int K, float* out) {
+  const int slot = ctx->kt_begin();
+  rowsum_pairs_kernel<<<cdiv(rows, 8), 256, 0, ctx->stream>>>(hi, lo, ld, rows, K, 1.0f, out);
+  DHO2G_LAUNCH();
+  ctx->kt_end(slot, "bias_rowsum", 4.0 * rows * (double)K);  // algorithmic bytes: hi + lo
+}
+
 static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, bool wgrad) {
   dho2g_ctx* ctx = m->ctx;
   const int L = m->L;
@@ -414,12 +445,17 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   for (int t = L - 1; t >= 0; --t) {
     const LayerDesc& ld = m->layers[t];
     const int j = t + 1;
-    if (do1)  // hvW = [RD^T | D^T] [A^T | RA^T]^T ; hv_b = sum_b rd (oracle.cpp:606-613)
-      gemm3_store(ctx, ld.out, ld.in + 1, t == 0 ? Bp : 2 * Bp, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p,
-                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f, out + ld.b_off);
-    else if (wgrad)  // gW = D^T A ; g_b = sum_b d (oracle.cpp:497-504)
-      gemm3_store(ctx, ld.out, ld.in + 1, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p,
-                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f, out + ld.b_off);
+    // weight block by GEMM; the bias block (sum over the batch of the A operand's first half) by a
+    // row sum, which keeps the GEMM's N a multiple of the tile width
+    if (do1) {  // hvW = [RD^T | D^T] [A^T | RA^T]^T ; hv_b = sum_b rd (oracle.cpp:606-613)
+      gemm3_store(ctx, ld.out, ld.in, t == 0 ? Bp : 2 * Bp, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, m->ART_hi[t].p,
+                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f);
+      bias_rowsum(ctx, m->DRT_hi[j].p, m->DRT_lo[j].p, ldT, ld.out, Bp, out + ld.b_off);
+    } else if (wgrad) {  // gW = D^T A ; g_b = sum_b d (oracle.cpp:497-504)
+      gemm3_store(ctx, ld.out, ld.in, Bp, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, m->ART_hi[t].p,
+                  m->ART_lo[t].p, ldT, out + ld.w_off, ld.in, 1.0f);
+      bias_rowsum(ctx, m->DRT_hi[j].p + Bp, m->DRT_lo[j].p + Bp, ldT, ld.out, Bp, out + ld.b_off);
+    }
     if (t == 0) continue;
     const int lda = 2 * ld.Pout;
     for (int pass = 0; pass < 2; ++pass) {

@@ -339,8 +339,9 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   } else {
     t->Xd.alloc(Xf.size());
     t->yd.alloc(yf.size());
-    DHO2G_CUDA(cudaMemcpy(t->Xd.p, Xf.data(), Xf.size() * sizeof(float), cudaMemcpyHostToDevice));
-    DHO2G_CUDA(cudaMemcpy(t->yd.p, yf.data(), yf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    // stream-ordered uploads (a pageable cudaMemcpy may return before its DMA lands)
+    DHO2G_CUDA(cudaMemcpyAsync(t->Xd.p, Xf.data(), Xf.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    DHO2G_CUDA(cudaMemcpyAsync(t->yd.p, yf.data(), yf.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
     t->Xptr = t->Xd.p;
     t->yptr = t->yd.p;
   }
@@ -362,7 +363,7 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   t->g_full.alloc(full);
   std::vector<float> w0f(n);
   for (size_t i = 0; i < n; ++i) w0f[i] = (float)w0[i];
-  DHO2G_CUDA(cudaMemcpy(t->w_a_full.p, w0f.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  DHO2G_CUDA(cudaMemcpyAsync(t->w_a_full.p, w0f.data(), n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->world == 1) {
     t->w_a_shard = t->w_a_full.p;
     t->g_shard = t->g_full.p;

@@ -1,6 +1,6 @@
 """Times the split-BF16x3 tcgen05 GEMM (store epilogue) on the C4 shapes through the test hook.
 
-    python scripts/gemm_bench.py
+    python scripts/gemm_bench.py [splits] [cta: 0 auto, 1 single-CTA, 2 CTA pair]
 Reports per-launch device time (CUDA events) and useful / issued TFLOP/s."""
 import os
 import sys
@@ -16,17 +16,19 @@ from paper_2505_00982_b200.api import test_gemm  # noqa: E402
 SHAPES = [  # (M, N, K, what)
     (1024, 3584, 7168, "HVP RZ/RU (B=1024, 2*3584)"),
     (1024, 3584, 3584, "HVP Z/U"),
-    (3584, 3585, 2048, "HVP weight block (K=2B)"),
+    (3584, 3584, 2048, "HVP weight block (K=2B)"),
     (8192, 3584, 3584, "grad Z/U (B=8192)"),
-    (3584, 3585, 8192, "grad weight block"),
+    (3584, 3584, 8192, "grad weight block"),
 ]
 
 
 def main():
     ctx = d.Context(0)
     splits = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    cta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     ctx.set_option("gemm_splits", splits)
-    print("gemm_splits", splits)
+    ctx.set_option("gemm_cta", cta)
+    print("gemm_splits", splits, "gemm_cta", cta)
     rng = np.random.default_rng(0)
     for M, N, K, what in SHAPES:
         A = rng.standard_normal((M, K)).astype(np.float32)

@@ -51,6 +51,50 @@ def test_gemm3_split_k_deterministic(ctx, splits):
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 129, 65), (512, 3585, 256), (1024, 272, 7168),
+                                   (2048, 1000, 3000), (1000, 16, 4096), (8, 40, 96)])
+@pytest.mark.parametrize("cta", [1, 2])
+def test_gemm3_cta_modes(ctx, M, N, K, cta):
+    """Single-CTA (128x128, split-K) and CTA-pair (cta_group::2, 256x256, stream-K) kernels: exact to
+    2e-5 of sum |a||b|, and the pair kernel's fixed-order stream-K combine is bitwise repeatable."""
+    rng = np.random.default_rng(M + 11 * N + 3 * K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    exact = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
+    ctx.set_option("gemm_cta", cta)
+    try:
+        c1 = run_gemm(ctx, A, B, 0)
+        c2 = run_gemm(ctx, A, B, 0)
+    finally:
+        ctx.set_option("gemm_cta", 0)
+    assert (c1 == c2).all()
+    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
+
+
+@pytest.mark.parametrize("M,N,K0,K1", [(256, 384, 130, 0), (300, 200, 100, 70), (700, 260, 64, 200),
+                                       (1024, 512, 1024, 1024)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("cta", [1, 2])
+def test_gemm3_segmented_operands(ctx, M, N, K0, K1, a_mn, b_mn, cta):
+    """K-major / MN-major operand windows with a two-segment K range (the MLP's [x | rx] contractions):
+    C = A0 B0^T + A1 B1^T exact to 2e-5 of sum |a||b|; tcgen05 and CUDA-core paths agree."""
+    from paper_2505_00982_b200.api import test_gemm_seg
+    rng = np.random.default_rng(M + N + K0 + 7 * K1 + 3 * a_mn + b_mn)
+    A0, B0 = rng.standard_normal((M, K0)), rng.standard_normal((N, K0))
+    A1, B1 = rng.standard_normal((M, K1)), rng.standard_normal((N, K1))
+    exact = A0 @ B0.T + A1 @ B1.T
+    scale = np.abs(A0) @ np.abs(B0).T + np.abs(A1) @ np.abs(B1).T
+    ctx.set_option("gemm_cta", cta)
+    try:
+        c = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
+    finally:
+        ctx.set_option("gemm_cta", 0)
+    s = test_gemm_seg(ctx, A0, B0, A1, B1, 1, a_mn, b_mn)
+    assert np.max(np.abs(c - exact) / scale) < 2e-5
+    assert np.max(np.abs(s - exact) / scale) < 2e-5
+
+
 # ------------------------------------------------------------------------------------ MLP oracle
 CASES = [([20, 16, 12, 5], 37, "tanh", "softmax_ce", 5), ([20, 16, 12, 5], 37, "relu", "softmax_ce", 5),
          ([20, 16, 12, 5], 37, "tanh", "mse", 5), ([13, 24, 1], 19, "tanh", "mse", 0),
@@ -123,6 +167,33 @@ def test_gemm_backends_agree_on_hvp(ctx, port):
         ctx.set_option("gemm", 0)
     h0 = mlp.hvp(w, v, b)
     assert rel_l2(h0, h1) < 2e-5
+
+
+def test_hvp_cta_modes_vs_checker(ctx, ref):
+    """Wide layers (several 256-row pair tiles, stream-K segments, narrow output layer): the
+    single-CTA and CTA-pair GEMM kernels both match the reference HVP/gradient (fp64, OpenMP)
+    to rel-L2 1e-4 and each other to 2e-5."""
+    from oracle.bindings import blobs_dataset
+    sizes = [512, 1024, 1024, 10]
+    B = 512
+    X, y = blobs_dataset(B, sizes[0], 10, seed=4)
+    mlp = d.MlpOracle(ctx, sizes)
+    w = mlp.init_params(2)
+    v = ref.rng_normal(8, len(w))
+    b = d.Batch(X, y, 10)
+    hv_ref = ref.mlp_hvp(sizes, w, v, X, y, 10)
+    g_ref = ref.mlp_grad(sizes, w, X, y, 10)
+    out = {}
+    for cta in (1, 2):
+        ctx.set_option("gemm_cta", cta)
+        try:
+            out[cta] = (mlp.hvp(w, v, b), mlp.grad(w, b))
+        finally:
+            ctx.set_option("gemm_cta", 0)
+        assert rel_l2(out[cta][0], hv_ref) < 1e-4
+        assert rel_l2(out[cta][1], g_ref) < 1e-4
+    assert rel_l2(out[1][0], out[2][0]) < 2e-5
+    assert rel_l2(out[1][1], out[2][1]) < 2e-5
 
 
 # ------------------------------------------------------------------------------------ Lanczos
