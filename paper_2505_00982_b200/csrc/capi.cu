@@ -130,6 +130,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     if (k == "gemm") ctx->gemm_backend = (int)value;
     else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
     else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
+    else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
     else if (k == "ktimers") {
       ctx->kt_flush();
@@ -328,6 +329,8 @@ int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, 
       ld.out = (int)sizes[t + 1];
       ld.Pin = (int)round_up(sizes[t], 8);
       ld.Pout = (int)round_up(sizes[t + 1], 8);
+      ld.Din = (int)round_up(sizes[t], 64);
+      ld.Dout = (int)round_up(sizes[t + 1], 64);
       ld.w_off = off;
       off += sizes[t] * sizes[t + 1];
       ld.b_off = off;
@@ -336,15 +339,11 @@ int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, 
     }
     m->dim = off;
     for (size_t s : m->sizes) m->smax = std::max(m->smax, s);
-    m->WV_hi.resize(m->L); m->WV_lo.resize(m->L); m->WVt_hi.resize(m->L); m->WVt_lo.resize(m->L);
+    m->WV_hi.resize(m->L); m->WV_lo.resize(m->L);
     for (int t = 0; t < m->L; ++t) {
       const LayerDesc& ld = m->layers[t];
       m->WV_hi[t].alloc((size_t)ld.out * 2 * ld.Pin);
       m->WV_lo[t].alloc((size_t)ld.out * 2 * ld.Pin);
-      if (t > 0) {
-        m->WVt_hi[t].alloc((size_t)ld.in * 2 * ld.Pout);
-        m->WVt_lo[t].alloc((size_t)ld.in * 2 * ld.Pout);
-      }
     }
     *out = m.release();
   });

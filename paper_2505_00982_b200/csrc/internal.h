@@ -44,6 +44,7 @@ struct dho2g_ctx {
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
   int use_graphs = 0;
+  int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled
@@ -75,7 +76,8 @@ struct dho2g_ctx {
 // ------------------------------------------------------------------------- MLP (oracle.hpp:113)
 struct LayerDesc {
   int in = 0, out = 0;    // sizes[t], sizes[t+1]
-  int Pin = 0, Pout = 0;  // round_up(., 8): half-width of the hi/lo operand pairs
+  int Pin = 0, Pout = 0;  // round_up(., 8): half-width of the [a | ra] and [V | W] operand pairs
+  int Din = 0, Dout = 0;  // round_up(., 64): half-width of the [d | rd] pairs (= their K segment length)
   size_t w_off = 0, b_off = 0;
 };
 
@@ -86,31 +88,32 @@ struct dho2g_mlp {
   size_t dim = 0;
   int act = 0, loss = 0;
   int L = 0;
-  // Weight operands per layer t: WV[t] = [V | W] rows o (out x 2Pin); WVt[t] = [V^T | W^T] rows k (in x 2Pout)
-  std::vector<dho2g::DevBuf<dho2g::bf16>> WV_hi, WV_lo, WVt_hi, WVt_lo;
-  // Batch operands per activation level j (width s_j = sizes[j], half-width P_j):
-  //  AR[j]  = [a | ra] rows b   (Bcap x 2P_j), j = 0..L-1
-  //  ART[j] = [a^T | ra^T] rows k (s_j x 2Bpcap), j = 0..L-1
-  //  DR[j]  = [d | rd] rows b   (Bcap x 2P_j), j = 1..L
-  //  DRT[j] = [rd^T | d^T] rows o (s_j x 2Bpcap), j = 1..L
-  std::vector<dho2g::DevBuf<dho2g::bf16>> AR_hi, AR_lo, ART_hi, ART_lo, DR_hi, DR_lo, DRT_hi, DRT_lo;
+  // Weight operands per layer t: WV[t] = [V | W] rows o (out x 2Pin). The forward GEMMs read it K-major
+  // (K = in), the backward GEMMs MN-major (K = out) — no transposed copy.
+  std::vector<dho2g::DevBuf<dho2g::bf16>> WV_hi, WV_lo;
+  // Batch operands per activation level j (width s_j = sizes[j], half-width P_j), row-major by sample:
+  //  AR[j] = [a | ra] rows b (Bcap x 2P_j), j = 0..L-1
+  //  DR[j] = [d | rd] rows b (Bcap x 2D_j, D_j = round_up(s_j, 64)), j = 1..L
+  // K-major operands of the forward / backward GEMMs and MN-major operands (K = batch) of the
+  // weight-block GEMMs.
+  std::vector<dho2g::DevBuf<dho2g::bf16>> AR_hi, AR_lo, DR_hi, DR_lo;
   std::vector<dho2g::DevBuf<float>> a32, ra32, d32, rd32, u32;  // fp32 B x s_j (u32: cached U = D W)
   dho2g::DevBuf<float> Z, RZ;                               // GEMM outputs (Bcap x max s)
   dho2g::DevBuf<float> lab;                                 // gathered labels (Bcap)
   dho2g::DevBuf<double> sample_loss;                        // per-sample loss (Bcap)
   dho2g::DevBuf<int> sample_correct;
-  size_t Bcap = 0, Bpcap = 0;
+  size_t Bcap = 0;
   size_t smax = 0;
   // host-API staging
   dho2g::DevBuf<float> w32, v32, X32, y32, out32;
   dho2g::DevBuf<int64_t> idx;
   dho2g::DevBuf<double> red;
+  dho2g::DevBuf<double> colpart;  // bias column-sum partials
   const float* w_cur = nullptr;        // params whose W halves are loaded
   const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
   const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)
   const void* input_owner = nullptr;   // operator whose curvature batch is packed at level 0
   const float* prepared = nullptr;     // w whose v-independent HVP quantities are cached
-  size_t ones_B = 0;                   // batch size the ones rows of ART were written for
 
   void ensure_batch(size_t B);
 };

@@ -404,6 +404,9 @@ constexpr int RC = 32;
 __global__ void __launch_bounds__(256) ritz_kernel(const float* __restrict__ D, size_t ldd, int me,
                                                    const float* __restrict__ Usel, int r, int c0,
                                                    float* __restrict__ V, size_t ldv, size_t rows) {
+  // V[:, c0 + c] = D[:, :me] Usel[:, c0 + c]. Each thread owns 2 adjacent rows (float2 loads of D),
+  // so every broadcast shared-memory read of Usel feeds 8 FMAs; basis columns go in groups of 8
+  // with all loads issued before the FMAs (groups of 8). Rows are padded to whole chunks (ldd, ldv even).
   extern __shared__ __align__(16) float us[];  // me x RC
   const int nc = min(RC, r - c0);
   for (int q = threadIdx.x; q < me * RC; q += blockDim.x) {
@@ -411,44 +414,58 @@ __global__ void __launch_bounds__(256) ritz_kernel(const float* __restrict__ D, 
     us[q] = c < nc ? Usel[(size_t)j * r + c0 + c] : 0.f;
   }
   __syncthreads();
-  for (size_t row = blockIdx.x * (size_t)blockDim.x + threadIdx.x; row < rows; row += (size_t)gridDim.x * blockDim.x) {
-    float acc[RC];
+  const size_t npairs = (rows + 1) / 2;
+  for (size_t pr = blockIdx.x * (size_t)blockDim.x + threadIdx.x; pr < npairs; pr += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = 2 * pr;
+    float a0[RC], a1[RC];
 #pragma unroll
-    for (int c = 0; c < RC; ++c) acc[c] = 0.f;
-    // basis columns in groups of 8: all 8 loads in flight before the FMAs (one latency per group)
+    for (int c = 0; c < RC; ++c) a0[c] = a1[c] = 0.f;
     int j = 0;
     for (; j + 8 <= me; j += 8) {
-      float x[8];
+      float2 x[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) x[t] = __ldg(D + (size_t)(j + t) * ldd + row);
+      for (int t = 0; t < 8; ++t) x[t] = __ldg(reinterpret_cast<const float2*>(D + (size_t)(j + t) * ldd + row));
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const float4* u4 = reinterpret_cast<const float4*>(us + (j + t) * RC);
 #pragma unroll
         for (int q = 0; q < RC / 4; ++q) {
           const float4 u = u4[q];
-          acc[4 * q] = fmaf(x[t], u.x, acc[4 * q]);
-          acc[4 * q + 1] = fmaf(x[t], u.y, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(x[t], u.z, acc[4 * q + 2]);
-          acc[4 * q + 3] = fmaf(x[t], u.w, acc[4 * q + 3]);
+          a0[4 * q] = fmaf(x[t].x, u.x, a0[4 * q]);
+          a0[4 * q + 1] = fmaf(x[t].x, u.y, a0[4 * q + 1]);
+          a0[4 * q + 2] = fmaf(x[t].x, u.z, a0[4 * q + 2]);
+          a0[4 * q + 3] = fmaf(x[t].x, u.w, a0[4 * q + 3]);
+          a1[4 * q] = fmaf(x[t].y, u.x, a1[4 * q]);
+          a1[4 * q + 1] = fmaf(x[t].y, u.y, a1[4 * q + 1]);
+          a1[4 * q + 2] = fmaf(x[t].y, u.z, a1[4 * q + 2]);
+          a1[4 * q + 3] = fmaf(x[t].y, u.w, a1[4 * q + 3]);
         }
       }
     }
     for (; j < me; ++j) {
-      const float x = __ldg(D + (size_t)j * ldd + row);
+      const float2 x = __ldg(reinterpret_cast<const float2*>(D + (size_t)j * ldd + row));
       const float4* u4 = reinterpret_cast<const float4*>(us + j * RC);
 #pragma unroll
       for (int q = 0; q < RC / 4; ++q) {
         const float4 u = u4[q];
-        acc[4 * q] = fmaf(x, u.x, acc[4 * q]);
-        acc[4 * q + 1] = fmaf(x, u.y, acc[4 * q + 1]);
-        acc[4 * q + 2] = fmaf(x, u.z, acc[4 * q + 2]);
-        acc[4 * q + 3] = fmaf(x, u.w, acc[4 * q + 3]);
+        a0[4 * q] = fmaf(x.x, u.x, a0[4 * q]);
+        a0[4 * q + 1] = fmaf(x.x, u.y, a0[4 * q + 1]);
+        a0[4 * q + 2] = fmaf(x.x, u.z, a0[4 * q + 2]);
+        a0[4 * q + 3] = fmaf(x.x, u.w, a0[4 * q + 3]);
+        a1[4 * q] = fmaf(x.y, u.x, a1[4 * q]);
+        a1[4 * q + 1] = fmaf(x.y, u.y, a1[4 * q + 1]);
+        a1[4 * q + 2] = fmaf(x.y, u.z, a1[4 * q + 2]);
+        a1[4 * q + 3] = fmaf(x.y, u.w, a1[4 * q + 3]);
       }
     }
+    const bool two = row + 1 < rows;
 #pragma unroll
     for (int c = 0; c < RC; ++c)
-      if (c < nc) V[(size_t)(c0 + c) * ldv + row] = acc[c];
+      if (c < nc) {
+        float* dst = V + (size_t)(c0 + c) * ldv + row;
+        if (two) *reinterpret_cast<float2*>(dst) = make_float2(a0[c], a1[c]);
+        else dst[0] = a0[c];
+      }
   }
 }
 
@@ -709,7 +726,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
     const size_t sm = (size_t)me * RC * sizeof(float);
     if (sm > 48 * 1024)
       DHO2G_CUDA(cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ritz_kernel<<<grid_for(ctx, lz->rows, 256, 8), 256, sm, st>>>(lz->D.p, lz->ldd, me, U.p, r, c0, ese->V.p, ese->ldv,
+    ritz_kernel<<<one_wave_grid(ritz_kernel, 256, sm, ctx->sm_count, cdiv(cdiv(lz->rows, 2), 256)), 256, sm, st>>>(lz->D.p, lz->ldd, me, U.p, r, c0, ese->V.p, ese->ldv,
                                                                   lz->rows);
     DHO2G_LAUNCH();
   }

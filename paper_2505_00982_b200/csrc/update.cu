@@ -8,6 +8,8 @@
 // Access pattern follows the Gram-Schmidt passes (lanczos.cu): row chunks of 2048 staged through
 // shared memory; "dot" work is split into (column, 512-row block) items so every warp streams
 // 2 KB contiguous per column; "axpy" work keeps 4 rows per thread with float4 loads.
+#include <cudaTypedefs.h>
+
 #include <cmath>
 
 #include "internal.h"
@@ -20,7 +22,6 @@ constexpr int kT = 256;
 constexpr int kW = kT / 32;
 constexpr int kCh = 2048;            // rows staged per chunk
 constexpr int kSubRows = 512;        // rows per warp dot item (32 lanes x 4 float4)
-constexpr int kItemsPerChunk = kCh / kSubRows;
 
 __device__ __forceinline__ double floored_den(double a, double fl, double sigma) {  // optimizer.cpp:75-79, :94-98
   double f;
@@ -75,13 +76,15 @@ __device__ void finish_partials(const double* acc, int nj, double* part, double*
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// acc[w][j] += V_j[r0 : r0 + kCh] . xs (xs staged in smem); V is padded to whole chunks
+// acc[w][j] += V_j[r0 : r0 + CH] . xs (xs staged in smem); V is padded to whole chunks
+template <int CH = kCh>
 __device__ __forceinline__ void chunk_dots(const float* __restrict__ V, size_t ldv, size_t r0, int R,
                                            const float* xs, double* acc) {
+  constexpr int kItems = CH / kSubRows;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int items = R * kItemsPerChunk;
+  const int items = R * kItems;
   for (int it = warp; it < items; it += kW) {
-    const int j = it / kItemsPerChunk, q = it % kItemsPerChunk;
+    const int j = it / kItems, q = it % kItems;
     const int rb = q * kSubRows + lane * 4;
     const float* col = V + (size_t)j * ldv + r0;
     float4 x[4];
@@ -144,7 +147,10 @@ __device__ __forceinline__ float base_step(const BaseHyper& hp, float gf, float&
   return s;
 }
 
-// ---- P2: g2 = g~ - V c, base step (moments), s, and sc = V^T s
+// ---- P2: g2 = g~ - V c, base step (moments), s, and sc = V^T s. Chunks of kCh2 = 1024 rows: the dots
+// re-read the chunk's V columns right after the correction pass read them, and with all resident
+// CTAs' chunks (~592 x R x 4 KB) inside the 126 MB L2 that re-read is an L2 hit.
+constexpr int kCh2 = 1024;
 __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V, size_t ldv, int R, size_t rows,
                                                     const float* __restrict__ g, const float* __restrict__ pi,
                                                     const float* __restrict__ w, const double* __restrict__ all1,
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
                                                     double* rankp, unsigned* ticket, int* bad) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* xs = reinterpret_cast<float*>(smem);
-  double* c = reinterpret_cast<double*>(smem + kCh * sizeof(float));
+  double* c = reinterpret_cast<double*>(smem + kCh2 * sizeof(float));
   double* acc = c + R;
   for (int j = threadIdx.x; j < R; j += kT) {
     double t = 0.0;
@@ -162,12 +168,12 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
   }
   for (int e = threadIdx.x; e < kW * R; e += kT) acc[e] = 0.0;
   const bool need_m = hp.kind != 0, need_v = hp.kind >= 2, need_w = hp.kind == 3;
-  const size_t nch = cdiv(rows, kCh);
+  const size_t nch = cdiv(rows, kCh2);
   int local_bad = 0;
   for (size_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
-    const size_t r0 = ch * kCh;
+    const size_t r0 = ch * kCh2;
     __syncthreads();
-    for (int e = threadIdx.x; e < kCh / 4; e += kT) {
+    for (int e = threadIdx.x; e < kCh2 / 4; e += kT) {
       const size_t r = r0 + 4 * (size_t)e;
       float4 x = ld4(g, r, rows);
       if (pi) {
@@ -209,10 +215,171 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
       reinterpret_cast<float4*>(xs)[e] = s;
     }
     __syncthreads();
-    if (R > 0) chunk_dots(V, ldv, r0, R, xs, acc);
+    if (R > 0) chunk_dots<kCh2>(V, ldv, r0, R, xs, acc);
   }
   if (local_bad) atomicOr(bad, 1);
   if (R > 0) finish_partials(acc, R, part, rankp, ticket);
+}
+
+// ---- P2 (bulk-copy staged): same math as upd_p2_kernel for R <= kP2MaxR. Each chunk of CH rows of
+// V (R columns) and of the row streams (g, pi, m, v, w) is brought into shared memory by
+// cp.async.bulk (double-buffered, one mbarrier per stage), so V is read from HBM exactly once for
+// both the correction g - V c and the dots V^T s (the register-staged kernel re-reads V for the dots
+// and loses the L2 race at large R x CH). Dot partials stay in per-lane fp64 registers until the end.
+constexpr int kP2MaxR = 48;
+constexpr int kP2CH = 256;     // rows per stage (one per thread)
+constexpr int kP2Streams = 5;  // g, pi, m, v, w
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Two CTAs per SM, each double-buffered: ~4 stages of (R + 5) x 1 KB in flight per SM.
+template <int CH, int NS>
+__global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant__ CUtensorMap mapV, int R, size_t rows,
+                                                          const float* __restrict__ g, const float* __restrict__ pi,
+                                                          const float* __restrict__ w,
+                                                          const double* __restrict__ all1, int world, BaseHyper hp,
+                                                          float* __restrict__ m, float* __restrict__ v,
+                                                          float* __restrict__ s_out, double* part, double* rankp,
+                                                          unsigned* ticket, int* bad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const size_t stage_floats = (size_t)(R + kP2Streams) * CH;
+  // tensor-copy destinations need 128-byte alignment
+  float* stg0 = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem) + 127) & ~uintptr_t(127));
+  float* xs = stg0 + NS * stage_floats;
+  double* c = reinterpret_cast<double*>(xs + CH);
+  double* acc = c + R;  // [kW][R]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(acc + kW * R);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool need_m = hp.kind != 0, need_v = hp.kind >= 2, need_w = hp.kind == 3;
+  const size_t nch = cdiv(rows, CH);
+
+  auto issue = [&](size_t i) {  // thread 0: stage i % NS <- chunk blockIdx.x + i * gridDim.x
+    const size_t ch = blockIdx.x + i * gridDim.x;
+    if (ch >= nch) return;
+    float* st = stg0 + (i % NS) * stage_floats;
+    const size_t r0 = ch * CH;
+    const bool full = r0 + CH <= rows;
+    uint32_t bytes = (uint32_t)R * CH * 4u;
+    if (full) bytes += (uint32_t)(1 + (pi ? 1 : 0) + (need_m ? 1 : 0) + (need_v ? 1 : 0) + (need_w ? 1 : 0)) * CH * 4u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[i % NS])), "r"(bytes)
+                 : "memory");
+    // all R columns of the chunk in one 2D tensor copy (box CH rows x R columns, column-major in smem)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_addr(st)),
+        "l"(reinterpret_cast<uint64_t>(&mapV)), "r"((int)r0), "r"(0), "r"(smem_addr(&bar[i % NS]))
+        : "memory");
+    if (full) {
+      float* ss = st + (size_t)R * CH;
+      bulk_g2s(ss, g + r0, CH * 4u, &bar[i % NS]);
+      if (pi) bulk_g2s(ss + CH, pi + r0, CH * 4u, &bar[i % NS]);
+      if (need_m) bulk_g2s(ss + 2 * CH, m + r0, CH * 4u, &bar[i % NS]);
+      if (need_v) bulk_g2s(ss + 3 * CH, v + r0, CH * 4u, &bar[i % NS]);
+      if (need_w) bulk_g2s(ss + 4 * CH, w + r0, CH * 4u, &bar[i % NS]);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NS; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < R; j += kT) {
+    double t = 0.0;
+    for (int r = 0; r < world; ++r) t += all1[(size_t)r * R + j];
+    c[j] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < NS; ++q) issue(q);
+  double lacc[kP2MaxR / kW];
+#pragma unroll
+  for (int q = 0; q < kP2MaxR / kW; ++q) lacc[q] = 0.0;
+  int local_bad = 0;
+  for (size_t i = 0; blockIdx.x + i * gridDim.x < nch; ++i) {
+    const size_t r0 = (blockIdx.x + i * gridDim.x) * CH;
+    const bool full = r0 + CH <= rows;
+    float* st = stg0 + (i % NS) * stage_floats;
+    bar_wait(&bar[i % NS], (uint32_t)((i / NS) & 1));
+    if (threadIdx.x < CH) {  // phase A: row r0 + threadIdx.x
+      const int t = threadIdx.x;
+      const size_t r = r0 + t;
+      const bool in = r < rows;
+      const float* ss = st + (size_t)R * CH;
+      float x = full ? ss[t] : (in ? g[r] : 0.f);
+      if (pi) x += full ? ss[CH + t] : (in ? pi[r] : 0.f);
+      // four independent fp64 partial sums (short dependency chains), combined in a fixed order
+      double g0 = x, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      int j = 0;
+      for (; j + 4 <= R; j += 4) {
+        g0 -= (double)st[(size_t)j * CH + t] * c[j];
+        g1 -= (double)st[(size_t)(j + 1) * CH + t] * c[j + 1];
+        g2 -= (double)st[(size_t)(j + 2) * CH + t] * c[j + 2];
+        g3 -= (double)st[(size_t)(j + 3) * CH + t] * c[j + 3];
+      }
+      for (; j < R; ++j) g0 -= (double)st[(size_t)j * CH + t] * c[j];
+      const float gm = (float)((g0 + g1) + (g2 + g3));
+      float sv = 0.f;
+      if (in) {
+        if (!isfinite(gm)) local_bad = 1;
+        float mm = need_m ? (full ? ss[2 * CH + t] : m[r]) : 0.f;
+        float vm = need_v ? (full ? ss[3 * CH + t] : v[r]) : 0.f;
+        const float ww = need_w ? (full ? ss[4 * CH + t] : w[r]) : 0.f;
+        sv = base_step(hp, gm, mm, vm, ww);
+        if (need_m) m[r] = mm;
+        if (need_v) v[r] = vm;
+        s_out[r] = sv;
+      }
+      xs[t] = sv;
+    }
+    __syncthreads();
+    // phase B: column j = warp + kW q, lanes stride the chunk with float4
+#pragma unroll
+    for (int q = 0; q < kP2MaxR / kW; ++q) {
+      const int j = warp + kW * q;
+      if (j < R) {
+        const float* col = st + (size_t)j * CH;
+        float f = 0.f;
+#pragma unroll
+        for (int k = 0; k < CH / 128; ++k) {
+          const float4 a = *reinterpret_cast<const float4*>(col + 4 * lane + 128 * k);
+          const float4 b = *reinterpret_cast<const float4*>(xs + 4 * lane + 128 * k);
+          f += a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+        }
+        lacc[q] += (double)f;
+      }
+    }
+    __syncthreads();  // stage (i % NS) and xs free
+    if (threadIdx.x == 0) issue(i + NS);
+  }
+  if (local_bad) atomicOr(bad, 1);
+#pragma unroll
+  for (int q = 0; q < kP2MaxR / kW; ++q) {
+    const int j = warp + kW * q;
+    const double t = warp_sum(lacc[q]);
+    if (j < R && lane == 0) acc[warp * R + j] = t;
+  }
+  for (int e = threadIdx.x; e < kW * R; e += kT)  // warps without column j contribute 0
+    if (e / R != (e % R) % kW) acc[e] = 0.0;
+  finish_partials(acc, R, part, rankp, ticket);
 }
 
 // ---- P3: w_a += base + newton (optionally materialized)
@@ -353,9 +520,9 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   if (!al16(a.g) || !al16(a.pi) || !al16(a.w_a) || !al16(a.w_decay) || !al16(a.newton_out) || !al16(a.base_out))
     fail(DHO2G_ARGUMENT, "split_update: vectors must be 16-byte aligned");
   const size_t smem_p1 = kCh * sizeof(float) + (size_t)kW * R * sizeof(double);
-  const size_t smem_p2 = kCh * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double);
+  const size_t smem_p2 = kCh2 * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double);
   const int gp = std::min(one_wave_grid(upd_p1_kernel, kT, smem_p1, ctx->sm_count, cdiv(rows, kCh)),
-                          one_wave_grid(upd_p2_kernel, kT, smem_p2, ctx->sm_count, cdiv(rows, kCh)));
+                          one_wave_grid(upd_p2_kernel, kT, smem_p2, ctx->sm_count, cdiv(rows, kCh2)));
   const int R1 = std::max(R, 1);
   o->part.ensure((size_t)gp * R1 + 8);
   o->rank1.ensure(R1);
@@ -378,9 +545,36 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   ++o->t;
   const BaseHyper hp = make_hyper(o->cfg, o->t);
   const int k2 = ctx->kt_begin();
-  upd_p2_kernel<<<gp, kT, smem_p2, st>>>(
-      V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p, o->v.p, o->s.p, o->part.p,
-      o->rank2.p, o->ticket.p + 1, o->bad.p);
+  if (R > 0 && R <= kP2MaxR && ctx->upd_p2_staged) {
+    // 256-row stages, double-buffered, two CTAs per SM (measured best of 128/256 rows x 2-4 stages x 1-2 CTAs)
+    const int CH = kP2CH;
+    const int NS = 2;
+    const size_t smem_t = ((size_t)NS * (R + kP2Streams) * CH + CH) * sizeof(float) +
+                          (size_t)(R + kW * R) * sizeof(double) + NS * sizeof(uint64_t) + 128;
+    auto kern = upd_p2_tma_kernel<kP2CH, 2>;
+    if (smem_t > 227 * 1024) fail(DHO2G_ARGUMENT, "split_update: staged pass 2 does not fit shared memory");
+    DHO2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
+    const int gt = std::min(gp, one_wave_grid(kern, kT, smem_t, ctx->sm_count, cdiv(rows, CH)));
+    // V_hat as a 2D fp32 tensor: inner = rows (stride 1), outer = R columns (stride ldv); box CH x R
+    CUtensorMap mapV;
+    {
+      cuuint64_t dims[2] = {(cuuint64_t)ldv, (cuuint64_t)R};
+      cuuint64_t strides[1] = {(cuuint64_t)ldv * sizeof(float)};
+      cuuint32_t box[2] = {(cuuint32_t)CH, (cuuint32_t)R};
+      cuuint32_t estr[2] = {1, 1};
+      auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx->encode_fn);
+      if (!enc || enc(&mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(V), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        fail(DHO2G_CUDA, "split_update: cuTensorMapEncodeTiled failed for V_hat");
+    }
+    kern<<<gt, kT, smem_t, st>>>(mapV, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p,
+                                 o->v.p, o->s.p, o->part.p, o->rank2.p, o->ticket.p + 1, o->bad.p);
+  } else {
+    upd_p2_kernel<<<gp, kT, smem_p2, st>>>(
+        V, ldv, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p, o->v.p, o->s.p, o->part.p,
+        o->rank2.p, o->ticket.p + 1, o->bad.p);
+  }
   DHO2G_LAUNCH();
   ctx->kt_end(k2, "upd_p2", rb * (R + 2 + (a.pi ? 1 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
                                   (o->cfg.kind == 3 ? 1 : 0)));
