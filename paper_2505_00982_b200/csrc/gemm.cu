@@ -351,16 +351,18 @@ __device__ __forceinline__ uint64_t op_desc(uint32_t tile_base, int kk) {
 }
 
 // Stage one 128-row (M or N) x 64-K operand tile (hi or lo) into smem through its map.
-template <bool MN, bool PAIR>
+// PANELS2: 2 = 128 MN rows (MN-major: two 64-wide boxes), 1 = 64 rows (the B half of a 128-wide pair tile;
+// K-major maps are then built with 64-row boxes).
+template <bool MN, bool PAIR, int PANELS2 = 2>
 __device__ __forceinline__ void load_op(uint8_t* dst, const CUtensorMap* map, const OpOff& o, int mn0, int kb,
                                         int kseg, uint64_t* bar) {
   const int k = kb * BK;
   const int seg = k >= kseg ? 1 : 0;
   const int kk = k - (seg ? kseg : 0);
-  if (MN) {  // two 64(MN) x 64(K) boxes
+  if (MN) {  // 64(MN) x 64(K) boxes
     tma_load_2d<PAIR>(dst, map, mn0 + o.off_in[seg], kk + o.off_out[seg], bar);
-    tma_load_2d<PAIR>(dst + 8192, map, mn0 + 64 + o.off_in[seg], kk + o.off_out[seg], bar);
-  } else {  // one 64(K) x 128(MN) box
+    if (PANELS2 == 2) tma_load_2d<PAIR>(dst + 8192, map, mn0 + 64 + o.off_in[seg], kk + o.off_out[seg], bar);
+  } else {  // one 64(K) x (64 PANELS2)(MN) box
     tma_load_2d<PAIR>(dst, map, kk + o.off_in[seg], mn0 + o.off_out[seg], bar);
   }
 }
@@ -403,8 +405,8 @@ CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t 
   return m;
 }
 // hi / lo maps of one operand: K-major boxes 64(K) x 128 rows, MN-major boxes 64(MN) x 64(K)
-void op_maps(void* encode_fn, const GOp& g, CUtensorMap& mh, CUtensorMap& ml) {
-  const uint32_t bi = 64, bo = g.mn_major ? 64 : 128;
+void op_maps(void* encode_fn, const GOp& g, CUtensorMap& mh, CUtensorMap& ml, uint32_t rows = 128) {
+  const uint32_t bi = 64, bo = g.mn_major ? 64 : rows;
   mh = make_map(encode_fn, g.hi, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
   ml = make_map(encode_fn, g.lo, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
 }
@@ -699,12 +701,10 @@ namespace tc2 {
 using namespace tc;
 
 constexpr int BM = 128;   // output rows per CTA (pair tile 256)
-constexpr int BNT = 256;  // pair tile columns (UMMA_N, max)
 constexpr int STAGES = 3;
-constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;  // A hi/lo (128 rows) + B hi/lo (128 = BNT/2 rows)
+constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;  // A hi/lo (128 rows) + B hi/lo (<= 128 = NT/2 rows) slots
 constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
-constexpr uint32_t TMEM_COLS = ACC * BNT;  // 512: the whole TMEM of the SM
-constexpr uint32_t PART_FLOATS = BM * BNT;  // one CTA's partial tile
+constexpr uint32_t PART_MAX = BM * 256;  // one CTA's partial tile (NT = 256)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -738,28 +738,68 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
   } while (!done);
 }
 
+// The tile space is walked in `phases` (groups of m-tiles or of n-tiles, pdim = 0 / 1) so that the operand
+// bytes touched concurrently by all pairs fit in L2; stream-K runs inside each phase.
 struct Work {
-  int nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
-  long long total;                        // tiles * nkb
-  __device__ __forceinline__ long long begin(int w) const { return total * w / workers; }
+  int mt, nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
+  int pdim, phases;
+  __device__ __forceinline__ void prange(int p, int& lo, int& cnt) const {
+    const int D = pdim ? nt : mt;
+    lo = D * p / phases;
+    cnt = D * (p + 1) / phases - lo;
+  }
+  __device__ __forceinline__ long long ptotal(int p) const {
+    int lo, cnt;
+    prange(p, lo, cnt);
+    return (long long)(pdim ? mt * cnt : cnt * nt) * nkb;
+  }
+  __device__ __forceinline__ long long begin(int p, int w) const { return ptotal(p) * w / workers; }
 };
 struct Seg {
-  int tile, k0, k1;
+  int phase, tile, k0, k1;  // tile: index inside the phase
+  int mtile, ntile;
 };
-__device__ __forceinline__ bool next_seg(const Work& wk, long long& a, long long end, Seg& s) {
-  if (a >= end) return false;
-  s.tile = (int)(a / wk.nkb);
-  s.k0 = (int)(a - (long long)s.tile * wk.nkb);
-  s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
-  a += s.k1 - s.k0;
-  return true;
-}
-__device__ __forceinline__ int tile_cols(const Work& wk, int n0) {  // MMA N of a tile (<= 256)
+// Iterates one worker's segments over all phases.
+struct Cursor {
+  int p, w;
+  long long a, end;
+  __device__ __forceinline__ void init(const Work& wk, int worker) {
+    w = worker;
+    p = 0;
+    a = wk.begin(0, w);
+    end = wk.begin(0, w + 1);
+  }
+  __device__ __forceinline__ bool next(const Work& wk, Seg& s) {
+    while (a >= end) {
+      if (++p >= wk.phases) return false;
+      a = wk.begin(p, w);
+      end = wk.begin(p, w + 1);
+    }
+    s.phase = p;
+    s.tile = (int)(a / wk.nkb);
+    s.k0 = (int)(a - (long long)s.tile * wk.nkb);
+    s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
+    a += s.k1 - s.k0;
+    int lo, cnt;
+    wk.prange(p, lo, cnt);
+    if (wk.pdim) {
+      s.mtile = s.tile / cnt;
+      s.ntile = lo + s.tile % cnt;
+    } else {
+      s.mtile = lo + s.tile / wk.nt;
+      s.ntile = s.tile % wk.nt;
+    }
+    return true;
+  }
+};
+template <int NT>
+__device__ __forceinline__ int tile_cols(const Work& wk, int n0) {  // MMA N of a tile (<= NT)
   const int c = wk.N - n0;
-  return c >= BNT ? BNT : ((c + wk.nround - 1) / wk.nround) * wk.nround;
+  return c >= NT ? NT : ((c + wk.nround - 1) / wk.nround) * wk.nround;
 }
 
-template <bool AMN, bool BMN>
+// NT: pair tile width (256, or 128 when 256-wide tiles would leave pairs with less than ~2 tiles)
+template <bool AMN, bool BMN, int NT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm3_tc2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Work wk,
@@ -773,10 +813,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
 
+  constexpr uint32_t TMEM_COLS = ACC * NT;
+  constexpr uint32_t PART_FLOATS = BM * NT;
+  constexpr uint32_t B_BYTES = (NT / 2) * BK * 2;  // one (hi or lo) B half-tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int worker = blockIdx.x >> 1;
-  const long long wbeg = wk.begin(worker), wend = wk.begin(worker + 1);
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -809,34 +851,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs): this CTA's halves of A and B into its ring
     uint32_t it = 0;
-    long long a = wbeg;
+    Cursor cur;
+    cur.init(wk, worker);
     Seg sg;
-    while (next_seg(wk, a, wend, sg)) {
-      const int m0 = (sg.tile / wk.nt) * 256 + (int)rank * BM, n0 = (sg.tile % wk.nt) * BNT;
-      const int nb = n0 + (int)rank * (tile_cols(wk, n0) / 2);
+    while (cur.next(wk, sg)) {
+      const int m0 = sg.mtile * 256 + (int)rank * BM, n0 = sg.ntile * NT;
+      const int nb = n0 + (int)rank * (tile_cols<NT>(wk, n0) / 2);
       for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
-        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * (2 * OP_BYTES + 2 * B_BYTES));
         load_op<AMN, true>(st, &mAh, oa, m0, kb, wk.kseg, &full[s]);
         load_op<AMN, true>(st + OP_BYTES, &mAl, oa, m0, kb, wk.kseg, &full[s]);
-        load_op<BMN, true>(st + 2 * OP_BYTES, &mBh, ob, nb, kb, wk.kseg, &full[s]);
-        load_op<BMN, true>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
+        load_op<BMN, true, NT / 128>(st + 2 * OP_BYTES, &mBh, ob, nb, kb, wk.kseg, &full[s]);
+        load_op<BMN, true, NT / 128>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
       }
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (leader CTA only)
     uint32_t it = 0, uc = 0;
-    long long a = wbeg;
+    Cursor cur;
+    cur.init(wk, worker);
     Seg sg;
-    while (next_seg(wk, a, wend, sg)) {
-      const int n0 = (sg.tile % wk.nt) * BNT;
-      const uint32_t ID = idesc(256, tile_cols(wk, n0), AMN, BMN);
+    while (cur.next(wk, sg)) {
+      const int n0 = sg.ntile * NT;
+      const uint32_t ID = idesc(256, tile_cols<NT>(wk, n0), AMN, BMN);
       const uint32_t ab = uc % ACC;
       mbar_wait_cluster(&tempty[ab], ((uc / ACC) & 1) ^ 1);
       fence_after();
-      const uint32_t acc_addr = tmem + ab * BNT;
+      const uint32_t acc_addr = tmem + ab * NT;
       for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
@@ -868,26 +912,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int ew = warp & 3;
     const int chalf = (warp - 4) >> 2;
     float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
-    const size_t slot_off = (size_t)(ew + 4 * chalf) * (32 * BNT / 2) + (size_t)lane * 4;
+    const size_t slot_off = (size_t)(ew + 4 * chalf) * (32 * NT / 2) + (size_t)lane * 4;
     uint32_t uc = 0;
-    long long a = wbeg;
+    Cursor cur;
+    cur.init(wk, worker);
     Seg sg;
-    while (next_seg(wk, a, wend, sg)) {
-      const int m0 = (sg.tile / wk.nt) * 256 + (int)rank * BM, n0 = (sg.tile % wk.nt) * BNT;
-      const int ncols = tile_cols(wk, n0);
+    while (cur.next(wk, sg)) {
+      const int m0 = sg.mtile * 256 + (int)rank * BM, n0 = sg.ntile * NT;
+      const int ncols = tile_cols<NT>(wk, n0);
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
-      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BNT;
+      const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
       if (sg.k0 != 0) {
         // non-head segment (first of this worker): publish the raw partial
-        float* p = ws + (size_t)(worker * 2 + rank) * PART_FLOATS + slot_off;
+        float* p = ws + ((size_t)(sg.phase * wk.workers + worker) * 2 + rank) * PART_FLOATS + slot_off;
 #pragma unroll 1
-        for (int c0 = chalf * (BNT / 2); c0 < (chalf + 1) * (BNT / 2); c0 += 16) {
+        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
-          float* q = p + (size_t)((c0 - chalf * (BNT / 2)) / 16) * (4 * 32 * 4);
+          float* q = p + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             __stcg(reinterpret_cast<float4*>(q + j * 128), make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
@@ -897,26 +942,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (lane == 0) arrive_leader(&tempty[ab]);
         __threadfence();
         epi_bar();
-        if (threadIdx.x == 128) st_release(flags + worker * 2 + rank, ready);
+        if (threadIdx.x == 128) st_release(flags + (sg.phase * wk.workers + worker) * 2 + rank, ready);
       } else {
         // head segment: later segments of this tile are the first segments of workers worker+1, ...
         const long long tile_end = (long long)(sg.tile + 1) * wk.nkb;
+        const int sbase = sg.phase * wk.workers;
         int wlast = worker;
         if (sg.k1 < wk.nkb) {
-          while (wlast + 1 < wk.workers && wk.begin(wlast + 1) < tile_end) ++wlast;
+          while (wlast + 1 < wk.workers && wk.begin(sg.phase, wlast + 1) < tile_end) ++wlast;
           if (threadIdx.x == 128)
             for (int w2 = worker + 1; w2 <= wlast; ++w2)
-              while (ld_acquire(flags + w2 * 2 + rank) != ready) __nanosleep(64);
+              while (ld_acquire(flags + (sbase + w2) * 2 + rank) != ready) __nanosleep(64);
           epi_bar();
         }
 #pragma unroll 1
-        for (int c0 = chalf * (BNT / 2); c0 < (chalf + 1) * (BNT / 2); c0 += 16) {
+        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
           for (int w2 = worker + 1; w2 <= wlast; ++w2) {
-            const float* q = ws + (size_t)(w2 * 2 + rank) * PART_FLOATS + slot_off +
-                             (size_t)((c0 - chalf * (BNT / 2)) / 16) * (4 * 32 * 4);
+            const float* q = ws + ((size_t)(sbase + w2) * 2 + rank) * PART_FLOATS + slot_off +
+                             (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
@@ -941,11 +987,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int NT>
 int max_pairs(dho2g_ctx* ctx) {
   static int pairs = 0;
   if (pairs > 0) return pairs;
-  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * (ctx->sm_count / 2));
   cfg.blockDim = dim3(384);
@@ -958,48 +1004,66 @@ int max_pairs(dho2g_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int clusters = 0;
-  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN>, &cfg));
+  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN, NT>, &cfg));
   if (clusters < 1) fail(DHO2G_CUDA, "gemm3_tc2: no CTA pair can be resident");
   pairs = clusters;
   return pairs;
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int NT>
 int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
-  const int pairs = max_pairs<AMN, BMN>(ctx);
-  // every worker gets >= 4 k-blocks (a segment shorter than that is mostly fixup traffic)
-  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, wk.total / 4));
-  ctx->gemm_ws.ensure((size_t)wk.workers * 2 * PART_FLOATS);
-  ctx->gemm_flags.ensure((size_t)wk.workers * 2 + 16);
+  const int pairs = max_pairs<AMN, BMN, NT>(ctx);
+  // every worker gets >= 4 k-blocks of its smallest phase (shorter segments are mostly fixup traffic)
+  const long long per_phase = (long long)wk.mt * wk.nt * wk.nkb / wk.phases;
+  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, per_phase / 4));
+  ctx->gemm_ws.ensure((size_t)wk.phases * wk.workers * 2 * PART_MAX);
+  ctx->gemm_flags.ensure((size_t)wk.phases * wk.workers * 2 + 16);
   unsigned epoch = ++ctx->gemm_epoch;
   if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
     ctx->gemm_epoch = epoch = 1;
   }
-  gemm3_tc2_kernel<AMN, BMN><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
+  gemm3_tc2_kernel<AMN, BMN, NT><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
       maps[0], maps[1], maps[2], maps[3], wk, oa, ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u);
   DHO2G_LAUNCH();
   return wk.workers;
 }
 
-int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
+template <int NT>
+int run_nt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   Work wk;
-  const int mt = (int)cdiv(M, 256);
-  wk.nt = (int)cdiv(N, BNT);
+  wk.mt = (int)cdiv(M, 256);
+  wk.nt = (int)cdiv(N, NT);
   wk.nkb = (int)cdiv(K, BK);
   wk.N = N;
   wk.kseg = kseg;
   wk.nround = B.mn_major ? 128 : 16;
-  wk.total = (long long)mt * wk.nt * wk.nkb;
   wk.workers = 1;
+  // L2 phases (off by default: measured on the HVP shapes, the extra stream-K fixups of more, smaller
+  // per-phase ranges cost more than the avoided operand re-reads; kept as option gemm_phases)
+  {
+    const double a_bytes = 4.0 * M * K, b_bytes = 4.0 * N * K;
+    wk.pdim = b_bytes >= a_bytes ? 1 : 0;
+    const int ph = ctx->gemm_phases > 0 ? ctx->gemm_phases : 1;
+    wk.phases = std::max(1, std::min(ph, wk.pdim ? wk.nt : wk.mt));
+  }
   CUtensorMap maps[4];
   op_maps(ctx->encode_fn, A, maps[0], maps[1]);
-  op_maps(ctx->encode_fn, B, maps[2], maps[3]);
+  op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2);
   const OpOff oa = op_off(A), ob = op_off(B);
-  if (A.mn_major && B.mn_major) return launch<true, true>(ctx, maps, wk, oa, ob, e);
-  if (A.mn_major) return launch<true, false>(ctx, maps, wk, oa, ob, e);
-  if (B.mn_major) return launch<false, true>(ctx, maps, wk, oa, ob, e);
-  return launch<false, false>(ctx, maps, wk, oa, ob, e);
+  if (A.mn_major && B.mn_major) return launch<true, true, NT>(ctx, maps, wk, oa, ob, e);
+  if (A.mn_major) return launch<true, false, NT>(ctx, maps, wk, oa, ob, e);
+  if (B.mn_major) return launch<false, true, NT>(ctx, maps, wk, oa, ob, e);
+  return launch<false, false, NT>(ctx, maps, wk, oa, ob, e);
+}
+
+int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e, int& nt_used) {
+  // 256-wide pair tiles. 128-wide ones (option gemm_pair_n = 128) let a pair overlap one tile's epilogue
+  // with the next tile's MMAs at M = 1024, but measured 5-20% slower on every C4 shape (A/B in
+  // scripts/prof_hvp.py --abopt gemm_pair_n).
+  const int nt = ctx->gemm_pair_n == 128 ? 128 : 256;
+  nt_used = nt;
+  return nt == 128 ? run_nt<128>(ctx, M, N, K, kseg, A, B, e) : run_nt<256>(ctx, M, N, K, kseg, A, B, e);
 }
 
 }  // namespace tc2
@@ -1014,7 +1078,7 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
   ctx->bump("gemm_calls", 1);
   ctx->bump("gemm_flops_issued", 3.0 * 2.0 * double(M) * double(N) * double(K));
   const int slot = ctx->kt_begin();
-  int splits = 1;
+  int splits = 1, pair_nt = 0;
   bool pair = false;
   if (ctx->gemm_backend == 1) {
     gemm3_simt(ctx, M, N, K, kseg, A, B, e);
@@ -1022,7 +1086,9 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
     if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
     // CTA pairs (256-row tiles) unless the GEMM is too short in M to fill them
     pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 128);
-    splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e) : tc1::run(ctx, M, N, K, kseg, A, B, e);
+    int nt = 0;
+    splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e, nt) : tc1::run(ctx, M, N, K, kseg, A, B, e);
+    pair_nt = nt;
   }
   if (slot >= 0) {  // name: backend:epilogue(+R)[operand majors]/(splits | pair), aggregated by prefix in the bench
     static const char* modes[] = {"store", "fwd", "fwdout", "bwd"};
@@ -1030,7 +1096,7 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
     if (A.mn_major || B.mn_major) std::snprintf(lay, sizeof(lay), "[%c%c]", A.mn_major ? 'm' : 'k', B.mn_major ? 'm' : 'k');
     char name[80];
     if (pair)
-      std::snprintf(name, sizeof(name), "gemm3_tcgen05:%s%s%s/pair", modes[e.mode], e.do1 ? "R" : "", lay);
+      std::snprintf(name, sizeof(name), "gemm3_tcgen05:%s%s%s/pair%d", modes[e.mode], e.do1 ? "R" : "", lay, pair_nt);
     else
       std::snprintf(name, sizeof(name), "%s:%s%s%s/s%d", ctx->gemm_backend == 1 ? "gemm3_simt" : "gemm3_tcgen05",
                     modes[e.mode], e.do1 ? "R" : "", lay, splits);

@@ -39,7 +39,8 @@ struct dho2g_ctx {
   int gemm_backend = 0;  // 0 tcgen05, 1 CUDA-core reference kernel
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
-  int gemm_pairs = 0;    // co-resident CTA pairs of the pair kernel (queried once)
+  int gemm_phases = 0;   // pair kernel L2 phases: 0/-1 off, k > 0 forced
+  int gemm_pair_n = 0;   // pair kernel tile width: 0 auto, 128, 256
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
@@ -108,7 +109,8 @@ struct dho2g_mlp {
   dho2g::DevBuf<float> w32, v32, X32, y32, out32;
   dho2g::DevBuf<int64_t> idx;
   dho2g::DevBuf<double> red;
-  dho2g::DevBuf<double> colpart;  // bias column-sum partials
+  dho2g::DevBuf<double> colpart;      // bias column-sum partials
+  dho2g::DevBuf<unsigned> coltickets;  // their per-column-block completion tickets
   const float* w_cur = nullptr;        // params whose W halves are loaded
   const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
   const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)

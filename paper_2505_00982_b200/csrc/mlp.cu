@@ -53,11 +53,11 @@ namespace {
 // WV[t][o][half*Pin + k] = scale * p(o, k), k < in (pads [in, Pin) stay zero). One row o per
 // blockIdx.y; each thread packs 8 elements (8 independent loads in flight), coalesced across the warp.
 constexpr int kPackPer = 8;
-__global__ void pack_weights_kernel(const float* __restrict__ p, const float* __restrict__ pscale, int in, int Pin,
-                                    int half, bf16* __restrict__ WVh, bf16* __restrict__ WVl) {
-  const int o = blockIdx.y;
+__global__ void pack_weights_kernel(const float* __restrict__ p, const float* __restrict__ pscale, int in, int out,
+                                    int Pin, int half, bf16* __restrict__ WVh, bf16* __restrict__ WVl) {
   const int k0 = blockIdx.x * (blockDim.x * kPackPer) + threadIdx.x;
   const float sc = pscale ? *pscale : 1.0f;
+  for (int o = blockIdx.y; o < out; o += gridDim.y) {
   const float* row = p + (size_t)o * in;
   float x[kPackPer];
 #pragma unroll
@@ -75,6 +75,7 @@ __global__ void pack_weights_kernel(const float* __restrict__ p, const float* __
       WVh[base + k] = h;
       WVl[base + k] = l;
     }
+  }
   }
 }
 
@@ -150,12 +151,15 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, in
 }
 
 // Bias block as a column sum of a row-major pair buffer: out[o] = sum_{b < B} (hi + lo)[b][off + o].
-// Stage 1: blocks of 64 columns (2 per lane, bf16x2 loads) x 8 row groups over one row chunk write
-// fp64 partials part[chunk][o]; stage 2 adds the chunks in order (deterministic).
+// Blocks of 64 columns (2 per lane, bf16x2 loads) x 8 row groups over one of kColChunks row chunks
+// write fp64 partials part[chunk][o]; the last block of each column block (ticket) adds the chunks
+// in order (deterministic, one launch).
 constexpr int kColChunks = 32;
 __global__ void colsum_pairs_kernel(const bf16* __restrict__ hi, const bf16* __restrict__ lo, int ld, int off,
-                                    int cols, int B, double* __restrict__ part) {
+                                    int cols, int B, double* __restrict__ part, unsigned* __restrict__ tickets,
+                                    float* __restrict__ out) {
   __shared__ double sh[8][64];
+  __shared__ bool last;
   const int c = blockIdx.x * 64 + 2 * threadIdx.x;
   const int rows_per = (B + kColChunks - 1) / kColChunks;
   const int r0 = blockIdx.y * rows_per, r1 = min(B, r0 + rows_per);
@@ -173,22 +177,28 @@ __global__ void colsum_pairs_kernel(const bf16* __restrict__ hi, const bf16* __r
   sh[threadIdx.y][2 * threadIdx.x] = a0;
   sh[threadIdx.y][2 * threadIdx.x + 1] = a1;
   __syncthreads();
-  if (threadIdx.y == 0) {
-    for (int q = 0; q < 2; ++q) {
-      const int cc = c + q;
-      if (cc >= cols) continue;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  if (tid < 64) {
+    const int cc = blockIdx.x * 64 + tid;
+    double t = 0.0;
+    for (int g = 0; g < 8; ++g) t += sh[g][tid];
+    if (cc < cols) part[(size_t)blockIdx.y * cols + cc] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < 64) {
+    const int cc = blockIdx.x * 64 + tid;
+    if (cc < cols) {
       double t = 0.0;
-      for (int g = 0; g < 8; ++g) t += sh[g][2 * threadIdx.x + q];
-      part[(size_t)blockIdx.y * cols + cc] = t;
+      for (int k = 0; k < (int)gridDim.y; ++k) t += __ldcg(part + (size_t)k * cols + cc);
+      out[cc] = (float)t;
     }
   }
-}
-__global__ void colsum_final_kernel(const double* __restrict__ part, int cols, float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  double t = 0.0;
-  for (int k = 0; k < kColChunks; ++k) t += part[(size_t)k * cols + c];
-  out[c] = (float)t;
+  if (tid == 0) tickets[blockIdx.x] = 0u;
 }
 
 // label gather
@@ -224,8 +234,11 @@ static void pack_params(dho2g_mlp* m, const float* p, const float* pscale, int h
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
     const int slot = m->ctx->kt_begin();
-    pack_weights_kernel<<<dim3(cdiv(ld.in, 128 * kPackPer), ld.out), 128, 0, st>>>(p + ld.w_off, pscale, ld.in, ld.Pin,
-                                                                                   half, m->WV_hi[t].p, m->WV_lo[t].p);
+    // one wave of resident blocks striding over the rows (short-lived per-row blocks cost more than the copy)
+    const int gx = (int)cdiv(ld.in, 128 * kPackPer);
+    const int gy = std::max(1, std::min(ld.out, m->ctx->sm_count * 16 / gx));
+    pack_weights_kernel<<<dim3(gx, gy), 128, 0, st>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
+                                                      m->WV_hi[t].p, m->WV_lo[t].p);
     DHO2G_LAUNCH();
     // algorithmic bytes: read fp32 (4) + write hi/lo (4)
     m->ctx->kt_end(slot, "pack_params", (double)ld.in * ld.out * 8.0);
@@ -310,10 +323,10 @@ static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool
 static void bias_colsum(dho2g_mlp* m, const bf16* hi, const bf16* lo, int ld, int off, int cols, int B, float* out) {
   dho2g_ctx* ctx = m->ctx;
   m->colpart.ensure((size_t)kColChunks * cols);
+  m->coltickets.ensure(cdiv(cols, 64));  // zeroed at allocation; each launch leaves them zero
   const int slot = ctx->kt_begin();
-  colsum_pairs_kernel<<<dim3(cdiv(cols, 64), kColChunks), dim3(32, 8), 0, ctx->stream>>>(hi, lo, ld, off, cols, B,
-                                                                                          m->colpart.p);
-  colsum_final_kernel<<<cdiv(cols, 128), 128, 0, ctx->stream>>>(m->colpart.p, cols, out);
+  colsum_pairs_kernel<<<dim3(cdiv(cols, 64), kColChunks), dim3(32, 8), 0, ctx->stream>>>(
+      hi, lo, ld, off, cols, B, m->colpart.p, m->coltickets.p, out);
   DHO2G_LAUNCH();
   ctx->kt_end(slot, "bias_colsum", 4.0 * cols * (double)B);  // algorithmic bytes: hi + lo
 }

@@ -25,7 +25,9 @@ def main():
     ap.add_argument("--grad", type=int, default=0)
     ap.add_argument("--splits", type=int, default=0)
     ap.add_argument("--cta", type=int, default=0, help="0 auto, 1 single-CTA, 2 CTA pair")
-    ap.add_argument("--ab", type=int, default=0, help="A/B rounds alternating --cta 1 and 2 (GEMM rows only)")
+    ap.add_argument("--ab", type=int, default=0, help="A/B rounds alternating --abopt values (GEMM rows only)")
+    ap.add_argument("--abopt", default="gemm_cta", help="context option to alternate in the A/B rounds")
+    ap.add_argument("--abvals", default="1,2", help="comma-separated values of --abopt")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     ctx = d.Context(0)
@@ -56,9 +58,9 @@ def main():
     if args.ab:
         run("warm", True)
         for r in range(args.ab):
-            for cta in (1, 2):
-                ctx.set_option("gemm_cta", cta)
-                run(f"r{r}/cta{cta}", True)
+            for val in [int(x) for x in args.abvals.split(",")]:
+                ctx.set_option(args.abopt, val)
+                run(f"r{r}/{args.abopt}={val}", True)
     else:
         run("", False)
     ctx.close()

@@ -72,6 +72,52 @@ def test_gemm3_cta_modes(ctx, M, N, K, cta):
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
 
+@pytest.mark.parametrize("M,N,K0,K1", [(256, 384, 130, 0), (300, 200, 100, 70), (1024, 3584, 448, 512),
+                                       (8, 40, 96, 0)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("pair_n", [128, 256])
+def test_gemm3_pair_tile_width(ctx, M, N, K0, K1, a_mn, b_mn, pair_n):
+    """CTA-pair kernel with 256x128 and 256x256 tiles (K-major / MN-major, two K segments)."""
+    from paper_2505_00982_b200.api import test_gemm_seg
+    rng = np.random.default_rng(M + 3 * N + K0 + K1 + pair_n + 5 * a_mn + b_mn)
+    A0, B0 = rng.standard_normal((M, K0)), rng.standard_normal((N, K0))
+    A1, B1 = rng.standard_normal((M, K1)), rng.standard_normal((N, K1))
+    exact = A0 @ B0.T + A1 @ B1.T
+    scale = np.abs(A0) @ np.abs(B0).T + np.abs(A1) @ np.abs(B1).T
+    ctx.set_option("gemm_cta", 2)
+    ctx.set_option("gemm_pair_n", pair_n)
+    try:
+        c1 = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
+        c2 = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
+    finally:
+        ctx.set_option("gemm_cta", 0)
+        ctx.set_option("gemm_pair_n", 0)
+    assert (c1 == c2).all()
+    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 3584, 512), (3000, 700, 300), (512, 1000, 4096)])
+@pytest.mark.parametrize("phases", [1, 2, 3, 5])
+def test_gemm3_pair_phases(ctx, M, N, K, phases):
+    """CTA-pair kernel walking the tile space in L2 phases (groups of m- or n-tiles, stream-K inside each):
+    exact to 2e-5 of sum |a||b| and bitwise repeatable."""
+    rng = np.random.default_rng(M + N + K + phases)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    exact = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
+    ctx.set_option("gemm_cta", 2)
+    ctx.set_option("gemm_phases", phases)
+    try:
+        c1 = run_gemm(ctx, A, B, 0)
+        c2 = run_gemm(ctx, A, B, 0)
+    finally:
+        ctx.set_option("gemm_cta", 0)
+        ctx.set_option("gemm_phases", 0)
+    assert (c1 == c2).all()
+    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
+
+
 @pytest.mark.parametrize("M,N,K0,K1", [(256, 384, 130, 0), (300, 200, 100, 70), (700, 260, 64, 200),
                                        (1024, 512, 1024, 1024)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
