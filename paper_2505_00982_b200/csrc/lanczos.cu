@@ -321,7 +321,7 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
             s_fail = 1;
           } else {
             double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-            double r = hypot(g, 1.0);
+            double r = sqrt(fma(g, g, 1.0));
             g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
             double s = 1.0, c = 1.0, p = 0.0;
             bool under = false;
@@ -329,7 +329,9 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
             for (int ii = mm - 1; ii >= l; --ii) {
               const double f = s * e[ii];
               const double b = c * e[ii];
-              r = hypot(f, g);
+              // sqrt(f^2 + g^2) instead of hypot: the entries of a Lanczos tridiagonal are O(||H||), far
+              // from fp64 over/underflow, and the serial chain is this kernel's latency
+              r = sqrt(fma(f, f, g * g));
               e[ii + 1] = r;
               if (r == 0.0) {
                 d[ii + 1] -= p;
@@ -337,8 +339,9 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
                 under = true;
                 break;
               }
-              s = f / r;
-              c = g / r;
+              const double ir = 1.0 / r;
+              s = f * ir;
+              c = g * ir;
               g = d[ii + 1] - p;
               r = (d[ii] - g) * s + 2.0 * c * b;
               p = s * r;
