@@ -63,6 +63,10 @@ extern unsigned long long g_launches;
 __host__ __device__ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
 
+// Incremented by every device (re)allocation: captured CUDA graphs hold raw pointers and are rebuilt
+// when it changes.
+extern unsigned long long g_alloc_gen;
+
 // RAII device allocation (cudaMalloc, zero-initialised).
 template <typename T>
 struct DevBuf {
@@ -83,6 +87,7 @@ struct DevBuf {
     n = count;
     if (count == 0) return;
     DHO2G_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    ++g_alloc_gen;
     // cudaMemset runs on the legacy stream, which does not order with the library's non-blocking
     // stream: complete it before any kernel can touch the buffer.
     DHO2G_CUDA(cudaMemset(p, 0, count * sizeof(T)));

@@ -9,6 +9,10 @@
 #include "internal.h"
 
 namespace dho2g {
+unsigned long long g_alloc_gen = 0;
+}  // namespace dho2g
+
+namespace dho2g {
 
 unsigned long long g_launches = 0;
 

@@ -44,7 +44,7 @@ struct dho2g_ctx {
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
-  int use_graphs = 0;
+  int use_graphs = 1;     // capture the Lanczos refresh into a CUDA graph (world 1)
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -248,6 +248,19 @@ struct dho2g_lanczos {
   dho2g::DevBuf<float> xU;
   dho2g::DevBuf<int> xstatus;
   double ms = 0.0;
+  // CUDA graph of the refresh launch sequence (world 1)
+  cudaGraphExec_t gexec = nullptr;
+  const void* gop = nullptr;
+  size_t gm = 0;
+  unsigned long long ggen = 0;
+  const unsigned* gflags = nullptr;
+  bool seen_eager = false, graph_failed = false;
+  unsigned long long glaunches = 0;  // kernel launches recorded in the graph
+  dho2g::DevBuf<uint64_t> seed_dev;
+  dho2g::HostBuf<uint64_t> seed_host;
+  ~dho2g_lanczos() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
 };
 
 struct dho2g_ese {

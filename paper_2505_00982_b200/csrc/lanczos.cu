@@ -35,8 +35,10 @@ __device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t i) {
   return z ^ (z >> 31);
 }
 
-__global__ void gauss_kernel(uint64_t s0, size_t begin, size_t rows, float* __restrict__ out, double* __restrict__ part) {
+__global__ void gauss_kernel(uint64_t s0, const uint64_t* __restrict__ s0p, size_t begin, size_t rows,
+                             float* __restrict__ out, double* __restrict__ part) {
   __shared__ double sh[32];
+  if (s0p) s0 = *s0p;  // graph replays read the refresh's seed from device memory
   double ss = 0.0;
   for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < rows; r += (size_t)gridDim.x * blockDim.x) {
     const size_t i = begin + r;
@@ -611,22 +613,21 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   lz->ticket.alloc(2);
 }
 
-void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
+// The refresh's launch sequence (v1, then m x [HVP, GS pass 1, GS pass 2, decide] with device-resident
+// predication) depends on the host only through the seed, so at world 1 it is captured once into a CUDA
+// graph and replayed; the seed goes through device memory. Captures are invalidated by any device
+// (re)allocation (pointers baked into the graph) and the split-K / stream-K flags are cleared inside the
+// graph (their epoch values are baked too).
+static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const uint64_t* s0p) {
   dho2g_ctx* ctx = lz->ctx;
   cudaStream_t st = ctx->stream;
   const size_t m = lz->m;
   const int world = ctx->world;
   const int stride = (int)(m + 2);
-  cudaEvent_t e0, e1;
-  DHO2G_CUDA(cudaEventCreate(&e0));
-  DHO2G_CUDA(cudaEventCreate(&e1));
-  DHO2G_CUDA(cudaEventRecord(e0, st));
-
   // v1 (lanczos.cpp:18-26) into column 0, raw; sigma_0 = 1/||v1||
   {
     const int gb = grid_for(ctx, lz->rows, 256);
-    gauss_kernel<<<gb, 256, 0, st>>>(seed * 0x9e3779b97f4a7c15ULL + 0x1234567ULL, lz->begin, lz->rows, lz->D.p,
-                                     lz->part.p);
+    gauss_kernel<<<gb, 256, 0, st>>>(s0, s0p, lz->begin, lz->rows, lz->D.p, lz->part.p);
     gauss_norm_kernel<<<1, 32, 0, st>>>(lz->part.p, gb, lz->rankp.p);
     DHO2G_LAUNCH();
     ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);
@@ -673,6 +674,82 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
                                          lz->opts.reorth_safeguard, lz->opts.safeguard_ratio, lz->opts.breakdown_rtol);
       DHO2G_LAUNCH();
     }
+  }
+}
+
+static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
+  dho2g_ctx* ctx = lz->ctx;
+  cudaStream_t st = ctx->stream;
+  if (!ctx->use_graphs || ctx->world != 1 || ctx->ktimers || op->kind == 3 || lz->graph_failed) return false;
+  lz->seed_dev.ensure(1);
+  lz->seed_host.ensure(1);
+  const bool valid = lz->gexec && lz->gop == op && lz->gm == lz->m && lz->ggen == g_alloc_gen &&
+                     lz->gflags == ctx->gemm_flags.p;
+  if (!valid) {
+    if (!lz->seen_eager) return false;  // first refresh runs eagerly (allocates every buffer)
+    if (lz->gexec) {
+      cudaGraphExecDestroy(lz->gexec);
+      lz->gexec = nullptr;
+    }
+    const unsigned long long gen0 = g_alloc_gen;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      lz->graph_failed = true;
+      return false;
+    }
+    bool ok = true;
+    const unsigned long long l0 = g_launches;
+    try {
+      if (ctx->gemm_flags.p)
+        DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), st));
+      lanczos_enqueue(lz, op, 0, lz->seed_dev.p);
+    } catch (...) {
+      ok = false;
+    }
+    const cudaError_t ec = cudaStreamEndCapture(st, &g);
+    if (!ok || ec != cudaSuccess || g == nullptr || g_alloc_gen != gen0) {
+      cudaGetLastError();
+      if (g) cudaGraphDestroy(g);
+      lz->graph_failed = true;
+      return false;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&lz->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      lz->gexec = nullptr;
+      lz->graph_failed = true;
+      return false;
+    }
+    lz->gop = op;
+    lz->gm = lz->m;
+    lz->ggen = g_alloc_gen;
+    lz->gflags = ctx->gemm_flags.p;
+    lz->glaunches = g_launches - l0;
+    g_launches = l0;  // captured, not launched
+    ctx->bump("lanczos_graph_captures", 1);
+  }
+  lz->seed_host.p[0] = s0;
+  DHO2G_CUDA(cudaMemcpyAsync(lz->seed_dev.p, lz->seed_host.p, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  DHO2G_CUDA(cudaGraphLaunch(lz->gexec, st));
+  g_launches += lz->glaunches;  // the graph's kernel launches
+  ctx->bump("lanczos_graph_launches", 1);
+  return true;
+}
+
+void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
+  dho2g_ctx* ctx = lz->ctx;
+  cudaStream_t st = ctx->stream;
+  const size_t m = lz->m;
+  cudaEvent_t e0, e1;
+  DHO2G_CUDA(cudaEventCreate(&e0));
+  DHO2G_CUDA(cudaEventCreate(&e1));
+  DHO2G_CUDA(cudaEventRecord(e0, st));
+  const uint64_t s0 = seed * 0x9e3779b97f4a7c15ULL + 0x1234567ULL;
+  if (!lanczos_graph(lz, op, s0)) {
+    lanczos_enqueue(lz, op, s0, nullptr);
+    lz->seen_eager = true;
   }
   DHO2G_CUDA(cudaEventRecord(e1, st));
   DHO2G_CUDA(cudaMemcpyAsync(&lz->host, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, st));
