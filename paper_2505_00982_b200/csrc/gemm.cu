@@ -95,10 +95,9 @@ __device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float 
   return v;
 }
 
-// Per-thread form (CUDA-core backend): 16 consecutive columns of one row.
-__device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16]) {
+// Per-thread form (CUDA-core backend): 16 consecutive columns of one row; x receives the values.
+__device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16], float (&x)[16]) {
   const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
-  float x[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j], vsc, epi_load(e, row, col0 + j)) : 0.f;
@@ -138,6 +137,12 @@ __device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, con
     sm[rl * 17 + cc] = x;
   }
   __syncwarp();
+  if (e.csum && row0 < e.M && lane < 16 && col0 + lane < e.N) {  // column sums of this 32-row block (rows >= M hold 0)
+    float t = 0.f;
+#pragma unroll 8
+    for (int rl = 0; rl < 32; ++rl) t += sm[rl * 17 + lane];
+    e.csum[(size_t)(row0 >> 5) * e.N + col0 + lane] = t;
+  }
   if (e.mode != EPI_STORE && e.Th) {
     const int row = row0 + lane;
     if (row < e.Bp) {
@@ -153,14 +158,33 @@ __device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, con
 
 namespace {
 // standalone epilogue over an fp32 accumulator matrix (CUDA-core backend)
+// blockDim (8, 32): 32 rows x 128 columns per block, so the 32-row column sums are a block reduction
 __global__ void epi_kernel(Epi e, const float* __restrict__ acc, int ldacc, int rows_pad) {
+  __shared__ float red[32][129];
   const int row = blockIdx.y * blockDim.y + threadIdx.y;
   const int col0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
-  if (row >= rows_pad || col0 >= e.N) return;
-  float v[16];
+  float x[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = (row < e.M && col0 + j < e.N) ? acc[(size_t)row * ldacc + col0 + j] : 0.f;
-  epi_apply16(e, row, col0, v);
+  for (int j = 0; j < 16; ++j) x[j] = 0.f;
+  if (row < rows_pad && col0 < e.N) {
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = (row < e.M && col0 + j < e.N) ? acc[(size_t)row * ldacc + col0 + j] : 0.f;
+    epi_apply16(e, row, col0, v, x);
+  }
+  if (!e.csum || (int)(blockIdx.y * blockDim.y) >= e.M) return;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) red[threadIdx.y][threadIdx.x * 16 + j] = (row < e.M) ? x[j] : 0.f;
+  __syncthreads();
+  if (threadIdx.y == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (col0 + j >= e.N) break;
+      float t = 0.f;
+      for (int rl = 0; rl < 32; ++rl) t += red[rl][threadIdx.x * 16 + j];
+      e.csum[(size_t)blockIdx.y * e.N + col0 + j] = t;
+    }
+  }
 }
 }  // namespace
 
@@ -257,8 +281,8 @@ static void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp&
   gemm3_simt_kernel<<<grid, 256, 0, ctx->stream>>>(M, N, K, kseg, A, B, acc, N);
   DHO2G_LAUNCH();
   const int rows_pad = e.mode == EPI_STORE ? M : std::max(M, e.Bp);
-  dim3 eb(8, 16);
-  dim3 eg(cdiv(cdiv(N, 16), 8), cdiv(rows_pad, 16));
+  dim3 eb(8, 32);
+  dim3 eg(cdiv(cdiv(N, 16), 8), cdiv(rows_pad, 32));
   epi_kernel<<<eg, eb, 0, ctx->stream>>>(e, acc, N, rows_pad);
   DHO2G_LAUNCH();
 }

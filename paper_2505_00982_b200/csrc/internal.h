@@ -110,6 +110,7 @@ struct dho2g_mlp {
   dho2g::DevBuf<int64_t> idx;
   dho2g::DevBuf<double> red;
   dho2g::DevBuf<double> colpart;      // bias column-sum partials
+  dho2g::DevBuf<float> csum;          // per-32-row column sums written by the backward epilogues
   dho2g::DevBuf<unsigned> coltickets;  // their per-column-block completion tickets
   const float* w_cur = nullptr;        // params whose W halves are loaded
   const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
@@ -144,7 +145,8 @@ void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);  // acc2 = {sum loss, s
 //  EPI_FWD_OUT output layer: do0: z = acc + bias ; do1: rz = acc + vscale*vbias   (fp32 only)
 //  EPI_BWD     do0: d = acc act'(a_in), u_out = acc ; do1: rd = acc act'(a_in) + u_in (-2 a_in ra_in)
 // writing the fp32 value (f0 / f1, B x N) and its bf16 (hi, lo) split into the row-major pair
-// buffer (R, half hR) and the transposed pair buffer (T, half hT; rows [M, Bp) get zeros).
+// buffer (R, half hR) and the transposed pair buffer (T, half hT; rows [M, Bp) get zeros), and, when
+// csum is set, fixed-order column sums of the values per 32-row block (the next layer's bias block).
 enum EpiMode { EPI_STORE = 0, EPI_FWD = 1, EPI_FWD_OUT = 2, EPI_BWD = 3 };
 struct Epi {
   int mode, M, N;
@@ -168,6 +170,7 @@ struct Epi {
   bf16* Th;
   bf16* Tl;
   int ldT, Bp, hT;
+  float* csum;  // optional: per 32-row block column sums of the epilogue values, [ceil(M/32)][N]
 };
 // One GEMM operand: a (hi, lo) bf16 pair buffer read through a TMA-style window. K-major: rows are
 // the M (or N) index, K contiguous; MN-major: rows are the K index, M (or N) contiguous. The K range

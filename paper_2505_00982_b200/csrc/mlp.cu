@@ -201,6 +201,16 @@ __global__ void colsum_pairs_kernel(const bf16* __restrict__ hi, const bf16* __r
   if (tid == 0) tickets[blockIdx.x] = 0u;
 }
 
+// Bias block from the per-32-row column sums the producing epilogue wrote: out[o] = sum_rb csum[rb][o]
+// (fixed order, fp64).
+__global__ void csum_final_kernel(const float* __restrict__ csum, int nrb, int cols, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  double t = 0.0;
+  for (int rb = 0; rb < nrb; ++rb) t += (double)csum[(size_t)rb * cols + c];
+  out[c] = (float)t;
+}
+
 // label gather
 __global__ void gather_labels_kernel(int B, const float* __restrict__ y, const int64_t* __restrict__ idx,
                                      float* __restrict__ out) {
@@ -339,6 +349,13 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   dho2g_ctx* ctx = m->ctx;
   const int L = m->L;
   const int Bi = (int)B;
+  const int nrb = (int)cdiv(B, 32);
+  // the bias block of layer t is the batch sum of level t+1's deltas: the epilogue that writes them (layer
+  // t+1's backward GEMM) also writes per-32-row column sums into m->csum; the output level's deltas come
+  // from the loss kernel and are summed by colsum_pairs_kernel
+  const bool need_bias = do1 || wgrad;
+  if (need_bias) m->csum.ensure((size_t)nrb * m->smax);
+  int csum_level = -1;
   for (int t = L - 1; t >= 0; --t) {
     const LayerDesc& ld = m->layers[t];
     const int j = t + 1;
@@ -368,7 +385,14 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.ldc = ld.in;
       e.alpha = 1.0f;
       gemm3x(ctx, ld.out, ld.in, K, kseg, A, X, e);
-      bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off);
+      if (csum_level == j) {
+        const int slot = ctx->kt_begin();
+        csum_final_kernel<<<cdiv(ld.out, 128), 128, 0, ctx->stream>>>(m->csum.p, nrb, ld.out, out + ld.b_off);
+        DHO2G_LAUNCH();
+        ctx->kt_end(slot, "bias_sum", 4.0 * nrb * (double)ld.out);
+      } else {
+        bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off);
+      }
     }
     if (t == 0) continue;
     for (int pass = 0; pass < 2; ++pass) {
@@ -388,6 +412,10 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.f0 = nullptr;  // fp32 deltas of hidden levels are not re-read (bias blocks come from the pairs)
       e.f1 = nullptr;
       e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Din; e.hR = r ? 1 : 0;
+      // column sums of the deltas this epilogue writes: rd for the Hessian's bias block, d for the gradient's
+      const bool sums = (r && do1) || (!r && wgrad && !do1);
+      e.csum = sums ? m->csum.p : nullptr;
+      if (sums) csum_level = t;
       // A = [d | rd] (K-major, K = out per segment), W = [V | W] rows o read MN-major (K = out)
       GOp A = gop_k(m->DR_hi[j].p, m->DR_lo[j].p, ldD, r ? ldD : ld.Dout, Bi);
       GOp W{};
