@@ -102,3 +102,26 @@ def test_trainer_diverges_loudly(ctx):
     cfg = d.TrainerConfig(kind="sgd", base=d.BaseConfig("sgd", lr=1e30), epochs=3, batch_size=8)
     with pytest.raises((d.TrainingDiverged, d.NumericError)):
         d.train(ctx, cfg, mlp, d.Dataset(X, y, 4, 7), mlp.init_params(1) * 10)
+
+
+def test_graph_refresh_bitwise_equal_to_eager(ctx):
+    """The CUDA-graph replay of the Lanczos refresh (captured on the second refresh) launches the same
+    kernels as the eager path: trajectories with 4 refreshes are bitwise identical."""
+    from oracle.bindings import blobs_dataset
+    sizes = [24, 32, 32, 5]
+    X, y = blobs_dataset(160, 24, 5, seed=4)
+    w0 = d.MlpOracle(ctx, sizes).init_params(3)
+    out = []
+    for graphs in (0, 1):
+        ctx.set_option("graphs", graphs)
+        try:
+            mlp = d.MlpOracle(ctx, sizes)
+            cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig("adam"), k=4, l=1, outer_rounds=4, inner_epochs=1,
+                                  epochs=1, batch_size=16, curvature_batch=64, seed=5)
+            out.append(d.train(ctx, cfg, mlp, d.Dataset(X, y, 5, 7), w0, workers=2))
+        finally:
+            ctx.set_option("graphs", 1)
+    assert out[0].ese_refreshes == out[1].ese_refreshes == 4
+    assert (out[0].w_final == out[1].w_final).all()
+    assert (out[0].loss == out[1].loss).all()
+    assert ctx.stat("lanczos_graph_launches") >= 2
