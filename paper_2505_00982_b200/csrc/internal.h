@@ -45,6 +45,7 @@ struct dho2g_ctx {
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
   int use_graphs = 1;     // capture the Lanczos refresh into a CUDA graph (world 1)
+  int ritz_tc = 1;        // Ritz vectors on the tensor cores when supported (0: CUDA-core kernel)
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -248,7 +249,7 @@ struct dho2g_lanczos {
   dho2g::LzDev host{};          // copy after run
   dho2g_lanczos_opts opts{1, 1e-6, 1e-10};
   dho2g::DevBuf<double> xZ, xev, xam, xamall, xpart;  // extract_ese scratch
-  dho2g::DevBuf<float> xU;
+  dho2g::DevBuf<float> xU, xUs;
   dho2g::DevBuf<int> xstatus;
   double ms = 0.0;
   // CUDA graph of the refresh launch sequence (world 1)
@@ -279,6 +280,10 @@ namespace dho2g {
 void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed);
 void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m);
 void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese);
+// Ritz vectors on the tensor cores (3xTF32, ritz_tc.cu); supported for r <= 64, me <= 96.
+bool ritz_tc_supported(int me, int r);
+void ritz_tc(dho2g_ctx* ctx, const float* D, size_t ldd, int me, const float* U, int r, float* V, size_t ldv,
+             size_t rows, DevBuf<float>& uscratch);
 }  // namespace dho2g
 
 // ------------------------------------------------------------------------- optimizer / update

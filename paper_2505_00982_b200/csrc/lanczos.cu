@@ -802,13 +802,17 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   ctx->kt_end(kq, "extract.tql2", 0.0);
   ese->V.ensure(ese->ldv * r);  // padded rows stay zero (Ritz writes rows < rows only)
   const int kr = ctx->kt_begin();
-  for (int c0 = 0; c0 < r; c0 += RC) {
-    const size_t sm = (size_t)me * RC * sizeof(float);
-    if (sm > 48 * 1024)
-      DHO2G_CUDA(cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ritz_kernel<<<one_wave_grid(ritz_kernel, 256, sm, ctx->sm_count, cdiv(cdiv(lz->rows, 2), 256)), 256, sm, st>>>(lz->D.p, lz->ldd, me, U.p, r, c0, ese->V.p, ese->ldv,
-                                                                  lz->rows);
-    DHO2G_LAUNCH();
+  if (ctx->ritz_tc && ritz_tc_supported(me, r)) {
+    ritz_tc(ctx, lz->D.p, lz->ldd, me, U.p, r, ese->V.p, ese->ldv, lz->rows, lz->xUs);
+  } else {
+    for (int c0 = 0; c0 < r; c0 += RC) {
+      const size_t sm = (size_t)me * RC * sizeof(float);
+      if (sm > 48 * 1024)
+        DHO2G_CUDA(cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      ritz_kernel<<<one_wave_grid(ritz_kernel, 256, sm, ctx->sm_count, cdiv(cdiv(lz->rows, 2), 256)), 256, sm, st>>>(
+          lz->D.p, lz->ldd, me, U.p, r, c0, ese->V.p, ese->ldv, lz->rows);
+      DHO2G_LAUNCH();
+    }
   }
   ctx->kt_end(kr, "extract.ritz", 4.0 * (double)lz->rows * (double)(me + r));
   DevBuf<double>& am = lz->xam;

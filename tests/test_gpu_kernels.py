@@ -428,3 +428,31 @@ def test_admm_round(ctx, port):
     assert np.max(np.abs(st.pi - pi_ref)) <= 1e-5 * np.max(np.abs(pi_ref))
     with pytest.raises(d.ArgumentError):
         d.make_admm_state(w_a, 0.0)
+
+
+@pytest.mark.parametrize("n,m,k,l", [(50_000, 80, 32, 0), (70_001, 40, 10, 3), (9_000, 96, 50, 14), (4_096, 20, 1, 0),
+                                     (30_000, 100, 20, 0)])
+def test_ritz_tensor_core_matches_cuda_core(ctx, port, n, m, k, l):
+    """Ritz vectors V = D U' on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, ~2^-21 of sum |D||U'|)
+    agree with the fp32 CUDA-core kernel: entries within 1e-5 of max|V| (the Ritz combinations cancel,
+    so entry-relative bounds are meaningless) and projectors within 1e-5 (SURVEY §8d bar: 1e-4).
+    m = 100 exceeds the tensor-core tile and takes the CUDA-core path."""
+    spec = 1.0 + (np.arange(n) % 997) * 0.37 + 0.01 * port.rng_normal(3, n)
+    op = d.diagonal_operator(ctx, spec)
+    st = d.lanczos_distributed(ctx, m, op, n, 17)
+    ke = min(k, st.iterations)
+    le = min(l, st.iterations - ke)
+    out = []
+    for tc in (0, 1):
+        ctx.set_option("ritz_tc", tc)
+        try:
+            ese = d.extract_ese_distributed(ctx, st, ke, le)
+            out.append((ese.eigvals, ese.eigvecs_shard(n)))
+        finally:
+            ctx.set_option("ritz_tc", 1)
+    assert (out[0][0] == out[1][0]).all()
+    V0, V1 = out[0][1], out[1][1]
+    assert np.max(np.abs(V1 - V0)) <= 1e-5 * np.max(np.abs(V0))
+    G = V0.T @ V1  # ||V1 V1^T - V0 V0^T||_F^2 = tr(V0^T V0)^2-ish terms, evaluated without n x n matrices
+    proj2 = np.sum((V0.T @ V0) ** 2) + np.sum((V1.T @ V1) ** 2) - 2 * np.sum(G ** 2)
+    assert np.sqrt(max(proj2, 0.0)) <= 1e-5
