@@ -130,7 +130,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     if (k == "gemm") ctx->gemm_backend = (int)value;
     else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
     else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
-    else if (k == "gemm_phases") ctx->gemm_phases = (int)value;
+    else if (k == "gemm_dp") ctx->gemm_dp = (int)value;
     else if (k == "gemm_pair_n") ctx->gemm_pair_n = (int)value;
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;

@@ -687,57 +687,52 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
   } while (!done);
 }
 
-// The tile space is walked in `phases` (groups of m-tiles or of n-tiles, pdim = 0 / 1) so that the operand
-// bytes touched concurrently by all pairs fit in L2; stream-K runs inside each phase.
+// Tile schedule (m-major tile order, tile = m * nt + n): the first `dp` tiles are data-parallel — worker
+// w takes whole tiles w, w + W, ..., so the tiles in flight at any time are consecutive and share their
+// A rows (a working set that fits L2; measured 9x operand re-reads from HBM on the gradient GEMMs with
+// stream-K over the whole space); the remaining tiles (about one wave) are stream-K: the
+// (tile, k-block) space is cut into W equal contiguous ranges.
 struct Work {
   int mt, nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
-  int pdim, phases;
-  __device__ __forceinline__ void prange(int p, int& lo, int& cnt) const {
-    const int D = pdim ? nt : mt;
-    lo = D * p / phases;
-    cnt = D * (p + 1) / phases - lo;
-  }
-  __device__ __forceinline__ long long ptotal(int p) const {
-    int lo, cnt;
-    prange(p, lo, cnt);
-    return (long long)(pdim ? mt * cnt : cnt * nt) * nkb;
-  }
-  __device__ __forceinline__ long long begin(int p, int w) const { return ptotal(p) * w / workers; }
+  int dp;                                      // data-parallel tiles
+  __device__ __forceinline__ long long sk_total() const { return (long long)(mt * nt - dp) * nkb; }
+  __device__ __forceinline__ long long begin(int /*phase*/, int w) const { return sk_total() * w / workers; }
 };
 struct Seg {
-  int phase, tile, k0, k1;  // tile: index inside the phase
+  int phase, tile, k0, k1;  // phase 0: data-parallel (tile = global index); 1: stream-K (tile = index after dp)
   int mtile, ntile;
 };
-// Iterates one worker's segments over all phases.
+// Iterates one worker's segments: its data-parallel tiles, then its stream-K range.
 struct Cursor {
-  int p, w;
+  int p, w, t;
   long long a, end;
   __device__ __forceinline__ void init(const Work& wk, int worker) {
     w = worker;
     p = 0;
-    a = wk.begin(0, w);
-    end = wk.begin(0, w + 1);
+    t = worker;
+    a = wk.begin(1, w);
+    end = wk.begin(1, w + 1);
   }
   __device__ __forceinline__ bool next(const Work& wk, Seg& s) {
-    while (a >= end) {
-      if (++p >= wk.phases) return false;
-      a = wk.begin(p, w);
-      end = wk.begin(p, w + 1);
-    }
-    s.phase = p;
-    s.tile = (int)(a / wk.nkb);
-    s.k0 = (int)(a - (long long)s.tile * wk.nkb);
-    s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
-    a += s.k1 - s.k0;
-    int lo, cnt;
-    wk.prange(p, lo, cnt);
-    if (wk.pdim) {
-      s.mtile = s.tile / cnt;
-      s.ntile = lo + s.tile % cnt;
+    int g;
+    if (p == 0 && t < wk.dp) {
+      s.phase = 0;
+      s.tile = g = t;
+      s.k0 = 0;
+      s.k1 = wk.nkb;
+      t += wk.workers;
     } else {
-      s.mtile = lo + s.tile / wk.nt;
-      s.ntile = s.tile % wk.nt;
+      p = 1;
+      if (a >= end) return false;
+      s.phase = 1;
+      s.tile = (int)(a / wk.nkb);
+      s.k0 = (int)(a - (long long)s.tile * wk.nkb);
+      s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
+      a += s.k1 - s.k0;
+      g = wk.dp + s.tile;
     }
+    s.mtile = g / wk.nt;
+    s.ntile = g % wk.nt;
     return true;
   }
 };
@@ -962,11 +957,15 @@ int max_pairs(dho2g_ctx* ctx) {
 template <bool AMN, bool BMN, int NT>
 int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
   const int pairs = max_pairs<AMN, BMN, NT>(ctx);
-  // every worker gets >= 4 k-blocks of its smallest phase (shorter segments are mostly fixup traffic)
-  const long long per_phase = (long long)wk.mt * wk.nt * wk.nkb / wk.phases;
-  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, per_phase / 4));
-  ctx->gemm_ws.ensure((size_t)wk.phases * wk.workers * 2 * PART_MAX);
-  ctx->gemm_flags.ensure((size_t)wk.phases * wk.workers * 2 + 16);
+  // every worker gets >= 4 k-blocks (shorter segments are mostly fixup traffic)
+  const long long tiles = (long long)wk.mt * wk.nt;
+  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, tiles * wk.nkb / 4));
+  // data-parallel waves, keeping the last ~1-2 waves of tiles for stream-K balancing (option gemm_dp = 0
+  // turns the data-parallel part off)
+  const long long waves = tiles / wk.workers;
+  wk.dp = (ctx->gemm_dp && waves >= 2) ? (int)((waves - 1) * wk.workers) : 0;
+  ctx->gemm_ws.ensure((size_t)2 * wk.workers * 2 * PART_MAX);
+  ctx->gemm_flags.ensure((size_t)2 * wk.workers * 2 + 16);
   unsigned epoch = ++ctx->gemm_epoch;
   if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
@@ -988,14 +987,7 @@ int run_nt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GO
   wk.kseg = kseg;
   wk.nround = B.mn_major ? 128 : 16;
   wk.workers = 1;
-  // L2 phases (off by default: measured on the HVP shapes, the extra stream-K fixups of more, smaller
-  // per-phase ranges cost more than the avoided operand re-reads; kept as option gemm_phases)
-  {
-    const double a_bytes = 4.0 * M * K, b_bytes = 4.0 * N * K;
-    wk.pdim = b_bytes >= a_bytes ? 1 : 0;
-    const int ph = ctx->gemm_phases > 0 ? ctx->gemm_phases : 1;
-    wk.phases = std::max(1, std::min(ph, wk.pdim ? wk.nt : wk.mt));
-  }
+  wk.dp = 0;  // set in launch() once the worker count is known
   CUtensorMap maps[4];
   op_maps(ctx->encode_fn, A, maps[0], maps[1]);
   op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2);

@@ -39,7 +39,7 @@ struct dho2g_ctx {
   int gemm_backend = 0;  // 0 tcgen05, 1 CUDA-core reference kernel
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
-  int gemm_phases = 0;   // pair kernel L2 phases: 0/-1 off, k > 0 forced
+  int gemm_dp = 1;       // pair kernel: data-parallel waves before the stream-K remainder (0: all stream-K)
   int gemm_pair_n = 0;   // pair kernel tile width: 0 auto, 128, 256
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;

@@ -96,24 +96,24 @@ def test_gemm3_pair_tile_width(ctx, M, N, K0, K1, a_mn, b_mn, pair_n):
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(1024, 3584, 512), (3000, 700, 300), (512, 1000, 4096)])
-@pytest.mark.parametrize("phases", [1, 2, 3, 5])
-def test_gemm3_pair_phases(ctx, M, N, K, phases):
-    """CTA-pair kernel walking the tile space in L2 phases (groups of m- or n-tiles, stream-K inside each):
-    exact to 2e-5 of sum |a||b| and bitwise repeatable."""
-    rng = np.random.default_rng(M + N + K + phases)
+@pytest.mark.parametrize("M,N,K", [(4096, 4096, 256), (6000, 2500, 300), (1024, 3584, 512), (8192, 768, 96)])
+@pytest.mark.parametrize("dp", [0, 1])
+def test_gemm3_pair_dp_stream_k(ctx, M, N, K, dp):
+    """CTA-pair kernel schedule: data-parallel waves of whole tiles, then stream-K over the remainder
+    (dp = 0: stream-K over everything). Exact to 2e-5 of sum |a||b| and bitwise repeatable."""
+    rng = np.random.default_rng(M + N + K + dp)
     A = rng.standard_normal((M, K)).astype(np.float32)
     B = rng.standard_normal((N, K)).astype(np.float32)
     exact = A.astype(np.float64) @ B.astype(np.float64).T
     scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
     ctx.set_option("gemm_cta", 2)
-    ctx.set_option("gemm_phases", phases)
+    ctx.set_option("gemm_dp", dp)
     try:
         c1 = run_gemm(ctx, A, B, 0)
         c2 = run_gemm(ctx, A, B, 0)
     finally:
         ctx.set_option("gemm_cta", 0)
-        ctx.set_option("gemm_phases", 0)
+        ctx.set_option("gemm_dp", 1)
     assert (c1 == c2).all()
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
