@@ -261,6 +261,9 @@ def run_ours(args, rank, world, dist):
     # ---- the same K steps again (fresh trainer, same warm-up) with CUDA-event timers around every kernel
     # launch on the library stream: per-kernel device times for the roofline and the step breakdown. The
     # timers cost host time per launch, so they are kept out of the `value` pass above.
+    # Kernels are serialised in this pass (no side-lane overlap of the weight-block GEMMs) so that each
+    # kernel's event-timed duration is its own.
+    ctx.set_option("bwd_overlap", 0)
     tr = d.Trainer(ctx, cfg, mlp, data, w0, workers=c["workers"])
     tr.step(args.warmup)
     ctx.synchronize()
@@ -274,6 +277,7 @@ def run_ours(args, rank, world, dist):
     ctx.mark(5)
     ms_inst = max_over_ranks(ctx.elapsed_ms(4, 5))
     ctx.set_option("ktimers", 0)
+    ctx.set_option("bwd_overlap", 1)
     kstats = ctx.kernel_stats()
     tr.close()
 
@@ -354,8 +358,9 @@ def run_ours(args, rank, world, dist):
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,
             "kernel_timers": {"note": "per-kernel CUDA-event timers on the library stream during a second pass of "
-                                      "the same K steps (fresh trainer, same warm-up); value comes from the "
-                                      "uninstrumented pass", "ms_per_step_instrumented": ms_inst / args.steps},
+                                      "the same K steps (fresh trainer, same warm-up), kernels serialised (the "
+                                      "weight-block GEMMs' side-stream overlap is off in this pass); value comes "
+                                      "from the uninstrumented, overlapped pass", "ms_per_step_instrumented": ms_inst / args.steps},
             "kernels": kern,
             "phases": phases, "gemm_detail": gemm_detail,
             "useful_tflops_per_step": (grad_flops(c["sizes"], c["b"] * c["workers"]) +

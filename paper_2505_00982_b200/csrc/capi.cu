@@ -117,6 +117,11 @@ int dho2g_ctx_destroy(dho2g_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->stream2) {
+      cudaStreamSynchronize(ctx->stream2);
+      cudaStreamDestroy(ctx->stream2);
+    }
+    for (cudaEvent_t ev : ctx->lane_events) cudaEventDestroy(ev);
     if (ctx->comm) dho2g::nccl().CommDestroy(ctx->comm);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -131,6 +136,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
     else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
     else if (k == "gemm_dp") ctx->gemm_dp = (int)value;
+    else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
     else if (k == "gemm_pair_n") ctx->gemm_pair_n = (int)value;
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;

@@ -959,7 +959,9 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
   const int pairs = max_pairs<AMN, BMN, NT>(ctx);
   // every worker gets >= 4 k-blocks (shorter segments are mostly fixup traffic)
   const long long tiles = (long long)wk.mt * wk.nt;
-  wk.workers = (int)std::min<long long>(pairs, std::max<long long>(1, tiles * wk.nkb / 4));
+  ctx->pairs_total = pairs;
+  const int cap = ctx->gemm_worker_cap > 0 ? std::min(ctx->gemm_worker_cap, pairs) : pairs;
+  wk.workers = (int)std::min<long long>(cap, std::max<long long>(1, tiles * wk.nkb / 4));
   // data-parallel waves, keeping the last ~1-2 waves of tiles for stream-K balancing (option gemm_dp = 0
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;

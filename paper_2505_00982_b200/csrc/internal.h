@@ -40,6 +40,13 @@ struct dho2g_ctx {
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
   int gemm_dp = 1;       // pair kernel: data-parallel waves before the stream-K remainder (0: all stream-K)
+  int gemm_worker_cap = 0;  // pair kernel: at most this many CTA pairs (0: all co-resident pairs)
+  int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
+  cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
+  dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
+  dho2g::DevBuf<unsigned> gemm_flags2;
+  std::vector<cudaEvent_t> lane_events;           // fork / join events (created on first use)
+  int pairs_total = 0;                            // co-resident CTA pairs of the pair kernel
   int gemm_pair_n = 0;   // pair kernel tile width: 0 auto, 128, 256
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;
@@ -258,6 +265,7 @@ struct dho2g_lanczos {
   size_t gm = 0;
   unsigned long long ggen = 0;
   const unsigned* gflags = nullptr;
+  const unsigned* gflags2 = nullptr;
   bool seen_eager = false, graph_failed = false;
   unsigned long long glaunches = 0;  // kernel launches recorded in the graph
   dho2g::DevBuf<uint64_t> seed_dev;

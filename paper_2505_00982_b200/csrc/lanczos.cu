@@ -684,7 +684,7 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
   lz->seed_dev.ensure(1);
   lz->seed_host.ensure(1);
   const bool valid = lz->gexec && lz->gop == op && lz->gm == lz->m && lz->ggen == g_alloc_gen &&
-                     lz->gflags == ctx->gemm_flags.p;
+                     lz->gflags == ctx->gemm_flags.p && lz->gflags2 == ctx->gemm_flags2.p;
   if (!valid) {
     if (!lz->seen_eager) return false;  // first refresh runs eagerly (allocates every buffer)
     if (lz->gexec) {
@@ -703,6 +703,8 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
     try {
       if (ctx->gemm_flags.p)
         DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), st));
+      if (ctx->gemm_flags2.p)  // the side lane's split / stream-K flags (baked epochs too)
+        DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags2.p, 0, ctx->gemm_flags2.n * sizeof(unsigned), st));
       lanczos_enqueue(lz, op, 0, lz->seed_dev.p);
     } catch (...) {
       ok = false;
@@ -726,6 +728,7 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
     lz->gm = lz->m;
     lz->ggen = g_alloc_gen;
     lz->gflags = ctx->gemm_flags.p;
+    lz->gflags2 = ctx->gemm_flags2.p;
     lz->glaunches = g_launches - l0;
     g_launches = l0;  // captured, not launched
     ctx->bump("lanczos_graph_captures", 1);

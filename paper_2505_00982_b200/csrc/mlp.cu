@@ -341,6 +341,35 @@ static void bias_colsum(dho2g_mlp* m, const bf16* hi, const bf16* lo, int ld, in
   ctx->kt_end(slot, "bias_colsum", 4.0 * cols * (double)B);  // algorithmic bytes: hi + lo
 }
 
+// Side lane: while active, the library's launches go to ctx->stream2 with the second GEMM workspace and a
+// CTA-pair budget, so a GEMM issued here runs concurrently with one issued on the main stream.
+struct SideLane {
+  dho2g_ctx* c;
+  cudaStream_t main;
+  int cap_saved;
+  SideLane(dho2g_ctx* ctx, int cap) : c(ctx), main(ctx->stream), cap_saved(ctx->gemm_worker_cap) {
+    c->stream = c->stream2;
+    std::swap(c->gemm_ws, c->gemm_ws2);
+    std::swap(c->gemm_flags, c->gemm_flags2);
+    c->gemm_worker_cap = cap;
+  }
+  ~SideLane() {
+    c->stream = main;
+    std::swap(c->gemm_ws, c->gemm_ws2);
+    std::swap(c->gemm_flags, c->gemm_flags2);
+    c->gemm_worker_cap = cap_saved;
+  }
+};
+
+static cudaEvent_t lane_event(dho2g_ctx* ctx, size_t i) {
+  while (ctx->lane_events.size() <= i) {
+    cudaEvent_t ev;
+    DHO2G_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ctx->lane_events.push_back(ev);
+  }
+  return ctx->lane_events[i];
+}
+
 // Backward pass. do0: deltas d (U GEMMs + fused act' epilogue) and, if wgrad, the gradient blocks.
 // do1: R-deltas (RU GEMMs + fused R-epilogue) and the Hessian blocks into `out`. The weight blocks
 // are GEMMs over the batch (both operands MN-major windows of the row-major pair buffers); the bias
@@ -351,16 +380,29 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   const int Bi = (int)B;
   const int nrb = (int)cdiv(B, 32);
   // the bias block of layer t is the batch sum of level t+1's deltas: the epilogue that writes them (layer
-  // t+1's backward GEMM) also writes per-32-row column sums into m->csum; the output level's deltas come
-  // from the loss kernel and are summed by colsum_pairs_kernel
+  // t+1's backward GEMM) also writes per-32-row column sums into m->csum (two buffers, by level parity);
+  // the output level's deltas come from the loss kernel and are summed by colsum_pairs_kernel
   const bool need_bias = do1 || wgrad;
-  if (need_bias) m->csum.ensure((size_t)nrb * m->smax);
+  if (need_bias) m->csum.ensure((size_t)2 * nrb * m->smax);
+  auto csum_buf = [&](int level) { return m->csum.p + (size_t)(level & 1) * nrb * m->smax; };
+  // Weight blocks (and bias blocks) of layer t only read level t+1's deltas and level t's activations, so
+  // they run on the side lane concurrently with the delta GEMM of layer t (main lane), the two sharing
+  // the CTA pairs in proportion to their flops. Fork: the side lane waits for level t+1's deltas; the
+  // main lane's next delta GEMM waits for the bias kernel that reads the csum buffer it will overwrite;
+  // join at the end.
+  const bool overlap = need_bias && ctx->bwd_overlap && ctx->gemm_backend == 0 && ctx->world >= 1 && L > 1;
+  if (overlap && !ctx->stream2) DHO2G_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+  size_t evn = 0;
+  cudaEvent_t bias_done = nullptr;
   int csum_level = -1;
   for (int t = L - 1; t >= 0; --t) {
     const LayerDesc& ld = m->layers[t];
     const int j = t + 1;
     const int ldD = 2 * ld.Dout, ldA = 2 * ld.Pin;
-    if (do1 || wgrad) {
+    // flops of this layer's delta GEMM (0 at t = 0) and weight GEMM, for the CTA-pair split
+    const double f_delta = t == 0 ? 0.0 : (double)Bi * ld.in * (do1 ? 2.0 * ld.Dout : (double)ld.out);
+    const double f_weight = (double)ld.out * ld.in * (do1 && t > 0 ? 2.0 * Bi : (double)Bi);
+    if (need_bias) {
       GOp A{}, X{};
       A.hi = m->DR_hi[j].p; A.lo = m->DR_lo[j].p; A.ld = ldD; A.mn_major = 1; A.inner = ldD; A.outer = Bi;
       X.hi = m->AR_hi[t].p; X.lo = m->AR_lo[t].p; X.ld = ldA; X.mn_major = 1; X.inner = ldA; X.outer = Bi;
@@ -384,14 +426,41 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.C = out + ld.w_off;
       e.ldc = ld.in;
       e.alpha = 1.0f;
-      gemm3x(ctx, ld.out, ld.in, K, kseg, A, X, e);
-      if (csum_level == j) {
-        const int slot = ctx->kt_begin();
-        csum_final_kernel<<<cdiv(ld.out, 128), 128, 0, ctx->stream>>>(m->csum.p, nrb, ld.out, out + ld.b_off);
-        DHO2G_LAUNCH();
-        ctx->kt_end(slot, "bias_sum", 4.0 * nrb * (double)ld.out);
+      auto weight_and_bias = [&]() {
+        if (csum_level == j) {
+          const int slot = ctx->kt_begin();
+          csum_final_kernel<<<cdiv(ld.out, 128), 128, 0, ctx->stream>>>(csum_buf(j), nrb, ld.out, out + ld.b_off);
+          DHO2G_LAUNCH();
+          ctx->kt_end(slot, "bias_sum", 4.0 * nrb * (double)ld.out);
+        } else {
+          bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off);
+        }
+        if (overlap) {
+          bias_done = lane_event(ctx, evn++);
+          DHO2G_CUDA(cudaEventRecord(bias_done, ctx->stream));
+        }
+        gemm3x(ctx, ld.out, ld.in, K, kseg, A, X, e);
+      };
+      if (overlap) {
+        cudaEvent_t fork = lane_event(ctx, evn++);
+        DHO2G_CUDA(cudaEventRecord(fork, ctx->stream));
+        DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream2, fork, 0));
+        const int pairs = ctx->pairs_total > 0 ? ctx->pairs_total : ctx->sm_count / 2;
+        const int side = t == 0 ? 0 : std::max(1, std::min(pairs - 1, (int)std::lround(pairs * f_weight /
+                                                                                          (f_weight + f_delta))));
+        SideLane lane(ctx, side);
+        weight_and_bias();
       } else {
-        bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off);
+        weight_and_bias();
+      }
+      if (overlap && t > 0) {
+        // the delta GEMM below writes csum_buf(t), which the bias kernel of layer t+1 read (same parity):
+        // wait for the side lane up to this layer's bias kernel (recorded before this layer's weight
+        // GEMM, so the two GEMMs of layer t still run concurrently)
+        DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, bias_done, 0));
+        const int pairs = ctx->pairs_total > 0 ? ctx->pairs_total : ctx->sm_count / 2;
+        const int side = std::max(1, std::min(pairs - 1, (int)std::lround(pairs * f_weight / (f_weight + f_delta))));
+        ctx->gemm_worker_cap = pairs - side;
       }
     }
     if (t == 0) continue;
@@ -414,7 +483,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Din; e.hR = r ? 1 : 0;
       // column sums of the deltas this epilogue writes: rd for the Hessian's bias block, d for the gradient's
       const bool sums = (r && do1) || (!r && wgrad && !do1);
-      e.csum = sums ? m->csum.p : nullptr;
+      e.csum = sums ? csum_buf(t) : nullptr;
       if (sums) csum_level = t;
       // A = [d | rd] (K-major, K = out per segment), W = [V | W] rows o read MN-major (K = out)
       GOp A = gop_k(m->DR_hi[j].p, m->DR_lo[j].p, ldD, r ? ldD : ld.Dout, Bi);
@@ -429,6 +498,12 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
         gemm3x(ctx, Bi, ld.in, ld.Dout + ld.out, ld.Dout, A, W, e);
       }
     }
+    if (overlap) ctx->gemm_worker_cap = 0;
+  }
+  if (overlap) {  // join: the caller's next launches (GS, reductions) read every weight / bias block
+    cudaEvent_t join = lane_event(ctx, evn++);
+    DHO2G_CUDA(cudaEventRecord(join, ctx->stream2));
+    DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, join, 0));
   }
 }
 
