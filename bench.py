@@ -254,6 +254,7 @@ def run_ours(args, rank, world, dist):
     launches = ctx.stat("launches") - launches0
     ms = max_over_ranks(ms)
     n_ref = tr.stat("refreshes") - refreshes0
+    graph_stats = {"captures": ctx.stat("lanczos_graph_captures"), "launches": ctx.stat("lanczos_graph_launches")}
     refresh_ms = (tr.stat("refresh_ms_total") - rms0) / n_ref if n_ref else None
     refresh_ms = max_over_ranks(refresh_ms) if refresh_ms is not None else None
     tr.close()
@@ -357,6 +358,7 @@ def run_ours(args, rank, world, dist):
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,
+            "refresh_graph": graph_stats,
             "kernel_timers": {"note": "per-kernel CUDA-event timers on the library stream during a second pass of "
                                       "the same K steps (fresh trainer, same warm-up), kernels serialised (the "
                                       "weight-block GEMMs' side-stream overlap is off in this pass); value comes "

@@ -63,9 +63,9 @@ extern unsigned long long g_launches;
 __host__ __device__ inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 __host__ __device__ inline size_t cdiv(size_t a, size_t b) { return (a + b - 1) / b; }
 
-// Incremented by every device (re)allocation: captured CUDA graphs hold raw pointers and are rebuilt
-// when it changes.
-extern unsigned long long g_alloc_gen;
+// Incremented when a buffer that a captured refresh graph may reference is (re)allocated (ensure_g,
+// MLP batch buffers, Lanczos state): captured CUDA graphs hold raw pointers and are rebuilt on change.
+extern unsigned long long g_graph_gen;
 
 // RAII device allocation (cudaMalloc, zero-initialised).
 template <typename T>
@@ -87,13 +87,18 @@ struct DevBuf {
     n = count;
     if (count == 0) return;
     DHO2G_CUDA(cudaMalloc(&p, count * sizeof(T)));
-    ++g_alloc_gen;
     // cudaMemset runs on the legacy stream, which does not order with the library's non-blocking
     // stream: complete it before any kernel can touch the buffer.
     DHO2G_CUDA(cudaMemset(p, 0, count * sizeof(T)));
     DHO2G_CUDA(cudaStreamSynchronize(0));
   }
   void ensure(size_t count) { if (count > n) alloc(count); }
+  void ensure_g(size_t count) {  // ensure() for buffers a captured CUDA graph may hold pointers to
+    if (count > n) {
+      alloc(count);
+      ++g_graph_gen;
+    }
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, in
 }  // namespace
 
 static void gemm3_simt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
-  ctx->simt_ws.ensure((size_t)M * N + 16);
+  ctx->simt_ws.ensure_g((size_t)M * N + 16);
   float* acc = ctx->simt_ws.p;
   dim3 grid(cdiv(N, ST_BN), cdiv(M, ST_BM));
   gemm3_simt_kernel<<<grid, 256, 0, ctx->stream>>>(M, N, K, kseg, A, B, acc, N);
@@ -611,8 +611,8 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   unsigned* flags = nullptr;
   unsigned epoch = 0;
   if (sc.splits > 1) {
-    ctx->gemm_ws.ensure((size_t)sc.tiles * BM * BN);
-    ctx->gemm_flags.ensure((size_t)sc.tiles);
+    ctx->gemm_ws.ensure_g((size_t)sc.tiles * BM * BN);
+    ctx->gemm_flags.ensure_g((size_t)sc.tiles);
     ws = ctx->gemm_ws.p;
     flags = ctx->gemm_flags.p;
     epoch = ++ctx->gemm_epoch;
@@ -966,8 +966,8 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;
   wk.dp = (ctx->gemm_dp && waves >= 2) ? (int)((waves - 1) * wk.workers) : 0;
-  ctx->gemm_ws.ensure((size_t)2 * wk.workers * 2 * PART_MAX);
-  ctx->gemm_flags.ensure((size_t)2 * wk.workers * 2 + 16);
+  ctx->gemm_ws.ensure_g((size_t)2 * wk.workers * 2 * PART_MAX);
+  ctx->gemm_flags.ensure_g((size_t)2 * wk.workers * 2 + 16);
   unsigned epoch = ++ctx->gemm_epoch;
   if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
@@ -1010,6 +1010,16 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
 }
 
 }  // namespace tc2
+
+void gemm_presize(dho2g_ctx* ctx) {
+  // both lanes' stream-K partials (2 schedule parts x pairs x 2 CTAs x 128 x 256) and flags; covers the
+  // single-CTA kernel's split-K partials for the small-M GEMMs too
+  const size_t pairs = (size_t)std::max(1, ctx->sm_count / 2);
+  ctx->gemm_ws.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_flags.ensure_g(2 * pairs * 2 + 16);
+  ctx->gemm_ws2.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_flags2.ensure_g(2 * pairs * 2 + 16);
+}
 
 // =============================================================================== dispatch
 void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {

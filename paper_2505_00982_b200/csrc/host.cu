@@ -9,7 +9,7 @@
 #include "internal.h"
 
 namespace dho2g {
-unsigned long long g_alloc_gen = 0;
+unsigned long long g_graph_gen = 0;
 }  // namespace dho2g
 
 namespace dho2g {

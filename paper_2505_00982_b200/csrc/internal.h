@@ -119,6 +119,8 @@ struct dho2g_mlp {
   dho2g::DevBuf<double> red;
   dho2g::DevBuf<double> colpart;      // bias column-sum partials
   dho2g::DevBuf<float> csum;          // per-32-row column sums written by the backward epilogues
+  std::vector<cudaEvent_t> pack_ev;   // per-layer 'packed' events of the side-lane weight packing (+ fork)
+  bool pack_pending = false;          // forward() must wait for pack_ev before each layer
   dho2g::DevBuf<unsigned> coltickets;  // their per-column-block completion tickets
   const float* w_cur = nullptr;        // params whose W halves are loaded
   const float* v_bias_ptr = nullptr;   // direction whose V halves are loaded (bias part read directly)
@@ -127,6 +129,9 @@ struct dho2g_mlp {
   const float* prepared = nullptr;     // w whose v-independent HVP quantities are cached
 
   void ensure_batch(size_t B);
+  ~dho2g_mlp() {
+    for (cudaEvent_t ev : pack_ev) cudaEventDestroy(ev);
+  }
 };
 
 namespace dho2g {
@@ -146,6 +151,8 @@ void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, 
                   size_t ncls, double* acc2);
 
 void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);  // acc2 = {sum loss, sum correct} of last batch
+// Allocates the batch-dependent buffers for batches up to B up front (graph-stable pointers).
+void mlp_presize(dho2g_mlp* m, size_t B);
 
 // GEMM epilogues (gemm.cu). One accumulator element (row, col) of a GEMM tile is turned into:
 //  EPI_STORE   C[row*ldc + col] = alpha*acc (column N-1 -> bias_out[row] when bias_out != null)
@@ -196,6 +203,7 @@ struct GOp {
   int off_in[2], off_out[2];
 };
 GOp gop_k(const bf16* hi, const bf16* lo, int ld, int K, int rows);  // plain K-major, one segment
+void gemm_presize(dho2g_ctx* ctx);  // both lanes' GEMM workspaces at their maximum size
 // acc = A[M x K] B[N x K]^T in split-BF16x3 (hi*hi + hi*lo + lo*hi), then the epilogue.
 // kseg: segment boundary (a multiple of 64) or >= K for a single segment.
 void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e);

@@ -611,6 +611,7 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   lz->rankp.alloc(m + 2);
   lz->allp.alloc((m + 2) * ctx->world);
   lz->ticket.alloc(2);
+  ++g_graph_gen;
 }
 
 // The refresh's launch sequence (v1, then m x [HVP, GS pass 1, GS pass 2, decide] with device-resident
@@ -677,13 +678,15 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
   }
 }
 
-static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
+// launch = false: capture / instantiate only (done right after the first, eager refresh, so that the
+// capture's host cost falls in that refresh rather than in a later one).
+static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, bool launch = true) {
   dho2g_ctx* ctx = lz->ctx;
   cudaStream_t st = ctx->stream;
   if (!ctx->use_graphs || ctx->world != 1 || ctx->ktimers || op->kind == 3 || lz->graph_failed) return false;
   lz->seed_dev.ensure(1);
   lz->seed_host.ensure(1);
-  const bool valid = lz->gexec && lz->gop == op && lz->gm == lz->m && lz->ggen == g_alloc_gen &&
+  const bool valid = lz->gexec && lz->gop == op && lz->gm == lz->m && lz->ggen == g_graph_gen &&
                      lz->gflags == ctx->gemm_flags.p && lz->gflags2 == ctx->gemm_flags2.p;
   if (!valid) {
     if (!lz->seen_eager) return false;  // first refresh runs eagerly (allocates every buffer)
@@ -691,7 +694,7 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
       cudaGraphExecDestroy(lz->gexec);
       lz->gexec = nullptr;
     }
-    const unsigned long long gen0 = g_alloc_gen;
+    const unsigned long long gen0 = g_graph_gen;
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
@@ -710,7 +713,7 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
       ok = false;
     }
     const cudaError_t ec = cudaStreamEndCapture(st, &g);
-    if (!ok || ec != cudaSuccess || g == nullptr || g_alloc_gen != gen0) {
+    if (!ok || ec != cudaSuccess || g == nullptr || g_graph_gen != gen0) {
       cudaGetLastError();
       if (g) cudaGraphDestroy(g);
       lz->graph_failed = true;
@@ -726,13 +729,14 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0) {
     }
     lz->gop = op;
     lz->gm = lz->m;
-    lz->ggen = g_alloc_gen;
+    lz->ggen = g_graph_gen;
     lz->gflags = ctx->gemm_flags.p;
     lz->gflags2 = ctx->gemm_flags2.p;
     lz->glaunches = g_launches - l0;
     g_launches = l0;  // captured, not launched
     ctx->bump("lanczos_graph_captures", 1);
   }
+  if (!launch) return true;
   lz->seed_host.p[0] = s0;
   DHO2G_CUDA(cudaMemcpyAsync(lz->seed_dev.p, lz->seed_host.p, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
   DHO2G_CUDA(cudaGraphLaunch(lz->gexec, st));
@@ -750,9 +754,10 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   DHO2G_CUDA(cudaEventCreate(&e1));
   DHO2G_CUDA(cudaEventRecord(e0, st));
   const uint64_t s0 = seed * 0x9e3779b97f4a7c15ULL + 0x1234567ULL;
+  bool eager = false;
   if (!lanczos_graph(lz, op, s0)) {
     lanczos_enqueue(lz, op, s0, nullptr);
-    lz->seen_eager = true;
+    lz->seen_eager = eager = true;
   }
   DHO2G_CUDA(cudaEventRecord(e1, st));
   DHO2G_CUDA(cudaMemcpyAsync(&lz->host, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, st));
@@ -765,6 +770,13 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   if (lz->host.stopped == 0) lz->host.iters = (int)m;
   ctx->bump("lanczos_runs", 1);
   ctx->bump("lanczos_ms", ms);
+  if (eager && !lz->gexec) {
+    // pre-capture the next refresh from the host state a refresh starts in (operator weights reloaded)
+    const bool wl = op->weights_loaded;
+    op->weights_loaded = false;
+    lanczos_graph(lz, op, s0, false);
+    op->weights_loaded = wl || op->weights_loaded;
+  }
 }
 
 void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese) {

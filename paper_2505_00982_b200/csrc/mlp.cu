@@ -22,6 +22,7 @@ using namespace dho2g;
 
 void dho2g_mlp::ensure_batch(size_t B) {
   if (B <= Bcap) return;
+  ++g_graph_gen;
   const size_t nB = round_up(B, 128);
   const int Ls = L;
   AR_hi.resize(Ls); AR_lo.resize(Ls);
@@ -239,19 +240,40 @@ __global__ void eval_reduce_kernel(int B, const double* __restrict__ loss, const
 
 namespace dho2g {
 
+// Packs the [V | W] halves. With the side lane enabled the packing kernels run on ctx->stream2 (forked
+// from the main stream, one event per layer) and forward() waits for layer t's event just before layer
+// t's GEMMs, so the bandwidth-bound packing of later layers overlaps the tensor-core GEMMs of earlier ones.
 static void pack_params(dho2g_mlp* m, const float* p, const float* pscale, int half) {
-  cudaStream_t st = m->ctx->stream;
+  dho2g_ctx* ctx = m->ctx;
+  const bool async = ctx->bwd_overlap && ctx->gemm_backend == 0;
+  cudaStream_t main = ctx->stream;
+  if (async) {
+    if (!ctx->stream2) DHO2G_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    while (m->pack_ev.size() < (size_t)m->L + 1) {
+      cudaEvent_t ev;
+      DHO2G_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      m->pack_ev.push_back(ev);
+    }
+    DHO2G_CUDA(cudaEventRecord(m->pack_ev[m->L], main));  // fork: p and the previous readers of WV
+    DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream2, m->pack_ev[m->L], 0));
+    ctx->stream = ctx->stream2;
+  }
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
-    const int slot = m->ctx->kt_begin();
+    const int slot = ctx->kt_begin();
     // one wave of resident blocks striding over the rows (short-lived per-row blocks cost more than the copy)
     const int gx = (int)cdiv(ld.in, 128 * kPackPer);
-    const int gy = std::max(1, std::min(ld.out, m->ctx->sm_count * 16 / gx));
-    pack_weights_kernel<<<dim3(gx, gy), 128, 0, st>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
-                                                      m->WV_hi[t].p, m->WV_lo[t].p);
+    const int gy = std::max(1, std::min(ld.out, ctx->sm_count * 16 / gx));
+    pack_weights_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
+                                                               m->WV_hi[t].p, m->WV_lo[t].p);
     DHO2G_LAUNCH();
     // algorithmic bytes: read fp32 (4) + write hi/lo (4)
-    m->ctx->kt_end(slot, "pack_params", (double)ld.in * ld.out * 8.0);
+    ctx->kt_end(slot, "pack_params", (double)ld.in * ld.out * 8.0);
+    if (async) DHO2G_CUDA(cudaEventRecord(m->pack_ev[t], ctx->stream));
+  }
+  if (async) {
+    ctx->stream = main;
+    m->pack_pending = true;
   }
 }
 
@@ -262,6 +284,13 @@ void mlp_load_weights(dho2g_mlp* m, const float* w) {
 }
 
 void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale) { pack_params(m, v, vscale, 0); }
+
+void mlp_presize(dho2g_mlp* m, size_t B) {
+  m->ensure_batch(B);
+  m->csum.ensure_g((size_t)2 * cdiv(B, 32) * m->smax);
+  m->colpart.ensure_g((size_t)kColChunks * m->smax);
+  m->coltickets.ensure_g(cdiv(m->smax, 64));
+}
 
 static void pack_rows(dho2g_ctx* ctx, int B, int s, int P, const float* X, const int64_t* idx, int ldX,
                       const float* x1, bf16* Rh, bf16* Rl) {
@@ -287,6 +316,7 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
   dho2g_ctx* ctx = m->ctx;
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
+    if (m->pack_pending) DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, m->pack_ev[t], 0));  // layer t packed
     const bool last = t + 1 == m->L;
     const int lda = 2 * ld.Pin;
     for (int pass = 0; pass < 2; ++pass) {
@@ -316,6 +346,7 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
               m->WV_lo[t].p, lda, e);
     }
   }
+  m->pack_pending = false;  // every layer's event has been waited on by the main stream
 }
 
 static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool do0, bool do1) {
@@ -332,8 +363,8 @@ static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool
 
 static void bias_colsum(dho2g_mlp* m, const bf16* hi, const bf16* lo, int ld, int off, int cols, int B, float* out) {
   dho2g_ctx* ctx = m->ctx;
-  m->colpart.ensure((size_t)kColChunks * cols);
-  m->coltickets.ensure(cdiv(cols, 64));  // zeroed at allocation; each launch leaves them zero
+  m->colpart.ensure_g((size_t)kColChunks * cols);
+  m->coltickets.ensure_g(cdiv(cols, 64));  // zeroed at allocation; each launch leaves them zero
   const int slot = ctx->kt_begin();
   colsum_pairs_kernel<<<dim3(cdiv(cols, 64), kColChunks), dim3(32, 8), 0, ctx->stream>>>(
       hi, lo, ld, off, cols, B, m->colpart.p, m->coltickets.p, out);
@@ -383,7 +414,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   // t+1's backward GEMM) also writes per-32-row column sums into m->csum (two buffers, by level parity);
   // the output level's deltas come from the loss kernel and are summed by colsum_pairs_kernel
   const bool need_bias = do1 || wgrad;
-  if (need_bias) m->csum.ensure((size_t)2 * nrb * m->smax);
+  if (need_bias) m->csum.ensure_g((size_t)2 * nrb * m->smax);
   auto csum_buf = [&](int level) { return m->csum.p + (size_t)(level & 1) * nrb * m->smax; };
   // Weight blocks (and bias blocks) of layer t only read level t+1's deltas and level t's activations, so
   // they run on the side lane concurrently with the delta GEMM of layer t (main lane), the two sharing

@@ -130,7 +130,7 @@ struct dho2g_trainer {
     std::vector<uint64_t> all(N);
     dho2g_curvature_indices(N, want, cfg.seed, refreshes, all.data());
     std::vector<int64_t> cidx(all.begin(), all.begin() + want);
-    op.idx.ensure(want);
+    op.idx.ensure_g(want);
     DHO2G_CUDA(cudaMemcpyAsync(op.idx.p, cidx.data(), want * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
     if (host_resident) h2d_bytes += (double)want * (D + 1) * sizeof(float) + want * sizeof(int64_t);
     op.B = want;
@@ -380,6 +380,23 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   if (t->rows)
     DHO2G_CUDA(cudaMemcpyAsync(t->w_sh.p, t->w_a_shard, t->rows * sizeof(float), cudaMemcpyDeviceToDevice, st));  // make_admm_state
   opt_alloc(&t->opt, ctx, cfg->base, t->rows);
+  // Steady-state sizes for everything a refresh touches (MLP batch buffers for the larger of the step,
+  // curvature and evaluation batches; both GEMM lanes' workspaces; the Lanczos state), so the refresh
+  // graph captured right after the first, eager refresh stays valid through the gradient steps.
+  {
+    const size_t b_step = (size_t)(t->c1 - t->c0) * cfg->batch_size;
+    size_t cb, ce;
+    shard_range(std::min<size_t>(cfg->curvature_batch, N), ctx->world, ctx->rank, &cb, &ce);
+    size_t eb, ee;
+    shard_range(N, ctx->world, ctx->rank, &eb, &ee);
+    const size_t b_eval = std::min<size_t>(ee - eb, 1024);
+    mlp_presize(mlp, std::max(std::max(b_step, ce - cb), std::max(b_eval, (size_t)1)));
+    gemm_presize(ctx);
+    if (cfg->trainer != 0 && (cfg->lanczos_m || (cfg->k + cfg->l >= 1 && cfg->k + cfg->l <= n))) {
+      const size_t m = cfg->lanczos_m ? cfg->lanczos_m : lanczos_budget(cfg->k, cfg->l, n);
+      if (m >= 1 && m <= n && m <= (size_t)kMaxLanczos - 1) lanczos_alloc(&t->lz, ctx, n, m);
+    }
+  }
   // curvature operator bound to (w_a, curvature batch) like the trainer.cpp:116 lambda
   t->op.ctx = ctx;
   t->op.kind = 0;
