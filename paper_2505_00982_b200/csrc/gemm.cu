@@ -957,11 +957,11 @@ int max_pairs(dho2g_ctx* ctx) {
 template <bool AMN, bool BMN, int NT>
 int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
   const int pairs = max_pairs<AMN, BMN, NT>(ctx);
-  // every worker gets >= 4 k-blocks (shorter segments are mostly fixup traffic)
+  // every worker gets >= gemm_min_kb k-blocks (shorter segments are mostly fix-up traffic)
   const long long tiles = (long long)wk.mt * wk.nt;
   ctx->pairs_total = pairs;
   const int cap = ctx->gemm_worker_cap > 0 ? std::min(ctx->gemm_worker_cap, pairs) : pairs;
-  wk.workers = (int)std::min<long long>(cap, std::max<long long>(1, tiles * wk.nkb / 4));
+  wk.workers = (int)std::min<long long>(cap, std::max<long long>(1, tiles * wk.nkb / std::max(1, ctx->gemm_min_kb)));
   // data-parallel waves, keeping the last ~1-2 waves of tiles for stream-K balancing (option gemm_dp = 0
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;
