@@ -315,30 +315,37 @@ inline OpOff op_off(const GOp& g) {
   return o;
 }
 
-template <bool MN>
+// Descriptor of the kk-th K=16 slice of a staged operand tile whose stage depth is BKT K-elements:
+//  MN-major: panels of 64 MN x BKT K-rows (128-byte rows, SW128): LBO = panel stride = BKT * 128 B,
+//            SBO = 1024 B, slice kk at +2 KB * kk;
+//  K-major, BKT = 64: 128-byte rows (SW128), SBO = 1024 B, slice at +32 B * kk;
+//  K-major, BKT = 32: 64-byte rows (SW64, layout 4), SBO = 512 B, slice at +32 B * kk.
+template <bool MN, int BKT = 64>
 __device__ __forceinline__ uint64_t op_desc(uint32_t tile_base, int kk) {
-  return MN ? sw128_desc(tile_base + kk * 2048, 8192, 1024) : sw128_desc(tile_base + kk * 32, 16, 1024);
+  if (MN) return sw128_desc(tile_base + kk * 2048, BKT * 128, 1024);
+  if (BKT == 64) return sw128_desc(tile_base + kk * 32, 16, 1024);
+  return umma_desc(tile_base + kk * 32, 16, 512, 4);
 }
 
 // Stage one 128-row (M or N) x 64-K operand tile (hi or lo) into smem through its map.
 // PANELS2: 2 = 128 MN rows (MN-major: two 64-wide boxes), 1 = 64 rows (the B half of a 128-wide pair tile;
 // K-major maps are then built with 64-row boxes).
-template <bool MN, bool PAIR, int PANELS2 = 2>
+template <bool MN, bool PAIR, int PANELS2 = 2, int BKT = 64>
 __device__ __forceinline__ void load_op(uint8_t* dst, const CUtensorMap* map, const OpOff& o, int mn0, int kb,
                                         int kseg, uint64_t* bar) {
-  const int k = kb * BK;
+  const int k = kb * BKT;
   const int seg = k >= kseg ? 1 : 0;
   const int kk = k - (seg ? kseg : 0);
-  if (MN) {  // 64(MN) x 64(K) boxes
+  if (MN) {  // 64(MN) x BKT(K) boxes
     tma_load_2d<PAIR>(dst, map, mn0 + o.off_in[seg], kk + o.off_out[seg], bar);
-    if (PANELS2 == 2) tma_load_2d<PAIR>(dst + 8192, map, mn0 + 64 + o.off_in[seg], kk + o.off_out[seg], bar);
-  } else {  // one 64(K) x (64 PANELS2)(MN) box
+    if (PANELS2 == 2) tma_load_2d<PAIR>(dst + BKT * 128, map, mn0 + 64 + o.off_in[seg], kk + o.off_out[seg], bar);
+  } else {  // one BKT(K) x (64 PANELS2)(MN) box
     tma_load_2d<PAIR>(dst, map, kk + o.off_in[seg], mn0 + o.off_out[seg], bar);
   }
 }
 
 CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                     uint32_t box_outer) {
+                     uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {ld * sizeof(bf16)};
@@ -346,18 +353,19 @@ CUtensorMap make_map(void* encode_fn, const bf16* ptr, uint64_t inner, uint64_t 
   cuuint32_t estr[2] = {1, 1};
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(encode_fn);
   CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(ptr), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(DHO2G_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") inner=" + std::to_string(inner) +
                          " outer=" + std::to_string(outer) + " ld=" + std::to_string(ld));
   return m;
 }
-// hi / lo maps of one operand: K-major boxes 64(K) x 128 rows, MN-major boxes 64(MN) x 64(K)
-void op_maps(void* encode_fn, const GOp& g, CUtensorMap& mh, CUtensorMap& ml, uint32_t rows = 128) {
-  const uint32_t bi = 64, bo = g.mn_major ? 64 : rows;
-  mh = make_map(encode_fn, g.hi, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
-  ml = make_map(encode_fn, g.lo, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo);
+// hi / lo maps of one operand: K-major boxes bk(K) x rows (SW128 for bk = 64, SW64 for bk = 32),
+// MN-major boxes 64(MN) x bk(K) (SW128)
+void op_maps(void* encode_fn, const GOp& g, CUtensorMap& mh, CUtensorMap& ml, uint32_t rows = 128, uint32_t bk = 64) {
+  const uint32_t bi = g.mn_major ? 64 : bk, bo = g.mn_major ? bk : rows;
+  const CUtensorMapSwizzle sw = (!g.mn_major && bk == 32) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  mh = make_map(encode_fn, g.hi, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo, sw);
+  ml = make_map(encode_fn, g.lo, (uint64_t)g.inner, (uint64_t)g.outer, (uint64_t)g.ld, bi, bo, sw);
 }
 void check_op(const GOp& g, const char* what) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -650,9 +658,14 @@ namespace tc2 {
 using namespace tc;
 
 constexpr int BM = 128;   // output rows per CTA (pair tile 256)
-constexpr int STAGES = 3;
-constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;  // A hi/lo (128 rows) + B hi/lo (<= 128 = NT/2 rows) slots
-constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
+// K-block depth BKT: 64 (3 stages of 64 KB, SW128) or 32 (6 stages of 32 KB, K-major operands SW64)
+template <int BKT>
+struct Pipe {
+  static constexpr int STAGES = BKT == 64 ? 3 : 6;
+  static constexpr uint32_t OPB = 128u * BKT * 2u;          // one 128-row (hi or lo) operand tile
+  static constexpr uint32_t STAGE_BYTES = 4 * OPB;          // A hi/lo + B hi/lo slots
+  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
+};
 constexpr uint32_t PART_MAX = BM * 256;  // one CTA's partial tile (NT = 256)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -743,12 +756,14 @@ __device__ __forceinline__ int tile_cols(const Work& wk, int n0) {  // MMA N of 
 }
 
 // NT: pair tile width (256, or 128 when 256-wide tiles would leave pairs with less than ~2 tiles)
-template <bool AMN, bool BMN, int NT>
+template <bool AMN, bool BMN, int NT, int BKT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm3_tc2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Work wk,
                      OpOff oa, OpOff ob, const __grid_constant__ Epi e, float* __restrict__ ws,
                      unsigned* __restrict__ flags, unsigned ready) {
+  constexpr int STAGES = Pipe<BKT>::STAGES;
+  constexpr uint32_t OP_BYTES = Pipe<BKT>::OPB, STAGE_BYTES = Pipe<BKT>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -759,7 +774,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 
   constexpr uint32_t TMEM_COLS = ACC * NT;
   constexpr uint32_t PART_FLOATS = BM * NT;
-  constexpr uint32_t B_BYTES = (NT / 2) * BK * 2;  // one (hi or lo) B half-tile
+  constexpr uint32_t B_BYTES = (NT / 2) * BKT * 2;  // one (hi or lo) B half-tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int worker = blockIdx.x >> 1;
@@ -806,10 +821,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
         uint8_t* st = smem + s * STAGE_BYTES;
         if (rank == 0) mbar_expect_tx(&full[s], 2 * (2 * OP_BYTES + 2 * B_BYTES));
-        load_op<AMN, true>(st, &mAh, oa, m0, kb, wk.kseg, &full[s]);
-        load_op<AMN, true>(st + OP_BYTES, &mAl, oa, m0, kb, wk.kseg, &full[s]);
-        load_op<BMN, true, NT / 128>(st + 2 * OP_BYTES, &mBh, ob, nb, kb, wk.kseg, &full[s]);
-        load_op<BMN, true, NT / 128>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
+        load_op<AMN, true, 2, BKT>(st, &mAh, oa, m0, kb, wk.kseg, &full[s]);
+        load_op<AMN, true, 2, BKT>(st + OP_BYTES, &mAl, oa, m0, kb, wk.kseg, &full[s]);
+        load_op<BMN, true, NT / 128, BKT>(st + 2 * OP_BYTES, &mBh, ob, nb, kb, wk.kseg, &full[s]);
+        load_op<BMN, true, NT / 128, BKT>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
       }
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
@@ -831,11 +846,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         fence_after();
         const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / UK; ++kk) {
-          const uint64_t dAh = op_desc<AMN>(base, kk);
-          const uint64_t dAl = op_desc<AMN>(base + OP_BYTES, kk);
-          const uint64_t dBh = op_desc<BMN>(base + 2 * OP_BYTES, kk);
-          const uint64_t dBl = op_desc<BMN>(base + 3 * OP_BYTES, kk);
+        for (int kk = 0; kk < BKT / UK; ++kk) {
+          const uint64_t dAh = op_desc<AMN, BKT>(base, kk);
+          const uint64_t dAl = op_desc<AMN, BKT>(base + OP_BYTES, kk);
+          const uint64_t dBh = op_desc<BMN, BKT>(base + 2 * OP_BYTES, kk);
+          const uint64_t dBl = op_desc<BMN, BKT>(base + 3 * OP_BYTES, kk);
           const uint32_t first = (kb > sg.k0 || kk > 0) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -931,15 +946,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-template <bool AMN, bool BMN, int NT>
+template <bool AMN, bool BMN, int NT, int BKT>
 int max_pairs(dho2g_ctx* ctx) {
   static int pairs = 0;
   if (pairs > 0) return pairs;
-  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN, NT, BKT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Pipe<BKT>::SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * (ctx->sm_count / 2));
   cfg.blockDim = dim3(384);
-  cfg.dynamicSmemBytes = SMEM;
+  cfg.dynamicSmemBytes = Pipe<BKT>::SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -948,15 +963,15 @@ int max_pairs(dho2g_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int clusters = 0;
-  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN, NT>, &cfg));
+  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN, NT, BKT>, &cfg));
   if (clusters < 1) fail(DHO2G_CUDA, "gemm3_tc2: no CTA pair can be resident");
   pairs = clusters;
   return pairs;
 }
 
-template <bool AMN, bool BMN, int NT>
+template <bool AMN, bool BMN, int NT, int BKT>
 int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
-  const int pairs = max_pairs<AMN, BMN, NT>(ctx);
+  const int pairs = max_pairs<AMN, BMN, NT, BKT>(ctx);
   // every worker gets >= gemm_min_kb k-blocks (shorter segments are mostly fix-up traffic)
   const long long tiles = (long long)wk.mt * wk.nt;
   ctx->pairs_total = pairs;
@@ -973,31 +988,31 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
     ctx->gemm_epoch = epoch = 1;
   }
-  gemm3_tc2_kernel<AMN, BMN, NT><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
+  gemm3_tc2_kernel<AMN, BMN, NT, BKT><<<2 * wk.workers, 384, Pipe<BKT>::SMEM, ctx->stream>>>(
       maps[0], maps[1], maps[2], maps[3], wk, oa, ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u);
   DHO2G_LAUNCH();
   return wk.workers;
 }
 
-template <int NT>
+template <int NT, int BKT>
 int run_nt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   Work wk;
   wk.mt = (int)cdiv(M, 256);
   wk.nt = (int)cdiv(N, NT);
-  wk.nkb = (int)cdiv(K, BK);
+  wk.nkb = (int)cdiv(K, BKT);
   wk.N = N;
   wk.kseg = kseg;
   wk.nround = B.mn_major ? 128 : 16;
   wk.workers = 1;
   wk.dp = 0;  // set in launch() once the worker count is known
   CUtensorMap maps[4];
-  op_maps(ctx->encode_fn, A, maps[0], maps[1]);
-  op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2);
+  op_maps(ctx->encode_fn, A, maps[0], maps[1], 128, BKT);
+  op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2, BKT);
   const OpOff oa = op_off(A), ob = op_off(B);
-  if (A.mn_major && B.mn_major) return launch<true, true, NT>(ctx, maps, wk, oa, ob, e);
-  if (A.mn_major) return launch<true, false, NT>(ctx, maps, wk, oa, ob, e);
-  if (B.mn_major) return launch<false, true, NT>(ctx, maps, wk, oa, ob, e);
-  return launch<false, false, NT>(ctx, maps, wk, oa, ob, e);
+  if (A.mn_major && B.mn_major) return launch<true, true, NT, BKT>(ctx, maps, wk, oa, ob, e);
+  if (A.mn_major) return launch<true, false, NT, BKT>(ctx, maps, wk, oa, ob, e);
+  if (B.mn_major) return launch<false, true, NT, BKT>(ctx, maps, wk, oa, ob, e);
+  return launch<false, false, NT, BKT>(ctx, maps, wk, oa, ob, e);
 }
 
 int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e, int& nt_used) {
@@ -1006,7 +1021,9 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   // scripts/prof_hvp.py --abopt gemm_pair_n).
   const int nt = ctx->gemm_pair_n == 128 ? 128 : 256;
   nt_used = nt;
-  return nt == 128 ? run_nt<128>(ctx, M, N, K, kseg, A, B, e) : run_nt<256>(ctx, M, N, K, kseg, A, B, e);
+  if (ctx->gemm_bk == 32) return nt == 128 ? run_nt<128, 32>(ctx, M, N, K, kseg, A, B, e)
+                                           : run_nt<256, 32>(ctx, M, N, K, kseg, A, B, e);
+  return nt == 128 ? run_nt<128, 64>(ctx, M, N, K, kseg, A, B, e) : run_nt<256, 64>(ctx, M, N, K, kseg, A, B, e);
 }
 
 }  // namespace tc2

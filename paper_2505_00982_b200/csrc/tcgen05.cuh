@@ -56,6 +56,15 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 //  K-major : 8-row x 128 B atoms stacked along M/N: LBO unused (1), SBO = 1024 B; K step = +32 B.
 //  MN-major: 64-element x 8-K-row atoms; LBO = 8 KB (next 64 M/N, one TMA box of 64 K-rows),
 //            SBO = 1024 B (next 8 K-rows); K step of 16 = +2 KB.
+// UMMA shared-memory descriptor with an explicit layout type (bits 61-63: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(lbo >> 4) << 16;
+  d |= (uint64_t)(sbo >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)(lbo >> 4) << 16;
