@@ -142,6 +142,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_pair_n") ctx->gemm_pair_n = (int)value;
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;
+    else if (k == "gs_sm_cap") ctx->gs_sm_cap = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
     else if (k == "ktimers") {
       ctx->kt_flush();

@@ -54,6 +54,7 @@ struct dho2g_ctx {
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;
   int use_graphs = 1;     // capture the Lanczos refresh into a CUDA graph (world 1)
+  int gs_sm_cap = 0;     // Gram-Schmidt grids sized for at most this many SMs (0: all; experiments)
   int ritz_tc = 1;        // Ritz vectors on the tensor cores when supported (0: CUDA-core kernel)
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   ncclComm_t comm = nullptr;

@@ -653,8 +653,9 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
     op->apply(vfull, &lz->st.p->sigma[i], lz->h.p, lz->begin, lz->rows, lz->base);
     const size_t smem1 = (size_t)kWarps * (active + 1) * sizeof(double);
     const size_t smem2 = (size_t)(active + 1) * sizeof(double);
-    const int g1 = one_wave_grid(gs_pass1_kernel, kThreads, smem1, ctx->sm_count, (size_t)nchunks);
-    const int g2 = one_wave_grid(gs_pass2_kernel, kThreads, smem2, ctx->sm_count, cdiv(ngroups / 128, kWarps));
+    const int gs_sms = ctx->gs_sm_cap > 0 ? std::min(ctx->gs_sm_cap, ctx->sm_count) : ctx->sm_count;
+    const int g1 = one_wave_grid(gs_pass1_kernel, kThreads, smem1, gs_sms, (size_t)nchunks);
+    const int g2 = one_wave_grid(gs_pass2_kernel, kThreads, smem2, gs_sms, cdiv(ngroups / 128, kWarps));
     for (int pass = 0; pass < (lz->opts.reorth_safeguard ? 2 : 1); ++pass) {
       const float* hsrc = pass == 0 ? lz->h.p : Dn;
       // algorithmic bytes: active columns of D + h (pass 1); + h' write (pass 2)
