@@ -599,7 +599,8 @@ void launch(dho2g_ctx* ctx, const CUtensorMap* maps, const Sched& sc, const OpOf
     DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     attr_set = true;
   }
-  const int grid = std::min(sc.units, ctx->sm_count);
+  const int ctas = ctx->gemm_worker_cap > 0 ? std::min(ctx->sm_count, 2 * ctx->gemm_worker_cap) : ctx->sm_count;
+  const int grid = std::min(sc.units, ctas);
   gemm3_tc_kernel<AMN, BMN><<<grid, 384, SMEM, ctx->stream>>>(maps[0], maps[1], maps[2], maps[3], sc, oa, ob, e, ws,
                                                               flags, epoch);
   DHO2G_LAUNCH();
@@ -612,8 +613,8 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   sc.tiles = sc.mt * sc.nt;
   sc.nkb = (int)cdiv(K, BK);
   sc.kseg = kseg;
-  sc.splits = ctx->gemm_splits > 0 ? std::min(ctx->gemm_splits, std::max(1, sc.nkb))
-                                   : pick_splits(sc.tiles, sc.nkb, ctx->sm_count);
+  const int ctas = ctx->gemm_worker_cap > 0 ? std::min(ctx->sm_count, 2 * ctx->gemm_worker_cap) : ctx->sm_count;
+  sc.splits = ctx->gemm_splits > 0 ? std::min(ctx->gemm_splits, std::max(1, sc.nkb)) : pick_splits(sc.tiles, sc.nkb, ctas);
   sc.units = sc.tiles * sc.splits;
   float* ws = nullptr;
   unsigned* flags = nullptr;
@@ -1054,8 +1055,10 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
     gemm3_simt(ctx, M, N, K, kseg, A, B, e);
   } else {
     if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    // CTA pairs (256-row tiles) unless the GEMM is too short in M to fill them
-    pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 128);
+    // CTA pairs (256-row tiles) unless M is too short to fill them; short-K weight blocks with both operands
+    // MN-major run faster as many 128 x 128 single-CTA tiles (measured 176 vs 200 us at 3584^2 x 2048)
+    const bool short_mm = A.mn_major && B.mn_major && K <= 2048 && ctx->gemm_mm_tc1;
+    pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 128 && !short_mm);
     int nt = 0;
     splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e, nt) : tc1::run(ctx, M, N, K, kseg, A, B, e);
     pair_nt = nt;

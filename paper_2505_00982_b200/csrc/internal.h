@@ -40,6 +40,7 @@ struct dho2g_ctx {
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
   int gemm_dp = 1;       // pair kernel: data-parallel waves before the stream-K remainder (0: all stream-K)
+  int gemm_mm_tc1 = 1;   // auto: short-K MN-major x MN-major GEMMs on the single-CTA kernel
   int gemm_bk = 64;      // pair kernel K-block depth: 64 (3 x 64 KB stages) or 32 (6 x 32 KB stages)
   int gemm_min_kb = 4;   // pair kernel: minimum k-blocks per CTA pair (caps the worker count of small GEMMs)
   int gemm_worker_cap = 0;  // pair kernel: at most this many CTA pairs (0: all co-resident pairs)
