@@ -137,10 +137,8 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
     else if (k == "gemm_dp") ctx->gemm_dp = (int)value;
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
-    else if (k == "gemm_bk") ctx->gemm_bk = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
-    else if (k == "gemm_pair_n") ctx->gemm_pair_n = (int)value;
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;
     else if (k == "gs_sm_cap") ctx->gs_sm_cap = (int)value;

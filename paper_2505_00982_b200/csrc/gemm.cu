@@ -110,12 +110,92 @@ __device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, con
   }
 }
 
-// Warp-cooperative form (tcgen05 epilogue): lane l holds row row0 + l, columns [col0, col0+16).
-// The 32x16 block is restaged through shared memory (sm: 32 x 17 floats) so that the row-major
-// traffic (fp32 inputs/outputs, row-major pairs, C) is coalesced (16 lanes per row segment), and the
-// transposed pair is written from the lane=row layout (32 consecutive rows per column).
-__device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, const float (&acc)[16], float* sm) {
+// Compile-time-mode forms used by the tcgen05 kernels (the mode is a template parameter of the kernel, so
+// each epilogue compiles to its own straight-line code; the generic forms above serve the CUDA-core path).
+template <int MODE>
+__device__ __forceinline__ EpiIn epi_load_t(const Epi& e, int row, int col) {
+  EpiIn in;
+  const size_t ei = (size_t)row * e.N + col;
+  if (MODE == EPI_FWD || MODE == EPI_FWD_OUT) {
+    if (e.do0) {
+      in.p0 = __ldg(e.bias + col);
+    } else {
+      in.p0 = __ldg(e.vbias + col);
+      if (MODE == EPI_FWD) in.p1 = __ldg(e.a_in + ei);
+    }
+  } else if (MODE == EPI_BWD) {
+    in.p1 = __ldg(e.a_in + ei);
+    if (e.do1) {
+      in.p0 = __ldg(e.u_in + ei);
+      if (!e.relu) in.p2 = __ldg(e.ra_in + ei);
+    }
+  }
+  return in;
+}
+
+template <int MODE>
+__device__ __forceinline__ float epi_elem_t(const Epi& e, int row, int col, float acc, float vsc, const EpiIn& in) {
+  const size_t ei = (size_t)row * e.N + col;
+  float v;
+  if (MODE == EPI_FWD || MODE == EPI_FWD_OUT) {
+    // oracle.cpp:548-563: a = act(z), z = W a + b ; ra = act'(a) (V a + W ra + v_b)
+    if (e.do0) {
+      const float z = acc + in.p0;
+      v = MODE == EPI_FWD_OUT ? z : (e.relu ? fmaxf(z, 0.f) : tanhf(z));
+      if (e.f0) e.f0[ei] = v;
+    } else {
+      const float rz = acc + vsc * in.p0;
+      v = MODE == EPI_FWD_OUT ? rz : act_prime(e.relu, in.p1) * rz;
+      if (e.f1) e.f1[ei] = v;
+    }
+  } else {  // EPI_BWD, oracle.cpp:626-635: d = u act'(a); rd = ru act'(a) + u (-2 a ra) (tanh)
+    const float a = in.p1;
+    const float ap = act_prime(e.relu, a);
+    if (e.do0) {
+      v = acc * ap;
+      if (e.f0) e.f0[ei] = v;
+      if (e.u_out) e.u_out[ei] = acc;
+    } else {
+      const float rap = (!e.relu && ap != 0.f) ? -2.f * a * in.p2 : 0.f;
+      v = acc * ap + in.p0 * rap;
+      if (e.f1) e.f1[ei] = v;
+    }
+  }
+  if (e.Rh) {
+    const size_t r = (size_t)row * (2 * e.P) + (size_t)e.hR * e.P + col;
+    split_bf16(v, e.Rh[r], e.Rl[r]);
+  }
+  return v;
+}
+
+// Warp-cooperative epilogue of a 32 x 16 accumulator block (lane l holds row row0 + l, columns
+// [col0, col0 + 16)). EPI_STORE writes each lane's 64 contiguous bytes directly (four 16-byte stores);
+// the layer epilogues restage the block through shared memory (sm: 32 x 17 floats) so that their
+// row-major inputs / outputs / bf16 pairs are coalesced, and write the transposed pair from the
+// lane = row layout.
+template <int MODE>
+__device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc)[16], float* sm) {
   const int lane = threadIdx.x & 31;
+  if (MODE == EPI_STORE) {
+    const int row = row0 + lane;
+    if (row >= e.M) return;
+    float* c = e.C + (size_t)row * e.ldc + col0;
+    if (!e.bias_out && col0 + 16 <= e.N && (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(c + 4 * q) =
+            make_float4(e.alpha * acc[4 * q], e.alpha * acc[4 * q + 1], e.alpha * acc[4 * q + 2], e.alpha * acc[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (col0 + j >= e.N) break;
+        const float v = e.alpha * acc[j];
+        if (e.bias_out && col0 + j == e.N - 1) e.bias_out[row] = v;
+        else c[j] = v;
+      }
+    }
+    return;
+  }
   const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
 #pragma unroll
   for (int j = 0; j < 16; ++j) sm[lane * 17 + j] = acc[j];
@@ -127,14 +207,14 @@ __device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, con
 #pragma unroll
   for (int it = 0; it < 16; ++it) {
     const int row = row0 + 2 * it + rr;
-    if (row < e.M && col < e.N) in[it] = epi_load(e, row, col);
+    if (row < e.M && col < e.N) in[it] = epi_load_t<MODE>(e, row, col);
   }
 #pragma unroll
   for (int it = 0; it < 16; ++it) {
     const int rl = 2 * it + rr;
     const int row = row0 + rl;
     float x = 0.f;
-    if (row < e.M && col < e.N) x = epi_elem(e, row, col, sm[rl * 17 + cc], vsc, in[it]);
+    if (row < e.M && col < e.N) x = epi_elem_t<MODE>(e, row, col, sm[rl * 17 + cc], vsc, in[it]);
     sm[rl * 17 + cc] = x;
   }
   __syncwarp();
@@ -144,7 +224,7 @@ __device__ __forceinline__ void epi_warp16(const Epi& e, int row0, int col0, con
     for (int rl = 0; rl < 32; ++rl) t += sm[rl * 17 + lane];
     e.csum[(size_t)(row0 >> 5) * e.N + col0 + lane] = t;
   }
-  if (e.mode != EPI_STORE && e.Th) {
+  if (e.Th) {
     const int row = row0 + lane;
     if (row < e.Bp) {
       const size_t base = (size_t)e.hT * e.Bp + row;
@@ -401,7 +481,7 @@ struct Sched {
   }
 };
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int MODE>
 __global__ void __launch_bounds__(384, 1)
     gemm3_tc_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Sched sc,
@@ -541,7 +621,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
         if (last) {
-          epi_warp16(e, m0 + ew * 32, n0 + c0, v, esm);
+          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
         } else {
           float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
@@ -591,19 +671,29 @@ int pick_splits(int tiles, int nkb, int sms) {
   return best;
 }
 
-template <bool AMN, bool BMN>
+template <bool AMN, bool BMN, int MODE>
 void launch(dho2g_ctx* ctx, const CUtensorMap* maps, const Sched& sc, const OpOff& oa, const OpOff& ob, const Epi& e,
             float* ws, unsigned* flags, unsigned epoch) {
   static bool attr_set = false;
   if (!attr_set) {
-    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc_kernel<AMN, BMN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SMEM));
     attr_set = true;
   }
   const int ctas = ctx->gemm_worker_cap > 0 ? std::min(ctx->sm_count, 2 * ctx->gemm_worker_cap) : ctx->sm_count;
   const int grid = std::min(sc.units, ctas);
-  gemm3_tc_kernel<AMN, BMN><<<grid, 384, SMEM, ctx->stream>>>(maps[0], maps[1], maps[2], maps[3], sc, oa, ob, e, ws,
-                                                              flags, epoch);
+  gemm3_tc_kernel<AMN, BMN, MODE><<<grid, 384, SMEM, ctx->stream>>>(maps[0], maps[1], maps[2], maps[3], sc, oa, ob,
+                                                                    e, ws, flags, epoch);
   DHO2G_LAUNCH();
+}
+
+template <int MODE>
+void launch_mode(dho2g_ctx* ctx, bool amn, bool bmn, const CUtensorMap* maps, const Sched& sc, const OpOff& oa,
+                 const OpOff& ob, const Epi& e, float* ws, unsigned* flags, unsigned epoch) {
+  if (amn && bmn) launch<true, true, MODE>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else if (amn) launch<true, false, MODE>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else if (bmn) launch<false, true, MODE>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  else launch<false, false, MODE>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
 }
 
 int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
@@ -634,10 +724,13 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   op_maps(ctx->encode_fn, A, maps[0], maps[1]);
   op_maps(ctx->encode_fn, B, maps[2], maps[3]);
   const OpOff oa = op_off(A), ob = op_off(B);
-  if (A.mn_major && B.mn_major) launch<true, true>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
-  else if (A.mn_major) launch<true, false>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
-  else if (B.mn_major) launch<false, true>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
-  else launch<false, false>(ctx, maps, sc, oa, ob, e, ws, flags, epoch);
+  const bool amn = A.mn_major != 0, bmn = B.mn_major != 0;
+  switch (e.mode) {
+    case EPI_STORE: launch_mode<EPI_STORE>(ctx, amn, bmn, maps, sc, oa, ob, e, ws, flags, epoch); break;
+    case EPI_FWD: launch_mode<EPI_FWD>(ctx, amn, bmn, maps, sc, oa, ob, e, ws, flags, epoch); break;
+    case EPI_FWD_OUT: launch_mode<EPI_FWD_OUT>(ctx, amn, bmn, maps, sc, oa, ob, e, ws, flags, epoch); break;
+    default: launch_mode<EPI_BWD>(ctx, amn, bmn, maps, sc, oa, ob, e, ws, flags, epoch); break;
+  }
   return sc.splits;
 }
 
@@ -659,14 +752,11 @@ namespace tc2 {
 using namespace tc;
 
 constexpr int BM = 128;   // output rows per CTA (pair tile 256)
-// K-block depth BKT: 64 (3 stages of 64 KB, SW128) or 32 (6 stages of 32 KB, K-major operands SW64)
-template <int BKT>
-struct Pipe {
-  static constexpr int STAGES = BKT == 64 ? 3 : 6;
-  static constexpr uint32_t OPB = 128u * BKT * 2u;          // one 128-row (hi or lo) operand tile
-  static constexpr uint32_t STAGE_BYTES = 4 * OPB;          // A hi/lo + B hi/lo slots
-  static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
-};
+constexpr int NT = 256;   // pair tile width (UMMA N)
+constexpr int BKT = 64;   // K-block depth (one 128-byte SW128 row of bf16)
+constexpr int STAGES = 3;
+constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;  // A hi/lo (128 rows) + B hi/lo (128 = NT/2 rows)
+constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256 + EPI_SMEM;
 constexpr uint32_t PART_MAX = BM * 256;  // one CTA's partial tile (NT = 256)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -757,14 +847,12 @@ __device__ __forceinline__ int tile_cols(const Work& wk, int n0) {  // MMA N of 
 }
 
 // NT: pair tile width (256, or 128 when 256-wide tiles would leave pairs with less than ~2 tiles)
-template <bool AMN, bool BMN, int NT, int BKT>
+template <bool AMN, bool BMN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm3_tc2_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Work wk,
                      OpOff oa, OpOff ob, const __grid_constant__ Epi e, float* __restrict__ ws,
                      unsigned* __restrict__ flags, unsigned ready) {
-  constexpr int STAGES = Pipe<BKT>::STAGES;
-  constexpr uint32_t OP_BYTES = Pipe<BKT>::OPB, STAGE_BYTES = Pipe<BKT>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -929,7 +1017,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
             }
           }
-          epi_warp16(e, m0 + ew * 32, n0 + c0, v, esm);
+          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
         }
         fence_before();
         __syncwarp();
@@ -947,15 +1035,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
-template <bool AMN, bool BMN, int NT, int BKT>
+template <bool AMN, bool BMN, int MODE>
 int max_pairs(dho2g_ctx* ctx) {
   static int pairs = 0;
   if (pairs > 0) return pairs;
-  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN, NT, BKT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Pipe<BKT>::SMEM));
+  DHO2G_CUDA(cudaFuncSetAttribute(gemm3_tc2_kernel<AMN, BMN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * (ctx->sm_count / 2));
   cfg.blockDim = dim3(384);
-  cfg.dynamicSmemBytes = Pipe<BKT>::SMEM;
+  cfg.dynamicSmemBytes = SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
@@ -964,15 +1052,15 @@ int max_pairs(dho2g_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int clusters = 0;
-  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN, NT, BKT>, &cfg));
+  DHO2G_CUDA(cudaOccupancyMaxActiveClusters(&clusters, gemm3_tc2_kernel<AMN, BMN, MODE>, &cfg));
   if (clusters < 1) fail(DHO2G_CUDA, "gemm3_tc2: no CTA pair can be resident");
   pairs = clusters;
   return pairs;
 }
 
-template <bool AMN, bool BMN, int NT, int BKT>
+template <bool AMN, bool BMN, int MODE>
 int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, const OpOff& ob, const Epi& e) {
-  const int pairs = max_pairs<AMN, BMN, NT, BKT>(ctx);
+  const int pairs = max_pairs<AMN, BMN, MODE>(ctx);
   // every worker gets >= gemm_min_kb k-blocks (shorter segments are mostly fix-up traffic)
   const long long tiles = (long long)wk.mt * wk.nt;
   ctx->pairs_total = pairs;
@@ -989,14 +1077,22 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
     ctx->gemm_epoch = epoch = 1;
   }
-  gemm3_tc2_kernel<AMN, BMN, NT, BKT><<<2 * wk.workers, 384, Pipe<BKT>::SMEM, ctx->stream>>>(
+  gemm3_tc2_kernel<AMN, BMN, MODE><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
       maps[0], maps[1], maps[2], maps[3], wk, oa, ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u);
   DHO2G_LAUNCH();
   return wk.workers;
 }
 
-template <int NT, int BKT>
-int run_nt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
+template <int MODE>
+int launch_mode(dho2g_ctx* ctx, const CUtensorMap* maps, const Work& wk, const OpOff& oa, const OpOff& ob,
+                const Epi& e, bool amn, bool bmn) {
+  if (amn && bmn) return launch<true, true, MODE>(ctx, maps, wk, oa, ob, e);
+  if (amn) return launch<true, false, MODE>(ctx, maps, wk, oa, ob, e);
+  if (bmn) return launch<false, true, MODE>(ctx, maps, wk, oa, ob, e);
+  return launch<false, false, MODE>(ctx, maps, wk, oa, ob, e);
+}
+
+int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e) {
   Work wk;
   wk.mt = (int)cdiv(M, 256);
   wk.nt = (int)cdiv(N, NT);
@@ -1007,24 +1103,16 @@ int run_nt(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GO
   wk.workers = 1;
   wk.dp = 0;  // set in launch() once the worker count is known
   CUtensorMap maps[4];
-  op_maps(ctx->encode_fn, A, maps[0], maps[1], 128, BKT);
-  op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2, BKT);
+  op_maps(ctx->encode_fn, A, maps[0], maps[1]);
+  op_maps(ctx->encode_fn, B, maps[2], maps[3], NT / 2);
   const OpOff oa = op_off(A), ob = op_off(B);
-  if (A.mn_major && B.mn_major) return launch<true, true, NT, BKT>(ctx, maps, wk, oa, ob, e);
-  if (A.mn_major) return launch<true, false, NT, BKT>(ctx, maps, wk, oa, ob, e);
-  if (B.mn_major) return launch<false, true, NT, BKT>(ctx, maps, wk, oa, ob, e);
-  return launch<false, false, NT, BKT>(ctx, maps, wk, oa, ob, e);
-}
-
-int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& B, const Epi& e, int& nt_used) {
-  // 256-wide pair tiles. 128-wide ones (option gemm_pair_n = 128) let a pair overlap one tile's epilogue
-  // with the next tile's MMAs at M = 1024, but measured 5-20% slower on every C4 shape (A/B in
-  // scripts/prof_hvp.py --abopt gemm_pair_n).
-  const int nt = ctx->gemm_pair_n == 128 ? 128 : 256;
-  nt_used = nt;
-  if (ctx->gemm_bk == 32) return nt == 128 ? run_nt<128, 32>(ctx, M, N, K, kseg, A, B, e)
-                                           : run_nt<256, 32>(ctx, M, N, K, kseg, A, B, e);
-  return nt == 128 ? run_nt<128, 64>(ctx, M, N, K, kseg, A, B, e) : run_nt<256, 64>(ctx, M, N, K, kseg, A, B, e);
+  const bool amn = A.mn_major != 0, bmn = B.mn_major != 0;
+  switch (e.mode) {
+    case EPI_STORE: return launch_mode<EPI_STORE>(ctx, maps, wk, oa, ob, e, amn, bmn);
+    case EPI_FWD: return launch_mode<EPI_FWD>(ctx, maps, wk, oa, ob, e, amn, bmn);
+    case EPI_FWD_OUT: return launch_mode<EPI_FWD_OUT>(ctx, maps, wk, oa, ob, e, amn, bmn);
+    default: return launch_mode<EPI_BWD>(ctx, maps, wk, oa, ob, e, amn, bmn);
+  }
 }
 
 }  // namespace tc2
@@ -1059,9 +1147,8 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
     // MN-major run faster as many 128 x 128 single-CTA tiles (measured 176 vs 200 us at 3584^2 x 2048)
     const bool short_mm = A.mn_major && B.mn_major && K <= 2048 && ctx->gemm_mm_tc1;
     pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 128 && !short_mm);
-    int nt = 0;
-    splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e, nt) : tc1::run(ctx, M, N, K, kseg, A, B, e);
-    pair_nt = nt;
+    splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e) : tc1::run(ctx, M, N, K, kseg, A, B, e);
+    pair_nt = pair ? tc2::NT : 0;
   }
   if (slot >= 0) {  // name: backend:epilogue(+R)[operand majors]/(splits | pair), aggregated by prefix in the bench
     static const char* modes[] = {"store", "fwd", "fwdout", "bwd"};

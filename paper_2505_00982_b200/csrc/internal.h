@@ -40,8 +40,8 @@ struct dho2g_ctx {
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
   int gemm_dp = 1;       // pair kernel: data-parallel waves before the stream-K remainder (0: all stream-K)
-  int gemm_mm_tc1 = 1;   // auto: short-K MN-major x MN-major GEMMs on the single-CTA kernel
-  int gemm_bk = 64;      // pair kernel K-block depth: 64 (3 x 64 KB stages) or 32 (6 x 32 KB stages)
+  int gemm_mm_tc1 = 0;   // auto: short-K MN-major x MN-major GEMMs on the single-CTA kernel (off: measured slower since the
+                         // compile-time epilogues)
   int gemm_min_kb = 4;   // pair kernel: minimum k-blocks per CTA pair (caps the worker count of small GEMMs)
   int gemm_worker_cap = 0;  // pair kernel: at most this many CTA pairs (0: all co-resident pairs)
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
@@ -50,7 +50,6 @@ struct dho2g_ctx {
   dho2g::DevBuf<unsigned> gemm_flags2;
   std::vector<cudaEvent_t> lane_events;           // fork / join events (created on first use)
   int pairs_total = 0;                            // co-resident CTA pairs of the pair kernel
-  int gemm_pair_n = 0;   // pair kernel tile width: 0 auto, 128, 256
   dho2g::DevBuf<float> gemm_ws, simt_ws;  // split-K partials / CUDA-core accumulators
   dho2g::DevBuf<unsigned> gemm_flags;
   unsigned gemm_epoch = 0;

@@ -72,51 +72,6 @@ def test_gemm3_cta_modes(ctx, M, N, K, cta):
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
 
-@pytest.mark.parametrize("M,N,K0,K1", [(256, 384, 130, 0), (300, 200, 100, 70), (1024, 3584, 448, 512),
-                                       (8, 40, 96, 0)])
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("pair_n", [128, 256])
-def test_gemm3_pair_tile_width(ctx, M, N, K0, K1, a_mn, b_mn, pair_n):
-    """CTA-pair kernel with 256x128 and 256x256 tiles (K-major / MN-major, two K segments)."""
-    from paper_2505_00982_b200.api import test_gemm_seg
-    rng = np.random.default_rng(M + 3 * N + K0 + K1 + pair_n + 5 * a_mn + b_mn)
-    A0, B0 = rng.standard_normal((M, K0)), rng.standard_normal((N, K0))
-    A1, B1 = rng.standard_normal((M, K1)), rng.standard_normal((N, K1))
-    exact = A0 @ B0.T + A1 @ B1.T
-    scale = np.abs(A0) @ np.abs(B0).T + np.abs(A1) @ np.abs(B1).T
-    ctx.set_option("gemm_cta", 2)
-    ctx.set_option("gemm_pair_n", pair_n)
-    try:
-        c1 = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
-        c2 = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
-    finally:
-        ctx.set_option("gemm_cta", 0)
-        ctx.set_option("gemm_pair_n", 0)
-    assert (c1 == c2).all()
-    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
-
-
-@pytest.mark.parametrize("M,N,K0,K1", [(300, 200, 100, 70), (1024, 3584, 448, 512), (2048, 1000, 3000, 0)])
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
-@pytest.mark.parametrize("bk", [32, 64])
-def test_gemm3_pair_k_block_depth(ctx, M, N, K0, K1, a_mn, b_mn, bk):
-    """CTA-pair kernel with 32-deep (6 stages, SW64 K-major operands) and 64-deep (3 stages, SW128) K-blocks."""
-    from paper_2505_00982_b200.api import test_gemm_seg
-    rng = np.random.default_rng(M + N + K0 + K1 + bk + 3 * a_mn + b_mn)
-    A0, B0 = rng.standard_normal((M, K0)), rng.standard_normal((N, K0))
-    A1, B1 = rng.standard_normal((M, K1)), rng.standard_normal((N, K1))
-    exact = A0 @ B0.T + A1 @ B1.T
-    scale = np.abs(A0) @ np.abs(B0).T + np.abs(A1) @ np.abs(B1).T
-    ctx.set_option("gemm_cta", 2)
-    ctx.set_option("gemm_bk", bk)
-    try:
-        c = test_gemm_seg(ctx, A0, B0, A1, B1, 0, a_mn, b_mn)
-    finally:
-        ctx.set_option("gemm_cta", 0)
-        ctx.set_option("gemm_bk", 64)
-    assert np.max(np.abs(c - exact) / scale) < 2e-5
-
-
 @pytest.mark.parametrize("M,N,K", [(4096, 4096, 256), (6000, 2500, 300), (1024, 3584, 512), (8192, 768, 96)])
 @pytest.mark.parametrize("dp", [0, 1])
 def test_gemm3_pair_dp_stream_k(ctx, M, N, K, dp):
