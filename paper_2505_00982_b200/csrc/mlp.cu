@@ -53,30 +53,39 @@ namespace {
 // ------------------------------------------------------------------ weight operand packing
 // WV[t][o][half*Pin + k] = scale * p(o, k), k < in (pads [in, Pin) stay zero). One row o per
 // blockIdx.y; each thread packs 8 elements (8 independent loads in flight), coalesced across the warp.
-constexpr int kPackPer = 8;
+constexpr int kPackPer = 8;  // elements per thread: 4 pairs
 __global__ void pack_weights_kernel(const float* __restrict__ p, const float* __restrict__ pscale, int in, int out,
                                     int Pin, int half, bf16* __restrict__ WVh, bf16* __restrict__ WVl) {
-  const int k0 = blockIdx.x * (blockDim.x * kPackPer) + threadIdx.x;
+  // thread t of the block owns column pairs (k, k+1), k = k0 + 2 t + 2 u blockDim for u < 4: coalesced fp32
+  // reads, 4-byte bf16x2 writes (k is even and so are Pin and the row base)
+  const int k0 = blockIdx.x * (blockDim.x * kPackPer) + 2 * threadIdx.x;
   const float sc = pscale ? *pscale : 1.0f;
   for (int o = blockIdx.y; o < out; o += gridDim.y) {
-  const float* row = p + (size_t)o * in;
-  float x[kPackPer];
+    const float* row = p + (size_t)o * in;
+    float x[kPackPer];
 #pragma unroll
-  for (int u = 0; u < kPackPer; ++u) {
-    const int k = k0 + u * blockDim.x;
-    x[u] = k < in ? __ldg(row + k) : 0.f;
-  }
-  const size_t base = (size_t)o * (2 * Pin) + (size_t)half * Pin;
-#pragma unroll
-  for (int u = 0; u < kPackPer; ++u) {
-    const int k = k0 + u * blockDim.x;
-    if (k < in) {
-      bf16 h, l;
-      split_bf16(x[u] * sc, h, l);
-      WVh[base + k] = h;
-      WVl[base + k] = l;
+    for (int u = 0; u < kPackPer / 2; ++u) {
+      const int k = k0 + 2 * u * blockDim.x;
+      x[2 * u] = k < in ? __ldg(row + k) : 0.f;
+      x[2 * u + 1] = k + 1 < in ? __ldg(row + k + 1) : 0.f;
     }
-  }
+    const size_t base = (size_t)o * (2 * Pin) + (size_t)half * Pin;
+#pragma unroll
+    for (int u = 0; u < kPackPer / 2; ++u) {
+      const int k = k0 + 2 * u * blockDim.x;
+      if (k < in) {
+        bf16 h0, l0, h1, l1;
+        split_bf16(x[2 * u] * sc, h0, l0);
+        split_bf16(x[2 * u + 1] * sc, h1, l1);
+        if (k + 1 < in) {
+          *reinterpret_cast<__nv_bfloat162*>(WVh + base + k) = __halves2bfloat162(h0, h1);
+          *reinterpret_cast<__nv_bfloat162*>(WVl + base + k) = __halves2bfloat162(l0, l1);
+        } else {
+          WVh[base + k] = h0;
+          WVl[base + k] = l0;
+        }
+      }
+    }
   }
 }
 
