@@ -104,6 +104,14 @@ int dho2g_op_mlp(dho2g_ctx* ctx, dho2g_mlp* mlp, const double* w, const double* 
 int dho2g_op_diag(dho2g_ctx* ctx, const double* spectrum, size_t n, dho2g_op** out);
 /* Dense symmetric n x n operator (column-major), the reference tests' matrix_hvp. */
 int dho2g_op_dense(dho2g_ctx* ctx, const double* mat, size_t n, dho2g_op** out);
+/* QuadraticOracle(spectrum, rotation_seed) (oracle.hpp:84-102, oracle.cpp:233-286): H = diag(spectrum)
+ * (rotation_seed 0) or Q^T diag(spectrum) Q with Q the reference's seeded Gram-Schmidt rotation.
+ * ARGUMENT for an empty spectrum or a zero / non-finite entry, NUMERIC for a degenerate rotation.
+ * With a communicator, create it after dho2g_comm_init (each rank keeps its columns of Q). */
+int dho2g_op_quadratic(dho2g_ctx* ctx, const double* spectrum, size_t n, uint64_t rotation_seed, dho2g_op** out);
+/* QuadraticOracle::apply_h / hvp / grad (the HvpFn of any operator) on host buffers: out = H x
+ * (full length on every rank; null to skip), *value = x^T H x / 2 (QuadraticOracle::value; null to skip). */
+int dho2g_op_apply(dho2g_op* op, const double* x, double* out, double* value);
 /* Host callback operator: out = H v, fp64 host buffers of length n. */
 typedef void (*dho2g_host_hvp)(void* user, const double* v, double* out, size_t n);
 int dho2g_op_host(dho2g_ctx* ctx, dho2g_host_hvp fn, void* user, size_t n, dho2g_op** out);
@@ -173,6 +181,11 @@ typedef struct {
 int dho2g_trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
                          const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
                          int workers, int host_resident, dho2g_trainer** out);
+/* The same loops on a QuadraticOracle problem (dho2g_op_quadratic; test_trainer.cpp:14-21): the
+ * dataset is Dataset::dummy(n_samples) (oracle.cpp:64-68), every gradient is H w, epoch_end's loss is
+ * w^T H w / 2 and accuracy is NaN. */
+int dho2g_trainer_create_quadratic(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_op* quad, size_t n_samples,
+                                   const double* w0, int workers, dho2g_trainer** out);
 int dho2g_trainer_destroy(dho2g_trainer* tr);
 /* Advance `steps` DHO2 steps (inner rounds, trainer.cpp:233-242) including every refresh and
  * ADMM w/dual update the schedule puts inside them. epoch_end evaluation (full-dataset loss,

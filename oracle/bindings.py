@@ -44,7 +44,7 @@ def _f64(a):
 class Op(C.Structure):
     _fields_ = [("kind", C.c_int), ("n", C.c_size_t), ("mat", _dp), ("sizes", _sp), ("n_sizes", C.c_int),
                 ("act", C.c_int), ("loss", C.c_int), ("w", _dp), ("X", _dp), ("y", _dp), ("B", C.c_size_t),
-                ("ncls", C.c_size_t)]
+                ("ncls", C.c_size_t), ("rot_seed", C.c_uint64), ("rot", _dp)]
 
 
 class BaseCfg(C.Structure):
@@ -118,6 +118,15 @@ class CpuChecker:
             tr = tr + [_dp]
             L.ref_set_parallel.argtypes = [C.c_int]
         getattr(L, p + "train_mlp").argtypes = tr
+        # QuadraticOracle (oracle.cpp:233-286)
+        getattr(L, p + "quadratic_rotation").argtypes = [C.c_size_t, C.c_uint64, _dp]
+        self._qapply = "quadratic_apply" if kind == "reference" else "quadratic_apply_seeded"
+        getattr(L, p + self._qapply).argtypes = [_dp, C.c_size_t, C.c_uint64, _dp, _dp, _dp]
+        tq = [C.POINTER(TrainCfg), _dp, C.c_size_t, C.c_uint64, C.c_size_t, _dp, C.c_int, _dp, C.c_size_t, _sp, _dp,
+              _dp, _dp, C.POINTER(C.c_int64), _sp, _sp]
+        if kind == "reference":
+            tq = tq + [_dp]
+        getattr(L, p + "train_quadratic").argtypes = tq
 
     # -- helpers
     def _call(self, name, *args):
@@ -227,7 +236,14 @@ class CpuChecker:
         if mat is not None:
             mat = _f64(np.asarray(mat, np.float64).T.reshape(-1) if np.ndim(mat) == 2 else mat)
             keep.append(mat)
-        o = Op(op["kind"], n, _d(mat) if mat is not None else None, None, 0, 0, 0, None, None, None, 0, 0)
+        o = Op(op["kind"], n, _d(mat) if mat is not None else None, None, 0, 0, 0, None, None, None, 0, 0, 0, None)
+        if op["kind"] == 1 and op.get("rot_seed", 0):
+            o.rot_seed = op["rot_seed"]
+            if self.kind != "reference":
+                Q = self.quadratic_rotation(n, op["rot_seed"])
+                Qc = _f64(Q.T.reshape(-1))
+                keep.append(Qc)
+                o.rot = _d(Qc)
         if op["kind"] == 2:
             sizes = self._sizes(op["sizes"])
             w, X, y = _f64(op["w"]), _f64(op["X"]), _f64(op["y"])
@@ -257,6 +273,20 @@ class CpuChecker:
             cols = it if bd.value else it + 1
             out["basis"] = basis[:n * cols].reshape(cols, n).T.copy()
         return out
+
+    # -- QuadraticOracle, oracle.cpp:233-286
+    def quadratic_rotation(self, n, rotation_seed):
+        """The rotation Q (n x n) of QuadraticOracle(spectrum, rotation_seed)."""
+        Q = np.zeros(n * n)
+        self._call("quadratic_rotation", n, rotation_seed, _d(Q))
+        return Q.reshape(n, n).T.copy()  # column-major storage -> Q[i, j]
+
+    def quadratic_apply(self, spectrum, rotation_seed, x):
+        """(apply_h(x), value(x)) of QuadraticOracle(spectrum, rotation_seed)."""
+        spectrum, x = _f64(spectrum), _f64(x)
+        out, val = np.empty(len(spectrum)), C.c_double()
+        self._call(self._qapply, _d(spectrum), len(spectrum), rotation_seed, _d(x), _d(out), C.byref(val))
+        return out, val.value
 
     # -- optimizer.cpp:37-154
     def base_steps(self, cfg, g_seq, w):
@@ -307,6 +337,30 @@ class CpuChecker:
         k = min(nrows.value, max_rows)
         return dict(w_final=wf, loss=rl[:k].copy(), acc=ra[:k].copy(), resid=rr[:k].copy(), epoch=re[:k].copy(),
                     refreshes=refr.value, safeguard_passes=sg.value, wall_ms=wall.value)
+
+
+def _train_quadratic(self, cfg, spectrum, rotation_seed, w0, workers=1, n_samples=None, max_rows=4096):
+    """train() on Problem{QuadraticOracle(spectrum, rotation_seed), Dataset::dummy(n_samples or workers), w0}
+    (tests/test_trainer.cpp:14-21)."""
+    spectrum, w0 = _f64(spectrum), _f64(w0)
+    n = len(spectrum)
+    wf = np.empty(n)
+    rl, ra, rr = np.empty(max_rows), np.empty(max_rows), np.empty(max_rows)
+    re = np.empty(max_rows, np.int64)
+    nrows, refr, sg = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    args = [C.byref(cfg), _d(spectrum), n, rotation_seed, n_samples or workers, _d(w0), workers, _d(wf), max_rows,
+            C.byref(nrows), _d(rl), _d(ra), _d(rr), re.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(refr),
+            C.byref(sg)]
+    wall = C.c_double()
+    if self.kind == "reference":
+        args.append(C.byref(wall))
+    self._call("train_quadratic", *args)
+    k = min(nrows.value, max_rows)
+    return dict(w_final=wf, loss=rl[:k].copy(), acc=ra[:k].copy(), resid=rr[:k].copy(), epoch=re[:k].copy(),
+                refreshes=refr.value, safeguard_passes=sg.value, wall_ms=wall.value)
+
+
+CpuChecker.train_quadratic = _train_quadratic
 
 
 def reference_available() -> bool:

@@ -600,9 +600,55 @@ int orc_tridiag_eig(size_t n, const double* diag, const double* off, double* val
   return rc;
 }
 
+/* ------------------------------------------- QuadraticOracle (oracle.cpp:233-286) */
+/* Constructor checks (:234-240) on the spectrum. */
+int orc_quadratic_check(const double* spec, size_t n) {
+  if (n == 0) FAIL(ORC_ARGUMENT, "quadratic oracle: empty spectrum");
+  for (size_t i = 0; i < n; ++i)
+    if (spec[i] == 0.0 || !isfinite(spec[i]))
+      FAIL(ORC_ARGUMENT, "quadratic oracle: spectrum entries must be nonzero and finite");
+  return ORC_OK;
+}
+
+/* Rotation Q (n x n column-major, :241-257): Rng(seed*phi) normals, then per column two passes
+ * of modified Gram-Schmidt against the earlier columns and a normalisation. */
+int orc_quadratic_rotation(size_t n, uint64_t rotation_seed, double* Q) {
+  orc_rng_normal(rotation_seed * 0x9e3779b97f4a7c15ULL, n * n, Q);
+  for (size_t j = 0; j < n; ++j) {
+    double* col = Q + j * n;
+    for (int pass = 0; pass < 2; ++pass)
+      for (size_t i = 0; i < j; ++i) {
+        const double* qi = Q + i * n;
+        const double c = dot(qi, col, n);
+        for (size_t t = 0; t < n; ++t) col[t] += -c * qi[t];
+      }
+    const double nrm = sqrt(dot(col, col, n));
+    if (nrm < 1e-12) FAIL(ORC_NUMERIC, "quadratic oracle: degenerate rotation draw");
+    const double inv = 1.0 / nrm;
+    for (size_t t = 0; t < n; ++t) col[t] *= inv;
+  }
+  return ORC_OK;
+}
+
+/* apply_h (:262-272): diag(spec) x, or Q^T (spec o (Q x)) when rotated (Q != NULL). */
+void orc_quadratic_apply(size_t n, const double* spec, const double* Q, const double* x, double* out) {
+  if (!Q) {
+    for (size_t i = 0; i < n; ++i) out[i] = spec[i] * x[i];
+    return;
+  }
+  double* qx = (double*)malloc(n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) { /* linalg::matvec: row i of column-major Q */
+    double acc = 0.0;
+    for (size_t j = 0; j < n; ++j) acc += Q[j * n + i] * x[j];
+    qx[i] = acc * spec[i];
+  }
+  for (size_t j = 0; j < n; ++j) out[j] = dot(Q + j * n, qx, n); /* matvec_transpose */
+  free(qx);
+}
+
 /* ------------------------------------------- operators for the Lanczos checker */
 typedef struct {
-  int kind; /* 0 dense symmetric col-major, 1 diagonal, 2 MLP hvp */
+  int kind; /* 0 dense symmetric col-major, 1 diagonal / rotated quadratic, 2 MLP hvp */
   size_t n;
   const double* mat;
   const size_t* sizes;
@@ -611,6 +657,8 @@ typedef struct {
   const double* X;
   const double* y;
   size_t B, ncls;
+  uint64_t rot_seed;  /* kind 1: QuadraticOracle(mat, rot_seed) */
+  const double* rot;  /* kind 1, rot_seed != 0: its rotation Q (orc_quadratic_rotation) */
 } orc_op;
 
 static int apply_op(const orc_op* op, const double* v, double* out) {
@@ -623,8 +671,8 @@ static int apply_op(const orc_op* op, const double* v, double* out) {
     }
     return ORC_OK;
   }
-  if (op->kind == 1) { /* QuadraticOracle::apply_h, diagonal branch oracle.cpp:264-268 */
-    for (size_t i = 0; i < n; ++i) out[i] = op->mat[i] * v[i];
+  if (op->kind == 1) { /* QuadraticOracle::apply_h, oracle.cpp:262-272 */
+    orc_quadratic_apply(n, op->mat, op->rot_seed ? op->rot : NULL, v, out);
     return ORC_OK;
   }
   return orc_mlp_hvp(op->sizes, op->n_sizes, op->act, op->loss, op->w, v, op->X, op->y, op->B, op->ncls, out);
@@ -957,6 +1005,9 @@ typedef struct {
   /* scratch */
   double *Xb, *yb, *gl, *g;
   uint64_t* perm;
+  /* QuadraticOracle problem (grad = H w for every batch; value = w^T H w / 2; no accuracy) */
+  const double* qspec;
+  const double* qrot;
 } trun;
 
 static void gather_batch(trun* R, const uint64_t* idx, size_t cnt) {
@@ -976,8 +1027,12 @@ static int mean_gradient(trun* R, const double* at, size_t round) {
     orc_shard(R->N, R->C, r, &sb, &se);
     const size_t len = se - sb;
     for (size_t j = 0; j < b; ++j) idx[j] = R->perm[sb + (round * b + j) % len];
-    gather_batch(R, idx, b);
-    rc = orc_mlp_grad(R->sizes, R->nl, R->act, R->loss, at, R->Xb, R->yb, b, R->ncls, r == 0 ? R->g : R->gl);
+    if (R->qspec) {
+      orc_quadratic_apply(R->n, R->qspec, R->qrot, at, r == 0 ? R->g : R->gl);
+    } else {
+      gather_batch(R, idx, b);
+      rc = orc_mlp_grad(R->sizes, R->nl, R->act, R->loss, at, R->Xb, R->yb, b, R->ncls, r == 0 ? R->g : R->gl);
+    }
     if (rc == ORC_OK && r > 0)
       for (size_t i = 0; i < R->n; ++i) R->g[i] += R->gl[i];
   }
@@ -1002,7 +1057,13 @@ static int refresh_ese(trun* R, const double* at, double* eigvals, double* V, si
   size_t m;
   int rc = orc_lanczos_budget(c->k, c->l, R->n, &m);
   if (rc == ORC_OK) {
-    orc_op op = {2, R->n, NULL, R->sizes, R->nl, R->act, R->loss, at, Xc, yc, want, R->ncls};
+    orc_op op = {2, R->n, NULL, R->sizes, R->nl, R->act, R->loss, at, Xc, yc, want, R->ncls, 0, NULL};
+    if (R->qspec) {
+      op.kind = 1;
+      op.mat = R->qspec;
+      op.rot_seed = R->qrot ? 1 : 0;
+      op.rot = R->qrot;
+    }
     double* dg = (double*)malloc((m + 1) * sizeof(double));
     double* of = (double*)malloc((m + 1) * sizeof(double));
     size_t iters, sg;
@@ -1025,12 +1086,20 @@ static int refresh_ese(trun* R, const double* at, double* eigvals, double* V, si
 
 /* epoch_end :150-172 */
 static int epoch_end(trun* R, const double* at, int64_t epoch, const double* resid_against) {
-  double loss, acc;
-  int rc = orc_mlp_value(R->sizes, R->nl, R->act, R->loss, at, R->X, R->y, R->N, R->ncls, &loss);
-  if (rc) return rc;
+  double loss, acc = NAN;
+  int rc = ORC_OK;
+  if (R->qspec) { /* QuadraticOracle::value, oracle.cpp:274-276 */
+    orc_quadratic_apply(R->n, R->qspec, R->qrot, at, R->gl);
+    loss = 0.5 * dot(at, R->gl, R->n);
+  } else {
+    rc = orc_mlp_value(R->sizes, R->nl, R->act, R->loss, at, R->X, R->y, R->N, R->ncls, &loss);
+    if (rc) return rc;
+  }
   if (!isfinite(loss)) FAIL(ORC_NUMERIC, "non-finite loss");
-  rc = orc_mlp_accuracy(R->sizes, R->nl, R->act, R->loss, at, R->X, R->y, R->N, R->ncls, &acc);
-  if (rc) return rc;
+  if (!R->qspec) {
+    rc = orc_mlp_accuracy(R->sizes, R->nl, R->act, R->loss, at, R->X, R->y, R->N, R->ncls, &acc);
+    if (rc) return rc;
+  }
   if (R->n_rows < R->max_rows) {
     R->row_loss[R->n_rows] = loss;
     R->row_acc[R->n_rows] = R->ncls > 0 ? acc : NAN;
@@ -1050,13 +1119,12 @@ static int epoch_end(trun* R, const double* at, int64_t epoch, const double* res
   return ORC_OK;
 }
 
-int orc_train_mlp(const orc_train_cfg* c, const size_t* sizes, int nl, int act, int loss, const double* X,
-                  const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0, int workers,
-                  double* w_final, size_t max_rows, size_t* n_rows, double* row_loss, double* row_acc,
-                  double* row_resid, int64_t* row_epoch, size_t* refreshes, size_t* safeguards) {
-  size_t n;
-  int rc = orc_mlp_dim(sizes, nl, &n);
-  if (rc) return rc;
+static int train_common(const orc_train_cfg* c, const size_t* sizes, int nl, int act, int loss, const double* X,
+                        const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0, int workers,
+                        double* w_final, size_t max_rows, size_t* n_rows, double* row_loss, double* row_acc,
+                        double* row_resid, int64_t* row_epoch, size_t* refreshes, size_t* safeguards, size_t n,
+                        const double* qspec, const double* qrot) {
+  int rc = ORC_OK;
   if (c->batch_size == 0) FAIL(ORC_ARGUMENT, "train: batch_size must be >= 1");
   if (N < (size_t)workers) FAIL(ORC_ARGUMENT, "train: fewer samples than workers");
   trun R;
@@ -1069,11 +1137,13 @@ int orc_train_mlp(const orc_train_cfg* c, const size_t* sizes, int nl, int act, 
   R.X = X;
   R.y = y;
   R.N = N;
-  R.D = sizes[0];
+  R.D = qspec ? 1 : sizes[0];
   R.ncls = ncls;
   R.n = n;
   R.dataset_seed = dataset_seed;
   R.C = workers;
+  R.qspec = qspec;
+  R.qrot = qrot;
   size_t sb, se;
   orc_shard(N, workers, 0, &sb, &se);
   R.rounds = (se - sb + c->batch_size - 1) / c->batch_size;
@@ -1182,5 +1252,60 @@ int orc_train_mlp(const orc_train_cfg* c, const size_t* sizes, int nl, int act, 
   free(nw);
   free(bs);
   free(work);
+  return rc;
+}
+
+int orc_train_mlp(const orc_train_cfg* c, const size_t* sizes, int nl, int act, int loss, const double* X,
+                  const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0, int workers,
+                  double* w_final, size_t max_rows, size_t* n_rows, double* row_loss, double* row_acc,
+                  double* row_resid, int64_t* row_epoch, size_t* refreshes, size_t* safeguards) {
+  size_t n;
+  int rc = orc_mlp_dim(sizes, nl, &n);
+  if (rc) return rc;
+  return train_common(c, sizes, nl, act, loss, X, y, N, ncls, dataset_seed, w0, workers, w_final, max_rows, n_rows,
+                      row_loss, row_acc, row_resid, row_epoch, refreshes, safeguards, n, NULL, NULL);
+}
+
+/* train() on Problem{QuadraticOracle(spec, rotation_seed), Dataset::dummy(N), w0}
+ * (tests/test_trainer.cpp:14-21; Dataset::dummy is oracle.cpp:64-68: D = 1, no classes, seed 0). */
+int orc_train_quadratic(const orc_train_cfg* c, const double* spec, size_t n, uint64_t rotation_seed, size_t N,
+                        const double* w0, int workers, double* w_final, size_t max_rows, size_t* n_rows,
+                        double* row_loss, double* row_acc, double* row_resid, int64_t* row_epoch,
+                        size_t* refreshes, size_t* safeguards) {
+  int rc = orc_quadratic_check(spec, n);
+  if (rc) return rc;
+  if (N == 0) FAIL(ORC_ARGUMENT, "Dataset::dummy: need at least one sample");
+  double* Q = NULL;
+  if (rotation_seed != 0) {
+    Q = (double*)malloc(n * n * sizeof(double));
+    rc = orc_quadratic_rotation(n, rotation_seed, Q);
+  }
+  double* X = (double*)calloc(N, sizeof(double));
+  double* y = (double*)calloc(N, sizeof(double));
+  if (rc == ORC_OK)
+    rc = train_common(c, NULL, 0, 0, 0, X, y, N, 0, 0, w0, workers, w_final, max_rows, n_rows, row_loss, row_acc,
+                      row_resid, row_epoch, refreshes, safeguards, n, spec, Q);
+  free(Q);
+  free(X);
+  free(y);
+  return rc;
+}
+
+/* QuadraticOracle(spec, rotation_seed): apply_h(x) and value(x) = x^T H x / 2 (oracle.cpp:274-276);
+ * same signature as the reference shim's ref_quadratic_apply. */
+int orc_quadratic_apply_seeded(const double* spec, size_t n, uint64_t rotation_seed, const double* x, double* out,
+                               double* value) {
+  int rc = orc_quadratic_check(spec, n);
+  if (rc) return rc;
+  double* Q = NULL;
+  if (rotation_seed != 0) {
+    Q = (double*)malloc(n * n * sizeof(double));
+    rc = orc_quadratic_rotation(n, rotation_seed, Q);
+  }
+  if (rc == ORC_OK) {
+    orc_quadratic_apply(n, spec, Q, x, out);
+    if (value) *value = 0.5 * dot(x, out, n);
+  }
+  free(Q);
   return rc;
 }

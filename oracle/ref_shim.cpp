@@ -96,6 +96,8 @@ struct ref_op {
   const double* y;
   std::size_t B;
   std::size_t ncls;
+  std::uint64_t rot_seed;  // kind 1: QuadraticOracle(mat, rot_seed)
+  const double* rot;       // (the port's precomputed rotation; unused here)
 };
 
 struct ref_base_cfg {
@@ -280,8 +282,9 @@ static HvpFn make_hvp(const ref_op* op, std::shared_ptr<void>& keep) {
     };
   }
   if (op->kind == 1) {
-    // QuadraticOracle(spectrum, 0).apply_h (oracle.cpp:262-268), the bench_main.cpp:84-88 operator
-    auto q = std::make_shared<QuadraticOracle>(Vector(op->mat, op->mat + op->n), 0);
+    // QuadraticOracle(spectrum, rot_seed).apply_h (oracle.cpp:262-272); seed 0 is the
+    // bench_main.cpp:84-88 diagonal operator
+    auto q = std::make_shared<QuadraticOracle>(Vector(op->mat, op->mat + op->n), op->rot_seed);
     keep = q;
     return [q](const Vector& v) { return q->apply_h(v); };
   }
@@ -446,6 +449,70 @@ int ref_train_mlp(const ref_train_cfg* c, const std::size_t* sizes, int nl, int 
     p.oracle = mlp;
     p.dataset = Dataset(sizes[0], ncls, std::vector<double>(X, X + N * sizes[0]),
                         std::vector<double>(y, y + N), dataset_seed);
+    const auto res = train(cfg, p, workers, Schedule::round_robin(), nullptr);
+    std::copy(res.w_final.begin(), res.w_final.end(), w_final);
+    *n_rows = res.metrics.size();
+    for (std::size_t i = 0; i < res.metrics.size() && i < max_rows; ++i) {
+      row_loss[i] = res.metrics[i].train_loss;
+      row_acc[i] = res.metrics[i].train_acc;
+      row_resid[i] = res.metrics[i].residual_norm;
+      row_epoch[i] = res.metrics[i].epoch;
+    }
+    *refreshes = res.ese_refreshes;
+    *safeguards = res.safeguard_passes;
+    *wall_ms = res.raw_wallclock_ms;
+  });
+}
+
+// QuadraticOracle (oracle.cpp:233-286): rotation, apply_h, value
+int ref_quadratic_rotation(std::size_t n, std::uint64_t rotation_seed, double* Q) {
+  return guarded([&] {
+    const QuadraticOracle q(Vector(n, 1.0), rotation_seed);
+    if (q.rotated()) std::copy(q.rotation().data().begin(), q.rotation().data().end(), Q);
+  });
+}
+
+int ref_quadratic_apply(const double* spec, std::size_t n, std::uint64_t rotation_seed, const double* x,
+                        double* out, double* value) {
+  return guarded([&] {
+    const QuadraticOracle q(Vector(spec, spec + n), rotation_seed);
+    const Vector xv(x, x + n);
+    const Vector h = q.apply_h(xv);
+    std::copy(h.begin(), h.end(), out);
+    if (value) *value = q.value(xv, Dataset::dummy(1).full_batch());
+  });
+}
+
+// trainer.cpp:273-298 on Problem{QuadraticOracle, Dataset::dummy(N), w0} (test_trainer.cpp:14-21)
+int ref_train_quadratic(const ref_train_cfg* c, const double* spec, std::size_t n, std::uint64_t rotation_seed,
+                        std::size_t N, const double* w0, int workers, double* w_final, std::size_t max_rows,
+                        std::size_t* n_rows, double* row_loss, double* row_acc, double* row_resid,
+                        std::int64_t* row_epoch, std::size_t* refreshes, std::size_t* safeguards,
+                        double* wall_ms) {
+  return guarded([&] {
+    TrainerConfig cfg;
+    cfg.kind = static_cast<TrainerKind>(c->trainer);
+    cfg.base = base_cfg(&c->base);
+    cfg.k = c->k;
+    cfg.l = c->l;
+    cfg.alpha = c->alpha;
+    cfg.eigval_floor = c->eigval_floor;
+    cfg.refresh_interval = c->refresh_interval;
+    cfg.curvature_batch = c->curvature_batch;
+    cfg.lanczos.reorth_safeguard = c->reorth_safeguard != 0;
+    cfg.lanczos.safeguard_ratio = c->safeguard_ratio;
+    cfg.lanczos.breakdown_rtol = c->breakdown_rtol;
+    cfg.sigma = c->sigma;
+    cfg.outer_rounds = c->outer_rounds;
+    cfg.inner_epochs = c->inner_epochs;
+    cfg.sigma_zero_reduction = c->sigma_zero_reduction != 0;
+    cfg.epochs = c->epochs;
+    cfg.batch_size = c->batch_size;
+    cfg.seed = c->seed;
+    Problem p;
+    p.oracle = std::make_shared<QuadraticOracle>(Vector(spec, spec + n), rotation_seed);
+    p.dataset = Dataset::dummy(N);
+    p.w0.assign(w0, w0 + n);
     const auto res = train(cfg, p, workers, Schedule::round_robin(), nullptr);
     std::copy(res.w_final.begin(), res.w_final.end(), w_final);
     *n_rows = res.metrics.size();

@@ -8,9 +8,9 @@ reference's C++ optimizer API (see api.py).
 from .api import *  # noqa: F401,F403
 from .api import (AdmmState, ArgumentError, BaseConfig, BaseOptimizer, Batch, Context, Dataset, Deltas,
                   DimensionError, DistLanczosOptions, DivergenceError, EseResult, LanczosOptions, MlpOracle,
-                  NumericError, ShardedLanczosResult, Trainer, TrainerConfig, TrainingDiverged, admm_deltas,
+                  NumericError, QuadraticOracle, ShardedLanczosResult, Trainer, TrainerConfig, TrainingDiverged, admm_deltas,
                   admm_dual_update, admm_w_update, blobs_dataset, extract_ese_distributed, fosi_deltas,
-                  lanczos_budget, lanczos_distributed, make_admm_state, shard_for_rank, train)
+                  lanczos_budget, lanczos_distributed, make_admm_state, quadratic_operator, shard_for_rank, train)
 from ._lib import LIB_PATH, EXPORTED  # noqa: F401
 
 __version__ = "0.1.0"

@@ -81,6 +81,8 @@ _SIGS = {
     "dho2g_op_mlp": ([vp, vp, dp, dp, dp, C.c_size_t, C.c_size_t, C.POINTER(vp)], C.c_int),
     "dho2g_op_diag": ([vp, dp, C.c_size_t, C.POINTER(vp)], C.c_int),
     "dho2g_op_dense": ([vp, dp, C.c_size_t, C.POINTER(vp)], C.c_int),
+    "dho2g_op_quadratic": ([vp, dp, C.c_size_t, C.c_uint64, C.POINTER(vp)], C.c_int),
+    "dho2g_op_apply": ([vp, dp, dp, dp], C.c_int),
     "dho2g_op_host": ([vp, HOST_HVP, vp, C.c_size_t, C.POINTER(vp)], C.c_int),
     "dho2g_op_destroy": ([vp], C.c_int),
     "dho2g_lanczos_run": ([vp, vp, C.c_size_t, C.c_uint64, C.POINTER(LanczosOpts), C.POINTER(vp)], C.c_int),
@@ -101,6 +103,7 @@ _SIGS = {
     "dho2g_admm_dual_update": ([vp, C.c_size_t, C.c_double, dp, dp, dp], C.c_int),
     "dho2g_trainer_create": ([vp, C.POINTER(TrainCfg), vp, dp, dp, C.c_size_t, C.c_size_t, C.c_uint64, dp, C.c_int,
                               C.c_int, C.POINTER(vp)], C.c_int),
+    "dho2g_trainer_create_quadratic": ([vp, C.POINTER(TrainCfg), vp, C.c_size_t, dp, C.c_int, C.POINTER(vp)], C.c_int),
     "dho2g_trainer_destroy": ([vp], C.c_int),
     "dho2g_trainer_step": ([vp, C.c_size_t, C.c_int], C.c_int),
     "dho2g_trainer_run": ([vp], C.c_int),

@@ -404,6 +404,92 @@ def diagonal_operator(ctx: Context, spectrum) -> Operator:
     return Operator(ctx, h, s.size)
 
 
+class QuadraticOracle:
+    """QuadraticOracle (oracle.hpp:84-102, oracle.cpp:233-286) on the device: H = diag(spectrum) for
+    rotation_seed 0, else Q^T diag(spectrum) Q with the reference's seeded Gram-Schmidt rotation Q.
+    value/grad/hvp ignore the batch, as in the reference. With a communicator, build it after comm_init."""
+
+    _close_order = 4
+
+    def __init__(self, ctx: Context, spectrum, rotation_seed: int = 0):
+        s = _f64(spectrum)
+        self.ctx, self._spectrum, self.rotation_seed = ctx, s.copy(), int(rotation_seed)
+        h = C.c_void_p()
+        check(lib.dho2g_op_quadratic(ctx.h, _d(s), s.size, self.rotation_seed, C.byref(h)))
+        self.h = h
+        self.n = s.size
+        ctx._adopt(self)
+
+    def dim(self) -> int:
+        return self.n
+
+    def spectrum(self):
+        return self._spectrum.copy()
+
+    def rotated(self) -> bool:
+        return self.rotation_seed != 0
+
+    def _apply(self, x, want_value):
+        x = _f64(x)
+        if x.size != self.n:
+            raise DimensionError("quadratic oracle: dimension mismatch")
+        out = np.empty(self.n)
+        v = C.c_double()
+        check(lib.dho2g_op_apply(self.h, _d(x), _d(out), C.byref(v) if want_value else None))
+        return out, v.value
+
+    def apply_h(self, x):
+        return self._apply(x, False)[0]
+
+    def value(self, w, batch=None) -> float:
+        return self._apply(w, True)[1]
+
+    def grad(self, w, batch=None):
+        return self.apply_h(w)
+
+    def hvp(self, w, v, batch=None):
+        return self.apply_h(v)
+
+    def accuracy(self, w, batch=None):
+        return None
+
+    def operator(self):
+        """The HvpFn view for lanczos_distributed (shares this oracle's device state)."""
+        return _BorrowedOperator(self)
+
+    def close(self):
+        if self.h:
+            lib.dho2g_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _BorrowedOperator:
+    def __init__(self, owner):
+        self._owner = owner
+        self.ctx, self.n = owner.ctx, owner.n
+
+    @property
+    def h(self):
+        return self._owner.h
+
+    def close(self):
+        pass
+
+
+def quadratic_operator(ctx: Context, spectrum, rotation_seed: int = 0) -> Operator:
+    """QuadraticOracle(spectrum, rotation_seed).apply_h as a Lanczos operator (oracle.cpp:262-272)."""
+    s = _f64(spectrum)
+    h = C.c_void_p()
+    check(lib.dho2g_op_quadratic(ctx.h, _d(s), s.size, int(rotation_seed), C.byref(h)))
+    return Operator(ctx, h, s.size)
+
+
 def dense_operator(ctx: Context, H) -> Operator:
     """matrix_hvp of the reference tests (test_support.hpp:74-82)."""
     H = np.asarray(H, np.float64)
@@ -727,6 +813,13 @@ class Dataset:
     def size(self):
         return len(self.labels)
 
+    @staticmethod
+    def dummy(n_samples: int) -> "Dataset":
+        """Dataset::dummy (oracle.cpp:64-68): one zero feature, no classes, shuffle seed 0."""
+        if n_samples == 0:
+            raise ArgumentError("Dataset::dummy: need at least one sample")
+        return Dataset(np.zeros((n_samples, 1)), np.zeros(n_samples), 0, 0)
+
 
 @dataclass
 class TrainResult:
@@ -747,8 +840,10 @@ class TrainResult:
 class Trainer:
     """TrainerRun (trainer.cpp:51-269) on the GPU. step() advances DHO2 steps (inner rounds)."""
 
-    def __init__(self, ctx: Context, cfg: TrainerConfig, mlp: MlpOracle, data: Dataset, w0, workers: int = 1,
+    def __init__(self, ctx: Context, cfg: TrainerConfig, mlp, data: Dataset, w0, workers: int = 1,
                  host_resident: bool = False):
+        """`mlp` is the Problem's oracle: an MlpOracle, or a QuadraticOracle (then `data` is
+        Dataset.dummy(k) as in test_trainer.cpp:14-21; its features are never read)."""
         self.ctx, self.cfg, self.mlp = ctx, cfg, mlp
         X = _f64(data.features)
         y = _f64(data.labels)
@@ -757,8 +852,11 @@ class Trainer:
             raise DimensionError("train: w0 length != oracle dimension")
         c = cfg.to_c()
         h = C.c_void_p()
-        check(lib.dho2g_trainer_create(ctx.h, C.byref(c), mlp.h, _d(X), _d(y), y.size, data.n_classes,
-                                       data.shuffle_seed, _d(w0), workers, int(host_resident), C.byref(h)))
+        if isinstance(mlp, QuadraticOracle):
+            check(lib.dho2g_trainer_create_quadratic(ctx.h, C.byref(c), mlp.h, y.size, _d(w0), workers, C.byref(h)))
+        else:
+            check(lib.dho2g_trainer_create(ctx.h, C.byref(c), mlp.h, _d(X), _d(y), y.size, data.n_classes,
+                                           data.shuffle_seed, _d(w0), workers, int(host_resident), C.byref(h)))
         self.h = h
         self.n = mlp.dim()
         ctx._adopt(self)

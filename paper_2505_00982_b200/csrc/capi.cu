@@ -139,6 +139,10 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
+    else if (k == "lanczos_recurrence") {
+      ctx->lanczos_recurrence = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;
     else if (k == "gs_sm_cap") ctx->gs_sm_cap = (int)value;
@@ -494,6 +498,73 @@ int dho2g_op_diag(dho2g_ctx* ctx, const double* spectrum, size_t n, dho2g_op** o
   });
 }
 
+// QuadraticOracle(spectrum, rotation_seed) (oracle.cpp:233-260) as a device operator.
+int dho2g_op_quadratic(dho2g_ctx* ctx, const double* spectrum, size_t n, uint64_t rotation_seed, dho2g_op** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (n == 0 || !spectrum) fail(DHO2G_ARGUMENT, "quadratic oracle: empty spectrum");
+    for (size_t i = 0; i < n; ++i)
+      if (spectrum[i] == 0.0 || !std::isfinite(spectrum[i]))
+        fail(DHO2G_ARGUMENT, "quadratic oracle: spectrum entries must be nonzero and finite");
+    auto op = std::make_unique<dho2g_op>();
+    op->ctx = ctx;
+    op->kind = rotation_seed ? 4 : 1;
+    op->n = n;
+    upload(op->mat, spectrum, n, ctx->stream);
+    if (rotation_seed) {
+      std::vector<double> Q(n * n);
+      if (!quadratic_rotation(n, rotation_seed, Q.data())) fail(DHO2G_NUMERIC, "quadratic oracle: degenerate rotation draw");
+      size_t b, e;
+      shard_range(n, ctx->world, ctx->rank, &b, &e);
+      op->q_begin = b;
+      op->q_rows = e - b;
+      // this rank's columns: Q^T[:, i] = row i of Q (for Q v) and Q[:, i] (for Q^T y), i in [b, e)
+      std::vector<double> qt(n * op->q_rows), qc(n * op->q_rows);
+      for (size_t i = b; i < e; ++i)
+        for (size_t j = 0; j < n; ++j) {
+          qt[(i - b) * n + j] = Q[j * n + i];
+          qc[(i - b) * n + j] = Q[i * n + j];
+        }
+      upload(op->qrot_t, qt.data(), qt.size(), ctx->stream);
+      upload(op->qrot, qc.data(), qc.size(), ctx->stream);
+      const size_t base = cdiv(n, (size_t)ctx->world);
+      op->qy.alloc(base * ctx->world);
+      op->qy_loc.alloc(std::max<size_t>(base, 1));
+    }
+    *out = op.release();
+  });
+}
+
+// apply_h on host buffers: out = H x (full n, every rank), value = x^T H x / 2 (oracle.cpp:274-276).
+int dho2g_op_apply(dho2g_op* op, const double* x, double* out, double* value) {
+  return guard([&] {
+    if (!op || !x) fail(DHO2G_ARGUMENT, "op_apply: null operator or input");
+    dho2g_ctx* ctx = op->ctx;
+    check_ctx(ctx);
+    const size_t n = op->n;
+    const size_t base = cdiv(n, (size_t)ctx->world);
+    size_t b, e;
+    shard_range(n, ctx->world, ctx->rank, &b, &e);
+    DevBuf<float> xd(base * ctx->world), hd(base * ctx->world), hs(std::max<size_t>(base, 1));
+    DevBuf<double> val(1);
+    const auto xf = to_f32(x, n);
+    cudaStream_t st = ctx->stream;
+    DHO2G_CUDA(cudaMemcpyAsync(xd.p, xf.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+    float* own = ctx->world == 1 ? hd.p : hs.p;
+    op->apply(xd.p, nullptr, own, b, e - b, base);
+    if (value) {
+      dot_dev(st, xd.p + b, own, e - b, 0.5, val.p);
+      ctx->allreduce_sum_f64_ordered(val.p, 1);
+    }
+    if (ctx->world > 1) ctx->allgather_f32(hs.p, hd.p, base);
+    if (out) download(hd.p, out, n, st);
+    if (value) {
+      DHO2G_CUDA(cudaMemcpyAsync(value, val.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+    }
+  });
+}
+
 int dho2g_op_dense(dho2g_ctx* ctx, const double* mat, size_t n, dho2g_op** out) {
   return guard([&] {
     check_ctx(ctx);
@@ -740,6 +811,18 @@ int dho2g_trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* 
   return guard([&] {
     check_ctx(ctx);
     *out = trainer_create(ctx, cfg, mlp, X, y, N, ncls, dataset_seed, w0, workers, host_resident);
+  });
+}
+// train() on Problem{QuadraticOracle, Dataset::dummy(n_samples), w0} (test_trainer.cpp:14-21):
+// Dataset::dummy is oracle.cpp:64-68 (one zero feature, no classes, shuffle seed 0).
+int dho2g_trainer_create_quadratic(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_op* quad, size_t n_samples,
+                                   const double* w0, int workers, dho2g_trainer** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!quad) fail(DHO2G_ARGUMENT, "train: null operator");
+    if (n_samples == 0) fail(DHO2G_ARGUMENT, "Dataset::dummy: need at least one sample");
+    const std::vector<double> zeros(n_samples, 0.0);
+    *out = trainer_create(ctx, cfg, nullptr, zeros.data(), zeros.data(), n_samples, 0, 0, w0, workers, 0, quad);
   });
 }
 int dho2g_trainer_destroy(dho2g_trainer* tr) {

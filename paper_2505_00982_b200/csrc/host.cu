@@ -48,6 +48,32 @@ double Rng::normal() {
   return radius * std::cos(angle);
 }
 
+// QuadraticOracle rotation (oracle.cpp:241-257): Rng(seed*phi) normals filled column-major, then
+// per column two modified Gram-Schmidt passes against the earlier columns and a normalisation.
+// Operator construction (setup, O(n^3) like the reference's "desk-scale" constructor), not a
+// per-iteration cost: every apply_h afterwards runs on the device.
+bool quadratic_rotation(size_t n, uint64_t rotation_seed, double* Q) {
+  Rng rng(rotation_seed * 0x9e3779b97f4a7c15ULL);
+  for (size_t i = 0; i < n * n; ++i) Q[i] = rng.normal();
+  for (size_t j = 0; j < n; ++j) {
+    double* col = Q + j * n;
+    for (int pass = 0; pass < 2; ++pass)
+      for (size_t i = 0; i < j; ++i) {
+        const double* qi = Q + i * n;
+        double c = 0.0;
+        for (size_t t = 0; t < n; ++t) c += qi[t] * col[t];
+        for (size_t t = 0; t < n; ++t) col[t] += -c * qi[t];
+      }
+    double nn = 0.0;
+    for (size_t t = 0; t < n; ++t) nn += col[t] * col[t];
+    const double nrm = std::sqrt(nn);
+    if (nrm < 1e-12) return false;
+    const double inv = 1.0 / nrm;
+    for (size_t t = 0; t < n; ++t) col[t] *= inv;
+  }
+  return true;
+}
+
 // rng.hpp:56-62 Fisher-Yates over iota
 void shuffle_iota(uint64_t seed, size_t n, uint64_t* out) {
   for (size_t i = 0; i < n; ++i) out[i] = i;

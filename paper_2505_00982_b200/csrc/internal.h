@@ -28,6 +28,7 @@ void shuffle_iota(uint64_t seed, size_t n, uint64_t* out);
 void shard_range(size_t n, int world, int rank, size_t* begin, size_t* end);
 size_t lanczos_budget(size_t k, size_t l, size_t n);
 int tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs, std::string* err);
+bool quadratic_rotation(size_t n, uint64_t rotation_seed, double* Q);  // false: degenerate draw
 
 }  // namespace dho2g
 
@@ -44,6 +45,7 @@ struct dho2g_ctx {
                          // compile-time epilogues)
   int gemm_min_kb = 4;   // pair kernel: minimum k-blocks per CTA pair (caps the worker count of small GEMMs)
   int gemm_worker_cap = 0;  // pair kernel: at most this many CTA pairs (0: all co-resident pairs)
+  int lanczos_recurrence = 1;  // Lanczos: recurrence-first projection (1) or the reference's plain CGS (0)
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
@@ -223,7 +225,7 @@ void dev_copy_f32_to_f64(cudaStream_t s, const float* src, double* dst, size_t n
 // ------------------------------------------------------------------------- operators / Lanczos
 struct dho2g_op {
   dho2g_ctx* ctx = nullptr;
-  int kind = 0;  // 0 mlp, 1 diag, 2 dense, 3 host
+  int kind = 0;  // 0 mlp, 1 diag (quadratic, rotation_seed 0), 2 dense, 3 host, 4 rotated quadratic
   size_t n = 0;
   dho2g_mlp* mlp = nullptr;
   dho2g::DevBuf<float> w, X, y, mat;
@@ -232,6 +234,10 @@ struct dho2g_op {
   const float* yptr = nullptr;
   dho2g::DevBuf<int64_t> idx;
   dho2g::DevBuf<float> hfull;  // full-length partial (padded to world * base)
+  // kind 4: this rank's columns of Q^T and Q (n x rows each, column-major), spec in `mat`, and the
+  // intermediate y = spec o (Q v) (own rows, then all-gathered to world * ceil(n/G))
+  dho2g::DevBuf<float> qrot_t, qrot, qy, qy_loc;
+  size_t q_begin = 0, q_rows = 0;
   size_t B = 0, ncls = 0, b0 = 0, b1 = 0;  // this rank's slice of the curvature batch
   double scale = 1.0;
   dho2g_host_hvp fn = nullptr;
@@ -250,6 +256,7 @@ struct LzDev {  // device-resident Lanczos scalars (fixed launch sequence; no ho
   float sigma[kMaxLanczos + 2];  // lazy column normalisation: v_j = sigma_j * D[:, j]
   double pre, beta;
   int iters, stopped, breakdown, safeguards, need_sg;
+  double gram[2][kMaxLanczos + 1];  // G_j = D_j^T D_i of the last two iterations (recurrence-first form)
 };
 }  // namespace dho2g
 
@@ -297,6 +304,8 @@ struct dho2g_ese {
 
 namespace dho2g {
 void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed);
+// out[0] = scale * <a, b> over rows (single CTA, deterministic)
+void dot_dev(cudaStream_t st, const float* a, const float* b, size_t rows, double scale, double* out);
 void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m);
 void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese);
 // Ritz vectors on the tensor cores (3xTF32, ritz_tc.cu); supported for r <= 64, me <= 96.
@@ -339,7 +348,7 @@ struct dho2g_trainer;
 namespace dho2g {
 dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
                               const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
-                              int workers, int host_resident);
+                              int workers, int host_resident, dho2g_op* quad = nullptr);
 void trainer_step(dho2g_trainer* tr, size_t steps, int with_eval);
 void trainer_run(dho2g_trainer* tr);
 void trainer_params(dho2g_trainer* tr, double* w);

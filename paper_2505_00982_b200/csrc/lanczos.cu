@@ -6,7 +6,23 @@
 //   all_gather(D_i)  ->  h = H v_i (operator)  ->
 //   pass 1: r_j = D_j^T h (j <= i), hh = ||h||^2           one read of D[:, 0..i] + h
 //   [all_gather of the (i+2) fp64 partials, rank-ordered sum]
-//   pass 2: h' = h - sum_j D_j sigma_j^2 r_j, ||h'||^2      one read of D[:, 0..i] + h, one write
+//   pass 2: h' = h - sum_j D_j e_j, ||h'||^2                one read of D[:, 0..i] + h, one write
+// with e_j = sigma_j^2 r_j (classical Gram-Schmidt, the reference's arithmetic) or, by default, the
+// recurrence-first form below.
+//
+// Recurrence-first projection (ctx option lanczos_recurrence, default on). The reference projects
+// the raw h = H v_i against all of V in one classical Gram-Schmidt pass. With a basis whose
+// orthogonality error is E (V^T V = I + E) that leaves V^T h' = -E V^T h, and V^T h is dominated by
+// (alpha_i, beta_{i-1}) ~ ||H||, so the error grows by ~||H||/beta every iteration: from the fp32
+// storage floor (1e-8) it reaches O(1) within ~25 iterations on spectra without a large gap (the
+// fp64 reference itself does so within ~50). Here pass 1 also accumulates
+// G_j = D_j^T D_i in the same sweep (D_i comes from L1: no extra HBM bytes), and pass 2 projects
+// h - alpha v_i - beta v_{i-1} (the three-term recurrence) against V with coefficients
+//   c_j = sigma_j (r_j - alpha sigma_i G_j - beta sigma_{i-1} G'_j),  G'_j = D_j^T D_{i-1} (kept
+// from the previous iteration), i.e. the same single sweep with
+//   e_j = sigma_j c_j + [j = i] alpha sigma_i + [j = i-1] beta sigma_{i-1}.
+// Now V^T h' = -E c with c = O(E ||H||): orthogonality stays at the fp32 floor. alpha (= v_i^T h,
+// pre-projection), pre-norm, beta = ||h'|| and the safeguard / breakdown rules are the reference's.
 //   [all_gather of ||h'||^2 partials] -> decide (safeguard / breakdown / beta) on device
 // The launch sequence is fixed (safeguard passes and post-breakdown iterations are predicated on
 // device flags), so the whole refresh needs no host round trip.
@@ -79,54 +95,125 @@ __global__ void lz_init_kernel(LzDev* st, const double* __restrict__ allp, int w
 
 // ------------------------------------------------------------------ GS pass 1: dots
 // rankp[j] = D_j^T h (j < active), rankp[active] = h^T h, fp64, deterministic order.
+// GRAM also accumulates G_j = D_j^T D_{active-1} (j < active) into rankp[goff + j].
+//
+// Butterfly reduction of K per-lane values at once: at each of the first log2(K) levels every lane
+// keeps half of its values and trades the other half with its partner, so K = 8 values take 9 fp64
+// shuffles (4 + 2 + 1 + 2) instead of 40. Lane l ends up holding value
+// sum_L ((l >> L) & 1) * (K >> (L + 1)), for l < K.
+template <int K>
+__device__ __forceinline__ double butterfly_sum(double (&v)[K], int lane) {
+  int n = K, level = 0;
+#pragma unroll
+  for (; n > 1; n >>= 1, ++level) {
+    const bool b = (lane >> level) & 1;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double send = b ? v[i] : v[i + n / 2];
+      const double keep = b ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << level);
+    }
+  }
+  double u = v[0];
+#pragma unroll
+  for (; level < 5; ++level) u += __shfl_xor_sync(0xffffffffu, u, 1 << level);
+  return u;
+}
+template <int K>
+__device__ __forceinline__ int butterfly_index(int lane) {
+  int idx = 0;
+#pragma unroll
+  for (int L = 0; (K >> (L + 1)) > 0; ++L) idx += ((lane >> L) & 1) * (K >> (L + 1));
+  return idx;
+}
+
+template <bool GRAM>
 __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restrict__ D, size_t ldd,
                                                             const float* __restrict__ h, int active, int nchunks,
                                                             int stride, double* __restrict__ part,
                                                             double* __restrict__ rankp, unsigned* ticket,
-                                                            const LzDev* st, int safeguard_pass) {
+                                                            const LzDev* st, int safeguard_pass, int goff) {
   if (st->stopped || (safeguard_pass && !st->need_sg)) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* acc = reinterpret_cast<double*>(smem);  // [kWarps][active+1]
+  double* acc = reinterpret_cast<double*>(smem);  // [kWarps][active+1 (+active)]
   __shared__ bool is_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nj = active + 1;
-  for (int e = threadIdx.x; e < kWarps * nj; e += kThreads) acc[e] = 0.0;
+  const int rowlen = nj + (GRAM ? active : 0);
+  for (int e = threadIdx.x; e < kWarps * rowlen; e += kThreads) acc[e] = 0.0;
   __syncthreads();
-  // Work items (chunk of this CTA, column j <= active, 512-row quarter q) are walked by the warps
-  // independently (no block barrier per chunk); h is read through L1 (reused by the nj items of a
-  // chunk). 4-term products in fp32, everything above in fp64.
-  const int items = nj * (kGsChunk / kSub);
+  // Each warp owns one 512-row quarter q of every chunk of this CTA (kWarps / 4 warps per quarter,
+  // splitting the columns j <= active between them, kCols columns per step). Its h segment (and
+  // D_i's, for G) is loaded into registers once per chunk; per column only D_j's 2 KB segment is
+  // streamed, so the sweep moves exactly the algorithmic bytes. 4-term products in fp32,
+  // everything above in fp64.
+  constexpr int kQuarters = kGsChunk / kSub;
+  constexpr int kPerQuarter = kWarps / kQuarters;
+  constexpr int kCols = 4;  // columns in flight per warp (4 x 2 KB)
+  const int q = warp % kQuarters, j0 = warp / kQuarters;
+  const int rb = q * kSub + lane * 4;
   const int my_chunks = blockIdx.x < nchunks ? (nchunks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const long long total = (long long)my_chunks * items;
-  for (long long idx = warp; idx < total; idx += kWarps) {
-    const int cl = (int)(idx / items), it = (int)(idx % items);
+  double* myacc = acc + warp * rowlen;
+  for (int cl = 0; cl < my_chunks; ++cl) {
     const size_t r0 = ((size_t)blockIdx.x + (size_t)cl * gridDim.x) * kGsChunk;
-    const int j = it / (kGsChunk / kSub), q = it % (kGsChunk / kSub);
-    const int rb = q * kSub + lane * 4;
-    const float* hc = h + r0 + rb;
-    float4 y[4];
+    float4 y[4], z[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) y[k] = __ldg(reinterpret_cast<const float4*>(hc + k * 128));
-    double s = 0.0;
-    if (j < active) {
-      const float* col = D + (size_t)j * ldd + r0 + rb;
-      float4 x[4];
+    for (int k = 0; k < 4; ++k) y[k] = __ldg(reinterpret_cast<const float4*>(h + r0 + rb + k * 128));
+    if (GRAM) {
+      const float* zc = D + (size_t)(active - 1) * ldd + r0 + rb;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + k * 128));
-#pragma unroll
-      for (int k = 0; k < 4; ++k) s += (double)(x[k].x * y[k].x + x[k].y * y[k].y + x[k].z * y[k].z + x[k].w * y[k].w);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) s += (double)(y[k].x * y[k].x + y[k].y * y[k].y + y[k].z * y[k].z + y[k].w * y[k].w);
+      for (int k = 0; k < 4; ++k) z[k] = __ldg(reinterpret_cast<const float4*>(zc + k * 128));
     }
-    s = warp_sum(s);
-    if (lane == 0) acc[warp * nj + j] += s;
+    for (int ja = j0; ja <= active; ja += kCols * kPerQuarter) {
+      constexpr int kVals = GRAM ? 2 * kCols : kCols;
+      // all kCols segments in flight before any arithmetic (j == active is the ||h||^2 item: x = y)
+      float4 x[kCols][4];
+#pragma unroll
+      for (int u = 0; u < kCols; ++u) {
+        const int j = ja + u * kPerQuarter;
+        const float* col = D + (size_t)min(j, active - 1) * ldd + r0 + rb;  // always a valid column
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[u][k] = __ldg(reinterpret_cast<const float4*>(col + k * 128));
+        if (j >= active) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) x[u][k] = j == active ? y[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      double v[kVals];
+#pragma unroll
+      for (int u = 0; u < kCols; ++u) {
+        double sv = 0.0, gv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sv += (double)(x[u][k].x * y[k].x + x[u][k].y * y[k].y + x[u][k].z * y[k].z + x[u][k].w * y[k].w);
+          if (GRAM)  // G_j = D_j^T D_i
+            gv += (double)(x[u][k].x * z[k].x + x[u][k].y * z[k].y + x[u][k].z * z[k].z + x[u][k].w * z[k].w);
+        }
+        if (GRAM) {
+          v[2 * u] = sv;
+          v[2 * u + 1] = gv;
+        } else {
+          v[u] = sv;
+        }
+      }
+      const double t = butterfly_sum<kVals>(v, lane);
+      if (lane < kVals) {
+        const int idx = butterfly_index<kVals>(lane);
+        const int u = GRAM ? idx >> 1 : idx;
+        const int j = ja + u * kPerQuarter;
+        if (GRAM && (idx & 1)) {
+          if (j < active) myacc[nj + j] += t;
+        } else if (j <= active) {
+          myacc[j] += t;
+        }
+      }
+    }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < nj; j += kThreads) {
+  for (int j = threadIdx.x; j < rowlen; j += kThreads) {
     double t = 0.0;
-    for (int w = 0; w < kWarps; ++w) t += acc[w * nj + j];
-    part[(size_t)blockIdx.x * stride + j] = t;
+    for (int w = 0; w < kWarps; ++w) t += acc[w * rowlen + j];
+    part[(size_t)blockIdx.x * stride + (j < nj ? j : goff + (j - nj))] = t;
   }
   __threadfence();
   __syncthreads();
@@ -134,7 +221,8 @@ __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restr
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int j = threadIdx.x; j < nj; j += kThreads) {
+  for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
+    const int j = jj < nj ? jj : goff + (jj - nj);
     double t = 0.0;
     for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * stride + j];
     rankp[j] = t;
@@ -149,24 +237,51 @@ __global__ void __launch_bounds__(kThreads) gs_pass2_kernel(const float* __restr
                                                             const float* hsrc, float* dst, int active, size_t ngroups,
                                                             const double* __restrict__ allp, int world, int stride,
                                                             double* __restrict__ part, double* __restrict__ rankb,
-                                                            unsigned* ticket, LzDev* st, int it, int safeguard_pass) {
+                                                            unsigned* ticket, LzDev* st, int it, int safeguard_pass,
+                                                            int gram, int goff) {
   if (st->stopped || (safeguard_pass && !st->need_sg)) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* e = reinterpret_cast<double*>(smem);
+  double* e = reinterpret_cast<double*>(smem);  // [active+1]
+  double* gj = e + (active + 1);                // [active] (recurrence-first form)
   __shared__ double red[kWarps];
+  __shared__ double alpha_s;
   __shared__ bool is_last;
+  const bool rec = gram && !safeguard_pass;
   for (int j = threadIdx.x; j <= active; j += kThreads) {
     double r = 0.0;
     for (int w = 0; w < world; ++w) r += allp[(size_t)w * stride + j];
     if (j < active) {
       const double sg = (double)st->sigma[j];
-      e[j] = sg * sg * r;
+      e[j] = rec ? r : sg * sg * r;
+      if (j == it) alpha_s = sg * r;
       if (!safeguard_pass && j == it && blockIdx.x == 0) st->diag[it] = sg * r;  // alpha = v_i^T h
+      if (rec) {
+        double g = 0.0;
+        for (int w = 0; w < world; ++w) g += allp[(size_t)w * stride + goff + j];
+        gj[j] = g;
+        if (blockIdx.x == 0) st->gram[it & 1][j] = g;  // G'_j of the next iteration
+      }
     } else if (!safeguard_pass && blockIdx.x == 0) {
       st->pre = sqrt(r);
     }
   }
   __syncthreads();
+  if (rec) {  // recurrence-first coefficients (header comment)
+    const double alpha = alpha_s;
+    const double si = (double)st->sigma[it];
+    const double beta = it > 0 ? st->off[it - 1] : 0.0;
+    const double sp = it > 0 ? (double)st->sigma[it - 1] : 0.0;
+    for (int j = threadIdx.x; j < active; j += kThreads) {
+      const double sj = (double)st->sigma[j];
+      const double gp = it == 0 ? 0.0 : (j < it ? st->gram[(it - 1) & 1][j] : gj[it - 1]);
+      const double c = sj * (e[j] - alpha * si * gj[j] - beta * sp * gp);
+      double ej = sj * c;
+      if (j == it) ej += alpha * si;
+      if (j == it - 1) ej += beta * sp;
+      e[j] = ej;
+    }
+    __syncthreads();
+  }
   // Each warp owns super-groups of 128 float4 groups (512 rows): per basis column it streams one
   // contiguous 2 KB segment (lane l reads groups l, l+32, l+64, l+96), like pass 1's work items.
   double ss = 0.0;
@@ -272,16 +387,38 @@ __global__ void diag_apply_kernel(const float* __restrict__ spec, const float* _
     h[r] = (float)((double)spec[r] * (double)(sc * v[r]));
 }
 
-__global__ void dense_apply_kernel(const float* __restrict__ H, size_t n, const float* __restrict__ v,
-                                   const float* vscale, float* __restrict__ h, size_t begin, size_t rows) {
+// out[r] = rs[r] * <M[:, r], vscale * v> for r < rows: one warp per column of a column-major
+// n x rows panel (coalesced 128-B reads), fp64 accumulation. The dense operator (H symmetric, so
+// row i == column i) and both GEMVs of the rotated quadratic (Q x with Q^T stored column-major,
+// then Q^T y) are this kernel; it streams the panel once, so it is HBM-bound at 4 B per element.
+__global__ void gemv_cols_kernel(const float* __restrict__ M, size_t n, size_t rows, const float* __restrict__ v,
+                                 const float* vscale, const float* __restrict__ rs, float* __restrict__ out) {
   const float sc = vscale ? *vscale : 1.f;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if ((size_t)warp >= rows) return;
-  const float* col = H + (begin + warp) * n;  // symmetric: row i == column i
+  const int lane = threadIdx.x & 31;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    const float* col = M + r * n;
+    double s0 = 0.0, s1 = 0.0;
+    size_t j = lane;
+    for (; j + 32 < n; j += 64) {
+      s0 += (double)__ldg(col + j) * (double)(sc * v[j]);
+      s1 += (double)__ldg(col + j + 32) * (double)(sc * v[j + 32]);
+    }
+    if (j < n) s0 += (double)__ldg(col + j) * (double)(sc * v[j]);
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) out[r] = (float)(rs ? (double)rs[r] * s : s);
+  }
+}
+
+// out[0] = scale * <a, b> over `rows` (one CTA, fixed order: deterministic). Used for the quadratic
+// oracle's value w^T H w / 2 on this rank's rows (O(n) next to the O(n^2) apply).
+__global__ void __launch_bounds__(1024) dot_one_cta_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                           size_t rows, double scale, double* __restrict__ out) {
+  __shared__ double red[32];
   double s = 0.0;
-  for (size_t j = lane; j < n; j += 32) s += (double)col[j] * (double)(sc * v[j]);
-  s = warp_sum(s);
-  if (lane == 0) h[warp] = (float)s;
+  for (size_t i = threadIdx.x; i < rows; i += blockDim.x) s += (double)a[i] * (double)b[i];
+  const double t = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = scale * t;
 }
 
 // ------------------------------------------------------------------ tridiagonal eigensolve
@@ -572,8 +709,27 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
     return;
   }
   if (kind == 2) {
-    dense_apply_kernel<<<cdiv(rows * 32, 256), 256, 0, st>>>(mat.p, n, vfull, vscale, h_shard, begin, rows);
-    DHO2G_LAUNCH();
+    if (rows) {
+      gemv_cols_kernel<<<grid_for(ctx, rows * 32, 256, 8), 256, 0, st>>>(mat.p + begin * n, n, rows, vfull, vscale,
+                                                                        nullptr, h_shard);
+      DHO2G_LAUNCH();
+    }
+    return;
+  }
+  if (kind == 4) {  // QuadraticOracle::apply_h, rotated (oracle.cpp:269-271): Q^T (spec o (Q v))
+    if (begin != q_begin || rows != q_rows) fail(DHO2G_ARGUMENT, "quadratic operator: sharding changed since creation");
+    float* yl = ctx->world == 1 ? qy.p : qy_loc.p;
+    if (rows) {
+      gemv_cols_kernel<<<grid_for(ctx, rows * 32, 256, 8), 256, 0, st>>>(qrot_t.p, n, rows, vfull, vscale,
+                                                                        mat.p + begin, yl);
+      DHO2G_LAUNCH();
+    }
+    if (ctx->world > 1) ctx->allgather_f32(qy_loc.p, qy.p, base);  // base == ceil(n/G): padded == global index
+    if (rows) {
+      gemv_cols_kernel<<<grid_for(ctx, rows * 32, 256, 8), 256, 0, st>>>(qrot.p, n, rows, qy.p, nullptr, nullptr,
+                                                                        h_shard);
+      DHO2G_LAUNCH();
+    }
     return;
   }
   // host callback (tests / reference HvpFn adapters)
@@ -593,6 +749,11 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
 
 namespace dho2g {
 
+void dot_dev(cudaStream_t st, const float* a, const float* b, size_t rows, double scale, double* out) {
+  dot_one_cta_kernel<<<1, 1024, 0, st>>>(a, b, rows, scale, out);
+  DHO2G_LAUNCH();
+}
+
 void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   lz->ctx = ctx;
   lz->n = n;
@@ -607,9 +768,15 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   lz->st.alloc(1);
   const int g1 = ctx->sm_count * 8;  // upper bound of the one-wave grids (256-thread CTAs, <= 8 per SM)
   const int g2 = ctx->sm_count * 8;
-  lz->part.alloc((size_t)std::max(g1, g2) * (m + 2) + 8);
-  lz->rankp.alloc(m + 2);
-  lz->allp.alloc((m + 2) * ctx->world);
+  // per-CTA / per-rank partial rows: [r_0..r_i, ||h||^2] at 0, [G_0..G_{i-1}] at m + 2
+  lz->part.alloc((size_t)std::max(g1, g2) * 2 * (m + 2) + 8);
+  lz->rankp.alloc(2 * (m + 2));
+  lz->allp.alloc(2 * (m + 2) * ctx->world);
+  const size_t smem1_max = (size_t)kWarps * (2 * m + 2) * sizeof(double);
+  if (smem1_max > 48 * 1024) {
+    DHO2G_CUDA(cudaFuncSetAttribute(gs_pass1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1_max));
+    DHO2G_CUDA(cudaFuncSetAttribute(gs_pass1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1_max));
+  }
   lz->ticket.alloc(2);
   ++g_graph_gen;
 }
@@ -624,7 +791,9 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
   cudaStream_t st = ctx->stream;
   const size_t m = lz->m;
   const int world = ctx->world;
-  const int stride = (int)(m + 2);
+  const int stride = (int)(2 * (m + 2));
+  const int goff = (int)(m + 2);
+  const int gram = ctx->lanczos_recurrence ? 1 : 0;
   // v1 (lanczos.cpp:18-26) into column 0, raw; sigma_0 = 1/||v1||
   {
     const int gb = grid_for(ctx, lz->rows, 256);
@@ -651,24 +820,27 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
       vfull = lz->vfull.p;
     }
     op->apply(vfull, &lz->st.p->sigma[i], lz->h.p, lz->begin, lz->rows, lz->base);
-    const size_t smem1 = (size_t)kWarps * (active + 1) * sizeof(double);
-    const size_t smem2 = (size_t)(active + 1) * sizeof(double);
+    const size_t smem1 = (size_t)kWarps * (active + 1 + (gram ? active : 0)) * sizeof(double);
+    const size_t smem2 = (size_t)(2 * active + 1) * sizeof(double);
     const int gs_sms = ctx->gs_sm_cap > 0 ? std::min(ctx->gs_sm_cap, ctx->sm_count) : ctx->sm_count;
-    const int g1 = one_wave_grid(gs_pass1_kernel, kThreads, smem1, gs_sms, (size_t)nchunks);
+    const int g1 = one_wave_grid(gram ? gs_pass1_kernel<true> : gs_pass1_kernel<false>, kThreads, smem1, gs_sms,
+                                 (size_t)nchunks);
     const int g2 = one_wave_grid(gs_pass2_kernel, kThreads, smem2, gs_sms, cdiv(ngroups / 128, kWarps));
     for (int pass = 0; pass < (lz->opts.reorth_safeguard ? 2 : 1); ++pass) {
       const float* hsrc = pass == 0 ? lz->h.p : Dn;
       // algorithmic bytes: active columns of D + h (pass 1); + h' write (pass 2)
       const double gsb = 4.0 * (double)lz->rows * (double)(active + 1);
       int ks = pass == 0 ? ctx->kt_begin() : -1;
-      gs_pass1_kernel<<<g1, kThreads, smem1, st>>>(lz->D.p, lz->ldd, hsrc, active, nchunks, stride, lz->part.p,
-                                                    lz->rankp.p, lz->ticket.p, lz->st.p, pass);
+      auto* k1 = pass == 0 && gram ? gs_pass1_kernel<true> : gs_pass1_kernel<false>;
+      k1<<<g1, kThreads, smem1, st>>>(lz->D.p, lz->ldd, hsrc, active, nchunks, stride, lz->part.p, lz->rankp.p,
+                                      lz->ticket.p, lz->st.p, pass, goff);
       DHO2G_LAUNCH();
       ctx->kt_end(ks, "gs_pass1", gsb);
       if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, stride);
       ks = pass == 0 ? ctx->kt_begin() : -1;
       gs_pass2_kernel<<<g2, kThreads, smem2, st>>>(lz->D.p, lz->ldd, hsrc, Dn, active, ngroups, allp, world, stride,
-                                                    lz->part.p, lz->rankp.p, lz->ticket.p + 1, lz->st.p, (int)i, pass);
+                                                    lz->part.p, lz->rankp.p, lz->ticket.p + 1, lz->st.p, (int)i, pass,
+                                                    gram, goff);
       DHO2G_LAUNCH();
       ctx->kt_end(ks, "gs_pass2", gsb + 4.0 * (double)lz->rows);
       if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);

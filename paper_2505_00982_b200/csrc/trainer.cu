@@ -24,6 +24,7 @@ struct dho2g_trainer {
   dho2g_ctx* ctx = nullptr;
   dho2g_train_cfg cfg{};
   dho2g_mlp* mlp = nullptr;
+  dho2g_op* quad = nullptr;  // QuadraticOracle problem (kind 1 / 4): grad = H w on every batch, no dataset reads
   size_t N = 0, D = 0, ncls = 0, n = 0;
   uint64_t dataset_seed = 0;
   int C = 1;
@@ -37,7 +38,7 @@ struct dho2g_trainer {
   size_t base = 0, begin = 0, end = 0, rows = 0;
   int c0 = 0, c1 = 1;  // logical workers on this rank
   // parameters / state
-  DevBuf<float> w_a_full, g_full, w_a_sh, g_sh, w_sh, pi_sh;
+  DevBuf<float> w_a_full, g_full, w_a_sh, g_sh, w_sh, pi_sh, hw_sh;
   float* w_a_shard = nullptr;
   float* g_shard = nullptr;
   dho2g_opt opt;
@@ -109,6 +110,13 @@ struct dho2g_trainer {
     B_local = idx.size();
     const double scale = (1.0 / (double)b) * (1.0 / (double)C);
     const int ph = ctx->kt_begin();
+    if (quad) {  // QuadraticOracle::grad = apply_h(w) for every worker's batch: the 1/C mean of C equal terms
+      quad->apply(w_a_full.p, nullptr, g_shard, begin, rows, base);
+      dot_dev(ctx->stream, w_a_shard, g_shard, rows, 0.5, stepacc.p);  // value(w) = w^T H w / 2
+      if (ctx->world > 1) ctx->allreduce_sum_f64_ordered(stepacc.p, 1);
+      ctx->kt_end(ph, "phase.grad", 0.0);
+      return;
+    }
     if (B_local > 0) {
       const int64_t* di = upload_indices(idx);
       mlp_load_weights(mlp, w_a_full.p);
@@ -126,22 +134,24 @@ struct dho2g_trainer {
   void refresh() {
     const auto t0 = std::chrono::steady_clock::now();
     const int ph = ctx->kt_begin();
-    const size_t want = std::min<size_t>(cfg.curvature_batch, N);
-    std::vector<uint64_t> all(N);
-    dho2g_curvature_indices(N, want, cfg.seed, refreshes, all.data());
-    std::vector<int64_t> cidx(all.begin(), all.begin() + want);
-    op.idx.ensure_g(want);
-    DHO2G_CUDA(cudaMemcpyAsync(op.idx.p, cidx.data(), want * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-    if (host_resident) h2d_bytes += (double)want * (D + 1) * sizeof(float) + want * sizeof(int64_t);
-    op.B = want;
-    shard_range(want, ctx->world, ctx->rank, &op.b0, &op.b1);  // HVP batch split across ranks
-    op.scale = 1.0 / (double)want;
-    op.weights_loaded = false;  // w_a changed since the last refresh
+    if (!quad) {
+      const size_t want = std::min<size_t>(cfg.curvature_batch, N);
+      std::vector<uint64_t> all(N);
+      dho2g_curvature_indices(N, want, cfg.seed, refreshes, all.data());
+      std::vector<int64_t> cidx(all.begin(), all.begin() + want);
+      op.idx.ensure_g(want);
+      DHO2G_CUDA(cudaMemcpyAsync(op.idx.p, cidx.data(), want * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+      if (host_resident) h2d_bytes += (double)want * (D + 1) * sizeof(float) + want * sizeof(int64_t);
+      op.B = want;
+      shard_range(want, ctx->world, ctx->rank, &op.b0, &op.b1);  // HVP batch split across ranks
+      op.scale = 1.0 / (double)want;
+      op.weights_loaded = false;  // w_a changed since the last refresh
+    }
     const size_t m = cfg.lanczos_m ? cfg.lanczos_m : lanczos_budget(cfg.k, cfg.l, n);
     if (m < 1 || m > n) fail(DHO2G_ARGUMENT, "lanczos_distributed: need 1 <= m <= n");
     if (m > (size_t)kMaxLanczos - 1) fail(DHO2G_ARGUMENT, "lanczos: m exceeds the device limit");
     if (lz.m != m) lanczos_alloc(&lz, ctx, n, m);
-    lanczos_run_into(&lz, &op, dho2g_mix_seed(cfg.seed, 0xbeef + refreshes));
+    lanczos_run_into(&lz, quad ? quad : &op, dho2g_mix_seed(cfg.seed, 0xbeef + refreshes));
     const size_t iters = (size_t)lz.host.iters;
     const size_t keff = std::min(cfg.k, iters);
     const size_t leff = std::min(cfg.l, iters - keff);
@@ -179,12 +189,17 @@ struct dho2g_trainer {
     size_t sb, se;
     shard_range(N, ctx->world, ctx->rank, &sb, &se);
     DHO2G_CUDA(cudaMemsetAsync(acc2.p, 0, 4 * sizeof(double), ctx->stream));
-    mlp_load_weights(mlp, w_a_full.p);
-    const size_t chunk = std::max<size_t>(mlp->Bcap, 1024);
-    for (size_t s0 = sb; s0 < se; s0 += chunk) {
-      const size_t cnt = std::min(chunk, se - s0);
-      if (host_resident) h2d_bytes += (double)cnt * (D + 1) * sizeof(float);
-      mlp_eval_dev(mlp, w_a_full.p, Xptr + s0 * D, yptr + s0, nullptr, cnt, ncls, acc2.p);
+    if (quad) {  // QuadraticOracle::value (oracle.cpp:274-276); accuracy is nullopt
+      quad->apply(w_a_full.p, nullptr, hw_sh.p, begin, rows, base);
+      dot_dev(ctx->stream, w_a_shard, hw_sh.p, rows, 0.5, acc2.p);
+    } else {
+      mlp_load_weights(mlp, w_a_full.p);
+      const size_t chunk = std::max<size_t>(mlp->Bcap, 1024);
+      for (size_t s0 = sb; s0 < se; s0 += chunk) {
+        const size_t cnt = std::min(chunk, se - s0);
+        if (host_resident) h2d_bytes += (double)cnt * (D + 1) * sizeof(float);
+        mlp_eval_dev(mlp, w_a_full.p, Xptr + s0 * D, yptr + s0, nullptr, cnt, ncls, acc2.p);
+      }
     }
     if (with_resid) residual_partial(acc2.p + 2);
     ctx->allreduce_sum_f64_ordered(acc2.p, 3);
@@ -196,7 +211,7 @@ struct dho2g_trainer {
     row.outer = outer;
     row.inner = inner;
     row.epoch = epoch;
-    row.loss = h[0] / (double)N;
+    row.loss = quad ? h[0] : h[0] / (double)N;
     if (!std::isfinite(row.loss))
       fail(DHO2G_DIVERGED, "non-finite loss at epoch " + std::to_string(epoch) + " (trainer " +
                                (cfg.trainer == 2 ? "dho2" : cfg.trainer == 1 ? "fosi" : "sgd") + ")");
@@ -303,7 +318,10 @@ namespace dho2g {
 
 dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
                               const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
-                              int workers, int host_resident) {
+                              int workers, int host_resident, dho2g_op* quad) {
+  if (!quad && !mlp) fail(DHO2G_ARGUMENT, "train: null oracle");
+  if (quad && quad->kind != 1 && quad->kind != 4) fail(DHO2G_ARGUMENT, "train: operator is not a QuadraticOracle");
+  if (quad && quad->ctx != ctx) fail(DHO2G_ARGUMENT, "train: operator belongs to another context");
   if (cfg->batch_size == 0) fail(DHO2G_ARGUMENT, "train: batch_size must be >= 1");
   if (workers < 1) fail(DHO2G_ARGUMENT, "run_workers: world_size must be >= 1");
   if (N < (size_t)workers) fail(DHO2G_ARGUMENT, "train: fewer samples than workers");
@@ -313,10 +331,11 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   t->ctx = ctx;
   t->cfg = *cfg;
   t->mlp = mlp;
+  t->quad = quad;
   t->N = N;
-  t->D = mlp->sizes[0];
-  t->ncls = ncls;
-  t->n = mlp->dim;
+  t->D = quad ? 1 : mlp->sizes[0];
+  t->ncls = quad ? 0 : ncls;
+  t->n = quad ? quad->n : mlp->dim;
   t->dataset_seed = dataset_seed;
   t->C = workers;
   t->host_resident = host_resident;
@@ -390,7 +409,8 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
     size_t eb, ee;
     shard_range(N, ctx->world, ctx->rank, &eb, &ee);
     const size_t b_eval = std::min<size_t>(ee - eb, 1024);
-    mlp_presize(mlp, std::max(std::max(b_step, ce - cb), std::max(b_eval, (size_t)1)));
+    if (!quad) mlp_presize(mlp, std::max(std::max(b_step, ce - cb), std::max(b_eval, (size_t)1)));
+    else t->hw_sh.alloc(std::max<size_t>(t->base, 1));
     gemm_presize(ctx);
     if (cfg->trainer != 0 && (cfg->lanczos_m || (cfg->k + cfg->l >= 1 && cfg->k + cfg->l <= n))) {
       const size_t m = cfg->lanczos_m ? cfg->lanczos_m : lanczos_budget(cfg->k, cfg->l, n);
@@ -449,6 +469,7 @@ double trainer_last_loss(dho2g_trainer* tr) {
   DHO2G_CUDA(cudaMemcpyAsync(h, tr->stepacc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, tr->ctx->stream));
   DHO2G_CUDA(cudaStreamSynchronize(tr->ctx->stream));
   tr->d2h_bytes += 2 * sizeof(double);
+  if (tr->quad) return h[0];
   return tr->B_local ? h[0] / (double)tr->B_local : 0.0;
 }
 bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v) {

@@ -302,8 +302,9 @@ def test_lanczos_large_diagonal(ctx, port):
     assert np.max(np.abs(ese.eigvals - ref["eigvals"]) / np.abs(ref["eigvals"])) <= 1e-4
     assert np.max(np.abs(st.tridiag.diag - ref["diag"]) / np.max(spec)) <= 1e-5
     V, Vr = ese.eigvecs_shard(n), ref["eigvecs"]
-    proj = 2 * V.shape[1] - 2 * np.linalg.norm(V.T @ Vr) ** 2
-    assert proj <= 1e-8  # ||V V^T - Vr Vr^T||_F^2 (sign-invariant)
+    # ||V V^T - Vr Vr^T||_F^2 (sign-invariant; exact also when the fp32 Ritz vectors are not unit to 1e-7)
+    proj = np.sum((V.T @ V) ** 2) + np.sum((Vr.T @ Vr) ** 2) - 2 * np.sum((V.T @ Vr) ** 2)
+    assert np.sqrt(max(proj, 0.0)) <= 1e-4
 
 
 def test_refresh_mlp_c1_eigenvalues(ctx, port):

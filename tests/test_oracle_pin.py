@@ -182,3 +182,104 @@ def test_golden_fixtures(port):
                     curvature_batch=40, seed=21)
     t = port.train_mlp(cfg, sizes, G["tr_X"], G["tr_y"], G["tr_w0"], workers=2, ncls=5)
     assert (t["w_final"] == G["tr_wfinal"]).all() and (t["loss"] == G["tr_loss"]).all()
+
+
+# ------------------------------------------------------------------------------------ QuadraticOracle
+# oracle.cpp:233-286: rotation, apply_h / value, Lanczos and train() on it.
+@pytest.mark.parametrize("n,seed", [(1, 5), (6, 3), (40, 9), (60, 4)])
+def test_quadratic_bitwise(port, ref, n, seed):
+    assert (port.quadratic_rotation(n, seed) == ref.quadratic_rotation(n, seed)).all()
+    spec = 0.5 + np.arange(float(n))
+    x = port.rng_normal(seed + 1, n)
+    for rs in (0, seed):
+        a, va = port.quadratic_apply(spec, rs, x)
+        b, vb = ref.quadratic_apply(spec, rs, x)
+        assert (a == b).all() and va == vb
+
+
+@pytest.mark.parametrize("workers", [1, 3])
+def test_lanczos_rotated_quadratic_bitwise(port, ref, workers):
+    spec = np.random.default_rng(200).uniform(-3.0, 3.0, 40)
+    spec[:6] = [10.0, 8.5, 7.2, 6.0, -9.0, -7.5]
+    op = dict(kind=1, n=40, mat=spec, rot_seed=9)
+    a = port.lanczos(op, 24, 13, k=4, l=2, workers=workers)
+    b = ref.lanczos(op, 24, 13, k=4, l=2, workers=workers)
+    assert (a["diag"] == b["diag"]).all() and (a["off"] == b["off"]).all()
+    assert (a["eigvals"] == b["eigvals"]).all() and (a["eigvecs"] == b["eigvecs"]).all()
+
+
+@pytest.mark.parametrize("trainer,base,workers,k", [("dho2", "adamw", 2, 4), ("fosi", "momentum", 1, 6),
+                                                     ("sgd", "sgd", 2, 0), ("dho2", "adam", 3, 3)])
+def test_train_quadratic_bitwise(port, ref, trainer, base, workers, k):
+    spec = 0.5 + np.arange(12.0)
+    w0 = port.rng_normal(41, 12)
+    cfg = train_cfg(trainer, base_cfg(base), k=k, alpha=1.0, sigma=0.1, outer_rounds=3, inner_epochs=2, epochs=4,
+                    batch_size=1, seed=15)
+    a = port.train_quadratic(cfg, spec, 6, w0, workers=workers)
+    b = ref.train_quadratic(cfg, spec, 6, w0, workers=workers)
+    assert (a["w_final"] == b["w_final"]).all() and (a["loss"] == b["loss"]).all()
+    assert np.array_equal(a["resid"], b["resid"], equal_nan=True) and a["refreshes"] == b["refreshes"]
+
+
+def test_quadratic_known_answers(port):  # test_oracle.cpp:32-66
+    h, v = port.quadratic_apply([4.0, 1.0], 0, [1.0, 1.0])
+    assert abs(v - 2.5) <= 1e-15 and (h == [4.0, 1.0]).all()
+    assert (port.quadratic_apply([4.0, 1.0], 0, [1.0, 0.0])[0] == [4.0, 0.0]).all()
+    spec = 0.5 + np.arange(6.0)
+    w = port.rng_normal(44, 6)
+    g = port.quadratic_apply(spec, 3, w)[0]
+    for i in range(6):  # gradient == central FD of value
+        e = np.zeros(6)
+        e[i] = 1e-5
+        fd = (port.quadratic_apply(spec, 3, w + e)[1] - port.quadratic_apply(spec, 3, w - e)[1]) / 2e-5
+        assert abs(g[i] - fd) <= 1e-6 * max(1.0, abs(fd))
+    H = np.stack([port.quadratic_apply(spec, 3, c)[0] for c in np.eye(6)], axis=1)
+    assert np.linalg.norm(H - H.T) <= 1e-12
+    assert np.allclose(np.linalg.eigvalsh(H), spec, rtol=1e-10, atol=0)
+    Q = port.quadratic_rotation(6, 3)
+    assert np.abs(Q.T @ Q - np.eye(6)).max() <= 1e-14
+    from oracle.bindings import CheckerError
+    for bad in ([], [1.0, 0.0], [1.0, np.inf]):
+        with pytest.raises(CheckerError):
+            port.quadratic_apply(bad, 0, np.ones(len(bad)))
+
+
+def test_train_quadratic_known_answers(port):  # test_trainer.cpp:47-99, :197-239
+    spec = np.array([9.0, 5, 3, 2, 1, 0.5])
+    w0 = port.rng_normal(8, 6)
+    one = port.train_quadratic(train_cfg("fosi", base_cfg("sgd", lr=0.0), k=6, alpha=1.0, epochs=1, batch_size=1,
+                                         seed=5), spec, 4, w0)
+    assert len(one["loss"]) == 1 and one["loss"][0] <= 1e-12 and np.linalg.norm(one["w_final"]) <= 1e-8
+    assert one["refreshes"] == 1
+    spec10 = 1.0 + np.arange(10.0)
+    for workers in (1, 2):
+        w0 = port.rng_normal(31, 10)
+        sgd = port.train_quadratic(train_cfg("sgd", base_cfg("sgd", lr=0.05), epochs=4, batch_size=1, seed=9),
+                                   spec10, 2, w0, workers=workers)
+        fosi = port.train_quadratic(train_cfg("fosi", base_cfg("sgd", lr=0.05), k=0, l=0, epochs=4, batch_size=1,
+                                              seed=9), spec10, 2, w0, workers=workers)
+        assert (sgd["w_final"] == fosi["w_final"]).all() and (sgd["loss"] == fosi["loss"]).all()
+        assert fosi["refreshes"] == 0
+    res = port.train_quadratic(train_cfg("dho2", base_cfg("adamw"), k=4, alpha=1.0, sigma=0.1, outer_rounds=3,
+                                         inner_epochs=2, batch_size=1, seed=15), 0.5 + np.arange(12.0), 6,
+                               port.rng_normal(41, 12), workers=2)
+    assert len(res["loss"]) == 6 and not np.isnan(res["resid"]).any()
+    from oracle.bindings import CheckerError
+    with pytest.raises(CheckerError):  # a diverging run aborts (test_trainer.cpp:181-195)
+        port.train_quadratic(train_cfg("sgd", base_cfg("sgd", lr=1e6), epochs=400, batch_size=1, seed=3),
+                             1.0 + 10.0 * np.arange(8.0), 1, port.rng_normal(2, 8))
+
+
+def test_golden_quadratic(port):
+    G = np.load(os.path.join(GOLDEN, "golden.npz"))
+    if "q_Q" not in G.files:
+        pytest.skip("quadratic fixtures not generated")
+    assert (port.quadratic_rotation(40, 9) == G["q_Q"]).all()
+    hx, val = port.quadratic_apply(G["q_spec"], 9, G["q_x"])
+    assert (hx == G["q_hx"]).all() and val == G["q_val"]
+    a = port.lanczos(dict(kind=1, n=40, mat=G["q_spec"], rot_seed=9), 24, 13, k=4, l=2, workers=2)
+    assert (a["diag"] == G["q_lz_diag"]).all() and (a["eigvecs"] == G["q_lz_eigvecs"]).all()
+    cfg = train_cfg("dho2", base_cfg("adamw"), k=4, alpha=1.0, sigma=0.1, outer_rounds=3, inner_epochs=2,
+                    batch_size=1, seed=15)
+    t = port.train_quadratic(cfg, G["t_spec"], 6, G["t_w0"], workers=2)
+    assert (t["w_final"] == G["t_wfinal"]).all() and (t["loss"] == G["t_loss"]).all()
