@@ -79,12 +79,26 @@ def _lanczos_rank(rank, world, port, n, m, seed, op, q):
         hs = np.zeros(base)
         hs[: e - b] = h
         active = i + 1
-        # pass 1: raw dots + ||h||^2, gathered and summed in rank order
-        p1 = np.concatenate([D[:, :active].T @ hs, [hs @ hs]])
+        # pass 1: raw dots, ||h||^2 and the Gram column G_j = D_j^T D_i, gathered and summed in rank order
+        p1 = np.concatenate([D[:, :active].T @ hs, [hs @ hs], D[:, :active].T @ D[:, i]])
         r = _ordered_sum(_allgather_vec(p1, world))
-        ecoef = sigma[:active] ** 2 * r[:active]
-        diag[i] = sigma[i] * r[i]
+        G = r[active + 1:]
+        r = r[: active + 1]
+        alpha = sigma[i] * r[i]
+        diag[i] = alpha
         pre = np.sqrt(r[active])
+        # pass 2 coefficients: recurrence-first projection (lanczos.cu header)
+        gp = np.zeros(active)
+        beta_prev = off[i - 1] if i > 0 else 0.0
+        if i > 0:
+            gp[:i] = G_prev
+            gp[i] = G[i - 1]
+        c = sigma[:active] * (r[:active] - alpha * sigma[i] * G - beta_prev * sigma[i - 1] * gp * (i > 0))
+        ecoef = sigma[:active] * c
+        ecoef[i] += alpha * sigma[i]
+        if i > 0:
+            ecoef[i - 1] += beta_prev * sigma[i - 1]
+        G_prev = G
         hp = hs - D[:, :active] @ ecoef
         b2 = _ordered_sum(_allgather_vec(np.array([hp @ hp]), world))[0]
         beta = np.sqrt(b2)
