@@ -59,6 +59,17 @@ int dho2g_ctx_kernel_name(dho2g_ctx* ctx, int i, char* buf, size_t len);
 int dho2g_nccl_unique_id(void* id_out_128);
 int dho2g_comm_init(dho2g_ctx* ctx, const void* nccl_id_128, int rank, int world);
 int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world);
+/* Accounting. Communication ledger (CommLedger, collectives.hpp:55-83): one row per
+ * collective round this rank took part in — event index, op ("all_gather", "reduce_scatter",
+ * "all_reduce"), logical floats, rank, modeled floats sent / received. Empty on a single GPU.
+ * Peak float slots per named device object (SlotMeter, accounting.hpp:11-27; names of
+ * dist_lanczos.cpp:41-84 and trainer.cpp:70-71, "vhat_partial" for the row-sharded V_hat). */
+size_t dho2g_ctx_ledger_rows(dho2g_ctx* ctx);
+int dho2g_ctx_ledger_row(dho2g_ctx* ctx, size_t i, int64_t* event, char* op, size_t op_len, int64_t* floats,
+                         int* rank, int64_t* sent, int64_t* received);
+size_t dho2g_ctx_memory_count(dho2g_ctx* ctx);
+int dho2g_ctx_memory_entry(dho2g_ctx* ctx, size_t i, char* name, size_t name_len, int64_t* slots);
+int dho2g_ctx_accounting_reset(dho2g_ctx* ctx);
 
 /* ---- host bookkeeping, bit-exact with the reference (no device needed) ---------------- */
 void dho2g_rng_u64(uint64_t seed, size_t n, uint64_t* out);           /* rng.hpp:18-23 */
@@ -68,6 +79,10 @@ uint64_t dho2g_mix_seed(uint64_t seed, uint64_t salt);                /* trainer
 int dho2g_shard(size_t n, int world, int rank, size_t* begin, size_t* end); /* collectives.cpp:10-20 */
 int dho2g_lanczos_budget(size_t k, size_t l, size_t n, size_t* m);    /* lanczos.cpp:10-16 */
 void dho2g_epoch_permutation(size_t N, uint64_t shuffle_seed, uint64_t epoch, uint64_t* out); /* oracle.cpp:56-62 */
+/* generate_synthetic_dataset (oracle.cpp:77-127): kind "two-gaussians" | "concentric-rings" |
+ * "linear-regression"; X holds n_samples x 3 doubles (row-major, *dim used), y n_samples. */
+int dho2g_synthetic_dataset(const char* kind, size_t n_samples, uint64_t seed, double* X, double* y, size_t* dim,
+                            size_t* ncls);
 /* Curvature batch indices of refresh number `refresh` (trainer.cpp:108-114). */
 void dho2g_curvature_indices(size_t N, size_t want, uint64_t seed, uint64_t refresh, uint64_t* out);
 /* Per-worker sample indices of round `round` (trainer.cpp:92-99). */
@@ -86,6 +101,8 @@ int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* layer_sizes, int n_sizes, int
 int dho2g_mlp_destroy(dho2g_mlp* mlp);
 size_t dho2g_mlp_dim(const dho2g_mlp* mlp);
 int dho2g_mlp_init_params(const dho2g_mlp* mlp, uint64_t seed, double* w);   /* oracle.cpp:386-394 */
+/* The same from the layer sizes alone (host only); *dim = parameter count, w may be NULL to query it. */
+int dho2g_init_params(const size_t* sizes, int n_sizes, uint64_t seed, double* w, size_t* dim);
 /* Synchronous host-buffer calls with the reference's semantics (pure, caller-owned fp64). */
 int dho2g_mlp_value(dho2g_mlp* mlp, const double* w, const double* X, const double* y, size_t B, size_t ncls,
                     double* out);
@@ -175,6 +192,8 @@ typedef struct {
   size_t epochs, batch_size;
   uint64_t seed;
   size_t lanczos_m; /* 0 = lanczos_budget(k, l, n) (trainer.cpp:117); else explicit m (C4) */
+  /* modeled clock of MetricsRow::wallclock_ms (trainer.cpp:137-148); 0 = the reference defaults 50 / 10 */
+  double model_bandwidth_gbps, model_gflops;
 } dho2g_train_cfg;
 /* Dataset (oracle.hpp:25-54) is uploaded once (device resident) unless host_resident != 0, in
  * which case every step gathers its batch from pinned host memory (end-to-end mode). */
@@ -198,6 +217,9 @@ int dho2g_trainer_params(dho2g_trainer* tr, double* w);      /* current w_a (tra
 size_t dho2g_trainer_rows(dho2g_trainer* tr);                /* MetricsRow count */
 int dho2g_trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid,
                           int64_t* epoch, int* refresh);
+/* The remaining MetricsRow fields (trainer.hpp:68-77): outer_k / inner_l (-1 outside DHO2) and the
+ * modeled wallclock_ms (ledger floats x 8 B / bandwidth + GS flops / GFLOP/s, trainer.cpp:137-148). */
+int dho2g_trainer_metrics_ex(dho2g_trainer* tr, size_t max_rows, int64_t* outer, int64_t* inner, double* wallclock);
 /* Mean minibatch loss of the last step (device->host read of the step's result). */
 int dho2g_trainer_last_loss(dho2g_trainer* tr, double* loss);
 /* Counters: "refreshes", "safeguard_passes", "steps", "refresh_ms_last", "h2d_bytes", ... */

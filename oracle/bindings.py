@@ -363,6 +363,72 @@ def _train_quadratic(self, cfg, spectrum, rotation_seed, w0, workers=1, n_sample
 CpuChecker.train_quadratic = _train_quadratic
 
 
+# ---- harness (harness.cpp), reference library only ----------------------------------------------
+def _ref_string(fn, *args):
+    need = C.c_size_t()
+    buf = C.create_string_buffer(1 << 16)
+    rc = fn(*args, buf, len(buf), C.byref(need))
+    return rc, buf, need
+
+
+class RefHarness:
+    """parse_config_text / build_problem / generate_synthetic_dataset / run_experiment / reports of
+    the unmodified reference (oracle/_ref/libdho2ref.so)."""
+
+    def __init__(self):
+        self.lib = C.CDLL(REF_SO)
+        L = self.lib
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_parse_config_json.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t, _sp]
+        L.ref_build_problem.argtypes = [C.c_char_p, C.c_size_t, _dp, _sp, C.c_size_t, _dp, _dp, _sp, _sp, _sp]
+        L.ref_synthetic_dataset.argtypes = [C.c_char_p, C.c_size_t, C.c_uint64, _dp, _dp, _sp, _sp]
+        L.ref_run_experiment_text.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
+        L.ref_memory_report.argtypes = [C.POINTER(C.c_char_p), C.c_int, C.c_char_p, C.c_size_t, _sp]
+        L.ref_comm_report.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, _sp]
+
+    def _err(self, rc):
+        if rc:
+            raise CheckerError(rc, self.lib.ref_last_error().decode())
+
+    def parse_config(self, text, origin="<text>"):
+        import json
+        rc, buf, _ = _ref_string(self.lib.ref_parse_config_json, text.encode(), origin.encode())
+        self._err(rc)
+        return json.loads(buf.value.decode())
+
+    def build_problem(self, text, max_n=1 << 16, max_samples=1 << 14):
+        w0 = np.empty(max_n)
+        X, y = np.empty(max_samples * 3), np.empty(max_samples)
+        n, ns, dim, ncls = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+        self._err(self.lib.ref_build_problem(text.encode(), max_n, _d(w0), C.byref(n), max_samples, _d(X), _d(y),
+                                             C.byref(ns), C.byref(dim), C.byref(ncls)))
+        return dict(w0=w0[: n.value].copy(), X=X[: ns.value * dim.value].reshape(ns.value, dim.value).copy(),
+                    y=y[: ns.value].copy(), n_classes=ncls.value)
+
+    def synthetic_dataset(self, kind, n_samples, seed):
+        X, y = np.empty(n_samples * 3), np.empty(n_samples)
+        dim, ncls = C.c_size_t(), C.c_size_t()
+        self._err(self.lib.ref_synthetic_dataset(kind.encode(), n_samples, seed, _d(X), _d(y), C.byref(dim),
+                                                 C.byref(ncls)))
+        return X[: n_samples * dim.value].reshape(n_samples, dim.value).copy(), y, ncls.value
+
+    def run_experiment(self, text):
+        rc = C.c_int()
+        self._err(self.lib.ref_run_experiment_text(text.encode(), C.byref(rc)))
+        return rc.value
+
+    def memory_report(self, dirs):
+        arr = (C.c_char_p * len(dirs))(*[d.encode() for d in dirs])
+        rc, buf, _ = _ref_string(self.lib.ref_memory_report, arr, len(dirs))
+        self._err(rc)
+        return buf.value.decode()
+
+    def comm_report(self, d):
+        rc, buf, _ = _ref_string(self.lib.ref_comm_report, d.encode())
+        self._err(rc)
+        return buf.value.decode()
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
 

@@ -15,9 +15,12 @@
 #include <string>
 #include <vector>
 
+#include <json.hpp>
+
 #include "dho2/collectives.hpp"
 #include "dho2/dist_lanczos.hpp"
 #include "dho2/errors.hpp"
+#include "dho2/harness.hpp"
 #include "dho2/kernels.hpp"
 #include "dho2/lanczos.hpp"
 #include "dho2/linalg.hpp"
@@ -526,6 +529,96 @@ int ref_train_quadratic(const ref_train_cfg* c, const double* spec, std::size_t 
     *safeguards = res.safeguard_passes;
     *wall_ms = res.raw_wallclock_ms;
   });
+}
+
+// ---- harness (harness.cpp): config parsing, problem construction, artifacts, reports ----------
+static int copy_out(const std::string& text, char* buf, std::size_t len, std::size_t* needed) {
+  if (needed) *needed = text.size() + 1;
+  if (buf && len) {
+    const std::size_t k = std::min(len - 1, text.size());
+    std::memcpy(buf, text.data(), k);
+    buf[k] = 0;
+  }
+  return 0;
+}
+
+// parse_config_text (harness.cpp:181-247) -> every parsed field as JSON (test comparison)
+int ref_parse_config_json(const char* text, const char* origin, char* buf, std::size_t len, std::size_t* needed) {
+  return guarded([&] {
+    const ExperimentConfig c = parse_config_text(text, origin);
+    const TrainerConfig t = build_trainer_config(c);
+    nlohmann::json j;
+    j["trainer"] = c.trainer;
+    j["workers"] = c.workers;
+    j["seed"] = c.seed;
+    j["schedule"] = c.schedule;
+    j["out_dir"] = c.out_dir;
+    j["loss_target"] = c.loss_target;
+    const auto& p = c.problem;
+    j["problem"] = {{"kind", p.kind}, {"n", p.n}, {"condition", p.condition}, {"rotation_seed", p.rotation_seed},
+                    {"spectrum", p.spectrum}, {"dataset", p.dataset}, {"csv_path", p.csv_path},
+                    {"label_col", p.label_col}, {"feature_cols", p.feature_cols}, {"samples", p.samples},
+                    {"dataset_seed", p.dataset_seed}, {"layers", p.layers}, {"activation", p.activation},
+                    {"loss", p.loss}};
+    j["train"] = {{"kind", static_cast<int>(t.kind)}, {"base_kind", static_cast<int>(t.base.kind)},
+                  {"lr", t.base.lr}, {"weight_decay", t.base.weight_decay}, {"beta1", t.base.beta1},
+                  {"beta2", t.base.beta2}, {"eps", t.base.eps}, {"momentum", t.base.momentum}, {"k", t.k},
+                  {"l", t.l}, {"alpha", t.alpha}, {"eigval_floor", t.eigval_floor},
+                  {"refresh_interval", t.refresh_interval}, {"curvature_batch", t.curvature_batch},
+                  {"reorth_safeguard", t.lanczos.reorth_safeguard}, {"safeguard_ratio", t.lanczos.safeguard_ratio},
+                  {"breakdown_rtol", t.lanczos.breakdown_rtol}, {"sigma", t.sigma},
+                  {"outer_rounds", t.outer_rounds}, {"inner_epochs", t.inner_epochs},
+                  {"sigma_zero_reduction", t.sigma_zero_reduction}, {"epochs", t.epochs},
+                  {"batch_size", t.batch_size}, {"seed", t.seed}, {"debug_hash_checks", t.debug_hash_checks},
+                  {"model_bandwidth_gbps", t.model_bandwidth_gbps}, {"model_gflops", t.model_gflops}};
+    copy_out(j.dump(), buf, len, needed);
+  });
+}
+
+// build_problem (harness.cpp:267-309): w0 and the data the problem trains on (n <= max_n)
+int ref_build_problem(const char* text, std::size_t max_n, double* w0, std::size_t* n, std::size_t max_samples,
+                      double* X, double* y, std::size_t* samples, std::size_t* dim, std::size_t* ncls) {
+  return guarded([&] {
+    const ExperimentConfig c = parse_config_text(text, "<text>");
+    const Problem p = build_problem(c);
+    *n = p.w0.size();
+    if (w0 && p.w0.size() <= max_n) std::copy(p.w0.begin(), p.w0.end(), w0);
+    *samples = p.dataset.size();
+    *dim = p.dataset.feature_dim();
+    *ncls = p.dataset.n_classes();
+    if (X && p.dataset.size() <= max_samples) {
+      std::copy(p.dataset.features().begin(), p.dataset.features().end(), X);
+      std::copy(p.dataset.labels().begin(), p.dataset.labels().end(), y);
+    }
+  });
+}
+
+// generate_synthetic_dataset (oracle.cpp:77-127)
+int ref_synthetic_dataset(const char* kind, std::size_t n_samples, std::uint64_t seed, double* X, double* y,
+                          std::size_t* dim, std::size_t* ncls) {
+  return guarded([&] {
+    const Dataset d = generate_synthetic_dataset(parse_dataset_kind(kind), n_samples, seed);
+    std::copy(d.features().begin(), d.features().end(), X);
+    std::copy(d.labels().begin(), d.labels().end(), y);
+    *dim = d.feature_dim();
+    *ncls = d.n_classes();
+  });
+}
+
+// run_experiment (harness.cpp:364-440) on a config text; *rc = its return value (0, or 2 if aborted)
+int ref_run_experiment_text(const char* text, int* rc) {
+  return guarded([&] { *rc = run_experiment(parse_config_text(text, "<text>")); });
+}
+
+int ref_memory_report(const char** dirs, int ndirs, char* buf, std::size_t len, std::size_t* needed) {
+  return guarded([&] {
+    std::vector<std::string> d(dirs, dirs + ndirs);
+    copy_out(memory_report(d), buf, len, needed);
+  });
+}
+
+int ref_comm_report(const char* dir, char* buf, std::size_t len, std::size_t* needed) {
+  return guarded([&] { copy_out(comm_report(dir), buf, len, needed); });
 }
 
 }  // extern "C"

@@ -41,7 +41,8 @@ class TrainCfg(C.Structure):
                 ("curvature_batch", C.c_size_t), ("reorth_safeguard", C.c_int), ("safeguard_ratio", C.c_double),
                 ("breakdown_rtol", C.c_double), ("sigma", C.c_double), ("outer_rounds", C.c_size_t),
                 ("inner_epochs", C.c_size_t), ("sigma_zero_reduction", C.c_int), ("epochs", C.c_size_t),
-                ("batch_size", C.c_size_t), ("seed", C.c_uint64), ("lanczos_m", C.c_size_t)]
+                ("batch_size", C.c_size_t), ("seed", C.c_uint64), ("lanczos_m", C.c_size_t),
+                ("model_bandwidth_gbps", C.c_double), ("model_gflops", C.c_double)]
 
 
 HOST_HVP = C.CFUNCTYPE(None, vp, dp, dp, C.c_size_t)
@@ -59,6 +60,11 @@ _SIGS = {
     "dho2g_nccl_unique_id": ([vp], C.c_int),
     "dho2g_comm_init": ([vp, vp, C.c_int, C.c_int], C.c_int),
     "dho2g_comm_rank": ([vp, ip, ip], C.c_int),
+    "dho2g_ctx_ledger_rows": ([vp], C.c_size_t),
+    "dho2g_ctx_ledger_row": ([vp, C.c_size_t, i64p, C.c_char_p, C.c_size_t, i64p, ip, i64p, i64p], C.c_int),
+    "dho2g_ctx_memory_count": ([vp], C.c_size_t),
+    "dho2g_ctx_memory_entry": ([vp, C.c_size_t, C.c_char_p, C.c_size_t, i64p], C.c_int),
+    "dho2g_ctx_accounting_reset": ([vp], C.c_int),
     "dho2g_rng_u64": ([C.c_uint64, C.c_size_t, up], None),
     "dho2g_rng_normal": ([C.c_uint64, C.c_size_t, dp], None),
     "dho2g_shuffle_iota": ([C.c_uint64, C.c_size_t, up], None),
@@ -66,6 +72,9 @@ _SIGS = {
     "dho2g_shard": ([C.c_size_t, C.c_int, C.c_int, sp, sp], C.c_int),
     "dho2g_lanczos_budget": ([C.c_size_t, C.c_size_t, C.c_size_t, sp], C.c_int),
     "dho2g_epoch_permutation": ([C.c_size_t, C.c_uint64, C.c_uint64, up], None),
+    "dho2g_init_params": ([C.POINTER(C.c_size_t), C.c_int, C.c_uint64, dp, C.POINTER(C.c_size_t)], C.c_int),
+    "dho2g_synthetic_dataset": ([C.c_char_p, C.c_size_t, C.c_uint64, dp, dp, C.POINTER(C.c_size_t),
+                                 C.POINTER(C.c_size_t)], C.c_int),
     "dho2g_curvature_indices": ([C.c_size_t, C.c_size_t, C.c_uint64, C.c_uint64, up], None),
     "dho2g_batch_indices": ([up, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t, up], C.c_int),
     "dho2g_blobs_dataset": ([C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, dp, dp], None),
@@ -110,6 +119,7 @@ _SIGS = {
     "dho2g_trainer_params": ([vp, dp], C.c_int),
     "dho2g_trainer_rows": ([vp], C.c_size_t),
     "dho2g_trainer_metrics": ([vp, C.c_size_t, dp, dp, dp, i64p, ip], C.c_int),
+    "dho2g_trainer_metrics_ex": ([vp, C.c_size_t, i64p, i64p, dp], C.c_int),
     "dho2g_trainer_last_loss": ([vp, dp], C.c_int),
     "dho2g_trainer_stat": ([vp, C.c_char_p, dp], C.c_int),
     "dho2g_trainer_eigvals": ([vp, dp, sp], C.c_int),

@@ -200,6 +200,32 @@ class Context:
             out[name] = (self.stat(f"kt.{name}.ms"), self.stat(f"kt.{name}.count"), self.stat(f"kt.{name}.work"))
         return out
 
+    def ledger(self):
+        """This rank's communication ledger rows (CommLedger::Row, collectives.hpp:58-65):
+        (event, op, floats, rank, sent, received). Empty on a single GPU."""
+        rows = []
+        ev, fl, se, rc = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        rk = C.c_int()
+        op = C.create_string_buffer(32)
+        for i in range(int(lib.dho2g_ctx_ledger_rows(self.h))):
+            check(lib.dho2g_ctx_ledger_row(self.h, i, C.byref(ev), op, 32, C.byref(fl), C.byref(rk), C.byref(se),
+                                           C.byref(rc)))
+            rows.append((ev.value, op.value.decode(), fl.value, rk.value, se.value, rc.value))
+        return rows
+
+    def memory(self):
+        """Peak float slots per named device object (SlotMeter::peak, accounting.hpp:11-27)."""
+        out = {}
+        name = C.create_string_buffer(64)
+        v = C.c_int64()
+        for i in range(int(lib.dho2g_ctx_memory_count(self.h))):
+            check(lib.dho2g_ctx_memory_entry(self.h, i, name, 64, C.byref(v)))
+            out[name.value.decode()] = v.value
+        return out
+
+    def reset_accounting(self):
+        check(lib.dho2g_ctx_accounting_reset(self.h))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -791,6 +817,9 @@ class TrainerConfig:
     batch_size: int = 16
     seed: int = 1
     lanczos_m: int = 0
+    debug_hash_checks: bool = False  # accepted for config parity; replicas are identical by construction
+    model_bandwidth_gbps: float = 50.0
+    model_gflops: float = 10.0
 
     def to_c(self):
         if self.kind not in TRAINERS:
@@ -799,7 +828,7 @@ class TrainerConfig:
                           self.refresh_interval, self.curvature_batch, int(self.lanczos.reorth_safeguard),
                           self.lanczos.safeguard_ratio, self.lanczos.breakdown_rtol, self.sigma, self.outer_rounds,
                           self.inner_epochs, int(self.sigma_zero_reduction), self.epochs, self.batch_size, self.seed,
-                          self.lanczos_m)
+                          self.lanczos_m, self.model_bandwidth_gbps, self.model_gflops)
 
 
 @dataclass
@@ -832,9 +861,28 @@ class TrainResult:
     ese_refresh: np.ndarray
     ese_refreshes: int
     safeguard_passes: int
+    outer_k: np.ndarray = None
+    inner_l: np.ndarray = None
+    wallclock_ms: np.ndarray = None  # modeled clock (trainer.cpp:137-148)
+    gs_flops: int = 0
+    memory: dict = None  # this rank's SlotMeter (per-rank list in the reference)
+    raw_wallclock_ms: float = 0.0
 
     def final_loss(self):
         return float(self.loss[-1]) if len(self.loss) else 0.0
+
+    def final_accuracy(self):
+        """trainer.cpp:27-30: None when the oracle has no accuracy."""
+        if not len(self.acc) or np.isnan(self.acc[-1]):
+            return None
+        return float(self.acc[-1])
+
+    def epochs_to_loss(self, target):
+        """trainer.cpp:32-37: epochs run until the first row whose loss is <= target."""
+        for e, v in zip(self.epoch, self.loss):
+            if v <= target:
+                return int(e) + 1
+        return None
 
 
 class Trainer:
@@ -901,8 +949,14 @@ class Trainer:
 
     def result(self) -> TrainResult:
         loss, acc, res, ep, rf = self.metrics()
+        n = len(loss)
+        outer, inner = np.empty(n, np.int64), np.empty(n, np.int64)
+        wall = np.empty(n)
+        check(lib.dho2g_trainer_metrics_ex(self.h, n, outer.ctypes.data_as(L.i64p), inner.ctypes.data_as(L.i64p),
+                                           _d(wall)))
         return TrainResult(self.params(), loss, acc, res, ep, rf.astype(bool), int(self.stat("refreshes")),
-                           int(self.stat("safeguard_passes")))
+                           int(self.stat("safeguard_passes")), outer, inner, wall, int(self.stat("gs_flops")),
+                           self.ctx.memory())
 
     def close(self):
         if self.h:
@@ -918,9 +972,13 @@ class Trainer:
 
 def train(ctx: Context, cfg: TrainerConfig, mlp: MlpOracle, data: Dataset, w0, workers: int = 1) -> TrainResult:
     """train() (trainer.hpp:95-96 / trainer.cpp:273-298)."""
+    import time
     tr = Trainer(ctx, cfg, mlp, data, w0, workers)
     try:
+        t0 = time.perf_counter()
         tr.run()
-        return tr.result()
+        res = tr.result()
+        res.raw_wallclock_ms = (time.perf_counter() - t0) * 1e3  # measured (trainer.cpp:280-296)
+        return res
     finally:
         tr.close()

@@ -250,6 +250,47 @@ int dho2g_comm_init(dho2g_ctx* ctx, const void* nccl_id_128, int rank, int world
   });
 }
 
+// ------------------------------------------------------------------ accounting (CommLedger / SlotMeter)
+size_t dho2g_ctx_ledger_rows(dho2g_ctx* ctx) { return ctx ? ctx->ledger.size() : 0; }
+int dho2g_ctx_ledger_row(dho2g_ctx* ctx, size_t i, int64_t* event, char* op, size_t op_len, int64_t* floats,
+                         int* rank, int64_t* sent, int64_t* received) {
+  return guard([&] {
+    if (!ctx || i >= ctx->ledger.size()) fail(DHO2G_ARGUMENT, "ledger: row out of range");
+    const auto& r = ctx->ledger[i];
+    if (event) *event = r.event;
+    if (op && op_len) {
+      std::strncpy(op, r.op.c_str(), op_len - 1);
+      op[op_len - 1] = 0;
+    }
+    if (floats) *floats = r.floats;
+    if (rank) *rank = r.rank;
+    if (sent) *sent = r.sent;
+    if (received) *received = r.received;
+  });
+}
+size_t dho2g_ctx_memory_count(dho2g_ctx* ctx) { return ctx ? ctx->slots.size() : 0; }
+int dho2g_ctx_memory_entry(dho2g_ctx* ctx, size_t i, char* name, size_t name_len, int64_t* slots) {
+  return guard([&] {
+    if (!ctx || i >= ctx->slots.size()) fail(DHO2G_ARGUMENT, "memory: entry out of range");
+    auto it = ctx->slots.begin();
+    std::advance(it, (long)i);
+    if (name && name_len) {
+      std::strncpy(name, it->first.c_str(), name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    if (slots) *slots = it->second;
+  });
+}
+int dho2g_ctx_accounting_reset(dho2g_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) fail(DHO2G_ARGUMENT, "null context");
+    ctx->ledger.clear();
+    ctx->ledger_next = 0;
+    ctx->ledger_sent = 0;
+    ctx->slots.clear();
+  });
+}
+
 int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world) {
   return guard([&] {
     if (!ctx) fail(DHO2G_ARGUMENT, "null context");
@@ -280,6 +321,53 @@ int dho2g_shard(size_t n, int world, int rank, size_t* begin, size_t* end) {
 int dho2g_lanczos_budget(size_t k, size_t l, size_t n, size_t* m) {
   return guard([&] { *m = lanczos_budget(k, l, n); });
 }
+int dho2g_synthetic_dataset(const char* kind, size_t n_samples, uint64_t seed, double* X, double* y, size_t* dim,
+                            size_t* ncls) {
+  return guard([&] {
+    const std::string k = kind ? kind : "";
+    uint64_t code;  // DatasetKind enumerators (oracle.hpp)
+    if (k == "two-gaussians") code = 0;
+    else if (k == "concentric-rings") code = 1;
+    else if (k == "linear-regression") code = 2;
+    else fail(DHO2G_ARGUMENT, "unknown dataset kind: '" + k + "'");
+    if (n_samples == 0) fail(DHO2G_ARGUMENT, "generate_synthetic_dataset: n_samples must be >= 1");
+    Rng rng(seed * 0x2545f4914f6cdd1dULL + code + 1);
+    if (code == 0) {  // alternating classes at means -1.5 / +1.5
+      for (size_t i = 0; i < n_samples; ++i) {
+        const double mean = (i % 2) == 0 ? -1.5 : 1.5;
+        X[2 * i] = mean + rng.normal();
+        X[2 * i + 1] = mean + rng.normal();
+        y[i] = (double)(i % 2);
+      }
+      *dim = 2;
+      *ncls = 2;
+    } else if (code == 1) {  // rings of radius 1 / 2.5
+      for (size_t i = 0; i < n_samples; ++i) {
+        const double radius = ((i % 2) == 0 ? 1.0 : 2.5) + 0.15 * rng.normal();
+        const double theta = 2.0 * 3.141592653589793 * rng.uniform();
+        X[2 * i] = radius * std::cos(theta);
+        X[2 * i + 1] = radius * std::sin(theta);
+        y[i] = (double)(i % 2);
+      }
+      *dim = 2;
+      *ncls = 2;
+    } else {  // y = beta^T x + 0.05 N(0,1), d = 3
+      double beta[3];
+      for (double& b : beta) b = rng.normal();
+      for (size_t i = 0; i < n_samples; ++i) {
+        double dot = 0.0;
+        for (size_t j = 0; j < 3; ++j) {
+          X[i * 3 + j] = rng.normal();
+          dot += beta[j] * X[i * 3 + j];
+        }
+        y[i] = dot + 0.05 * rng.normal();
+      }
+      *dim = 3;
+      *ncls = 0;
+    }
+  });
+}
+
 void dho2g_epoch_permutation(size_t N, uint64_t shuffle_seed, uint64_t epoch, uint64_t* out) {
   shuffle_iota(shuffle_seed * 0x9e3779b97f4a7c15ULL + epoch + 1, N, out);
 }
@@ -382,6 +470,28 @@ int dho2g_mlp_init_params(const dho2g_mlp* mlp, uint64_t seed, double* w) {  // 
     for (const LayerDesc& l : mlp->layers) {
       const double sd = 1.0 / std::sqrt(static_cast<double>(l.in));
       for (size_t k = 0; k < (size_t)l.in * l.out; ++k) w[l.w_off + k] = sd * rng.normal();
+    }
+  });
+}
+
+// The same draw from the layer sizes alone (no context / device): layer-major W then b (oracle.cpp:312-323).
+int dho2g_init_params(const size_t* sizes, int n_sizes, uint64_t seed, double* w, size_t* dim) {
+  return guard([&] {
+    if (!sizes || n_sizes < 3) fail(DHO2G_ARGUMENT, "mlp oracle: need at least one hidden layer");
+    size_t off = 0;
+    std::vector<size_t> w_off;
+    for (int t = 0; t + 1 < n_sizes; ++t) {
+      if (sizes[t] == 0 || sizes[t + 1] == 0) fail(DHO2G_ARGUMENT, "mlp oracle: zero layer size");
+      w_off.push_back(off);
+      off += sizes[t] * sizes[t + 1] + sizes[t + 1];
+    }
+    *dim = off;
+    if (!w) return;
+    std::fill(w, w + off, 0.0);
+    Rng rng(seed * 0x9e3779b97f4a7c15ULL + 17);
+    for (int t = 0; t + 1 < n_sizes; ++t) {
+      const double sd = 1.0 / std::sqrt(static_cast<double>(sizes[t]));
+      for (size_t k = 0; k < sizes[t] * sizes[t + 1]; ++k) w[w_off[t] + k] = sd * rng.normal();
     }
   });
 }
@@ -841,6 +951,9 @@ size_t dho2g_trainer_rows(dho2g_trainer* tr) { return tr ? trainer_rows(tr) : 0;
 int dho2g_trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
                           int* refresh) {
   return guard([&] { trainer_metrics(tr, max_rows, loss, acc, resid, epoch, refresh); });
+}
+int dho2g_trainer_metrics_ex(dho2g_trainer* tr, size_t max_rows, int64_t* outer, int64_t* inner, double* wallclock) {
+  return guard([&] { trainer_metrics_ex(tr, max_rows, outer, inner, wallclock); });
 }
 int dho2g_trainer_last_loss(dho2g_trainer* tr, double* loss) {
   return guard([&] { *loss = trainer_last_loss(tr); });

@@ -251,7 +251,7 @@ void dho2g_ctx::kt_flush() {
   }
 }
 
-void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count) {
+void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
   if (world == 1) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     return;
@@ -259,9 +259,12 @@ void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count) {
   DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream));
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 8 * world);
+  const int64_t c = (int64_t)count, w1 = world - 1;
+  if (std::string(op) == "all_reduce") ledger_add(op, c, c * w1, c * w1);  // collectives.cpp:306-319 model
+  else ledger_add(op, c * world, c * w1, c * w1);
 }
 
-void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count) {
+void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, const char* op) {
   if (world == 1) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
@@ -269,6 +272,8 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count) {
   DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream));
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
+  const int64_t c = (int64_t)count, w1 = world - 1;
+  ledger_add(op, c * world, c * w1, c * w1);
 }
 
 void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count) {
@@ -279,6 +284,8 @@ void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count)
   DHO2G_NCCLCHK(dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream));
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
+  const int64_t c = (int64_t)count, w1 = world - 1;
+  ledger_add("reduce_scatter", c * world, c * w1, c * w1);
 }
 
 namespace {
@@ -294,7 +301,7 @@ __global__ void ordered_sum_kernel(const double* __restrict__ all, double* __res
 void dho2g_ctx::allreduce_sum_f64_ordered(double* inout, size_t count) {
   if (world == 1) return;
   gather_f64.ensure(count * world);
-  allgather_f64(inout, gather_f64.p, count);
+  allgather_f64(inout, gather_f64.p, count, "all_reduce");
   ordered_sum_kernel<<<(unsigned)std::min<size_t>(dho2g::cdiv(count, 256), 1024), 256, 0, stream>>>(
       gather_f64.p, inout, count, world);
   DHO2G_LAUNCH();

@@ -78,11 +78,36 @@ struct dho2g_ctx {
   dho2g::DevBuf<double> gather_f64;  // world * count scratch for ordered all-reduces
   dho2g::DevBuf<double> pinned_dummy;
 
-  // Collectives (NCCL over NVLink at world > 1; identity at world == 1).
-  void allgather_f64(const double* send, double* recv, size_t count);
-  void allgather_f32(const float* send, float* recv, size_t count);
+  // Collectives (NCCL over NVLink at world > 1; identity at world == 1). `op` names the logical
+  // collective in the communication ledger (an all-gather of partials that every rank then sums in
+  // rank order is the reference's "all_reduce").
+  void allgather_f64(const double* send, double* recv, size_t count, const char* op = "all_gather");
+  void allgather_f32(const float* send, float* recv, size_t count, const char* op = "all_gather");
   void reduce_scatter_f32(const float* send, float* recv, size_t count);
   void allreduce_sum_f64_ordered(double* inout, size_t count);  // all_gather + rank-ordered sum
+  // Communication ledger (CommLedger, collectives.hpp:55-83): one row per collective this rank took
+  // part in (world > 1 only: a single GPU communicates nothing). floats = the round's logical result
+  // length; sent / received model ring traffic of this rank, in floats.
+  struct LedgerRow {
+    int64_t event;
+    std::string op;
+    int64_t floats;
+    int rank;
+    int64_t sent, received;
+  };
+  std::vector<LedgerRow> ledger;
+  int64_t ledger_next = 0;
+  int64_t ledger_sent = 0;  // this rank's floats sent, all rounds
+  void ledger_add(const char* op, int64_t floats, int64_t sent, int64_t received) {
+    ledger.push_back({ledger_next++, op, floats, rank, sent, received});
+    ledger_sent += sent;
+  }
+  // Peak float-slot accounting per named device object (SlotMeter, accounting.hpp:11-27).
+  std::map<std::string, int64_t> slots;
+  void meter(const char* name, int64_t n) {
+    auto& p = slots[name];
+    if (n > p) p = n;
+  }
   void sync();
   void bump(const char* key, double v) { stats[key] += v; }
 };
@@ -256,6 +281,7 @@ struct LzDev {  // device-resident Lanczos scalars (fixed launch sequence; no ho
   float sigma[kMaxLanczos + 2];  // lazy column normalisation: v_j = sigma_j * D[:, j]
   double pre, beta;
   int iters, stopped, breakdown, safeguards, need_sg;
+  long long sg_cols;  // sum over safeguard passes of the active column count (gs_flops accounting)
   double gram[2][kMaxLanczos + 1];  // G_j = D_j^T D_i of the last two iterations (recurrence-first form)
 };
 }  // namespace dho2g
@@ -353,6 +379,7 @@ void trainer_step(dho2g_trainer* tr, size_t steps, int with_eval);
 void trainer_run(dho2g_trainer* tr);
 void trainer_params(dho2g_trainer* tr, double* w);
 size_t trainer_rows(dho2g_trainer* tr);
+void trainer_metrics_ex(dho2g_trainer* tr, size_t max_rows, int64_t* outer, int64_t* inner, double* wallclock);
 void trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
                      int* refresh);
 double trainer_last_loss(dho2g_trainer* tr);

@@ -89,6 +89,7 @@ __global__ void lz_init_kernel(LzDev* st, const double* __restrict__ allp, int w
   st->breakdown = 0;
   st->safeguards = 0;
   st->need_sg = 0;
+  st->sg_cols = 0;
   st->pre = 0.0;
   st->beta = 0.0;
 }
@@ -365,6 +366,7 @@ __global__ void lz_decide_kernel(LzDev* st, const double* __restrict__ allb, int
   if (!safeguard_pass && safeguard_on && beta > rtol * pre && beta < ratio * pre) {
     st->need_sg = 1;
     st->safeguards += 1;
+    st->sg_cols += it + 1;
     return;
   }
   st->need_sg = 0;
@@ -778,6 +780,11 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
     DHO2G_CUDA(cudaFuncSetAttribute(gs_pass1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1_max));
   }
   lz->ticket.alloc(2);
+  // SlotMeter names of dist_lanczos.cpp:41-84 (logical slots; the basis is stored padded to ldd rows)
+  ctx->meter("D_shard", (int64_t)(lz->rows * (m + 1)));
+  ctx->meter("B", (int64_t)(2 * m + 1));
+  ctx->meter("h_shard", (int64_t)lz->rows);
+  if (ctx->world > 1) ctx->meter("v_full", (int64_t)n);
   ++g_graph_gen;
 }
 
@@ -800,7 +807,7 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
     gauss_kernel<<<gb, 256, 0, st>>>(s0, s0p, lz->begin, lz->rows, lz->D.p, lz->part.p);
     gauss_norm_kernel<<<1, 32, 0, st>>>(lz->part.p, gb, lz->rankp.p);
     DHO2G_LAUNCH();
-    ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);
+    ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1, "all_reduce");
     lz_init_kernel<<<1, 32, 0, st>>>(lz->st.p, lz->allp.p, world, 1);
     DHO2G_LAUNCH();
   }
@@ -836,14 +843,14 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
                                       lz->ticket.p, lz->st.p, pass, goff);
       DHO2G_LAUNCH();
       ctx->kt_end(ks, "gs_pass1", gsb);
-      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, stride);
+      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, stride, "all_reduce");
       ks = pass == 0 ? ctx->kt_begin() : -1;
       gs_pass2_kernel<<<g2, kThreads, smem2, st>>>(lz->D.p, lz->ldd, hsrc, Dn, active, ngroups, allp, world, stride,
                                                     lz->part.p, lz->rankp.p, lz->ticket.p + 1, lz->st.p, (int)i, pass,
                                                     gram, goff);
       DHO2G_LAUNCH();
       ctx->kt_end(ks, "gs_pass2", gsb + 4.0 * (double)lz->rows);
-      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1);
+      if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, 1, "all_reduce");
       lz_decide_kernel<<<1, 32, 0, st>>>(lz->st.p, allb, world, world > 1 ? 1 : 1, (int)i, pass,
                                          lz->opts.reorth_safeguard, lz->opts.safeguard_ratio, lz->opts.breakdown_rtol);
       DHO2G_LAUNCH();
@@ -989,6 +996,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   DHO2G_LAUNCH();
   ctx->kt_end(kq, "extract.tql2", 0.0);
   ese->V.ensure(ese->ldv * r);  // padded rows stay zero (Ritz writes rows < rows only)
+  ctx->meter("vhat_partial", (int64_t)(lz->rows * r));  // V_hat stays row-sharded: no "vhat" assembly
   const int kr = ctx->kt_begin();
   if (ctx->ritz_tc && ritz_tc_supported(me, r)) {
     ritz_tc(ctx, lz->D.p, lz->ldd, me, U.p, r, ese->V.p, ese->ldv, lz->rows, lz->xUs);

@@ -17,6 +17,7 @@ using namespace dho2g;
 struct MetricsRowH {
   int64_t outer = -1, inner = -1, epoch = 0;
   double loss = 0, acc = NAN, resid = NAN;
+  double wallclock = 0;  // modeled clock (trainer.cpp:137-148)
   int refresh = 0;
 };
 
@@ -52,6 +53,8 @@ struct dho2g_trainer {
   std::vector<uint64_t> perm;
   int64_t perm_epoch = -1;
   size_t refreshes = 0, safeguards = 0, steps = 0;
+  int64_t gs_flops = 0;     // reference accounting (dist_lanczos.cpp:73): 4 active rows + rows per projection
+  double sent_host = 0;     // staging for the all-rank floats-sent total of the modeled clock
   double refresh_ms_last = 0, refresh_ms_total = 0;
   bool refreshed_this_epoch = false;
   bool done = false;
@@ -160,6 +163,11 @@ struct dho2g_trainer {
     ctx->kt_end(ph, "phase.refresh", 0.0);
     last_eigvals = ese.eigvals;
     safeguards += (size_t)lz.host.safeguards;
+    {
+      const int64_t it = (int64_t)lz.host.iters, r = (int64_t)lz.rows;
+      gs_flops += 4 * r * (it * (it + 1) / 2) + it * r;                                  // one projection per iteration
+      gs_flops += 4 * r * (int64_t)lz.host.sg_cols + (int64_t)lz.host.safeguards * r;  // safeguard passes
+    }
     ++refreshes;
     refresh_ms_last = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     refresh_ms_total += refresh_ms_last;
@@ -202,11 +210,13 @@ struct dho2g_trainer {
       }
     }
     if (with_resid) residual_partial(acc2.p + 2);
-    ctx->allreduce_sum_f64_ordered(acc2.p, 3);
-    double h[3];
-    DHO2G_CUDA(cudaMemcpyAsync(h, acc2.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    sent_host = (double)ctx->ledger_sent;  // this rank's ledger traffic; summed over ranks below
+    DHO2G_CUDA(cudaMemcpyAsync(acc2.p + 3, &sent_host, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->allreduce_sum_f64_ordered(acc2.p, 4);
+    double h[4];
+    DHO2G_CUDA(cudaMemcpyAsync(h, acc2.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
-    d2h_bytes += 3 * sizeof(double);
+    d2h_bytes += 4 * sizeof(double);
     MetricsRowH row;
     row.outer = outer;
     row.inner = inner;
@@ -218,6 +228,12 @@ struct dho2g_trainer {
     row.acc = ncls > 0 ? h[1] / (double)N : NAN;
     row.resid = with_resid ? std::sqrt(h[2]) : NAN;
     row.refresh = refreshed ? 1 : 0;
+    {  // modeled_ms (trainer.cpp:137-148): ledger floats x 8 B over the modeled bandwidth + GS flops
+      const double world = (double)ctx->world;
+      const double bw = cfg.model_bandwidth_gbps > 0 ? cfg.model_bandwidth_gbps : 50.0;
+      const double gf = cfg.model_gflops > 0 ? cfg.model_gflops : 10.0;
+      row.wallclock = h[3] * 8.0 / (bw * 1.25e5 * world) + (double)gs_flops / (gf * 1e6 * world);
+    }
     metrics.push_back(row);
     check_opt_flags(&opt);
   }
@@ -399,6 +415,10 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   if (t->rows)
     DHO2G_CUDA(cudaMemcpyAsync(t->w_sh.p, t->w_a_shard, t->rows * sizeof(float), cudaMemcpyDeviceToDevice, st));  // make_admm_state
   opt_alloc(&t->opt, ctx, cfg->base, t->rows);
+  // SlotMeter names of trainer.cpp:70-71 (w_a replicated; moments row-sharded)
+  ctx->meter("w", (int64_t)n);
+  ctx->meter("moments", (int64_t)(t->rows * (cfg->base.kind == 0 ? 0 : cfg->base.kind == 1 ? 1 : 2)));
+  if (ctx->world > 1) ctx->meter("h_full", (int64_t)n);
   // Steady-state sizes for everything a refresh touches (MLP batch buffers for the larger of the step,
   // curvature and evaluation batches; both GEMM lanes' workspaces; the Lanczos state), so the refresh
   // graph captured right after the first, eager refresh stays valid through the gradient steps.
@@ -453,6 +473,14 @@ void trainer_params(dho2g_trainer* tr, double* w) {
   for (size_t i = 0; i < tr->n; ++i) w[i] = f[i];
 }
 size_t trainer_rows(dho2g_trainer* tr) { return tr->metrics.size(); }
+void trainer_metrics_ex(dho2g_trainer* tr, size_t max_rows, int64_t* outer, int64_t* inner, double* wallclock) {
+  for (size_t i = 0; i < tr->metrics.size() && i < max_rows; ++i) {
+    const auto& m = tr->metrics[i];
+    if (outer) outer[i] = m.outer;
+    if (inner) inner[i] = m.inner;
+    if (wallclock) wallclock[i] = m.wallclock;
+  }
+}
 void trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* acc, double* resid, int64_t* epoch,
                      int* refresh) {
   for (size_t i = 0; i < tr->metrics.size() && i < max_rows; ++i) {
@@ -475,6 +503,7 @@ double trainer_last_loss(dho2g_trainer* tr) {
 bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v) {
   if (key == "refreshes") *v = (double)tr->refreshes;
   else if (key == "safeguard_passes") *v = (double)tr->safeguards;
+  else if (key == "gs_flops") *v = (double)tr->gs_flops;
   else if (key == "steps") *v = (double)tr->steps;
   else if (key == "refresh_ms_last") *v = tr->refresh_ms_last;
   else if (key == "refresh_ms_total") *v = tr->refresh_ms_total;

@@ -540,7 +540,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
                                                                                          o->ticket.p);
     DHO2G_LAUNCH();
     ctx->kt_end(k1, "upd_p1", rb * (R + 1 + (a.pi ? 1 : 0)));
-    if (world > 1) ctx->allgather_f64(o->rank1.p, o->all1.p, R);
+    if (world > 1) ctx->allgather_f64(o->rank1.p, o->all1.p, R, "all_reduce");
   }
   ++o->t;
   const BaseHyper hp = make_hyper(o->cfg, o->t);
@@ -578,7 +578,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   DHO2G_LAUNCH();
   ctx->kt_end(k2, "upd_p2", rb * (R + 2 + (a.pi ? 1 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
                                   (o->cfg.kind == 3 ? 1 : 0)));
-  if (R > 0 && world > 1) ctx->allgather_f64(o->rank2.p, o->all2.p, R);
+  if (R > 0 && world > 1) ctx->allgather_f64(o->rank2.p, o->all2.p, R, "all_reduce");
   const int g3 = one_wave_grid(upd_p3_kernel, kT, (size_t)2 * R1 * sizeof(double), ctx->sm_count, cdiv(cdiv(rows, 4), kT));
   const int k3 = ctx->kt_begin();
   upd_p3_kernel<<<g3, kT, (size_t)2 * R1 * sizeof(double), st>>>(V, ldv, R, rows, o->s.p, all1, all2, world,
