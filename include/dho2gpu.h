@@ -233,6 +233,9 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
 /* Two-segment form C = A0 B0^T + A1 B1^T (A0: M x K0, A1: M x K1, B0: N x K0, B1: N x K1; K1 = 0: one
  * segment) with each operand stored K-major (a_mn / b_mn = 0) or MN-major (1), the layouts the MLP's
  * concatenated contractions use. */
+/* ---- test hook: each collective wrapper through a 1-rank NCCL communicator (plumbing check on one GPU).
+ * The context must have no communicator; *max_err = worst element error (0 expected). */
+int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err);
 int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const float* A0, const float* A1,
                         const float* B0, const float* B1, float* C, int backend, int a_mn, int b_mn);
 

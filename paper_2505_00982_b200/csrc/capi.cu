@@ -1079,3 +1079,60 @@ int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const floa
 }
 
 }  // extern "C"
+
+// Test hook: every collective wrapper through a 1-rank NCCL communicator on this GPU (the NCCL
+// plumbing — run-time binding, communicator init, datatypes, counts, stream order, ledger rows —
+// exercised on a one-GPU box). Returns the worst element error in *max_err (exact copies: 0).
+int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (ctx->world != 1 || ctx->comm) fail(DHO2G_ARGUMENT, "test_collectives: needs a context without a communicator");
+    ncclUniqueId id;
+    DHO2G_NCCLCHK(dho2g::nccl().GetUniqueId(&id));
+    DHO2G_NCCLCHK(dho2g::nccl().CommInitRank(&ctx->comm, 1, id, 0));
+    ctx->nccl_force = true;
+    double err = 0.0;
+    try {
+      cudaStream_t st = ctx->stream;
+      const size_t n = 4099;
+      std::vector<float> hf(n);
+      std::vector<double> hd(n);
+      for (size_t i = 0; i < n; ++i) {
+        hf[i] = (float)(i % 97) - 48.5f;
+        hd[i] = 1.0 / (double)(i + 1);
+      }
+      DevBuf<float> a(n), b(n);
+      DevBuf<double> c(n), e(n);
+      DHO2G_CUDA(cudaMemcpyAsync(a.p, hf.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+      DHO2G_CUDA(cudaMemcpyAsync(c.p, hd.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+      std::vector<float> of(n);
+      std::vector<double> od(n);
+      ctx->allgather_f32(a.p, b.p, n);
+      DHO2G_CUDA(cudaMemcpyAsync(of.data(), b.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < n; ++i) err = std::max(err, (double)std::fabs(of[i] - hf[i]));
+      DHO2G_CUDA(cudaMemsetAsync(b.p, 0, n * sizeof(float), st));
+      ctx->reduce_scatter_f32(a.p, b.p, n);
+      DHO2G_CUDA(cudaMemcpyAsync(of.data(), b.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < n; ++i) err = std::max(err, (double)std::fabs(of[i] - hf[i]));
+      ctx->allgather_f64(c.p, e.p, n, "all_reduce");
+      ctx->allreduce_sum_f64_ordered(c.p, n);
+      DHO2G_CUDA(cudaMemcpyAsync(od.data(), c.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < n; ++i) err = std::max(err, std::fabs(od[i] - hd[i]));
+      DHO2G_CUDA(cudaMemcpyAsync(od.data(), e.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+      for (size_t i = 0; i < n; ++i) err = std::max(err, std::fabs(od[i] - hd[i]));
+    } catch (...) {
+      ctx->nccl_force = false;
+      dho2g::nccl().CommDestroy(ctx->comm);
+      ctx->comm = nullptr;
+      throw;
+    }
+    ctx->nccl_force = false;
+    DHO2G_NCCLCHK(dho2g::nccl().CommDestroy(ctx->comm));
+    ctx->comm = nullptr;
+    *max_err = err;
+  });
+}

@@ -252,7 +252,7 @@ void dho2g_ctx::kt_flush() {
 }
 
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
-  if (world == 1) {
+  if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     return;
   }
@@ -265,7 +265,7 @@ void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, co
 }
 
 void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, const char* op) {
-  if (world == 1) {
+  if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
@@ -277,7 +277,7 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, cons
 }
 
 void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count) {
-  if (world == 1) {
+  if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
@@ -299,7 +299,7 @@ __global__ void ordered_sum_kernel(const double* __restrict__ all, double* __res
 }  // namespace
 
 void dho2g_ctx::allreduce_sum_f64_ordered(double* inout, size_t count) {
-  if (world == 1) return;
+  if (world == 1 && !nccl_force) return;
   gather_f64.ensure(count * world);
   allgather_f64(inout, gather_f64.p, count, "all_reduce");
   ordered_sum_kernel<<<(unsigned)std::min<size_t>(dho2g::cdiv(count, 256), 1024), 256, 0, stream>>>(

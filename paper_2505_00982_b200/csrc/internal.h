@@ -61,6 +61,7 @@ struct dho2g_ctx {
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
   void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled
   std::map<std::string, double> stats;
   // Per-kernel device timers (CUDA events on this stream), enabled by option "ktimers".

@@ -433,3 +433,18 @@ def test_ritz_tensor_core_matches_cuda_core(ctx, port, n, m, k, l):
     G = V0.T @ V1  # ||V1 V1^T - V0 V0^T||_F^2 = tr(V0^T V0)^2-ish terms, evaluated without n x n matrices
     proj2 = np.sum((V0.T @ V0) ** 2) + np.sum((V1.T @ V1) ** 2) - 2 * np.sum(G ** 2)
     assert np.sqrt(max(proj2, 0.0)) <= 1e-5
+
+
+def test_nccl_collectives_one_rank(ctx):
+    """The NCCL path of every collective wrapper (run-time libnccl binding, 1-rank communicator,
+    datatypes, counts, stream order) and the ledger rows it records."""
+    import ctypes as C
+    from paper_2505_00982_b200._lib import lib
+    ctx.reset_accounting()
+    err = C.c_double(-1.0)
+    d.check(lib.dho2g_test_collectives(ctx.h, C.byref(err)))
+    assert err.value == 0.0
+    rows = ctx.ledger()
+    assert [r[1] for r in rows] == ["all_gather", "reduce_scatter", "all_reduce", "all_reduce"]
+    assert all(r[4] == 0 and r[5] == 0 for r in rows)  # one rank: no traffic
+    ctx.reset_accounting()
