@@ -122,7 +122,7 @@ int dho2g_ctx_destroy(dho2g_ctx* ctx) {
       cudaStreamDestroy(ctx->stream2);
     }
     for (cudaEvent_t ev : ctx->lane_events) cudaEventDestroy(ev);
-    if (ctx->comm) dho2g::nccl().CommDestroy(ctx->comm);
+    if (ctx->comm) dho2g::nccl().CommAbort(ctx->comm);  // non-blocking communicator: abort frees at once
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -139,6 +139,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
+    else if (k == "nccl_timeout_s") ctx->nccl_timeout_s = value;
     else if (k == "lanczos_recurrence") {
       ctx->lanczos_recurrence = (int)value;
       ++g_graph_gen;  // baked into captured refresh graphs
@@ -246,7 +247,12 @@ int dho2g_comm_init(dho2g_ctx* ctx, const void* nccl_id_128, int rank, int world
     if (world == 1) return;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id_128, sizeof(id));
-    DHO2G_NCCLCHK(dho2g::nccl().CommInitRank(&ctx->comm, world, id, rank));
+    // non-blocking init + polling: a rank that never joins is a DeadlockError after nccl_timeout_s
+    // (test_collectives.cpp:245-258), not a hang
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    dho2g::nccl_call(ctx, dho2g::nccl().CommInitRankConfig(&ctx->comm, world, id, rank, &cfg), "comm_init");
+    dho2g::nccl_settle(ctx, "comm_init");
   });
 }
 

@@ -4,7 +4,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <numeric>
+#include <thread>
 
 #include "internal.h"
 
@@ -97,6 +99,9 @@ const NcclApi& nccl() {
     a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
     a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.CommInitRankConfig = reinterpret_cast<decltype(a.CommInitRankConfig)>(sym("ncclCommInitRankConfig"));
+    a.CommGetAsyncError = reinterpret_cast<decltype(a.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+    a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(sym("ncclCommAbort"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
     a.ReduceScatter = reinterpret_cast<decltype(a.ReduceScatter)>(sym("ncclReduceScatter"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
@@ -200,7 +205,65 @@ int tridiag_eig_host(size_t n, const double* diag, const double* off, double* va
 }  // namespace dho2g
 
 // ------------------------------------------------------------------------- context collectives
-void dho2g_ctx::sync() { DHO2G_CUDA(cudaStreamSynchronize(stream)); }
+void dho2g_ctx::sync() { dho2g::wait_stream(this, stream); }
+
+namespace dho2g {
+// Failure detection (the reference's DeadlockError, collectives.cpp:257-262): with a communicator,
+// host waits poll the stream and NCCL's asynchronous error state instead of blocking, so a rank that
+// never arrives (or a failed peer) surfaces as DEADLOCK / NCCL after ctx->nccl_timeout_s instead of
+// a hang; the communicator is aborted first (its kernels are released) and the context falls back to
+// a single rank.
+static void nccl_give_up(dho2g_ctx* ctx, int code, const std::string& msg) {
+  if (ctx->comm) nccl().CommAbort(ctx->comm);
+  ctx->comm = nullptr;
+  ctx->world = 1;
+  ctx->rank = 0;
+  fail(code, msg);
+}
+
+static void nccl_poll(dho2g_ctx* ctx, const char* what, std::chrono::steady_clock::time_point t0, int spin) {
+  ncclResult_t ae = ncclSuccess;
+  nccl().CommGetAsyncError(ctx->comm, &ae);
+  if (ae != ncclSuccess && ae != ncclInProgress)
+    nccl_give_up(ctx, DHO2G_NCCL, std::string(what) + ": " + nccl().GetErrorString(ae));
+  const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (el > ctx->nccl_timeout_s)
+    nccl_give_up(ctx, DHO2G_DEADLOCK, std::string("collective '") + what + "' timed out on rank " +
+                                          std::to_string(ctx->rank) + ": a rank is missing from the round");
+  if (spin > 2000) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  else std::this_thread::yield();
+}
+
+void nccl_settle(dho2g_ctx* ctx, const char* what) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    ncclResult_t ae = ncclSuccess;
+    nccl().CommGetAsyncError(ctx->comm, &ae);
+    if (ae == ncclSuccess) return;
+    nccl_poll(ctx, what, t0, spin);
+  }
+}
+
+void nccl_call(dho2g_ctx* ctx, ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return;
+  if (r == ncclInProgress) return nccl_settle(ctx, what);  // non-blocking communicator
+  nccl_give_up(ctx, DHO2G_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+void wait_stream(dho2g_ctx* ctx, cudaStream_t s) {
+  if (!ctx->comm) {
+    DHO2G_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) DHO2G_CUDA(e);
+    nccl_poll(ctx, "stream wait", t0, spin);
+  }
+}
+}  // namespace dho2g
 
 int dho2g_ctx::kt_begin() {
   if (!ktimers) return -1;
@@ -256,7 +319,7 @@ void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, co
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream));
+  dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 8 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;
@@ -269,7 +332,7 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, cons
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  DHO2G_NCCLCHK(dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream));
+  dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;
@@ -281,7 +344,8 @@ void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count)
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  DHO2G_NCCLCHK(dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream));
+  dho2g::nccl_call(this, dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream),
+                   "reduce_scatter");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;

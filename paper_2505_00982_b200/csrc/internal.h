@@ -62,6 +62,7 @@ struct dho2g_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
+  double nccl_timeout_s = 600.0;  // host waits with a communicator give up (DEADLOCK) after this long
   void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled
   std::map<std::string, double> stats;
   // Per-kernel device timers (CUDA events on this stream), enabled by option "ktimers".
@@ -331,6 +332,10 @@ struct dho2g_ese {
 
 namespace dho2g {
 void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed);
+// Host waits that notice a missing / failed rank (NCCL async errors, timeout) when a communicator exists.
+void wait_stream(dho2g_ctx* ctx, cudaStream_t s);
+void nccl_call(dho2g_ctx* ctx, ncclResult_t r, const char* what);
+void nccl_settle(dho2g_ctx* ctx, const char* what);
 // out[0] = scale * <a, b> over rows (single CTA, deterministic)
 void dot_dev(cudaStream_t st, const float* a, const float* b, size_t rows, double scale, double* out);
 void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m);

@@ -941,7 +941,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   }
   DHO2G_CUDA(cudaEventRecord(e1, st));
   DHO2G_CUDA(cudaMemcpyAsync(&lz->host, lz->st.p, sizeof(LzDev), cudaMemcpyDeviceToHost, st));
-  DHO2G_CUDA(cudaStreamSynchronize(st));
+  wait_stream(lz->ctx, st);
   float ms = 0.f;
   DHO2G_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   lz->ms = ms;
@@ -1035,7 +1035,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   DHO2G_CUDA(cudaMemcpyAsync(h_am.data(), amall.p, h_am.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
   DHO2G_CUDA(cudaMemcpyAsync(ese->eigvals.data(), ese->ev_dev.p, r * sizeof(double), cudaMemcpyDeviceToHost, st));
   DHO2G_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  DHO2G_CUDA(cudaStreamSynchronize(st));
+  wait_stream(lz->ctx, st);
   if (h_status) fail(DHO2G_NUMERIC, "tridiag_eig: QL iteration did not converge");
   ese->sign.assign(r, 1.f);
   for (int c = 0; c < r; ++c) {

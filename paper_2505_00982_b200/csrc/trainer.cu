@@ -215,7 +215,7 @@ struct dho2g_trainer {
     ctx->allreduce_sum_f64_ordered(acc2.p, 4);
     double h[4];
     DHO2G_CUDA(cudaMemcpyAsync(h, acc2.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+    wait_stream(ctx, ctx->stream);
     d2h_bytes += 4 * sizeof(double);
     MetricsRowH row;
     row.outer = outer;
@@ -327,7 +327,7 @@ void dho2g_trainer::residual_partial(double* out) {
   resid_kernel<<<nb, 256, 0, ctx->stream>>>(rows, w_a_shard, w_sh.p, part.p);
   sum_kernel<<<1, 32, 0, ctx->stream>>>(part.p, nb, out);
   DHO2G_LAUNCH();
-  DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+  wait_stream(ctx, ctx->stream);
 }
 
 namespace dho2g {
@@ -451,7 +451,7 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   t->idx_dev.alloc(t->idx_stride * dho2g_trainer::kSlots);
   t->acc2.alloc(4);
   t->stepacc.alloc(2);
-  DHO2G_CUDA(cudaStreamSynchronize(st));
+  wait_stream(ctx, st);
   return t.release();
 }
 
@@ -469,7 +469,7 @@ void trainer_run(dho2g_trainer* tr) {
 void trainer_params(dho2g_trainer* tr, double* w) {
   std::vector<float> f(tr->n);
   DHO2G_CUDA(cudaMemcpyAsync(f.data(), tr->w_a_full.p, tr->n * sizeof(float), cudaMemcpyDeviceToHost, tr->ctx->stream));
-  DHO2G_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  wait_stream(tr->ctx, tr->ctx->stream);
   for (size_t i = 0; i < tr->n; ++i) w[i] = f[i];
 }
 size_t trainer_rows(dho2g_trainer* tr) { return tr->metrics.size(); }
@@ -495,7 +495,7 @@ void trainer_metrics(dho2g_trainer* tr, size_t max_rows, double* loss, double* a
 double trainer_last_loss(dho2g_trainer* tr) {
   double h[2] = {0, 0};
   DHO2G_CUDA(cudaMemcpyAsync(h, tr->stepacc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, tr->ctx->stream));
-  DHO2G_CUDA(cudaStreamSynchronize(tr->ctx->stream));
+  wait_stream(tr->ctx, tr->ctx->stream);
   tr->d2h_bytes += 2 * sizeof(double);
   if (tr->quad) return h[0];
   return tr->B_local ? h[0] / (double)tr->B_local : 0.0;

@@ -591,7 +591,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
 void check_opt_flags(dho2g_opt* o) {
   int bad = 0;
   DHO2G_CUDA(cudaMemcpyAsync(&bad, o->bad.p, sizeof(int), cudaMemcpyDeviceToHost, o->ctx->stream));
-  DHO2G_CUDA(cudaStreamSynchronize(o->ctx->stream));
+  wait_stream(o->ctx, o->ctx->stream);
   if (bad) {
     DHO2G_CUDA(cudaMemsetAsync(o->bad.p, 0, sizeof(int), o->ctx->stream));
     fail(DHO2G_NUMERIC, "BaseOptimizer: non-finite gradient");

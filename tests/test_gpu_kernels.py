@@ -448,3 +448,29 @@ def test_nccl_collectives_one_rank(ctx):
     assert [r[1] for r in rows] == ["all_gather", "reduce_scatter", "all_reduce", "all_reduce"]
     assert all(r[4] == 0 and r[5] == 0 for r in rows)  # one rank: no traffic
     ctx.reset_accounting()
+
+
+def test_missing_rank_is_deadlock_error():
+    """test_collectives.cpp:245-258 on the device path: a rank that never joins surfaces as
+    DeadlockError after the timeout (non-blocking NCCL init + polling + abort), not a hang. Run in a
+    child process so a misbehaving NCCL teardown cannot take the test session with it."""
+    import subprocess
+    import sys
+    code = (
+        "import time, paper_2505_00982_b200 as d\n"
+        "c = d.Context(0)\n"
+        "c.set_option('nccl_timeout_s', 3)\n"
+        "t0 = time.time()\n"
+        "try:\n"
+        "    c.comm_init(d.Context.nccl_unique_id(), 0, 2)\n"
+        "    print('NO ERROR')\n"
+        "except d.DeadlockError as e:\n"
+        "    print('DEADLOCK', round(time.time() - t0, 1), c.world, e)\n"
+    )
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=180)
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("DEADLOCK")]
+    assert line, out.stdout + out.stderr
+    secs, world = line[0].split()[1:3]
+    assert 2.5 <= float(secs) < 60 and world == "1"
+    assert "timed out on rank 0" in out.stdout
