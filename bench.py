@@ -210,6 +210,9 @@ def run_ours(args, rank, world, dist):
     c = CONFIGS[args.config]
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ctx = d.Context(local)
+    for kv in filter(None, os.environ.get("DHO2G_OPTIONS", "").split(",")):  # A/B hook: key=value,...
+        key, val = kv.split("=")
+        ctx.set_option(key.strip(), float(val))
     if world > 1:
         nid = [d.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)

@@ -139,6 +139,10 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
+    else if (k == "gemm_pdl") {
+      ctx->gemm_pdl = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
     else if (k == "nccl_timeout_s") ctx->nccl_timeout_s = value;
     else if (k == "lanczos_recurrence") {
       ctx->lanczos_recurrence = (int)value;

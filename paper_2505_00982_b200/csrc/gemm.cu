@@ -895,6 +895,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   cluster_sync();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above (barriers, tensor-map prefetch, TMEM allocation)
+  // may overlap the previous kernel's tail; no global memory is touched before the previous grid has
+  // completed and flushed (a no-op when launched without the attribute).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs): this CTA's halves of A and B into its ring
@@ -916,6 +920,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         load_op<BMN, true, NT / 128, BKT>(st + 3 * OP_BYTES, &mBl, ob, nb, kb, wk.kseg, &full[s]);
       }
     }
+    // all operand loads issued: the next kernel in the stream may start its prologue on freed SMs
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   } else if (warp == 1 && lane == 0 && rank == 0) {
     // ---------------- MMA issuer (leader CTA only)
     uint32_t it = 0, uc = 0;
@@ -1077,8 +1083,18 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
     ctx->gemm_epoch = epoch = 1;
   }
-  gemm3_tc2_kernel<AMN, BMN, MODE><<<2 * wk.workers, 384, SMEM, ctx->stream>>>(
-      maps[0], maps[1], maps[2], maps[3], wk, oa, ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * wk.workers);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = ctx->gemm_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  DHO2G_CUDA(cudaLaunchKernelEx(&cfg, gemm3_tc2_kernel<AMN, BMN, MODE>, maps[0], maps[1], maps[2], maps[3], wk, oa,
+                                ob, e, ctx->gemm_ws.p, ctx->gemm_flags.p, epoch * 16u + 15u));
   DHO2G_LAUNCH();
   return wk.workers;
 }

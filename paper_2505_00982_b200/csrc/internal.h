@@ -46,6 +46,8 @@ struct dho2g_ctx {
   int gemm_min_kb = 4;   // pair kernel: minimum k-blocks per CTA pair (caps the worker count of small GEMMs)
   int gemm_worker_cap = 0;  // pair kernel: at most this many CTA pairs (0: all co-resident pairs)
   int lanczos_recurrence = 1;  // Lanczos: recurrence-first projection (1) or the reference's plain CGS (0)
+  int gemm_pdl = 1;      // CTA-pair GEMMs launched with programmatic dependent launch (prologue overlaps the
+                         // previous kernel's tail)
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
