@@ -632,6 +632,9 @@ int dho2g_op_quadratic(dho2g_ctx* ctx, const double* spectrum, size_t n, uint64_
     op->n = n;
     upload(op->mat, spectrum, n, ctx->stream);
     if (rotation_seed) {
+      // the rotation is dense (n^2 fp64 on the host, O(n^3) to build, 8 n^2 bytes in HBM): desk-scale
+      // problems only, like the reference's constructor (oracle.cpp:246)
+      if (n > 32768) fail(DHO2G_ARGUMENT, "quadratic oracle: a rotated spectrum is limited to n <= 32768");
       std::vector<double> Q(n * n);
       if (!quadratic_rotation(n, rotation_seed, Q.data())) fail(DHO2G_NUMERIC, "quadratic oracle: degenerate rotation draw");
       size_t b, e;
