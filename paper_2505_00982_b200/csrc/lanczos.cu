@@ -448,14 +448,18 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
   if (tid == 0) s_fail = 0;
   __syncthreads();
   const double eps = 2.220446049250313e-16;
+  if (tid == 0) s_mm = n - 1;
+  __syncthreads();
   for (int l = 0; l < n && n > 1; ++l) {
     int iter = 0;
     for (;;) {
+      // mm = first index >= l with a negligible off-diagonal (n-1 if none): every thread tests its
+      // indices, the smallest wins (the reference scans serially, linalg.cpp:160-164; same result)
+      for (int q = l + tid; q + 1 < n; q += blockDim.x)
+        if (fabs(e[q]) <= eps * (fabs(d[q]) + fabs(d[q + 1]))) atomicMin(&s_mm, q);
+      __syncthreads();
       if (tid == 0) {
-        int mm;
-        for (mm = l; mm + 1 < n; ++mm)
-          if (fabs(e[mm]) <= eps * (fabs(d[mm]) + fabs(d[mm + 1]))) break;
-        s_mm = mm;
+        const int mm = s_mm;
         s_cnt = 0;
         if (mm != l) {
           if (iter++ == 60) {
@@ -467,30 +471,39 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
             double s = 1.0, c = 1.0, p = 0.0;
             bool under = false;
             int cnt = 0;
+            // the serial chain is this kernel's latency: d[ii+1] is carried in a register and the next
+            // e / d entries (untouched by this step) are read one step ahead
+            double dk = d[mm], ek = e[mm - 1], dn = d[mm - 1];
             for (int ii = mm - 1; ii >= l; --ii) {
-              const double f = s * e[ii];
-              const double b = c * e[ii];
-              // sqrt(f^2 + g^2) instead of hypot: the entries of a Lanczos tridiagonal are O(||H||), far
-              // from fp64 over/underflow, and the serial chain is this kernel's latency
-              r = sqrt(fma(f, f, g * g));
-              e[ii + 1] = r;
-              if (r == 0.0) {
-                d[ii + 1] -= p;
+              const double en = ii > l ? e[ii - 1] : 0.0, dnn = ii > l ? d[ii - 1] : 0.0;
+              const double f = s * ek;
+              const double b = c * ek;
+              // 1/sqrt(f^2 + g^2) instead of hypot and a division: the entries of a Lanczos tridiagonal
+              // are O(||H||), far from fp64 over/underflow
+              const double h2 = fma(f, f, g * g);
+              if (h2 == 0.0) {
+                e[ii + 1] = 0.0;
+                d[ii + 1] = dk - p;
                 e[mm] = 0.0;
                 under = true;
                 break;
               }
-              const double ir = 1.0 / r;
+              const double ir = rsqrt(h2);
+              r = h2 * ir;
+              e[ii + 1] = r;
               s = f * ir;
               c = g * ir;
-              g = d[ii + 1] - p;
-              r = (d[ii] - g) * s + 2.0 * c * b;
+              g = dk - p;
+              r = (dn - g) * s + 2.0 * c * b;
               p = s * r;
               d[ii + 1] = g + p;
               g = c * r - b;
               cs[cnt] = c;
               sn[cnt] = s;
               ++cnt;
+              dk = dn;
+              dn = dnn;
+              ek = en;
             }
             s_cnt = cnt;
             if (!under) {
@@ -503,20 +516,29 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
       }
       __syncthreads();
       const int mm = s_mm, cnt = s_cnt, failed = s_fail;
-      __syncthreads();  // everyone has read the sweep descriptor before thread 0 rewrites it
+      __syncthreads();  // everyone has read the sweep descriptor before it is rewritten
+      if (tid == 0) s_mm = n - 1;  // reset for the next scan
+      __syncthreads();
       if (failed) {
         if (tid == 0) *status = 1;
         return;
       }
       if (mm == l) break;
       for (int k = tid; k < n; k += blockDim.x) {
-        for (int q = 0; q < cnt; ++q) {
-          const int ii = mm - 1 - q;
-          const double c = cs[q], s = sn[q];
-          const double f = Z[(size_t)(ii + 1) * n + k];
-          const double z0 = Z[(size_t)ii * n + k];
-          Z[(size_t)(ii + 1) * n + k] = s * z0 + c * f;
-          Z[(size_t)ii * n + k] = c * z0 - s * f;
+        // rotation q turns rows (ii, ii+1), ii = mm-1-q: row ii+1 is final after it and row ii is carried
+        // (in a register) into rotation q+1, so only the untouched row ii-1 is loaded per step
+        if (cnt > 0) {
+          double f = Z[(size_t)mm * n + k];
+          double z0 = Z[(size_t)(mm - 1) * n + k];
+          for (int q = 0; q < cnt; ++q) {
+            const int ii = mm - 1 - q;
+            const double zn = q + 1 < cnt ? Z[(size_t)(ii - 1) * n + k] : 0.0;
+            const double c = cs[q], s = sn[q];
+            Z[(size_t)(ii + 1) * n + k] = s * z0 + c * f;
+            f = c * z0 - s * f;
+            z0 = zn;
+          }
+          Z[(size_t)(mm - cnt) * n + k] = f;
         }
       }
       __syncthreads();
