@@ -61,6 +61,8 @@ struct dho2g_ctx {
   int gs_sm_cap = 0;     // Gram-Schmidt grids sized for at most this many SMs (0: all; experiments)
   int ritz_tc = 1;        // Ritz vectors on the tensor cores when supported (0: CUDA-core kernel)
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
+  int upd_p2_variant = 5; // staged pass 2: 5 row-dot (R <= 32, else 0), 0 256-row x2 stages x2 CTAs/SM +
+                          // column-dot phase, 1 128x2x4, 2 128x3x3, 3 128x4x2, 4 512x2x1
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
 // both the correction g - V c and the dots V^T s (the register-staged kernel re-reads V for the dots
 // and loses the L2 race at large R x CH). Dot partials stay in per-lane fp64 registers until the end.
 constexpr int kP2MaxR = 48;
-constexpr int kP2CH = 256;     // rows per stage (one per thread)
+
 constexpr int kP2Streams = 5;  // g, pi, m, v, w
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -251,8 +251,11 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
 }
 
 // Two CTAs per SM, each double-buffered: ~4 stages of (R + 5) x 1 KB in flight per SM.
-template <int CH, int NS>
-__global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant__ CUtensorMap mapV, int R, size_t rows,
+// ROWDOT (R <= 32): each thread also accumulates its rows' contributions to V_hat^T s in 32 fp64
+// registers while the row is at hand (no second pass over the stage, one barrier per chunk); the block
+// reduction happens once at the end.
+template <int CH, int NS, int MINB, bool ROWDOT = false>
+__global__ void __launch_bounds__(kT, MINB) upd_p2_tma_kernel(const __grid_constant__ CUtensorMap mapV, int R, size_t rows,
                                                           const float* __restrict__ g, const float* __restrict__ pi,
                                                           const float* __restrict__ w,
                                                           const double* __restrict__ all1, int world, BaseHyper hp,
@@ -282,12 +285,21 @@ __global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the stage
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[i % NS])), "r"(bytes)
                  : "memory");
-    // all R columns of the chunk in one 2D tensor copy (box CH rows x R columns, column-major in smem)
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_addr(st)),
-        "l"(reinterpret_cast<uint64_t>(&mapV)), "r"((int)r0), "r"(0), "r"(smem_addr(&bar[i % NS]))
-        : "memory");
+    // all R columns of the chunk in one tensor copy (column-major in smem): a 2D box CH rows x R columns,
+    // or for CH > 256 (the box-dimension limit) a 3D box 256 x CH/256 x R over rows viewed as 256-row blocks
+    if constexpr (CH <= 256) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+              "r"(smem_addr(st)),
+          "l"(reinterpret_cast<uint64_t>(&mapV)), "r"((int)r0), "r"(0), "r"(smem_addr(&bar[i % NS]))
+          : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];" ::"r"(smem_addr(st)),
+          "l"(reinterpret_cast<uint64_t>(&mapV)), "r"(0), "r"((int)(r0 / 256)), "r"(0), "r"(smem_addr(&bar[i % NS]))
+          : "memory");
+    }
     if (full) {
       float* ss = st + (size_t)R * CH;
       bulk_g2s(ss, g + r0, CH * 4u, &bar[i % NS]);
@@ -313,14 +325,17 @@ __global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant
   double lacc[kP2MaxR / kW];
 #pragma unroll
   for (int q = 0; q < kP2MaxR / kW; ++q) lacc[q] = 0.0;
+  constexpr int kRowR = ROWDOT ? 32 : 1;
+  double pacc[kRowR];
+#pragma unroll
+  for (int q = 0; q < kRowR; ++q) pacc[q] = 0.0;
   int local_bad = 0;
   for (size_t i = 0; blockIdx.x + i * gridDim.x < nch; ++i) {
     const size_t r0 = (blockIdx.x + i * gridDim.x) * CH;
     const bool full = r0 + CH <= rows;
     float* st = stg0 + (i % NS) * stage_floats;
     bar_wait(&bar[i % NS], (uint32_t)((i / NS) & 1));
-    if (threadIdx.x < CH) {  // phase A: row r0 + threadIdx.x
-      const int t = threadIdx.x;
+    for (int t = threadIdx.x; t < CH; t += kT) {  // phase A: rows r0 + t
       const size_t r = r0 + t;
       const bool in = r < rows;
       const float* ss = st + (size_t)R * CH;
@@ -348,12 +363,18 @@ __global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant
         if (need_v) v[r] = vm;
         s_out[r] = sv;
       }
-      xs[t] = sv;
+      if constexpr (ROWDOT) {
+#pragma unroll
+        for (int q = 0; q < kRowR; ++q)
+          if (q < R) pacc[q] += (double)st[(size_t)q * CH + t] * (double)sv;
+      } else {
+        xs[t] = sv;
+      }
     }
     __syncthreads();
     // phase B: column j = warp + kW q, lanes stride the chunk with float4
 #pragma unroll
-    for (int q = 0; q < kP2MaxR / kW; ++q) {
+    for (int q = 0; q < (ROWDOT ? 0 : kP2MaxR / kW); ++q) {
       const int j = warp + kW * q;
       if (j < R) {
         const float* col = st + (size_t)j * CH;
@@ -367,18 +388,26 @@ __global__ void __launch_bounds__(kT, 2) upd_p2_tma_kernel(const __grid_constant
         lacc[q] += (double)f;
       }
     }
-    __syncthreads();  // stage (i % NS) and xs free
+    if constexpr (!ROWDOT) __syncthreads();  // stage (i % NS) and xs free (ROWDOT: the barrier above)
     if (threadIdx.x == 0) issue(i + NS);
   }
   if (local_bad) atomicOr(bad, 1);
+  if constexpr (ROWDOT) {
 #pragma unroll
-  for (int q = 0; q < kP2MaxR / kW; ++q) {
-    const int j = warp + kW * q;
-    const double t = warp_sum(lacc[q]);
-    if (j < R && lane == 0) acc[warp * R + j] = t;
+    for (int q = 0; q < kRowR; ++q) {
+      const double t = warp_sum(pacc[q]);
+      if (q < R && lane == 0) acc[warp * R + q] = t;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kP2MaxR / kW; ++q) {
+      const int j = warp + kW * q;
+      const double t = warp_sum(lacc[q]);
+      if (j < R && lane == 0) acc[warp * R + j] = t;
+    }
+    for (int e = threadIdx.x; e < kW * R; e += kT)  // warps without column j contribute 0
+      if (e / R != (e % R) % kW) acc[e] = 0.0;
   }
-  for (int e = threadIdx.x; e < kW * R; e += kT)  // warps without column j contribute 0
-    if (e / R != (e % R) % kW) acc[e] = 0.0;
   finish_partials(acc, R, part, rankp, ticket);
 }
 
@@ -524,7 +553,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const int gp = std::min(one_wave_grid(upd_p1_kernel, kT, smem_p1, ctx->sm_count, cdiv(rows, kCh)),
                           one_wave_grid(upd_p2_kernel, kT, smem_p2, ctx->sm_count, cdiv(rows, kCh2)));
   const int R1 = std::max(R, 1);
-  o->part.ensure((size_t)gp * R1 + 8);
+  o->part.ensure((size_t)4 * gp * R1 + 8);  // the staged pass 2 may run up to 4 gp CTAs
   o->rank1.ensure(R1);
   o->rank2.ensure(R1);
   o->all1.ensure((size_t)R1 * world);
@@ -546,27 +575,49 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const BaseHyper hp = make_hyper(o->cfg, o->t);
   const int k2 = ctx->kt_begin();
   if (R > 0 && R <= kP2MaxR && ctx->upd_p2_staged) {
-    // 256-row stages, double-buffered, two CTAs per SM (measured best of 128/256 rows x 2-4 stages x 1-2 CTAs)
-    const int CH = kP2CH;
-    const int NS = 2;
+    // stage shape / depth / CTAs per SM (option upd_p2_variant). Default 5: 256-row stages, double-buffered,
+    // two CTAs per SM, V_hat^T s accumulated per row in registers (C4, r = 32: 93 % of HBM peak vs 78 % for
+    // the separate column-dot phase of variant 0)
+    int var = (ctx->upd_p2_variant == 4 && ldv % 256) ? 0 : ctx->upd_p2_variant;  // 3D view needs 256 | ldv
+    if (var == 5 && R > 32) var = 0;                                                  // row dots: R <= 32
+    const int CH = (var == 0 || var == 5) ? 256 : (var == 4 ? 512 : 128);
+    const int NS = var == 2 ? 3 : (var == 3 ? 4 : 2);
     const size_t smem_t = ((size_t)NS * (R + kP2Streams) * CH + CH) * sizeof(float) +
                           (size_t)(R + kW * R) * sizeof(double) + NS * sizeof(uint64_t) + 128;
-    auto kern = upd_p2_tma_kernel<kP2CH, 2>;
+    auto kern = var == 1 ? upd_p2_tma_kernel<128, 2, 4>
+              : var == 2 ? upd_p2_tma_kernel<128, 3, 3>
+              : var == 3 ? upd_p2_tma_kernel<128, 4, 2>
+              : var == 4 ? upd_p2_tma_kernel<512, 2, 1>
+              : var == 5 ? upd_p2_tma_kernel<256, 2, 2, true>
+                         : upd_p2_tma_kernel<256, 2, 2>;
     if (smem_t > 227 * 1024) fail(DHO2G_ARGUMENT, "split_update: staged pass 2 does not fit shared memory");
     DHO2G_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
-    const int gt = std::min(gp, one_wave_grid(kern, kT, smem_t, ctx->sm_count, cdiv(rows, CH)));
+    const int gt = std::min(gp * 4, one_wave_grid(kern, kT, smem_t, ctx->sm_count, cdiv(rows, CH)));
     // V_hat as a 2D fp32 tensor: inner = rows (stride 1), outer = R columns (stride ldv); box CH x R
     CUtensorMap mapV;
     {
-      cuuint64_t dims[2] = {(cuuint64_t)ldv, (cuuint64_t)R};
-      cuuint64_t strides[1] = {(cuuint64_t)ldv * sizeof(float)};
-      cuuint32_t box[2] = {(cuuint32_t)CH, (cuuint32_t)R};
-      cuuint32_t estr[2] = {1, 1};
       auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ctx->encode_fn);
-      if (!enc || enc(&mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(V), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        fail(DHO2G_CUDA, "split_update: cuTensorMapEncodeTiled failed for V_hat");
+      CUresult rc = CUDA_ERROR_INVALID_VALUE;
+      if (CH <= 256) {
+        cuuint64_t dims[2] = {(cuuint64_t)ldv, (cuuint64_t)R};
+        cuuint64_t strides[1] = {(cuuint64_t)ldv * sizeof(float)};
+        cuuint32_t box[2] = {(cuuint32_t)CH, (cuuint32_t)R};
+        cuuint32_t estr[2] = {1, 1};
+        if (enc)
+          rc = enc(&mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(V), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      } else {  // rows as (256, ldv / 256) blocks (ldv is a multiple of the 2048-row GS chunk)
+        cuuint64_t dims[3] = {256, (cuuint64_t)(ldv / 256), (cuuint64_t)R};
+        cuuint64_t strides[2] = {256 * sizeof(float), (cuuint64_t)ldv * sizeof(float)};
+        cuuint32_t box[3] = {256, (cuuint32_t)(CH / 256), (cuuint32_t)R};
+        cuuint32_t estr[3] = {1, 1, 1};
+        if (enc)
+          rc = enc(&mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(V), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      }
+      if (rc != CUDA_SUCCESS) fail(DHO2G_CUDA, "split_update: cuTensorMapEncodeTiled failed for V_hat");
     }
     kern<<<gt, kT, smem_t, st>>>(mapV, R, rows, a.g, a.pi, a.w_decay ? a.w_decay : a.w_a, all1, world, hp, o->m.p,
                                  o->v.p, o->s.p, o->part.p, o->rank2.p, o->ticket.p + 1, o->bad.p);

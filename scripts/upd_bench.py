@@ -23,8 +23,10 @@ def main():
     ese = d.EseResult.from_host(ctx, ev, V)
     del V
     g, pi, w = rng.standard_normal(n), rng.standard_normal(n), rng.standard_normal(n)
-    for staged in (1, 0, 1, 0):
+    variants = [(1, v) for v in (0, 1, 5)] + [(0, 0)] + [(1, v) for v in (0, 1, 5)]
+    for staged, var in variants:
         ctx.set_option("upd_p2_staged", staged)
+        ctx.set_option("upd_p2_variant", var)
         opt = d.BaseOptimizer(ctx, d.BaseConfig("adamw", lr=1e-3), n)
         d.admm_deltas(g, pi, ese, opt, w, 0.3, 0.05)  # warm-up
         ctx.set_option("ktimers_reset", 1)
@@ -34,7 +36,7 @@ def main():
         ctx.set_option("ktimers", 0)
         for k, (ms, cnt, work) in sorted(ctx.kernel_stats().items()):
             if k.startswith("upd_"):
-                print(f"staged={staged} {k} n={n} r={r} {ms / cnt * 1e3:9.1f} us  {work / (ms / 1e3) / 1e9:8.1f} GB/s")
+                print(f"staged={staged} var={var} {k} n={n} r={r} {ms / cnt * 1e3:9.1f} us  {work / (ms / 1e3) / 1e9:8.1f} GB/s")
     ctx.close()
 
 
