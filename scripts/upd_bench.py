@@ -1,6 +1,6 @@
 """Update-pass bandwidth (P1/P2/P3 of the fused FOSI/ADMM split update) at rank r, n rows.
 
-    python scripts/upd_bench.py [n] [r]
+    python scripts/upd_bench.py [n] [r] [staged variants, e.g. 0,5]
 Times both P2 variants (bulk-copy staged / register-staged) with the kernel timers."""
 import os
 import sys
@@ -23,7 +23,10 @@ def main():
     ese = d.EseResult.from_host(ctx, ev, V)
     del V
     g, pi, w = rng.standard_normal(n), rng.standard_normal(n), rng.standard_normal(n)
-    variants = [(1, v) for v in (0, 1, 5)] + [(0, 0)] + [(1, v) for v in (0, 1, 5)]
+    if len(sys.argv) > 3:  # explicit staged-variant list, e.g. "5" or "0,5"
+        variants = [(1, int(v)) for v in sys.argv[3].split(",")]
+    else:
+        variants = [(1, v) for v in (0, 1, 5)] + [(0, 0)] + [(1, v) for v in (0, 1, 5)]
     for staged, var in variants:
         ctx.set_option("upd_p2_staged", staged)
         ctx.set_option("upd_p2_variant", var)
