@@ -69,7 +69,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -78,17 +78,29 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([x.strip() for x in line.split(",")] + [time.time()])
+
+    def mark(self):
+        """Start of the timed region (the sampler itself is started earlier so that it is already
+        reporting when a short timed region begins)."""
+        self.t0 = time.time()
 
     def stop(self):
         if not self.proc:
             return None
+        t1 = time.time()
+        time.sleep(0.25)  # the sample covering the end of the region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        rows = [r for r in self.rows if len(r) >= 9]
+        rows = [r for r in self.rows if len(r) >= 10]
+        t0 = getattr(self, "t0", 0.0)
+        inside = [r for r in rows if t0 <= r[-1] <= t1 + 0.25]
+        if not inside and rows:  # region shorter than the sampling interval: the nearest sample
+            inside = [min(rows, key=lambda r: abs(r[-1] - t1))]
+        rows = inside
         if not rows:
             return None
         sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
@@ -239,6 +251,8 @@ def run_ours(args, rank, world, dist):
 
     # ---- device-resident timed run (value): K steps, no per-kernel instrumentation
     tr = d.Trainer(ctx, cfg, mlp, data, w0, workers=c["workers"])
+    sampler = ClockSampler(local)
+    sampler.start()
     tr.step(args.warmup)
     ctx.synchronize()
     rounds = int(tr.stat("rounds_per_epoch"))
@@ -246,8 +260,7 @@ def run_ours(args, rank, world, dist):
     launches0 = ctx.stat("launches")
     barrier()
     ctx.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler.mark()
     ctx.mark(0)
     for _ in range(args.steps):
         tr.step(1)
