@@ -317,8 +317,10 @@ def run_ours(args, rank, world, dist):
         e2e = {"value": args.steps / (ems / 1e3), "unit": "steps/s",
                "h2d_bytes_per_step": (tr.stat("h2d_bytes") - h0) / args.steps,
                "d2h_bytes_per_step": (tr.stat("d2h_bytes") - d0) / args.steps,
-               "note": "dataset pinned in host memory; each step's batch (and each refresh's curvature batch) is "
-                       "gathered over PCIe by the packing kernel; per-step loss read back"}
+               "note": "dataset pinned in host memory; each step's batch is gathered on a host thread into "
+                       "pinned staging and copied host->device by the copy engine during the preceding step "
+                       "(every step's inputs cross PCIe inside the timed region); each refresh's curvature "
+                       "batch is read over PCIe by the packing kernel; per-step loss read back"}
         tr.close()
 
     if rank != 0:

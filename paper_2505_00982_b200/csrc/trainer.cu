@@ -8,7 +8,11 @@
 // replicated eigensolve -> sharded Ritz vectors.
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
 
 #include "internal.h"
 
@@ -19,6 +23,33 @@ struct MetricsRowH {
   double loss = 0, acc = NAN, resid = NAN;
   double wallclock = 0;  // modeled clock (trainer.cpp:137-148)
   int refresh = 0;
+};
+
+// End-to-end mode (dataset in pinned host memory): the next step's batch is gathered on a host thread
+// into a pinned staging slot and copied to the device by the copy engine while the current step
+// computes, instead of being read over PCIe by the packing kernel on the critical path. Every step's
+// inputs still cross PCIe once, inside the step that precedes it.
+struct BatchPrefetch {
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool quit = false;
+  bool pending = false;  // a job is queued or running
+  // job
+  std::vector<int64_t> idx;
+  int slot = 0;
+  int64_t epoch = -1;
+  size_t round = 0;
+  // per slot: what it holds, pinned host staging, device copy, events
+  int64_t key_epoch[2] = {-1, -1};
+  size_t key_round[2] = {0, 0};
+  size_t rows[2] = {0, 0};
+  dho2g::HostBuf<float> hx[2], hy[2];
+  dho2g::DevBuf<float> dx[2], dy[2];
+  cudaEvent_t copied[2] = {}, consumed[2] = {};
+  cudaStream_t cs = nullptr;
+  std::exception_ptr err;
+  int next = 0;
 };
 
 struct dho2g_trainer {
@@ -70,9 +101,127 @@ struct dho2g_trainer {
   double h2d_bytes = 0, d2h_bytes = 0;
   std::vector<double> last_eigvals;
 
+  BatchPrefetch pf;
+
   ~dho2g_trainer() {
+    if (pf.th.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(pf.mu);
+        pf.quit = true;
+      }
+      pf.cv.notify_all();
+      pf.th.join();
+    }
+    for (int q = 0; q < 2; ++q) {
+      if (pf.copied[q]) cudaEventDestroy(pf.copied[q]);
+      if (pf.consumed[q]) cudaEventDestroy(pf.consumed[q]);
+    }
+    if (pf.cs) {
+      cudaStreamSynchronize(pf.cs);
+      cudaStreamDestroy(pf.cs);
+    }
     for (auto& e : idx_ev)
       if (e) cudaEventDestroy(e);
+  }
+
+  // this rank's sample indices of one step (trainer.cpp:94-98)
+  void step_indices(const std::vector<uint64_t>& pm, size_t round, std::vector<int64_t>& idx) const {
+    const size_t b = cfg.batch_size;
+    idx.clear();
+    idx.reserve((size_t)(c1 - c0) * b);
+    for (int c = c0; c < c1; ++c) {
+      size_t sb, se;
+      shard_range(N, C, c, &sb, &se);
+      const size_t len = se - sb;
+      for (size_t j = 0; j < b; ++j) idx.push_back((int64_t)pm[sb + (round * b + j) % len]);
+    }
+  }
+
+  void prefetch_worker() {
+    cudaSetDevice(ctx->device);
+    for (;;) {
+      std::unique_lock<std::mutex> lk(pf.mu);
+      pf.cv.wait(lk, [&] { return pf.quit || pf.pending; });
+      if (pf.quit) return;
+      const int q = pf.slot;
+      std::vector<int64_t> idx = pf.idx;
+      lk.unlock();
+      try {
+        DHO2G_CUDA(cudaEventSynchronize(pf.copied[q]));  // the slot's previous host->device copy is done
+        const size_t B = idx.size();
+        for (size_t j = 0; j < B; ++j) {
+          std::memcpy(pf.hx[q].p + j * D, Xh.p + (size_t)idx[j] * D, D * sizeof(float));
+          pf.hy[q].p[j] = yh.p[idx[j]];
+        }
+        DHO2G_CUDA(cudaStreamWaitEvent(pf.cs, pf.consumed[q], 0));  // the step that read the slot is done
+        DHO2G_CUDA(cudaMemcpyAsync(pf.dx[q].p, pf.hx[q].p, B * D * sizeof(float), cudaMemcpyHostToDevice, pf.cs));
+        DHO2G_CUDA(cudaMemcpyAsync(pf.dy[q].p, pf.hy[q].p, B * sizeof(float), cudaMemcpyHostToDevice, pf.cs));
+        DHO2G_CUDA(cudaEventRecord(pf.copied[q], pf.cs));
+      } catch (...) {
+        lk.lock();
+        pf.err = std::current_exception();
+        pf.pending = false;
+        pf.cv.notify_all();
+        continue;
+      }
+      lk.lock();
+      pf.key_epoch[q] = pf.epoch;
+      pf.key_round[q] = pf.round;
+      pf.rows[q] = idx.size();
+      pf.pending = false;
+      pf.cv.notify_all();
+    }
+  }
+
+  void prefetch_init() {
+    const size_t cap = (size_t)(c1 - c0) * cfg.batch_size;
+    for (int q = 0; q < 2; ++q) {
+      pf.hx[q].ensure(std::max<size_t>(cap * D, 1));
+      pf.hy[q].ensure(std::max<size_t>(cap, 1));
+      pf.dx[q].alloc(std::max<size_t>(cap * D, 1));
+      pf.dy[q].alloc(std::max<size_t>(cap, 1));
+      DHO2G_CUDA(cudaEventCreateWithFlags(&pf.copied[q], cudaEventDisableTiming));
+      DHO2G_CUDA(cudaEventCreateWithFlags(&pf.consumed[q], cudaEventDisableTiming));
+      DHO2G_CUDA(cudaEventRecord(pf.copied[q], ctx->stream));
+      DHO2G_CUDA(cudaEventRecord(pf.consumed[q], ctx->stream));
+    }
+    DHO2G_CUDA(cudaStreamCreateWithFlags(&pf.cs, cudaStreamNonBlocking));
+    pf.th = std::thread([this] { prefetch_worker(); });
+  }
+
+  // queue the gather + copy of the step that will run at (epoch, round)
+  void prefetch(int64_t epoch, size_t round) {
+    std::vector<uint64_t> pm;
+    const std::vector<uint64_t>* use = &perm;
+    if (epoch != perm_epoch) {
+      pm.resize(N);
+      dho2g_epoch_permutation(N, dataset_seed, (uint64_t)epoch, pm.data());
+      use = &pm;
+    }
+    std::vector<int64_t> idx;
+    step_indices(*use, round, idx);
+    std::unique_lock<std::mutex> lk(pf.mu);
+    pf.cv.wait(lk, [&] { return !pf.pending; });
+    pf.idx.swap(idx);
+    pf.slot = pf.next;
+    pf.next ^= 1;
+    pf.epoch = epoch;
+    pf.round = round;
+    pf.key_epoch[pf.slot] = -1;
+    pf.pending = true;
+    h2d_bytes += (double)pf.idx.size() * (D + 1) * sizeof(float);
+    lk.unlock();
+    pf.cv.notify_all();
+  }
+
+  // the staged slot holding (epoch, round), or -1
+  int prefetched(int64_t epoch, size_t round) {
+    std::unique_lock<std::mutex> lk(pf.mu);
+    pf.cv.wait(lk, [&] { return !pf.pending; });
+    if (pf.err) std::rethrow_exception(std::exchange(pf.err, nullptr));
+    for (int q = 0; q < 2; ++q)
+      if (pf.key_epoch[q] == epoch && pf.key_round[q] == round) return q;
+    return -1;
   }
 
   const int64_t* upload_indices(const std::vector<int64_t>& idx) {
@@ -103,13 +252,7 @@ struct dho2g_trainer {
   void mean_gradient(size_t round) {
     const size_t b = cfg.batch_size;
     std::vector<int64_t> idx;
-    idx.reserve((size_t)(c1 - c0) * b);
-    for (int c = c0; c < c1; ++c) {
-      size_t sb, se;
-      shard_range(N, C, c, &sb, &se);
-      const size_t len = se - sb;
-      for (size_t j = 0; j < b; ++j) idx.push_back((int64_t)perm[sb + (round * b + j) % len]);
-    }
+    step_indices(perm, round, idx);
     B_local = idx.size();
     const double scale = (1.0 / (double)b) * (1.0 / (double)C);
     const int ph = ctx->kt_begin();
@@ -121,11 +264,18 @@ struct dho2g_trainer {
       return;
     }
     if (B_local > 0) {
-      const int64_t* di = upload_indices(idx);
+      const int q = pf.th.joinable() ? prefetched(perm_epoch, round) : -1;
       mlp_load_weights(mlp, w_a_full.p);
-      mlp_grad_dev(mlp, w_a_full.p, Xptr, yptr, di, B_local, ncls, scale, g_full.p);
+      if (q >= 0 && pf.rows[q] == B_local) {  // batch staged on the device by the previous step
+        DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, pf.copied[q], 0));
+        mlp_grad_dev(mlp, w_a_full.p, pf.dx[q].p, pf.dy[q].p, nullptr, B_local, ncls, scale, g_full.p);
+        DHO2G_CUDA(cudaEventRecord(pf.consumed[q], ctx->stream));
+      } else {
+        const int64_t* di = upload_indices(idx);
+        mlp_grad_dev(mlp, w_a_full.p, Xptr, yptr, di, B_local, ncls, scale, g_full.p);
+        if (host_resident) h2d_bytes += (double)B_local * (D + 1) * sizeof(float);
+      }
       mlp_loss_sum(mlp, B_local, stepacc.p);
-      if (host_resident) h2d_bytes += (double)B_local * (D + 1) * sizeof(float);
     } else {
       DHO2G_CUDA(cudaMemsetAsync(g_full.p, 0, n * sizeof(float), ctx->stream));
     }
@@ -275,6 +425,7 @@ struct dho2g_trainer {
           if (k_outer >= cfg.outer_rounds) done = true;
         }
       }
+      if (pf.th.joinable() && !done) prefetch((int64_t)(k_outer * cfg.inner_epochs + l_inner), r);
     } else {  // run_fosi (:187-209) / run_first_order (:174-185)
       if (epoch_fo >= cfg.epochs) {
         done = true;
@@ -297,6 +448,7 @@ struct dho2g_trainer {
         ++epoch_fo;
         if (epoch_fo >= cfg.epochs) done = true;
       }
+      if (pf.th.joinable() && !done) prefetch((int64_t)epoch_fo, r);
     }
   }
 };
@@ -451,6 +603,7 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   t->idx_dev.alloc(t->idx_stride * dho2g_trainer::kSlots);
   t->acc2.alloc(4);
   t->stepacc.alloc(2);
+  if (host_resident && !quad && N > 0) t->prefetch_init();
   wait_stream(ctx, st);
   return t.release();
 }

@@ -125,3 +125,28 @@ def test_graph_refresh_bitwise_equal_to_eager(ctx):
     assert (out[0].w_final == out[1].w_final).all()
     assert (out[0].loss == out[1].loss).all()
     assert ctx.stat("lanczos_graph_launches") >= 2
+
+
+@pytest.mark.parametrize("trainer", ["dho2", "fosi"])
+def test_host_resident_matches_device_resident(ctx, trainer):
+    """End-to-end mode (dataset in pinned host memory; each next batch gathered on a host thread and
+    copied while the current step computes) is bitwise the device-resident run, across epoch edges."""
+    from oracle.bindings import blobs_dataset
+    sizes = [20, 16, 12, 5]
+    X, y = blobs_dataset(100, 20, 5, seed=7)
+    w0 = d.MlpOracle(ctx, sizes).init_params(2)
+    out = []
+    for host in (False, True):
+        mlp = d.MlpOracle(ctx, sizes)
+        cfg = d.TrainerConfig(kind=trainer, base=d.BaseConfig("adam"), k=3, l=1, outer_rounds=2, inner_epochs=2,
+                              epochs=3, batch_size=16, curvature_batch=40, seed=21)
+        tr = d.Trainer(ctx, cfg, mlp, d.Dataset(X, y, 5, 7), w0, workers=2, host_resident=host)
+        losses = []
+        while not tr.stat("done"):
+            tr.step(1, with_eval=True)
+            losses.append(tr.last_loss())
+        res = tr.result()
+        out.append((res.w_final, np.array(losses), res.loss, tr.stat("h2d_bytes")))
+        tr.close()
+    assert (out[0][0] == out[1][0]).all() and (out[0][1] == out[1][1]).all() and (out[0][2] == out[1][2]).all()
+    assert out[1][3] > 0
