@@ -258,6 +258,7 @@ def run_ours(args, rank, world, dist):
     rounds = int(tr.stat("rounds_per_epoch"))
     refreshes0, rms0 = tr.stat("refreshes"), tr.stat("refresh_ms_total")
     launches0 = ctx.stat("launches")
+    nccl0 = (ctx.stat("nccl_calls"), ctx.stat("nccl_bytes")) if world > 1 else (0.0, 0.0)
     barrier()
     ctx.synchronize()
     sampler.mark()
@@ -268,6 +269,11 @@ def run_ours(args, rank, world, dist):
     ms = ctx.elapsed_ms(0, 1)
     clocks = sampler.stop()
     launches = ctx.stat("launches") - launches0
+    nccl = None
+    if world > 1:  # NCCL traffic of the timed steps; its time is inside the steps, not separated
+        calls, nbytes = ctx.stat("nccl_calls") - nccl0[0], ctx.stat("nccl_bytes") - nccl0[1]
+        nccl = {"calls_per_step": calls / args.steps, "bytes_per_step": nbytes / args.steps,
+                "algbw_GBps_if_serial": nbytes / (ms / 1e3) / 1e9 if ms > 0 else None}
     ms = max_over_ranks(ms)
     n_ref = tr.stat("refreshes") - refreshes0
     graph_stats = {"captures": ctx.stat("lanczos_graph_captures"), "launches": ctx.stat("lanczos_graph_launches")}
@@ -376,7 +382,7 @@ def run_ours(args, rank, world, dist):
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,
-            "refresh_graph": graph_stats,
+            "refresh_graph": graph_stats, "nccl": nccl,
             "kernel_timers": {"note": "per-kernel CUDA-event timers on the library stream during a second pass of "
                                       "the same K steps (fresh trainer, same warm-up), kernels serialised (the "
                                       "weight-block GEMMs' side-stream overlap is off in this pass); value comes "
