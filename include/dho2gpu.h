@@ -236,6 +236,9 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
 /* ---- test hook: each collective wrapper through a 1-rank NCCL communicator (plumbing check on one GPU).
  * The context must have no communicator; *max_err = worst element error (0 expected). */
 int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err);
+/* ---- test hook: per-CTA timelines (globaltimer ns: start, last MMA, last epilogue start, end) of pair-GEMM
+ * launches; on = 1 arms a buffer for n_ctas CTA slots, on = 0 copies it to out and disarms. */
+int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_t n_ctas);
 int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const float* A0, const float* A1,
                         const float* B0, const float* B1, float* C, int backend, int a_mn, int b_mn);
 

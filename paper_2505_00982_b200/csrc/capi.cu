@@ -1150,3 +1150,22 @@ int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err) {
     *max_err = err;
   });
 }
+
+// Test hook: per-CTA timelines of pair-GEMM launches (gemm.cu g_gemm_trace). on = 1 arms a zeroed buffer
+// of n_ctas x 4 u64 (each later pair-GEMM launch overwrites it); on = 0 copies it to out and disarms.
+int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_t n_ctas) {
+  return guard([&] {
+    check_ctx(ctx);
+    static DevBuf<unsigned long long> buf;
+    if (on) {
+      buf.alloc(n_ctas * 4);
+      gemm_trace_set(buf.p);
+    } else {
+      DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+      gemm_trace_set(nullptr);
+      if (out && buf.p)
+        DHO2G_CUDA(cudaMemcpy(out, buf.p, std::min(n_ctas * 4, buf.n) * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost));
+    }
+  });
+}

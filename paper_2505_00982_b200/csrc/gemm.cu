@@ -749,6 +749,15 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
 // (which processes it last) adds the later segments' partials in segment order and runs the fused
 // epilogue. The combine order is fixed by the schedule, so results are deterministic.
 namespace tc2 {
+// Optional per-CTA timeline of one pair-GEMM launch (option gemm_trace; investigation only): globaltimer
+// ns at [0] start of work (after the prologue), [1] last MMA issued (leader), [2] start of the last
+// segment's epilogue work, [3] end, per CTA slot blockIdx.x.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 using namespace tc;
 
 constexpr int BM = 128;   // output rows per CTA (pair tile 256)
@@ -899,6 +908,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // may overlap the previous kernel's tail; no global memory is touched before the previous grid has
   // completed and flushed (a no-op when launched without the attribute).
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long* trace = g_gemm_trace ? g_gemm_trace + (size_t)blockIdx.x * 4 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs): this CTA's halves of A and B into its ring
@@ -961,6 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       commit2(&tfull[ab]);
       ++uc;
     }
+    if (trace) trace[1] = gtimer();
   } else if (warp >= 4) {
     // ---------------- epilogue warps (both CTAs): 8 warps = 4 TMEM lane quadrants x 2 column halves
     const int ew = warp & 3;
@@ -977,6 +989,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
+      if (trace && threadIdx.x == 128) trace[2] = gtimer();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
       if (sg.k0 != 0) {
         // non-head segment (first of this worker): publish the raw partial
@@ -1034,6 +1047,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
   fence_before();
   __syncthreads();
+  if (trace && threadIdx.x == 0) trace[3] = gtimer();
   cluster_sync();
   if (warp == 2) {
     fence_after();
@@ -1198,4 +1212,12 @@ void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf1
   gemm3(ctx, M, N, K, Ahi, Alo, lda, Bhi, Blo, ldb, e);
 }
 
+}  // namespace dho2g
+
+// Test hook (option gemm_trace): route the next pair-GEMM launches' per-CTA timelines into buf (4 u64 per
+// CTA slot); buf = nullptr switches tracing off.
+namespace dho2g {
+void gemm_trace_set(unsigned long long* buf) {
+  DHO2G_CUDA(cudaMemcpyToSymbol(tc2::g_gemm_trace, &buf, sizeof(buf)));
+}
 }  // namespace dho2g
