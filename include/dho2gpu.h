@@ -40,6 +40,7 @@ typedef struct dho2g_lanczos dho2g_lanczos;/* ShardedLanczosResult (dist_lanczos
 typedef struct dho2g_ese dho2g_ese;        /* EseResult (lanczos.hpp:45-52), V_hat row-sharded */
 typedef struct dho2g_opt dho2g_opt;        /* BaseOptimizer (optimizer.hpp:28-46) */
 typedef struct dho2g_trainer dho2g_trainer;/* TrainerRun (trainer.cpp:51-269) */
+typedef struct dho2g_fabric dho2g_fabric;  /* in-process rendezvous for several ranks on one GPU (test backend) */
 
 /* ---- context, errors, collectives (collectives.hpp:88-125) ---------------------------- */
 const char* dho2g_last_error(void);
@@ -59,6 +60,13 @@ int dho2g_ctx_kernel_name(dho2g_ctx* ctx, int i, char* buf, size_t len);
 int dho2g_nccl_unique_id(void* id_out_128);
 int dho2g_comm_init(dho2g_ctx* ctx, const void* nccl_id_128, int rank, int world);
 int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world);
+/* Test backend for the multi-rank data path on fewer GPUs than ranks (the reference's in-process
+ * run_workers, collectives.hpp:124-125): `world` contexts, one host thread each, share a fabric; every
+ * collective is a host-side rendezvous plus stream-ordered device copies between the ranks' buffers
+ * (events, no kernel ever waits on another rank). Sums are in ascending rank order. */
+int dho2g_local_fabric_create(int world, dho2g_fabric** out);
+int dho2g_local_fabric_destroy(dho2g_fabric* fab);
+int dho2g_comm_init_local(dho2g_ctx* ctx, dho2g_fabric* fab, int rank);
 /* Accounting. Communication ledger (CommLedger, collectives.hpp:55-83): one row per
  * collective round this rank took part in — event index, op ("all_gather", "reduce_scatter",
  * "all_reduce"), logical floats, rank, modeled floats sent / received. Empty on a single GPU.

@@ -60,6 +60,9 @@ _SIGS = {
     "dho2g_nccl_unique_id": ([vp], C.c_int),
     "dho2g_comm_init": ([vp, vp, C.c_int, C.c_int], C.c_int),
     "dho2g_comm_rank": ([vp, ip, ip], C.c_int),
+    "dho2g_local_fabric_create": ([C.c_int, C.POINTER(vp)], C.c_int),
+    "dho2g_local_fabric_destroy": ([vp], C.c_int),
+    "dho2g_comm_init_local": ([vp, vp, C.c_int], C.c_int),
     "dho2g_ctx_ledger_rows": ([vp], C.c_size_t),
     "dho2g_ctx_ledger_row": ([vp, C.c_size_t, i64p, C.c_char_p, C.c_size_t, i64p, ip, i64p, i64p], C.c_int),
     "dho2g_ctx_memory_count": ([vp], C.c_size_t),

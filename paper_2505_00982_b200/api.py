@@ -157,6 +157,27 @@ def tridiag_eig(diag, off):
 
 
 # ----------------------------------------------------------------------------- context
+class LocalFabric:
+    """In-process rendezvous for `world` ranks on one GPU (include/dho2gpu.h: dho2g_local_fabric_create): the
+    multi-rank data path of the library without NCCL, each rank a Context driven by its own host thread."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib.dho2g_local_fabric_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def close(self):
+        if self.h:
+            lib.dho2g_local_fabric_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One GPU (rank). The reference's Worker (collectives.hpp:88-117) becomes a NCCL rank."""
 
@@ -199,6 +220,10 @@ class Context:
             name = buf.value.decode()
             out[name] = (self.stat(f"kt.{name}.ms"), self.stat(f"kt.{name}.count"), self.stat(f"kt.{name}.work"))
         return out
+
+    def comm_init_local(self, fabric: "LocalFabric", rank: int):
+        """Join an in-process fabric as `rank` (several ranks on one GPU, one host thread each)."""
+        check(lib.dho2g_comm_init_local(self.h, fabric.h, rank))
 
     def ledger(self):
         """This rank's communication ledger rows (CommLedger::Row, collectives.hpp:58-65):

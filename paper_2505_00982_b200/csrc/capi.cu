@@ -302,6 +302,27 @@ int dho2g_ctx_accounting_reset(dho2g_ctx* ctx) {
   });
 }
 
+int dho2g_local_fabric_create(int world, dho2g_fabric** out) {
+  return guard([&] {
+    if (world < 1 || !out) fail(DHO2G_ARGUMENT, "local fabric: world_size must be >= 1");
+    *out = new dho2g_fabric(world);
+  });
+}
+int dho2g_local_fabric_destroy(dho2g_fabric* fab) {
+  return guard([&] { delete fab; });
+}
+int dho2g_comm_init_local(dho2g_ctx* ctx, dho2g_fabric* fab, int rank) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!fab) fail(DHO2G_ARGUMENT, "local fabric: null");
+    if (rank < 0 || rank >= fab->world) fail(DHO2G_ARGUMENT, "Shard: rank out of range");
+    if (ctx->comm) fail(DHO2G_ARGUMENT, "local fabric: context already has a communicator");
+    ctx->rank = rank;
+    ctx->world = fab->world;
+    ctx->fabric = fab->world > 1 ? fab : nullptr;
+  });
+}
+
 int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world) {
   return guard([&] {
     if (!ctx) fail(DHO2G_ARGUMENT, "null context");

@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cmath>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <numeric>
 #include <thread>
 
@@ -314,12 +316,63 @@ void dho2g_ctx::kt_flush() {
   }
 }
 
+// ------------------------------------------------------------------ in-process fabric (test backend)
+// Ranks are contexts on one GPU, each driven by its own host thread. A collective is: record "ready" on
+// the caller's stream, rendezvous (host), copy / reduce every rank's deposit on the caller's stream after
+// waiting for the depositor's "ready" event, record "done", rendezvous, and make the caller's stream wait
+// for every rank's "done" (so no rank overwrites a send buffer a peer still reads). Only host threads and
+// stream events synchronise: no kernel waits on another rank.
+
+namespace {
+__global__ void fabric_sum_kernel(const float* __restrict__ parts, float* __restrict__ out, size_t count, int world) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    float s = parts[i];
+    for (int r = 1; r < world; ++r) s += parts[(size_t)r * count + i];  // ascending rank order
+    out[i] = s;
+  }
+}
+}  // namespace
+
+// kind 0: all-gather (recv = world x count, rank q's block from q); kind 1: reduce-scatter of float
+// (recv = count, sum over ranks of their block `rank`)
+static void fabric_collective(dho2g_ctx* ctx, const void* send, void* recv, size_t count, size_t elem, int kind) {
+  dho2g_fabric* f = ctx->fabric;
+  const int W = f->world, r = ctx->rank;
+  DHO2G_CUDA(cudaEventRecord(f->ready[r], ctx->stream));
+  f->send[r] = send;
+  f->barrier();
+  if (kind == 0) {
+    for (int q = 0; q < W; ++q) {
+      DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, f->ready[q], 0));
+      char* dst = static_cast<char*>(recv) + (size_t)q * count * elem;
+      if (dst != f->send[q])
+        DHO2G_CUDA(cudaMemcpyAsync(dst, f->send[q], count * elem, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  } else {
+    ctx->fabric_scratch.ensure((size_t)W * count);
+    for (int q = 0; q < W; ++q) {
+      DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, f->ready[q], 0));
+      DHO2G_CUDA(cudaMemcpyAsync(ctx->fabric_scratch.p + (size_t)q * count,
+                                 static_cast<const float*>(f->send[q]) + (size_t)r * count, count * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    fabric_sum_kernel<<<(unsigned)std::min<size_t>(dho2g::cdiv(count, 256), 1184), 256, 0, ctx->stream>>>(
+        ctx->fabric_scratch.p, static_cast<float*>(recv), count, W);
+    DHO2G_LAUNCH();
+  }
+  DHO2G_CUDA(cudaEventRecord(f->done[r], ctx->stream));
+  f->barrier();
+  for (int q = 0; q < W; ++q) DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, f->done[q], 0));
+  f->barrier();  // every rank has issued its waits before any "done" / "ready" is recorded again
+}
+
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
   if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream), "all_gather");
+  if (fabric) fabric_collective(this, send, recv, count, sizeof(double), 0);
+  else dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 8 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;
@@ -332,7 +385,8 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, cons
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream), "all_gather");
+  if (fabric) fabric_collective(this, send, recv, count, sizeof(float), 0);
+  else dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;
@@ -344,8 +398,9 @@ void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count)
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
   }
-  dho2g::nccl_call(this, dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream),
-                   "reduce_scatter");
+  if (fabric) fabric_collective(this, send, recv, count, sizeof(float), 1);
+  else dho2g::nccl_call(this, dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream),
+                        "reduce_scatter");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
   const int64_t c = (int64_t)count, w1 = world - 1;

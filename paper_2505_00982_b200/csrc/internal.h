@@ -1,7 +1,10 @@
 // Internal object layouts shared by the translation units of libdho2gpu.so.
 #pragma once
 
+#include <chrono>
+#include <condition_variable>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -64,6 +67,8 @@ struct dho2g_ctx {
   int upd_p2_variant = 5; // staged pass 2: 5 row-dot (R <= 32, else 0), 0 256-row x2 stages x2 CTAs/SM +
                           // column-dot phase, 1 128x2x4, 2 128x3x3, 3 128x4x2, 4 512x2x1
   ncclComm_t comm = nullptr;
+  dho2g_fabric* fabric = nullptr;  // in-process test backend (dho2g_comm_init_local) instead of NCCL
+  dho2g::DevBuf<float> fabric_scratch;
   int rank = 0, world = 1;
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
   double nccl_timeout_s = 600.0;  // host waits with a communicator give up (DEADLOCK) after this long
@@ -398,3 +403,38 @@ bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v);
 void trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count);
 void trainer_destroy(dho2g_trainer* tr);
 }  // namespace dho2g
+
+// In-process rendezvous for several ranks on one GPU (dho2g_comm_init_local; collectives in host.cu).
+struct dho2g_fabric {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  std::vector<const void*> send;
+  std::vector<cudaEvent_t> ready, done;
+  explicit dho2g_fabric(int w) : world(w), send(w, nullptr), ready(w, nullptr), done(w, nullptr) {
+    for (int r = 0; r < w; ++r) {
+      DHO2G_CUDA(cudaEventCreateWithFlags(&ready[r], cudaEventDisableTiming));
+      DHO2G_CUDA(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+    }
+  }
+  ~dho2g_fabric() {
+    for (int r = 0; r < world; ++r) {
+      cudaEventDestroy(ready[r]);
+      cudaEventDestroy(done[r]);
+    }
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      if (!cv.wait_for(lk, std::chrono::seconds(600), [&] { return gen != g; }))
+        dho2g::fail(DHO2G_DEADLOCK, "local fabric: a rank is missing from the round");
+    }
+  }
+};

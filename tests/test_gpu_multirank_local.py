@@ -1,0 +1,120 @@
+"""The multi-rank (G > 1) device path run for real on one GPU: 2 and 3 ranks, each a Context driven by
+its own host thread, joined by the in-process fabric (dho2g_comm_init_local) instead of NCCL. Every
+collective is a host rendezvous plus stream-ordered copies between the ranks' buffers (events only: no
+kernel waits on another rank). This exercises the CUDA code's sharding — row ranges, padded all-gathers,
+the HVP batch split + reduce-scatter, the GS partial all-reduces, the sharded Ritz vectors and sign argmax,
+the sharded update, the trainer's gradient reduce-scatter and parameter all-gather — against the same
+computation at G = 1. Reductions run in a different order than at G = 1 (rank-ordered fp64 sums, fp32
+reduce-scatter), so results agree to fp32 rounding, not bitwise."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2505_00982_b200 as d
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(world, fn):
+    fab = d.LocalFabric(world)
+    out, errs = [None] * world, []
+
+    def worker(r):
+        c = d.Context(0)
+        try:
+            c.comm_init_local(fab, r)
+            out[r] = fn(c, r)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+        finally:
+            c.close()
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    fab.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def lanczos_on(make_op, n, m, k, l, seed):
+    def fn(ctx, rank):
+        op = make_op(ctx)
+        st = d.lanczos_distributed(ctx, m, op, n, seed)
+        ese = d.extract_ese_distributed(ctx, st, k, l)
+        b, e = d.shard_for_rank(n, ctx.world, rank)
+        return st.tridiag.diag.copy(), st.tridiag.offdiag.copy(), ese.eigvals.copy(), ese.eigvecs_shard(e - b), \
+            ctx.ledger()
+    return fn
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_lanczos_diag_sharded(world):
+    n, m = 50_003, 30
+    spec = 1.0 + (np.arange(n) % 997) * 0.01
+    spec[:3] = [40.0, 30.0, -5.0]
+    fn = lanczos_on(lambda c: d.diagonal_operator(c, spec), n, m, 3, 2, 11)
+    (d1, o1, e1, v1, _), = run_ranks(1, fn)
+    outs = run_ranks(world, fn)
+    for dg, of, ev, _, ledger in outs:
+        assert np.abs(dg - d1).max() <= 1e-5 * 40 and np.abs(of - o1).max() <= 1e-5 * 40
+        assert np.abs(ev - e1).max() <= 1e-5 * 40
+        assert {r[1] for r in ledger} >= {"all_gather", "all_reduce"}
+    V = np.concatenate([o[3] for o in outs], axis=0)  # row shards in rank order
+    G = V.T @ v1  # sign-invariant: matching Ritz vectors have |cos| = 1
+    assert np.abs(np.abs(np.diag(G)) - 1).max() <= 1e-4
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_lanczos_mlp_sharded(world):
+    from oracle.bindings import blobs_dataset
+    sizes = [20, 16, 12, 5]
+    X, y = blobs_dataset(37, 20, 5, seed=3)
+
+    def make(c):
+        mlp = d.MlpOracle(c, sizes)
+        w = mlp.init_params(1)
+        make.keep = mlp
+        return d.mlp_hvp_operator(c, mlp, w, d.Batch(X, y, 5))
+
+    nparam = sum(sizes[i] * sizes[i + 1] + sizes[i + 1] for i in range(len(sizes) - 1))
+    fn = lanczos_on(make, nparam, 20, 4, 2, 77)
+    (d1, o1, e1, v1, _), = run_ranks(1, fn)
+    for dg, of, ev, _, ledger in run_ranks(world, fn):
+        scale = np.abs(e1).max()
+        assert np.abs(dg - d1).max() <= 1e-5 * scale and np.abs(ev - e1).max() <= 1e-5 * scale
+        assert "reduce_scatter" in {r[1] for r in ledger}  # batch-split HVP partials
+
+
+def test_lanczos_rotated_quadratic_sharded():
+    spec = np.linspace(-3.0, 9.0, 300)  # (no zero entry: the constructor rejects one)
+    fn = lanczos_on(lambda c: d.quadratic_operator(c, spec, 5), 300, 24, 3, 1, 4)
+    (d1, o1, e1, _, _), = run_ranks(1, fn)
+    for dg, of, ev, _, _ in run_ranks(2, fn):
+        assert np.abs(dg - d1).max() <= 1e-5 * 9 and np.abs(ev - e1).max() <= 1e-5 * 9
+
+
+@pytest.mark.parametrize("world,trainer,base", [(2, "dho2", "adamw"), (3, "fosi", "momentum"), (2, "sgd", "sgd")])
+def test_trainer_sharded(world, trainer, base):
+    from oracle.bindings import blobs_dataset
+    sizes = [20, 16, 12, 5]
+    X, y = blobs_dataset(160, 20, 5, seed=7)
+
+    def fn(c, rank):
+        mlp = d.MlpOracle(c, sizes)
+        w0 = mlp.init_params(2)
+        cfg = d.TrainerConfig(kind=trainer, base=d.BaseConfig(base), k=3, l=1, outer_rounds=2, inner_epochs=2,
+                              epochs=3, batch_size=8, curvature_batch=40, seed=21)
+        res = d.train(c, cfg, mlp, d.Dataset(X, y, 5, 7), w0, workers=4)
+        return res.w_final, res.loss, res.ese_refreshes, len(c.ledger())
+
+    (w1, l1, r1, n1), = run_ranks(1, fn)
+    assert n1 == 0  # one GPU: no communication rounds
+    for w, loss, refr, nrows in run_ranks(world, fn):
+        assert refr == r1 and len(loss) == len(l1) and nrows > 0
+        assert np.linalg.norm(w - w1) / np.linalg.norm(w1) <= 1e-5
+        assert np.abs(loss - l1).max() <= 1e-4 * np.abs(l1).max()
