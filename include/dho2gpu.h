@@ -78,6 +78,8 @@ int dho2g_ctx_ledger_row(dho2g_ctx* ctx, size_t i, int64_t* event, char* op, siz
 size_t dho2g_ctx_memory_count(dho2g_ctx* ctx);
 int dho2g_ctx_memory_entry(dho2g_ctx* ctx, size_t i, char* name, size_t name_len, int64_t* slots);
 int dho2g_ctx_accounting_reset(dho2g_ctx* ctx);
+/* All-gather of `count` host doubles per rank (rank order) through the context's collectives; every rank calls. */
+int dho2g_ctx_allgather_host(dho2g_ctx* ctx, const double* in, size_t count, double* out);
 
 /* ---- host bookkeeping, bit-exact with the reference (no device needed) ---------------- */
 void dho2g_rng_u64(uint64_t seed, size_t n, uint64_t* out);           /* rng.hpp:18-23 */

@@ -248,6 +248,13 @@ class Context:
             out[name.value.decode()] = v.value
         return out
 
+    def allgather_host(self, values):
+        """All-gather host doubles across ranks (rank order); every rank must call it."""
+        x = _f64(np.atleast_1d(values))
+        out = np.empty(x.size * self.world)
+        check(lib.dho2g_ctx_allgather_host(self.h, _d(x), x.size, _d(out)))
+        return out.reshape(self.world, x.size)
+
     def reset_accounting(self):
         check(lib.dho2g_ctx_accounting_reset(self.h))
 

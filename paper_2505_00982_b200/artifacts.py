@@ -142,7 +142,10 @@ def run_experiment(ctx: Context, cfg: TrainerConfig, oracle, data: Dataset, w0, 
         res.raw_wallclock_ms = (time.perf_counter() - t0) * 1e3
     finally:
         tr.close()
-    meters = [ctx.memory()]  # this rank; a multi-GPU launcher gathers one per rank
+    meters = [ctx.memory()]
+    if ctx.world > 1:  # every rank's D_shard peak, in rank order (the reference lists one per worker)
+        slots = ctx.allgather_host([float(meters[0].get("D_shard", 0))])[:, 0]
+        meters = [dict(meters[0]) if r == ctx.rank else {"D_shard": int(v)} for r, v in enumerate(slots)]
     write_metrics_csv(paths.metrics_csv, cfg.kind, res)
     write_ledger_csv(paths.ledger_csv, ctx.ledger())
     write_memory_csv(paths.memory_csv, meters)

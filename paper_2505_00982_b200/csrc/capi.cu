@@ -1190,3 +1190,16 @@ int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_
     }
   });
 }
+
+// Host-level all-gather of `count` doubles per rank through the context's collectives (rank order), e.g.
+// for run artifacts that list per-rank accounting. Every rank must call it.
+int dho2g_ctx_allgather_host(dho2g_ctx* ctx, const double* in, size_t count, double* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    DevBuf<double> a(std::max<size_t>(count, 1)), b(std::max<size_t>(count * ctx->world, 1));
+    DHO2G_CUDA(cudaMemcpyAsync(a.p, in, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->allgather_f64(a.p, b.p, count);
+    DHO2G_CUDA(cudaMemcpyAsync(out, b.p, count * ctx->world * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    wait_stream(ctx, ctx->stream);
+  });
+}

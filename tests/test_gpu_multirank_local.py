@@ -118,3 +118,28 @@ def test_trainer_sharded(world, trainer, base):
         assert refr == r1 and len(loss) == len(l1) and nrows > 0
         assert np.linalg.norm(w - w1) / np.linalg.norm(w1) <= 1e-5
         assert np.abs(loss - l1).max() <= 1e-4 * np.abs(l1).max()
+
+
+def test_comm_ledger_report_two_ranks(tmp_path):
+    """The ledger of a 2-rank device run (artifacts.run_experiment) satisfies the device comm_report: GS
+    partial and beta all-reduces per iteration and pass, traffic conserved, plus the reference-schema
+    memory accounting (D_shard = ceil(n/G)(m+1))."""
+    from oracle.bindings import blobs_dataset
+    from paper_2505_00982_b200 import artifacts as A
+    sizes = [20, 16, 12, 5]
+    X, y = blobs_dataset(160, 20, 5, seed=7)
+
+    def fn(c, rank):
+        mlp = d.MlpOracle(c, sizes)
+        cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig("adam"), k=3, l=1, outer_rounds=2, inner_epochs=1,
+                              batch_size=8, curvature_batch=40, seed=21)
+        out = str(tmp_path / f"rank{rank}")
+        rc = A.run_experiment(c, cfg, mlp, d.Dataset(X, y, 5, 7), mlp.init_params(2), out, workers=4)
+        return rc, out
+
+    outs = run_ranks(2, fn)
+    for rc, out in outs:
+        assert rc == 0
+        rep = A.comm_report(out)
+        assert "communication ledger: OK" in rep, rep
+        assert "memory accounting: OK" in A.memory_report([out])
