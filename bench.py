@@ -115,11 +115,14 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def cpu_reference_sample(cfgname, threads=None, reps=1):
+def _ref_components(cfgname, parts=("grad", "hvp", "gs", "upd")):
     """Times the UNMODIFIED reference (oracle/_ref/libdho2ref.so, -O2 -fopenmp) on bounded samples of the
-    workload and extrapolates one DHO2 step (gradient + split update + 1/(P*rounds) of a refresh).
-    Returns (steps_per_sec, refresh_ms, detail)."""
+    workload's components: per-sample gradient and HVP cost, one Gram-Schmidt projection, one update pass.
+    Models above ~20M parameters are timed on a two-hidden-layer slice [D, H, H, K] of the same widths and
+    scaled by the flop ratio (the oracle's per-sample loops cost ~linearly in flops; measured within ~10 %
+    of a three-hidden-layer slice), so one component sample stays a few seconds of CPU work."""
     from oracle.bindings import CpuChecker, base_cfg, blobs_dataset, reference_available
+    import numpy as np
     kind = "reference" if reference_available() else "port"
     R = CpuChecker(kind)
     c = CONFIGS[cfgname]
@@ -127,41 +130,63 @@ def cpu_reference_sample(cfgname, threads=None, reps=1):
     n = mlp_dim(sizes)
     T = R.max_threads()
     Bs = 16 * T  # one 16-sample chunk per OpenMP thread (oracle.cpp:374-382)
-    X, y = blobs_dataset(Bs, sizes[0], sizes[-1], seed=7)
-    w = R.mlp_init(sizes, 1)
-    v = R.rng_normal(5, n)
-    t0 = time.perf_counter()
-    R.mlp_grad(sizes, w, X, y, sizes[-1])
-    t_grad = (time.perf_counter() - t0) / Bs
-    t0 = time.perf_counter()
-    R.mlp_hvp(sizes, w, v, X, y, sizes[-1])
-    t_hvp = (time.perf_counter() - t0) / Bs
-    del w, v
-    ns = min(n, 1 << 20)
+    tsizes = sizes if n <= 20_000_000 else [sizes[0], sizes[1], sizes[2], sizes[-1]]
     m = c["m"] or R.lanczos_budget(c["k"], 0, n)
-    r = c["k"]
-    import numpy as np
-    D = np.asarray(R.rng_normal(3, ns * (m // 2 + 1))).reshape(m // 2 + 1, ns).T
-    h = R.rng_normal(4, ns)
-    t0 = time.perf_counter()
-    _project(R, D, h)
-    t_gs_mid = time.perf_counter() - t0  # one projection over m/2+1 active columns
-    V = np.asarray(R.rng_normal(6, ns * r)).reshape(r, ns).T
-    g = R.rng_normal(7, ns)[None, :]
-    t0 = time.perf_counter()
-    R.deltas_seq(base_cfg(c["base"]), np.linspace(1, 2, r), V, g, np.zeros(ns), 0.1, pi=np.zeros(ns), sigma=1e-2)
-    t_upd = (time.perf_counter() - t0) * n / ns
-    scale = n / ns
-    gs_refresh = t_gs_mid * scale * m  # sum_i (i+1) ~ m * (m/2+1)
-    refresh_s = m * t_hvp * c["curv"] + gs_refresh
-    step_s = t_grad * c["b"] * c["workers"] + t_upd
+    ns = min(n, 1 << 20)
+    out = dict(kind=kind, cores=T, Bs=Bs, tsizes=tsizes, m=m, ns=ns)
+    if "grad" in parts or "hvp" in parts:
+        X, y = blobs_dataset(Bs, sizes[0], sizes[-1], seed=7)
+        w = R.mlp_init(tsizes, 1)
+        if "grad" in parts:
+            t0 = time.perf_counter()
+            R.mlp_grad(tsizes, w, X, y, sizes[-1])
+            out["grad"] = (time.perf_counter() - t0) / Bs * grad_flops(sizes, 1) / grad_flops(tsizes, 1)
+        if "hvp" in parts:
+            v = R.rng_normal(5, mlp_dim(tsizes))
+            t0 = time.perf_counter()
+            R.mlp_hvp(tsizes, w, v, X, y, sizes[-1])
+            out["hvp"] = (time.perf_counter() - t0) / Bs * hvp_flops(sizes, 1) / hvp_flops(tsizes, 1)
+    if "gs" in parts:
+        D = np.asarray(R.rng_normal(3, ns * (m // 2 + 1))).reshape(m // 2 + 1, ns).T
+        h = R.rng_normal(4, ns)
+        t0 = time.perf_counter()
+        _project(R, D, h)
+        out["gs"] = (time.perf_counter() - t0) * (n / ns) * m  # sum_i (i+1) ~ m (m/2+1) columns per refresh
+    if "upd" in parts:
+        r = c["k"]
+        V = np.asarray(R.rng_normal(6, ns * r)).reshape(r, ns).T
+        g = R.rng_normal(7, ns)[None, :]
+        t0 = time.perf_counter()
+        R.deltas_seq(base_cfg(c["base"]), np.linspace(1, 2, r), V, g, np.zeros(ns), 0.1, pi=np.zeros(ns), sigma=1e-2)
+        out["upd"] = (time.perf_counter() - t0) * n / ns
+    return out
+
+
+def _ref_combine(cfgname, comp):
+    """One DHO2 step from component times: gradient + split update + 1/(P*rounds) of a refresh
+    (m HVPs on the curvature batch + the Gram-Schmidt sweeps). Returns (steps/s, refresh ms, sample text)."""
+    c = CONFIGS[cfgname]
+    n = mlp_dim(c["sizes"])
+    m = comp["m"]
+    refresh_s = m * comp["hvp"] * c["curv"] + comp["gs"]
+    step_s = comp["grad"] * c["b"] * c["workers"] + comp["upd"]
     rounds = -(-(-(-c["N"] // c["workers"])) // c["b"])
     per_step = step_s + refresh_s / (c["P"] * rounds)
-    sample = (f"{kind} lib, {T} OpenMP threads: grad+hvp on {Bs} samples (per-sample cost x {c['b'] * c['workers']} / "
-              f"{c['curv']}), project_out over {ns} rows x {m // 2 + 1} cols and admm_deltas({c['base']}) on {ns} rows, "
-              f"extrapolated linearly to n={n}, m={m}; refresh amortised over {c['P'] * rounds} steps")
-    return 1.0 / per_step, refresh_s * 1e3, dict(kind=kind, cores=T, sample=sample, t_grad_sample=t_grad,
-                                                 t_hvp_sample=t_hvp, t_update_step=t_upd, gs_refresh_s=gs_refresh)
+    ts = comp["tsizes"]
+    sliced = "" if list(ts) == list(c["sizes"]) else f" of the slice {'-'.join(map(str, ts))} (x flop ratio)"
+    sample = (f"{comp['kind']} lib, {comp['cores']} OpenMP threads: grad+hvp on {comp['Bs']} samples{sliced} "
+              f"(per-sample cost x {c['b'] * c['workers']} / {c['curv']}), project_out over {comp['ns']} rows x "
+              f"{m // 2 + 1} cols and admm_deltas({c['base']}) on {comp['ns']} rows, extrapolated linearly to n={n}, "
+              f"m={m}; refresh amortised over {c['P'] * rounds} steps")
+    return 1.0 / per_step, refresh_s * 1e3, sample
+
+
+def cpu_reference_sample(cfgname):
+    """All components once (the cpu_baseline leg of our own bench line). Returns (steps/s, refresh ms, detail)."""
+    comp = _ref_components(cfgname)
+    v, rm, sample = _ref_combine(cfgname, comp)
+    return v, rm, dict(kind=comp["kind"], cores=comp["cores"], sample=sample, t_grad_sample=comp["grad"],
+                       t_hvp_sample=comp["hvp"], t_update_step=comp["upd"], gs_refresh_s=comp["gs"])
 
 
 def _project(R, D, h):
@@ -186,18 +211,29 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     os.environ.setdefault("OMP_NUM_THREADS", str(min(os.cpu_count() or 1, 16)))
-    vals, rms = [], []
+    # each step samples half of the components (alternating), so that one step is a few seconds of CPU work
+    # and the whole --steps K --warmup W run stays within minutes; the timed steps' samples are averaged
+    samples = {"grad": [], "hvp": [], "gs": [], "upd": []}
+    comp = None
     for s in range(args.warmup + args.steps):
-        v, rm, det = cpu_reference_sample(args.config)
+        # warm-up steps only warm the library and its thread pool (the cheapest component); timed steps
+        # alternate between the two halves of the components
+        parts = ("upd",) if s < args.warmup else (("grad", "gs") if (s - args.warmup) % 2 == 0 else ("hvp", "upd"))
+        comp = _ref_components(args.config, parts)
         if s >= args.warmup:
-            vals.append(v)
-            rms.append(rm)
-    value = sum(vals) / len(vals)
+            for p in parts:
+                samples[p].append(comp[p])
+    for p in samples:  # K = 1: fill the component the timed step did not sample from the warm-up
+        if not samples[p]:
+            samples[p].append(_ref_components(args.config, (p,))[p])
+    comp.update({p: sum(v) / len(v) for p, v in samples.items()})
+    value, refresh_ms, sample = _ref_combine(args.config, comp)
+    det = {"kind": comp["kind"], "cores": comp["cores"], "sample": sample + "; components sampled alternately per step"}
     line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_json(args.config, world),
-            "refresh_ms": sum(rms) / len(rms),
+            "refresh_ms": refresh_ms,
             "cpu_baseline": {"value": value, "unit": "steps/s", "cores": det["cores"], "kind": det["kind"],
                              "sample": det["sample"]},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
