@@ -325,6 +325,7 @@ struct dho2g_lanczos {
   unsigned long long glaunches = 0;  // kernel launches recorded in the graph
   dho2g::DevBuf<uint64_t> seed_dev;
   dho2g::HostBuf<uint64_t> seed_host;
+  dho2g::DevBuf<double> seed_chk;  // [2] own seed halves, [2 world] gathered (multi-rank seed check)
   ~dho2g_lanczos() {
     if (gexec) cudaGraphExecDestroy(gexec);
   }

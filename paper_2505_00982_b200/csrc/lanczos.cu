@@ -951,6 +951,21 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   dho2g_ctx* ctx = lz->ctx;
   cudaStream_t st = ctx->stream;
   const size_t m = lz->m;
+  if (ctx->world > 1) {
+    // v1 is drawn from the shared seed on every rank; a mismatched seed would silently blend slices of
+    // different vectors (dist_lanczos.cpp:47-52 checks the same with a hash of v1): compare the seeds
+    lz->seed_chk.ensure(2 + 2 * (size_t)ctx->world);
+    double mine[2] = {(double)(uint32_t)(seed >> 32), (double)(uint32_t)seed};
+    DHO2G_CUDA(cudaMemcpyAsync(lz->seed_chk.p, mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+    ctx->allgather_f64(lz->seed_chk.p, lz->seed_chk.p + 2, 2, "hash_check");
+    std::vector<double> all(2 * (size_t)ctx->world);
+    DHO2G_CUDA(cudaMemcpyAsync(all.data(), lz->seed_chk.p + 2, all.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                               st));
+    wait_stream(ctx, st);
+    for (int r = 0; r < ctx->world; ++r)
+      if (all[2 * r] != mine[0] || all[2 * r + 1] != mine[1])
+        fail(DHO2G_DIVERGENCE, "lanczos_distributed: seed mismatch across ranks");
+  }
   cudaEvent_t e0, e1;
   DHO2G_CUDA(cudaEventCreate(&e0));
   DHO2G_CUDA(cudaEventCreate(&e1));

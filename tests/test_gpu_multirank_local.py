@@ -143,3 +143,18 @@ def test_comm_ledger_report_two_ranks(tmp_path):
         rep = A.comm_report(out)
         assert "communication ledger: OK" in rep, rep
         assert "memory accounting: OK" in A.memory_report([out])
+
+
+def test_seed_mismatch_is_divergence_error():
+    """test_dist_lanczos.cpp:123-138: ranks that disagree on the Lanczos seed fail with DivergenceError."""
+    spec = 1.0 + np.arange(1000) * 0.01
+
+    def fn(c, rank):
+        op = d.diagonal_operator(c, spec)
+        try:
+            d.lanczos_distributed(c, 10, op, 1000, 7 + rank)
+        except d.DivergenceError as e:
+            return str(e)
+        return "no error"
+
+    assert all("seed mismatch" in r for r in run_ranks(2, fn))
