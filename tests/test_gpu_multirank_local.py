@@ -158,3 +158,17 @@ def test_seed_mismatch_is_divergence_error():
         return "no error"
 
     assert all("seed mismatch" in r for r in run_ranks(2, fn))
+
+
+def test_lanczos_uneven_and_empty_shards():
+    """Shard::for_rank leaves trailing ranks empty (collectives.cpp:10-20): n = 7 over 5 ranks is 2,2,2,1,0."""
+    n, m = 7, 5
+    spec = np.array([5.0, 4.0, 3.0, 2.0, 1.0, 0.5, -1.0])
+    fn = lanczos_on(lambda c: d.diagonal_operator(c, spec), n, m, 2, 1, 3)
+    (d1, o1, e1, v1, _), = run_ranks(1, fn)
+    outs = run_ranks(5, fn)
+    assert [o[3].shape[0] for o in outs] == [2, 2, 2, 1, 0]
+    for dg, of, ev, _, _ in outs:
+        assert np.abs(dg - d1).max() <= 1e-5 * 5 and np.abs(ev - e1).max() <= 1e-5 * 5
+    V = np.concatenate([o[3] for o in outs], axis=0)
+    assert np.abs(np.abs(np.diag(V.T @ v1)) - 1).max() <= 1e-4
