@@ -172,3 +172,21 @@ def test_lanczos_uneven_and_empty_shards():
         assert np.abs(dg - d1).max() <= 1e-5 * 5 and np.abs(ev - e1).max() <= 1e-5 * 5
     V = np.concatenate([o[3] for o in outs], axis=0)
     assert np.abs(np.abs(np.diag(V.T @ v1)) - 1).max() <= 1e-4
+
+
+def test_quadratic_trainer_with_empty_shard():
+    """A rotated-quadratic DHO2 run over 4 ranks with n = 6 (shards 2,2,2,0) against 1 rank."""
+    spec = np.array([9.0, 5.0, 3.0, 2.0, 1.0, 0.5])
+
+    def fn(c, rank):
+        q = d.QuadraticOracle(c, spec, 4)
+        w0 = np.linspace(-1.0, 1.5, 6)
+        cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig("momentum", lr=0.05), k=3, alpha=0.5, sigma=0.1,
+                              outer_rounds=3, inner_epochs=2, batch_size=1, seed=5)
+        res = d.train(c, cfg, q, d.Dataset.dummy(4), w0, workers=4)
+        q.close()
+        return res.w_final, res.loss
+
+    (w1, l1), = run_ranks(1, fn)
+    for w, loss in run_ranks(4, fn):
+        assert np.abs(w - w1).max() <= 1e-5 * np.abs(w1).max() and np.abs(loss - l1).max() <= 1e-5 * l1.max()
