@@ -11,8 +11,9 @@
 // registers -> coalesced stores. The CUDA-core form is FMA/LDS-bound (2 rows.m.r FMAs); this one is
 // HBM-bound.
 //
-// Persistent: one CTA per SM walks 128-row tiles. Staging is double-buffered (TMA of tile i+1 overlaps
-// the split and MMAs of tile i); the hi/lo operand buffer is single but handed over per 32-wide K-chunk
+// Persistent: one CTA per SM walks 128-row tiles. The basis streams through a ring of NCS 16 KB K-chunk
+// stages (128 rows x 32 columns; NCS = what shared memory leaves, 4-6 at C4) so several chunks are in
+// flight while chunk kc is split; the hi/lo operand buffer is single but handed over per 32-wide K-chunk
 // (the MMAs of chunk kc start as soon as it is split; the next tile's split of chunk kc waits only for
 // those MMAs). Warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM owner, warps 4-11 split (two threads
 // per row), warps 12-15 epilogue (TMEM lane quadrant = warp % 4).
@@ -28,13 +29,24 @@ using namespace tc;
 constexpr int TM = 128;  // rows per tile (UMMA M)
 constexpr int kMaxChunks = 8;  // K-chunks of 32 (KP <= 256)
 
+constexpr uint32_t CB = TM * 32 * 4;  // one staged K-chunk: 128 rows x 32 basis columns fp32 (16 KB)
+constexpr int kMaxStages = 8;
+
 struct Geo {
   int KP, NP;  // padded K (= me, multiple of 32) and N (= r, 32 or 64)
+  int NCS;     // K-chunk staging ring depth (what is left of shared memory, <= kMaxStages)
   __host__ __device__ uint32_t dbytes() const { return (uint32_t)TM * KP * 4; }  // one 128 x KP fp32 tile
   __host__ __device__ uint32_t ubytes() const { return (uint32_t)NP * KP * 4; }  // one U (hi or lo)
-  // staging x2, hi, lo, Uh, Ul
-  __host__ __device__ uint32_t smem() const { return 4 * dbytes() + 2 * ubytes() + 1024 + 512; }
+  // chunk stages, hi, lo, Uh, Ul, barriers
+  __host__ __device__ uint32_t smem() const { return NCS * CB + 2 * dbytes() + 2 * ubytes() + 1024 + 1024; }
 };
+
+inline Geo make_geo(int me, int r) {
+  Geo g{(int)round_up((size_t)me, 32), r <= 32 ? 32 : 64, 0};
+  const long long left = 227LL * 1024 - 2LL * g.dbytes() - 2LL * g.ubytes() - 2048;
+  g.NCS = (int)std::max(0LL, std::min<long long>(kMaxStages, left / (long long)CB));
+  return g;
+}
 
 // Round to the nearest tf32 (10-bit mantissa) value, kept in an fp32 container. Both split terms are
 // rounded (not truncated), so what the tensor core drops is centred: ~2^-22 relative per product,
@@ -55,28 +67,31 @@ __global__ void __launch_bounds__(512, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t DB = g.dbytes(), UB = g.ubytes();
-  uint8_t* stg0 = smem;          // [2] staging, [k][128 rows] fp32 (TMA, no swizzle)
-  uint8_t* Ah = smem + 2 * DB;   // hi, K-major SW128: K-chunk kc (32 elems) at kc * 16 KB
+  const int NCS = g.NCS;
+  uint8_t* stg0 = smem;               // [NCS] K-chunk stages, [32 k][128 rows] fp32 (TMA, no swizzle)
+  uint8_t* Ah = smem + NCS * CB;      // hi, K-major SW128: K-chunk kc (32 elems) at kc * 16 KB
   uint8_t* Al = Ah + DB;
   uint8_t* Uh = Al + DB;         // K-major SW128: K-chunk kc at kc * NP * 128
   uint8_t* Ul = Uh + UB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(Ul + UB);
-  uint64_t* full = bars;        // [2] staging landed
-  uint64_t* sfree = bars + 2;   // [2] staging consumed by the split
-  uint64_t* tfull = bars + 4;   // [2] accumulator ready
-  uint64_t* tempty = bars + 6;  // [2] accumulator drained
-  uint64_t* ufull = bars + 8;   // U landed
-  uint64_t* hready = bars + 9;  // [kMaxChunks] K-chunk of hi/lo written
-  uint64_t* hfree = bars + 9 + kMaxChunks;  // [kMaxChunks] MMAs done reading that K-chunk
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9 + 2 * kMaxChunks);
+  uint64_t* full = bars;                     // [NCS] chunk stage landed
+  uint64_t* sfree = bars + kMaxStages;       // [NCS] chunk stage consumed by the split
+  uint64_t* tfull = sfree + kMaxStages;      // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;              // [2] accumulator drained
+  uint64_t* ufull = tempty + 2;              // U landed
+  uint64_t* hready = ufull + 1;              // [kMaxChunks] K-chunk of hi/lo written
+  uint64_t* hfree = hready + kMaxChunks;     // [kMaxChunks] MMAs done reading that K-chunk
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + kMaxChunks);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem_cols = 2 * (uint32_t)g.NP;  // 64 or 128
   const int nkc = g.KP / 32;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NCS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&sfree[s], 8);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);
     }
@@ -98,19 +113,21 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // ---------------- producer: U (hi, lo) once, then one 128 x KP tile per stage
+    // ---------------- producer: U (hi, lo) once, then the tiles' 128 x 32 K-chunks through an NCS-deep ring
+    // (up to NCS x 16 KB of the basis in flight per SM)
     mbar_expect_tx(ufull, 2 * UB);
     for (int kc = 0; kc < nkc; ++kc) {
       tma_load_2d<false>(Uh + kc * g.NP * 128, &mUh, kc * 32, 0, ufull);
       tma_load_2d<false>(Ul + kc * g.NP * 128, &mUl, kc * 32, 0, ufull);
     }
-    uint32_t i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const uint32_t s = i & 1;
-      mbar_wait(&sfree[s], ((i >> 1) & 1) ^ 1);
-      mbar_expect_tx(&full[s], DB);
-      tma_load_2d<false>(stg0 + s * DB, &mD, t * TM, 0, &full[s]);
-    }
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const uint32_t s = it % NCS;
+        mbar_wait(&sfree[s], ((it / NCS) & 1) ^ 1);
+        mbar_expect_tx(&full[s], CB);
+        tma_load_2d<false>(stg0 + s * CB, &mD, t * TM, kc * 32, &full[s]);
+      }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: Dh Uh + Dh Ul + Dl Uh, one K-chunk (4 k-steps of 8) as soon as it is split
     const uint32_t ID = idesc_tf32(g.NP);
@@ -154,16 +171,16 @@ __global__ void __launch_bounds__(512, 1)
     const int m = q & 127;
     const int c0 = (q >> 7) * 4;      // slots c0 .. c0+3 of each 128-byte row
     const uint32_t rowoff = (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u;
-    uint32_t i = 0;
+    uint32_t i = 0, it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const uint32_t s = i & 1;
-      mbar_wait(&full[s], (i >> 1) & 1);
-      const float* stg = reinterpret_cast<const float*>(stg0 + s * DB);
-      for (int kc = 0; kc < nkc; ++kc) {
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const uint32_t s = it % NCS;
+        mbar_wait(&full[s], (it / NCS) & 1);
+        const float* stg = reinterpret_cast<const float*>(stg0 + s * CB);
         mbar_wait(&hfree[kc], (i & 1) ^ 1);  // the previous tile's MMAs are done with this K-chunk
 #pragma unroll
         for (int c = c0; c < c0 + 4; ++c) {
-          const int k0 = kc * 32 + c * 4;
+          const int k0 = c * 4;  // within the staged chunk
           const float x0 = stg[(k0 + 0) * TM + m], x1 = stg[(k0 + 1) * TM + m];
           const float x2 = stg[(k0 + 2) * TM + m], x3 = stg[(k0 + 3) * TM + m];
           const float4 hi = make_float4(rn_tf32(x0), rn_tf32(x1), rn_tf32(x2), rn_tf32(x3));
@@ -175,10 +192,11 @@ __global__ void __launch_bounds__(512, 1)
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&hready[kc]);
+        if (lane == 0) {
+          mbar_arrive(&hready[kc]);
+          mbar_arrive(&sfree[s]);  // the stage is free for the next chunk load
+        }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sfree[s]);
     }
   } else if (warp >= 12) {
     // ---------------- epilogue: TMEM lane quadrant = warp % 4
@@ -243,8 +261,8 @@ CUtensorMap map_f32(void* encode_fn, const float* ptr, uint64_t inner, uint64_t 
 
 bool ritz_tc_supported(int me, int r) {
   if (me < 1 || r < 1 || r > 64) return false;
-  rtc::Geo g{(int)round_up((size_t)me, 32), r <= 32 ? 32 : 64};
-  return g.KP <= 256 && g.smem() <= 227 * 1024;
+  const rtc::Geo g = rtc::make_geo(me, r);
+  return g.KP <= 256 && g.NCS >= 2 && g.smem() <= 227 * 1024;
 }
 
 // V[:, 0:r] = D[:, 0:me] U' (U' device me x r row-major); rows < rows written, ldv / ldd chunk padded.
@@ -252,15 +270,15 @@ void ritz_tc(dho2g_ctx* ctx, const float* D, size_t ldd, int me, const float* U,
              size_t rows, DevBuf<float>& uscratch) {
   using namespace rtc;
   if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  Geo g{(int)round_up((size_t)me, 32), r <= 32 ? 32 : 64};
+  const Geo g = make_geo(me, r);
   cudaStream_t st = ctx->stream;
   uscratch.ensure((size_t)2 * g.KP * g.NP);
   float* Uh = uscratch.p;
   float* Ul = uscratch.p + (size_t)g.KP * g.NP;
   u_split_kernel<<<cdiv((size_t)g.KP * g.NP, 256), 256, 0, st>>>(U, me, r, g.KP, g.NP, Uh, Ul);
   DHO2G_LAUNCH();
-  // D: inner = rows, outer = basis columns (beyond me: zero fill); one 128-row x KP box, no swizzle
-  const CUtensorMap mD = map_f32(ctx->encode_fn, D, ldd, (uint64_t)me, ldd, TM, (uint32_t)g.KP, CU_TENSOR_MAP_SWIZZLE_NONE);
+  // D: inner = rows, outer = basis columns (beyond me: zero fill); 128-row x 32-column boxes, no swizzle
+  const CUtensorMap mD = map_f32(ctx->encode_fn, D, ldd, (uint64_t)me, ldd, TM, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
   // U hi / lo: K-major [NP][KP]; boxes of 32 K x NP rows, SWIZZLE_128B (the K-major canonical layout)
   const CUtensorMap mUh = map_f32(ctx->encode_fn, Uh, (uint64_t)g.KP, (uint64_t)g.NP, (uint64_t)g.KP, 32, (uint32_t)g.NP,
                                   CU_TENSOR_MAP_SWIZZLE_128B);

@@ -412,8 +412,8 @@ def test_admm_round(ctx, port):
 def test_ritz_tensor_core_matches_cuda_core(ctx, port, n, m, k, l):
     """Ritz vectors V = D U' on the tensor cores (tcgen05 kind::tf32, 3xTF32 split, ~2^-21 of sum |D||U'|)
     agree with the fp32 CUDA-core kernel: entries within 1e-5 of max|V| (the Ritz combinations cancel,
-    so entry-relative bounds are meaningless) and projectors within 1e-5 (SURVEY §8d bar: 1e-4).
-    m = 100 exceeds the tensor-core tile and takes the CUDA-core path."""
+    so entry-relative bounds are meaningless) and projectors within 3e-5 (SURVEY §8d bar: 1e-4; the
+    split's error grows with the K = m + 1 of the sums: 1.3e-5 measured at m = 100)."""
     spec = 1.0 + (np.arange(n) % 997) * 0.37 + 0.01 * port.rng_normal(3, n)
     op = d.diagonal_operator(ctx, spec)
     st = d.lanczos_distributed(ctx, m, op, n, 17)
@@ -432,7 +432,7 @@ def test_ritz_tensor_core_matches_cuda_core(ctx, port, n, m, k, l):
     assert np.max(np.abs(V1 - V0)) <= 1e-5 * np.max(np.abs(V0))
     G = V0.T @ V1  # ||V1 V1^T - V0 V0^T||_F^2 = tr(V0^T V0)^2-ish terms, evaluated without n x n matrices
     proj2 = np.sum((V0.T @ V0) ** 2) + np.sum((V1.T @ V1) ** 2) - 2 * np.sum(G ** 2)
-    assert np.sqrt(max(proj2, 0.0)) <= 1e-5
+    assert np.sqrt(max(proj2, 0.0)) <= 3e-5
 
 
 def test_nccl_collectives_one_rank(ctx):
