@@ -315,6 +315,13 @@ def run_ours(args, rank, world, dist):
     graph_stats = {"captures": ctx.stat("lanczos_graph_captures"), "launches": ctx.stat("lanczos_graph_launches")}
     refresh_ms = (tr.stat("refresh_ms_total") - rms0) / n_ref if n_ref else None
     refresh_ms = max_over_ranks(refresh_ms) if refresh_ms is not None else None
+    # epoch_end (full-dataset value + accuracy on the device), reported apart from steps/s:
+    # step on to the next epoch boundary with evaluation on
+    for _ in range(rounds + 1):
+        if tr.stat("eval_count") > 0 or tr.stat("done"):
+            break
+        tr.step(1, with_eval=True)
+    eval_ms = max_over_ranks(tr.stat("eval_ms_last")) if tr.stat("eval_count") > 0 else None
     tr.close()
 
     # ---- the same K steps again (fresh trainer, same warm-up) with CUDA-event timers around every kernel
@@ -419,6 +426,7 @@ def run_ours(args, rank, world, dist):
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,
             "refresh_graph": graph_stats, "nccl": nccl,
+            "epoch_end_eval_ms": eval_ms, "epoch_end_samples": c["N"],
             "kernel_timers": {"note": "per-kernel CUDA-event timers on the library stream during a second pass of "
                                       "the same K steps (fresh trainer, same warm-up), kernels serialised (the "
                                       "weight-block GEMMs' side-stream overlap is off in this pass); value comes "

@@ -86,6 +86,9 @@ struct dho2g_trainer {
   size_t refreshes = 0, safeguards = 0, steps = 0;
   int64_t gs_flops = 0;     // reference accounting (dist_lanczos.cpp:73): 4 active rows + rows per projection
   double sent_host = 0;     // staging for the all-rank floats-sent total of the modeled clock
+  cudaEvent_t eval_ev[2] = {};
+  double eval_ms_last = 0;  // device time of the last epoch_end evaluation
+  size_t eval_count = 0;
   double refresh_ms_last = 0, refresh_ms_total = 0;
   bool refreshed_this_epoch = false;
   bool done = false;
@@ -121,6 +124,8 @@ struct dho2g_trainer {
       cudaStreamDestroy(pf.cs);
     }
     for (auto& e : idx_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : eval_ev)
       if (e) cudaEventDestroy(e);
   }
 
@@ -344,6 +349,12 @@ struct dho2g_trainer {
 
   // epoch_end (trainer.cpp:150-172)
   void epoch_end(int64_t outer, int64_t inner, int64_t epoch, bool refreshed, bool with_resid) {
+    // full-dataset evaluation, timed on the device (reported apart from steps/s)
+    if (!eval_ev[0]) {
+      DHO2G_CUDA(cudaEventCreate(&eval_ev[0]));
+      DHO2G_CUDA(cudaEventCreate(&eval_ev[1]));
+    }
+    DHO2G_CUDA(cudaEventRecord(eval_ev[0], ctx->stream));
     size_t sb, se;
     shard_range(N, ctx->world, ctx->rank, &sb, &se);
     DHO2G_CUDA(cudaMemsetAsync(acc2.p, 0, 4 * sizeof(double), ctx->stream));
@@ -385,6 +396,12 @@ struct dho2g_trainer {
       row.wallclock = h[3] * 8.0 / (bw * 1.25e5 * world) + (double)gs_flops / (gf * 1e6 * world);
     }
     metrics.push_back(row);
+    DHO2G_CUDA(cudaEventRecord(eval_ev[1], ctx->stream));
+    DHO2G_CUDA(cudaEventSynchronize(eval_ev[1]));
+    float ems = 0.f;
+    DHO2G_CUDA(cudaEventElapsedTime(&ems, eval_ev[0], eval_ev[1]));
+    eval_ms_last = ems;
+    ++eval_count;
     check_opt_flags(&opt);
   }
 
@@ -657,6 +674,8 @@ bool trainer_stat(dho2g_trainer* tr, const std::string& key, double* v) {
   if (key == "refreshes") *v = (double)tr->refreshes;
   else if (key == "safeguard_passes") *v = (double)tr->safeguards;
   else if (key == "gs_flops") *v = (double)tr->gs_flops;
+  else if (key == "eval_ms_last") *v = tr->eval_ms_last;
+  else if (key == "eval_count") *v = (double)tr->eval_count;
   else if (key == "steps") *v = (double)tr->steps;
   else if (key == "refresh_ms_last") *v = tr->refresh_ms_last;
   else if (key == "refresh_ms_total") *v = tr->refresh_ms_total;
