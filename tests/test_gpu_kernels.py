@@ -249,6 +249,28 @@ def test_lanczos_dense_matches_checker(ctx, port):
     assert np.max(np.abs(V - Vr)) <= 1e-4  # same sign convention (lanczos.cpp:82-94)
 
 
+def test_lanczos_galerkin_and_orthonormality(ctx, port):  # test_lanczos.cpp:47-61
+    """D^T D = I and D^T H D = B on a random symmetric operator (fp32 basis: 1e-6 -> 2e-6 and 1e-5 ||H||)."""
+    H = random_symmetric(port, 50, 123)
+    st = d.lanczos_distributed(ctx, 20, d.dense_operator(ctx, H), 50, 9)
+    assert st.iterations == 20
+    Dm = st.basis_shard[:, :20]
+    assert np.abs(Dm.T @ Dm - np.eye(20)).max() <= 2e-6
+    B = np.diag(st.tridiag.diag) + np.diag(st.tridiag.offdiag[:19], 1) + np.diag(st.tridiag.offdiag[:19], -1)
+    assert np.linalg.norm(Dm.T @ H @ Dm - B) <= 1e-5 * np.abs(np.linalg.eigvalsh(H)).max()
+
+
+def test_lanczos_seed_determinism_bitwise(ctx, port):  # test_lanczos.cpp:85-93
+    H = random_symmetric(port, 30, 5)
+    op = d.dense_operator(ctx, H)
+    a = d.lanczos_distributed(ctx, 12, op, 30, 21)
+    b = d.lanczos_distributed(ctx, 12, op, 30, 21)
+    c = d.lanczos_distributed(ctx, 12, op, 30, 22)
+    assert (a.basis_shard == b.basis_shard).all() and (a.tridiag.diag == b.tridiag.diag).all()
+    assert (a.tridiag.offdiag == b.tridiag.offdiag).all()
+    assert not (c.tridiag.diag == a.tridiag.diag).all()
+
+
 def test_lanczos_identity_breakdown(ctx):  # test_lanczos.cpp:22-33
     st, ese = run_lanczos(ctx, d.dense_operator(ctx, np.eye(6)), 6, 4, 11, k=1)
     assert st.breakdown and st.iterations == 1 and st.tridiag.dim() == 1
