@@ -414,6 +414,22 @@ def test_deltas_known_answers(ctx):  # test_optimizer.cpp:78-199
         d.BaseOptimizer(ctx, d.BaseConfig("adam"), 2).step([1.0, np.inf], [0.0, 0.0])
 
 
+def test_delta_orthogonality_random_draws(ctx, port):  # test_optimizer.cpp:201-227
+    """Newton and base deltas are orthogonal (base lives in the complement of span(V_hat)) over 25 draws;
+    fp32 device arithmetic: |<newton, base>| <= 1e-6 |newton| |base| (reference: 1e-8 in fp64)."""
+    H = random_symmetric(port, 12, 7)
+    w, U = np.linalg.eigh(H)
+    idx = list(np.argsort(-w)[:3]) + [int(np.argmin(w))]
+    ese = d.EseResult.from_host(ctx, w[idx], U[:, idx])
+    opt = d.BaseOptimizer(ctx, d.BaseConfig("adam"), 12)
+    draws = port.rng_normal(4242, 25 * 24).reshape(25, 24)
+    for t in range(25):
+        g, pi = draws[t, :12], draws[t, 12:]
+        dl = d.admm_deltas(g, pi, ese, opt, np.zeros(12), 0.2, 0.05)
+        dot = float(np.dot(dl.newton, dl.base))
+        assert abs(dot) <= max(1e-6 * np.linalg.norm(dl.newton) * np.linalg.norm(dl.base), 1e-12)
+
+
 def test_admm_round(ctx, port):
     n = 1000
     w_a, pi, w_a2 = port.rng_normal(1, n), port.rng_normal(2, n), port.rng_normal(3, n)
