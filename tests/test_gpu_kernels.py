@@ -430,6 +430,32 @@ def test_delta_orthogonality_random_draws(ctx, port):  # test_optimizer.cpp:201-
         assert abs(dot) <= max(1e-6 * np.linalg.norm(dl.newton) * np.linalg.norm(dl.base), 1e-12)
 
 
+def test_optimizer_reference_cases(ctx, port):  # test_optimizer.cpp:55-71, :171-186, :229-244
+    mom = d.BaseOptimizer(ctx, d.BaseConfig("momentum", lr=0.5), 2)
+    assert np.abs(mom.step([0.0, 0.0], [1.0, 1.0])).max() == 0.0  # zero gradient, zero moments
+    adamw = d.BaseOptimizer(ctx, d.BaseConfig("adamw", lr=0.1, weight_decay=0.05), 2)
+    dw = adamw.step([0.0, 0.0], [2.0, -4.0])  # pure decoupled decay
+    assert np.allclose(dw, [-0.1 * 0.05 * 2.0, 0.1 * 0.05 * 4.0], rtol=1e-6, atol=0)
+    # admm_deltas(pi = 0, sigma = 0) == fosi_deltas
+    H = random_symmetric(port, 8, 99)
+    w_, U = np.linalg.eigh(H)
+    idx = [int(np.argmax(w_)), int(np.argsort(-w_)[1]), int(np.argmin(w_))]
+    ese = d.EseResult.from_host(ctx, w_[idx], U[:, idx])
+    g, w = port.rng_normal(98, 8), port.rng_normal(97, 8)
+    a, b = d.BaseOptimizer(ctx, d.BaseConfig("adam"), 8), d.BaseOptimizer(ctx, d.BaseConfig("adam"), 8)
+    f = d.fosi_deltas(g, ese, a, w, 0.3)
+    m = d.admm_deltas(g, np.zeros(8), ese, b, w, 0.3, 0.0)
+    assert np.abs(f.newton - m.newton).max() <= 1e-7 * np.abs(f.newton).max()
+    assert np.abs(f.base - m.base).max() <= 1e-7 * np.abs(f.base).max()
+    # the eigenvalue floor keeps the Newton step finite and the negative direction's sign
+    V = np.zeros((3, 2))
+    V[0, 0] = V[1, 1] = 1.0
+    ese = d.EseResult.from_host(ctx, [1e-12, -1e-13], V)
+    zero = d.BaseOptimizer(ctx, d.BaseConfig("sgd", lr=0.0), 3)
+    dl = d.fosi_deltas([1.0, 1.0, 1.0], ese, zero, np.zeros(3), 1.0, 1e-6)
+    assert np.isfinite(dl.newton).all() and abs(dl.newton[0]) <= 1.0 / 1e-6 + 1.0 and dl.newton[1] > 0.0
+
+
 def test_admm_round(ctx, port):
     n = 1000
     w_a, pi, w_a2 = port.rng_normal(1, n), port.rng_normal(2, n), port.rng_normal(3, n)
