@@ -164,6 +164,22 @@ def test_mlp_hvp_linear_symmetric(ctx, port):  # test_oracle.cpp:107-132
     assert abs(u @ hv - v @ hu) <= 1e-4 * max(1.0, abs(u @ hv))
 
 
+def test_mlp_pure_and_zero_case(ctx):  # test_oracle.cpp:68-79 and :152-160
+    from paper_2505_00982_b200.config import synthetic_dataset
+    data = synthetic_dataset("two-gaussians", 40, 23)
+    mlp = d.MlpOracle(ctx, [2, 8, 2], "relu", "softmax_ce")
+    w = mlp.init_params(9)
+    b = d.Batch(data.features, data.labels, 2)
+    g1, g2 = mlp.grad(w, b), mlp.grad(w, b)
+    assert (g1 == g2).all()  # repeated calls are bitwise identical
+    v = np.linspace(-1.0, 1.0, w.size)
+    assert (mlp.hvp(w, v, b) == mlp.hvp(w, v, b)).all()
+    z = d.MlpOracle(ctx, [2, 4, 1], "tanh", "mse")
+    bz = d.Batch(np.array([[1.0, 2.0], [-1.0, 0.5], [0.0, 3.0]]), np.zeros(3), 0)
+    wz = np.zeros(z.dim())
+    assert z.value(wz, bz) == 0.0 and np.abs(z.grad(wz, bz)).max() == 0.0
+
+
 def test_mlp_argument_errors(ctx):
     with pytest.raises(d.ArgumentError):
         d.MlpOracle(ctx, [2, 2])
