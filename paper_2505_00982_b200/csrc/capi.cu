@@ -139,6 +139,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
+    else if (k == "hvp_route") ctx->hvp_route = (int)value;
     else if (k == "upd_p2_variant") ctx->upd_p2_variant = (int)value;
     else if (k == "gemm_pdl") {
       ctx->gemm_pdl = (int)value;

@@ -61,8 +61,15 @@ __device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float 
   float v;
   if (e.mode == EPI_STORE) {
     v = e.alpha * acc;
-    if (e.bias_out && col == e.N - 1) e.bias_out[row] = v;
-    else e.C[(size_t)row * e.ldc + col] = v;
+    if (e.route) {
+      const long long flat = e.route_flat0 + (long long)row * e.ldc + col;
+      const long long q = flat / e.route_base;
+      e.route[q][e.route_rank * e.route_base + (flat - q * e.route_base)] = v;
+    } else if (e.bias_out && col == e.N - 1) {
+      e.bias_out[row] = v;
+    } else {
+      e.C[(size_t)row * e.ldc + col] = v;
+    }
     return 0.f;
   }
   if (e.mode == EPI_FWD || e.mode == EPI_FWD_OUT) {
@@ -179,6 +186,24 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
   if (MODE == EPI_STORE) {
     const int row = row0 + lane;
     if (row >= e.M) return;
+    if (e.route) {  // fused reduce-scatter: each element straight into its owner's slot for this rank
+      const long long f0 = e.route_flat0 + (long long)row * e.ldc + col0;
+      long long q = f0 / e.route_base;
+      long long edge = (q + 1) * e.route_base;  // a 16-element run crosses at most one shard edge
+      float* dst = e.route[q] + e.route_rank * e.route_base - q * e.route_base;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (col0 + j >= e.N) break;
+        const long long f = f0 + j;
+        if (f >= edge) {
+          ++q;
+          edge += e.route_base;
+          dst = e.route[q] + e.route_rank * e.route_base - q * e.route_base;
+        }
+        dst[f] = e.alpha * acc[j];
+      }
+      return;
+    }
     float* c = e.C + (size_t)row * e.ldc + col0;
     if (!e.bias_out && col0 + 16 <= e.N && (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
 #pragma unroll

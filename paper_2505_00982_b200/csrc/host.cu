@@ -417,6 +417,12 @@ __global__ void ordered_sum_kernel(const double* __restrict__ all, double* __res
 }
 }  // namespace
 
+void dho2g_ctx::barrier() {
+  if (world == 1) return;
+  barrier_buf.ensure(1 + (size_t)world);
+  allgather_f64(barrier_buf.p, barrier_buf.p + 1, 1, "barrier");
+}
+
 void dho2g_ctx::allreduce_sum_f64_ordered(double* inout, size_t count) {
   if (world == 1 && !nccl_force) return;
   gather_f64.ensure(count * world);

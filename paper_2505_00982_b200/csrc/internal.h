@@ -51,6 +51,8 @@ struct dho2g_ctx {
   int lanczos_recurrence = 1;  // Lanczos: recurrence-first projection (1) or the reference's plain CGS (0)
   int gemm_pdl = 1;      // CTA-pair GEMMs launched with programmatic dependent launch (prologue overlaps the
                          // previous kernel's tail)
+  int hvp_route = 0;      // world > 1: batch-split HVP partials stored straight into the owners' buffers
+                         // (peer memory) instead of a reduce-scatter after the HVP
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
@@ -96,6 +98,8 @@ struct dho2g_ctx {
   void allgather_f32(const float* send, float* recv, size_t count, const char* op = "all_gather");
   void reduce_scatter_f32(const float* send, float* recv, size_t count);
   void allreduce_sum_f64_ordered(double* inout, size_t count);  // all_gather + rank-ordered sum
+  void barrier();  // stream-ordered: returns on each rank's stream once every rank's prior work is done
+  dho2g::DevBuf<double> barrier_buf;
   // Communication ledger (CommLedger, collectives.hpp:55-83): one row per collective this rank took
   // part in (world > 1 only: a single GPU communicates nothing). floats = the round's logical result
   // length; sent / received model ring traffic of this rank, in floats.
@@ -168,6 +172,10 @@ struct dho2g_mlp {
   const float* v_scale_ptr = nullptr;  // device scalar multiplying the direction (lazy Lanczos norm)
   const void* input_owner = nullptr;   // operator whose curvature batch is packed at level 0
   const float* prepared = nullptr;     // w whose v-independent HVP quantities are cached
+  // fused HVP -> reduce-scatter: the weight-block GEMMs store straight into the owners' receive slots
+  float* const* route = nullptr;
+  long long route_base = 0;
+  int route_rank = 0;
 
   void ensure_batch(size_t B);
   ~dho2g_mlp() {
@@ -227,6 +235,13 @@ struct Epi {
   bf16* Tl;
   int ldT, Bp, hT;
   float* csum;  // optional: per 32-row block column sums of the epilogue values, [ceil(M/32)][N]
+  // EPI_STORE routed to the owning ranks (fused GEMM -> reduce-scatter over peer memory): element
+  // (row, col) has flat index route_flat0 + row*ldc + col; its owner q = flat / route_base receives it at
+  // route[q][route_rank * route_base + flat - q * route_base]. C is unused when route is set.
+  float* const* route;
+  long long route_flat0;
+  long long route_base;
+  int route_rank;
 };
 // One GEMM operand: a (hi, lo) bf16 pair buffer read through a TMA-style window. K-major: rows are
 // the M (or N) index, K contiguous; MN-major: rows are the K index, M (or N) contiguous. The K range
@@ -270,6 +285,13 @@ struct dho2g_op {
   const float* yptr = nullptr;
   dho2g::DevBuf<int64_t> idx;
   dho2g::DevBuf<float> hfull;  // full-length partial (padded to world * base)
+  // fused HVP -> reduce-scatter (ctx option hvp_route, world > 1): this rank's receive buffer (one
+  // base-long slot per sender), the device table of every rank's receive buffer, IPC-opened peers
+  dho2g::DevBuf<float> recv;
+  dho2g::DevBuf<float*> route_tab;
+  std::vector<void*> ipc_opened;
+  void route_setup(size_t base);
+  ~dho2g_op();
   // kind 4: this rank's columns of Q^T and Q (n x rows each, column-major), spec in `mat`, and the
   // intermediate y = spec o (Q v) (own rows, then all-gathered to world * ceil(n/G))
   dho2g::DevBuf<float> qrot_t, qrot, qy, qy_loc;

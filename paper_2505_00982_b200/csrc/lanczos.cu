@@ -27,6 +27,7 @@
 // The launch sequence is fixed (safeguard passes and post-breakdown iterations are predicated on
 // device flags), so the whole refresh needs no host round trip.
 #include <cmath>
+#include <cstring>
 
 #include "internal.h"
 
@@ -423,6 +424,27 @@ __global__ void __launch_bounds__(1024) dot_one_cta_kernel(const float* __restri
   if (threadIdx.x == 0) out[0] = scale * t;
 }
 
+// ------------------------------------------------------------------ fused HVP -> reduce-scatter helpers
+// (the weight-block GEMM epilogues store their elements into the owners' receive slots directly; these
+// move the rest: bias blocks, an empty batch slice's zeros, and each owner's ordered sum of its slots)
+__global__ void route_copy_kernel(const float* __restrict__ src, long long flat0, long long count,
+                                  float* const* __restrict__ route, long long base, int rank) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    const long long f = flat0 + i;
+    const long long q = f / base;
+    route[q][rank * base + (f - q * base)] = src ? src[f] : 0.f;
+  }
+}
+
+__global__ void slot_sum_kernel(const float* __restrict__ recv, long long base, int world, long long rows,
+                                float* __restrict__ h) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+    float s = recv[r];
+    for (int q = 1; q < world; ++q) s += recv[(long long)q * base + r];  // ascending rank order
+    h[r] = s;
+  }
+}
+
 // ------------------------------------------------------------------ tridiagonal eigensolve
 // Single CTA, fp64 implicit-shift QL (linalg.cpp:140-226). Thread 0 runs the scalar recurrence
 // of each sweep and records its Givens rotations; every thread then applies the sweep's
@@ -711,7 +733,8 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
   cudaStream_t st = ctx->stream;
   if (kind == 0) {
     dho2g_mlp* m = mlp;
-    if (m->w_cur != wptr || !weights_loaded || m->input_owner != this) {
+    // a rank whose slice of the curvature batch is empty (B < G) contributes zeros and runs no HVP
+    if (b1 > b0 && (m->w_cur != wptr || !weights_loaded || m->input_owner != this)) {
       if (idx.p) mlp_set_input(m, Xptr, yptr, idx.p + b0, b1 - b0, true);
       else mlp_set_input(m, Xptr + b0 * m->sizes[0], yptr + b0, nullptr, b1 - b0, true);
       mlp_load_weights(m, wptr);
@@ -719,6 +742,36 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
       weights_loaded = true;
     }
     float* out = ctx->world == 1 ? h_shard : hfull.p;
+    if (ctx->world > 1 && ctx->hvp_route) {
+      // fused reduce-scatter: the weight-block GEMMs write every W element straight into its owner's
+      // receive slot for this rank (peer memory); bias blocks and an empty slice are routed by copies;
+      // after a barrier each owner sums its slots in rank order
+      route_setup(base);
+      const int G = ctx->world;
+      const int g = grid_for(ctx, n, 256);
+      if (b1 > b0) {
+        m->route = route_tab.p;
+        m->route_base = (long long)base;
+        m->route_rank = ctx->rank;
+        try {
+          mlp_hvp_dev(m, vfull, vscale, b1 - b0, ncls, scale, out);
+        } catch (...) {
+          m->route = nullptr;
+          throw;
+        }
+        m->route = nullptr;
+        for (const LayerDesc& ld : m->layers)
+          route_copy_kernel<<<grid_for(ctx, ld.out, 256), 256, 0, st>>>(out, (long long)ld.b_off, ld.out, route_tab.p,
+                                                                     (long long)base, ctx->rank);
+      } else {
+        route_copy_kernel<<<g, 256, 0, st>>>(nullptr, 0, (long long)n, route_tab.p, (long long)base, ctx->rank);
+      }
+      DHO2G_LAUNCH();
+      ctx->barrier();  // every rank's stores into this rank's slots are complete
+      slot_sum_kernel<<<grid_for(ctx, rows, 256), 256, 0, st>>>(recv.p, (long long)base, G, (long long)rows, h_shard);
+      DHO2G_LAUNCH();
+      return;
+    }
     if (b1 > b0) {
       mlp_hvp_dev(m, vfull, vscale, b1 - b0, ncls, scale, out);
     } else {
@@ -769,6 +822,58 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
   for (size_t r = 0; r < rows; ++r) pin.p[r] = (float)hv_out[begin + r];
   DHO2G_CUDA(cudaMemcpyAsync(h_shard, pin.p, rows * sizeof(float), cudaMemcpyHostToDevice, st));
   DHO2G_CUDA(cudaStreamSynchronize(st));
+}
+
+// Receive buffer (world slots of base floats) and the table of every rank's buffer: raw pointers on the
+// in-process fabric (one address space), CUDA IPC handles exchanged through the communicator otherwise
+// (peer access over NVLink).
+void dho2g_op::route_setup(size_t base) {
+  const int G = ctx->world;
+  if (recv.p && recv.n >= base * G && route_tab.p) return;
+  recv.alloc(base * G);
+  route_tab.alloc(G);
+  std::vector<float*> tab(G, nullptr);
+  dho2g::DevBuf<double> ex(16 * (size_t)(G + 1));
+  if (ctx->fabric) {
+    double mine;
+    const float* p = recv.p;
+    std::memcpy(&mine, &p, sizeof(mine));
+    DHO2G_CUDA(cudaMemcpyAsync(ex.p, &mine, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->allgather_f64(ex.p, ex.p + 16, 1, "all_gather");
+    std::vector<double> all(G);
+    DHO2G_CUDA(cudaMemcpyAsync(all.data(), ex.p + 16, G * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    dho2g::wait_stream(ctx, ctx->stream);
+    for (int q = 0; q < G; ++q) std::memcpy(&tab[q], &all[q], sizeof(float*));
+  } else {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    DHO2G_CUDA(cudaIpcGetMemHandle(&h, recv.p));
+    double mine[8];
+    std::memcpy(mine, &h, 64);
+    DHO2G_CUDA(cudaMemcpyAsync(ex.p, mine, 64, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->allgather_f64(ex.p, ex.p + 16, 8, "all_gather");
+    std::vector<double> all(8 * (size_t)G);
+    DHO2G_CUDA(cudaMemcpyAsync(all.data(), ex.p + 16, all.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    dho2g::wait_stream(ctx, ctx->stream);
+    for (int q = 0; q < G; ++q) {
+      if (q == ctx->rank) {
+        tab[q] = recv.p;
+        continue;
+      }
+      cudaIpcMemHandle_t hq;
+      std::memcpy(&hq, &all[8 * (size_t)q], 64);
+      void* ptr = nullptr;
+      DHO2G_CUDA(cudaIpcOpenMemHandle(&ptr, hq, cudaIpcMemLazyEnablePeerAccess));
+      ipc_opened.push_back(ptr);
+      tab[q] = static_cast<float*>(ptr);
+    }
+  }
+  DHO2G_CUDA(cudaMemcpyAsync(route_tab.p, tab.data(), G * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
+  dho2g::wait_stream(ctx, ctx->stream);
+}
+
+dho2g_op::~dho2g_op() {
+  for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
 }
 
 namespace dho2g {

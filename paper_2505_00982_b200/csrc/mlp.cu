@@ -466,6 +466,12 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.C = out + ld.w_off;
       e.ldc = ld.in;
       e.alpha = 1.0f;
+      if (m->route) {  // fused reduce-scatter (dho2g_op::apply, hvp_route)
+        e.route = m->route;
+        e.route_flat0 = (long long)ld.w_off;
+        e.route_base = m->route_base;
+        e.route_rank = m->route_rank;
+      }
       auto weight_and_bias = [&]() {
         if (csum_level == j) {
           const int slot = ctx->kt_begin();
