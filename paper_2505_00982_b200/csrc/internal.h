@@ -291,6 +291,11 @@ struct dho2g_op {
   dho2g::DevBuf<float*> route_tab;
   std::vector<void*> ipc_opened;
   void route_setup(size_t base);
+  // fused reduce-scatter around any MLP pass that writes a full-length partial (HVP, gradient):
+  // route_begin arms the weight-block GEMM epilogues of `mlp`; route_end routes the bias blocks of `full`
+  // (or zeros when this rank computed nothing), runs the barrier and sums this rank's slots into `shard`
+  void route_begin(size_t base);
+  void route_end(const float* full, bool empty, float* shard, size_t rows, size_t base);
   ~dho2g_op();
   // kind 4: this rank's columns of Q^T and Q (n x rows each, column-major), spec in `mat`, and the
   // intermediate y = spec o (Q v) (own rows, then all-gathered to world * ceil(n/G))

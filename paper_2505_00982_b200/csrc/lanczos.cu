@@ -746,30 +746,16 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
       // fused reduce-scatter: the weight-block GEMMs write every W element straight into its owner's
       // receive slot for this rank (peer memory); bias blocks and an empty slice are routed by copies;
       // after a barrier each owner sums its slots in rank order
-      route_setup(base);
-      const int G = ctx->world;
-      const int g = grid_for(ctx, n, 256);
       if (b1 > b0) {
-        m->route = route_tab.p;
-        m->route_base = (long long)base;
-        m->route_rank = ctx->rank;
+        route_begin(base);
         try {
           mlp_hvp_dev(m, vfull, vscale, b1 - b0, ncls, scale, out);
         } catch (...) {
           m->route = nullptr;
           throw;
         }
-        m->route = nullptr;
-        for (const LayerDesc& ld : m->layers)
-          route_copy_kernel<<<grid_for(ctx, ld.out, 256), 256, 0, st>>>(out, (long long)ld.b_off, ld.out, route_tab.p,
-                                                                     (long long)base, ctx->rank);
-      } else {
-        route_copy_kernel<<<g, 256, 0, st>>>(nullptr, 0, (long long)n, route_tab.p, (long long)base, ctx->rank);
       }
-      DHO2G_LAUNCH();
-      ctx->barrier();  // every rank's stores into this rank's slots are complete
-      slot_sum_kernel<<<grid_for(ctx, rows, 256), 256, 0, st>>>(recv.p, (long long)base, G, (long long)rows, h_shard);
-      DHO2G_LAUNCH();
+      route_end(out, b1 <= b0, h_shard, rows, base);
       return;
     }
     if (b1 > b0) {
@@ -870,6 +856,32 @@ void dho2g_op::route_setup(size_t base) {
   }
   DHO2G_CUDA(cudaMemcpyAsync(route_tab.p, tab.data(), G * sizeof(float*), cudaMemcpyHostToDevice, ctx->stream));
   dho2g::wait_stream(ctx, ctx->stream);
+}
+
+void dho2g_op::route_begin(size_t base) {
+  route_setup(base);
+  mlp->route = route_tab.p;
+  mlp->route_base = (long long)base;
+  mlp->route_rank = ctx->rank;
+}
+
+void dho2g_op::route_end(const float* full, bool empty, float* shard, size_t rows, size_t base) {
+  cudaStream_t st = ctx->stream;
+  route_setup(base);
+  mlp->route = nullptr;
+  if (!empty) {
+    for (const LayerDesc& ld : mlp->layers)
+      route_copy_kernel<<<grid_for(ctx, ld.out, 256), 256, 0, st>>>(full, (long long)ld.b_off, ld.out, route_tab.p,
+                                                                 (long long)base, ctx->rank);
+  } else {
+    route_copy_kernel<<<grid_for(ctx, n, 256), 256, 0, st>>>(nullptr, 0, (long long)n, route_tab.p, (long long)base,
+                                                          ctx->rank);
+  }
+  DHO2G_LAUNCH();
+  ctx->barrier();  // every rank's stores into this rank's slots are complete
+  slot_sum_kernel<<<grid_for(ctx, rows, 256), 256, 0, st>>>(recv.p, (long long)base, ctx->world, (long long)rows,
+                                                            shard);
+  DHO2G_LAUNCH();
 }
 
 dho2g_op::~dho2g_op() {

@@ -268,9 +268,11 @@ struct dho2g_trainer {
       ctx->kt_end(ph, "phase.grad", 0.0);
       return;
     }
+    const bool routed = ctx->world > 1 && ctx->hvp_route;  // fused gradient reduce-scatter (peer memory)
     if (B_local > 0) {
       const int q = pf.th.joinable() ? prefetched(perm_epoch, round) : -1;
       mlp_load_weights(mlp, w_a_full.p);
+      if (routed) op.route_begin(base);
       if (q >= 0 && pf.rows[q] == B_local) {  // batch staged on the device by the previous step
         DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, pf.copied[q], 0));
         mlp_grad_dev(mlp, w_a_full.p, pf.dx[q].p, pf.dy[q].p, nullptr, B_local, ncls, scale, g_full.p);
@@ -281,10 +283,11 @@ struct dho2g_trainer {
         if (host_resident) h2d_bytes += (double)B_local * (D + 1) * sizeof(float);
       }
       mlp_loss_sum(mlp, B_local, stepacc.p);
-    } else {
+    } else if (!routed) {
       DHO2G_CUDA(cudaMemsetAsync(g_full.p, 0, n * sizeof(float), ctx->stream));
     }
-    if (ctx->world > 1) ctx->reduce_scatter_f32(g_full.p, g_shard, base);
+    if (routed) op.route_end(g_full.p, B_local == 0, g_shard, rows, base);
+    else if (ctx->world > 1) ctx->reduce_scatter_f32(g_full.p, g_shard, base);
     ctx->kt_end(ph, "phase.grad", 0.0);
   }
 

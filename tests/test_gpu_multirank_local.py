@@ -220,3 +220,26 @@ def test_fused_hvp_reduce_scatter(world, B):
         assert np.abs(dg - d1).max() <= 5e-5 * np.abs(d1).max() and np.abs(of - o1).max() <= 5e-5 * np.abs(o1).max()
         assert np.abs(dg - dp).max() <= 5e-5 * np.abs(d1).max()
         assert "reduce_scatter" not in ops and "barrier" in ops and "reduce_scatter" in ops_plain
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_trainer_fused_reduce_scatter(world):
+    """hvp_route = 1 for the whole trainer: the refresh's HVPs and every step's gradient store their partials
+    straight into the owners' slots (no reduce-scatter); the trajectory matches the 1-rank run."""
+    from oracle.bindings import blobs_dataset
+    sizes = [20, 16, 12, 5]
+    X, y = blobs_dataset(160, 20, 5, seed=7)
+
+    def fn(c, rank):
+        c.set_option("hvp_route", 1)
+        mlp = d.MlpOracle(c, sizes)
+        cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig("adamw"), k=3, l=1, outer_rounds=2, inner_epochs=2,
+                              batch_size=8, curvature_batch=40, seed=21)
+        res = d.train(c, cfg, mlp, d.Dataset(X, y, 5, 7), mlp.init_params(2), workers=4)
+        return res.w_final, res.loss, {r[1] for r in c.ledger()}
+
+    (w1, l1, _), = run_ranks(1, fn)
+    for w, loss, ops in run_ranks(world, fn):
+        assert "reduce_scatter" not in ops and "barrier" in ops
+        assert np.linalg.norm(w - w1) / np.linalg.norm(w1) <= 1e-5
+        assert np.abs(loss - l1).max() <= 1e-4 * np.abs(l1).max()
