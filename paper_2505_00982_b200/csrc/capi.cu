@@ -1125,7 +1125,11 @@ int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err) {
     if (ctx->world != 1 || ctx->comm) fail(DHO2G_ARGUMENT, "test_collectives: needs a context without a communicator");
     ncclUniqueId id;
     DHO2G_NCCLCHK(dho2g::nccl().GetUniqueId(&id));
-    DHO2G_NCCLCHK(dho2g::nccl().CommInitRank(&ctx->comm, 1, id, 0));
+    // the same non-blocking communicator dho2g_comm_init creates (collectives may return ncclInProgress)
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    dho2g::nccl_call(ctx, dho2g::nccl().CommInitRankConfig(&ctx->comm, 1, id, 0, &cfg), "comm_init");
+    dho2g::nccl_settle(ctx, "comm_init");
     ctx->nccl_force = true;
     double err = 0.0;
     try {
@@ -1160,14 +1164,15 @@ int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err) {
       DHO2G_CUDA(cudaMemcpyAsync(od.data(), e.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
       DHO2G_CUDA(cudaStreamSynchronize(st));
       for (size_t i = 0; i < n; ++i) err = std::max(err, std::fabs(od[i] - hd[i]));
+      ctx->sync();  // the polled wait of a context with a communicator
     } catch (...) {
       ctx->nccl_force = false;
-      dho2g::nccl().CommDestroy(ctx->comm);
+      if (ctx->comm) dho2g::nccl().CommAbort(ctx->comm);
       ctx->comm = nullptr;
       throw;
     }
     ctx->nccl_force = false;
-    DHO2G_NCCLCHK(dho2g::nccl().CommDestroy(ctx->comm));
+    dho2g::nccl().CommAbort(ctx->comm);  // non-blocking communicator: abort releases it at once
     ctx->comm = nullptr;
     *max_err = err;
   });
