@@ -45,12 +45,13 @@ def lanczos_cell(ctx, n, k, hbm):
     gs_ms = sum(v[0] for kk, v in ks.items() if kk.startswith("gs_"))
     gs_b = sum(v[2] for kk, v in ks.items() if kk.startswith("gs_"))
     rz = ks.get("extract.ritz", (0.0, 0, 0.0))
+    tq = ks.get("extract.tql2", (0.0, 0, 0.0))
     ese.close()
     st.close()
     op.close()
     gbs = gs_b / (gs_ms / 1e3) / 1e9
     return (f"lanczos n={n:>11,d} k={k:>3d} m={m:>3d}: refresh {ms:9.1f} ms  GS {gs_ms:9.1f} ms {gbs:7.0f} GB/s "
-            f"({gbs / hbm:.2f} of HBM)  ritz {rz[0]:7.1f} ms")
+            f"({gbs / hbm:.2f} of HBM)  ritz {rz[0]:7.1f} ms  eig {tq[0]:6.1f} ms")
 
 
 def hvp_cell(ctx, H, tf_peak):
