@@ -65,8 +65,8 @@ struct dho2g_ctx {
   int use_graphs = 1;     // capture the Lanczos refresh into a CUDA graph (world 1)
   int gs_sm_cap = 0;     // Gram-Schmidt grids sized for at most this many SMs (0: all; experiments)
   int ritz_tc = 1;        // Ritz vectors on the tensor cores when supported (0: CUDA-core kernel)
-  int tql2_split = -1;    // eigensolve: 1 QL chain, shared-memory rotation replay, selection; 0 single-CTA tql2;
-                          // -1 split from m = 192 (measured: 0.9x at m <= 128, 1.3x at 512, 1.7x at 1000)
+  int tql2_split = 1;     // eigensolve: 1 QL chain with a concurrent shared-memory rotation replay, then
+                          // selection (1.3x at m = 40-80, 2.0x at 512, 2.7x at 1000); 0 single-CTA tql2
   int upd_p2_staged = 1;  // update pass 2: 1 bulk-copy staged (R <= 48), 0 register-staged
   int upd_p2_variant = 5; // staged pass 2: 5 row-dot (R <= 32, else 0), 0 256-row x2 stages x2 CTAs/SM +
                           // column-dot phase, 1 128x2x4, 2 128x3x3, 3 128x4x2, 4 512x2x1

@@ -510,13 +510,14 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
                 under = true;
                 break;
               }
+              const double gb2 = 2.0 * g * b;  // 2 c b = (2 g b) / r: off the rsqrt's critical path
               const double ir = rsqrt(h2);
               r = h2 * ir;
               e[ii + 1] = r;
               s = f * ir;
               c = g * ir;
               g = dk - p;
-              r = (dn - g) * s + 2.0 * c * b;
+              r = fma(dn - g, s, gb2 * ir);
               p = s * r;
               d[ii + 1] = g + p;
               g = c * r - b;
@@ -586,141 +587,182 @@ __global__ void tql2_kernel(const LzDev* st, int n, int keff, int leff, double* 
   if (tid == 0) *status = 0;
 }
 
-// Split form of tql2_kernel (ctx option tql2_split, default): the same QL sweeps and rotations, the
-// rotation stream decoupled from its application. Every component k of the eigenvector slots is
-// rotated independently of the others, so the application needs no synchronisation with the scalar
-// chain once the stream is recorded:
-//   tql2_ql_kernel     one warp: the implicit-shift QL chain (linalg.cpp:140-197) with a warp-ballot
-//                      scan for the negligible off-diagonal; writes each sweep's (mm, cnt, offset) and
-//                      its rotations (c, s) to a log in HBM (worst case 30 n (n-1) rotations: at most
-//                      60 sweeps per l before the reference's iteration limit fires).
-//   tql2_apply_kernel  ceil(n / T) CTAs of T threads; thread t owns component k = blockIdx * T + t of
-//                      all n slots in shared memory (n * T * 8 bytes) and replays the log with the
-//                      register-carried rotation order of tql2_kernel (bit-identical arithmetic).
+// Split form of tql2_kernel (ctx option tql2_split): the same QL sweeps and rotations, with the
+// rotation stream decoupled from its application. Every component k of the eigenvector slots is rotated
+// independently of the others, so the application only has to follow the recorded stream:
+//   tql2_pipe_kernel   1 + ceil(n / T) CTAs of 32 threads. The first CTA to start (ticket 0) is the
+//                      producer: one warp runs the implicit-shift QL chain (linalg.cpp:140-197) with a
+//                      warp-ballot deflation scan and appends each sweep's (mm, cnt, offset) and its
+//                      rotations (c, s) to a log in HBM (worst case 30 n (n-1) rotations: at most 60
+//                      sweeps per l before the reference's iteration limit), publishing the sweep count
+//                      with st.release every >= 256 rotations. Every other CTA is a consumer: lane t < T
+//                      owns component k of all n slots in shared memory (n * T * 8 bytes), stages each
+//                      published sweep's rotations into shared memory (coalesced L2 loads, all lanes) and
+//                      replays them with the register-carried order of tql2_kernel (same arithmetic).
+//                      The producer never waits on a consumer and is the first CTA running, so the spin
+//                      cannot deadlock; the replay overlaps the chain and trails it by one batch.
 //   tql2_select_kernel stable ascending order, extreme selection and U' (as the tail of tql2_kernel).
-// The single-CTA kernel serialises the chain with an L2-bound application per sweep (512 threads x
-// 16 B per rotation through one SM's L2 port at m = 512); here the application runs from shared
-// memory on n / T SMs after the chain, which bounds the eigensolve by the chain alone.
-__global__ void __launch_bounds__(32) tql2_ql_kernel(const LzDev* st, int n, double2* __restrict__ rot,
-                                                     int4* __restrict__ sweep, int* __restrict__ nsweep,
-                                                     double* __restrict__ dout, int* __restrict__ status) {
-  extern __shared__ double sh[];
-  double* d = sh;
-  double* e = d + n;
-  const int lane = threadIdx.x;
-  for (int i = lane; i < n; i += 32) {
-    d[i] = st->diag[i];
-    e[i] = (i + 1 < n) ? st->off[i] : 0.0;
-  }
-  __syncwarp();
-  const double eps = 2.220446049250313e-16;
-  int ns = 0, off = 0;
-  for (int l = 0; l < n && n > 1; ++l) {
-    int iter = 0;
-    for (;;) {
-      // first q >= l with a negligible e[q] (linalg.cpp:160-164), n - 1 if none
-      int mm = n - 1;
-      for (int q0 = l; q0 + 1 < n; q0 += 32) {
-        const int q = q0 + lane;
-        const bool hit = q + 1 < n && fabs(e[q]) <= eps * (fabs(d[q]) + fabs(d[q + 1]));
-        const unsigned b = __ballot_sync(0xffffffffu, hit);
-        if (b) {
-          mm = q0 + __ffs(b) - 1;
-          break;
-        }
-      }
-      if (mm == l) break;
-      if (iter++ == 60) {
-        if (lane == 0) *status = 1;
-        return;
-      }
-      int cnt = 0;
-      if (lane == 0) {
-        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = sqrt(fma(g, g, 1.0));
-        g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
-        double s = 1.0, c = 1.0, p = 0.0;
-        bool under = false;
-        double dk = d[mm], ek = e[mm - 1], dn = d[mm - 1];
-        double2* out = rot + off;
-        for (int ii = mm - 1; ii >= l; --ii) {
-          const double en = ii > l ? e[ii - 1] : 0.0, dnn = ii > l ? d[ii - 1] : 0.0;
-          const double f = s * ek;
-          const double b = c * ek;
-          const double h2 = fma(f, f, g * g);
-          if (h2 == 0.0) {
-            e[ii + 1] = 0.0;
-            d[ii + 1] = dk - p;
-            e[mm] = 0.0;
-            under = true;
-            break;
-          }
-          const double ir = rsqrt(h2);
-          r = h2 * ir;
-          e[ii + 1] = r;
-          s = f * ir;
-          c = g * ir;
-          g = dk - p;
-          r = (dn - g) * s + 2.0 * c * b;
-          p = s * r;
-          d[ii + 1] = g + p;
-          g = c * r - b;
-          out[cnt] = make_double2(c, s);
-          ++cnt;
-          dk = dn;
-          dn = dnn;
-          ek = en;
-        }
-        if (!under) {
-          d[l] -= p;
-          e[l] = g;
-          e[mm] = 0.0;
-        }
-        if (cnt > 0) sweep[ns] = make_int4(mm, cnt, off, 0);
-      }
-      cnt = __shfl_sync(0xffffffffu, cnt, 0);
-      if (cnt > 0) {
-        ++ns;
-        off += cnt;
-      }
-      __syncwarp();  // lane 0's d / e updates are visible to the next scan
-    }
-  }
-  for (int i = lane; i < n; i += 32) dout[i] = d[i];
-  if (lane == 0) {
-    *nsweep = ns;
-    *status = 0;
-  }
+// The single-CTA kernel alternates the chain with an L2-bound application (512 threads x 16 B per
+// rotation through one SM at m = 512); here the eigensolve costs the chain alone.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void tql2_apply_kernel(int n, const double2* __restrict__ rot, const int4* __restrict__ sweep,
-                                  const int* __restrict__ nsweep, const int* __restrict__ status,
-                                  double* __restrict__ Z) {
-  extern __shared__ double zs[];  // zs[i * T + t] = Z[i][k]: slot i, this thread's component k
-  const int T = blockDim.x, t = threadIdx.x;
-  const int k = blockIdx.x * T + t;
-  if (k >= n || *status != 0) return;  // threads touch only their own column: no block barrier below
-  for (int i = 0; i < n; ++i) zs[(size_t)i * T + t] = (i == k) ? 1.0 : 0.0;
-  const int ns = *nsweep;
-  for (int w = 0; w < ns; ++w) {
-    const int4 sw = __ldg(sweep + w);
-    const int mm = sw.x, cnt = sw.y;
-    const double2* r = rot + sw.z;
-    double f = zs[(size_t)mm * T + t];
-    double z0 = zs[(size_t)(mm - 1) * T + t];
-#pragma unroll 4
-    for (int q = 0; q < cnt; ++q) {
-      const int ii = mm - 1 - q;
-      const double zn = q + 1 < cnt ? zs[(size_t)(ii - 1) * T + t] : 0.0;
-      const double2 cs = __ldg(r + q);
-      const double c = cs.x, s = cs.y;
-      zs[(size_t)(ii + 1) * T + t] = s * z0 + c * f;
-      f = c * z0 - s * f;
-      z0 = zn;
+// sync[0] ticket, sync[1] published sweeps, sync[2] done (zeroed before the launch)
+__global__ void __launch_bounds__(32) tql2_pipe_kernel(const LzDev* st, int n, int T, double2* __restrict__ rot,
+                                                       int4* __restrict__ sweep, int* __restrict__ sync,
+                                                       double* __restrict__ dout, int* __restrict__ status,
+                                                       double* __restrict__ Z) {
+  extern __shared__ double sh[];
+  __shared__ int s_role;
+  const int lane = threadIdx.x;
+  if (lane == 0) s_role = atomicAdd(sync, 1);
+  __syncwarp();
+  const int role = s_role;
+  if (role == 0) {  // ------------------------------------------------ producer: the QL chain
+    double* d = sh;
+    double* e = d + n;
+    for (int i = lane; i < n; i += 32) {
+      d[i] = st->diag[i];
+      e[i] = (i + 1 < n) ? st->off[i] : 0.0;
     }
-    zs[(size_t)(mm - cnt) * T + t] = f;
+    __syncwarp();
+    const double eps = 2.220446049250313e-16;
+    int ns = 0, off = 0, pub = 0, fail = 0;
+    for (int l = 0; l < n && n > 1 && !fail; ++l) {
+      int iter = 0;
+      for (;;) {
+        // first q >= l with a negligible e[q] (linalg.cpp:160-164), n - 1 if none
+        int mm = n - 1;
+        for (int q0 = l; q0 + 1 < n; q0 += 32) {
+          const int q = q0 + lane;
+          const bool hit = q + 1 < n && fabs(e[q]) <= eps * (fabs(d[q]) + fabs(d[q + 1]));
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (b) {
+            mm = q0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        if (mm == l) break;
+        if (iter++ == 60) {
+          fail = 1;
+          break;
+        }
+        int cnt = 0;
+        if (lane == 0) {
+          double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+          double r = sqrt(fma(g, g, 1.0));
+          g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+          double s = 1.0, c = 1.0, p = 0.0;
+          bool under = false;
+          double dk = d[mm], ek = e[mm - 1], dn = d[mm - 1];
+          double2* out = rot + off;
+          for (int ii = mm - 1; ii >= l; --ii) {
+            const double en = ii > l ? e[ii - 1] : 0.0, dnn = ii > l ? d[ii - 1] : 0.0;
+            const double f = s * ek;
+            const double b = c * ek;
+            const double h2 = fma(f, f, g * g);
+            if (h2 == 0.0) {
+              e[ii + 1] = 0.0;
+              d[ii + 1] = dk - p;
+              e[mm] = 0.0;
+              under = true;
+              break;
+            }
+            const double gb2 = 2.0 * g * b;  // 2 c b = (2 g b) / r: off the rsqrt's critical path
+            const double ir = rsqrt(h2);
+            r = h2 * ir;
+            e[ii + 1] = r;
+            s = f * ir;
+            c = g * ir;
+            g = dk - p;
+            r = fma(dn - g, s, gb2 * ir);
+            p = s * r;
+            d[ii + 1] = g + p;
+            g = c * r - b;
+            out[cnt] = make_double2(c, s);
+            ++cnt;
+            dk = dn;
+            dn = dnn;
+            ek = en;
+          }
+          if (!under) {
+            d[l] -= p;
+            e[l] = g;
+            e[mm] = 0.0;
+          }
+          if (cnt > 0) {
+            sweep[ns] = make_int4(mm, cnt, off, 0);
+            if (off + cnt - pub >= 256) {  // batch the publications (each release drains the stores)
+              st_release_gpu(sync + 1, ns + 1);
+              pub = off + cnt;
+            }
+          }
+        }
+        cnt = __shfl_sync(0xffffffffu, cnt, 0);
+        if (cnt > 0) {
+          ++ns;
+          off += cnt;
+        }
+        __syncwarp();  // lane 0's d / e updates are visible to the next scan
+      }
+    }
+    for (int i = lane; i < n; i += 32) dout[i] = d[i];
+    if (lane == 0) {
+      *status = fail;
+      st_release_gpu(sync + 1, ns);
+      st_release_gpu(sync + 2, 1);
+    }
+    return;
   }
-  for (int i = 0; i < n; ++i) Z[(size_t)i * n + k] = zs[(size_t)i * T + t];
+  // ------------------------------------------------------------------ consumer: replay the log
+  double* zs = sh;                                              // zs[i * T + t]: slot i, component k
+  double2* stage = reinterpret_cast<double2*>(zs + (size_t)n * T);  // one sweep's rotations
+  const int k = (role - 1) * T + lane;
+  const bool own = lane < T && k < n;
+  if (own)
+    for (int i = 0; i < n; ++i) zs[(size_t)i * T + lane] = (i == k) ? 1.0 : 0.0;
+  int w = 0;
+  for (;;) {
+    int avail = ld_acquire_gpu(sync + 1);
+    if (w >= avail) {
+      if (!ld_acquire_gpu(sync + 2)) {
+        __nanosleep(128);
+        continue;
+      }
+      avail = ld_acquire_gpu(sync + 1);  // final count (released before done)
+      if (w >= avail) break;
+    }
+    for (; w < avail; ++w) {
+      const int4 sw = __ldcg(sweep + w);
+      const int mm = sw.x, cnt = sw.y;
+      for (int q = lane; q < cnt; q += 32) stage[q] = __ldcg(rot + sw.z + q);
+      __syncwarp();
+      if (own) {
+        double f = zs[(size_t)mm * T + lane];
+        double z0 = zs[(size_t)(mm - 1) * T + lane];
+#pragma unroll 4
+        for (int q = 0; q < cnt; ++q) {
+          const int ii = mm - 1 - q;
+          const double zn = q + 1 < cnt ? zs[(size_t)(ii - 1) * T + lane] : 0.0;
+          const double2 cs = stage[q];
+          const double c = cs.x, s = cs.y;
+          zs[(size_t)(ii + 1) * T + lane] = s * z0 + c * f;
+          f = c * z0 - s * f;
+          z0 = zn;
+        }
+        zs[(size_t)(mm - cnt) * T + lane] = f;
+      }
+      __syncwarp();  // the stage is rewritten by the next sweep
+    }
+  }
+  if (own)
+    for (int i = 0; i < n; ++i) Z[(size_t)i * n + k] = zs[(size_t)i * T + lane];
 }
 
 __global__ void tql2_select_kernel(const LzDev* st, int n, int keff, int leff, const double* __restrict__ dall,
@@ -1308,26 +1350,29 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   const int threads = (int)std::min<size_t>(1024, round_up((size_t)me, 32));
   const int kx = ctx->kt_begin();
   const int kq = ctx->kt_begin();
-  if (ctx->tql2_split > 0 || (ctx->tql2_split < 0 && me >= 192)) {
-    // log capacity: at most 60 sweeps per l, each of at most n - 1 - l rotations (tql2_ql_kernel)
+  if (ctx->tql2_split) {
+    // log capacity: at most 60 sweeps per l, each of at most n - 1 - l rotations (tql2_pipe_kernel)
     const size_t cap = std::max<size_t>(1, (size_t)30 * me * (me - 1));
     lz->xrot.ensure(cap);
     lz->xsweep.ensure((size_t)60 * me + 1);
-    lz->xnsweep.ensure(1);
+    lz->xnsweep.ensure(4);
     lz->xd.ensure(me);
-    tql2_ql_kernel<<<1, 32, (size_t)me * 2 * sizeof(double), st>>>(lz->st.p, me, lz->xrot.p, lz->xsweep.p,
-                                                                    lz->xnsweep.p, lz->xd.p, status.p);
+    DHO2G_CUDA(cudaMemsetAsync(lz->xnsweep.p, 0, 4 * sizeof(int), st));
+    const int T = me <= 800 ? 32 : 16;  // consumer: n * T * 8 bytes of slots + n * 16 bytes of staging
+    const size_t sp = std::max((size_t)me * T * sizeof(double) + (size_t)me * sizeof(double2),
+                               (size_t)me * 2 * sizeof(double));
+    if (sp > 48 * 1024)
+      DHO2G_CUDA(cudaFuncSetAttribute(tql2_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
+    const int k1 = ctx->kt_begin();
+    tql2_pipe_kernel<<<(unsigned)(1 + cdiv((size_t)me, (size_t)T)), 32, sp, st>>>(
+        lz->st.p, me, T, lz->xrot.p, lz->xsweep.p, lz->xnsweep.p, lz->xd.p, status.p, Z.p);
     DHO2G_LAUNCH();
-    const int T = me <= 800 ? 32 : 16;  // n * T * 8 bytes of shared memory per CTA
-    const size_t sa = (size_t)me * T * sizeof(double);
-    if (sa > 48 * 1024)
-      DHO2G_CUDA(cudaFuncSetAttribute(tql2_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa));
-    tql2_apply_kernel<<<(unsigned)cdiv((size_t)me, (size_t)T), T, sa, st>>>(me, lz->xrot.p, lz->xsweep.p,
-                                                                           lz->xnsweep.p, status.p, Z.p);
-    DHO2G_LAUNCH();
+    ctx->kt_end(k1, "eig.pipe", 0.0);
+    const int k3 = ctx->kt_begin();
     tql2_select_kernel<<<1, threads, (size_t)me * (sizeof(double) + sizeof(int)), st>>>(
         lz->st.p, me, (int)k, (int)l, lz->xd.p, Z.p, U.p, ese->ev_dev.p, evall.p, status.p);
     DHO2G_LAUNCH();
+    ctx->kt_end(k3, "eig.select", 0.0);
   } else {
     const size_t smem = (size_t)me * 4 * sizeof(double) + (size_t)me * sizeof(int);
     if (smem > 48 * 1024)

@@ -31,11 +31,14 @@ def main():
             for _ in range(3):
                 d.extract_ese_distributed(ctx, st, k, 0)
             ctx.set_option("ktimers", 0)
-            ms, cnt, _ = ctx.kernel_stats()["extract.tql2"]
+            ks = ctx.kernel_stats()
+            ms, cnt, _ = ks["extract.tql2"]
             res[split] = ms / cnt
-        ctx.set_option("tql2_split", -1)
+            if split:
+                parts = "  ".join(f"{kk} {v[0] / v[1]:.3f}" for kk, v in sorted(ks.items()) if kk.startswith("eig."))
+        ctx.set_option("tql2_split", 1)
         print(f"tql2 m={st.iterations:5d}: single-CTA {res[0]:8.3f} ms   split {res[1]:8.3f} ms   "
-              f"({res[0] / res[1]:.1f}x)", flush=True)
+              f"({res[0] / res[1]:.1f}x)   [{parts}]", flush=True)
     ctx.close()
 
 

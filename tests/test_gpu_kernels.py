@@ -518,9 +518,9 @@ def test_ritz_tensor_core_matches_cuda_core(ctx, port, n, m, k, l):
 @pytest.mark.parametrize("n,m,k,l", [(20_000, 80, 32, 0), (9_000, 40, 10, 3), (4_096, 2, 1, 1), (60_000, 512, 128, 0),
                                      (30_000, 900, 16, 16), (3_000, 1, 1, 0)])
 def test_tql2_split_matches_single_cta(ctx, n, m, k, l):
-    """The split eigensolve (QL chain -> rotation log -> shared-memory replay -> selection) replays the
-    single-CTA tql2's rotations in the same order with the same arithmetic: eigenvalues and Ritz vectors
-    bit-identical, at m = 1 (no sweep), small m, the C4 m = 80, the C5 m = 512 and m = 900 (16-thread
+    """The split eigensolve (QL chain producing a rotation log, consumer CTAs replaying it concurrently
+    from shared memory, then selection) replays the single-CTA tql2's rotations in the same order with
+    the same arithmetic: eigenvalues and Ritz vectors bit-identical, at m = 1 (no sweep), small m, the C4 m = 80, the C5 m = 512 and m = 900 (16-column
     replay CTAs)."""
     spec = 1.0 + np.sin(np.arange(n) * 0.731) * 3.0 + (np.arange(n) % 7 == 0) * 0.5
     op = d.diagonal_operator(ctx, spec)
@@ -534,7 +534,7 @@ def test_tql2_split_matches_single_cta(ctx, n, m, k, l):
             ese = d.extract_ese_distributed(ctx, st, ke, le)
             out.append((ese.eigvals, ese.eigvecs_shard(n)))
         finally:
-            ctx.set_option("tql2_split", -1)
+            ctx.set_option("tql2_split", 1)
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
 
