@@ -168,6 +168,10 @@ int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs_shard);
 /* Build an ESE from host data (tests feed the reference's eigenpairs): V is n x r column-major. */
 int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, size_t n, size_t r,
                         dho2g_ese** out);
+/* The same from a device-resident fp32 V (column-major, leading dimension ld_src >= n); this rank's rows
+ * are copied device to device (a caller holding V_hat in HBM does not stage 13 GB through the host). */
+int dho2g_ese_from_device(dho2g_ctx* ctx, const double* eigvals, const float* V_dev, size_t ld_src, size_t n,
+                          size_t r, dho2g_ese** out);
 int dho2g_ese_destroy(dho2g_ese* ese);
 
 /* ---- update step (optimizer.hpp:16-80) ---------------------------------------------- */

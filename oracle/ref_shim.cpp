@@ -403,6 +403,63 @@ int ref_deltas_seq(const ref_base_cfg* c, std::size_t n, std::size_t r, const do
   });
 }
 
+// Parity-at-scale input generator (tests/scale_inputs.py h24_np / unif_np, same bits): a 24-bit counter
+// hash, so a 100,989,962 x 32 V_hat can be built inside this process (no second 26 GB copy) and on the
+// device by the GPU test. Values are 24-bit integers times powers of two: exact in fp32.
+static inline std::int64_t h24(std::int64_t i, std::int64_t salt) {
+  const std::int64_t M = 0xFFFFFF;
+  std::int64_t x = ((i & M) * 0x9E3779 + (i >> 24) * 0x7F4A7D + salt * 0x2545F5 + 0x1234) & M;
+  x = ((x ^ (x >> 12)) * 0x2C1B3D) & M;
+  x = ((x ^ (x >> 11)) * 0x297A2D) & M;
+  return x ^ (x >> 13);
+}
+static inline double unif24(std::int64_t i, std::int64_t salt, double scale) {
+  return static_cast<double>(h24(i, salt) - (1 << 23)) * (scale * 0x1p-23);
+}
+
+// optimizer.cpp:81-129 on hashed inputs: T consecutive admm_deltas (one BaseOptimizer, w advanced by
+// base + newton after each step as in trainer.cpp:240-241). V_hat[:, j] = unif(i, salt_v + j) * v_scale,
+// g_t = unif(i, salt_g + t) * g_scale, pi = unif(i, salt_pi) * pi_scale, w0 = unif(i, salt_w) * w_scale.
+// Returns newton_t, base_t and w after the T steps at the n_idx sampled indices, plus full-vector
+// sums of squares (norm2 per step for newton and base).
+int ref_deltas_hashed(const ref_base_cfg* c, std::size_t n, std::size_t r, const double* eigvals, int T,
+                      double alpha, double sigma, double floor, std::int64_t salt_v, double v_scale,
+                      std::int64_t salt_g, double g_scale, std::int64_t salt_pi, double pi_scale,
+                      std::int64_t salt_w, double w_scale, const std::int64_t* idx, std::size_t n_idx,
+                      double* newton_at, double* base_at, double* w_at, double* sq_newton, double* sq_base) {
+  return guarded([&] {
+    BaseOptimizer opt(base_cfg(c), n);
+    EseResult ese;
+    ese.k = r;
+    ese.eigvals.assign(eigvals, eigvals + r);
+    ese.eigvecs = TallMatrix(n, r);
+    double* V = ese.eigvecs.data().data();
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i)
+      for (std::size_t j = 0; j < r; ++j) V[j * n + i] = unif24(i, salt_v + static_cast<std::int64_t>(j), v_scale);
+    Vector wv(n), piv(n), gv(n);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i) {
+      wv[i] = unif24(i, salt_w, w_scale);
+      piv[i] = unif24(i, salt_pi, pi_scale);
+    }
+    for (int t = 0; t < T; ++t) {
+#pragma omp parallel for schedule(static)
+      for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i) gv[i] = unif24(i, salt_g + t, g_scale);
+      const Deltas d = admm_deltas(gv, piv, ese, opt, wv, alpha, sigma, floor);
+      for (std::size_t q = 0; q < n_idx; ++q) {
+        newton_at[t * n_idx + q] = d.newton[idx[q]];
+        base_at[t * n_idx + q] = d.base[idx[q]];
+      }
+      sq_newton[t] = linalg::dot(d.newton, d.newton);
+      sq_base[t] = linalg::dot(d.base, d.base);
+      linalg::axpy(1.0, d.base, wv);
+      linalg::axpy(1.0, d.newton, wv);
+    }
+    for (std::size_t q = 0; q < n_idx; ++q) w_at[q] = wv[idx[q]];
+  });
+}
+
 // optimizer.cpp:131-154
 int ref_admm_round(std::size_t n, double sigma, const double* w_a, const double* pi, double* w_out,
                    const double* w_a_after, double* pi_out) {

@@ -684,6 +684,15 @@ class EseResult:
         check(lib.dho2g_ese_from_host(ctx.h, _d(eigvals), _d(_colmajor(V)), n, r, C.byref(h)))
         return cls(ctx, h, r, 0)
 
+    @classmethod
+    def from_device(cls, ctx: Context, eigvals, V_ptr: int, ld: int, n: int, r: int):
+        """From a device-resident fp32 V (column-major, leading dimension ld, e.g. a torch tensor's
+        data_ptr()); copied device to device."""
+        eigvals = _f64(eigvals)
+        h = C.c_void_p()
+        check(lib.dho2g_ese_from_device(ctx.h, _d(eigvals), C.c_void_p(V_ptr), ld, n, r, C.byref(h)))
+        return cls(ctx, h, r, 0)
+
     def close(self):
         if self.h:
             lib.dho2g_ese_destroy(self.h)

@@ -857,6 +857,34 @@ int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, 
   });
 }
 
+// The same EseResult from a device-resident fp32 V (column-major, leading dimension ld_src >= n): this
+// rank's rows are copied device to device, so a caller that already holds V_hat in HBM (a 101 M x 32
+// basis is 13 GB) does not stage it through the host.
+int dho2g_ese_from_device(dho2g_ctx* ctx, const double* eigvals, const float* V_dev, size_t ld_src, size_t n, size_t r,
+                          dho2g_ese** out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (ld_src < n) fail(DHO2G_ARGUMENT, "ese_from_device: leading dimension < n");
+    auto e = std::make_unique<dho2g_ese>();
+    e->ctx = ctx;
+    e->n = n;
+    e->r = r;
+    shard_range(n, ctx->world, ctx->rank, &e->begin, &e->end);
+    e->rows = e->end - e->begin;
+    e->ldv = round_up(std::max<size_t>(cdiv(n, (size_t)ctx->world), 1), kGsChunk);
+    e->eigvals.assign(eigvals, eigvals + r);
+    e->sign.assign(r, 1.f);
+    e->V.alloc(e->ldv * std::max<size_t>(r, 1));
+    e->ev_dev.alloc(std::max<size_t>(r, 1));
+    if (r && e->rows)
+      DHO2G_CUDA(cudaMemcpy2DAsync(e->V.p, e->ldv * sizeof(float), V_dev + e->begin, ld_src * sizeof(float),
+                                   e->rows * sizeof(float), r, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (r) DHO2G_CUDA(cudaMemcpyAsync(e->ev_dev.p, eigvals, r * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = e.release();
+  });
+}
+
 int dho2g_ese_destroy(dho2g_ese* ese) {
   return guard([&] { delete ese; });
 }

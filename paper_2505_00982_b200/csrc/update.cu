@@ -101,28 +101,60 @@ __device__ __forceinline__ void chunk_dots(const float* __restrict__ V, size_t l
   }
 }
 
-// ---- P1: c = V^T (g + pi)
+// acc[w][j] += V_j[r0 : r0 + kCh] . xs with xs in fp64 and fp64 products: c feeds g2 = g~ - V c, which
+// cancels to ~1e-8 of |g~| on some rows, and Adam's m/sqrt(v) is steep there (slope lr/eps at |g2| ~ eps),
+// so c needs ~1e-10 relative accuracy; fp32 products over 1e8 rows give ~1e-7.
+__device__ __forceinline__ void chunk_dots_f64(const float* __restrict__ V, size_t ldv, size_t r0, int R,
+                                               const double* xs, double* acc) {
+  constexpr int kItems = kCh / kSubRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int items = R * kItems;
+  for (int it = warp; it < items; it += kW) {
+    const int j = it / kItems, q = it % kItems;
+    const int rb = q * kSubRows + lane * 4;
+    const float* col = V + (size_t)j * ldv + r0;
+    float4 x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __ldg(reinterpret_cast<const float4*>(col + rb + k * 128));
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 a = *reinterpret_cast<const double2*>(xs + rb + k * 128);
+      const double2 b = *reinterpret_cast<const double2*>(xs + rb + k * 128 + 2);
+      s0 = fma((double)x[k].x, a.x, s0);
+      s1 = fma((double)x[k].y, a.y, s1);
+      s0 = fma((double)x[k].z, b.x, s0);
+      s1 = fma((double)x[k].w, b.y, s1);
+    }
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) acc[warp * R + j] += s;
+  }
+}
+
+// ---- P1: c = V^T (g + pi), g~ formed in fp64 (optimizer.cpp:91) and fp64 products
 __global__ void __launch_bounds__(kT) upd_p1_kernel(const float* __restrict__ V, size_t ldv, int R, size_t rows,
                                                     const float* __restrict__ g, const float* __restrict__ pi,
                                                     double* part, double* rankp, unsigned* ticket) {
   extern __shared__ __align__(16) unsigned char smem[];
-  float* xs = reinterpret_cast<float*>(smem);
-  double* acc = reinterpret_cast<double*>(smem + kCh * sizeof(float));
+  double* xs = reinterpret_cast<double*>(smem);
+  double* acc = xs + kCh;
   for (int e = threadIdx.x; e < kW * R; e += kT) acc[e] = 0.0;
   const size_t nch = cdiv(rows, kCh);
   for (size_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const size_t r0 = c * kCh;
     __syncthreads();
     for (int e = threadIdx.x; e < kCh / 4; e += kT) {
-      float4 x = ld4(g, r0 + 4 * e, rows);
+      const float4 x = ld4(g, r0 + 4 * e, rows);
+      double2 a = make_double2(x.x, x.y), b = make_double2(x.z, x.w);
       if (pi) {
         const float4 p = ld4(pi, r0 + 4 * e, rows);
-        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
+        a.x += p.x; a.y += p.y; b.x += p.z; b.y += p.w;
       }
-      reinterpret_cast<float4*>(xs)[e] = x;
+      reinterpret_cast<double2*>(xs)[2 * e] = a;
+      reinterpret_cast<double2*>(xs)[2 * e + 1] = b;
     }
     __syncthreads();
-    chunk_dots(V, ldv, r0, R, xs, acc);
+    chunk_dots_f64(V, ldv, r0, R, xs, acc);
   }
   finish_partials(acc, R, part, rankp, ticket);
 }
@@ -175,12 +207,12 @@ __global__ void __launch_bounds__(kT) upd_p2_kernel(const float* __restrict__ V,
     __syncthreads();
     for (int e = threadIdx.x; e < kCh2 / 4; e += kT) {
       const size_t r = r0 + 4 * (size_t)e;
-      float4 x = ld4(g, r, rows);
-      if (pi) {
-        const float4 p = ld4(pi, r, rows);
-        x.x += p.x; x.y += p.y; x.z += p.z; x.w += p.w;
-      }
+      const float4 x = ld4(g, r, rows);
       double g0 = x.x, g1 = x.y, g2 = x.z, g3 = x.w;
+      if (pi) {  // g~ = g + pi in fp64 (optimizer.cpp:91)
+        const float4 p = ld4(pi, r, rows);
+        g0 += p.x; g1 += p.y; g2 += p.z; g3 += p.w;
+      }
       int j = 0;
       for (; j + 4 <= R; j += 4) {
         float4 d[4];
@@ -339,8 +371,10 @@ __global__ void __launch_bounds__(kT, MINB) upd_p2_tma_kernel(const __grid_const
       const size_t r = r0 + t;
       const bool in = r < rows;
       const float* ss = st + (size_t)R * CH;
-      float x = full ? ss[t] : (in ? g[r] : 0.f);
-      if (pi) x += full ? ss[CH + t] : (in ? pi[r] : 0.f);
+      // g~ = g + pi in fp64 (optimizer.cpp:91 adds in fp64): an fp32 sum rounds away bits that matter
+      // where g2 = g~ - V c nearly cancels and Adam's m/sqrt(v) is steep
+      double x = full ? ss[t] : (in ? g[r] : 0.f);
+      if (pi) x += (double)(full ? ss[CH + t] : (in ? pi[r] : 0.f));
       // four independent fp64 partial sums (short dependency chains), combined in a fixed order
       double g0 = x, g1 = 0.0, g2 = 0.0, g3 = 0.0;
       int j = 0;
@@ -548,7 +582,7 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(a.g) || !al16(a.pi) || !al16(a.w_a) || !al16(a.w_decay) || !al16(a.newton_out) || !al16(a.base_out))
     fail(DHO2G_ARGUMENT, "split_update: vectors must be 16-byte aligned");
-  const size_t smem_p1 = kCh * sizeof(float) + (size_t)kW * R * sizeof(double);
+  const size_t smem_p1 = kCh * sizeof(double) + (size_t)kW * R * sizeof(double);
   const size_t smem_p2 = kCh2 * sizeof(float) + (size_t)R * sizeof(double) + (size_t)kW * R * sizeof(double);
   const int gp = std::min(one_wave_grid(upd_p1_kernel, kT, smem_p1, ctx->sm_count, cdiv(rows, kCh)),
                           one_wave_grid(upd_p2_kernel, kT, smem_p2, ctx->sm_count, cdiv(rows, kCh2)));
