@@ -139,6 +139,18 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;
+    else if (k == "gemm_chunk_kb") {
+      ctx->gemm_chunk_kb = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
+    else if (k == "gemm_chunk_kb1") {
+      ctx->gemm_chunk_kb1 = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
+    else if (k == "gemm_f16") {
+      ctx->gemm_f16 = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
     else if (k == "hvp_route") ctx->hvp_route = (int)value;
     else if (k == "upd_p2_variant") ctx->upd_p2_variant = (int)value;
     else if (k == "gemm_pdl") {
@@ -482,6 +494,8 @@ int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, 
       m->WV_hi[t].alloc((size_t)ld.out * 2 * ld.Pin);
       m->WV_lo[t].alloc((size_t)ld.out * 2 * ld.Pin);
     }
+    m->scl.alloc((size_t)3 * m->L);
+    m->amax.alloc((size_t)5 * (m->L + 1));
     *out = m.release();
   });
 }
@@ -598,7 +612,9 @@ int dho2g_mlp_hvp(dho2g_mlp* m, const double* w, const double* v, const double* 
     m->out32.ensure(m->dim);
     mlp_set_input(m, m->X32.p, m->y32.p, nullptr, B, true);
     mlp_load_weights(m, m->w32.p);
-    mlp_hvp_dev(m, m->v32.p, nullptr, B, ncls, 1.0 / (double)B, m->out32.p);
+    double vmax = 0.0;  // the fp16 operand scale of the direction halves is sized from max |v|
+    for (size_t i = 0; i < m->dim; ++i) vmax = std::max(vmax, std::fabs(v[i]));
+    mlp_hvp_dev(m, m->v32.p, nullptr, B, ncls, 1.0 / (double)B, m->out32.p, (float)std::max(vmax, 1e-30));
     download(m->out32.p, hv, m->dim, m->ctx->stream);
   });
 }
@@ -1035,12 +1051,18 @@ int dho2g_trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count) {
 // ------------------------------------------------------------------ test hook
 namespace {
 __global__ void split_rows_kernel(const float* __restrict__ src, int rows, int K, int ld, bf16* __restrict__ hi,
-                                  bf16* __restrict__ lo) {
+                                  bf16* __restrict__ lo, int f16, float sc) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= (size_t)rows * ld) return;
   const int r = (int)(i / ld), k = (int)(i % ld);
   const float x = k < K ? src[(size_t)r * K + k] : 0.f;
-  split_bf16(x, hi[i], lo[i]);
+  if (f16) split_f16(x, sc, hi[i], lo[i]);
+  else split_bf16(x, hi[i], lo[i]);
+}
+float host_absmax(const float* x, size_t n) {
+  float m = 0.f;
+  for (size_t i = 0; i < n; ++i) m = std::max(m, std::fabs(x[i]));
+  return m;
 }
 }  // namespace
 
@@ -1052,12 +1074,35 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
     DevBuf<bf16> ah((size_t)M * ld), al((size_t)M * ld), bh((size_t)N * ld), bl((size_t)N * ld);
     DHO2G_CUDA(cudaMemcpyAsync(a.p, A, sizeof(float) * M * K, cudaMemcpyHostToDevice, ctx->stream));
     DHO2G_CUDA(cudaMemcpyAsync(b.p, B, sizeof(float) * N * K, cudaMemcpyHostToDevice, ctx->stream));
-    split_rows_kernel<<<cdiv((size_t)M * ld, 256), 256, 0, ctx->stream>>>(a.p, M, K, ld, ah.p, al.p);
-    split_rows_kernel<<<cdiv((size_t)N * ld, 256), 256, 0, ctx->stream>>>(b.p, N, K, ld, bh.p, bl.p);
+    // operand format as the MLP uses it (ctx option gemm_f16): power-of-two scales from max |A|, max |B|
+    const int f16 = ctx->gemm_f16 ? 1 : 0;
+    const float sc[2] = {f16 ? pow2_scale(host_absmax(A, (size_t)M * K)) : 1.f,
+                         f16 ? pow2_scale(host_absmax(B, (size_t)N * K)) : 1.f};
+    DevBuf<float> scd(2);
+    DHO2G_CUDA(cudaMemcpyAsync(scd.p, sc, sizeof(sc), cudaMemcpyHostToDevice, ctx->stream));
+    split_rows_kernel<<<cdiv((size_t)M * ld, 256), 256, 0, ctx->stream>>>(a.p, M, K, ld, ah.p, al.p, f16, sc[0]);
+    split_rows_kernel<<<cdiv((size_t)N * ld, 256), 256, 0, ctx->stream>>>(b.p, N, K, ld, bh.p, bl.p, f16, sc[1]);
     DHO2G_LAUNCH();
     const int saved = ctx->gemm_backend;
     ctx->gemm_backend = backend;
-    gemm3_store(ctx, M, N, K, ah.p, al.p, ld, bh.p, bl.p, ld, c.p, N, 1.0f);
+    Epi e{};
+    e.mode = EPI_STORE;
+    e.M = M;
+    e.N = N;
+    e.C = c.p;
+    e.ldc = N;
+    e.alpha = 1.0f;
+    e.f16 = f16;
+    e.sa = f16 ? scd.p : nullptr;
+    e.sb = f16 ? scd.p + 1 : nullptr;
+    GOp ga = gop_k(ah.p, al.p, ld, K, M), gb = gop_k(bh.p, bl.p, ld, K, N);
+    ga.f16 = gb.f16 = f16;
+    try {
+      gemm3x(ctx, M, N, K, K, ga, gb, e);
+    } catch (...) {
+      ctx->gemm_backend = saved;
+      throw;
+    }
     ctx->gemm_backend = saved;
     DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
     DHO2G_CUDA(cudaMemcpy(Cout, c.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
@@ -1066,7 +1111,7 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
 
 // Physical operand for the segmented test: X0 (MN x K0), X1 (MN x K1) row-major logical.
 static GOp test_operand(dho2g_ctx* ctx, int MN, int K0, int K1, int kseg, const float* X0, const float* X1, int mn_major,
-                        DevBuf<bf16>& hi, DevBuf<bf16>& lo) {
+                        DevBuf<bf16>& hi, DevBuf<bf16>& lo, float* sc) {
   std::vector<float> h;
   GOp g{};
   g.mn_major = mn_major;
@@ -1103,7 +1148,9 @@ static GOp test_operand(dho2g_ctx* ctx, int MN, int K0, int K1, int kseg, const 
   // kernel runs on the library's (non-blocking) stream
   DHO2G_CUDA(cudaMemcpyAsync(f.p, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice, ctx->stream));
   const int rows = (int)(h.size() / g.ld);
-  split_rows_kernel<<<cdiv(h.size(), 256), 256, 0, ctx->stream>>>(f.p, rows, g.ld, g.ld, hi.p, lo.p);
+  g.f16 = ctx->gemm_f16 ? 1 : 0;
+  *sc = g.f16 ? pow2_scale(host_absmax(h.data(), h.size())) : 1.f;
+  split_rows_kernel<<<cdiv(h.size(), 256), 256, 0, ctx->stream>>>(f.p, rows, g.ld, g.ld, hi.p, lo.p, g.f16, *sc);
   DHO2G_LAUNCH();
   DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
   g.hi = hi.p;
@@ -1119,9 +1166,11 @@ int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const floa
     const int kseg = K1 > 0 ? (int)round_up((size_t)K0, 64) : K0;
     const int K = K1 > 0 ? kseg + K1 : K0;
     DevBuf<bf16> ah, al, bh, bl;
-    const GOp A = test_operand(ctx, M, K0, K1, kseg, A0, A1, a_mn, ah, al);
-    const GOp B = test_operand(ctx, N, K0, K1, kseg, B0, B1, b_mn, bh, bl);
-    DevBuf<float> c((size_t)M * N);
+    float sc[2];
+    const GOp A = test_operand(ctx, M, K0, K1, kseg, A0, A1, a_mn, ah, al, &sc[0]);
+    const GOp B = test_operand(ctx, N, K0, K1, kseg, B0, B1, b_mn, bh, bl, &sc[1]);
+    DevBuf<float> c((size_t)M * N), scd(2);
+    DHO2G_CUDA(cudaMemcpyAsync(scd.p, sc, sizeof(sc), cudaMemcpyHostToDevice, ctx->stream));
     Epi e{};
     e.mode = EPI_STORE;
     e.M = M;
@@ -1129,6 +1178,9 @@ int dho2g_test_gemm_seg(dho2g_ctx* ctx, int M, int N, int K0, int K1, const floa
     e.C = c.p;
     e.ldc = N;
     e.alpha = 1.0f;
+    e.f16 = A.f16;
+    e.sa = A.f16 ? scd.p : nullptr;
+    e.sb = A.f16 ? scd.p + 1 : nullptr;
     const int saved = ctx->gemm_backend;
     ctx->gemm_backend = backend;
     try {

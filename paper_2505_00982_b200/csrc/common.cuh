@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -145,6 +146,29 @@ inline int one_wave_grid(Kernel kernel, int threads, size_t smem, int sm_count, 
 __device__ __forceinline__ void split_bf16(float x, bf16& hi, bf16& lo) {
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+// Scaled-fp16 pair: x s = hi + lo with 11 + 11 significant bits (vs 8 + 8 for bf16) for |x s| in
+// [2^-3, 2^15); s is a power of two chosen from max |x| (pow2_scale), so the scaling is exact and
+// elements far below the maximum lose bits only at the 2^-25 / s absolute level. Stored in the same
+// 16-bit buffers as the bf16 pairs.
+__device__ __forceinline__ void split_f16(float x, float s, bf16& hi, bf16& lo) {
+  const float y = x * s;
+  const __half h = __float2half_rn(y);
+  const __half l = __float2half_rn(y - __half2float(h));
+  hi = __ushort_as_bfloat16(__half_as_ushort(h));
+  lo = __ushort_as_bfloat16(__half_as_ushort(l));
+}
+__device__ __forceinline__ float f16_bits_to_float(bf16 x) {
+  return __half2float(__ushort_as_half(__bfloat16_as_ushort(x)));
+}
+// Largest power of two s with mx * s < 2^14 (a 4x margin below the fp16 maximum); 1 for mx == 0.
+__host__ __device__ __forceinline__ float pow2_scale(float mx) {
+  if (!(mx > 0.f)) return 1.f;
+  int e;
+  frexpf(mx, &e);  // mx < 2^e
+  e = 14 - e;
+  e = e > 100 ? 100 : (e < -100 ? -100 : e);
+  return ldexpf(1.f, e);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

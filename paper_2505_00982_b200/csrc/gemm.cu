@@ -104,11 +104,24 @@ __device__ __forceinline__ float epi_elem(const Epi& e, int row, int col, float 
 }
 
 // Per-thread form (CUDA-core backend): 16 consecutive columns of one row; x receives the values.
+__device__ __forceinline__ float acc_unscale(const Epi& e) { return e.sa ? 1.f / (*e.sa * *e.sb) : 1.f; }
+__device__ __forceinline__ void amax_warp(const Epi& e, float m) {  // m >= 0 per lane
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(e.amax, __float_as_uint(m));
+}
+
 __device__ __forceinline__ void epi_apply16(const Epi& e, int row, int col0, const float (&acc)[16], float (&x)[16]) {
   const float vsc = (e.do1 && e.vscale) ? *e.vscale : 1.f;
+  const float inv = acc_unscale(e);
+  float m = 0.f;
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j], vsc, epi_load(e, row, col0 + j)) : 0.f;
+  for (int j = 0; j < 16; ++j) {
+    x[j] = (row < e.M && col0 + j < e.N) ? epi_elem(e, row, col0 + j, acc[j] * inv, vsc, epi_load(e, row, col0 + j))
+                                         : 0.f;
+    m = fmaxf(m, fabsf(x[j]));
+  }
+  if (e.amax && e.mode != EPI_STORE && m > 0.f) atomicMax(e.amax, __float_as_uint(m));
   if (e.mode != EPI_STORE && e.Th && row < e.Bp) {  // transposed pair; pad rows [M, Bp) get zeros
     const size_t base = (size_t)e.hT * e.Bp + row;
 #pragma unroll
@@ -181,8 +194,12 @@ __device__ __forceinline__ float epi_elem_t(const Epi& e, int row, int col, floa
 // row-major inputs / outputs / bf16 pairs are coalesced, and write the transposed pair from the
 // lane = row layout.
 template <int MODE>
-__device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc)[16], float* sm) {
+__device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc_in)[16], float* sm) {
   const int lane = threadIdx.x & 31;
+  float acc[16];
+  const float inv = acc_unscale(e);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = acc_in[j] * inv;
   if (MODE == EPI_STORE) {
     const int row = row0 + lane;
     if (row >= e.M) return;
@@ -234,6 +251,7 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
     const int row = row0 + 2 * it + rr;
     if (row < e.M && col < e.N) in[it] = epi_load_t<MODE>(e, row, col);
   }
+  float mx = 0.f;
 #pragma unroll
   for (int it = 0; it < 16; ++it) {
     const int rl = 2 * it + rr;
@@ -241,7 +259,9 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
     float x = 0.f;
     if (row < e.M && col < e.N) x = epi_elem_t<MODE>(e, row, col, sm[rl * 17 + cc], vsc, in[it]);
     sm[rl * 17 + cc] = x;
+    mx = fmaxf(mx, fabsf(x));
   }
+  if (e.amax) amax_warp(e, mx);
   __syncwarp();
   if (e.csum && row0 < e.M && lane < 16 && col0 + lane < e.N) {  // column sums of this 32-row block (rows >= M hold 0)
     float t = 0.f;
@@ -329,8 +349,13 @@ __device__ __forceinline__ void gop_load(const GOp& op, int mn, int MN, int k, i
   gop_coord(op, mn, k, kseg, in, out);
   if (in < 0 || in >= op.inner || out < 0 || out >= op.outer) return;
   const size_t i = (size_t)out * op.ld + in;
-  h = __bfloat162float(op.hi[i]);
-  l = __bfloat162float(op.lo[i]);
+  if (op.f16) {
+    h = f16_bits_to_float(op.hi[i]);
+    l = f16_bits_to_float(op.lo[i]);
+  } else {
+    h = __bfloat162float(op.hi[i]);
+    l = __bfloat162float(op.lo[i]);
+  }
 }
 
 __global__ void __launch_bounds__(256) gemm3_simt_kernel(int M, int N, int K, int kseg, const GOp A, const GOp B,
@@ -406,6 +431,10 @@ constexpr uint32_t EPI_SMEM = 8 * 32 * 17 * 4;  // per epilogue warp: 32 x 16 re
 __host__ __device__ constexpr uint32_t idesc(int M, int N, bool amn, bool bmn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((amn ? 1u : 0u) << 15) | ((bmn ? 1u : 0u) << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// the same with F16 operands (A / B format fields 0) for the scaled-fp16 pairs
+__host__ __device__ constexpr uint32_t idesc_fmt(uint32_t id, bool f16) {
+  return f16 ? (id & ~((7u << 7) | (7u << 10))) : id;
 }
 
 struct OpOff {  // per-segment coordinate offsets of one operand (GOp minus pointers / extents)
@@ -496,6 +525,7 @@ constexpr uint32_t TMEM_COLS = ACC * BN;
 
 struct Sched {
   int mt, nt, tiles, splits, units, nkb, kseg;  // nkb: k-blocks total
+  int chunk;  // k-blocks per TMEM accumulation chunk (drained into an fp32 running sum), >= unit length: off
   __device__ __forceinline__ void unit(int u, int& m0, int& n0, int& split, int& tile, int& kb0, int& kb1) const {
     split = u / tiles;
     tile = u - split * tiles;
@@ -568,16 +598,18 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread), accumulator double-buffered in TMEM
-    constexpr uint32_t ID = idesc(BM, BN, AMN, BMN);
+    const uint32_t ID = idesc_fmt(idesc(BM, BN, AMN, BMN), e.f16 != 0);
     uint32_t it = 0, uc = 0;
-    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
+    for (int u = blockIdx.x; u < sc.units; u += gridDim.x) {
       int m0, n0, split, tile, kb0, kb1;
       sc.unit(u, m0, n0, split, tile, kb0, kb1);
+     for (int c0 = kb0; c0 < kb1 || c0 == kb0; c0 += sc.chunk, ++uc) {  // one accumulator per chunk
+      const int c1 = min(kb1, c0 + sc.chunk);
       const uint32_t ab = uc % ACC;
       mbar_wait(&tempty[ab], ((uc / ACC) & 1) ^ 1);  // epilogue drained this buffer
       fence_after();
       const uint32_t acc_addr = tmem + ab * BN;
-      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+      for (int kb = c0; kb < c1; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         fence_after();
@@ -588,7 +620,7 @@ __global__ void __launch_bounds__(384, 1)
           const uint64_t dAl = op_desc<AMN>(base + OP_BYTES, kk);
           const uint64_t dBh = op_desc<BMN>(base + 2 * OP_BYTES, kk);
           const uint64_t dBl = op_desc<BMN>(base + 3 * OP_BYTES, kk);
-          const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
+          const uint32_t first = (kb > c0 || kk > 0) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
@@ -606,6 +638,7 @@ __global__ void __launch_bounds__(384, 1)
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                        smem_u32(&tfull[ab]))
                    : "memory");  // accumulator ready for the epilogue
+     }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue warps: TMEM -> registers -> (split-K combine) -> fused epilogue
@@ -614,9 +647,40 @@ __global__ void __launch_bounds__(384, 1)
     const int chalf = (warp - 4) >> 2;
     float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
     uint32_t uc = 0;
+    // this thread's elements of the fp32 running sum over a unit's chunks (thread-private, same layout as
+    // the split-K partials)
+    float* run = ws ? ws + ((size_t)sc.tiles + blockIdx.x) * BM * BN + (size_t)(ew + 4 * chalf) * (32 * BN / 2) +
+                          (size_t)lane * 4
+                    : nullptr;
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
       sc.unit(u, m0, n0, split, tile, kb0, kb1);
+      // chunks before the last: TMEM -> += running sum (fp32, round to nearest) -> free the accumulator
+      const int nchunks = kb1 > kb0 ? (kb1 - kb0 + sc.chunk - 1) / sc.chunk : 1;
+      for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
+        const uint32_t ab = uc % ACC;
+        mbar_wait(&tfull[ab], (uc / ACC) & 1);
+        fence_after();
+        const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
+#pragma unroll 1
+        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
+          float v[16];
+          tmem_ld16(tb + (uint32_t)c0, v);
+          float* q = run + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float4 t = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (c > 0) {
+              const float4 o = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
+              t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
+            }
+            __stcg(reinterpret_cast<float4*>(q + j * 128), t);
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[ab]);
+      }
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
@@ -637,6 +701,14 @@ __global__ void __launch_bounds__(384, 1)
       for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
         float v[16];
         tmem_ld16(tbase + (uint32_t)c0, v);
+        if (nchunks > 1) {  // + the earlier chunks
+          const float* q = run + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
+            v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+          }
+        }
         if (split > 0) {
           const float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
@@ -731,11 +803,18 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   const int ctas = ctx->gemm_worker_cap > 0 ? std::min(ctx->sm_count, 2 * ctx->gemm_worker_cap) : ctx->sm_count;
   sc.splits = ctx->gemm_splits > 0 ? std::min(ctx->gemm_splits, std::max(1, sc.nkb)) : pick_splits(sc.tiles, sc.nkb, ctas);
   sc.units = sc.tiles * sc.splits;
+  const int per_unit = (sc.nkb + sc.splits - 1) / sc.splits;
+  sc.chunk = (ctx->gemm_chunk_kb1 > 0 && ctx->gemm_chunk_kb1 < per_unit) ? ctx->gemm_chunk_kb1 : std::max(per_unit, 1);
   float* ws = nullptr;
   unsigned* flags = nullptr;
   unsigned epoch = 0;
+  const int ctas1 = std::min(sc.units, ctas);
+  if (sc.chunk < per_unit) {  // running sums after the split-K partials: one BM x BN slot per CTA
+    ctx->gemm_ws.ensure_g(((size_t)sc.tiles + ctas1) * BM * BN);
+    ws = ctx->gemm_ws.p;
+  }
   if (sc.splits > 1) {
-    ctx->gemm_ws.ensure_g((size_t)sc.tiles * BM * BN);
+    ctx->gemm_ws.ensure_g(((size_t)sc.tiles + (sc.chunk < per_unit ? ctas1 : 0)) * BM * BN);
     ctx->gemm_flags.ensure_g((size_t)sc.tiles);
     ws = ctx->gemm_ws.p;
     flags = ctx->gemm_flags.p;
@@ -833,6 +912,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
 struct Work {
   int mt, nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
   int dp;                                      // data-parallel tiles
+  int chunk;  // k-blocks per TMEM accumulation chunk (drained into an fp32 running sum); >= nkb: off
   __device__ __forceinline__ long long sk_total() const { return (long long)(mt * nt - dp) * nkb; }
   __device__ __forceinline__ long long begin(int /*phase*/, int w) const { return sk_total() * w / workers; }
 };
@@ -966,12 +1046,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     Seg sg;
     while (cur.next(wk, sg)) {
       const int n0 = sg.ntile * NT;
-      const uint32_t ID = idesc(256, tile_cols<NT>(wk, n0), AMN, BMN);
+      const uint32_t ID = idesc_fmt(idesc(256, tile_cols<NT>(wk, n0), AMN, BMN), e.f16 != 0);
+     for (int c0 = sg.k0; c0 < sg.k1; c0 += wk.chunk) {  // one accumulator per chunk
+      const int c1 = min(sg.k1, c0 + wk.chunk);
       const uint32_t ab = uc % ACC;
       mbar_wait_cluster(&tempty[ab], ((uc / ACC) & 1) ^ 1);
       fence_after();
       const uint32_t acc_addr = tmem + ab * NT;
-      for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+      for (int kb = c0; kb < c1; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         fence_after();
@@ -982,7 +1064,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const uint64_t dAl = op_desc<AMN, BKT>(base + OP_BYTES, kk);
           const uint64_t dBh = op_desc<BMN, BKT>(base + 2 * OP_BYTES, kk);
           const uint64_t dBl = op_desc<BMN, BKT>(base + 3 * OP_BYTES, kk);
-          const uint32_t first = (kb > sg.k0 || kk > 0) ? 1u : 0u;
+          const uint32_t first = (kb > c0 || kk > 0) ? 1u : 0u;
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_addr),
@@ -996,6 +1078,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       commit2(&tfull[ab]);
       ++uc;
+     }
     }
     if (trace) trace[1] = gtimer();
   } else if (warp >= 4) {
@@ -1008,14 +1091,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     Cursor cur;
     cur.init(wk, worker);
     Seg sg;
+    // this thread's elements of the fp32 running sum over a segment's chunks (thread-private, after the
+    // stream-K partial slots)
+    float* run = ws + ((size_t)(2 * wk.workers + worker) * 2 + rank) * PART_FLOATS + slot_off;
     while (cur.next(wk, sg)) {
       const int m0 = sg.mtile * 256 + (int)rank * BM, n0 = sg.ntile * NT;
       const int ncols = tile_cols<NT>(wk, n0);
+      // chunks before the last: TMEM -> += running sum (fp32, round to nearest) -> free the accumulator
+      const int nchunks = (sg.k1 - sg.k0 + wk.chunk - 1) / wk.chunk;
+      for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
+        const uint32_t ab = uc % ACC;
+        mbar_wait(&tfull[ab], (uc / ACC) & 1);
+        fence_after();
+        const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
+#pragma unroll 1
+        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
+          if (c0 >= ncols) break;
+          float v[16];
+          tmem_ld16(tb + (uint32_t)c0, v);
+          float* q = run + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float4 t = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (c > 0) {
+              const float4 o = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
+              t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
+            }
+            __stcg(reinterpret_cast<float4*>(q + j * 128), t);
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_leader(&tempty[ab]);
+      }
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
       if (trace && threadIdx.x == 128) trace[2] = gtimer();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
+      auto add_run = [&](int c0, float (&v)[16]) {  // + the earlier chunks
+        if (nchunks < 2) return;
+        const float* q = run + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
+          v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
+        }
+      };
       if (sg.k0 != 0) {
         // non-head segment (first of this worker): publish the raw partial
         float* p = ws + ((size_t)(sg.phase * wk.workers + worker) * 2 + rank) * PART_FLOATS + slot_off;
@@ -1024,6 +1146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
+          add_run(c0, v);
           float* q = p + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -1052,6 +1175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
+          add_run(c0, v);
           for (int w2 = worker + 1; w2 <= wlast; ++w2) {
             const float* q = ws + ((size_t)(sbase + w2) * 2 + rank) * PART_FLOATS + slot_off +
                              (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
@@ -1115,8 +1239,10 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;
   wk.dp = (ctx->gemm_dp && waves >= 2) ? (int)((waves - 1) * wk.workers) : 0;
-  ctx->gemm_ws.ensure_g((size_t)2 * wk.workers * 2 * PART_MAX);
+  // stream-K partial slots (2 schedule parts x workers x 2 CTAs) + one running-sum slot per CTA
+  ctx->gemm_ws.ensure_g((size_t)3 * wk.workers * 2 * PART_MAX);
   ctx->gemm_flags.ensure_g((size_t)2 * wk.workers * 2 + 16);
+  wk.chunk = ctx->gemm_chunk_kb > 0 ? ctx->gemm_chunk_kb : wk.nkb;
   unsigned epoch = ++ctx->gemm_epoch;
   if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
@@ -1176,9 +1302,9 @@ void gemm_presize(dho2g_ctx* ctx) {
   // both lanes' stream-K partials (2 schedule parts x pairs x 2 CTAs x 128 x 256) and flags; covers the
   // single-CTA kernel's split-K partials for the small-M GEMMs too
   const size_t pairs = (size_t)std::max(1, ctx->sm_count / 2);
-  ctx->gemm_ws.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_ws.ensure_g(3 * pairs * 2 * tc2::PART_MAX);
   ctx->gemm_flags.ensure_g(2 * pairs * 2 + 16);
-  ctx->gemm_ws2.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_ws2.ensure_g(3 * pairs * 2 * tc2::PART_MAX);
   ctx->gemm_flags2.ensure_g(2 * pairs * 2 + 16);
 }
 
@@ -1189,6 +1315,7 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
   if (kseg < K && (kseg <= 0 || kseg % tc::BK)) fail(DHO2G_ARGUMENT, "gemm3: K segment boundary must be a multiple of 64");
   tc::check_op(A, "A");
   tc::check_op(B, "B");
+  if (A.f16 != B.f16 || (A.f16 != 0) != (e.f16 != 0)) fail(DHO2G_ARGUMENT, "gemm3: operand formats differ");
   ctx->bump("gemm_calls", 1);
   ctx->bump("gemm_flops_issued", 3.0 * 2.0 * double(M) * double(N) * double(K));
   const int slot = ctx->kt_begin();

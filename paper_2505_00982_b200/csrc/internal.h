@@ -54,6 +54,13 @@ struct dho2g_ctx {
   int hvp_route = 0;      // world > 1: batch-split HVP partials stored straight into the owners' buffers
                          // (peer memory) instead of a reduce-scatter after the HVP
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
+  int gemm_chunk_kb = 0; // tcgen05 GEMMs: drain the TMEM accumulator into an fp32 running sum every this many
+                         // 64-deep k-blocks (0: never). The tensor core's accumulation truncates, so its error
+                         // grows with the chain length; short chains + round-to-nearest fp32 sums bound it.
+  int gemm_chunk_kb1 = 8; // the same for the single-CTA kernel (small-M GEMMs: C1/C2 HVPs and gradients), where
+                         // the drains are cheap
+  int gemm_f16 = 1;      // MLP GEMM operands as power-of-two-scaled fp16 (hi, lo) pairs (22 significant bits)
+                         // instead of bf16 pairs (16 bits); same tcgen05 kind::f16 rate
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
   dho2g::DevBuf<unsigned> gemm_flags2;
@@ -178,6 +185,24 @@ struct dho2g_mlp {
   float* const* route = nullptr;
   long long route_base = 0;
   int route_rank = 0;
+  // Scaled-fp16 operand state (ctx option gemm_f16): one power-of-two scale per pair buffer
+  //   scl[t] AR[t] (t < L), scl[L + j - 1] DR[j] (1 <= j <= L), scl[2L + t] WV[t]
+  // and max |x| slots (float bits) of the fp32 tensors the pairs are split from
+  //   amax[j] a_j, amax[(L+1) + j] ra_j, amax[2(L+1) + j] d_j, amax[3(L+1) + j] rd_j (j <= L),
+  //   amax[4(L+1) + t] W_t, amax[4(L+1) + L] the level-0 input batch.
+  int f16 = 0;              // format of the currently packed operands
+  float wv_vbound = 0.f;    // bound on |direction| the WV scales were chosen for
+  dho2g::DevBuf<float> scl;
+  dho2g::DevBuf<unsigned> amax;
+  float* s_ar(int t) { return scl.p + t; }
+  float* s_dr(int j) { return scl.p + L + j - 1; }
+  float* s_wv(int t) { return scl.p + 2 * L + t; }
+  unsigned* mx_a(int j) { return amax.p + j; }
+  unsigned* mx_ra(int j) { return amax.p + (L + 1) + j; }
+  unsigned* mx_d(int j) { return amax.p + 2 * (L + 1) + j; }
+  unsigned* mx_rd(int j) { return amax.p + 3 * (L + 1) + j; }
+  unsigned* mx_w(int t) { return amax.p + 4 * (L + 1) + t; }
+  unsigned* mx_x() { return amax.p + 4 * (L + 1) + L; }
 
   void ensure_batch(size_t B);
   ~dho2g_mlp() {
@@ -196,7 +221,9 @@ void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, 
                   size_t ncls, double scale, float* g);
 // Caches A, Z, softmax, D and U at the loaded point (Lanczos applies H m times at one point).
 void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale);
-void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv);
+// vbound: an upper bound on |vscale * v| (1 for the unit Lanczos directions); sizes the fp16 operand scale
+void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv,
+                 float vbound = 1.0f);
 // Forward-only evaluation: adds sum of per-sample loss and correct count into acc[0], acc[1] (fp64).
 void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double* acc2);
@@ -244,6 +271,14 @@ struct Epi {
   long long route_flat0;
   long long route_base;
   int route_rank;
+  // Scaled-fp16 operands (option gemm_f16): f16 selects the fp16 operand format of the MMAs; sa / sb are
+  // the device power-of-two scales of the A / B pair buffers (acc is multiplied by 1 / (sa sb) before the
+  // epilogue math, exactly); amax, if set, receives max |value| over the values the epilogue writes
+  // (float bits, atomicMax) for the split that turns them into the next operand.
+  int f16;
+  const float* sa;
+  const float* sb;
+  unsigned* amax;
 };
 // One GEMM operand: a (hi, lo) bf16 pair buffer read through a TMA-style window. K-major: rows are
 // the M (or N) index, K contiguous; MN-major: rows are the K index, M (or N) contiguous. The K range
@@ -253,12 +288,13 @@ struct Epi {
 //   MN-major: inner = mn + off_in[seg], outer = kk + off_out[seg]
 // and address outer * ld + inner; coordinates outside [0, inner) x [0, outer) read as zero.
 struct GOp {
-  const bf16* hi;
+  const bf16* hi;  // (hi, lo) 16-bit pairs: bf16, or fp16 scaled by a power of two when f16 is set
   const bf16* lo;
   int ld;
   int mn_major;
   int inner, outer;
   int off_in[2], off_out[2];
+  int f16;
 };
 GOp gop_k(const bf16* hi, const bf16* lo, int ld, int K, int rows);  // plain K-major, one segment
 void gemm_presize(dho2g_ctx* ctx);  // both lanes' GEMM workspaces at their maximum size

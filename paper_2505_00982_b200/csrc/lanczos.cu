@@ -941,7 +941,8 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
   if (kind == 0) {
     dho2g_mlp* m = mlp;
     // a rank whose slice of the curvature batch is empty (B < G) contributes zeros and runs no HVP
-    if (b1 > b0 && (m->w_cur != wptr || !weights_loaded || m->input_owner != this)) {
+    if (b1 > b0 && (m->w_cur != wptr || !weights_loaded || m->input_owner != this ||
+                    m->f16 != (ctx->gemm_f16 ? 1 : 0))) {
       if (idx.p) mlp_set_input(m, Xptr, yptr, idx.p + b0, b1 - b0, true);
       else mlp_set_input(m, Xptr + b0 * m->sizes[0], yptr + b0, nullptr, b1 - b0, true);
       mlp_load_weights(m, wptr);

@@ -113,14 +113,153 @@ __global__ void pack_rows_kernel(int B, int s, int P, const float* __restrict__ 
   }
 }
 
+// ------------------------------------------------------------------ scaled-fp16 operands (gemm_f16)
+// max |x| into a slot (float bits; nonnegative floats order like their bit patterns)
+__device__ __forceinline__ void slot_max(unsigned* slot, float m) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(slot, __float_as_uint(m));
+}
+__global__ void absmax_kernel(const float* __restrict__ p, size_t n, unsigned* slot) {
+  float m = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(__ldg(p + i)));
+  slot_max(slot, m);
+}
+__global__ void absmax_rows_kernel(const float* __restrict__ X, const int64_t* __restrict__ idx, int ldX, int B, int s,
+                                   unsigned* slot) {
+  float m = 0.f;
+  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+    const float* row = X + (size_t)(idx ? idx[b] : b) * ldX;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < s; k += gridDim.x * blockDim.x) m = fmaxf(m, fabsf(row[k]));
+  }
+  slot_max(slot, m);
+}
+
+// [V | W] packing as scaled fp16: the W half (half 1) picks the scale from max |W| and the bound on the
+// direction halves that will share it, and publishes it; the V half (half 0) uses the published scale.
+__global__ void pack_weights_f16_kernel(const float* __restrict__ p, const float* __restrict__ pscale, int in, int out,
+                                        int Pin, int half, const unsigned* __restrict__ wmax, float vbound,
+                                        float* __restrict__ sout, bf16* __restrict__ WVh, bf16* __restrict__ WVl) {
+  const int k0 = blockIdx.x * (blockDim.x * kPackPer) + 2 * threadIdx.x;
+  float sc;
+  if (half == 1) {
+    sc = pow2_scale(fmaxf(__uint_as_float(*wmax), vbound));
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *sout = sc;
+  } else {
+    sc = *sout;
+  }
+  const float ps = pscale ? *pscale : 1.0f;
+  for (int o = blockIdx.y; o < out; o += gridDim.y) {
+    const float* row = p + (size_t)o * in;
+    float x[kPackPer];
+#pragma unroll
+    for (int u = 0; u < kPackPer / 2; ++u) {
+      const int k = k0 + 2 * u * blockDim.x;
+      x[2 * u] = k < in ? __ldg(row + k) : 0.f;
+      x[2 * u + 1] = k + 1 < in ? __ldg(row + k + 1) : 0.f;
+    }
+    const size_t base = (size_t)o * (2 * Pin) + (size_t)half * Pin;
+#pragma unroll
+    for (int u = 0; u < kPackPer / 2; ++u) {
+      const int k = k0 + 2 * u * blockDim.x;
+      if (k < in) {
+        bf16 h0, l0, h1, l1;
+        split_f16(x[2 * u] * ps, sc, h0, l0);
+        split_f16(x[2 * u + 1] * ps, sc, h1, l1);
+        if (k + 1 < in) {
+          *reinterpret_cast<__nv_bfloat162*>(WVh + base + k) = __halves2bfloat162(h0, h1);
+          *reinterpret_cast<__nv_bfloat162*>(WVl + base + k) = __halves2bfloat162(l0, l1);
+        } else {
+          WVh[base + k] = h0;
+          WVl[base + k] = l0;
+        }
+      }
+    }
+  }
+}
+
+// One level's [x | rx] pair buffer (rows b, half-width P, pads [s, P) zero) from fp32 sources as scaled
+// fp16: x from X rows (idx-gathered, level 0) or x32 (B x s), rx from rx32; the scale covers every half
+// written (max of the given slots) and block 0 publishes it for the consuming GEMMs. Grid-stride over
+// (row, 4-column group): float4 reads where the row width allows, 8-byte pair writes.
+__device__ __forceinline__ void split4(const float (&x)[4], float sc, bf16* h, bf16* l) {
+  bf16 hh[4], ll[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) split_f16(x[u], sc, hh[u], ll[u]);
+  *reinterpret_cast<uint2*>(h) = *reinterpret_cast<const uint2*>(hh);
+  *reinterpret_cast<uint2*>(l) = *reinterpret_cast<const uint2*>(ll);
+}
+__device__ __forceinline__ void load4(const float* row, int k, int s, bool vec, float (&x)[4]) {
+  if (vec && k + 3 < s) {
+    const float4 v = *reinterpret_cast<const float4*>(row + k);
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = k + u < s ? row[k + u] : 0.f;
+  }
+}
+__global__ void split_pair_kernel(int B, int s, int P, const float* __restrict__ X, const int64_t* __restrict__ idx,
+                                  int ldX, const float* __restrict__ x32, const float* __restrict__ rx32,
+                                  const unsigned* __restrict__ mxx, const unsigned* __restrict__ mxr,
+                                  float* __restrict__ sout, bf16* __restrict__ Rh, bf16* __restrict__ Rl) {
+  float mx = 0.f;
+  if (mxx) mx = fmaxf(mx, __uint_as_float(*mxx));
+  if (mxr) mx = fmaxf(mx, __uint_as_float(*mxr));
+  const float sc = pow2_scale(mx);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sout = sc;
+  const int G = P / 4;  // P is a multiple of 8
+  const bool vx = X ? (ldX % 4 == 0) : (s % 4 == 0), vr = s % 4 == 0;
+  const size_t total = (size_t)B * G;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / G), k = (int)(i - (size_t)b * G) * 4;
+    const size_t r = (size_t)b * (2 * P) + k;
+    float x[4];
+    if (X || x32) {
+      const float* row = X ? X + (size_t)(idx ? idx[b] : b) * ldX : x32 + (size_t)b * s;
+      load4(row, k, s, vx, x);
+      split4(x, sc, Rh + r, Rl + r);
+    }
+    if (rx32) {
+      load4(rx32 + (size_t)b * s, k, s, vr, x);
+      split4(x, sc, Rh + r + P, Rl + r + P);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ output layer delta
 // oracle.cpp:476-495 (delta) and :572-599 (R-delta); also per-sample loss / correctness.
+__device__ void output_delta_row(int b, int O, int mse, int ncls, int do0, int do1, double scale,
+                                 const float* __restrict__ z, const float* __restrict__ rz,
+                                 const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
+                                 double* __restrict__ loss, int* __restrict__ correct);
 __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, int do1, double scale,
                                     const float* __restrict__ z, const float* __restrict__ rz,
                                     const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
-                                    double* __restrict__ loss, int* __restrict__ correct) {
+                                    double* __restrict__ loss, int* __restrict__ correct, unsigned* mxd,
+                                    unsigned* mxrd) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mxd || mxrd) {  // max |d|, |rd| for the scaled-fp16 split (this thread's row, after the deltas below)
+    float md = 0.f, mr = 0.f;
+    if (b < B) {
+      output_delta_row(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
+      for (int j = 0; j < O; ++j) {
+        if (do0) md = fmaxf(md, fabsf(d[(size_t)b * O + j]));
+        if (do1) mr = fmaxf(mr, fabsf(rd[(size_t)b * O + j]));
+      }
+    }
+    if (mxd) slot_max(mxd, md);
+    if (mxrd) slot_max(mxrd, mr);
+    return;
+  }
   if (b >= B) return;
+  output_delta_row(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
+}
+
+__device__ void output_delta_row(int b, int O, int mse, int ncls, int do0, int do1, double scale,
+                                 const float* __restrict__ z, const float* __restrict__ rz,
+                                 const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
+                                 double* __restrict__ loss, int* __restrict__ correct) {
   const float* o = z + (size_t)b * O;
   const float* ro = do1 ? rz + (size_t)b * O : nullptr;
   float* dd = d + (size_t)b * O;
@@ -165,16 +304,24 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, in
 // write fp64 partials part[chunk][o]; the last block of each column block (ticket) adds the chunks
 // in order (deterministic, one launch).
 constexpr int kColChunks = 32;
+// (src32: the same sums over an fp32 B x cols source instead of the pairs — the scaled-fp16 mode, where the
+// exact fp32 deltas are at hand)
 __global__ void colsum_pairs_kernel(const bf16* __restrict__ hi, const bf16* __restrict__ lo, int ld, int off,
                                     int cols, int B, double* __restrict__ part, unsigned* __restrict__ tickets,
-                                    float* __restrict__ out) {
+                                    float* __restrict__ out, const float* __restrict__ src32) {
   __shared__ double sh[8][64];
   __shared__ bool last;
   const int c = blockIdx.x * 64 + 2 * threadIdx.x;
   const int rows_per = (B + kColChunks - 1) / kColChunks;
   const int r0 = blockIdx.y * rows_per, r1 = min(B, r0 + rows_per);
   float a0 = 0.f, a1 = 0.f;
-  if (c < cols) {
+  if (src32) {
+    if (c < cols)
+      for (int b = r0 + threadIdx.y; b < r1; b += 8) {
+        a0 += src32[(size_t)b * cols + c];
+        if (c + 1 < cols) a1 += src32[(size_t)b * cols + c + 1];
+      }
+  } else if (c < cols) {
 #pragma unroll 4
     for (int b = r0 + threadIdx.y; b < r1; b += 8) {
       const size_t i = (size_t)b * ld + off + c;
@@ -269,12 +416,24 @@ static void pack_params(dho2g_mlp* m, const float* p, const float* pscale, int h
   }
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
+    if (m->f16 && half == 1) {  // the W half fixes the layer's scale: max |W| first
+      if (t == 0) DHO2G_CUDA(cudaMemsetAsync(m->mx_w(0), 0, m->L * sizeof(unsigned), ctx->stream));
+      const size_t nw = (size_t)ld.in * ld.out;
+      absmax_kernel<<<(int)std::min<size_t>(cdiv(nw, 256), (size_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+          p + ld.w_off, nw, m->mx_w(t));
+      DHO2G_LAUNCH();
+    }
     const int slot = ctx->kt_begin();
     // one wave of resident blocks striding over the rows (short-lived per-row blocks cost more than the copy)
     const int gx = (int)cdiv(ld.in, 128 * kPackPer);
     const int gy = std::max(1, std::min(ld.out, ctx->sm_count * 16 / gx));
-    pack_weights_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
-                                                               m->WV_hi[t].p, m->WV_lo[t].p);
+    if (m->f16)
+      pack_weights_f16_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
+                                                                     m->mx_w(t), m->wv_vbound, m->s_wv(t),
+                                                                     m->WV_hi[t].p, m->WV_lo[t].p);
+    else
+      pack_weights_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(p + ld.w_off, pscale, ld.in, ld.out, ld.Pin, half,
+                                                                 m->WV_hi[t].p, m->WV_lo[t].p);
     DHO2G_LAUNCH();
     // algorithmic bytes: read fp32 (4) + write hi/lo (4)
     ctx->kt_end(slot, "pack_params", (double)ld.in * ld.out * 8.0);
@@ -286,9 +445,21 @@ static void pack_params(dho2g_mlp* m, const float* p, const float* pscale, int h
   }
 }
 
+// The operand format follows the ctx option; a change invalidates everything packed in the old one.
+static void sync_format(dho2g_mlp* m) {
+  const int f = m->ctx->gemm_f16 ? 1 : 0;
+  if (m->f16 == f) return;
+  m->f16 = f;
+  m->w_cur = nullptr;
+  m->input_owner = nullptr;
+  m->prepared = nullptr;
+}
+
 void mlp_load_weights(dho2g_mlp* m, const float* w) {
+  sync_format(m);
   m->w_cur = w;
   m->prepared = nullptr;
+  if (m->wv_vbound < 1.0f) m->wv_vbound = 1.0f;  // unit Lanczos directions
   pack_params(m, w, nullptr, 1);
 }
 
@@ -309,12 +480,35 @@ static void pack_rows(dho2g_ctx* ctx, int B, int s, int P, const float* X, const
   ctx->kt_end(slot, "pack_rows", (double)B * s * 4.0 * ((X ? 2.0 : 0.0) + (x1 ? 2.0 : 0.0)));
 }
 
+// level-j pair buffer as scaled fp16 from fp32 sources (see split_pair_kernel)
+static void split_pair(dho2g_mlp* m, int B, int s, int P, const float* X, const int64_t* idx, int ldX, const float* x32,
+                       const float* rx32, const unsigned* mxx, const unsigned* mxr, float* sout, bf16* Rh, bf16* Rl) {
+  dho2g_ctx* ctx = m->ctx;
+  const int slot = ctx->kt_begin();
+  const size_t work = (size_t)B * (P / 4);
+  const int grid = (int)std::max<size_t>(1, std::min<size_t>(cdiv(work, 256), (size_t)ctx->sm_count * 8));
+  split_pair_kernel<<<grid, 256, 0, ctx->stream>>>(B, s, P, X, idx, ldX, x32, rx32, mxx, mxr, sout, Rh, Rl);
+  DHO2G_LAUNCH();
+  ctx->kt_end(slot, "split_pair", (double)B * s * 8.0 * (((X || x32) ? 1.0 : 0.0) + (rx32 ? 1.0 : 0.0)));
+}
+
 void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool /*with_r*/) {
+  sync_format(m);
   m->ensure_batch(B);
   m->input_owner = nullptr;
   m->prepared = nullptr;
   const int s0 = (int)m->sizes[0];
-  pack_rows(m->ctx, (int)B, s0, (int)round_up(s0, 8), X, idx, s0, nullptr, m->AR_hi[0].p, m->AR_lo[0].p);
+  if (m->f16) {
+    dho2g_ctx* ctx = m->ctx;
+    DHO2G_CUDA(cudaMemsetAsync(m->mx_x(), 0, sizeof(unsigned), ctx->stream));
+    absmax_rows_kernel<<<dim3((unsigned)cdiv(s0, 256), (unsigned)std::min<size_t>(B, 1024)), 256, 0, ctx->stream>>>(
+        X, idx, s0, (int)B, s0, m->mx_x());
+    DHO2G_LAUNCH();
+    split_pair(m, (int)B, s0, (int)round_up(s0, 8), X, idx, s0, nullptr, nullptr, m->mx_x(), nullptr, m->s_ar(0),
+               m->AR_hi[0].p, m->AR_lo[0].p);
+  } else {
+    pack_rows(m->ctx, (int)B, s0, (int)round_up(s0, 8), X, idx, s0, nullptr, m->AR_hi[0].p, m->AR_lo[0].p);
+  }
   gather_labels_kernel<<<cdiv(B, 256), 256, 0, m->ctx->stream>>>((int)B, y, idx, m->lab.p);
   DHO2G_LAUNCH();
 }
@@ -323,6 +517,10 @@ void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* 
 // (RZ GEMM + fused R-epilogue over the cached activations).
 static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) {
   dho2g_ctx* ctx = m->ctx;
+  if (m->f16) {  // max slots of the levels this pass writes (a or ra, levels 1..L), one memset
+    if (do0) DHO2G_CUDA(cudaMemsetAsync(m->mx_a(1), 0, m->L * sizeof(unsigned), ctx->stream));
+    if (do1) DHO2G_CUDA(cudaMemsetAsync(m->mx_ra(1), 0, m->L * sizeof(unsigned), ctx->stream));
+  }
   for (int t = 0; t < m->L; ++t) {
     const LayerDesc& ld = m->layers[t];
     if (m->pack_pending) DHO2G_CUDA(cudaStreamWaitEvent(ctx->stream, m->pack_ev[t], 0));  // layer t packed
@@ -344,15 +542,25 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
       e.a_in = m->a32[t + 1].p;
       e.f0 = m->a32[t + 1].p;
       e.f1 = m->ra32[t + 1].p;
-      if (!last) {
+      if (m->f16) {  // fp32 outputs + max |.|, split below with the scale that covers them
+        e.f16 = 1;
+        e.sa = m->s_ar(t);
+        e.sb = m->s_wv(t);
+        if (!last) e.amax = r ? m->mx_ra(t + 1) : m->mx_a(t + 1);  // (cleared at the top)
+      } else if (!last) {
         e.Rh = m->AR_hi[t + 1].p; e.Rl = m->AR_lo[t + 1].p; e.P = ld.Pout; e.hR = r ? 1 : 0;
       }
-      if (!r)  // Z = A W^T
-        gemm3(ctx, (int)B, ld.out, ld.in, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p + ld.Pin,
-              m->WV_lo[t].p + ld.Pin, lda, e);
-      else  // RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
-        gemm3(ctx, (int)B, ld.out, t == 0 ? ld.in : 2 * ld.Pin, m->AR_hi[t].p, m->AR_lo[t].p, lda, m->WV_hi[t].p,
-              m->WV_lo[t].p, lda, e);
+      const int K = r ? (t == 0 ? ld.in : 2 * ld.Pin) : ld.in;
+      // Z = A W^T ; RZ = [A | RA] [V | W]^T (ra = 0 at the input layer: K = in only)
+      GOp A = gop_k(m->AR_hi[t].p, m->AR_lo[t].p, lda, K, (int)B);
+      GOp W = r ? gop_k(m->WV_hi[t].p, m->WV_lo[t].p, lda, K, ld.out)
+                : gop_k(m->WV_hi[t].p + ld.Pin, m->WV_lo[t].p + ld.Pin, lda, K, ld.out);
+      A.f16 = W.f16 = m->f16;
+      gemm3x(ctx, (int)B, ld.out, K, K, A, W, e);
+      if (m->f16 && !last)  // [a | ra] of level t+1: the R pass rewrites a too, so both halves share one scale
+        split_pair(m, (int)B, ld.out, ld.Pout, nullptr, nullptr, 0, m->a32[t + 1].p, r ? m->ra32[t + 1].p : nullptr,
+                   m->mx_a(t + 1), r ? m->mx_ra(t + 1) : nullptr, m->s_ar(t + 1), m->AR_hi[t + 1].p,
+                   m->AR_lo[t + 1].p);
     }
   }
   m->pack_pending = false;  // every layer's event has been waited on by the main stream
@@ -361,22 +569,31 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
 static void output_delta(dho2g_mlp* m, size_t B, size_t ncls, double scale, bool do0, bool do1) {
   const int L = m->L;
   const int O = (int)m->sizes[L];
-  output_delta_kernel<<<cdiv(B, 128), 128, 0, m->ctx->stream>>>((int)B, O, m->loss, (int)ncls, do0, do1, scale,
-                                                                   m->a32[L].p, m->ra32[L].p, m->lab.p, m->d32[L].p,
-                                                                   m->rd32[L].p, m->sample_loss.p,
-                                                                   m->sample_correct.p);
+  cudaStream_t st = m->ctx->stream;
+  unsigned* mxd = (m->f16 && do0) ? m->mx_d(L) : nullptr;
+  unsigned* mxrd = (m->f16 && do1) ? m->mx_rd(L) : nullptr;
+  if (mxd) DHO2G_CUDA(cudaMemsetAsync(mxd, 0, sizeof(unsigned), st));
+  if (mxrd) DHO2G_CUDA(cudaMemsetAsync(mxrd, 0, sizeof(unsigned), st));
+  output_delta_kernel<<<cdiv(B, 128), 128, 0, st>>>((int)B, O, m->loss, (int)ncls, do0, do1, scale, m->a32[L].p,
+                                                    m->ra32[L].p, m->lab.p, m->d32[L].p, m->rd32[L].p,
+                                                    m->sample_loss.p, m->sample_correct.p, mxd, mxrd);
   DHO2G_LAUNCH();
-  pack_rows(m->ctx, (int)B, O, (int)round_up(O, 64), do0 ? m->d32[L].p : nullptr, nullptr, O,
-            do1 ? m->rd32[L].p : nullptr, m->DR_hi[L].p, m->DR_lo[L].p);
+  if (m->f16)  // [d | rd]: the R pass rewrites d (cached) so both halves share one scale
+    split_pair(m, (int)B, O, (int)round_up(O, 64), nullptr, nullptr, 0, m->d32[L].p, do1 ? m->rd32[L].p : nullptr,
+               m->mx_d(L), do1 ? m->mx_rd(L) : nullptr, m->s_dr(L), m->DR_hi[L].p, m->DR_lo[L].p);
+  else
+    pack_rows(m->ctx, (int)B, O, (int)round_up(O, 64), do0 ? m->d32[L].p : nullptr, nullptr, O,
+              do1 ? m->rd32[L].p : nullptr, m->DR_hi[L].p, m->DR_lo[L].p);
 }
 
-static void bias_colsum(dho2g_mlp* m, const bf16* hi, const bf16* lo, int ld, int off, int cols, int B, float* out) {
+static void bias_colsum(dho2g_mlp* m, const bf16* hi, const bf16* lo, int ld, int off, int cols, int B, float* out,
+                        const float* src32 = nullptr) {
   dho2g_ctx* ctx = m->ctx;
   m->colpart.ensure_g((size_t)kColChunks * cols);
   m->coltickets.ensure_g(cdiv(cols, 64));  // zeroed at allocation; each launch leaves them zero
   const int slot = ctx->kt_begin();
   colsum_pairs_kernel<<<dim3(cdiv(cols, 64), kColChunks), dim3(32, 8), 0, ctx->stream>>>(
-      hi, lo, ld, off, cols, B, m->colpart.p, m->coltickets.p, out);
+      hi, lo, ld, off, cols, B, m->colpart.p, m->coltickets.p, out, src32);
   DHO2G_LAUNCH();
   ctx->kt_end(slot, "bias_colsum", 4.0 * cols * (double)B);  // algorithmic bytes: hi + lo
 }
@@ -419,6 +636,10 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
   const int L = m->L;
   const int Bi = (int)B;
   const int nrb = (int)cdiv(B, 32);
+  if (m->f16 && L > 1) {  // max slots of the hidden levels this pass writes (d or rd), one memset
+    if (do0) DHO2G_CUDA(cudaMemsetAsync(m->mx_d(1), 0, (L - 1) * sizeof(unsigned), ctx->stream));
+    if (do1) DHO2G_CUDA(cudaMemsetAsync(m->mx_rd(1), 0, (L - 1) * sizeof(unsigned), ctx->stream));
+  }
   // the bias block of layer t is the batch sum of level t+1's deltas: the epilogue that writes them (layer
   // t+1's backward GEMM) also writes per-32-row column sums into m->csum (two buffers, by level parity);
   // the output level's deltas come from the loss kernel and are summed by colsum_pairs_kernel
@@ -446,6 +667,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       GOp A{}, X{};
       A.hi = m->DR_hi[j].p; A.lo = m->DR_lo[j].p; A.ld = ldD; A.mn_major = 1; A.inner = ldD; A.outer = Bi;
       X.hi = m->AR_hi[t].p; X.lo = m->AR_lo[t].p; X.ld = ldA; X.mn_major = 1; X.inner = ldA; X.outer = Bi;
+      A.f16 = X.f16 = m->f16;
       int K, kseg;
       if (do1) {  // hvW = RD^T A + D^T RA ; hv_b = sum_b rd (oracle.cpp:606-613)
         A.off_in[0] = ld.Dout; A.off_in[1] = 0;
@@ -466,6 +688,11 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.C = out + ld.w_off;
       e.ldc = ld.in;
       e.alpha = 1.0f;
+      if (m->f16) {
+        e.f16 = 1;
+        e.sa = m->s_dr(j);
+        e.sb = m->s_ar(t);
+      }
       if (m->route) {  // fused reduce-scatter (dho2g_op::apply, hvp_route)
         e.route = m->route;
         e.route_flat0 = (long long)ld.w_off;
@@ -478,8 +705,9 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
           csum_final_kernel<<<cdiv(ld.out, 128), 128, 0, ctx->stream>>>(csum_buf(j), nrb, ld.out, out + ld.b_off);
           DHO2G_LAUNCH();
           ctx->kt_end(slot, "bias_sum", 4.0 * nrb * (double)ld.out);
-        } else {
-          bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off);
+        } else {  // (scaled fp16: the exact fp32 deltas)
+          bias_colsum(m, m->DR_hi[j].p, m->DR_lo[j].p, ldD, do1 ? ld.Dout : 0, ld.out, Bi, out + ld.b_off,
+                      m->f16 ? (do1 ? m->rd32[j].p : m->d32[j].p) : nullptr);
         }
         if (overlap) {
           bias_done = lane_event(ctx, evn++);
@@ -524,9 +752,18 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       e.ra_in = m->ra32[t].p;
       e.u_in = m->u32[t].p;
       e.u_out = wgrad ? nullptr : m->u32[t].p;  // U is only re-read by the R-epilogue of the HVP
-      e.f0 = nullptr;  // fp32 deltas of hidden levels are not re-read (bias blocks come from the pairs)
-      e.f1 = nullptr;
-      e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Din; e.hR = r ? 1 : 0;
+      if (m->f16) {  // fp32 deltas + max |.|, split below with the scale that covers them
+        e.f16 = 1;
+        e.sa = m->s_dr(j);
+        e.sb = m->s_wv(t);
+        e.f0 = m->d32[t].p;
+        e.f1 = m->rd32[t].p;
+        e.amax = r ? m->mx_rd(t) : m->mx_d(t);  // (levels 1..L-1 cleared at the top)
+      } else {
+        e.f0 = nullptr;  // fp32 deltas of hidden levels are not re-read (bias blocks come from the pairs)
+        e.f1 = nullptr;
+        e.Rh = m->DR_hi[t].p; e.Rl = m->DR_lo[t].p; e.P = ld.Din; e.hR = r ? 1 : 0;
+      }
       // column sums of the deltas this epilogue writes: rd for the Hessian's bias block, d for the gradient's
       const bool sums = (r && do1) || (!r && wgrad && !do1);
       e.csum = sums ? csum_buf(t) : nullptr;
@@ -535,6 +772,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       GOp A = gop_k(m->DR_hi[j].p, m->DR_lo[j].p, ldD, r ? ldD : ld.Dout, Bi);
       GOp W{};
       W.hi = m->WV_hi[t].p; W.lo = m->WV_lo[t].p; W.ld = ldA; W.mn_major = 1; W.inner = ldA; W.outer = ld.out;
+      A.f16 = W.f16 = m->f16;
       if (!r) {  // U = D W
         W.off_in[0] = ld.Pin;
         gemm3x(ctx, Bi, ld.in, ld.out, ld.out, A, W, e);
@@ -543,6 +781,9 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
         W.off_in[0] = 0; W.off_in[1] = ld.Pin;
         gemm3x(ctx, Bi, ld.in, ld.Dout + ld.out, ld.Dout, A, W, e);
       }
+      if (m->f16)  // [d | rd] of level t
+        split_pair(m, Bi, ld.in, ld.Din, nullptr, nullptr, 0, m->d32[t].p, r ? m->rd32[t].p : nullptr, m->mx_d(t),
+                   r ? m->mx_rd(t) : nullptr, m->s_dr(t), m->DR_hi[t].p, m->DR_lo[t].p);
     }
     if (overlap) ctx->gemm_worker_cap = 0;
   }
@@ -569,7 +810,12 @@ void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale) {
   m->prepared = m->w_cur;
 }
 
-void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv) {
+void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv,
+                 float vbound) {
+  if (m->f16 && vbound > m->wv_vbound) {  // the W halves' scale must also cover this direction
+    m->wv_vbound = vbound;
+    pack_params(m, m->w_cur, nullptr, 1);
+  }
   if (m->prepared != m->w_cur) mlp_prepare_point(m, B, ncls, scale);
   m->v_bias_ptr = v;
   m->v_scale_ptr = vscale;
