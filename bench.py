@@ -449,6 +449,86 @@ def run_ours(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- multi-rank launch
+def launch_cmd(argv, gpus, port):
+    """The torchrun command `bench.py --gpus N` re-executes itself under when started without a rank
+    environment: one rank per GPU, 127.0.0.1 rendezvous (the reference's run_workers, collectives.cpp:461-468,
+    one std::thread per worker -> one process per GPU here)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def self_launch(gpus):
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's init log names every rank
+    return subprocess.call(launch_cmd(sys.argv[1:], gpus, port), env=env)
+
+
+def run_fabric(args):
+    """--fabric: N ranks as host threads on ONE GPU joined by the in-process fabric (dho2g_comm_init_local):
+    the multi-rank code path (sharded basis/update, batch-split HVP, collectives as host rendezvous +
+    event-ordered copies) run end to end. A functional check of the launcher and the N-rank path, NOT a
+    multi-GPU measurement (the ranks share one GPU)."""
+    import threading
+
+    import paper_2505_00982_b200 as d
+    c = CONFIGS[args.config]
+    N = args.gpus
+    fab = d.LocalFabric(N)
+    res, errs = [None] * N, []
+    bar = threading.Barrier(N)
+    X, y = d.blobs_dataset(c["N"], c["sizes"][0], c["sizes"][-1], seed=7)
+
+    def worker(r):
+        ctx = d.Context(0)
+        try:
+            ctx.comm_init_local(fab, r)
+            mlp = d.MlpOracle(ctx, c["sizes"])
+            w0 = mlp.init_params(1)
+            cfg = d.TrainerConfig(kind="dho2", base=d.BaseConfig(c["base"]), k=c["k"], l=0, alpha=0.1, sigma=1e-2,
+                                  outer_rounds=10**6, inner_epochs=c["P"], batch_size=c["b"],
+                                  curvature_batch=c["curv"], seed=1, lanczos_m=c["m"])
+            tr = d.Trainer(ctx, cfg, mlp, d.Dataset(X, y, c["sizes"][-1], 7), w0, workers=c["workers"])
+            tr.step(args.warmup)
+            ctx.synchronize()
+            bar.wait()
+            r0 = tr.stat("refreshes")
+            ctx.mark(0)
+            for _ in range(args.steps):
+                tr.step(1)
+            ctx.mark(1)
+            res[r] = dict(ms=ctx.elapsed_ms(0, 1), refreshes=tr.stat("refreshes") - r0, world=ctx.world,
+                          loss=tr.last_loss(), ledger_rows=len(ctx.ledger()))
+            tr.close()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            bar.abort()
+        finally:
+            ctx.close()
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(N)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    fab.close()
+    if errs:
+        raise errs[0]
+    ms = max(r["ms"] for r in res)
+    line = {"metric": METRIC, "value": args.steps / (ms / 1e3), "unit": "steps/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_json(args.config, N),
+            "fabric": f"{N} ranks on one GPU through the in-process fabric: launcher / N-rank path check, "
+                      "not a multi-GPU measurement",
+            "ranks": [{"world": r["world"], "refreshes": r["refreshes"], "loss": r["loss"],
+                       "collective_rows": r["ledger_rows"]} for r in res]}
+    print(json.dumps(line), flush=True)
+
+
 def traffic_from_profiles(kernel):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -466,12 +546,24 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fabric", action="store_true",
+                    help="N ranks on ONE GPU via the in-process fabric (launcher / N-rank path check, not a measurement)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.fabric:
+        if args.impl == "reference":
+            ap.error("--fabric runs our arm only")
+        return run_fabric(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # started as `python bench.py --gpus N`: become N ranks (one per GPU) under torchrun
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; timing {world} ranks", file=sys.stderr)
     dist = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))

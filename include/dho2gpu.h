@@ -250,6 +250,9 @@ int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const f
 /* ---- test hook: each collective wrapper through a 1-rank NCCL communicator (plumbing check on one GPU).
  * The context must have no communicator; *max_err = worst element error (0 expected). */
 int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err);
+/* The same collectives captured into a CUDA graph and replayed (the multi-rank refresh graph captures
+ * its NCCL calls this way). */
+int dho2g_test_collectives_graph(dho2g_ctx* ctx, double* max_err);
 /* ---- test hook: per-CTA timelines (globaltimer ns: start, last MMA, last epilogue start, end) of pair-GEMM
  * launches; on = 1 arms a buffer for n_ctas CTA slots, on = 0 copies it to out and disarms. */
 int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_t n_ctas);

@@ -70,6 +70,7 @@ _SIGS = {
     "dho2g_ctx_accounting_reset": ([vp], C.c_int),
     "dho2g_ctx_allgather_host": ([vp, dp, C.c_size_t, dp], C.c_int),
     "dho2g_test_collectives": ([vp, dp], C.c_int),
+    "dho2g_test_collectives_graph": ([vp, dp], C.c_int),
     "dho2g_test_gemm_trace": ([vp, C.c_int, C.POINTER(C.c_uint64), C.c_size_t], C.c_int),
     "dho2g_rng_u64": ([C.c_uint64, C.c_size_t, up], None),
     "dho2g_rng_normal": ([C.c_uint64, C.c_size_t, dp], None),

@@ -33,6 +33,7 @@ int guard(F&& f) {
 
 void check_ctx(dho2g_ctx* c) {
   if (!c) fail(DHO2G_ARGUMENT, "null context");
+  c->check_usable();
   DHO2G_CUDA(cudaSetDevice(c->device));
 }
 
@@ -167,6 +168,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "tql2_split") ctx->tql2_split = (int)value;
     else if (k == "gs_sm_cap") ctx->gs_sm_cap = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
+    else if (k == "graphs_multirank") ctx->graphs_multirank = (int)value;
     else if (k == "ktimers") {
       ctx->kt_flush();
       ctx->ktimers = value != 0.0;
@@ -1020,10 +1022,16 @@ int dho2g_trainer_destroy(dho2g_trainer* tr) {
   return guard([&] { trainer_destroy(tr); });
 }
 int dho2g_trainer_step(dho2g_trainer* tr, size_t steps, int with_eval) {
-  return guard([&] { trainer_step(tr, steps, with_eval); });
+  return guard([&] {
+    check_ctx(trainer_ctx(tr));
+    trainer_step(tr, steps, with_eval);
+  });
 }
 int dho2g_trainer_run(dho2g_trainer* tr) {
-  return guard([&] { trainer_run(tr); });
+  return guard([&] {
+    check_ctx(trainer_ctx(tr));
+    trainer_run(tr);
+  });
 }
 int dho2g_trainer_params(dho2g_trainer* tr, double* w) {
   return guard([&] { trainer_params(tr, w); });
@@ -1254,6 +1262,72 @@ int dho2g_test_collectives(dho2g_ctx* ctx, double* max_err) {
     }
     ctx->nccl_force = false;
     dho2g::nccl().CommAbort(ctx->comm);  // non-blocking communicator: abort releases it at once
+    ctx->comm = nullptr;
+    *max_err = err;
+  });
+}
+
+// Test hook: the same collectives captured into a CUDA graph (as the multi-rank refresh graph captures
+// them), instantiated and replayed twice on a 1-rank NCCL communicator. *max_err: worst element error.
+int dho2g_test_collectives_graph(dho2g_ctx* ctx, double* max_err) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (ctx->world != 1 || ctx->comm) fail(DHO2G_ARGUMENT, "test_collectives: needs a context without a communicator");
+    ncclUniqueId id;
+    DHO2G_NCCLCHK(dho2g::nccl().GetUniqueId(&id));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    dho2g::nccl_call(ctx, dho2g::nccl().CommInitRankConfig(&ctx->comm, 1, id, 0, &cfg), "comm_init");
+    dho2g::nccl_settle(ctx, "comm_init");
+    ctx->nccl_force = true;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    double err = 0.0;
+    try {
+      cudaStream_t st = ctx->stream;
+      const size_t n = 4099;
+      std::vector<float> hf(n), of(n);
+      std::vector<double> hd(n), od(n);
+      for (size_t i = 0; i < n; ++i) {
+        hf[i] = (float)(i % 89) - 44.5f;
+        hd[i] = 1.0 / (double)(i + 3);
+      }
+      DevBuf<float> a(n), b(n), c(n);
+      DevBuf<double> x(n);
+      DHO2G_CUDA(cudaMemcpyAsync(a.p, hf.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+      DHO2G_CUDA(cudaMemcpyAsync(x.p, hd.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+      DHO2G_CUDA(cudaStreamSynchronize(st));
+      ctx->gather_f64.ensure(n);  // allocation outside the capture
+      DHO2G_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      ctx->allgather_f32(a.p, b.p, n);
+      ctx->reduce_scatter_f32(b.p, c.p, n);
+      ctx->allreduce_sum_f64_ordered(x.p, n);
+      DHO2G_CUDA(cudaStreamEndCapture(st, &g));
+      DHO2G_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      for (int rep = 0; rep < 2; ++rep) {
+        DHO2G_CUDA(cudaMemsetAsync(c.p, 0, n * sizeof(float), st));
+        DHO2G_CUDA(cudaGraphLaunch(ge, st));
+        DHO2G_CUDA(cudaMemcpyAsync(of.data(), c.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+        DHO2G_CUDA(cudaMemcpyAsync(od.data(), x.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        ctx->sync();
+        for (size_t i = 0; i < n; ++i) {
+          err = std::max(err, (double)std::fabs(of[i] - hf[i]));
+          err = std::max(err, std::fabs(od[i] - hd[i]));
+        }
+      }
+      ctx->bump("test_graph_nodes", 1);
+    } catch (...) {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      ctx->nccl_force = false;
+      if (ctx->comm) dho2g::nccl().CommAbort(ctx->comm);
+      ctx->comm = nullptr;
+      throw;
+    }
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    ctx->nccl_force = false;
+    dho2g::nccl().CommAbort(ctx->comm);
     ctx->comm = nullptr;
     *max_err = err;
   });

@@ -208,18 +208,23 @@ int tridiag_eig_host(size_t n, const double* diag, const double* off, double* va
 
 // ------------------------------------------------------------------------- context collectives
 void dho2g_ctx::sync() { dho2g::wait_stream(this, stream); }
+void dho2g_ctx::check_usable() const {
+  if (failed)
+    dho2g::fail(DHO2G_NCCL, "context unusable after a failed collective (" + failed_msg +
+                                "); create a new context and communicator");
+}
 
 namespace dho2g {
 // Failure detection (the reference's DeadlockError, collectives.cpp:257-262): with a communicator,
 // host waits poll the stream and NCCL's asynchronous error state instead of blocking, so a rank that
 // never arrives (or a failed peer) surfaces as DEADLOCK / NCCL after ctx->nccl_timeout_s instead of
-// a hang; the communicator is aborted first (its kernels are released) and the context falls back to
-// a single rank.
+// a hang; the communicator is aborted first (its kernels are released) and the context is marked failed
+// (it does not go on as a single rank with the failed group's shards).
 static void nccl_give_up(dho2g_ctx* ctx, int code, const std::string& msg) {
   if (ctx->comm) nccl().CommAbort(ctx->comm);
   ctx->comm = nullptr;
-  ctx->world = 1;
-  ctx->rank = 0;
+  ctx->failed = true;  // every later call on this context raises (dho2g_ctx::check_usable)
+  ctx->failed_msg = msg;
   fail(code, msg);
 }
 
@@ -367,6 +372,7 @@ static void fabric_collective(dho2g_ctx* ctx, const void* send, void* recv, size
 }
 
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
+  check_usable();
   if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
     return;
@@ -381,6 +387,7 @@ void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, co
 }
 
 void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, const char* op) {
+  check_usable();
   if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;
@@ -394,6 +401,7 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, cons
 }
 
 void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count) {
+  check_usable();
   if (world == 1 && !nccl_force) {
     if (send != recv) DHO2G_CUDA(cudaMemcpyAsync(recv, send, count * sizeof(float), cudaMemcpyDeviceToDevice, stream));
     return;

@@ -81,7 +81,14 @@ struct dho2g_ctx {
   dho2g_fabric* fabric = nullptr;  // in-process test backend (dho2g_comm_init_local) instead of NCCL
   dho2g::DevBuf<float> fabric_scratch;
   int rank = 0, world = 1;
+  int graphs_multirank = 1;  // refresh CUDA graph also at world > 1 (NCCL communicator; not the fabric)
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
+  // Set when a collective failed (DEADLOCK / NCCL): the communicator is aborted and every later call on
+  // this context raises (its shards, offsets and buffers belong to the failed group, so it must not go on
+  // as a single rank). The reference throws out of the failed round the same way (collectives.cpp:257-262).
+  bool failed = false;
+  std::string failed_msg;
+  void check_usable() const;
   double nccl_timeout_s = 600.0;  // host waits with a communicator give up (DEADLOCK) after this long
   void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled
   std::map<std::string, double> stats;
@@ -458,6 +465,7 @@ void check_opt_flags(dho2g_opt* o);
 
 struct dho2g_trainer;
 namespace dho2g {
+dho2g_ctx* trainer_ctx(dho2g_trainer* tr);
 dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_mlp* mlp, const double* X,
                               const double* y, size_t N, size_t ncls, uint64_t dataset_seed, const double* w0,
                               int workers, int host_resident, dho2g_op* quad = nullptr);

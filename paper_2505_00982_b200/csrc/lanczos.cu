@@ -1210,7 +1210,11 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
 static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, bool launch = true) {
   dho2g_ctx* ctx = lz->ctx;
   cudaStream_t st = ctx->stream;
-  if (!ctx->use_graphs || ctx->world != 1 || ctx->ktimers || op->kind == 3 || lz->graph_failed) return false;
+  // multi-rank: NCCL collectives are captured with the kernels (dho2g_test_collectives_graph); the in-process
+  // fabric's host rendezvous cannot be
+  if (!ctx->use_graphs || (ctx->world != 1 && (ctx->fabric || !ctx->graphs_multirank)) || ctx->ktimers ||
+      op->kind == 3 || lz->graph_failed)
+    return false;
   lz->seed_dev.ensure(1);
   lz->seed_host.ensure(1);
   const bool valid = lz->gexec && lz->gop == op && lz->gm == lz->m && lz->ggen == g_graph_gen &&

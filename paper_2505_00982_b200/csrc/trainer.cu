@@ -631,6 +631,10 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
 }  // namespace dho2g
 
 namespace dho2g {
+dho2g_ctx* trainer_ctx(dho2g_trainer* tr) {
+  if (!tr) fail(DHO2G_ARGUMENT, "null trainer");
+  return tr->ctx;
+}
 void trainer_step(dho2g_trainer* tr, size_t steps, int with_eval) {
   for (size_t s = 0; s < steps && !tr->done; ++s) tr->step_one(with_eval != 0);
 }

@@ -554,6 +554,16 @@ def test_nccl_collectives_one_rank(ctx):
     ctx.reset_accounting()
 
 
+def test_nccl_collectives_captured_in_graph(ctx):
+    """The multi-rank refresh graph captures its NCCL calls: all-gather, reduce-scatter and the ordered
+    fp64 all-reduce captured into a CUDA graph on a 1-rank NCCL communicator, replayed twice, exact."""
+    import ctypes as C
+    from paper_2505_00982_b200._lib import lib
+    err = C.c_double(-1.0)
+    d.check(lib.dho2g_test_collectives_graph(ctx.h, C.byref(err)))
+    assert err.value == 0.0
+
+
 def test_missing_rank_is_deadlock_error():
     """test_collectives.cpp:245-258 on the device path: a rank that never joins surfaces as
     DeadlockError after the timeout (non-blocking NCCL init + polling + abort), not a hang. Run in a
@@ -570,11 +580,17 @@ def test_missing_rank_is_deadlock_error():
         "    print('NO ERROR')\n"
         "except d.DeadlockError as e:\n"
         "    print('DEADLOCK', round(time.time() - t0, 1), c.world, e)\n"
+        "try:\n"  # the failed context refuses further work instead of running on as one rank
+        "    d.MlpOracle(c, [2, 3, 2])\n"
+        "    print('STILL USABLE')\n"
+        "except d.NcclError as e:\n"
+        "    print('FAILED CONTEXT', e)\n"
     )
     root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=180)
     line = [ln for ln in out.stdout.splitlines() if ln.startswith("DEADLOCK")]
     assert line, out.stdout + out.stderr
     secs, world = line[0].split()[1:3]
-    assert 2.5 <= float(secs) < 60 and world == "1"
+    assert 2.5 <= float(secs) < 60 and world == "2"
     assert "timed out on rank 0" in out.stdout
+    assert "FAILED CONTEXT" in out.stdout and "unusable after a failed collective" in out.stdout
