@@ -521,7 +521,8 @@ using namespace tc;
 constexpr int BM = 128, BN = 128, STAGES = 3;
 constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;
 constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
-constexpr uint32_t TMEM_COLS = ACC * BN;
+constexpr uint32_t TMEM_COLS = 4 * BN;  // two accumulators + the chunked-accumulation running sum (+ spare)
+constexpr uint32_t SUM_COL = ACC * BN;
 
 struct Sched {
   int mt, nt, tiles, splits, units, nkb, kseg;  // nkb: k-blocks total
@@ -647,15 +648,11 @@ __global__ void __launch_bounds__(384, 1)
     const int chalf = (warp - 4) >> 2;
     float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
     uint32_t uc = 0;
-    // this thread's elements of the fp32 running sum over a unit's chunks (thread-private, same layout as
-    // the split-K partials)
-    float* run = ws ? ws + ((size_t)sc.tiles + blockIdx.x) * BM * BN + (size_t)(ew + 4 * chalf) * (32 * BN / 2) +
-                          (size_t)lane * 4
-                    : nullptr;
+    const uint32_t tsum = tmem + ((uint32_t)(ew * 32) << 16) + SUM_COL;  // chunk running sum (TMEM)
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
       sc.unit(u, m0, n0, split, tile, kb0, kb1);
-      // chunks before the last: TMEM -> += running sum (fp32, round to nearest) -> free the accumulator
+      // chunks before the last: running sum (TMEM) += chunk (round-to-nearest fp32), free the accumulator
       const int nchunks = kb1 > kb0 ? (kb1 - kb0 + sc.chunk - 1) / sc.chunk : 1;
       for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
         const uint32_t ab = uc % ACC;
@@ -663,20 +660,9 @@ __global__ void __launch_bounds__(384, 1)
         fence_after();
         const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
 #pragma unroll 1
-        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
-          float v[16];
-          tmem_ld16(tb + (uint32_t)c0, v);
-          float* q = run + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float4 t = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            if (c > 0) {
-              const float4 o = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
-              t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
-            }
-            __stcg(reinterpret_cast<float4*>(q + j * 128), t);
-          }
-        }
+        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16)
+          tmem_drain16(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
+        tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[ab]);
@@ -702,12 +688,10 @@ __global__ void __launch_bounds__(384, 1)
         float v[16];
         tmem_ld16(tbase + (uint32_t)c0, v);
         if (nchunks > 1) {  // + the earlier chunks
-          const float* q = run + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+          float t[16];
+          tmem_ld16(tsum + (uint32_t)c0, t);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
-            v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
-          }
+          for (int j = 0; j < 16; ++j) v[j] += t[j];
         }
         if (split > 0) {
           const float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
@@ -808,13 +792,8 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   float* ws = nullptr;
   unsigned* flags = nullptr;
   unsigned epoch = 0;
-  const int ctas1 = std::min(sc.units, ctas);
-  if (sc.chunk < per_unit) {  // running sums after the split-K partials: one BM x BN slot per CTA
-    ctx->gemm_ws.ensure_g(((size_t)sc.tiles + ctas1) * BM * BN);
-    ws = ctx->gemm_ws.p;
-  }
   if (sc.splits > 1) {
-    ctx->gemm_ws.ensure_g(((size_t)sc.tiles + (sc.chunk < per_unit ? ctas1 : 0)) * BM * BN);
+    ctx->gemm_ws.ensure_g((size_t)sc.tiles * BM * BN);
     ctx->gemm_flags.ensure_g((size_t)sc.tiles);
     ws = ctx->gemm_ws.p;
     flags = ctx->gemm_flags.p;
@@ -1049,8 +1028,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t ID = idesc_fmt(idesc(256, tile_cols<NT>(wk, n0), AMN, BMN), e.f16 != 0);
      for (int c0 = sg.k0; c0 < sg.k1; c0 += wk.chunk) {  // one accumulator per chunk
       const int c1 = min(sg.k1, c0 + wk.chunk);
-      const uint32_t ab = uc % ACC;
-      mbar_wait_cluster(&tempty[ab], ((uc / ACC) & 1) ^ 1);
+      // chunked: one accumulator (the other TMEM half holds the running sum); else double-buffered
+      const uint32_t nacc = wk.chunk < wk.nkb ? 1u : (uint32_t)ACC;
+      const uint32_t ab = uc % nacc;
+      mbar_wait_cluster(&tempty[ab], ((uc / nacc) & 1) ^ 1);
       fence_after();
       const uint32_t acc_addr = tmem + ab * NT;
       for (int kb = c0; kb < c1; ++kb, ++it) {
@@ -1091,52 +1072,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     Cursor cur;
     cur.init(wk, worker);
     Seg sg;
-    // this thread's elements of the fp32 running sum over a segment's chunks (thread-private, after the
-    // stream-K partial slots)
-    float* run = ws + ((size_t)(2 * wk.workers + worker) * 2 + rank) * PART_FLOATS + slot_off;
+    const uint32_t nacc = wk.chunk < wk.nkb ? 1u : (uint32_t)ACC;  // chunked: TMEM half 1 = running sum
+    const uint32_t tsum = tmem + ((uint32_t)(ew * 32) << 16) + NT;
     while (cur.next(wk, sg)) {
       const int m0 = sg.mtile * 256 + (int)rank * BM, n0 = sg.ntile * NT;
       const int ncols = tile_cols<NT>(wk, n0);
-      // chunks before the last: TMEM -> += running sum (fp32, round to nearest) -> free the accumulator
+      // chunks before the last: running sum (TMEM) += chunk (round-to-nearest fp32), free the accumulator
       const int nchunks = (sg.k1 - sg.k0 + wk.chunk - 1) / wk.chunk;
       for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
-        const uint32_t ab = uc % ACC;
-        mbar_wait(&tfull[ab], (uc / ACC) & 1);
+        const uint32_t ab = uc % nacc;
+        mbar_wait(&tfull[ab], (uc / nacc) & 1);
         fence_after();
         const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
 #pragma unroll 1
         for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
           if (c0 >= ncols) break;
-          float v[16];
-          tmem_ld16(tb + (uint32_t)c0, v);
-          float* q = run + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float4 t = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            if (c > 0) {
-              const float4 o = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
-              t.x += o.x; t.y += o.y; t.z += o.z; t.w += o.w;
-            }
-            __stcg(reinterpret_cast<float4*>(q + j * 128), t);
-          }
+          tmem_drain16(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
         }
+        tmem_wait_st();
         fence_before();
         __syncwarp();
         if (lane == 0) arrive_leader(&tempty[ab]);
       }
-      const uint32_t ab = uc % ACC;
-      mbar_wait(&tfull[ab], (uc / ACC) & 1);
+      const uint32_t ab = uc % nacc;
+      mbar_wait(&tfull[ab], (uc / nacc) & 1);
       fence_after();
       if (trace && threadIdx.x == 128) trace[2] = gtimer();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
       auto add_run = [&](int c0, float (&v)[16]) {  // + the earlier chunks
         if (nchunks < 2) return;
-        const float* q = run + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
+        float t[16];
+        tmem_ld16(tsum + (uint32_t)c0, t);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 t = __ldcg(reinterpret_cast<const float4*>(q + j * 128));
-          v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
-        }
+        for (int j = 0; j < 16; ++j) v[j] += t[j];
       };
       if (sg.k0 != 0) {
         // non-head segment (first of this worker): publish the raw partial
@@ -1239,10 +1207,10 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;
   wk.dp = (ctx->gemm_dp && waves >= 2) ? (int)((waves - 1) * wk.workers) : 0;
-  // stream-K partial slots (2 schedule parts x workers x 2 CTAs) + one running-sum slot per CTA
-  ctx->gemm_ws.ensure_g((size_t)3 * wk.workers * 2 * PART_MAX);
+  // stream-K partial slots (2 schedule parts x workers x 2 CTAs)
+  ctx->gemm_ws.ensure_g((size_t)2 * wk.workers * 2 * PART_MAX);
   ctx->gemm_flags.ensure_g((size_t)2 * wk.workers * 2 + 16);
-  wk.chunk = ctx->gemm_chunk_kb > 0 ? ctx->gemm_chunk_kb : wk.nkb;
+  wk.chunk = (e.chunk_kb > 0 && e.chunk_kb < wk.nkb) ? e.chunk_kb : wk.nkb;
   unsigned epoch = ++ctx->gemm_epoch;
   if (epoch >= (1u << 27)) {  // flags hold epoch * 16 + 15 here (epoch * 16 + split in tc1): recycle
     DHO2G_CUDA(cudaMemsetAsync(ctx->gemm_flags.p, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
@@ -1302,9 +1270,9 @@ void gemm_presize(dho2g_ctx* ctx) {
   // both lanes' stream-K partials (2 schedule parts x pairs x 2 CTAs x 128 x 256) and flags; covers the
   // single-CTA kernel's split-K partials for the small-M GEMMs too
   const size_t pairs = (size_t)std::max(1, ctx->sm_count / 2);
-  ctx->gemm_ws.ensure_g(3 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_ws.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
   ctx->gemm_flags.ensure_g(2 * pairs * 2 + 16);
-  ctx->gemm_ws2.ensure_g(3 * pairs * 2 * tc2::PART_MAX);
+  ctx->gemm_ws2.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
   ctx->gemm_flags2.ensure_g(2 * pairs * 2 + 16);
 }
 

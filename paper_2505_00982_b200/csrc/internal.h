@@ -54,9 +54,10 @@ struct dho2g_ctx {
   int hvp_route = 0;      // world > 1: batch-split HVP partials stored straight into the owners' buffers
                          // (peer memory) instead of a reduce-scatter after the HVP
   int bwd_overlap = 1;   // backward: weight-block GEMM on a side stream, concurrent with the delta GEMM
-  int gemm_chunk_kb = 0; // tcgen05 GEMMs: drain the TMEM accumulator into an fp32 running sum every this many
-                         // 64-deep k-blocks (0: never). The tensor core's accumulation truncates, so its error
-                         // grows with the chain length; short chains + round-to-nearest fp32 sums bound it.
+  int gemm_chunk_kb = 8;  // HVP (curvature) GEMMs on the CTA-pair kernel: drain the TMEM accumulator into an
+                         // fp32 running sum every this many 64-deep k-blocks (0: never). The tensor core's
+                         // accumulation truncates, so its error grows with the chain length (measured: linear);
+                         // short chains + round-to-nearest fp32 sums bound it.
   int gemm_chunk_kb1 = 8; // the same for the single-CTA kernel (small-M GEMMs: C1/C2 HVPs and gradients), where
                          // the drains are cheap
   int gemm_f16 = 1;      // MLP GEMM operands as power-of-two-scaled fp16 (hi, lo) pairs (22 significant bits)
@@ -198,6 +199,7 @@ struct dho2g_mlp {
   //   amax[j] a_j, amax[(L+1) + j] ra_j, amax[2(L+1) + j] d_j, amax[3(L+1) + j] rd_j (j <= L),
   //   amax[4(L+1) + t] W_t, amax[4(L+1) + L] the level-0 input batch.
   int f16 = 0;              // format of the currently packed operands
+  int chunk_kb = 0;         // Epi::chunk_kb of the GEMMs being issued (the HVP path sets it)
   float wv_vbound = 0.f;    // bound on |direction| the WV scales were chosen for
   dho2g::DevBuf<float> scl;
   dho2g::DevBuf<unsigned> amax;
@@ -286,6 +288,9 @@ struct Epi {
   const float* sa;
   const float* sb;
   unsigned* amax;
+  // CTA-pair kernel: k-blocks per TMEM accumulation chunk, drained into an fp32 running sum in TMEM (0: one
+  // chain per segment). Set for the curvature (HVP) GEMMs, whose precision the Lanczos refresh needs.
+  int chunk_kb;
 };
 // One GEMM operand: a (hi, lo) bf16 pair buffer read through a TMA-style window. K-major: rows are
 // the M (or N) index, K contiguous; MN-major: rows are the K index, M (or N) contiguous. The K range

@@ -530,6 +530,7 @@ static void forward(dho2g_mlp* m, const float* w, size_t B, bool do0, bool do1) 
       const bool r = pass == 1;
       if ((r && !do1) || (!r && !do0)) continue;
       Epi e{};
+      e.chunk_kb = m->chunk_kb;
       e.mode = last ? EPI_FWD_OUT : EPI_FWD;
       e.M = (int)B;
       e.N = ld.out;
@@ -682,6 +683,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
         K = kseg = Bi;
       }
       Epi e{};
+      e.chunk_kb = m->chunk_kb;
       e.mode = EPI_STORE;
       e.M = ld.out;
       e.N = ld.in;
@@ -742,6 +744,7 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
       const bool r = pass == 1;
       if ((r && !do1) || (!r && !do0)) continue;
       Epi e{};
+      e.chunk_kb = m->chunk_kb;
       e.mode = EPI_BWD;
       e.M = Bi;
       e.N = ld.in;
@@ -802,8 +805,16 @@ void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, 
   backward(m, B, g, true, false, true);
 }
 
+// The curvature GEMMs (the HVP point and the HVPs) run with chunked TMEM accumulation (ctx gemm_chunk_kb).
+struct ChunkScope {
+  dho2g_mlp* m;
+  explicit ChunkScope(dho2g_mlp* mm) : m(mm) { m->chunk_kb = m->ctx->gemm_chunk_kb; }
+  ~ChunkScope() { m->chunk_kb = 0; }
+};
+
 void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale) {
   // input and weights must already be loaded (mlp_set_input / mlp_load_weights)
+  ChunkScope cs(m);
   forward(m, m->w_cur, B, true, false);
   output_delta(m, B, ncls, scale, true, false);
   backward(m, B, nullptr, true, false, false);
@@ -817,6 +828,7 @@ void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, si
     pack_params(m, m->w_cur, nullptr, 1);
   }
   if (m->prepared != m->w_cur) mlp_prepare_point(m, B, ncls, scale);
+  ChunkScope cs(m);
   m->v_bias_ptr = v;
   m->v_scale_ptr = vscale;
   mlp_load_direction(m, v, vscale);
