@@ -9,7 +9,7 @@ OBJS     := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 HDRS     := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/dho2gpu.h
 LIB      := $(PKG)/libdho2gpu.so
 
-all: $(LIB) oracle
+all: $(LIB) oracle dropin
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -ldl -lpthread -lrt
@@ -26,4 +26,8 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+# the reference-side drop-in test binary (needs the reference objects and the library)
+dropin: $(LIB) oracle
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C integration; fi
+
+.PHONY: all oracle dropin clean

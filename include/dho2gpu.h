@@ -165,6 +165,9 @@ size_t dho2g_ese_count(const dho2g_ese* ese);
 int dho2g_ese_eigvals(const dho2g_ese* ese, double* vals);
 /* This rank's rows of V_hat (sign convention of lanczos.cpp:82-94 applied), column-major. */
 int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs_shard);
+/* The full V_hat (n x r, column-major) on every rank, as extract_ese_distributed returns it after its
+ * gather_rows (dist_lanczos.cpp:148-156). Collective: every rank calls it. */
+int dho2g_ese_gather(const dho2g_ese* ese, double* vecs_full);
 /* Build an ESE from host data (tests feed the reference's eigenpairs): V is n x r column-major. */
 int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, size_t n, size_t r,
                         dho2g_ese** out);

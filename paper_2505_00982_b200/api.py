@@ -675,6 +675,15 @@ class EseResult:
             check(lib.dho2g_ese_eigvecs(self.h, _d(out)))
         return out.reshape(r, rows).T
 
+    def eigvecs_full(self, n: int):
+        """The full V_hat (n x r) on every rank (extract_ese_distributed's gather_rows,
+        dist_lanczos.cpp:148-156); collective at world > 1."""
+        r = self.count()
+        out = np.empty(n * r)
+        if r:
+            check(lib.dho2g_ese_gather(self.h, _d(out)))
+        return out.reshape(r, n).T
+
     @classmethod
     def from_host(cls, ctx: Context, eigvals, V):
         eigvals = _f64(eigvals)

@@ -557,6 +557,7 @@ int dho2g_mlp_value(dho2g_mlp* m, const double* w, const double* X, const double
                     double* out) {
   return guard([&] {
     check_ctx(m->ctx);
+    std::lock_guard<std::mutex> lk(m->ctx->api_mu);
     check_batch(m, B, ncls);
     mlp_stage(m, w, X, y, B);
     m->red.ensure(2 * 16);
@@ -574,6 +575,7 @@ int dho2g_mlp_accuracy(dho2g_mlp* m, const double* w, const double* X, const dou
                        double* acc) {
   return guard([&] {
     check_ctx(m->ctx);
+    std::lock_guard<std::mutex> lk(m->ctx->api_mu);
     if (ncls == 0) {  // oracle.cpp:650: nullopt for regression
       *acc = -1.0;
       return;
@@ -595,6 +597,7 @@ int dho2g_mlp_grad(dho2g_mlp* m, const double* w, const double* X, const double*
                    double* g) {
   return guard([&] {
     check_ctx(m->ctx);
+    std::lock_guard<std::mutex> lk(m->ctx->api_mu);
     check_batch(m, B, ncls);
     mlp_stage(m, w, X, y, B);
     m->out32.ensure(m->dim);
@@ -608,6 +611,7 @@ int dho2g_mlp_hvp(dho2g_mlp* m, const double* w, const double* v, const double* 
                   size_t ncls, double* hv) {
   return guard([&] {
     check_ctx(m->ctx);
+    std::lock_guard<std::mutex> lk(m->ctx->api_mu);
     check_batch(m, B, ncls);
     mlp_stage(m, w, X, y, B);
     upload(m->v32, v, m->dim, m->ctx->stream);
@@ -844,6 +848,40 @@ int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs) {
       if (ese->rows)
         DHO2G_CUDA(cudaMemcpy(f.data(), ese->V.p + c * ese->ldv, ese->rows * sizeof(float), cudaMemcpyDeviceToHost));
       for (size_t r = 0; r < ese->rows; ++r) vecs[c * ese->rows + r] = (double)(ese->sign[c] * f[r]);
+    }
+  });
+}
+
+// The full V_hat (n x r, column-major) on every rank: extract_ese_distributed's gather_rows
+// (dist_lanczos.cpp:148-156) for callers that need the reference's EseResult shape. One all-gather of
+// each column's padded shard (equal counts on every rank), rows reassembled by Shard::for_rank.
+int dho2g_ese_gather(const dho2g_ese* ese, double* vecs_full) {
+  return guard([&] {
+    dho2g_ctx* ctx = ese->ctx;
+    check_ctx(ctx);
+    const int W = ctx->world;
+    if (W == 1) {
+      DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::vector<float> f(ese->rows);
+      for (size_t c = 0; c < ese->r; ++c) {
+        if (ese->rows)
+          DHO2G_CUDA(cudaMemcpy(f.data(), ese->V.p + c * ese->ldv, ese->rows * sizeof(float), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < ese->rows; ++i) vecs_full[c * ese->n + i] = (double)(ese->sign[c] * f[i]);
+      }
+      return;
+    }
+    DevBuf<float> all((size_t)W * ese->ldv);
+    std::vector<float> h((size_t)W * ese->ldv);
+    for (size_t c = 0; c < ese->r; ++c) {
+      ctx->allgather_f32(ese->V.p + c * ese->ldv, all.p, ese->ldv, "gather_rows");
+      DHO2G_CUDA(cudaMemcpyAsync(h.data(), all.p, h.size() * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+      ctx->sync();
+      for (int q = 0; q < W; ++q) {
+        size_t b, e;
+        shard_range(ese->n, W, q, &b, &e);
+        for (size_t i = 0; i < e - b; ++i)
+          vecs_full[c * ese->n + b + i] = (double)(ese->sign[c] * h[(size_t)q * ese->ldv + i]);
+      }
     }
   });
 }

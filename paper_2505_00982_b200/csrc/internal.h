@@ -89,6 +89,11 @@ struct dho2g_ctx {
   // as a single rank). The reference throws out of the failed round the same way (collectives.cpp:257-262).
   bool failed = false;
   std::string failed_msg;
+  // Serialises the host-API oracle entry points (dho2g_mlp_value/grad/hvp/accuracy) on this context: they
+  // stage through the model's buffers and the context stream, and the reference calls Oracle::grad / hvp
+  // from every worker thread at once (trainer.cpp:92-103, dist_lanczos.cpp:79; "safe for concurrent use",
+  // oracle.hpp:70-71).
+  std::mutex api_mu;
   void check_usable() const;
   double nccl_timeout_s = 600.0;  // host waits with a communicator give up (DEADLOCK) after this long
   void* encode_fn = nullptr;  // PFN_cuTensorMapEncodeTiled

@@ -90,6 +90,26 @@ def test_lanczos_mlp_sharded(world):
         assert "reduce_scatter" in {r[1] for r in ledger}  # batch-split HVP partials
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_ese_gather_full_vhat_on_every_rank(world):
+    """dho2g_ese_gather: every rank receives the whole V_hat, as extract_ese_distributed's gather_rows
+    does (dist_lanczos.cpp:148-156), equal to the 1-rank V_hat to fp32 rounding (same signs)."""
+    n, m = 40_009, 24
+    spec = 1.0 + (np.arange(n) % 991) * 0.01
+    spec[:3] = [30.0, 20.0, -4.0]
+
+    def fn(c, rank):
+        st = d.lanczos_distributed(c, m, d.diagonal_operator(c, spec), n, 5)
+        ese = d.extract_ese_distributed(c, st, 3, 1)
+        return ese.eigvecs_full(n)
+
+    (v1,), outs = run_ranks(1, fn), run_ranks(world, fn)
+    for V in outs:
+        assert V.shape == (n, 4)
+        assert np.abs(V - v1).max() <= 1e-4 * np.abs(v1).max()
+    assert all(np.array_equal(outs[0], V) for V in outs[1:])  # the same bits on every rank
+
+
 def test_lanczos_rotated_quadratic_sharded():
     spec = np.linspace(-3.0, 9.0, 300)  # (no zero entry: the constructor rejects one)
     fn = lanczos_on(lambda c: d.quadratic_operator(c, spec, 5), 300, 24, 3, 1, 4)
