@@ -166,6 +166,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "upd_p2_staged") ctx->upd_p2_staged = (int)value;
     else if (k == "ritz_tc") ctx->ritz_tc = (int)value;
     else if (k == "tql2_split") ctx->tql2_split = (int)value;
+    else if (k == "tql2_log_cap") ctx->tql2_log_cap = (long long)value;
     else if (k == "gs_sm_cap") ctx->gs_sm_cap = (int)value;
     else if (k == "graphs") ctx->use_graphs = (int)value;
     else if (k == "graphs_multirank") ctx->graphs_multirank = (int)value;

@@ -82,6 +82,7 @@ struct dho2g_ctx {
   dho2g_fabric* fabric = nullptr;  // in-process test backend (dho2g_comm_init_local) instead of NCCL
   dho2g::DevBuf<float> fabric_scratch;
   int rank = 0, world = 1;
+  long long tql2_log_cap = 0;  // split eigensolve's rotation-log entries (0: 2 m^2 + 4096); tests shrink it
   int graphs_multirank = 1;  // refresh CUDA graph also at world > 1 (NCCL communicator; not the fabric)
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
   // Set when a collective failed (DEADLOCK / NCCL): the communicator is aborted and every later call on
@@ -374,6 +375,7 @@ struct LzDev {  // device-resident Lanczos scalars (fixed launch sequence; no ho
   float sigma[kMaxLanczos + 2];  // lazy column normalisation: v_j = sigma_j * D[:, j]
   double pre, beta;
   int iters, stopped, breakdown, safeguards, need_sg;
+  int nonfinite;  // the operator returned non-finite values (dist_lanczos.cpp:80-82): stop, raise on the host
   long long sg_cols;  // sum over safeguard passes of the active column count (gs_flops accounting)
   double gram[2][kMaxLanczos + 1];  // G_j = D_j^T D_i of the last two iterations (recurrence-first form)
 };

@@ -91,6 +91,7 @@ __global__ void lz_init_kernel(LzDev* st, const double* __restrict__ allp, int w
   st->safeguards = 0;
   st->need_sg = 0;
   st->sg_cols = 0;
+  st->nonfinite = 0;
   st->pre = 0.0;
   st->beta = 0.0;
 }
@@ -358,6 +359,14 @@ __global__ void lz_decide_kernel(LzDev* st, const double* __restrict__ allb, int
   for (int w = 0; w < world; ++w) b2 += allb[(size_t)w * stride];
   const double beta = sqrt(b2);
   const double pre = st->pre;
+  // dist_lanczos.cpp:80-82: a non-finite HVP stops the run (NaN fails every comparison below, so without
+  // this it would flow into B and surface only as a non-converging eigensolve)
+  if (!isfinite(pre) || !isfinite(beta) || !isfinite(st->diag[it])) {
+    st->nonfinite = 1;
+    st->stopped = 1;
+    st->iters = it;
+    return;
+  }
   // fp32 adaptation of the reference thresholds (fp64 there): h and D are stored in fp32, so an
   // exactly invariant subspace leaves a residual at the fp32 rounding floor (~3e-8 pre), never at
   // 1e-10 pre; and a projection that cancels beyond ~1e-3 loses orthogonality at eps32/ratio.
@@ -614,10 +623,12 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
 }
 
 // sync[0] ticket, sync[1] published sweeps, sync[2] done (zeroed before the launch)
+// status: 1 = no convergence within the reference's 60 sweeps per l, 2 = the rotation log (cap entries) is full
+// (the host reruns the eigensolve with the single-CTA kernel)
 __global__ void __launch_bounds__(32) tql2_pipe_kernel(const LzDev* st, int n, int T, double2* __restrict__ rot,
-                                                       int4* __restrict__ sweep, int* __restrict__ sync,
-                                                       double* __restrict__ dout, int* __restrict__ status,
-                                                       double* __restrict__ Z) {
+                                                       long long cap, int4* __restrict__ sweep,
+                                                       int* __restrict__ sync, double* __restrict__ dout,
+                                                       int* __restrict__ status, double* __restrict__ Z) {
   extern __shared__ double sh[];
   __shared__ int s_role;
   const int lane = threadIdx.x;
@@ -651,6 +662,10 @@ __global__ void __launch_bounds__(32) tql2_pipe_kernel(const LzDev* st, int n, i
         if (mm == l) break;
         if (iter++ == 60) {
           fail = 1;
+          break;
+        }
+        if ((long long)off + (mm - l) > cap) {  // this sweep could overflow the log
+          fail = 2;
           break;
         }
         int cnt = 0;
@@ -1024,6 +1039,14 @@ void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, si
 void dho2g_op::route_setup(size_t base) {
   const int G = ctx->world;
   if (recv.p && recv.n >= base * G && route_tab.p) return;
+  if (recv.p) {
+    // growing: every rank is here (route_setup is collective); once all ranks have finished with the old
+    // receive buffers (barrier) the stale peer mappings are closed before the owners free them
+    ctx->barrier();
+    dho2g::wait_stream(ctx, ctx->stream);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    ipc_opened.clear();
+  }
   recv.alloc(base * G);
   route_tab.alloc(G);
   std::vector<float*> tab(G, nullptr);
@@ -1313,6 +1336,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   lz->ms = ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (lz->host.nonfinite) fail(DHO2G_NUMERIC, "lanczos_distributed: hvp returned non-finite values");
   if (lz->host.stopped == 0) lz->host.iters = (int)m;
   ctx->bump("lanczos_runs", 1);
   ctx->bump("lanczos_ms", ms);
@@ -1356,8 +1380,10 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   const int kx = ctx->kt_begin();
   const int kq = ctx->kt_begin();
   if (ctx->tql2_split) {
-    // log capacity: at most 60 sweeps per l, each of at most n - 1 - l rotations (tql2_pipe_kernel)
-    const size_t cap = std::max<size_t>(1, (size_t)30 * me * (me - 1));
+    // log capacity: QL takes ~1-2 sweeps of <= n - 1 - l rotations per l, ~n^2 rotations in all; 2 n^2 is
+    // kept (the reference's limit, 60 sweeps per l, would need 30 n (n - 1): 500 MB at m = 1023). A log that
+    // fills up makes the kernel stop with status 2 and the single-CTA kernel redoes the eigensolve.
+    const size_t cap = ctx->tql2_log_cap > 0 ? (size_t)ctx->tql2_log_cap : (size_t)2 * me * me + 4096;
     lz->xrot.ensure(cap);
     lz->xsweep.ensure((size_t)60 * me + 1);
     lz->xnsweep.ensure(4);
@@ -1370,7 +1396,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
       DHO2G_CUDA(cudaFuncSetAttribute(tql2_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp));
     const int k1 = ctx->kt_begin();
     tql2_pipe_kernel<<<(unsigned)(1 + cdiv((size_t)me, (size_t)T)), 32, sp, st>>>(
-        lz->st.p, me, T, lz->xrot.p, lz->xsweep.p, lz->xnsweep.p, lz->xd.p, status.p, Z.p);
+        lz->st.p, me, T, lz->xrot.p, (long long)cap, lz->xsweep.p, lz->xnsweep.p, lz->xd.p, status.p, Z.p);
     DHO2G_LAUNCH();
     ctx->kt_end(k1, "eig.pipe", 0.0);
     const int k3 = ctx->kt_begin();
@@ -1427,6 +1453,18 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   DHO2G_CUDA(cudaMemcpyAsync(ese->eigvals.data(), ese->ev_dev.p, r * sizeof(double), cudaMemcpyDeviceToHost, st));
   DHO2G_CUDA(cudaMemcpyAsync(&h_status, status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   wait_stream(lz->ctx, st);
+  if (h_status == 2 && ctx->tql2_split) {  // rotation log full: the single-CTA eigensolve (bit-identical)
+    ctx->bump("tql2_log_overflows", 1);
+    ctx->tql2_split = 0;
+    try {
+      extract_ese_into(ctx, lz, k, l, ese);
+    } catch (...) {
+      ctx->tql2_split = 1;
+      throw;
+    }
+    ctx->tql2_split = 1;
+    return;
+  }
   if (h_status) fail(DHO2G_NUMERIC, "tridiag_eig: QL iteration did not converge");
   ese->sign.assign(r, 1.f);
   for (int c = 0; c < r; ++c) {

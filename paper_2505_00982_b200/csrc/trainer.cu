@@ -386,6 +386,9 @@ struct dho2g_trainer {
     row.inner = inner;
     row.epoch = epoch;
     row.loss = quad ? h[0] : h[0] / (double)N;
+    // a non-finite gradient raises the reference's NumericError (optimizer.cpp:38-40) before the loss check
+    // can report the divergence it causes
+    check_opt_flags(&opt);
     if (!std::isfinite(row.loss))
       fail(DHO2G_DIVERGED, "non-finite loss at epoch " + std::to_string(epoch) + " (trainer " +
                                (cfg.trainer == 2 ? "dho2" : cfg.trainer == 1 ? "fosi" : "sgd") + ")");

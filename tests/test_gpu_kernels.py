@@ -314,6 +314,21 @@ def test_extract_known_diagonal_signs(ctx):  # test_lanczos.cpp:95-111
     assert V[0, 0] >= 1 - 1e-5 and V[3, 1] >= 1 - 1e-5
 
 
+def test_lanczos_nonfinite_hvp_raises(ctx, port):  # dist_lanczos.cpp:80-82
+    H = random_symmetric(port, 30, 5)
+    calls = []
+
+    def hvp(v):
+        calls.append(1)
+        out = H @ v
+        if len(calls) == 4:
+            out[7] = np.nan
+        return out
+
+    with pytest.raises(d.NumericError, match="non-finite"):
+        d.lanczos_distributed(ctx, 10, d.host_operator(ctx, hvp, 30), 30, 3)
+
+
 def test_lanczos_rejects_bad_m(ctx):
     op = d.diagonal_operator(ctx, np.arange(1.0, 5.0))
     with pytest.raises(d.ArgumentError):
@@ -537,6 +552,25 @@ def test_tql2_split_matches_single_cta(ctx, n, m, k, l):
             ctx.set_option("tql2_split", 1)
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_tql2_log_overflow_falls_back_bit_identical(ctx):
+    """The split eigensolve's rotation log is sized for typical QL (2 m^2 entries, not the reference's
+    worst case of 30 m (m - 1)); a log that fills up stops the kernel with status 2 and the single-CTA
+    eigensolve redoes the extraction: results bit-identical to the unconstrained split form."""
+    n, m = 20_000, 80
+    spec = 1.0 + np.sin(np.arange(n) * 0.731) * 3.0
+    st = d.lanczos_distributed(ctx, m, d.diagonal_operator(ctx, spec), n, 5)
+    ref = d.extract_ese_distributed(ctx, st, 8, 2)
+    e0, v0 = ref.eigvals, ref.eigvecs_shard(n)
+    before = ctx.stat("tql2_log_overflows")
+    ctx.set_option("tql2_log_cap", 200)
+    try:
+        ese = d.extract_ese_distributed(ctx, st, 8, 2)
+    finally:
+        ctx.set_option("tql2_log_cap", 0)
+    assert ctx.stat("tql2_log_overflows") == before + 1
+    assert np.array_equal(ese.eigvals, e0) and np.array_equal(ese.eigvecs_shard(n), v0)
 
 
 def test_nccl_collectives_one_rank(ctx):
