@@ -115,7 +115,26 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def _ref_components(cfgname, parts=("grad", "hvp", "gs", "upd")):
+def cpu_info():
+    """Host the CPU baseline runs on (nproc, OMP threads, CPU model)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS"), "cpu_model": model}
+
+
+def _use_all_cores():
+    """OpenMP threads = every host core (set before the reference library loads)."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+
+
+def _ref_components(cfgname, parts=("grad", "hvp", "gs", "upd"), parallel=True):
     """Times the UNMODIFIED reference (oracle/_ref/libdho2ref.so, -O2 -fopenmp) on bounded samples of the
     workload's components: per-sample gradient and HVP cost, one Gram-Schmidt projection, one update pass.
     Models above ~20M parameters are timed on a two-hidden-layer slice [D, H, H, K] of the same widths and
@@ -125,6 +144,7 @@ def _ref_components(cfgname, parts=("grad", "hvp", "gs", "upd")):
     import numpy as np
     kind = "reference" if reference_available() else "port"
     R = CpuChecker(kind)
+    R.set_parallel(parallel)  # kernels::set_parallel (kernels.cpp:8-13): OpenMP or serial
     c = CONFIGS[cfgname]
     sizes = c["sizes"]
     n = mlp_dim(sizes)
@@ -133,7 +153,7 @@ def _ref_components(cfgname, parts=("grad", "hvp", "gs", "upd")):
     tsizes = sizes if n <= 20_000_000 else [sizes[0], sizes[1], sizes[2], sizes[-1]]
     m = c["m"] or R.lanczos_budget(c["k"], 0, n)
     ns = min(n, 1 << 20)
-    out = dict(kind=kind, cores=T, Bs=Bs, tsizes=tsizes, m=m, ns=ns)
+    out = dict(kind=kind, cores=T, Bs=Bs, tsizes=tsizes, m=m, ns=ns, parallel=parallel)
     if "grad" in parts or "hvp" in parts:
         X, y = blobs_dataset(Bs, sizes[0], sizes[-1], seed=7)
         w = R.mlp_init(tsizes, 1)
@@ -181,12 +201,23 @@ def _ref_combine(cfgname, comp):
     return 1.0 / per_step, refresh_s * 1e3, sample
 
 
+def _component_detail(comp):
+    """Measured per-component times (extrapolated to the workload) and the sample sizes behind them."""
+    return {"per_sample_grad_s": comp["grad"], "per_sample_hvp_s": comp["hvp"], "gs_per_refresh_s": comp["gs"],
+            "update_per_step_s": comp["upd"], "sample_batch": comp["Bs"], "sample_model": comp["tsizes"],
+            "sample_rows": comp["ns"], "m": comp["m"], "threads": comp["cores"]}
+
+
 def cpu_reference_sample(cfgname):
-    """All components once (the cpu_baseline leg of our own bench line). Returns (steps/s, refresh ms, detail)."""
+    """All components once with OpenMP on every core, and once serial (kernels::set_parallel(false)); the
+    cpu_baseline leg of our own bench line. Returns (steps/s, refresh ms, detail)."""
+    _use_all_cores()
     comp = _ref_components(cfgname)
     v, rm, sample = _ref_combine(cfgname, comp)
-    return v, rm, dict(kind=comp["kind"], cores=comp["cores"], sample=sample, t_grad_sample=comp["grad"],
-                       t_hvp_sample=comp["hvp"], t_update_step=comp["upd"], gs_refresh_s=comp["gs"])
+    ser = _ref_components(cfgname, parallel=False)
+    vs, rms, _ = _ref_combine(cfgname, ser)
+    return v, rm, dict(kind=comp["kind"], cores=comp["cores"], sample=sample, openmp=_component_detail(comp),
+                       serial={"value": vs, "refresh_ms": rms, **_component_detail(ser)}, host=cpu_info())
 
 
 def _project(R, D, h):
@@ -210,7 +241,7 @@ def _project(R, D, h):
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(min(os.cpu_count() or 1, 16)))
+    _use_all_cores()
     # each step samples half of the components (alternating), so that one step is a few seconds of CPU work
     # and the whole --steps K --warmup W run stays within minutes; the timed steps' samples are averaged
     samples = {"grad": [], "hvp": [], "gs": [], "upd": []}
@@ -228,14 +259,21 @@ def run_reference(args, rank, world):
             samples[p].append(_ref_components(args.config, (p,))[p])
     comp.update({p: sum(v) / len(v) for p, v in samples.items()})
     value, refresh_ms, sample = _ref_combine(args.config, comp)
-    det = {"kind": comp["kind"], "cores": comp["cores"], "sample": sample + "; components sampled alternately per step"}
+    # the serial library (kernels::set_parallel(false), kernels.cpp:8-13), one sample after the timed steps:
+    # reported beside the OpenMP value (OpenMP is slower than serial for project_out on some hosts)
+    ser = _ref_components(args.config, parallel=False)
+    vs, rms, _ = _ref_combine(args.config, ser)
+    det = {"kind": comp["kind"], "cores": comp["cores"], "sample": sample + "; components sampled alternately per step",
+           "openmp": _component_detail(comp), "serial": {"value": vs, "refresh_ms": rms, **_component_detail(ser)},
+           "host": cpu_info()}
     line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_json(args.config, world),
             "refresh_ms": refresh_ms,
             "cpu_baseline": {"value": value, "unit": "steps/s", "cores": det["cores"], "kind": det["kind"],
-                             "sample": det["sample"]},
+                             "sample": det["sample"], "openmp": det["openmp"], "serial": det["serial"],
+                             "host": det["host"]},
             "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -443,7 +481,8 @@ def run_ours(args, rank, world, dist):
         try:
             v, rm, det = cpu_reference_sample(args.config)
             line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": det["cores"], "kind": det["kind"],
-                                    "sample": det["sample"], "refresh_ms": rm}
+                                    "sample": det["sample"], "refresh_ms": rm, "openmp": det["openmp"],
+                                    "serial": det["serial"], "host": det["host"]}
         except Exception as e:  # the baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
