@@ -15,7 +15,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BENCH_NAMES = {"gemm3_tc2_kernel": "gemm3_tcgen05", "gemm3_tc_kernel": "gemm3_tcgen05", "gs_pass1_kernel": "gs_pass1",
                "gs_pass2_kernel": "gs_pass2", "upd_p1_kernel": "upd_p1", "upd_p2_tma_kernel": "upd_p2",
                "upd_p2_kernel": "upd_p2", "upd_p3_kernel": "upd_p3", "pack_weights_kernel": "pack_params",
-               "colsum_pairs_kernel": "bias_colsum", "ritz_kernel": "extract.ritz"}
+               "colsum_pairs_kernel": "bias_colsum", "ritz_kernel": "extract.ritz",
+               "pack_weights_f16_kernel": "pack_params", "split_pair_kernel": "split_pair",
+               "ritz_tc_kernel": "extract.ritz"}
 
 
 def short(name):
