@@ -453,17 +453,17 @@ def run_ours(args, rank, world, dist):
                 "peak": peaks["tf_sus"] if is_gemm else peaks["hbm"], "unit": k["unit"], "frac": k["frac"],
                 "peak_source": f"{peaks['src']} ({'bf16_tflops_sustained' if is_gemm else 'hbm_gbs'})",
                 "traffic": traffic_from_profiles(dom),
-                "work_def": ("useful split-BF16x3 GEMM flops 2*M*N*K per launch (tensor pipe issues 3x)"
+                "work_def": ("useful GEMM flops 2*M*N*K per launch (the hi/lo split issues 3x on the tensor pipe)"
                              if is_gemm else "algorithmic bytes per launch (SURVEY §8d)")}
         if is_gemm:
             roof["issued_frac"] = round(3 * k["achieved"] / peaks["tf_sus"], 4)
-            # split-BF16x3 issues 3 MMAs per useful product: the useful-flop ceiling is 1/3 of the peak. In
+            # the hi/lo split issues 3 MMAs per useful product: the useful-flop ceiling is 1/3 of the peak. In
             # isolation at full clock the pair GEMMs reach the burst peak (profiles/r01_gemm_timeline.txt);
             # inside the C4 step the SM clock is power-capped (see "clocks")
             roof["useful_ceiling_frac"] = round(1.0 / 3.0, 4)
     line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (split-bf16x3 tensor-core GEMMs, fp64 reductions)",
+            "vs_baseline": None, "dtype": "f32 (tensor-core GEMMs on scaled-fp16 hi/lo pairs, 3 MMAs per product; fp64 reductions)",
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,

@@ -2,8 +2,9 @@
  * dho2gpu.h — C ABI of the B200-native DHO2 curvature-and-update hot path.
  *
  * Plain pointers and sizes only (no torch / STL types). Host buffers are fp64 like the
- * reference's dho2::Vector; device state is fp32 (split-BF16x3 on the tensor cores for the
- * MLP contractions, fp64 accumulation for every reduction, fp64 tridiagonal eigensolve).
+ * reference's dho2::Vector; device state is fp32 (three tensor-core MMAs per product on
+ * power-of-two-scaled fp16 (hi, lo) operand pairs for the MLP contractions, fp64 accumulation
+ * for every reduction, fp64 tridiagonal eigensolve).
  * Every entry point returns a dho2g_status; the matching reference exception type is named
  * beside each code, and dho2g_last_error() returns the message (thread-local).
  *
@@ -100,9 +101,6 @@ int dho2g_batch_indices(const uint64_t* perm, size_t N, int workers, int worker,
                         uint64_t* out);
 /* Build-defined "blobs-D" synthetic data, row-major fp64. */
 void dho2g_blobs_dataset(size_t N, size_t D, size_t n_classes, uint64_t seed, double* X, double* y);
-/* Eigensolve on the host fp64 (same algorithm as the device kernel; for the C ABI users
- * that hold a tridiagonal matrix, linalg.hpp:113). vecs: n x n column-major. */
-int dho2g_tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs);
 
 /* ---- model/loss plugin: Oracle (oracle.hpp:72-80), MlpOracle (oracle.hpp:113-141) ----- */
 /* act: 0 tanh, 1 relu. loss: 0 softmax_ce, 1 mse (oracle.hpp:103-107). */
@@ -244,7 +242,7 @@ int dho2g_trainer_stat(dho2g_trainer* tr, const char* key, double* value);
 /* Last refresh's eigenvalues (k+l) and tridiagonal matrix. */
 int dho2g_trainer_eigvals(dho2g_trainer* tr, double* vals, size_t* count);
 
-/* ---- test hook: one split-BF16x3 GEMM C = A B^T over host fp32 (A: M x K, B: N x K, row-major).
+/* ---- test hook: one split (hi, lo) GEMM C = A B^T (operand format per ctx option gemm_f16) over host fp32 (A: M x K, B: N x K, row-major).
  * backend 0 = tcgen05 kernel, 1 = CUDA-core reference kernel. ------------------------------- */
 int dho2g_test_gemm(dho2g_ctx* ctx, int M, int N, int K, const float* A, const float* B, float* C, int backend);
 /* Two-segment form C = A0 B0^T + A1 B1^T (A0: M x K0, A1: M x K1, B0: N x K0, B1: N x K1; K1 = 0: one

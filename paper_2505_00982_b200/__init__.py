@@ -1,8 +1,8 @@
 """B200-native DHO2 curvature-and-update hot path (arXiv 2505.00982).
 
-libdho2gpu.so (hand-written sm_100a CUDA: tcgen05/TMA split-BF16x3 GEMMs for the HVP and
-gradient, fused Gram-Schmidt passes, single-CTA fp64 tridiagonal eigensolve, fused FOSI/ADMM
-update, NCCL collectives) behind a C ABI (include/dho2gpu.h); this package mirrors the
+libdho2gpu.so (hand-written sm_100a CUDA: tcgen05/TMA GEMMs on scaled-fp16 (hi, lo) operand pairs for
+the HVP and gradient, fused Gram-Schmidt passes, fp64 tridiagonal eigensolve, fused FOSI/ADMM update,
+NCCL collectives) behind a C ABI (include/dho2gpu.h); this package mirrors the
 reference's C++ optimizer API (see api.py).
 """
 from .api import *  # noqa: F401,F403

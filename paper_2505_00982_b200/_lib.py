@@ -85,7 +85,6 @@ _SIGS = {
     "dho2g_curvature_indices": ([C.c_size_t, C.c_size_t, C.c_uint64, C.c_uint64, up], None),
     "dho2g_batch_indices": ([up, C.c_size_t, C.c_int, C.c_int, C.c_size_t, C.c_size_t, up], C.c_int),
     "dho2g_blobs_dataset": ([C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint64, dp, dp], None),
-    "dho2g_tridiag_eig_host": ([C.c_size_t, dp, dp, dp, dp], C.c_int),
     "dho2g_mlp_create": ([vp, sp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)], C.c_int),
     "dho2g_mlp_destroy": ([vp], C.c_int),
     "dho2g_mlp_dim": ([vp], C.c_size_t),

@@ -147,15 +147,6 @@ def blobs_dataset(N: int, D: int, n_classes: int = 10, seed: int = 7):
     return X, y
 
 
-def tridiag_eig(diag, off):
-    """linalg::tridiag_eig (linalg.cpp:140-226) on the host (the device kernel serves extract_ese)."""
-    diag, off = _f64(diag), _f64(off)
-    n = len(diag)
-    vals, vecs = np.empty(n), np.empty(n * n)
-    check(lib.dho2g_tridiag_eig_host(n, _d(diag), _d(off) if n > 1 else None, _d(vals), _d(vecs)))
-    return vals, vecs.reshape(n, n).T
-
-
 # ----------------------------------------------------------------------------- context
 class LocalFabric:
     """In-process rendezvous for `world` ranks on one GPU (include/dho2gpu.h: dho2g_local_fabric_create): the
@@ -299,7 +290,7 @@ class Context:
 
 
 def test_gemm(ctx: "Context", A, B, backend: int = 0):
-    """One split-BF16x3 GEMM C = A B^T (test hook; backend 0 tcgen05, 1 CUDA-core)."""
+    """One split (hi, lo) GEMM C = A B^T in the ctx operand format (test hook; backend 0 tcgen05, 1 CUDA-core)."""
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)
     M, K = A.shape

@@ -452,12 +452,6 @@ void dho2g_blobs_dataset(size_t N, size_t D, size_t n_classes, uint64_t seed, do
     });
   for (auto& x : th) x.join();
 }
-int dho2g_tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs) {
-  std::string err;
-  const int rc = tridiag_eig_host(n, diag, off, vals, vecs, &err);
-  if (rc) g_err = err;
-  return rc;
-}
 
 // ------------------------------------------------------------------ MLP plugin
 int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, int loss, dho2g_mlp** out) {

@@ -130,79 +130,6 @@ size_t lanczos_budget(size_t k, size_t l, size_t n) {
   return std::min(n, std::max(4 * (k + l), log_term));
 }
 
-// Host fp64 implicit-shift QL (linalg.cpp:140-226 semantics: ascending, stable order,
-// NumericError after 60 sweeps). The device path uses the single-CTA kernel in lanczos.cu.
-int tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs,
-                     std::string* err) {
-  if (n == 0) {
-    *err = "tridiag_eig: empty matrix";
-    return DHO2G_ARGUMENT;
-  }
-  for (size_t i = 0; i < n; ++i)
-    if (!std::isfinite(diag[i]) || (i + 1 < n && !std::isfinite(off[i]))) {
-      *err = "tridiag_eig: non-finite entries";
-      return DHO2G_NUMERIC;
-    }
-  std::vector<double> d(diag, diag + n), e(n, 0.0), z(n * n, 0.0);
-  for (size_t i = 0; i + 1 < n; ++i) e[i] = off[i];
-  for (size_t i = 0; i < n; ++i) z[i * n + i] = 1.0;
-  const double eps = 2.220446049250313e-16;
-  for (size_t l = 0; l < n && n > 1; ++l) {
-    int iter = 0;
-    size_t mm;
-    for (;;) {
-      for (mm = l; mm + 1 < n; ++mm) {
-        if (std::abs(e[mm]) <= eps * (std::abs(d[mm]) + std::abs(d[mm + 1]))) break;
-      }
-      if (mm == l) break;
-      if (iter++ == 60) {
-        *err = "tridiag_eig: QL iteration did not converge";
-        return DHO2G_NUMERIC;
-      }
-      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-      double r = std::hypot(g, 1.0);
-      g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
-      double s = 1.0, c = 1.0, p = 0.0;
-      bool under = false;
-      for (size_t ii = mm; ii-- > l;) {
-        double f = s * e[ii];
-        const double b = c * e[ii];
-        r = std::hypot(f, g);
-        e[ii + 1] = r;
-        if (r == 0.0) {
-          d[ii + 1] -= p;
-          e[mm] = 0.0;
-          under = true;
-          break;
-        }
-        s = f / r;
-        c = g / r;
-        g = d[ii + 1] - p;
-        r = (d[ii] - g) * s + 2.0 * c * b;
-        p = s * r;
-        d[ii + 1] = g + p;
-        g = c * r - b;
-        for (size_t k = 0; k < n; ++k) {
-          f = z[(ii + 1) * n + k];
-          z[(ii + 1) * n + k] = s * z[ii * n + k] + c * f;
-          z[ii * n + k] = c * z[ii * n + k] - s * f;
-        }
-      }
-      if (under) continue;
-      d[l] -= p;
-      e[l] = g;
-      e[mm] = 0.0;
-    }
-  }
-  std::vector<size_t> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return d[a] < d[b]; });
-  for (size_t j = 0; j < n; ++j) {
-    vals[j] = d[order[j]];
-    std::copy(z.begin() + order[j] * n, z.begin() + (order[j] + 1) * n, vecs + j * n);
-  }
-  return DHO2G_OK;
-}
 
 }  // namespace dho2g
 

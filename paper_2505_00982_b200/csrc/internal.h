@@ -30,7 +30,6 @@ struct Rng {  // rng.hpp:14-68 (SplitMix64 + Box-Muller with spare)
 void shuffle_iota(uint64_t seed, size_t n, uint64_t* out);
 void shard_range(size_t n, int world, int rank, size_t* begin, size_t* end);
 size_t lanczos_budget(size_t k, size_t l, size_t n);
-int tridiag_eig_host(size_t n, const double* diag, const double* off, double* vals, double* vecs, std::string* err);
 bool quadratic_rotation(size_t n, uint64_t rotation_seed, double* Q);  // false: degenerate draw
 
 }  // namespace dho2g

@@ -95,17 +95,6 @@ def test_blobs_dataset_matches_checker():
     assert (np.bincount(y.astype(int)) == 30).all()
 
 
-def test_host_tridiag_matches_checker(port):
-    dd, e = port.rng_normal(3, 30), port.rng_normal(4, 29)
-    a, A = d.tridiag_eig(dd, e)
-    b, Bv = port.tridiag_eig(dd, e)
-    assert (a == b).all() and (A == Bv).all()
-    with pytest.raises(d.NumericError):
-        d.tridiag_eig([1.0, float("nan")], [0.0])
-    with pytest.raises(d.ArgumentError):
-        d.tridiag_eig([], [])
-
-
 def test_mlp_init_params_without_gpu_is_refused():
     """Device objects need a CUDA context; without a GPU the call fails loudly (no fallback)."""
     import torch
