@@ -518,6 +518,7 @@ void check_op(const GOp& g, const char* what) {
 // partials are combined in a fixed order through a global workspace + release/acquire flags.
 namespace tc1 {
 using namespace tc;
+constexpr size_t kTc1Tickets = 4096;  // offset of the split-K tickets in ctx->gemm_flags
 constexpr int BM = 128, BN = 128, STAGES = 3;
 constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;
 constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
@@ -550,6 +551,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* tfull = empty + STAGES;  // [ACC]
   uint64_t* tempty = tfull + ACC;    // [ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
+  __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -671,53 +673,67 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
-      // split-K partial, private layout [warp slot][chunk][q][lane][4] so every float4 access of a
-      // warp is one contiguous 512 B segment
-      float* wtile = ws ? ws + (size_t)tile * BM * BN + (size_t)(ew + 4 * chalf) * (32 * BN / 2) + (size_t)lane * 4
-                        : nullptr;
-      const bool last = split == sc.splits - 1;
-      if (split > 0) {  // wait for the previous split of this tile (fixed combine order)
-        if (threadIdx.x == 128) {
-          const unsigned want = epoch * 16u + (unsigned)split;
-          while (ld_acquire(flags + tile) != want) __nanosleep(64);
-        }
-        epi_bar();
-      }
-#pragma unroll 1
-      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
-        float v[16];
+      auto acc16 = [&](int c0, float (&v)[16]) {  // this unit's sum: TMEM chunk (+ the earlier chunks)
         tmem_ld16(tbase + (uint32_t)c0, v);
-        if (nchunks > 1) {  // + the earlier chunks
+        if (nchunks > 1) {
           float t[16];
           tmem_ld16(tsum + (uint32_t)c0, t);
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] += t[j];
         }
-        if (split > 0) {
-          const float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+      };
+      if (sc.splits == 1) {
+#pragma unroll 1
+        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
+          float v[16];
+          acc16(c0, v);
+          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[ab]);
+        continue;
+      }
+      // split-K: every split publishes its partial (private layout [split][warp slot][chunk][q][lane][4], each
+      // warp float4 access one contiguous 512 B segment) and takes a ticket; the LAST split to arrive adds all
+      // partials in split order (deterministic: the order does not depend on who arrives last) and runs the
+      // epilogue. No split waits for another, so the latency is one mainloop plus one exchange.
+      const size_t slot_off = (size_t)(ew + 4 * chalf) * (32 * BN / 2) + (size_t)lane * 4;
+      auto part = [&](int s2) { return ws + ((size_t)tile * sc.splits + s2) * BM * BN + slot_off; };
+#pragma unroll 1
+      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
+        float v[16];
+        acc16(c0, v);
+        float* p = part(split) + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          __stcg(reinterpret_cast<float4*>(p + q * 128), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      __threadfence();
+      epi_bar();
+      if (threadIdx.x == 128) s_last = atomicAdd(flags + tile, 1u) == (unsigned)(sc.splits - 1);
+      epi_bar();
+      if (!s_last) continue;
+      __threadfence();
+#pragma unroll 1
+      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int s2 = 0; s2 < sc.splits; ++s2) {
+          const float* p = part(s2) + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float4 t = __ldcg(reinterpret_cast<const float4*>(p + q * 128));
             v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
           }
         }
-        if (last) {
-          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
-        } else {
-          float* p = wtile + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            __stcg(reinterpret_cast<float4*>(p + q * 128), make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-        }
+        epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[ab]);
-      if (!last) {  // publish this split's partial
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 128) st_release(flags + tile, epoch * 16u + (unsigned)(split + 1));
-      }
+      if (threadIdx.x == 128) flags[tile] = 0u;  // ticket back to zero for the next launch
     }
   }
   fence_before();
@@ -730,6 +746,9 @@ __global__ void __launch_bounds__(384, 1)
 
 // split-K factor that best fills the persistent grid (work quantization), >= 8 k-blocks per split
 int pick_splits(int tiles, int nkb, int sms) {
+  // Few tiles (the small-M GEMMs of small problems): split K for latency — the splits run concurrently and the
+  // last one to finish combines them — keeping >= 2 k-blocks per split.
+  if (tiles * 4 <= sms) return std::max(1, std::min(std::min(sms / tiles, nkb / 2), 16));
   // Split only when whole-tile scheduling leaves the persistent grid badly quantised (the HVP GEMMs at
   // M = B = 1024: 224 tiles on 148 SMs); each extra split costs ~5% (partial write + read).
   // Measured on B200: profiles/r01_gemm_splits.txt.
@@ -793,15 +812,11 @@ int run(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const GOp& 
   unsigned* flags = nullptr;
   unsigned epoch = 0;
   if (sc.splits > 1) {
-    ctx->gemm_ws.ensure_g((size_t)sc.tiles * BM * BN);
-    ctx->gemm_flags.ensure_g((size_t)sc.tiles);
+    // one partial per (tile, split); tickets past the pair kernel's flags (they return to zero after each use)
+    ctx->gemm_ws.ensure_g((size_t)sc.tiles * sc.splits * BM * BN);
+    ctx->gemm_flags.ensure_g(kTc1Tickets + (size_t)sc.tiles);
     ws = ctx->gemm_ws.p;
-    flags = ctx->gemm_flags.p;
-    epoch = ++ctx->gemm_epoch;
-    if (epoch >= (1u << 27)) {  // flag encoding epoch * 16 + split: recycle
-      DHO2G_CUDA(cudaMemsetAsync(flags, 0, ctx->gemm_flags.n * sizeof(unsigned), ctx->stream));
-      ctx->gemm_epoch = epoch = 1;
-    }
+    flags = ctx->gemm_flags.p + kTc1Tickets;
   }
   CUtensorMap maps[4];
   op_maps(ctx->encode_fn, A, maps[0], maps[1]);
@@ -1271,9 +1286,9 @@ void gemm_presize(dho2g_ctx* ctx) {
   // single-CTA kernel's split-K partials for the small-M GEMMs too
   const size_t pairs = (size_t)std::max(1, ctx->sm_count / 2);
   ctx->gemm_ws.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
-  ctx->gemm_flags.ensure_g(2 * pairs * 2 + 16);
+  ctx->gemm_flags.ensure_g(tc1::kTc1Tickets + 2048);  // pair-kernel flags, then the single-CTA tickets
   ctx->gemm_ws2.ensure_g(2 * pairs * 2 * tc2::PART_MAX);
-  ctx->gemm_flags2.ensure_g(2 * pairs * 2 + 16);
+  ctx->gemm_flags2.ensure_g(tc1::kTc1Tickets + 2048);
 }
 
 // =============================================================================== dispatch
