@@ -1371,15 +1371,19 @@ int dho2g_test_collectives_graph(dho2g_ctx* ctx, double* max_err) {
 int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_t n_ctas) {
   return guard([&] {
     check_ctx(ctx);
+    // on: 1 arms the pair kernel's trace (4 stamps per CTA), 2 the single-CTA kernel's (8 stamps per CTA);
+    // 0 disarms both and copies the buffer out
     static DevBuf<unsigned long long> buf;
     if (on) {
-      buf.alloc(n_ctas * 4);
-      gemm_trace_set(buf.p);
+      buf.alloc(n_ctas * (on == 2 ? 8 : 4));
+      if (on == 2) gemm_trace1_set(buf.p);
+      else gemm_trace_set(buf.p);
     } else {
       DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
       gemm_trace_set(nullptr);
+      gemm_trace1_set(nullptr);
       if (out && buf.p)
-        DHO2G_CUDA(cudaMemcpy(out, buf.p, std::min(n_ctas * 4, buf.n) * sizeof(unsigned long long),
+        DHO2G_CUDA(cudaMemcpy(out, buf.p, std::min(n_ctas * 8, buf.n) * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost));
     }
   });

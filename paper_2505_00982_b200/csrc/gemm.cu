@@ -519,6 +519,15 @@ void check_op(const GOp& g, const char* what) {
 namespace tc1 {
 using namespace tc;
 constexpr size_t kTc1Tickets = 4096;  // offset of the split-K tickets in ctx->gemm_flags
+// Optional per-CTA timeline (test hook, investigation only): globaltimer ns at [0] entry, [1] setup done,
+// [2] first stage landed (MMA thread), [3] last MMA committed, [4] final accumulator ready (epilogue),
+// [5] epilogue done, [6] CTA joined, [7] TMEM freed.
+__device__ unsigned long long* g_tc1_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer1() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int BM = 128, BN = 128, STAGES = 3;
 constexpr uint32_t STAGE_BYTES = 4 * OP_BYTES;
 constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_SMEM;
@@ -552,6 +561,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + ACC;    // [ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
   __shared__ int s_last;
+  unsigned long long* trace = g_tc1_trace ? g_tc1_trace + (size_t)blockIdx.x * 8 : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = gtimer1();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -581,6 +592,7 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (trace && threadIdx.x == 0) trace[1] = gtimer1();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer: continuous ring over all k-blocks of this CTA's units
@@ -616,6 +628,7 @@ __global__ void __launch_bounds__(384, 1)
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         fence_after();
+        if (trace && it == 0) trace[2] = gtimer1();
         const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BK / UK; ++kk) {
@@ -643,6 +656,7 @@ __global__ void __launch_bounds__(384, 1)
                    : "memory");  // accumulator ready for the epilogue
      }
     }
+    if (trace) trace[3] = gtimer1();
   } else if (warp >= 4) {
     // ---------------- epilogue warps: TMEM -> registers -> (split-K combine) -> fused epilogue
     // 8 warps: warp w reads TMEM lane quadrant w % 4 (hardware rule) and column half (w - 4) / 4.
@@ -672,6 +686,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t ab = uc % ACC;
       mbar_wait(&tfull[ab], (uc / ACC) & 1);
       fence_after();
+      if (trace && threadIdx.x == 128) trace[4] = gtimer1();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
       auto acc16 = [&](int c0, float (&v)[16]) {  // this unit's sum: TMEM chunk (+ the earlier chunks)
         tmem_ld16(tbase + (uint32_t)c0, v);
@@ -723,11 +738,25 @@ __global__ void __launch_bounds__(384, 1)
         float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (int s2 = 0; s2 < sc.splits; ++s2) {
-          const float* p = part(s2) + (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+        const size_t blk = (size_t)((c0 - chalf * (BN / 2)) / 16) * (4 * 32 * 4);
+        int s2 = 0;
+        for (; s2 + 4 <= sc.splits; s2 += 4) {  // 16 loads in flight, then the adds in split order
+          float4 t[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[u][q] = __ldcg(reinterpret_cast<const float4*>(part(s2 + u) + blk + q * 128));
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              v[4 * q] += t[u][q].x; v[4 * q + 1] += t[u][q].y; v[4 * q + 2] += t[u][q].z; v[4 * q + 3] += t[u][q].w;
+            }
+        }
+        for (; s2 < sc.splits; ++s2) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float4 t = __ldcg(reinterpret_cast<const float4*>(p + q * 128));
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(part(s2) + blk + q * 128));
             v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
           }
         }
@@ -735,12 +764,15 @@ __global__ void __launch_bounds__(384, 1)
       }
       if (threadIdx.x == 128) flags[tile] = 0u;  // ticket back to zero for the next launch
     }
+    if (trace && threadIdx.x == 128) trace[5] = gtimer1();
   }
   fence_before();
   __syncthreads();
+  if (trace && threadIdx.x == 0) trace[6] = gtimer1();
   if (warp == 2) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    if (trace && lane == 0) trace[7] = gtimer1();
   }
 }
 
@@ -748,7 +780,9 @@ __global__ void __launch_bounds__(384, 1)
 int pick_splits(int tiles, int nkb, int sms) {
   // Few tiles (the small-M GEMMs of small problems): split K for latency — the splits run concurrently and the
   // last one to finish combines them — keeping >= 2 k-blocks per split.
-  if (tiles * 4 <= sms) return std::max(1, std::min(std::min(sms / tiles, nkb / 2), 16));
+  // (Measured per-CTA timelines at M = 128, K = 1568: 4-8 splits minimise the launch; beyond, the last
+  // split's combine costs more than the shorter mainloops save.)
+  if (tiles * 4 <= sms) return std::max(1, std::min(std::min(sms / tiles, nkb / 4), 8));
   // Split only when whole-tile scheduling leaves the persistent grid badly quantised (the HVP GEMMs at
   // M = B = 1024: 224 tiles on 148 SMs); each extra split costs ~5% (partial write + read).
   // Measured on B200: profiles/r01_gemm_splits.txt.
@@ -1354,5 +1388,8 @@ void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf1
 namespace dho2g {
 void gemm_trace_set(unsigned long long* buf) {
   DHO2G_CUDA(cudaMemcpyToSymbol(tc2::g_gemm_trace, &buf, sizeof(buf)));
+}
+void gemm_trace1_set(unsigned long long* buf) {
+  DHO2G_CUDA(cudaMemcpyToSymbol(tc1::g_tc1_trace, &buf, sizeof(buf)));
 }
 }  // namespace dho2g
