@@ -151,6 +151,37 @@ def test_mlp_oracle_vs_checker(ctx, port, sizes, B, act, loss, ncls):
         assert mlp.accuracy(w, batch) is None
 
 
+@pytest.mark.parametrize("act,loss,xscale", [("tanh", "softmax_ce", 1e-3), ("relu", "mse", 1e-4), ("relu", "softmax_ce", 300.0),
+                                             ("relu", "softmax_ce", 1e4)])
+def test_mlp_scaled_fp16_operands_any_magnitude(ctx, port, act, loss, xscale):
+    """Scaled-fp16 operand pairs (option gemm_f16) take each buffer's scale from the max of the values it holds:
+    inputs 1e-4 .. 1e4, relu activations (unbounded) and MSE deltas stay within the fp32 tolerance of the
+    checker, and agree with the bf16-pair path."""
+    from oracle.bindings import blobs_dataset
+    sizes, ncls = [24, 32, 16, 6], 6
+    X, y = blobs_dataset(50, 24, ncls, seed=13)
+    X = X * xscale
+    a, lo = {"tanh": 0, "relu": 1}[act], {"softmax_ce": 0, "mse": 1}[loss]
+    w = port.mlp_init(sizes, 5)
+    v = port.rng_normal(17, len(w))
+    hv_ref = port.mlp_hvp(sizes, w, v, X, y, ncls, a, lo)
+    g_ref = port.mlp_grad(sizes, w, X, y, ncls, a, lo)
+    out = {}
+    for f16 in (1, 0):
+        ctx.set_option("gemm_f16", f16)
+        try:
+            mlp = d.MlpOracle(ctx, sizes, act, loss)
+            b = d.Batch(X, y, ncls)
+            out[f16] = (mlp.hvp(w, v, b), mlp.grad(w, b))
+            mlp.close()
+        finally:
+            ctx.set_option("gemm_f16", 1)
+        assert np.isfinite(out[f16][0]).all() and np.isfinite(out[f16][1]).all()
+        assert rel_l2(out[f16][0], hv_ref) < 1e-4 and rel_l2(out[f16][1], g_ref) < 1e-4
+    # the 22-bit pairs are at least as close to the checker as the 16-bit ones (small-problem noise margin)
+    assert rel_l2(out[1][0], hv_ref) <= 2.0 * rel_l2(out[0][0], hv_ref) + 1e-7
+
+
 def test_mlp_hvp_linear_symmetric(ctx, port):  # test_oracle.cpp:107-132
     from oracle.bindings import blobs_dataset
     sizes = [30, 24, 6]
