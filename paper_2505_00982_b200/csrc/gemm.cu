@@ -676,8 +676,8 @@ __global__ void __launch_bounds__(384, 1)
         fence_after();
         const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * BN;
 #pragma unroll 1
-        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16)
-          tmem_drain16(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
+        for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32)
+          tmem_drain32(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
         tmem_wait_st();
         fence_before();
         __syncwarp();
@@ -1134,9 +1134,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         fence_after();
         const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
 #pragma unroll 1
-        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
-          if (c0 >= ncols) break;
-          tmem_drain16(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
+        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 32) {
+          if (c0 >= ncols) break;  // (MMA N is a multiple of 16; a 32-wide drain past it touches unused columns)
+          tmem_drain32(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
         }
         tmem_wait_st();
         fence_before();

@@ -95,18 +95,33 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-// v = acc chunk (+ running sum when `add`), running sum <- v: one drain step of a chunked accumulation
-// (the running sum is kept in TMEM, round-to-nearest fp32 adds on the CUDA cores)
-__device__ __forceinline__ void tmem_drain16(uint32_t acc, uint32_t sum, bool add) {
-  float v[16];
-  tmem_ld16(acc, v);
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// v = acc chunk (+ running sum when `add`), running sum <- v over 32 columns (two 16-column blocks): one
+// drain step of a chunked accumulation (the running sum is kept in TMEM, round-to-nearest fp32 adds on the
+// CUDA cores). All loads are issued before one wait.
+__device__ __forceinline__ void tmem_drain32(uint32_t acc, uint32_t sum, bool add) {
+  uint32_t a0[16], a1[16], s0[16], s1[16];
+  tmem_ld16_nowait(acc, a0);
+  tmem_ld16_nowait(acc + 16, a1);
   if (add) {
-    float t[16];
-    tmem_ld16(sum, t);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += t[j];
+    tmem_ld16_nowait(sum, s0);
+    tmem_ld16_nowait(sum + 16, s1);
   }
-  tmem_st16(sum, v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  float v0[16], v1[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v0[j] = __uint_as_float(a0[j]) + (add ? __uint_as_float(s0[j]) : 0.f);
+    v1[j] = __uint_as_float(a1[j]) + (add ? __uint_as_float(s1[j]) : 0.f);
+  }
+  tmem_st16(sum, v0);
+  tmem_st16(sum + 16, v1);
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
