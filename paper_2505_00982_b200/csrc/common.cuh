@@ -176,6 +176,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Deterministic fold of n strided partials by one warp: lane l adds x[b * stride] for b = l, l + 32, ... in
+// order, then the fixed xor-butterfly; every lane returns the total. The order depends only on n, never
+// on timing, and n / 32 loads per lane are in flight instead of one thread's n-long dependent chain.
+__device__ __forceinline__ double warp_fold(const double* x, int n, size_t stride) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+#pragma unroll 4
+  for (int b = lane; b < n; b += 32) t += __ldcg(x + (size_t)b * stride);
+  return warp_sum(t);
+}
 __device__ __forceinline__ float warp_sumf(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -224,11 +224,10 @@ __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restr
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
+  for (int jj = warp; jj < rowlen; jj += kWarps) {  // a warp per value, lanes over the CTA partials
     const int j = jj < nj ? jj : goff + (jj - nj);
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * stride + j];
-    rankp[j] = t;
+    const double t = warp_fold(part + j, (int)gridDim.x, (size_t)stride);
+    if (lane == 0) rankp[j] = t;
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
@@ -342,12 +341,13 @@ __global__ void __launch_bounds__(kThreads) gs_pass2_kernel(const float* __restr
   __syncthreads();
   if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!is_last || threadIdx.x != 0) return;
+  if (!is_last || warp != 0) return;
   __threadfence();
-  double s = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b];
-  rankb[0] = s;
-  *ticket = 0u;
+  const double s = warp_fold(part, (int)gridDim.x, 1);
+  if (lane == 0) {
+    rankb[0] = s;
+    *ticket = 0u;
+  }
 }
 
 // ------------------------------------------------------------------ decide (dist_lanczos.cpp:91-111)

@@ -68,10 +68,10 @@ __device__ void finish_partials(const double* acc, int nj, double* part, double*
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int j = threadIdx.x; j < nj; j += kT) {
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * nj + j];
-    rankp[j] = t;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < nj; j += kW) {  // a warp per value, lanes over the CTA partials (fixed order)
+    const double t = warp_fold(part + j, (int)gridDim.x, (size_t)nj);
+    if (lane == 0) rankp[j] = t;
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
