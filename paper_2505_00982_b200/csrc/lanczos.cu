@@ -224,10 +224,19 @@ __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restr
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int jj = warp; jj < rowlen; jj += kWarps) {  // a warp per value, lanes over the CTA partials
-    const int j = jj < nj ? jj : goff + (jj - nj);
-    const double t = warp_fold(part + j, (int)gridDim.x, (size_t)stride);
-    if (lane == 0) rankp[j] = t;
+  if (rowlen <= 4 * kWarps) {  // few values: a warp per value, lanes over the CTA partials
+    for (int jj = warp; jj < rowlen; jj += kWarps) {
+      const int j = jj < nj ? jj : goff + (jj - nj);
+      const double t = warp_fold(part + j, (int)gridDim.x, (size_t)stride);
+      if (lane == 0) rankp[j] = t;
+    }
+  } else {  // many values (long bases): a thread per value, its chain over the partials in CTA order
+    for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
+      const int j = jj < nj ? jj : goff + (jj - nj);
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * stride + j];
+      rankp[j] = t;
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
