@@ -492,6 +492,8 @@ int dho2g_mlp_create(dho2g_ctx* ctx, const size_t* sizes, int n_sizes, int act, 
       m->WV_lo[t].alloc((size_t)ld.out * 2 * ld.Pin);
     }
     m->scl.alloc((size_t)3 * m->L);
+    m->sclx.alloc((size_t)3 * m->L);
+    m->sticket.alloc((size_t)3 * m->L);
     m->amax.alloc((size_t)5 * (m->L + 1));
     *out = m.release();
   });

@@ -207,6 +207,8 @@ struct dho2g_mlp {
   int chunk_kb = 0;         // Epi::chunk_kb of the GEMMs being issued (the HVP path sets it)
   float wv_vbound = 0.f;    // bound on |direction| the WV scales were chosen for
   dho2g::DevBuf<float> scl;
+  dho2g::DevBuf<float> sclx;        // scale of the x half of each pair buffer (split_pair_kernel), same index
+  dho2g::DevBuf<unsigned> sticket;  // its update tickets
   dho2g::DevBuf<unsigned> amax;
   float* s_ar(int t) { return scl.p + t; }
   float* s_dr(int j) { return scl.p + L + j - 1; }

@@ -180,49 +180,86 @@ __global__ void pack_weights_f16_kernel(const float* __restrict__ p, const float
 }
 
 // One level's [x | rx] pair buffer (rows b, half-width P, pads [s, P) zero) from fp32 sources as scaled
-// fp16: x from X rows (idx-gathered, level 0) or x32 (B x s), rx from rx32; the scale covers every half
-// written (max of the given slots) and block 0 publishes it for the consuming GEMMs. Grid-stride over
-// (row, 4-column group): float4 reads where the row width allows, 8-byte pair writes.
-__device__ __forceinline__ void split4(const float (&x)[4], float sc, bf16* h, bf16* l) {
-  bf16 hh[4], ll[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) split_f16(x[u], sc, hh[u], ll[u]);
-  *reinterpret_cast<uint2*>(h) = *reinterpret_cast<const uint2*>(hh);
-  *reinterpret_cast<uint2*>(l) = *reinterpret_cast<const uint2*>(ll);
-}
-__device__ __forceinline__ void load4(const float* row, int k, int s, bool vec, float (&x)[4]) {
-  if (vec && k + 3 < s) {
-    const float4 v = *reinterpret_cast<const float4*>(row + k);
-    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+// fp16: x from X rows (idx-gathered, level 0) or x32 (B x s), rx from rx32. One scale covers both halves:
+//   x only (the point / gradient passes): s = pow2_scale(max |x|), written, and recorded in *sx;
+//   x and rx (an HVP: x is the point's cached value, already in the buffer at scale *sx): the x half is
+//   rewritten only when max(|x|, |rx|) needs a smaller scale than *sx (then *sx shrinks); otherwise only
+//   rx is written, at *sx. *sx is read by every block at its start and updated by the last block to finish
+//   (ticket), so no block sees a half-updated value.
+// Block 0 publishes the scale for the consuming GEMMs (*sout). 2D grid: rows over y, 8-column groups over x.
+__device__ __forceinline__ void load8(const float* row, int k, int s, bool vec, float (&x)[8]) {
+  if (vec && k + 7 < s) {
+    const float4 a = *reinterpret_cast<const float4*>(row + k), b = *reinterpret_cast<const float4*>(row + k + 4);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
   } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) x[u] = k + u < s ? row[k + u] : 0.f;
+    for (int u = 0; u < 8; ++u) x[u] = k + u < s ? row[k + u] : 0.f;
   }
 }
-__global__ void split_pair_kernel(int B, int s, int P, const float* __restrict__ X, const int64_t* __restrict__ idx,
-                                  int ldX, const float* __restrict__ x32, const float* __restrict__ rx32,
-                                  const unsigned* __restrict__ mxx, const unsigned* __restrict__ mxr,
-                                  float* __restrict__ sout, bf16* __restrict__ Rh, bf16* __restrict__ Rl) {
+__device__ __forceinline__ void split8(const float (&x)[8], float sc, bf16* h, bf16* l) {
+  bf16 hh[8], ll[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) split_f16(x[u], sc, hh[u], ll[u]);
+  *reinterpret_cast<uint4*>(h) = *reinterpret_cast<const uint4*>(hh);
+  *reinterpret_cast<uint4*>(l) = *reinterpret_cast<const uint4*>(ll);
+}
+__global__ void __launch_bounds__(128) split_pair_kernel(int B, int s, int P, const float* __restrict__ X,
+                                                         const int64_t* __restrict__ idx, int ldX,
+                                                         const float* __restrict__ x32, const float* __restrict__ rx32,
+                                                         const unsigned* __restrict__ mxx,
+                                                         const unsigned* __restrict__ mxr, float* __restrict__ sout,
+                                                         float* sx, unsigned* ticket, bf16* __restrict__ Rh,
+                                                         bf16* __restrict__ Rl) {
   float mx = 0.f;
   if (mxx) mx = fmaxf(mx, __uint_as_float(*mxx));
   if (mxr) mx = fmaxf(mx, __uint_as_float(*mxr));
-  const float sc = pow2_scale(mx);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sout = sc;
-  const int G = P / 4;  // P is a multiple of 8
+  const float s_need = pow2_scale(mx);
+  const bool has_x = X != nullptr || x32 != nullptr;
+  bool wx = has_x;
+  float sc = s_need;
+  if (has_x && rx32) {
+    const float s_have = *sx;
+    wx = !(s_have > 0.f) || s_need < s_have;
+    sc = wx ? s_need : s_have;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *sout = sc;
+  const int G = P / 8;  // P is a multiple of 8
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const bool vx = X ? (ldX % 4 == 0) : (s % 4 == 0), vr = s % 4 == 0;
-  const size_t total = (size_t)B * G;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int b = (int)(i / G), k = (int)(i - (size_t)b * G) * 4;
-    const size_t r = (size_t)b * (2 * P) + k;
-    float x[4];
-    if (X || x32) {
-      const float* row = X ? X + (size_t)(idx ? idx[b] : b) * ldX : x32 + (size_t)b * s;
-      load4(row, k, s, vx, x);
-      split4(x, sc, Rh + r, Rl + r);
+  if (g < G) {
+    const int k = g * 8;
+    // two rows per step, all four loads issued before the first split (one memory latency per two rows)
+    for (int b = blockIdx.y; b < B; b += 2 * gridDim.y) {
+      const int b2 = b + gridDim.y;
+      const bool two = b2 < B;
+      float x0[8], x1[8], r0[8], r1[8];
+      if (wx) {
+        load8(X ? X + (size_t)(idx ? idx[b] : b) * ldX : x32 + (size_t)b * s, k, s, vx, x0);
+        if (two) load8(X ? X + (size_t)(idx ? idx[b2] : b2) * ldX : x32 + (size_t)b2 * s, k, s, vx, x1);
+      }
+      if (rx32) {
+        load8(rx32 + (size_t)b * s, k, s, vr, r0);
+        if (two) load8(rx32 + (size_t)b2 * s, k, s, vr, r1);
+      }
+      const size_t o0 = (size_t)b * (2 * P) + k, o1 = (size_t)b2 * (2 * P) + k;
+      if (wx) {
+        split8(x0, sc, Rh + o0, Rl + o0);
+        if (two) split8(x1, sc, Rh + o1, Rl + o1);
+      }
+      if (rx32) {
+        split8(r0, sc, Rh + o0 + P, Rl + o0 + P);
+        if (two) split8(r1, sc, Rh + o1 + P, Rl + o1 + P);
+      }
     }
-    if (rx32) {
-      load4(rx32 + (size_t)b * s, k, s, vr, x);
-      split4(x, sc, Rh + r + P, Rl + r + P);
+  }
+  if (wx) {  // record the x half's scale once every block is done with *sx
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1) {
+        *sx = sc;
+        *ticket = 0u;
+      }
     }
   }
 }
@@ -485,11 +522,15 @@ static void split_pair(dho2g_mlp* m, int B, int s, int P, const float* X, const 
                        const float* rx32, const unsigned* mxx, const unsigned* mxr, float* sout, bf16* Rh, bf16* Rl) {
   dho2g_ctx* ctx = m->ctx;
   const int slot = ctx->kt_begin();
-  const size_t work = (size_t)B * (P / 4);
-  const int grid = (int)std::max<size_t>(1, std::min<size_t>(cdiv(work, 256), (size_t)ctx->sm_count * 8));
-  split_pair_kernel<<<grid, 256, 0, ctx->stream>>>(B, s, P, X, idx, ldX, x32, rx32, mxx, mxr, sout, Rh, Rl);
+  const int gx = (int)cdiv((size_t)(P / 8), 128);
+  // one wave of resident blocks (12 of 128 threads per SM at this kernel's register count), rows strided
+  const int gy = (int)std::max<size_t>(1, std::min<size_t>((size_t)B, std::max<size_t>(1, (size_t)ctx->sm_count * 12 / gx)));
+  const size_t bi = (size_t)(sout - m->scl.p);  // this buffer's x-half scale and ticket
+  split_pair_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(B, s, P, X, idx, ldX, x32, rx32, mxx, mxr, sout,
+                                                          m->sclx.p + bi, m->sticket.p + bi, Rh, Rl);
   DHO2G_LAUNCH();
-  ctx->kt_end(slot, "split_pair", (double)B * s * 8.0 * (((X || x32) ? 1.0 : 0.0) + (rx32 ? 1.0 : 0.0)));
+  // algorithmic bytes: rx always, x when this call may rewrite it (counted as written: an upper bound)
+  ctx->kt_end(slot, "split_pair", (double)B * s * 8.0 * ((rx32 ? 1.0 : 0.0) + ((X || x32) && !rx32 ? 1.0 : 0.0)));
 }
 
 void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool /*with_r*/) {
