@@ -166,6 +166,9 @@ int dho2g_ese_eigvecs(const dho2g_ese* ese, double* vecs_shard);
 /* The full V_hat (n x r, column-major) on every rank, as extract_ese_distributed returns it after its
  * gather_rows (dist_lanczos.cpp:148-156). Collective: every rank calls it. */
 int dho2g_ese_gather(const dho2g_ese* ese, double* vecs_full);
+/* This rank's V_hat rows (signs applied) into a caller-owned device fp32 buffer, column-major with
+ * leading dimension ld >= rows (checks that keep a large V_hat on the device). */
+int dho2g_ese_eigvecs_device(const dho2g_ese* ese, float* dst, size_t ld);
 /* Build an ESE from host data (tests feed the reference's eigenpairs): V is n x r column-major. */
 int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, size_t n, size_t r,
                         dho2g_ese** out);

@@ -109,6 +109,7 @@ _SIGS = {
     "dho2g_ese_eigvals": ([vp, dp], C.c_int),
     "dho2g_ese_eigvecs": ([vp, dp], C.c_int),
     "dho2g_ese_gather": ([vp, dp], C.c_int),
+    "dho2g_ese_eigvecs_device": ([vp, vp, C.c_size_t], C.c_int),
     "dho2g_ese_from_host": ([vp, dp, dp, C.c_size_t, C.c_size_t, C.POINTER(vp)], C.c_int),
     "dho2g_ese_from_device": ([vp, dp, vp, C.c_size_t, C.c_size_t, C.c_size_t, C.POINTER(vp)], C.c_int),
     "dho2g_ese_destroy": ([vp], C.c_int),

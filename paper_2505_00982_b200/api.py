@@ -675,6 +675,11 @@ class EseResult:
             check(lib.dho2g_ese_gather(self.h, _d(out)))
         return out.reshape(r, n).T
 
+    def eigvecs_to_device(self, ptr: int, ld: int):
+        """This rank's V_hat rows (signs applied) into a device fp32 buffer (column-major, leading dimension
+        ld), e.g. a torch tensor's data_ptr()."""
+        check(lib.dho2g_ese_eigvecs_device(self.h, C.c_void_p(ptr), ld))
+
     @classmethod
     def from_host(cls, ctx: Context, eigvals, V):
         eigvals = _f64(eigvals)

@@ -883,6 +883,24 @@ int dho2g_ese_gather(const dho2g_ese* ese, double* vecs_full) {
   });
 }
 
+// This rank's V_hat rows (signs applied) into a caller-owned device fp32 buffer (column-major, leading dimension
+// ld >= rows): for checks that keep a 101 M x 32 V_hat on the device.
+__global__ void ese_copy_kernel(const float* __restrict__ V, size_t ldv, size_t rows, float sign, float* dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = sign * V[i];
+}
+int dho2g_ese_eigvecs_device(const dho2g_ese* ese, float* dst, size_t ld) {
+  return guard([&] {
+    check_ctx(ese->ctx);
+    if (ld < ese->rows) fail(DHO2G_ARGUMENT, "ese_eigvecs_device: leading dimension < rows");
+    for (size_t c = 0; c < ese->r; ++c)
+      ese_copy_kernel<<<(unsigned)std::max<size_t>(1, std::min<size_t>(cdiv(ese->rows, 256), 4096)), 256, 0,
+                        ese->ctx->stream>>>(ese->V.p + c * ese->ldv, ese->ldv, ese->rows, ese->sign[c], dst + c * ld);
+    DHO2G_LAUNCH();
+    DHO2G_CUDA(cudaStreamSynchronize(ese->ctx->stream));
+  });
+}
+
 int dho2g_ese_from_host(dho2g_ctx* ctx, const double* eigvals, const double* V, size_t n, size_t r, dho2g_ese** out) {
   return guard([&] {
     check_ctx(ctx);
