@@ -152,6 +152,22 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
       ctx->gemm_f16 = (int)value;
       ++g_graph_gen;  // baked into captured refresh graphs
     }
+    else if (k == "mlp_small") {
+      ctx->mlp_small = (int)value;
+      ++g_graph_gen;  // baked into captured refresh graphs
+    }
+    else if (k == "lanczos_small") {
+      ctx->lanczos_small = (int)value;
+      ++g_graph_gen;
+    }
+    else if (k == "mlp_small_mflop") {
+      ctx->mlp_small_mflop = value;
+      ++g_graph_gen;
+    }
+    else if (k == "mlp_small_ctas_per_sm") {
+      ctx->mlp_small_ctas_per_sm = (int)value;
+      ++g_graph_gen;
+    }
     else if (k == "hvp_route") ctx->hvp_route = (int)value;
     else if (k == "upd_p2_variant") ctx->upd_p2_variant = (int)value;
     else if (k == "gemm_pdl") {

@@ -206,4 +206,34 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// Butterfly reduction of K per-lane values at once: at each of the first log2(K) levels every lane
+// keeps half of its values and trades the other half with its partner, so K = 8 values take 9 fp64
+// shuffles (4 + 2 + 1 + 2) instead of 40. Lane l ends up holding value
+// sum_L ((l >> L) & 1) * (K >> (L + 1)), for l < K.
+template <int K>
+__device__ __forceinline__ double butterfly_sum(double (&v)[K], int lane) {
+  int n = K, level = 0;
+#pragma unroll
+  for (; n > 1; n >>= 1, ++level) {
+    const bool b = (lane >> level) & 1;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double send = b ? v[i] : v[i + n / 2];
+      const double keep = b ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << level);
+    }
+  }
+  double u = v[0];
+#pragma unroll
+  for (; level < 5; ++level) u += __shfl_xor_sync(0xffffffffu, u, 1 << level);
+  return u;
+}
+template <int K>
+__device__ __forceinline__ int butterfly_index(int lane) {
+  int idx = 0;
+#pragma unroll
+  for (int L = 0; (K >> (L + 1)) > 0; ++L) idx += ((lane >> L) & 1) * (K >> (L + 1));
+  return idx;
+}
+
 }  // namespace dho2g

@@ -14,6 +14,9 @@
 namespace dho2g {
 
 constexpr int kMaxLanczos = 1024;  // m <= 1023 (C5 sweep needs 512)
+// fp32 adaptation of the reference's breakdown / safeguard thresholds (lz_decide_kernel)
+constexpr double kBreakdownFloor32 = 4e-6;
+constexpr double kSafeguardFloor32 = 1e-3;
 constexpr int kGsChunk = 2048;     // rows per GS pass-1 chunk; shard rows are padded to this
 
 // ------------------------------------------------------------------------- host bookkeeping
@@ -61,6 +64,11 @@ struct dho2g_ctx {
                          // the drains are cheap
   int gemm_f16 = 1;      // MLP GEMM operands as power-of-two-scaled fp16 (hi, lo) pairs (22 significant bits)
                          // instead of bf16 pairs (16 bits); same tcgen05 kind::f16 rate
+  int mlp_small = 1;      // MLP passes of small models (HVP <= mlp_small_mflop MFLOP) as one persistent CUDA-core
+                         // launch each (mlp_small.cu) instead of the tcgen05 GEMM sequence
+  double mlp_small_mflop = 2000.0;
+  int lanczos_small = 1;  // world 1, small MLP operator, m <= 512: the whole refresh as one persistent launch
+  int mlp_small_ctas_per_sm = 1;
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
   dho2g::DevBuf<unsigned> gemm_flags2;
@@ -220,6 +228,21 @@ struct dho2g_mlp {
   unsigned* mx_w(int t) { return amax.p + 4 * (L + 1) + t; }
   unsigned* mx_x() { return amax.p + 4 * (L + 1) + L; }
 
+  // Lazily packed operands: the W halves of w_cur (wv_packed == w_cur once packed for the current load) and
+  // the level-0 batch (input_packed); the small-model path reads fp32 directly and never packs them.
+  const float* wv_packed = nullptr;
+  bool input_packed = false;
+  const float* x_src = nullptr;  // current batch: rows X[idx[b]] (idx null: b), labels y likewise
+  const int64_t* x_idx = nullptr;
+  const float* y_src = nullptr;
+  size_t x_B = 0;
+  bool prepared_small = false;   // the cached point quantities came from the small-model path
+  dho2g::DevBuf<float> x0, y0;   // small-model path: device copy of a host-resident batch
+  dho2g::DevBuf<float> sm_part;  // small-model path: split partials, tickets, grid-barrier words
+  dho2g::DevBuf<unsigned> sm_tickets;
+  dho2g::DevBuf<unsigned long long> sm_bar;
+  int sm_bar_nb = 0;  // grid size the barrier counter is a multiple of
+
   void ensure_batch(size_t B);
   ~dho2g_mlp() {
     for (cudaEvent_t ev : pack_ev) cudaEventDestroy(ev);
@@ -244,7 +267,15 @@ void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, si
 void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double* acc2);
 
-void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);  // acc2 = {sum loss, sum correct} of last batch
+void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);
+// Small-model path (mlp_small.cu): eligibility (ctx option mlp_small, HVP flops at batch B), one persistent
+// launch per pass (mode 0 gradient, 1 point preparation, 2 HVP, 3 evaluation), scratch presizing.
+bool mlp_small_eligible(const dho2g_mlp* m, size_t B);
+void mlp_small_run(dho2g_mlp* m, int mode, size_t B, const float* w, const float* v, const float* vscale, float* out,
+                   size_t ncls, double scale);
+void mlp_small_presize(dho2g_mlp* m, size_t B);
+bool lanczos_small_eligible(const dho2g_lanczos* lz, const dho2g_op* op);
+void lanczos_small_run(dho2g_lanczos* lz, dho2g_op* op);  // m iterations (after v1 / lz_init) in one launch  // acc2 = {sum loss, sum correct} of last batch
 // Allocates the batch-dependent buffers for batches up to B up front (graph-stable pointers).
 void mlp_presize(dho2g_mlp* m, size_t B);
 
@@ -365,6 +396,7 @@ struct dho2g_op {
   std::vector<double> hv_in, hv_out;
   dho2g::HostBuf<float> pin;
   bool weights_loaded = false;
+  void load_mlp_input();  // kind 0: this rank's curvature batch and the weights into the model (once per point)
   // h_shard[r] = (H (vscale * vfull))[begin + r]
   void apply(const float* vfull, const float* vscale, float* h_shard, size_t begin, size_t rows, size_t base);
 };
@@ -402,6 +434,7 @@ struct dho2g_lanczos {
   dho2g::DevBuf<int4> xsweep;   // split tql2: per-sweep (mm, cnt, log offset)
   dho2g::DevBuf<int> xnsweep;
   dho2g::DevBuf<double> xd;     // split tql2: eigenvalues in slot order
+  dho2g::DevBuf<double> sm_part1, sm_part2;  // fused small-model refresh: per-CTA Gram-Schmidt partials
   double ms = 0.0;
   // CUDA graph of the refresh launch sequence (world 1)
   cudaGraphExec_t gexec = nullptr;

@@ -38,9 +38,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSub = 512;  // rows per warp work item (32 lanes x 4 float4)
-constexpr double kBreakdownFloor32 = 4e-6;
 constexpr int kP2Unroll = 4;  // basis columns in flight per pass-2 thread (x 4 float4)
-constexpr double kSafeguardFloor32 = 1e-3;
 
 // ------------------------------------------------------------------ start vector
 // seeded_unit_gaussian (lanczos.cpp:18-26): Rng(seed*phi + 0x1234567).fill_normal, computed
@@ -100,36 +98,7 @@ __global__ void lz_init_kernel(LzDev* st, const double* __restrict__ allp, int w
 // rankp[j] = D_j^T h (j < active), rankp[active] = h^T h, fp64, deterministic order.
 // GRAM also accumulates G_j = D_j^T D_{active-1} (j < active) into rankp[goff + j].
 //
-// Butterfly reduction of K per-lane values at once: at each of the first log2(K) levels every lane
-// keeps half of its values and trades the other half with its partner, so K = 8 values take 9 fp64
-// shuffles (4 + 2 + 1 + 2) instead of 40. Lane l ends up holding value
-// sum_L ((l >> L) & 1) * (K >> (L + 1)), for l < K.
-template <int K>
-__device__ __forceinline__ double butterfly_sum(double (&v)[K], int lane) {
-  int n = K, level = 0;
-#pragma unroll
-  for (; n > 1; n >>= 1, ++level) {
-    const bool b = (lane >> level) & 1;
-#pragma unroll
-    for (int i = 0; i < n / 2; ++i) {
-      const double send = b ? v[i] : v[i + n / 2];
-      const double keep = b ? v[i + n / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << level);
-    }
-  }
-  double u = v[0];
-#pragma unroll
-  for (; level < 5; ++level) u += __shfl_xor_sync(0xffffffffu, u, 1 << level);
-  return u;
-}
-template <int K>
-__device__ __forceinline__ int butterfly_index(int lane) {
-  int idx = 0;
-#pragma unroll
-  for (int L = 0; (K >> (L + 1)) > 0; ++L) idx += ((lane >> L) & 1) * (K >> (L + 1));
-  return idx;
-}
-
+// (butterfly_sum / butterfly_index: common.cuh)
 template <bool GRAM>
 __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restrict__ D, size_t ldd,
                                                             const float* __restrict__ h, int active, int nchunks,
@@ -960,19 +929,24 @@ int grid_for(dho2g_ctx* ctx, size_t work, int threads, int per_sm = 4) {
 }  // namespace
 
 // ------------------------------------------------------------------ dho2g_op::apply
+void dho2g_op::load_mlp_input() {
+  dho2g_mlp* m = mlp;
+  // a rank whose slice of the curvature batch is empty (B < G) contributes zeros and runs no HVP
+  if (b1 > b0 && (m->w_cur != wptr || !weights_loaded || m->input_owner != this ||
+                  m->f16 != (ctx->gemm_f16 ? 1 : 0))) {
+    if (idx.p) mlp_set_input(m, Xptr, yptr, idx.p + b0, b1 - b0, true);
+    else mlp_set_input(m, Xptr + b0 * m->sizes[0], yptr + b0, nullptr, b1 - b0, true);
+    mlp_load_weights(m, wptr);
+    m->input_owner = this;
+    weights_loaded = true;
+  }
+}
+
 void dho2g_op::apply(const float* vfull, const float* vscale, float* h_shard, size_t begin, size_t rows, size_t base) {
   cudaStream_t st = ctx->stream;
   if (kind == 0) {
     dho2g_mlp* m = mlp;
-    // a rank whose slice of the curvature batch is empty (B < G) contributes zeros and runs no HVP
-    if (b1 > b0 && (m->w_cur != wptr || !weights_loaded || m->input_owner != this ||
-                    m->f16 != (ctx->gemm_f16 ? 1 : 0))) {
-      if (idx.p) mlp_set_input(m, Xptr, yptr, idx.p + b0, b1 - b0, true);
-      else mlp_set_input(m, Xptr + b0 * m->sizes[0], yptr + b0, nullptr, b1 - b0, true);
-      mlp_load_weights(m, wptr);
-      m->input_owner = this;
-      weights_loaded = true;
-    }
+    load_mlp_input();
     float* out = ctx->world == 1 ? h_shard : hfull.p;
     if (ctx->world > 1 && ctx->hvp_route) {
       // fused reduce-scatter: the weight-block GEMMs write every W element straight into its owner's
@@ -1191,6 +1165,10 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
     DHO2G_LAUNCH();
   }
 
+  if (lanczos_small_eligible(lz, op)) {  // small MLP operator: the m iterations as one persistent launch
+    lanczos_small_run(lz, op);
+    return;
+  }
   const int nchunks = (int)(lz->ldd / kGsChunk);
   const size_t ngroups = lz->ldd / 4;
   const double* allp = world > 1 ? lz->allp.p : lz->rankp.p;

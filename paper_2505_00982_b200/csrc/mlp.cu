@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include "internal.h"
+#include "mlp_dev.cuh"
 
 using namespace dho2g;
 
@@ -265,11 +266,7 @@ __global__ void __launch_bounds__(128) split_pair_kernel(int B, int s, int P, co
 }
 
 // ------------------------------------------------------------------ output layer delta
-// oracle.cpp:476-495 (delta) and :572-599 (R-delta); also per-sample loss / correctness.
-__device__ void output_delta_row(int b, int O, int mse, int ncls, int do0, int do1, double scale,
-                                 const float* __restrict__ z, const float* __restrict__ rz,
-                                 const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
-                                 double* __restrict__ loss, int* __restrict__ correct);
+// (output_delta_row: mlp_dev.cuh)
 __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, int do1, double scale,
                                     const float* __restrict__ z, const float* __restrict__ rz,
                                     const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
@@ -279,7 +276,7 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, in
   if (mxd || mxrd) {  // max |d|, |rd| for the scaled-fp16 split (this thread's row, after the deltas below)
     float md = 0.f, mr = 0.f;
     if (b < B) {
-      output_delta_row(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
+      output_delta_row<false>(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
       for (int j = 0; j < O; ++j) {
         if (do0) md = fmaxf(md, fabsf(d[(size_t)b * O + j]));
         if (do1) mr = fmaxf(mr, fabsf(rd[(size_t)b * O + j]));
@@ -290,50 +287,7 @@ __global__ void output_delta_kernel(int B, int O, int mse, int ncls, int do0, in
     return;
   }
   if (b >= B) return;
-  output_delta_row(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
-}
-
-__device__ void output_delta_row(int b, int O, int mse, int ncls, int do0, int do1, double scale,
-                                 const float* __restrict__ z, const float* __restrict__ rz,
-                                 const float* __restrict__ lab, float* __restrict__ d, float* __restrict__ rd,
-                                 double* __restrict__ loss, int* __restrict__ correct) {
-  const float* o = z + (size_t)b * O;
-  const float* ro = do1 ? rz + (size_t)b * O : nullptr;
-  float* dd = d + (size_t)b * O;
-  float* rdd = do1 ? rd + (size_t)b * O : nullptr;
-  const float y = lab[b];
-  int best = 0;
-  for (int j = 1; j < O; ++j)
-    if (o[j] > o[best]) best = j;
-  if (do0) correct[b] = (ncls > 0 && best == (int)y) ? 1 : 0;
-  if (!mse) {
-    const int lbl = (int)y;
-    const float mx = o[best];
-    double den = 0.0;
-    for (int j = 0; j < O; ++j) den += exp((double)o[j] - (double)mx);
-    double sdot = 0.0;
-    for (int j = 0; j < O; ++j) {
-      const double soft = exp((double)o[j] - (double)mx) / den;
-      if (do0) dd[j] = (float)((soft - (j == lbl ? 1.0 : 0.0)) * scale);
-      if (do1) sdot += soft * ro[j];
-    }
-    if (do1)
-      for (int j = 0; j < O; ++j) {
-        const double soft = exp((double)o[j] - (double)mx) / den;
-        rdd[j] = (float)(soft * (ro[j] - sdot) * scale);
-      }
-    if (do0) loss[b] = (double)mx + log(den) - (double)o[lbl];
-  } else {
-    double acc = 0.0;
-    for (int j = 0; j < O; ++j) {
-      const float t = ncls > 0 ? (j == (int)y ? 1.f : 0.f) : (j == 0 ? y : 0.f);
-      const float df = o[j] - t;
-      if (do0) dd[j] = (float)(df * scale);
-      if (do1) rdd[j] = (float)(ro[j] * scale);
-      acc += 0.5 * (double)df * (double)df;
-    }
-    if (do0) loss[b] = acc;
-  }
+  output_delta_row<false>(b, O, mse, ncls, do0, do1, scale, z, rz, lab, d, rd, loss, correct);
 }
 
 // Bias block as a column sum of a row-major pair buffer: out[o] = sum_{b < B} (hi + lo)[b][off + o].
@@ -403,6 +357,17 @@ __global__ void csum_final_kernel(const float* __restrict__ csum, int nrb, int c
   double t = 0.0;
   for (int rb = 0; rb < nrb; ++rb) t += (double)csum[(size_t)rb * cols + c];
   out[c] = (float)t;
+}
+
+// batch rows X[idx[b]] (and labels) into a dense device copy
+__global__ void gather_rows_kernel(const float* __restrict__ X, const float* __restrict__ y, const int64_t* __restrict__ idx,
+                                   int B, int s, float* __restrict__ out, float* __restrict__ yout) {
+  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+    const int64_t r = idx ? idx[b] : b;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < s) out[(size_t)b * s + c] = X[(size_t)r * s + c];
+    if (blockIdx.x == 0 && threadIdx.x == 0) yout[b] = y[r];
+  }
 }
 
 // label gather
@@ -488,22 +453,32 @@ static void sync_format(dho2g_mlp* m) {
   if (m->f16 == f) return;
   m->f16 = f;
   m->w_cur = nullptr;
+  m->wv_packed = nullptr;
+  m->input_packed = false;
   m->input_owner = nullptr;
   m->prepared = nullptr;
 }
 
+// The W halves are packed on first use by the tensor-core path (the small-model path reads w directly).
 void mlp_load_weights(dho2g_mlp* m, const float* w) {
   sync_format(m);
   m->w_cur = w;
+  m->wv_packed = nullptr;
   m->prepared = nullptr;
   if (m->wv_vbound < 1.0f) m->wv_vbound = 1.0f;  // unit Lanczos directions
-  pack_params(m, w, nullptr, 1);
+}
+
+static void ensure_weights_packed(dho2g_mlp* m, bool force = false) {
+  if (!force && m->wv_packed == m->w_cur) return;
+  pack_params(m, m->w_cur, nullptr, 1);
+  m->wv_packed = m->w_cur;
 }
 
 void mlp_load_direction(dho2g_mlp* m, const float* v, const float* vscale) { pack_params(m, v, vscale, 0); }
 
 void mlp_presize(dho2g_mlp* m, size_t B) {
   m->ensure_batch(B);
+  mlp_small_presize(m, B);
   m->csum.ensure_g((size_t)2 * cdiv(B, 32) * m->smax);
   m->colpart.ensure_g((size_t)kColChunks * m->smax);
   m->coltickets.ensure_g(cdiv(m->smax, 64));
@@ -533,11 +508,48 @@ static void split_pair(dho2g_mlp* m, int B, int s, int P, const float* X, const 
   ctx->kt_end(slot, "split_pair", (double)B * s * 8.0 * ((rx32 ? 1.0 : 0.0) + ((X || x32) && !rx32 ? 1.0 : 0.0)));
 }
 
+static void ensure_input_packed(dho2g_mlp* m);
+
+// Records the batch; the tensor-core path's level-0 operands are packed here unless the small-model path
+// (which reads X and y directly) takes batches of this size.
 void mlp_set_input(dho2g_mlp* m, const float* X, const float* y, const int64_t* idx, size_t B, bool /*with_r*/) {
   sync_format(m);
   m->ensure_batch(B);
   m->input_owner = nullptr;
   m->prepared = nullptr;
+  m->x_src = X;
+  m->x_idx = idx;
+  m->y_src = y;
+  m->x_B = B;
+  m->input_packed = false;
+  if (!mlp_small_eligible(m, B)) {
+    ensure_input_packed(m);
+    return;
+  }
+  // The small-model path reads X in every pass: a batch in host memory (the end-to-end mode's dataset,
+  // mapped pinned) is gathered to the device once here instead of crossing PCIe in every HVP.
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, X) != cudaSuccess) cudaGetLastError();
+  if (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged) {
+    const size_t s0 = m->sizes[0];
+    m->x0.ensure_g(round_up(B, 128) * s0);
+    m->y0.ensure_g(round_up(B, 128));
+    gather_rows_kernel<<<dim3((unsigned)cdiv(s0, 128), (unsigned)std::min<size_t>(B, 65535)), 128, 0, m->ctx->stream>>>(
+        X, y, idx, (int)B, (int)s0, m->x0.p, m->y0.p);
+    DHO2G_LAUNCH();
+    m->x_src = m->x0.p;
+    m->y_src = m->y0.p;
+    m->x_idx = nullptr;
+  }
+}
+
+static void ensure_input_packed(dho2g_mlp* m) {
+  if (m->input_packed) return;
+  m->input_packed = true;
+  const float* X = m->x_src;
+  const float* y = m->y_src;
+  const int64_t* idx = m->x_idx;
+  const size_t B = m->x_B;
   const int s0 = (int)m->sizes[0];
   if (m->f16) {
     dho2g_ctx* ctx = m->ctx;
@@ -841,6 +853,11 @@ static void backward(dho2g_mlp* m, size_t B, float* out, bool do0, bool do1, boo
 void mlp_grad_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double scale, float* g) {
   mlp_set_input(m, X, y, idx, B, false);
+  if (mlp_small_eligible(m, B)) {
+    mlp_small_run(m, 0, B, w, nullptr, nullptr, g, ncls, scale);
+    return;
+  }
+  ensure_weights_packed(m);
   forward(m, w, B, true, false);
   output_delta(m, B, ncls, scale, true, false);
   backward(m, B, g, true, false, true);
@@ -855,6 +872,15 @@ struct ChunkScope {
 
 void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale) {
   // input and weights must already be loaded (mlp_set_input / mlp_load_weights)
+  if (mlp_small_eligible(m, B)) {
+    mlp_small_run(m, 1, B, m->w_cur, nullptr, nullptr, nullptr, ncls, scale);
+    m->prepared = m->w_cur;
+    m->prepared_small = true;
+    return;
+  }
+  ensure_input_packed(m);
+  ensure_weights_packed(m);
+  m->prepared_small = false;
   ChunkScope cs(m);
   forward(m, m->w_cur, B, true, false);
   output_delta(m, B, ncls, scale, true, false);
@@ -864,11 +890,16 @@ void mlp_prepare_point(dho2g_mlp* m, size_t B, size_t ncls, double scale) {
 
 void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, size_t ncls, double scale, float* hv,
                  float vbound) {
+  if (mlp_small_eligible(m, B)) {
+    if (m->prepared != m->w_cur || !m->prepared_small) mlp_prepare_point(m, B, ncls, scale);
+    mlp_small_run(m, 2, B, m->w_cur, v, vscale, hv, ncls, scale);
+    return;
+  }
   if (m->f16 && vbound > m->wv_vbound) {  // the W halves' scale must also cover this direction
     m->wv_vbound = vbound;
-    pack_params(m, m->w_cur, nullptr, 1);
+    ensure_weights_packed(m, true);
   }
-  if (m->prepared != m->w_cur) mlp_prepare_point(m, B, ncls, scale);
+  if (m->prepared != m->w_cur || m->prepared_small) mlp_prepare_point(m, B, ncls, scale);
   ChunkScope cs(m);
   m->v_bias_ptr = v;
   m->v_scale_ptr = vscale;
@@ -881,8 +912,13 @@ void mlp_hvp_dev(dho2g_mlp* m, const float* v, const float* vscale, size_t B, si
 void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, const int64_t* idx, size_t B,
                   size_t ncls, double* acc2) {
   mlp_set_input(m, X, y, idx, B, false);
-  forward(m, w, B, true, false);
-  output_delta(m, B, ncls, 1.0, true, false);
+  if (mlp_small_eligible(m, B)) {
+    mlp_small_run(m, 3, B, w, nullptr, nullptr, nullptr, ncls, 1.0);
+  } else {
+    ensure_weights_packed(m);
+    forward(m, w, B, true, false);
+    output_delta(m, B, ncls, 1.0, true, false);
+  }
   eval_reduce_kernel<<<1, 1024, 0, m->ctx->stream>>>((int)B, m->sample_loss.p, m->sample_correct.p, acc2);
   DHO2G_LAUNCH();
 }

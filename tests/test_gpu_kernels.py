@@ -123,8 +123,16 @@ CASES = [([20, 16, 12, 5], 37, "tanh", "softmax_ce", 5), ([20, 16, 12, 5], 37, "
          ([784, 256, 10], 128, "tanh", "softmax_ce", 10), ([64, 96, 96, 96, 10], 200, "tanh", "softmax_ce", 10)]
 
 
+@pytest.fixture(params=[0, 1], ids=["tensor", "small"])
+def mlp_path(ctx, request):
+    """MLP tests below run on the tcgen05 GEMM path (mlp_small = 0) and the small-model path."""
+    ctx.set_option("mlp_small", request.param)
+    yield request.param
+    ctx.set_option("mlp_small", 1)
+
+
 @pytest.mark.parametrize("sizes,B,act,loss,ncls", CASES)
-def test_mlp_oracle_vs_checker(ctx, port, sizes, B, act, loss, ncls):
+def test_mlp_oracle_vs_checker(ctx, port, sizes, B, act, loss, ncls, mlp_path):
     from oracle.bindings import blobs_dataset
     X, y = blobs_dataset(B, sizes[0], max(ncls, 1), seed=11)
     if ncls == 0:
@@ -169,6 +177,7 @@ def test_mlp_scaled_fp16_operands_any_magnitude(ctx, port, act, loss, xscale):
     out = {}
     for f16 in (1, 0):
         ctx.set_option("gemm_f16", f16)
+        ctx.set_option("mlp_small", 0)  # the tensor-core operand formats
         try:
             mlp = d.MlpOracle(ctx, sizes, act, loss)
             b = d.Batch(X, y, ncls)
@@ -176,13 +185,14 @@ def test_mlp_scaled_fp16_operands_any_magnitude(ctx, port, act, loss, xscale):
             mlp.close()
         finally:
             ctx.set_option("gemm_f16", 1)
+            ctx.set_option("mlp_small", 1)
         assert np.isfinite(out[f16][0]).all() and np.isfinite(out[f16][1]).all()
         assert rel_l2(out[f16][0], hv_ref) < 1e-4 and rel_l2(out[f16][1], g_ref) < 1e-4
     # the 22-bit pairs are at least as close to the checker as the 16-bit ones (small-problem noise margin)
     assert rel_l2(out[1][0], hv_ref) <= 2.0 * rel_l2(out[0][0], hv_ref) + 1e-7
 
 
-def test_mlp_hvp_linear_symmetric(ctx, port):  # test_oracle.cpp:107-132
+def test_mlp_hvp_linear_symmetric(ctx, port, mlp_path):  # test_oracle.cpp:107-132
     from oracle.bindings import blobs_dataset
     sizes = [30, 24, 6]
     X, y = blobs_dataset(64, 30, 6, seed=2)
@@ -195,7 +205,7 @@ def test_mlp_hvp_linear_symmetric(ctx, port):  # test_oracle.cpp:107-132
     assert abs(u @ hv - v @ hu) <= 1e-4 * max(1.0, abs(u @ hv))
 
 
-def test_mlp_pure_and_zero_case(ctx):  # test_oracle.cpp:68-79 and :152-160
+def test_mlp_pure_and_zero_case(ctx, mlp_path):  # test_oracle.cpp:68-79 and :152-160
     from paper_2505_00982_b200.config import synthetic_dataset
     data = synthetic_dataset("two-gaussians", 40, 23)
     mlp = d.MlpOracle(ctx, [2, 8, 2], "relu", "softmax_ce")
@@ -234,7 +244,11 @@ def test_gemm_backends_agree_on_hvp(ctx, port):
         h1 = mlp.hvp(w, v, b)
     finally:
         ctx.set_option("gemm", 0)
-    h0 = mlp.hvp(w, v, b)
+    ctx.set_option("mlp_small", 0)
+    try:
+        h0 = mlp.hvp(w, v, b)
+    finally:
+        ctx.set_option("mlp_small", 1)
     assert rel_l2(h0, h1) < 2e-5
 
 

@@ -368,8 +368,9 @@ def test_c2_exact_config_trajectory(ctx, port):
     assert np.max(np.abs(res.residual_norm - ref["resid"]) / ref["resid"]) <= 1e-3
 
 
+@pytest.mark.parametrize("small", [1, 0])
 @pytest.mark.parametrize("recurrence", [0, 1])
-def test_c1_refresh_both_arithmetics(ctx, port, recurrence):
+def test_c1_refresh_both_arithmetics(ctx, port, recurrence, small):
     """C1 refresh (784-256-10, B = 128, m = 40, k = 10) against the checker in both projection modes:
     the faithful classical Gram-Schmidt of the raw h (lanczos_recurrence = 0, dist_lanczos.cpp:58-74 as
     written) and the default recurrence-first projection."""
@@ -380,11 +381,13 @@ def test_c1_refresh_both_arithmetics(ctx, port, recurrence):
     w = mlp.init_params(1)
     op = d.mlp_hvp_operator(ctx, mlp, w, d.Batch(X, y, 10))
     ctx.set_option("lanczos_recurrence", recurrence)
+    ctx.set_option("mlp_small", small)  # the small-model path (one persistent launch per HVP) or the tcgen05 GEMMs
     try:
         st = d.lanczos_distributed(ctx, 40, op, mlp.dim(), 4242)
         ese = d.extract_ese_distributed(ctx, st, 10, 0)
     finally:
         ctx.set_option("lanczos_recurrence", 1)
+        ctx.set_option("mlp_small", 1)
     ref = port.lanczos(dict(kind=2, n=mlp.dim(), sizes=sizes, w=w, X=X, y=y, ncls=10), 40, 4242, k=10,
                        want_basis=False)
     hn = np.abs(ref["eigvals"]).max()
@@ -393,7 +396,7 @@ def test_c1_refresh_both_arithmetics(ctx, port, recurrence):
     e_o = np.abs(st.tridiag.offdiag - ref["off"]) / hn
     V, Vr = T(ese.eigvecs_shard(mlp.dim()).T.copy()), T(ref["eigvecs"].T.copy())
     proj = projector_dist(V, Vr)
-    print(f"C1 refresh recurrence={recurrence}: eigenvalues {e_ev:.2e}, B diag {e_d.max():.2e} off {e_o.max():.2e} "
+    print(f"C1 refresh recurrence={recurrence} small={small}: eigenvalues {e_ev:.2e}, B diag {e_d.max():.2e} off {e_o.max():.2e} "
           f"(first 20 iterations {e_d[:20].max():.2e}), projector {proj:.2e}")
     assert st.iterations == ref["iterations"] == 40
     assert e_ev <= 1e-4
