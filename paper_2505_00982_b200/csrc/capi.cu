@@ -160,6 +160,10 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
       ctx->lanczos_small = (int)value;
       ++g_graph_gen;
     }
+    else if (k == "lanczos_small_max_n") {
+      ctx->lanczos_small_max_n = value;
+      ++g_graph_gen;
+    }
     else if (k == "mlp_small_mflop") {
       ctx->mlp_small_mflop = value;
       ++g_graph_gen;

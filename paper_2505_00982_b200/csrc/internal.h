@@ -67,7 +67,8 @@ struct dho2g_ctx {
   int mlp_small = 1;      // MLP passes of small models (HVP <= mlp_small_mflop MFLOP) as one persistent CUDA-core
                          // launch each (mlp_small.cu) instead of the tcgen05 GEMM sequence
   double mlp_small_mflop = 2000.0;
-  int lanczos_small = 1;  // world 1, small MLP operator, m <= 512: the whole refresh as one persistent launch
+  int lanczos_small = 1;  // world 1, small MLP operator (2: also diagonal), m <= 512: the whole refresh as one launch
+  double lanczos_small_max_n = 4e6;
   int mlp_small_ctas_per_sm = 1;
   cudaStream_t stream2 = nullptr;                 // side lane (created on first use)
   dho2g::DevBuf<float> gemm_ws2;                  // its GEMM workspace / flags (swapped in by SideLane)
@@ -434,7 +435,9 @@ struct dho2g_lanczos {
   dho2g::DevBuf<int4> xsweep;   // split tql2: per-sweep (mm, cnt, log offset)
   dho2g::DevBuf<int> xnsweep;
   dho2g::DevBuf<double> xd;     // split tql2: eigenvalues in slot order
-  dho2g::DevBuf<double> sm_part1, sm_part2;  // fused small-model refresh: per-CTA Gram-Schmidt partials
+  dho2g::DevBuf<double> sm_part1, sm_part2;  // fused refresh: per-CTA Gram-Schmidt partials
+  dho2g::DevBuf<unsigned long long> sm_bar;  // fused refresh of a diagonal operator: grid-barrier words
+  int sm_bar_nb = 0;
   double ms = 0.0;
   // CUDA graph of the refresh launch sequence (world 1)
   cudaGraphExec_t gexec = nullptr;

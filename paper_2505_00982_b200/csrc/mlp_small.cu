@@ -841,6 +841,8 @@ struct LzArgs {
   int n, m, gram, sg_on, stride, goff, ngs, rs;
   int sv_off;  // byte offset of the per-CTA arrays: after the stage ring / the pass-1 scratch, whichever is larger
   double ratio, rtol;  // floored on the host (fp32 adaptation, lanczos.cu)
+  int kind;            // operator: 0 small MLP (pass_phases), 1 diagonal (h = spec o (sigma_i D_i), diag_apply_kernel)
+  const float* spec;
 };
 
 // This CTA's slice: rows [blockIdx.x rs, min(n, (blockIdx.x + 1) rs)), float4 groups g = tid + kThr q
@@ -855,49 +857,54 @@ __device__ void gs_dots(const LzArgs& a, const float* y, int active, int it, boo
   const int ng = (int)max(0LL, (r1 - r0 + 3) / 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nj = active + 1, rowlen = nj + (gram ? active : 0);
-  float4 yv[kGsq], zv[kGsq];
+  for (int e = lane; e < rowlen; e += 32) sacc[warp * rowlen + e] = 0.0;  // warp-private rows
+  __syncwarp();
+  // row tiles of kThr kGsq float4 groups: y (and D_i) in registers per tile, columns in batches of 8
+  for (int g0 = 0; g0 < ng; g0 += kThr * kGsq) {
+    float4 yv[kGsq], zv[kGsq];
 #pragma unroll
-  for (int q = 0; q < kGsq; ++q) {
-    const int g = tid + kThr * q;
-    const bool on = g < ng;
-    yv[q] = on ? __ldcg(reinterpret_cast<const float4*>(y + r0) + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-    zv[q] = (on && gram) ? __ldcg(reinterpret_cast<const float4*>(a.D + (long long)it * a.ldd + r0) + g)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  for (int j0 = 0; j0 < nj; j0 += 8) {
-    float4 x[8][kGsq];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int j = j0 + u;
-#pragma unroll
-      for (int q = 0; q < kGsq; ++q) {
-        const int g = tid + kThr * q;
-        if (j < active && g < ng) x[u][q] = __ldcg(reinterpret_cast<const float4*>(a.D + (long long)j * a.ldd + r0) + g);
-        else x[u][q] = j == active ? yv[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    for (int q = 0; q < kGsq; ++q) {
+      const int g = g0 + tid + kThr * q;
+      const bool on = g < ng;
+      yv[q] = on ? __ldcg(reinterpret_cast<const float4*>(y + r0) + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+      zv[q] = (on && gram) ? __ldcg(reinterpret_cast<const float4*>(a.D + (long long)it * a.ldd + r0) + g)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    double v[16];
+    for (int j0 = 0; j0 < nj; j0 += 8) {
+      float4 x[8][kGsq];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      double sy = 0.0, sz = 0.0;
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u;
 #pragma unroll
-      for (int q = 0; q < kGsq; ++q) {
-        sy += (double)x[u][q].x * yv[q].x + (double)x[u][q].y * yv[q].y + (double)x[u][q].z * yv[q].z +
-              (double)x[u][q].w * yv[q].w;
-        sz += (double)x[u][q].x * zv[q].x + (double)x[u][q].y * zv[q].y + (double)x[u][q].z * zv[q].z +
-              (double)x[u][q].w * zv[q].w;
+        for (int q = 0; q < kGsq; ++q) {
+          const int g = g0 + tid + kThr * q;
+          if (j < active && g < ng) x[u][q] = __ldcg(reinterpret_cast<const float4*>(a.D + (long long)j * a.ldd + r0) + g);
+          else x[u][q] = j == active ? yv[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
-      v[2 * u] = sy;
-      v[2 * u + 1] = sz;
-    }
-    const double t = butterfly_sum<16>(v, lane);
-    if (lane < 16) {
-      const int idx = butterfly_index<16>(lane);
-      const int j = j0 + (idx >> 1);
-      if (idx & 1) {
-        if (gram && j < active) sacc[warp * rowlen + nj + j] = t;
-      } else if (j < nj) {
-        sacc[warp * rowlen + j] = t;
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double sy = 0.0, sz = 0.0;
+#pragma unroll
+        for (int q = 0; q < kGsq; ++q) {
+          sy += (double)x[u][q].x * yv[q].x + (double)x[u][q].y * yv[q].y + (double)x[u][q].z * yv[q].z +
+                (double)x[u][q].w * yv[q].w;
+          sz += (double)x[u][q].x * zv[q].x + (double)x[u][q].y * zv[q].y + (double)x[u][q].z * zv[q].z +
+                (double)x[u][q].w * zv[q].w;
+        }
+        v[2 * u] = sy;
+        v[2 * u + 1] = sz;
+      }
+      const double t = butterfly_sum<16>(v, lane);
+      if (lane < 16) {
+        const int idx = butterfly_index<16>(lane);
+        const int j = j0 + (idx >> 1);
+        if (idx & 1) {
+          if (gram && j < active) sacc[warp * rowlen + nj + j] += t;
+        } else if (j < nj) {
+          sacc[warp * rowlen + j] += t;
+        }
       }
     }
   }
@@ -974,7 +981,14 @@ __global__ void __launch_bounds__(kThr) lanczos_small_kernel(const SmallNet net_
     // ---- HVP: h = H (sigma_it D_it)
     const bool trace_it = it == 20;
     if (trace_it) stamp(c, 20);
-    pass_phases(net, c, a.D + (long long)it * a.ldd, sig[it], ring, s_last, sg, &bar_next);
+    if (a.kind == 0) {
+      pass_phases(net, c, a.D + (long long)it * a.ldd, sig[it], ring, s_last, sg, &bar_next);
+    } else {  // diagonal operator (diag_apply_kernel's arithmetic)
+      const float sc = sig[it];
+      const float* vi = a.D + (long long)it * a.ldd;
+      for (long long r = (long long)blockIdx.x * kThr + tid; r < a.n; r += (long long)nb * kThr)
+        a.h[r] = (float)((double)__ldg(a.spec + r) * (double)(sc * __ldcg(vi + r)));
+    }
     grid_barrier(c.bar, nb, &bar_next);
     if (trace_it) stamp(c, 21);
     float* Dn = a.D + (long long)(it + 1) * a.ldd;
@@ -1034,44 +1048,46 @@ __global__ void __launch_bounds__(kThr) lanczos_small_kernel(const SmallNet net_
       if (gs_cta) {
         const long long r0 = (long long)blockIdx.x * a.rs, r1 = min((long long)a.n, r0 + a.rs);
         const int ng = (int)max(0LL, (r1 - r0 + 3) / 4);
-        double acc[kGsq][4];
+        double ss = 0.0;
+        for (int g0 = 0; g0 < ng; g0 += kThr * kGsq) {
+          double acc[kGsq][4];
 #pragma unroll
-        for (int q = 0; q < kGsq; ++q) {
-          const int g = tid + kThr * q;
-          const float4 h4 = g < ng ? __ldcg(reinterpret_cast<const float4*>(hsrc + r0) + g) : make_float4(0.f, 0.f, 0.f, 0.f);
-          acc[q][0] = h4.x; acc[q][1] = h4.y; acc[q][2] = h4.z; acc[q][3] = h4.w;
-        }
-        for (int j0 = 0; j0 < active; j0 += 8) {
-          float4 d[8][kGsq];
+          for (int q = 0; q < kGsq; ++q) {
+            const int g = g0 + tid + kThr * q;
+            const float4 h4 = g < ng ? __ldcg(reinterpret_cast<const float4*>(hsrc + r0) + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[q][0] = h4.x; acc[q][1] = h4.y; acc[q][2] = h4.z; acc[q][3] = h4.w;
+          }
+          for (int j0 = 0; j0 < active; j0 += 8) {
+            float4 d[8][kGsq];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 8; ++u)
 #pragma unroll
-            for (int q = 0; q < kGsq; ++q) {
-              const int g = tid + kThr * q;
-              d[u][q] = (j0 + u < active && g < ng)
-                            ? __ldcg(reinterpret_cast<const float4*>(a.D + (long long)(j0 + u) * a.ldd + r0) + g)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+              for (int q = 0; q < kGsq; ++q) {
+                const int g = g0 + tid + kThr * q;
+                d[u][q] = (j0 + u < active && g < ng)
+                              ? __ldcg(reinterpret_cast<const float4*>(a.D + (long long)(j0 + u) * a.ldd + r0) + g)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const double cj = j0 + u < active ? se[j0 + u] : 0.0;
+            for (int u = 0; u < 8; ++u) {
+              const double cj = j0 + u < active ? se[j0 + u] : 0.0;
 #pragma unroll
-            for (int q = 0; q < kGsq; ++q) {
-              acc[q][0] -= (double)d[u][q].x * cj;
-              acc[q][1] -= (double)d[u][q].y * cj;
-              acc[q][2] -= (double)d[u][q].z * cj;
-              acc[q][3] -= (double)d[u][q].w * cj;
+              for (int q = 0; q < kGsq; ++q) {
+                acc[q][0] -= (double)d[u][q].x * cj;
+                acc[q][1] -= (double)d[u][q].y * cj;
+                acc[q][2] -= (double)d[u][q].z * cj;
+                acc[q][3] -= (double)d[u][q].w * cj;
+              }
             }
           }
-        }
-        double ss = 0.0;
 #pragma unroll
-        for (int q = 0; q < kGsq; ++q) {
-          const int g = tid + kThr * q;
-          if (g < ng) {
-            const float4 o = make_float4((float)acc[q][0], (float)acc[q][1], (float)acc[q][2], (float)acc[q][3]);
-            __stcg(reinterpret_cast<float4*>(Dn + r0) + g, o);
-            ss += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+          for (int q = 0; q < kGsq; ++q) {
+            const int g = g0 + tid + kThr * q;
+            if (g < ng) {
+              const float4 o = make_float4((float)acc[q][0], (float)acc[q][1], (float)acc[q][2], (float)acc[q][3]);
+              __stcg(reinterpret_cast<float4*>(Dn + r0) + g, o);
+              ss += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+            }
           }
         }
         ss = warp_sum(ss);
@@ -1220,12 +1236,7 @@ static void setup_call(dho2g_mlp* m, int mode, size_t B, const float* w, const f
 // Cooperative launch of `kernel` on ctas CTAs (kThr threads, smem dynamic bytes); the barrier counter is reset
 // when the grid size changes (generations are counted in units of it).
 template <typename... Args>
-static void coop_launch(dho2g_mlp* m, void (*kernel)(Args...), int ctas, size_t smem, Args... args) {
-  dho2g_ctx* ctx = m->ctx;
-  if (m->sm_bar_nb != ctas) {
-    DHO2G_CUDA(cudaMemsetAsync(m->sm_bar.p, 0, m->sm_bar.n * sizeof(unsigned long long), ctx->stream));
-    m->sm_bar_nb = ctas;
-  }
+static void coop_launch(dho2g_ctx* ctx, void (*kernel)(Args...), int ctas, size_t smem, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)ctas);
   cfg.blockDim = dim3(kThr);
@@ -1275,7 +1286,11 @@ void mlp_small_run(dho2g_mlp* m, int mode, size_t B, const float* w, const float
     c.trace = tbuf.p;
   }
   const int slot = ctx->kt_begin();
-  coop_launch(m, mlp_small_kernel, ctas, kSmem, net, c);
+  if (m->sm_bar_nb != ctas) {  // barrier generations are counted in units of the grid size
+    DHO2G_CUDA(cudaMemsetAsync(m->sm_bar.p, 0, m->sm_bar.n * sizeof(unsigned long long), ctx->stream));
+    m->sm_bar_nb = ctas;
+  }
+  coop_launch(ctx, mlp_small_kernel, ctas, kSmem, net, c);
   ctx->kt_end(slot, names[mode], 0.0);
   if (tracing) {
     std::vector<unsigned long long> h((size_t)ctas * 32);
@@ -1312,21 +1327,28 @@ static size_t lz_small_smem(size_t m) {
 
 bool lanczos_small_eligible(const dho2g_lanczos* lz, const dho2g_op* op) {
   const dho2g_ctx* ctx = lz->ctx;
-  if (!ctx->lanczos_small || op->kind != 0 || ctx->world != 1 || op->b1 <= op->b0) return false;
-  if (lz->m > 512 || lz->rows != lz->n) return false;  // pass-1 partials fit the stage ring up to m = 512
-  if (cdiv(lz->n, (size_t)ctx->sm_count) > (size_t)kGsq * kThr * 4) return false;  // <= 2 float4 groups / thread
-  return mlp_small_eligible(op->mlp, op->b1 - op->b0);
+  if (!ctx->lanczos_small || ctx->world != 1 || lz->m > 512 || lz->rows != lz->n) return false;  // (m: smem)
+  // diagonal operator: supported (kind 1), but only on request (lanczos_small 2): at n >= 1e6 the
+  // launch-per-step Gram-Schmidt kernels stream HBM faster (measured: profiles/r02_c5_fused.txt)
+  if (op->kind == 1) return ctx->lanczos_small == 2 && lz->n <= (size_t)ctx->lanczos_small_max_n;
+  if (op->kind != 0 || op->b1 <= op->b0) return false;
+  return lz->n <= (size_t)ctx->lanczos_small_max_n && mlp_small_eligible(op->mlp, op->b1 - op->b0);
 }
 
 void lanczos_small_run(dho2g_lanczos* lz, dho2g_op* op) {
   dho2g_ctx* ctx = lz->ctx;
-  dho2g_mlp* m = op->mlp;
-  const size_t B = op->b1 - op->b0;
-  op->load_mlp_input();
-  if (m->prepared != m->w_cur || !m->prepared_small) mlp_prepare_point(m, B, op->ncls, op->scale);
-  SmallNet net;
-  SmallCall c;
-  setup_call(m, SM_HVP, B, m->w_cur, nullptr, nullptr, lz->h.p, op->ncls, op->scale, net, c);
+  SmallNet net{};
+  SmallCall c{};
+  dho2g_mlp* m = op->kind == 0 ? op->mlp : nullptr;
+  if (m) {
+    const size_t B = op->b1 - op->b0;
+    op->load_mlp_input();
+    if (m->prepared != m->w_cur || !m->prepared_small) mlp_prepare_point(m, B, op->ncls, op->scale);
+    setup_call(m, SM_HVP, B, m->w_cur, nullptr, nullptr, lz->h.p, op->ncls, op->scale, net, c);
+  } else {  // diagonal operator: the launch only needs the barrier words (kept on the Lanczos state)
+    if (!lz->sm_bar.p) lz->sm_bar.ensure_g((size_t)kBarShards * kBarStride);
+    c.bar = lz->sm_bar.p;
+  }
   const size_t smem = lz_small_smem(lz->m);
   static size_t attr = 0;
   const int ctas = coop_ctas(ctx, lanczos_small_kernel, smem, &attr);
@@ -1341,9 +1363,11 @@ void lanczos_small_run(dho2g_lanczos* lz, dho2g_op* op) {
   a.sg_on = lz->opts.reorth_safeguard ? 1 : 0;
   a.stride = (int)(2 * (lz->m + 2));
   a.goff = (int)(lz->m + 2);
-  a.ngs = (int)std::min<size_t>((size_t)ctas, std::max<size_t>(1, cdiv(lz->n, 256)));
+  a.ngs = (int)std::min<size_t>((size_t)ctas, std::max<size_t>(1, cdiv(lz->n, 256)));  // >= 64 groups per slice
   a.rs = (int)round_up(cdiv(lz->n, (size_t)a.ngs), 4);
   a.sv_off = (int)lz_small_scratch(lz->m);
+  a.kind = op->kind;
+  a.spec = op->kind == 1 ? op->mat.p + lz->begin : nullptr;
   a.ratio = std::max(lz->opts.safeguard_ratio, kSafeguardFloor32);
   a.rtol = std::max(lz->opts.breakdown_rtol, kBreakdownFloor32);
   lz->sm_part1.ensure_g((size_t)a.ngs * a.stride);
@@ -1359,7 +1383,12 @@ void lanczos_small_run(dho2g_lanczos* lz, dho2g_op* op) {
     c.trace_t = getenv("DHO2G_SMALL_TRACE")[0] - '0';
   }
   const int slot = ctx->kt_begin();
-  coop_launch(m, lanczos_small_kernel, ctas, smem, net, c, a);
+  int& bar_nb = m ? m->sm_bar_nb : lz->sm_bar_nb;
+  if (bar_nb != ctas) {  // barrier generations are counted in units of the grid size
+    DHO2G_CUDA(cudaMemsetAsync(c.bar, 0, (size_t)kBarShards * kBarStride * sizeof(unsigned long long), ctx->stream));
+    bar_nb = ctas;
+  }
+  coop_launch(ctx, lanczos_small_kernel, ctas, smem, net, c, a);
   if (tracing) {  // iteration 20: 20 start, 21 h complete, 22 pass-1 partials, 23 barrier, 24 sums, 25 pass 2, 26 barrier
     std::vector<unsigned long long> hb((size_t)ctas * 32);
     DHO2G_CUDA(cudaMemcpyAsync(hb.data(), tbuf.p, hb.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1381,8 +1410,11 @@ void lanczos_small_run(dho2g_lanczos* lz, dho2g_op* op) {
     }
     fprintf(stderr, "\n");
   }
-  // algorithmic bytes of the Gram-Schmidt sweeps (the §8d figure) for the record; HVP work is not counted
-  ctx->kt_end(slot, "lanczos_small", 0.0);
+  // algorithmic bytes of the Gram-Schmidt sweeps (the §8d figure, as gs_pass1 / gs_pass2 count them: pass 1
+  // reads the active columns and h, pass 2 the same plus the new column), m iterations; the HVPs are not counted
+  double gsb = 0.0;
+  for (size_t i = 0; i < lz->m; ++i) gsb += 4.0 * (double)lz->n * (2.0 * (double)(i + 2) + 1.0);
+  ctx->kt_end(slot, "lanczos_small", gsb);
 }
 
 }  // namespace dho2g

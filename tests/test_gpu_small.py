@@ -192,3 +192,32 @@ def test_small_path_trainer_graph_bitwise(ctx):
     assert (out[0].w_final == out[1].w_final).all()
     assert (out[0].loss == out[1].loss).all()
     assert ctx.stat("lanczos_graph_launches") - g0 >= 1
+
+
+@pytest.mark.parametrize("n,m", [(1_200_000, 24), (1000, 30)])
+def test_fused_refresh_diagonal_operator(ctx, n, m):
+    """The fused refresh on a diagonal operator (lanczos_small = 2; several row tiles per CTA slice at
+    n = 1.2 M) against the launch-per-step path, and the identity operator's breakdown after one step."""
+    spec = 1.0 + (np.arange(n, dtype=np.float64) % 97) * 0.37
+    op = d.diagonal_operator(ctx, spec)
+    out = []
+    try:
+        for fused in (2, 0):
+            ctx.set_option("lanczos_small", fused)
+            st = d.lanczos_distributed(ctx, m, op, n, 7)
+            out.append((st.iterations, st.breakdown, st.tridiag.diag.copy(), st.tridiag.offdiag.copy()))
+            st.close()
+        (i1, b1, d1, o1), (i0, b0, d0, o0) = out
+        assert i1 == i0 and b1 == b0
+        k = min(i0, 12)
+        assert np.max(np.abs(d1[:k] - d0[:k])) <= 1e-5 * spec.max()
+        assert np.max(np.abs(o1[:k] - o0[:k])) <= 1e-5 * spec.max()
+        ident = d.diagonal_operator(ctx, np.ones(n))
+        ctx.set_option("lanczos_small", 2)
+        st = d.lanczos_distributed(ctx, m, ident, n, 7)
+        assert st.breakdown and st.iterations == 1 and abs(st.tridiag.diag[0] - 1.0) < 1e-6
+        st.close()
+        ident.close()
+    finally:
+        ctx.set_option("lanczos_small", 1)
+    op.close()
