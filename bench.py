@@ -463,7 +463,10 @@ def run_ours(args, rank, world, dist):
             roof["useful_ceiling_frac"] = round(1.0 / 3.0, 4)
     line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32 (tensor-core GEMMs on scaled-fp16 hi/lo pairs, 3 MMAs per product; fp64 reductions)",
+            "vs_baseline": None,
+            "dtype": ("f32 (small-model path: fp32 FMA on the CUDA cores, one launch per pass / per refresh; fp64 "
+                      "reductions)" if hvp_flops(c["sizes"], c["curv"]) <= 2e9 else
+                      "f32 (tensor-core GEMMs on scaled-fp16 hi/lo pairs, 3 MMAs per product; fp64 reductions)"),
             "data": "synthetic blobs (SURVEY §8d), random-init weights", "config": config_json(args.config, world),
             "refresh_ms": refresh_ms, "refreshes_in_timed_region": n_ref, "rounds_per_epoch": rounds,
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,

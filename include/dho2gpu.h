@@ -68,6 +68,14 @@ int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world);
 int dho2g_local_fabric_create(int world, dho2g_fabric** out);
 int dho2g_local_fabric_destroy(dho2g_fabric* fab);
 int dho2g_comm_init_local(dho2g_ctx* ctx, dho2g_fabric* fab, int rank);
+/* Host-transport communicator: ranks in separate processes (possibly on the SAME GPU) whose collectives go
+ * through a caller-supplied host all-gather (e.g. a gloo process group): fn(user, send, recv, bytes) must
+ * gather `bytes` from every rank into recv (world x bytes, rank order) and return 0. Every collective is a
+ * device->host copy, the callback and a host->device copy (reduce-scatter sums in ascending rank order on
+ * the device). For tests of the multi-process data path without NCCL — notably the CUDA-IPC peer pointers
+ * of the fused HVP -> reduce-scatter (option hvp_route), which need separate processes. */
+typedef int (*dho2g_host_allgather)(void* user, const void* send, void* recv, size_t bytes);
+int dho2g_comm_init_host(dho2g_ctx* ctx, int rank, int world, dho2g_host_allgather fn, void* user);
 /* Accounting. Communication ledger (CommLedger, collectives.hpp:55-83): one row per
  * collective round this rank took part in — event index, op ("all_gather", "reduce_scatter",
  * "all_reduce"), logical floats, rank, modeled floats sent / received. Empty on a single GPU.

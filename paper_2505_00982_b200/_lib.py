@@ -46,6 +46,7 @@ class TrainCfg(C.Structure):
 
 
 HOST_HVP = C.CFUNCTYPE(None, vp, dp, dp, C.c_size_t)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, vp, vp, vp, C.c_size_t)  # dho2g_host_allgather
 
 _SIGS = {
     "dho2g_last_error": ([], C.c_char_p),
@@ -63,6 +64,7 @@ _SIGS = {
     "dho2g_local_fabric_create": ([C.c_int, C.POINTER(vp)], C.c_int),
     "dho2g_local_fabric_destroy": ([vp], C.c_int),
     "dho2g_comm_init_local": ([vp, vp, C.c_int], C.c_int),
+    "dho2g_comm_init_host": ([vp, C.c_int, C.c_int, HOST_ALLGATHER, vp], C.c_int),
     "dho2g_ctx_ledger_rows": ([vp], C.c_size_t),
     "dho2g_ctx_ledger_row": ([vp, C.c_size_t, i64p, C.c_char_p, C.c_size_t, i64p, ip, i64p, i64p], C.c_int),
     "dho2g_ctx_memory_count": ([vp], C.c_size_t),

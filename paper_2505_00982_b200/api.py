@@ -216,6 +216,22 @@ class Context:
         """Join an in-process fabric as `rank` (several ranks on one GPU, one host thread each)."""
         check(lib.dho2g_comm_init_local(self.h, fabric.h, rank))
 
+    def comm_init_host(self, rank: int, world: int, allgather):
+        """Host-transport communicator (dho2g_comm_init_host): ranks in separate processes, possibly on the same
+        GPU, whose collectives go through `allgather(send: bytes) -> bytes` (every rank's `send`, concatenated in
+        rank order), e.g. over a gloo process group."""
+        def _cb(user, send, recv, nbytes):
+            try:
+                out = allgather(C.string_at(send, nbytes))
+                if len(out) != nbytes * world:
+                    return 1
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception:  # noqa: BLE001 — reported to the library as a failed collective
+                return 1
+        self._host_ag = L.HOST_ALLGATHER(_cb)  # kept alive with the context
+        check(lib.dho2g_comm_init_host(self.h, rank, world, self._host_ag, None))
+
     def ledger(self):
         """This rank's communication ledger rows (CommLedger::Row, collectives.hpp:58-65):
         (event, op, floats, rank, sent, received). Empty on a single GPU."""

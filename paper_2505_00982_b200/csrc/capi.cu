@@ -360,6 +360,21 @@ int dho2g_comm_init_local(dho2g_ctx* ctx, dho2g_fabric* fab, int rank) {
   });
 }
 
+int dho2g_comm_init_host(dho2g_ctx* ctx, int rank, int world, dho2g_host_allgather fn, void* user) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!fn) fail(DHO2G_ARGUMENT, "host communicator: null all-gather");
+    if (world < 1 || rank < 0 || rank >= world) fail(DHO2G_ARGUMENT, "Shard: rank out of range");
+    if (ctx->comm || ctx->fabric) fail(DHO2G_ARGUMENT, "host communicator: context already has a communicator");
+    ctx->rank = rank;
+    ctx->world = world;
+    if (world > 1) {
+      ctx->host_ag = fn;
+      ctx->host_ag_user = user;
+    }
+  });
+}
+
 int dho2g_comm_rank(dho2g_ctx* ctx, int* rank, int* world) {
   return guard([&] {
     if (!ctx) fail(DHO2G_ARGUMENT, "null context");

@@ -298,6 +298,35 @@ static void fabric_collective(dho2g_ctx* ctx, const void* send, void* recv, size
   f->barrier();  // every rank has issued its waits before any "done" / "ready" is recorded again
 }
 
+// Host-transport communicator: send -> pinned host, the caller's all-gather, pinned host -> recv (all-gather) or
+// the ascending-rank sum of this rank's slices (reduce-scatter, fabric_sum_kernel).
+static void host_collective(dho2g_ctx* ctx, const void* send, void* recv, size_t count, size_t elem, int kind) {
+  const int W = ctx->world, r = ctx->rank;
+  const size_t bytes = count * elem * (kind == 0 ? 1 : (size_t)W);  // reduce-scatter: the full-length partial
+  ctx->host_ag_buf.ensure(bytes * (size_t)(W + 1));
+  char* hs = ctx->host_ag_buf.p;
+  char* hr = hs + bytes;
+  DHO2G_CUDA(cudaMemcpyAsync(hs, send, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  dho2g::wait_stream(ctx, ctx->stream);
+  if (ctx->host_ag(ctx->host_ag_user, hs, hr, bytes) != 0) {
+    ctx->failed = true;
+    ctx->failed_msg = "host communicator: all-gather callback failed";
+    dho2g::fail(DHO2G_NCCL, ctx->failed_msg);
+  }
+  if (kind == 0) {
+    DHO2G_CUDA(cudaMemcpyAsync(recv, hr, bytes * W, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    ctx->fabric_scratch.ensure((size_t)W * count);
+    for (int q = 0; q < W; ++q)
+      DHO2G_CUDA(cudaMemcpyAsync(ctx->fabric_scratch.p + (size_t)q * count, hr + (size_t)q * bytes + (size_t)r * count * 4,
+                                 count * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    fabric_sum_kernel<<<(unsigned)std::min<size_t>(dho2g::cdiv(count, 256), 1184), 256, 0, ctx->stream>>>(
+        ctx->fabric_scratch.p, static_cast<float*>(recv), count, W);
+    DHO2G_LAUNCH();
+  }
+  dho2g::wait_stream(ctx, ctx->stream);  // the staging buffer is reused by the next collective
+}
+
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
   check_usable();
   if (world == 1 && !nccl_force) {
@@ -305,6 +334,7 @@ void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, co
     return;
   }
   if (fabric) fabric_collective(this, send, recv, count, sizeof(double), 0);
+  else if (host_ag) host_collective(this, send, recv, count, sizeof(double), 0);
   else dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclDouble, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 8 * world);
@@ -320,6 +350,7 @@ void dho2g_ctx::allgather_f32(const float* send, float* recv, size_t count, cons
     return;
   }
   if (fabric) fabric_collective(this, send, recv, count, sizeof(float), 0);
+  else if (host_ag) host_collective(this, send, recv, count, sizeof(float), 0);
   else dho2g::nccl_call(this, dho2g::nccl().AllGather(send, recv, count, ncclFloat, comm, stream), "all_gather");
   bump("nccl_calls", 1);
   bump("nccl_bytes", double(count) * 4 * world);
@@ -334,6 +365,7 @@ void dho2g_ctx::reduce_scatter_f32(const float* send, float* recv, size_t count)
     return;
   }
   if (fabric) fabric_collective(this, send, recv, count, sizeof(float), 1);
+  else if (host_ag) host_collective(this, send, recv, count, sizeof(float), 1);
   else dho2g::nccl_call(this, dho2g::nccl().ReduceScatter(send, recv, count, ncclFloat, ncclSum, comm, stream),
                         "reduce_scatter");
   bump("nccl_calls", 1);

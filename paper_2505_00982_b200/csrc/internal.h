@@ -88,6 +88,10 @@ struct dho2g_ctx {
                           // column-dot phase, 1 128x2x4, 2 128x3x3, 3 128x4x2, 4 512x2x1
   ncclComm_t comm = nullptr;
   dho2g_fabric* fabric = nullptr;  // in-process test backend (dho2g_comm_init_local) instead of NCCL
+  dho2g_host_allgather host_ag = nullptr;  // host-transport backend (dho2g_comm_init_host) instead of NCCL
+  void* host_ag_user = nullptr;
+  dho2g::HostBuf<char> host_ag_buf;        // its pinned staging (send, then world x recv)
+  bool host_rendezvous() const { return fabric != nullptr || host_ag != nullptr; }  // collectives on the host
   dho2g::DevBuf<float> fabric_scratch;
   int rank = 0, world = 1;
   long long tql2_log_cap = 0;  // split eigensolve's rotation-log entries (0: 2 m^2 + 4096); tests shrink it

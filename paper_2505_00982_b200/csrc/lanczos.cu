@@ -1221,8 +1221,8 @@ static bool lanczos_graph(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, bool lau
   dho2g_ctx* ctx = lz->ctx;
   cudaStream_t st = ctx->stream;
   // multi-rank: NCCL collectives are captured with the kernels (dho2g_test_collectives_graph); the in-process
-  // fabric's host rendezvous cannot be
-  if (!ctx->use_graphs || (ctx->world != 1 && (ctx->fabric || !ctx->graphs_multirank)) || ctx->ktimers ||
+  // fabric's / host communicator's host rendezvous cannot be
+  if (!ctx->use_graphs || (ctx->world != 1 && (ctx->host_rendezvous() || !ctx->graphs_multirank)) || ctx->ktimers ||
       op->kind == 3 || lz->graph_failed)
     return false;
   lz->seed_dev.ensure(1);
