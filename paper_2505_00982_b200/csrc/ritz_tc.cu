@@ -11,12 +11,12 @@
 // registers -> coalesced stores. The CUDA-core form is FMA/LDS-bound (2 rows.m.r FMAs); this one is
 // HBM-bound.
 //
-// Persistent: one CTA per SM walks 128-row tiles. The basis streams through a ring of NCS 16 KB K-chunk
-// stages (128 rows x 32 columns; NCS = what shared memory leaves, 4-6 at C4) so several chunks are in
-// flight while chunk kc is split; the hi/lo operand buffer is single but handed over per 32-wide K-chunk
-// (the MMAs of chunk kc start as soon as it is split; the next tile's split of chunk kc waits only for
-// those MMAs). Warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM owner, warps 4-11 split (two threads
-// per row), warps 12-15 epilogue (TMEM lane quadrant = warp % 4).
+// Persistent: one CTA per SM walks 128-row tiles as one stream of 32-wide K-chunks. The basis streams through
+// a ring of NCS 16 KB K-chunk stages (128 rows x 32 columns, NCS = what shared memory leaves) and the split
+// hi/lo operands through a ring of NSL chunk slots (2 x 16 KB each, 4 at C4), so the split runs up to NSL
+// chunks ahead of the MMAs instead of alternating with them (round 2: 0.55 -> see DESIGN §9 of HBM at C4).
+// Warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM owner, warps 4-11 split (two threads per row), warps
+// 12-15 epilogue (TMEM lane quadrant = warp % 4).
 #include <cudaTypedefs.h>
 
 #include "internal.h"
@@ -27,24 +27,28 @@ namespace rtc {
 using namespace tc;
 
 constexpr int TM = 128;  // rows per tile (UMMA M)
-constexpr int kMaxChunks = 8;  // K-chunks of 32 (KP <= 256)
 
 constexpr uint32_t CB = TM * 32 * 4;  // one staged K-chunk: 128 rows x 32 basis columns fp32 (16 KB)
 constexpr int kMaxStages = 8;
+constexpr int kMaxSlots = 4;
 
 struct Geo {
   int KP, NP;  // padded K (= me, multiple of 32) and N (= r, 32 or 64)
   int NCS;     // K-chunk staging ring depth (what is left of shared memory, <= kMaxStages)
-  __host__ __device__ uint32_t dbytes() const { return (uint32_t)TM * KP * 4; }  // one 128 x KP fp32 tile
+  int NSL;     // hi/lo chunk slots (4, or 2 when U is large)
   __host__ __device__ uint32_t ubytes() const { return (uint32_t)NP * KP * 4; }  // one U (hi or lo)
-  // chunk stages, hi, lo, Uh, Ul, barriers
-  __host__ __device__ uint32_t smem() const { return NCS * CB + 2 * dbytes() + 2 * ubytes() + 1024 + 1024; }
+  // chunk stages, hi slots, lo slots, Uh, Ul, barriers
+  __host__ __device__ uint32_t smem() const { return NCS * CB + 2 * NSL * CB + 2 * ubytes() + 1024 + 1024; }
 };
 
 inline Geo make_geo(int me, int r) {
-  Geo g{(int)round_up((size_t)me, 32), r <= 32 ? 32 : 64, 0};
-  const long long left = 227LL * 1024 - 2LL * g.dbytes() - 2LL * g.ubytes() - 2048;
-  g.NCS = (int)std::max(0LL, std::min<long long>(kMaxStages, left / (long long)CB));
+  Geo g{(int)round_up((size_t)me, 32), r <= 32 ? 32 : 64, 0, kMaxSlots};
+  for (;;) {
+    const long long left = 227LL * 1024 - 2LL * g.NSL * CB - 2LL * g.ubytes() - 2048;
+    g.NCS = (int)std::max(0LL, std::min<long long>(kMaxStages, left / (long long)CB));
+    if (g.NCS >= 2 || g.NSL <= 2) break;
+    g.NSL = 2;
+  }
   return g;
 }
 
@@ -66,12 +70,12 @@ __global__ void __launch_bounds__(512, 1)
                    size_t ldv, int ntiles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t DB = g.dbytes(), UB = g.ubytes();
-  const int NCS = g.NCS;
+  const uint32_t UB = g.ubytes();
+  const int NCS = g.NCS, NSL = g.NSL;
   uint8_t* stg0 = smem;               // [NCS] K-chunk stages, [32 k][128 rows] fp32 (TMA, no swizzle)
-  uint8_t* Ah = smem + NCS * CB;      // hi, K-major SW128: K-chunk kc (32 elems) at kc * 16 KB
-  uint8_t* Al = Ah + DB;
-  uint8_t* Uh = Al + DB;         // K-major SW128: K-chunk kc at kc * NP * 128
+  uint8_t* Ah = smem + NCS * CB;      // [NSL] hi chunk slots, K-major SW128 (128 rows x 32 elems, 16 KB each)
+  uint8_t* Al = Ah + NSL * CB;        // [NSL] lo chunk slots
+  uint8_t* Uh = Al + NSL * CB;   // K-major SW128: K-chunk kc at kc * NP * 128
   uint8_t* Ul = Uh + UB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(Ul + UB);
   uint64_t* full = bars;                     // [NCS] chunk stage landed
@@ -79,9 +83,9 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* tfull = sfree + kMaxStages;      // [2] accumulator ready
   uint64_t* tempty = tfull + 2;              // [2] accumulator drained
   uint64_t* ufull = tempty + 2;              // U landed
-  uint64_t* hready = ufull + 1;              // [kMaxChunks] K-chunk of hi/lo written
-  uint64_t* hfree = hready + kMaxChunks;     // [kMaxChunks] MMAs done reading that K-chunk
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + kMaxChunks);
+  uint64_t* hready = ufull + 1;              // [NSL] hi/lo chunk slot written
+  uint64_t* hfree = hready + kMaxSlots;      // [NSL] MMAs done reading that slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfree + kMaxSlots);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem_cols = 2 * (uint32_t)g.NP;  // 64 or 128
   const int nkc = g.KP / 32;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(512, 1)
       mbar_init(&tempty[s], 4);
     }
     mbar_init(ufull, 1);
-    for (int c = 0; c < kMaxChunks; ++c) {
+    for (int c = 0; c < kMaxSlots; ++c) {
       mbar_init(&hready[c], 8);
       mbar_init(&hfree[c], 1);
     }
@@ -111,6 +115,10 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  // each CTA walks one contiguous range of row tiles (consecutive loads of a basis column are adjacent in
+  // memory: longer DRAM bursts than a grid-strided walk)
+  const int tpc = (ntiles + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int t0 = (int)blockIdx.x * tpc, t1 = min(ntiles, t0 + tpc);
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer: U (hi, lo) once, then the tiles' 128 x 32 K-chunks through an NCS-deep ring
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(512, 1)
       tma_load_2d<false>(Ul + kc * g.NP * 128, &mUl, kc * 32, 0, ufull);
     }
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+    for (int t = t0; t < t1; ++t)
       for (int kc = 0; kc < nkc; ++kc, ++it) {
         const uint32_t s = it % NCS;
         mbar_wait(&sfree[s], ((it / NCS) & 1) ^ 1);
@@ -134,16 +142,17 @@ __global__ void __launch_bounds__(512, 1)
     mbar_wait(ufull, 0);
     fence_after();
     const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), uh = smem_u32(Uh), ul = smem_u32(Ul);
-    uint32_t i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    uint32_t i = 0, it = 0;
+    for (int t = t0; t < t1; ++t, ++i) {
       const uint32_t ab = i & 1;
       mbar_wait(&tempty[ab], ((i >> 1) & 1) ^ 1);
       const uint32_t acc = tmem + ab * (uint32_t)g.NP;
-      for (int kc = 0; kc < nkc; ++kc) {
-        mbar_wait(&hready[kc], i & 1);
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const uint32_t h = it % NSL;
+        mbar_wait(&hready[h], (it / NSL) & 1);
         fence_after();
         for (int s4 = 0; s4 < 4; ++s4) {
-          const uint32_t ao = (uint32_t)kc * 16384u + (uint32_t)s4 * 32u;
+          const uint32_t ao = h * CB + (uint32_t)s4 * 32u;
           const uint32_t uo = (uint32_t)kc * (uint32_t)g.NP * 128u + (uint32_t)s4 * 32u;
           const uint64_t aH = sw128_desc(ah + ao, 16, 1024), aL = sw128_desc(al + ao, 16, 1024);
           const uint64_t bH = sw128_desc(uh + uo, 16, 1024), bL = sw128_desc(ul + uo, 16, 1024);
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(512, 1)
                        "r"(ID));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&hfree[kc]))
+                         smem_u32(&hfree[h]))
                      : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -171,20 +180,20 @@ __global__ void __launch_bounds__(512, 1)
     const int m = q & 127;
     const int c0 = (q >> 7) * 4;      // slots c0 .. c0+3 of each 128-byte row
     const uint32_t rowoff = (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u;
-    uint32_t i = 0, it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    uint32_t it = 0;
+    for (int t = t0; t < t1; ++t) {
       for (int kc = 0; kc < nkc; ++kc, ++it) {
-        const uint32_t s = it % NCS;
+        const uint32_t s = it % NCS, h = it % NSL;
         mbar_wait(&full[s], (it / NCS) & 1);
         const float* stg = reinterpret_cast<const float*>(stg0 + s * CB);
-        mbar_wait(&hfree[kc], (i & 1) ^ 1);  // the previous tile's MMAs are done with this K-chunk
+        mbar_wait(&hfree[h], ((it / NSL) & 1) ^ 1);  // the MMAs of this slot's previous chunk are done
 #pragma unroll
         for (int c = c0; c < c0 + 4; ++c) {
           const int k0 = c * 4;  // within the staged chunk
           const float x0 = stg[(k0 + 0) * TM + m], x1 = stg[(k0 + 1) * TM + m];
           const float x2 = stg[(k0 + 2) * TM + m], x3 = stg[(k0 + 3) * TM + m];
           const float4 hi = make_float4(rn_tf32(x0), rn_tf32(x1), rn_tf32(x2), rn_tf32(x3));
-          const uint32_t off = (uint32_t)kc * 16384u + rowoff + (uint32_t)((c ^ (m & 7)) * 16);
+          const uint32_t off = h * CB + rowoff + (uint32_t)((c ^ (m & 7)) * 16);
           *reinterpret_cast<float4*>(Ah + off) = hi;
           *reinterpret_cast<float4*>(Al + off) =
               make_float4(rn_tf32(x0 - hi.x), rn_tf32(x1 - hi.y), rn_tf32(x2 - hi.z), rn_tf32(x3 - hi.w));
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(512, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&hready[kc]);
+          mbar_arrive(&hready[h]);
           mbar_arrive(&sfree[s]);  // the stage is free for the next chunk load
         }
       }
@@ -202,7 +211,7 @@ __global__ void __launch_bounds__(512, 1)
     // ---------------- epilogue: TMEM lane quadrant = warp % 4
     const int sw = warp & 3;
     uint32_t i = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    for (int t = t0; t < t1; ++t, ++i) {
       const uint32_t ab = i & 1;
       mbar_wait(&tfull[ab], (i >> 1) & 1);
       fence_after();
