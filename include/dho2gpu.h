@@ -220,6 +220,10 @@ typedef struct {
   size_t lanczos_m; /* 0 = lanczos_budget(k, l, n) (trainer.cpp:117); else explicit m (C4) */
   /* modeled clock of MetricsRow::wallclock_ms (trainer.cpp:137-148); 0 = the reference defaults 50 / 10 */
   double model_bandwidth_gbps, model_gflops;
+  /* TrainerConfig::debug_hash_checks (trainer.cpp:120, :128, :157): sets the context's hash_checks option —
+   * B compared across ranks after each refresh and at extraction, the parameter replicas at every epoch end
+   * (DivergenceError on a mismatch) */
+  int debug_hash_checks;
 } dho2g_train_cfg;
 /* Dataset (oracle.hpp:25-54) is uploaded once (device resident) unless host_resident != 0, in
  * which case every step gathers its batch from pinned host memory (end-to-end mode). */

@@ -42,7 +42,7 @@ class TrainCfg(C.Structure):
                 ("breakdown_rtol", C.c_double), ("sigma", C.c_double), ("outer_rounds", C.c_size_t),
                 ("inner_epochs", C.c_size_t), ("sigma_zero_reduction", C.c_int), ("epochs", C.c_size_t),
                 ("batch_size", C.c_size_t), ("seed", C.c_uint64), ("lanczos_m", C.c_size_t),
-                ("model_bandwidth_gbps", C.c_double), ("model_gflops", C.c_double)]
+                ("model_bandwidth_gbps", C.c_double), ("model_gflops", C.c_double), ("debug_hash_checks", C.c_int)]
 
 
 HOST_HVP = C.CFUNCTYPE(None, vp, dp, dp, C.c_size_t)

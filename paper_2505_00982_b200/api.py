@@ -650,7 +650,11 @@ def lanczos_distributed(ctx: Context, m: int, op: Operator, n: int, seed: int,
     o = (opts or DistLanczosOptions()).lanczos
     lo = L.LanczosOpts(int(o.reorth_safeguard), o.safeguard_ratio, o.breakdown_rtol)
     h = C.c_void_p()
-    check(lib.dho2g_lanczos_run(ctx.h, op.h, m, seed, C.byref(lo), C.byref(h)))
+    ctx.set_option("hash_checks", int(bool((opts or DistLanczosOptions()).hash_checks)))
+    try:
+        check(lib.dho2g_lanczos_run(ctx.h, op.h, m, seed, C.byref(lo), C.byref(h)))
+    finally:
+        ctx.set_option("hash_checks", 0)
     return ShardedLanczosResult(ctx, h, m)
 
 
@@ -726,10 +730,16 @@ class EseResult:
             pass
 
 
-def extract_ese_distributed(ctx: Context, state: ShardedLanczosResult, k: int, l: int) -> EseResult:
-    """dist_lanczos.hpp:39-41: device tql2 + selection + Ritz vectors (V_hat stays sharded)."""
+def extract_ese_distributed(ctx: Context, state: ShardedLanczosResult, k: int, l: int,
+                            hash_check: bool = False) -> EseResult:
+    """dist_lanczos.hpp:39-41: device tql2 + selection + Ritz vectors (V_hat stays sharded); hash_check: B
+    compared across ranks first (DivergenceError "B differs across ranks")."""
     h = C.c_void_p()
-    check(lib.dho2g_extract_ese(ctx.h, state.h, k, l, C.byref(h)))
+    ctx.set_option("hash_checks", int(bool(hash_check)))
+    try:
+        check(lib.dho2g_extract_ese(ctx.h, state.h, k, l, C.byref(h)))
+    finally:
+        ctx.set_option("hash_checks", 0)
     return EseResult(ctx, h, k, l)
 
 
@@ -879,7 +889,7 @@ class TrainerConfig:
     batch_size: int = 16
     seed: int = 1
     lanczos_m: int = 0
-    debug_hash_checks: bool = False  # accepted for config parity; replicas are identical by construction
+    debug_hash_checks: bool = False  # cross-rank B / parameter-replica hashes (trainer.cpp:120-157; context option)
     model_bandwidth_gbps: float = 50.0
     model_gflops: float = 10.0
 
@@ -890,7 +900,7 @@ class TrainerConfig:
                           self.refresh_interval, self.curvature_batch, int(self.lanczos.reorth_safeguard),
                           self.lanczos.safeguard_ratio, self.lanczos.breakdown_rtol, self.sigma, self.outer_rounds,
                           self.inner_epochs, int(self.sigma_zero_reduction), self.epochs, self.batch_size, self.seed,
-                          self.lanczos_m, self.model_bandwidth_gbps, self.model_gflops)
+                          self.lanczos_m, self.model_bandwidth_gbps, self.model_gflops, int(self.debug_hash_checks))
 
 
 @dataclass

@@ -10,6 +10,8 @@
 #include <numeric>
 #include <thread>
 
+#include <cstring>
+
 #include "internal.h"
 
 namespace dho2g {
@@ -326,6 +328,73 @@ static void host_collective(dho2g_ctx* ctx, const void* send, void* recv, size_t
   }
   dho2g::wait_stream(ctx, ctx->stream);  // the staging buffer is reused by the next collective
 }
+
+namespace dho2g {
+uint64_t tridiag_hash_host(const double* diag, const double* off, size_t upto) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  auto mix = [&h](double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, sizeof(b));
+    h ^= b;
+    h *= 0x100000001b3ULL;
+  };
+  for (size_t i = 0; i < upto; ++i) mix(diag[i]);
+  for (size_t i = 0; i < upto; ++i) mix(off[i]);
+  return h;
+}
+
+// FNV-1a over the fp32 bits: one thread per 4096-element chunk, then the chunk hashes in order (one thread)
+__global__ void hash_chunks_kernel(const float* __restrict__ v, size_t n, unsigned long long* __restrict__ ch,
+                                   size_t nch) {
+  const size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (c >= nch) return;
+  unsigned long long h = 0xcbf29ce484222325ULL;
+  const size_t e = min(n, (c + 1) * 4096);
+  for (size_t i = c * 4096; i < e; ++i) {
+    h ^= (unsigned long long)__float_as_uint(v[i]);
+    h *= 0x100000001b3ULL;
+  }
+  ch[c] = h;
+}
+__global__ void hash_final_kernel(const unsigned long long* __restrict__ ch, size_t nch, double* out2) {
+  unsigned long long h = 0xcbf29ce484222325ULL;
+  for (size_t c = 0; c < nch; ++c) {
+    h ^= ch[c];
+    h *= 0x100000001b3ULL;
+  }
+  out2[0] = (double)(unsigned)(h >> 32);
+  out2[1] = (double)(unsigned)h;
+}
+
+uint64_t device_hash_f32(dho2g_ctx* ctx, const float* v, size_t n) {
+  const size_t nch = std::max<size_t>(1, cdiv(n, 4096));
+  DevBuf<unsigned long long> ch(nch);
+  DevBuf<double> o(2);
+  hash_chunks_kernel<<<(unsigned)cdiv(nch, 256), 256, 0, ctx->stream>>>(v, n, ch.p, nch);
+  hash_final_kernel<<<1, 1, 0, ctx->stream>>>(ch.p, nch, o.p);
+  DHO2G_LAUNCH();
+  double h[2];
+  DHO2G_CUDA(cudaMemcpyAsync(h, o.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  wait_stream(ctx, ctx->stream);
+  return ((uint64_t)(unsigned)h[0] << 32) | (uint64_t)(unsigned)h[1];
+}
+
+// Worker::all_equal (collectives.cpp): every rank's value equal to every other's
+bool ranks_all_equal(dho2g_ctx* ctx, uint64_t h) {
+  if (ctx->world == 1) return true;
+  if (ctx->hash_checks == 2) h ^= (uint64_t)ctx->rank;  // test hook: a simulated divergence on ranks > 0
+  DevBuf<double> ex(2 + 2 * (size_t)ctx->world);
+  const double mine[2] = {(double)(uint32_t)(h >> 32), (double)(uint32_t)h};
+  DHO2G_CUDA(cudaMemcpyAsync(ex.p, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+  ctx->allgather_f64(ex.p, ex.p + 2, 2, "hash_check");
+  std::vector<double> all(2 * (size_t)ctx->world);
+  DHO2G_CUDA(cudaMemcpyAsync(all.data(), ex.p + 2, all.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  wait_stream(ctx, ctx->stream);
+  for (int r = 1; r < ctx->world; ++r)
+    if (all[2 * r] != all[0] || all[2 * r + 1] != all[1]) return false;
+  return true;
+}
+}  // namespace dho2g
 
 void dho2g_ctx::allgather_f64(const double* send, double* recv, size_t count, const char* op) {
   check_usable();

@@ -96,6 +96,9 @@ struct dho2g_ctx {
   int rank = 0, world = 1;
   long long tql2_log_cap = 0;  // split eigensolve's rotation-log entries (0: 2 m^2 + 4096); tests shrink it
   int graphs_multirank = 1;  // refresh CUDA graph also at world > 1 (NCCL communicator; not the fabric)
+  int hash_checks = 0;  // debug cross-rank checks (DistLanczosOptions::hash_checks / debug_hash_checks):
+                        // B after a refresh and at extraction, the parameter replicas at every epoch end
+                        // (2: test hook, ranks > 0 perturb their hash — a simulated divergence)
   bool nccl_force = false;  // test hook: route world-1 collectives through a 1-rank NCCL communicator
   // Set when a collective failed (DEADLOCK / NCCL): the communicator is aborted and every later call on
   // this context raises (its shards, offsets and buffers belong to the failed group, so it must not go on
@@ -273,6 +276,11 @@ void mlp_eval_dev(dho2g_mlp* m, const float* w, const float* X, const float* y, 
                   size_t ncls, double* acc2);
 
 void mlp_loss_sum(dho2g_mlp* m, size_t B, double* acc2);
+// Debug hash checks (dist_lanczos.cpp:11-29): the reference's FNV-1a of the fp64 bits of B's entries, and a
+// chunked FNV of a device vector's fp32 bits; all_equal across ranks (an all-gather of the two 32-bit halves).
+uint64_t tridiag_hash_host(const double* diag, const double* off, size_t upto);
+uint64_t device_hash_f32(dho2g_ctx* ctx, const float* v, size_t n);
+bool ranks_all_equal(dho2g_ctx* ctx, uint64_t h);
 // Small-model path (mlp_small.cu): eligibility (ctx option mlp_small, HVP flops at batch B), one persistent
 // launch per pass (mode 0 gradient, 1 point preparation, 2 HVP, 3 evaluation), scratch presizing.
 bool mlp_small_eligible(const dho2g_mlp* m, size_t B);

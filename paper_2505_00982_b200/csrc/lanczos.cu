@@ -1325,6 +1325,11 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed) {
   cudaEventDestroy(e1);
   if (lz->host.nonfinite) fail(DHO2G_NUMERIC, "lanczos_distributed: hvp returned non-finite values");
   if (lz->host.stopped == 0) lz->host.iters = (int)m;
+  if (ctx->hash_checks) {  // dist_lanczos.cpp:104 / :113, checked once for the whole B (no round trip per step)
+    const size_t it = (size_t)lz->host.iters;
+    if (!ranks_all_equal(ctx, tridiag_hash_host(lz->host.diag, lz->host.off, it)))
+      fail(DHO2G_DIVERGENCE, "lanczos_distributed: B diverged across ranks (seed mismatch?)");
+  }
   ctx->bump("lanczos_runs", 1);
   ctx->bump("lanczos_ms", ms);
   if (eager && !lz->gexec) {
@@ -1351,6 +1356,8 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   }
   if (me < 1) fail(DHO2G_ARGUMENT, "extract_ese_distributed: empty Lanczos state");
   if (k + l > (size_t)me) fail(DHO2G_ARGUMENT, "extract_ese_distributed: k+l exceeds the filled block");
+  if (ctx->hash_checks && !ranks_all_equal(ctx, tridiag_hash_host(lz->host.diag, lz->host.off, (size_t)me)))
+    fail(DHO2G_DIVERGENCE, "extract_ese_distributed: B differs across ranks");  // dist_lanczos.cpp:134
   const int r = (int)(k + l);
   ese->r = r;
   // scratch persists in the Lanczos state (no allocation, hence no implicit device sync, per refresh)

@@ -392,6 +392,8 @@ struct dho2g_trainer {
     if (!std::isfinite(row.loss))
       fail(DHO2G_DIVERGED, "non-finite loss at epoch " + std::to_string(epoch) + " (trainer " +
                                (cfg.trainer == 2 ? "dho2" : cfg.trainer == 1 ? "fosi" : "sgd") + ")");
+    if (ctx->hash_checks && !ranks_all_equal(ctx, device_hash_f32(ctx, w_a_full.p, n)))  // trainer.cpp:157
+      fail(DHO2G_DIVERGENCE, "train: parameter replicas diverged at epoch " + std::to_string(epoch));
     row.acc = ncls > 0 ? h[1] / (double)N : NAN;
     row.resid = with_resid ? std::sqrt(h[2]) : NAN;
     row.refresh = refreshed ? 1 : 0;
@@ -521,6 +523,7 @@ dho2g_trainer* trainer_create(dho2g_ctx* ctx, const dho2g_train_cfg* cfg, dho2g_
   auto t = std::make_unique<dho2g_trainer>();
   t->ctx = ctx;
   t->cfg = *cfg;
+  ctx->hash_checks = cfg->debug_hash_checks ? 1 : 0;  // trainer.cpp:120 / :128 / :157 (context-wide)
   t->mlp = mlp;
   t->quad = quad;
   t->N = N;

@@ -263,3 +263,71 @@ def test_trainer_fused_reduce_scatter(world):
         assert "reduce_scatter" not in ops and "barrier" in ops
         assert np.linalg.norm(w - w1) / np.linalg.norm(w1) <= 1e-5
         assert np.abs(loss - l1).max() <= 1e-4 * np.abs(l1).max()
+
+
+def test_debug_hash_checks_two_ranks():
+    """DistLanczosOptions.hash_checks / extract hash_check / TrainerConfig.debug_hash_checks
+    (dist_lanczos.cpp:104-134, trainer.cpp:157): the replicated B and parameters hash equal on every rank, so
+    the checks pass; with the test hook (option hash_checks = 2: ranks > 0 perturb their hash) each check
+    raises the reference's DivergenceError."""
+    import ctypes as C
+    from paper_2505_00982_b200 import _lib as L
+    from paper_2505_00982_b200.api import check
+    n, m = 20_011, 12
+    spec = 1.0 + (np.arange(n) % 97) * 0.1
+
+    def fn(c, rank):
+        op = d.diagonal_operator(c, spec)
+        st = d.lanczos_distributed(c, m, op, n, 5, d.DistLanczosOptions(hash_checks=True))
+        ese = d.extract_ese_distributed(c, st, 3, 0, hash_check=True)
+        msgs = []
+        c.set_option("hash_checks", 2)  # (the Python wrappers reset the option: call the C ABI directly)
+        try:
+            lo = L.LanczosOpts(1, 1e-6, 1e-10)
+            for call in (lambda h: L.lib.dho2g_lanczos_run(c.h, op.h, m, 5, C.byref(lo), C.byref(h)),
+                         lambda h: L.lib.dho2g_extract_ese(c.h, st.h, 3, 0, C.byref(h))):
+                h = C.c_void_p()
+                try:
+                    check(call(h))
+                except d.DivergenceError as e:
+                    msgs.append(str(e))
+        finally:
+            c.set_option("hash_checks", 0)
+        return st.iterations, ese.eigvals.copy(), msgs
+
+    out = run_ranks(2, fn)
+    assert out[0][0] == out[1][0] == m
+    assert (out[0][1] == out[1][1]).all()
+    for _, _, msgs in out:
+        assert len(msgs) == 2
+        assert "B diverged across ranks" in msgs[0] and "B differs across ranks" in msgs[1]
+
+
+@pytest.mark.parametrize("kind", ["dho2", "sgd"])
+def test_trainer_debug_hash_checks_two_ranks(kind):
+    from oracle.bindings import blobs_dataset
+    sizes = [12, 10, 3]
+    X, y = blobs_dataset(96, 12, 3, seed=2)
+
+    def fn(c, rank, hook):
+        mlp = d.MlpOracle(c, sizes)
+        w = mlp.init_params(1)
+        cfg = d.TrainerConfig(kind=kind, base=d.BaseConfig("adam"), k=3, l=0, outer_rounds=2, inner_epochs=1,
+                              epochs=2, batch_size=16, curvature_batch=32, seed=3, debug_hash_checks=True)
+        tr = d.Trainer(c, cfg, mlp, d.Dataset(X, y, 3, 7), w, workers=2)
+        if hook:
+            c.set_option("hash_checks", 2)
+        try:
+            tr.run()
+            return tr.params().copy()
+        except d.DivergenceError as e:
+            return str(e)
+        finally:
+            c.set_option("hash_checks", 0)
+
+    out = run_ranks(2, lambda c, r: fn(c, r, False))
+    assert (out[0] == out[1]).all()
+    out = run_ranks(2, lambda c, r: fn(c, r, True))
+    # (the refresh's B check comes first in a DHO2 run; a first-order run reaches the epoch-end parameter check)
+    want = "diverged across ranks" if kind == "dho2" else "parameter replicas diverged at epoch"
+    assert all(isinstance(o, str) and want in o for o in out)
