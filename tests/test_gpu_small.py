@@ -29,7 +29,11 @@ def kernels_of(ctx, fn):
 CASES = [([784, 256, 10], 128, "tanh", "softmax_ce", 10), ([784, 256, 10], 512, "relu", "softmax_ce", 10),
          ([20, 16, 12, 5], 37, "tanh", "mse", 5), ([13, 24, 1], 1, "tanh", "mse", 0),
          ([64, 96, 96, 96, 10], 200, "relu", "mse", 10), ([33, 70, 41, 7], 65, "tanh", "softmax_ce", 7),
-         ([5, 2, 3], 300, "tanh", "softmax_ce", 3)]
+         ([5, 2, 3], 300, "tanh", "softmax_ce", 3),
+         ([20, 16, 40], 50, "tanh", "mse", 40),            # output wider than a tile: separate output phase
+         ([30, 40, 33], 70, "relu", "softmax_ce", 33),
+         ([12] + [9] * 7 + [4], 45, "tanh", "softmax_ce", 4),  # L = 8, the deepest small-path model
+         ([3000, 24, 10], 64, "relu", "softmax_ce", 10)]   # long K (input 3000) on the first layer
 
 
 @pytest.mark.parametrize("sizes,B,act,loss,ncls", CASES)
@@ -66,6 +70,22 @@ def test_small_path_vs_checker_and_tensor_path(ctx, port, sizes, B, act, loss, n
         ctx.set_option("mlp_small", 1)
     assert not any(k.startswith("mlp_small") for k in ks_t)
     assert rel_l2(hv_t, hv) < 1e-4 and rel_l2(g_t, g) < 1e-4
+    mlp.close()
+
+
+def test_small_path_depth_limit(ctx, port):
+    """Models deeper than the small path supports (L > 8) take the tensor-core path, with the same results."""
+    from oracle.bindings import blobs_dataset
+    sizes = [12] + [9] * 8 + [4]
+    X, y = blobs_dataset(40, 12, 4, seed=5)
+    mlp = d.MlpOracle(ctx, sizes)
+    w = port.mlp_init(sizes, 2)
+    v = port.rng_normal(4, len(w))
+    b = d.Batch(X, y, 4)
+    (hv, g), ks = kernels_of(ctx, lambda: (mlp.hvp(w, v, b), mlp.grad(w, b)))
+    assert not any(k.startswith("mlp_small") for k in ks)
+    assert rel_l2(hv, port.mlp_hvp(sizes, w, v, X, y, 4, 0, 0)) < 1e-4
+    assert rel_l2(g, port.mlp_grad(sizes, w, X, y, 4, 0, 0)) < 1e-4
     mlp.close()
 
 
