@@ -30,7 +30,7 @@ constexpr int TM = 128;  // rows per tile (UMMA M)
 
 constexpr uint32_t CB = TM * 32 * 4;  // one staged K-chunk: 128 rows x 32 basis columns fp32 (16 KB)
 constexpr int kMaxStages = 8;
-constexpr int kMaxSlots = 4;
+constexpr int kMaxSlots = 2;
 
 struct Geo {
   int KP, NP;  // padded K (= me, multiple of 32) and N (= r, 32 or 64)
@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(512, 1)
                    const __grid_constant__ CUtensorMap mUl, Geo g, int r, size_t rows, float* __restrict__ V,
                    size_t ldv, int ntiles) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned, derived from smem_raw by pointer arithmetic so that the compiler keeps the shared
+  // address space (LDS / STS instead of generic loads and stores in the split)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t UB = g.ubytes();
   const int NCS = g.NCS, NSL = g.NSL;
   uint8_t* stg0 = smem;               // [NCS] K-chunk stages, [32 k][128 rows] fp32 (TMA, no swizzle)
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(512, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NCS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&sfree[s], 8);
+      mbar_init(&sfree[s], 4);  // one split group (4 warps) per chunk
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(512, 1)
     }
     mbar_init(ufull, 1);
     for (int c = 0; c < kMaxSlots; ++c) {
-      mbar_init(&hready[c], 8);
+      mbar_init(&hready[c], 4);
       mbar_init(&hfree[c], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -175,28 +177,30 @@ __global__ void __launch_bounds__(512, 1)
                    : "memory");
     }
   } else if (warp >= 4 && warp < 12) {
-    // ---------------- transpose-split: 8 warps, thread = (row m, half of each K-chunk's 16-byte slots)
+    // ---------------- transpose-split: two groups of 4 warps take alternate chunks (two chunks in flight),
+    // thread = row m, all 8 16-byte slots of the chunk's 128-byte row
     const int q = threadIdx.x - 128;  // 0..255
-    const int m = q & 127;
-    const int c0 = (q >> 7) * 4;      // slots c0 .. c0+3 of each 128-byte row
+    const int grp = q >> 7, m = q & 127;
     const uint32_t rowoff = (uint32_t)(m >> 3) * 1024u + (uint32_t)(m & 7) * 128u;
     uint32_t it = 0;
     for (int t = t0; t < t1; ++t) {
       for (int kc = 0; kc < nkc; ++kc, ++it) {
+        if ((int)(it & 1) != grp) continue;
         const uint32_t s = it % NCS, h = it % NSL;
         mbar_wait(&full[s], (it / NCS) & 1);
         const float* stg = reinterpret_cast<const float*>(stg0 + s * CB);
         mbar_wait(&hfree[h], ((it / NSL) & 1) ^ 1);  // the MMAs of this slot's previous chunk are done
+        float x[32];
 #pragma unroll
-        for (int c = c0; c < c0 + 4; ++c) {
-          const int k0 = c * 4;  // within the staged chunk
-          const float x0 = stg[(k0 + 0) * TM + m], x1 = stg[(k0 + 1) * TM + m];
-          const float x2 = stg[(k0 + 2) * TM + m], x3 = stg[(k0 + 3) * TM + m];
-          const float4 hi = make_float4(rn_tf32(x0), rn_tf32(x1), rn_tf32(x2), rn_tf32(x3));
+        for (int k = 0; k < 32; ++k) x[k] = stg[k * TM + m];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 hi = make_float4(rn_tf32(x[4 * c]), rn_tf32(x[4 * c + 1]), rn_tf32(x[4 * c + 2]),
+                                        rn_tf32(x[4 * c + 3]));
           const uint32_t off = h * CB + rowoff + (uint32_t)((c ^ (m & 7)) * 16);
           *reinterpret_cast<float4*>(Ah + off) = hi;
-          *reinterpret_cast<float4*>(Al + off) =
-              make_float4(rn_tf32(x0 - hi.x), rn_tf32(x1 - hi.y), rn_tf32(x2 - hi.z), rn_tf32(x3 - hi.w));
+          *reinterpret_cast<float4*>(Al + off) = make_float4(rn_tf32(x[4 * c] - hi.x), rn_tf32(x[4 * c + 1] - hi.y),
+                                                             rn_tf32(x[4 * c + 2] - hi.z), rn_tf32(x[4 * c + 3] - hi.w));
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
