@@ -157,6 +157,8 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
       ++g_graph_gen;  // baked into captured refresh graphs
     }
     else if (k == "hash_checks") ctx->hash_checks = (int)value;
+    else if (k == "upd_small") ctx->upd_small = (int)value;
+    else if (k == "upd_small_max_rows") ctx->upd_small_max_rows = value;
     else if (k == "lanczos_small") {
       ctx->lanczos_small = (int)value;
       ++g_graph_gen;

@@ -67,6 +67,8 @@ struct dho2g_ctx {
   int mlp_small = 1;      // MLP passes of small models (HVP <= mlp_small_mflop MFLOP) as one persistent CUDA-core
                          // launch each (mlp_small.cu) instead of the tcgen05 GEMM sequence
   double mlp_small_mflop = 2000.0;
+  int upd_small = 1;  // world 1, r <= 32, rows <= upd_small_max_rows: the update's three passes as one launch
+  double upd_small_max_rows = 4e6;
   int lanczos_small = 1;  // world 1, small MLP operator (2: also diagonal), m <= 512: the whole refresh as one launch
   double lanczos_small_max_n = 4e6;
   int mlp_small_ctas_per_sm = 1;
@@ -505,6 +507,8 @@ struct dho2g_opt {
   dho2g::DevBuf<double> part, rank1, rank2, all1, all2;
   dho2g::DevBuf<unsigned> ticket;
   dho2g::DevBuf<int> bad;  // non-finite gradient flag
+  dho2g::DevBuf<unsigned long long> sbar;  // small-n fused update: grid-barrier words
+  int sbar_nb = 0;
 };
 
 namespace dho2g {

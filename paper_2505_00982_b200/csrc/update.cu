@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "internal.h"
+#include "coop.cuh"
 
 using namespace dho2g;
 
@@ -445,6 +446,146 @@ __global__ void __launch_bounds__(kT, MINB) upd_p2_tma_kernel(const __grid_const
   finish_partials(acc, R, part, rankp, ticket);
 }
 
+// ---- small n (world 1, r <= 32): P1, P2 and P3 as ONE cooperative launch. Each CTA owns a contiguous slice of
+// rows (rs rows, float4 groups g = tid + kT q); the r-length reductions are per-CTA partial rows + a grid
+// barrier + the fixed-order cross-CTA sum that every CTA performs (reduce_rows): no tickets, no launches
+// between the passes. Same per-element arithmetic as upd_p1 / upd_p2 / upd_p3 (c in fp64 products of
+// g~ = g + pi formed in fp64; V^T s as fp32 4-term products summed in fp64).
+constexpr int kSmallR = 32;
+__global__ void __launch_bounds__(kT) upd_small_kernel(const float* __restrict__ V, size_t ldv, int R, size_t rows,
+                                                       int rs, const float* __restrict__ g, const float* __restrict__ pi,
+                                                       const float* __restrict__ w, BaseHyper hp, float* __restrict__ m,
+                                                       float* __restrict__ v, float* __restrict__ s_out,
+                                                       const double* __restrict__ eigvals, double alpha, double sigma,
+                                                       double fl, float* __restrict__ w_a, float* __restrict__ newton_out,
+                                                       float* __restrict__ base_out, double* part1, double* part2,
+                                                       unsigned long long* bar, int* bad) {
+  __shared__ double c[kSmallR], sc[kSmallR], nbv[kSmallR];
+  __shared__ double sacc[kW * kSmallR];
+  __shared__ unsigned long long bar_next;
+  const unsigned nb = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) bar_next = 0ull;
+  const size_t r0 = (size_t)blockIdx.x * rs, r1 = min(rows, r0 + (size_t)rs);
+  const int ng = r1 > r0 ? (int)((r1 - r0 + 3) / 4) : 0;
+  const bool need_m = hp.kind != 0, need_v = hp.kind >= 2, need_w = hp.kind == 3;
+  auto cta_row = [&](const double (&acc)[kSmallR], double* part) {  // warp sums -> this CTA's partial row
+#pragma unroll
+    for (int j = 0; j < kSmallR; ++j) {
+      if (j >= R) break;
+      const double t = warp_sum(acc[j]);
+      if (lane == 0) sacc[warp * kSmallR + j] = t;
+    }
+    __syncthreads();
+    if (tid < R) {
+      double t = 0.0;
+      for (int q = 0; q < kW; ++q) t += sacc[q * kSmallR + tid];
+      __stcg(part + (size_t)blockIdx.x * kSmallR + tid, t);
+    }
+  };
+  // ---- P1: c = V^T (g + pi)
+  {
+    double acc[kSmallR];
+#pragma unroll
+    for (int j = 0; j < kSmallR; ++j) acc[j] = 0.0;
+    for (int q = tid; q < ng; q += kT) {
+      const size_t r = r0 + 4 * (size_t)q;
+      const float4 x = ld4(g, r, rows);
+      double g0 = x.x, g1 = x.y, g2 = x.z, g3 = x.w;
+      if (pi) {
+        const float4 p = ld4(pi, r, rows);
+        g0 += p.x; g1 += p.y; g2 += p.z; g3 += p.w;
+      }
+#pragma unroll
+      for (int j = 0; j < kSmallR; ++j) {
+        if (j >= R) break;
+        const float4 d = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
+        acc[j] = fma((double)d.x, g0, acc[j]);
+        acc[j] = fma((double)d.y, g1, acc[j]);
+        acc[j] = fma((double)d.z, g2, acc[j]);
+        acc[j] = fma((double)d.w, g3, acc[j]);
+      }
+    }
+    cta_row(acc, part1);
+  }
+  grid_barrier(bar, nb, &bar_next);
+  reduce_rows<kT>(part1, (int)nb, kSmallR, R, sacc, c);
+  // ---- P2: g2 = g~ - V c, base step, s; sc partials = V^T s
+  int local_bad = 0;
+  {
+    double acc[kSmallR];
+#pragma unroll
+    for (int j = 0; j < kSmallR; ++j) acc[j] = 0.0;
+    for (int q = tid; q < ng; q += kT) {
+      const size_t r = r0 + 4 * (size_t)q;
+      const float4 x = ld4(g, r, rows);
+      double g0 = x.x, g1 = x.y, g2 = x.z, g3 = x.w;
+      if (pi) {
+        const float4 p = ld4(pi, r, rows);
+        g0 += p.x; g1 += p.y; g2 += p.z; g3 += p.w;
+      }
+      float4 d[kSmallR];
+#pragma unroll
+      for (int j = 0; j < kSmallR; ++j)
+        if (j < R) d[j] = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
+#pragma unroll
+      for (int j = 0; j < kSmallR; ++j) {
+        if (j >= R) break;
+        const double cj = c[j];
+        g0 -= (double)d[j].x * cj; g1 -= (double)d[j].y * cj; g2 -= (double)d[j].z * cj; g3 -= (double)d[j].w * cj;
+      }
+      const float4 gm = make_float4((float)g0, (float)g1, (float)g2, (float)g3);
+      if (!isfinite(gm.x) || !isfinite(gm.y) || !isfinite(gm.z) || !isfinite(gm.w)) local_bad = 1;
+      float4 mm = need_m ? ld4(m, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 vm = need_v ? ld4(v, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 ww = need_w ? ld4(w, r, rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 sv;
+      sv.x = base_step(hp, gm.x, mm.x, vm.x, ww.x);
+      sv.y = r + 1 < rows ? base_step(hp, gm.y, mm.y, vm.y, ww.y) : 0.f;
+      sv.z = r + 2 < rows ? base_step(hp, gm.z, mm.z, vm.z, ww.z) : 0.f;
+      sv.w = r + 3 < rows ? base_step(hp, gm.w, mm.w, vm.w, ww.w) : 0.f;
+      if (need_m) st4(m, r, rows, mm);
+      if (need_v) st4(v, r, rows, vm);
+      st4(s_out, r, rows, sv);
+#pragma unroll
+      for (int j = 0; j < kSmallR; ++j) {
+        if (j >= R) break;
+        acc[j] += (double)(d[j].x * sv.x + d[j].y * sv.y + d[j].z * sv.z + d[j].w * sv.w);  // fp32 4-term
+      }
+    }
+    if (local_bad) atomicOr(bad, 1);
+    cta_row(acc, part2);
+  }
+  grid_barrier(bar, nb, &bar_next);
+  reduce_rows<kT>(part2, (int)nb, kSmallR, R, sacc, sc);
+  if (tid < R) nbv[tid] = alpha * (c[tid] / floored_den(eigvals[tid], fl, sigma));
+  __syncthreads();
+  // ---- P3: w_a += (s - V sc) + (-V (alpha c / den))
+  for (int q = tid; q < ng; q += kT) {
+    const size_t r = r0 + 4 * (size_t)q;
+    const float4 s4 = ld4(s_out, r, rows);  // (this thread wrote it in P2)
+    double b0 = s4.x, b1 = s4.y, b2 = s4.z, b3 = s4.w, n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+#pragma unroll
+    for (int j = 0; j < kSmallR; ++j) {
+      if (j >= R) break;
+      const float4 d = __ldg(reinterpret_cast<const float4*>(V + (size_t)j * ldv + r));
+      const double a = sc[j], b = nbv[j];
+      b0 -= (double)d.x * a; b1 -= (double)d.y * a; b2 -= (double)d.z * a; b3 -= (double)d.w * a;
+      n0 -= (double)d.x * b; n1 -= (double)d.y * b; n2 -= (double)d.z * b; n3 -= (double)d.w * b;
+    }
+    const float4 bf = make_float4((float)b0, (float)b1, (float)b2, (float)b3);
+    const float4 nf = make_float4((float)n0, (float)n1, (float)n2, (float)n3);
+    if (newton_out) st4(newton_out, r, rows, nf);
+    if (base_out) st4(base_out, r, rows, bf);
+    if (w_a) {
+      float4 wv = ld4(w_a, r, rows);
+      wv.x += bf.x; wv.y += bf.y; wv.z += bf.z; wv.w += bf.w;  // trainer.cpp:240-241 order: base, then newton
+      wv.x += nf.x; wv.y += nf.y; wv.z += nf.z; wv.w += nf.w;
+      st4(w_a, r, rows, wv);
+    }
+  }
+}
+
 // ---- P3: w_a += base + newton (optionally materialized)
 __global__ void __launch_bounds__(kT) upd_p3_kernel(const float* __restrict__ V, size_t ldv, int R, size_t rows,
                                                     const float* __restrict__ s, const double* __restrict__ all1,
@@ -596,6 +737,36 @@ void split_update(dho2g_opt* o, const dho2g_ese* ese, const UpdateArgs& a) {
   const double* all2 = world > 1 ? o->all2.p : o->rank2.p;
   const double rb = 4.0 * (double)rows;  // algorithmic bytes per row-vector pass
   const bool adam = o->cfg.kind >= 2;
+  if (world == 1 && R > 0 && R <= kSmallR && ctx->upd_small && rows <= (size_t)ctx->upd_small_max_rows) {
+    // one cooperative launch for the three passes (small n: the three launches' fixed costs dominate)
+    ++o->t;
+    const BaseHyper hp = make_hyper(o->cfg, o->t);
+    const int nbk = ctx->sm_count;
+    const int rs = (int)round_up(cdiv(rows, (size_t)nbk), 4);
+    o->part.ensure((size_t)2 * nbk * kSmallR);
+    o->sbar.ensure_g((size_t)kBarShards * kBarStride);
+    if (o->sbar_nb != nbk) {
+      DHO2G_CUDA(cudaMemsetAsync(o->sbar.p, 0, o->sbar.n * sizeof(unsigned long long), st));
+      o->sbar_nb = nbk;
+    }
+    const float* wdec = a.w_decay ? a.w_decay : a.w_a;
+    double* p1 = o->part.p;
+    double* p2 = o->part.p + (size_t)nbk * kSmallR;
+    const double* ev = ese->ev_dev.p;
+    float* s_out = o->s.p;
+    unsigned long long* barp = o->sbar.p;
+    int* badp = o->bad.p;
+    void* args[] = {(void*)&V, (void*)&ldv, (void*)&R, (void*)&rows, (void*)&rs, (void*)&a.g, (void*)&a.pi,
+                    (void*)&wdec, (void*)&hp, (void*)&o->m.p, (void*)&o->v.p, (void*)&s_out, (void*)&ev,
+                    (void*)&a.alpha, (void*)&a.sigma, (void*)&a.floor, (void*)&a.w_a, (void*)&a.newton_out,
+                    (void*)&a.base_out, (void*)&p1, (void*)&p2, (void*)&barp, (void*)&badp};
+    const int k0 = ctx->kt_begin();
+    DHO2G_CUDA(cudaLaunchCooperativeKernel((void*)upd_small_kernel, dim3((unsigned)nbk), dim3(kT), args, 0, st));
+    DHO2G_LAUNCH();
+    ctx->kt_end(k0, "upd_small", rb * (3.0 * R + 5.0 + (a.pi ? 2 : 0) + (adam ? 4 : (o->cfg.kind == 1 ? 2 : 0)) +
+                                       (o->cfg.kind == 3 ? 1 : 0) + (a.w_a ? 2 : 0)));
+    return;
+  }
   if (R > 0) {
     const int k1 = ctx->kt_begin();
     upd_p1_kernel<<<gp, kT, smem_p1, st>>>(V, ldv, R, rows, a.g, a.pi,

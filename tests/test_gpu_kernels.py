@@ -422,10 +422,14 @@ def test_refresh_mlp_c1_eigenvalues(ctx, port):
 
 
 # ------------------------------------------------------------------------------------ update
+@pytest.mark.parametrize("fused", [1, 0], ids=["one-launch", "three-pass"])
 @pytest.mark.parametrize("kind", ["sgd", "momentum", "adam", "adamw"])
 @pytest.mark.parametrize("admm", [False, True])
-def test_deltas_vs_checker(ctx, port, kind, admm):
+def test_deltas_vs_checker(ctx, port, kind, admm, fused):
+    """The update passes (fused into one cooperative launch at small n, option upd_small; or the three
+    bandwidth passes) against the checker's BaseOptimizer / split_deltas sequence."""
     from oracle.bindings import base_cfg
+    ctx.set_option("upd_small", fused)
     n, r, T = 20000, 8, 4
     V = np.linalg.qr(port.rng_normal(1, n * r).reshape(n, r))[0]
     ev = np.array([50.0, 20.0, 7.0, 3.0, 1e-9, -1e-13, -2.0, 0.5])
@@ -442,6 +446,7 @@ def test_deltas_vs_checker(ctx, port, kind, admm):
         # update pass fed identical g, pi, w, V: per-element within 2e-6 of the vector's max (fp32)
         assert np.max(np.abs(dl.newton - nw_ref[t])) <= 2e-6 * np.max(np.abs(nw_ref[t]))
         assert np.max(np.abs(dl.base - bs_ref[t])) <= 5e-6 * np.max(np.abs(bs_ref[t]))
+    ctx.set_option("upd_small", 1)
 
 
 @pytest.mark.parametrize("n,r", [(4099, 33), (65537, 48), (3001, 50), (512, 1)])
