@@ -493,8 +493,8 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m);
 void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho2g_ese* ese);
 // Ritz vectors on the tensor cores (3xTF32, ritz_tc.cu); supported for r <= 64, me <= 96.
 bool ritz_tc_supported(int me, int r);
-void ritz_tc(dho2g_ctx* ctx, const float* D, size_t ldd, int me, const float* U, int r, float* V, size_t ldv,
-             size_t rows, DevBuf<float>& uscratch);
+void ritz_tc(dho2g_ctx* ctx, const float* D, size_t ldd, int me, const float* U, const float* sigma, int r, float* V,
+             size_t ldv, size_t rows, DevBuf<float>& uscratch);
 }  // namespace dho2g
 
 // ------------------------------------------------------------------------- optimizer / update

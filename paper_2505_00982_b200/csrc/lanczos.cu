@@ -1410,7 +1410,7 @@ void extract_ese_into(dho2g_ctx* ctx, dho2g_lanczos* lz, size_t k, size_t l, dho
   ctx->meter("vhat_partial", (int64_t)(lz->rows * r));  // V_hat stays row-sharded: no "vhat" assembly
   const int kr = ctx->kt_begin();
   if (ctx->ritz_tc && ritz_tc_supported(me, r)) {
-    ritz_tc(ctx, lz->D.p, lz->ldd, me, U.p, r, ese->V.p, ese->ldv, lz->rows, lz->xUs);
+    ritz_tc(ctx, lz->D.p, lz->ldd, me, U.p, &lz->st.p->sigma[0], r, ese->V.p, ese->ldv, lz->rows, lz->xUs);
   } else {
     for (int c0 = 0; c0 < r; c0 += RC) {
       const size_t sm = (size_t)me * RC * sizeof(float);
