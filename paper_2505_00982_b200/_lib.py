@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdho2gpu.so")
+LIB_PATH = os.environ.get("DHO2G_LIB") or os.path.join(_HERE, "libdho2gpu.so")  # override: A/B experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

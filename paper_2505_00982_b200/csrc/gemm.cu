@@ -1077,10 +1077,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const uint32_t ID = idesc_fmt(idesc(256, tile_cols<NT>(wk, n0), AMN, BMN), e.f16 != 0);
      for (int c0 = sg.k0; c0 < sg.k1; c0 += wk.chunk) {  // one accumulator per chunk
       const int c1 = min(sg.k1, c0 + wk.chunk);
-      // chunked: one accumulator (the other TMEM half holds the running sum); else double-buffered
-      const uint32_t nacc = wk.chunk < wk.nkb ? 1u : (uint32_t)ACC;
-      const uint32_t ab = uc % nacc;
-      mbar_wait_cluster(&tempty[ab], ((uc / nacc) & 1) ^ 1);
+      // double-buffered (a chunked accumulation keeps its running sum in the epilogue warps' registers)
+      const uint32_t ab = uc % ACC;
+      mbar_wait_cluster(&tempty[ab], ((uc / ACC) & 1) ^ 1);
       fence_after();
       const uint32_t acc_addr = tmem + ab * NT;
       for (int kb = c0; kb < c1; ++kb, ++it) {
@@ -1121,40 +1120,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     Cursor cur;
     cur.init(wk, worker);
     Seg sg;
-    const uint32_t nacc = wk.chunk < wk.nkb ? 1u : (uint32_t)ACC;  // chunked: TMEM half 1 = running sum
-    const uint32_t tsum = tmem + ((uint32_t)(ew * 32) << 16) + NT;
+    const uint32_t nacc = (uint32_t)ACC;
+    const int cbase = chalf * (NT / 2);
     while (cur.next(wk, sg)) {
       const int m0 = sg.mtile * 256 + (int)rank * BM, n0 = sg.ntile * NT;
       const int ncols = tile_cols<NT>(wk, n0);
-      // chunks before the last: running sum (TMEM) += chunk (round-to-nearest fp32), free the accumulator
+      // chunks before the last: running sum (this thread's row x 128 columns, in registers) += chunk
+      // (round-to-nearest fp32), then free the accumulator for the MMAs of the chunk after next. Columns
+      // past the MMA's N hold unused values.
       const int nchunks = (sg.k1 - sg.k0 + wk.chunk - 1) / wk.chunk;
-      for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
+      if (nchunks > 1) {
+        float rs[NT / 2];
+#pragma unroll
+        for (int j = 0; j < NT / 2; ++j) rs[j] = 0.f;
+        for (int c = 0; c + 1 < nchunks; ++c, ++uc) {
+          const uint32_t ab = uc % nacc;
+          mbar_wait(&tfull[ab], (uc / nacc) & 1);
+          fence_after();
+          const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT + (uint32_t)cbase;
+#pragma unroll
+          for (int q = 0; q < NT / 32; ++q) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tb + (uint32_t)(16 * q), r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rs[16 * q + j] += __uint_as_float(r[j]);
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_leader(&tempty[ab]);
+        }
+        // fold the running sum into the last chunk's accumulator: acc = last + sum
         const uint32_t ab = uc % nacc;
         mbar_wait(&tfull[ab], (uc / nacc) & 1);
         fence_after();
-        const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
-#pragma unroll 1
-        for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 32) {
-          if (c0 >= ncols) break;  // (MMA N is a multiple of 16; a 32-wide drain past it touches unused columns)
-          tmem_drain32(tb + (uint32_t)c0, tsum + (uint32_t)c0, c > 0);
+        const uint32_t tb = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT + (uint32_t)cbase;
+#pragma unroll
+        for (int q = 0; q < NT / 32; ++q) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tb + (uint32_t)(16 * q), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) + rs[16 * q + j];
+          tmem_st16(tb + (uint32_t)(16 * q), v);
         }
         tmem_wait_st();
-        fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_leader(&tempty[ab]);
       }
       const uint32_t ab = uc % nacc;
       mbar_wait(&tfull[ab], (uc / nacc) & 1);
       fence_after();
       if (trace && threadIdx.x == 128) trace[2] = gtimer();
       const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + ab * NT;
-      auto add_run = [&](int c0, float (&v)[16]) {  // + the earlier chunks
-        if (nchunks < 2) return;
-        float t[16];
-        tmem_ld16(tsum + (uint32_t)c0, t);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] += t[j];
-      };
       if (sg.k0 != 0) {
         // non-head segment (first of this worker): publish the raw partial
         float* p = ws + ((size_t)(sg.phase * wk.workers + worker) * 2 + rank) * PART_FLOATS + slot_off;
@@ -1163,7 +1180,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
-          add_run(c0, v);
           float* q = p + (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -1192,7 +1208,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
-          add_run(c0, v);
           for (int w2 = worker + 1; w2 <= wlast; ++w2) {
             const float* q = ws + ((size_t)(sbase + w2) * 2 + rank) * PART_FLOATS + slot_off +
                              (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
