@@ -39,7 +39,6 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kSub = 512;  // rows per warp work item (32 lanes x 4 float4)
 constexpr int kP2Unroll = 4;  // basis columns in flight per pass-2 thread (x 4 float4)
-constexpr int kGsGroup = 32;  // GS pass 1: CTA partial rows per first-level reduction group
 
 // ------------------------------------------------------------------ start vector
 // seeded_unit_gaussian (lanczos.cpp:18-26): Rng(seed*phi + 0x1234567).fill_normal, computed
@@ -188,39 +187,25 @@ __global__ void __launch_bounds__(kThreads) gs_pass1_kernel(const float* __restr
     for (int w = 0; w < kWarps; ++w) t += acc[w * rowlen + j];
     part[(size_t)blockIdx.x * stride + (j < nj ? j : goff + (j - nj))] = t;
   }
-  // Two-level fixed-order reduction of the CTA partial rows: the last CTA of each group of kGsGroup CTAs
-  // sums its group's rows (in CTA order) into a group row, the last group finisher sums the group rows (in
-  // group order). A single last CTA summing ~10^3 rows of up to 2m + 2 values read ~1.5 MB through one SM:
-  // a serial tail of tens of us per pass.
   __threadfence();
   __syncthreads();
-  const int G = (int)gridDim.x, grp = (int)blockIdx.x / kGsGroup, ngrp = (G + kGsGroup - 1) / kGsGroup;
-  const int b0 = grp * kGsGroup, b1 = min(G, b0 + kGsGroup);
-  if (threadIdx.x == 0) is_last = atomicAdd(ticket + 1 + grp, 1u) == (unsigned)(b1 - b0 - 1);
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  double* gpart = part + (size_t)G * stride;  // group rows after the CTA rows
-  for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
-    const int j = jj < nj ? jj : goff + (jj - nj);
-    double t = 0.0;
-#pragma unroll 8
-    for (int bb = b0; bb < b1; ++bb) t += __ldcg(part + (size_t)bb * stride + j);
-    gpart[(size_t)grp * stride + j] = t;
-  }
-  if (threadIdx.x == 0) ticket[1 + grp] = 0u;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == (unsigned)(ngrp - 1);
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
-    const int j = jj < nj ? jj : goff + (jj - nj);
-    double t = 0.0;
-#pragma unroll 8
-    for (int g = 0; g < ngrp; ++g) t += __ldcg(gpart + (size_t)g * stride + j);
-    rankp[j] = t;
+  if (rowlen <= 4 * kWarps) {  // few values: a warp per value, lanes over the CTA partials
+    for (int jj = warp; jj < rowlen; jj += kWarps) {
+      const int j = jj < nj ? jj : goff + (jj - nj);
+      const double t = warp_fold(part + j, (int)gridDim.x, (size_t)stride);
+      if (lane == 0) rankp[j] = t;
+    }
+  } else {  // many values (long bases): a thread per value, its chain over the partials in CTA order
+    for (int jj = threadIdx.x; jj < rowlen; jj += kThreads) {
+      const int j = jj < nj ? jj : goff + (jj - nj);
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += part[(size_t)b * stride + j];
+      rankp[j] = t;
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
@@ -1139,8 +1124,7 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
   const int g1 = ctx->sm_count * 8;  // upper bound of the one-wave grids (256-thread CTAs, <= 8 per SM)
   const int g2 = ctx->sm_count * 8;
   // per-CTA / per-rank partial rows: [r_0..r_i, ||h||^2] at 0, [G_0..G_{i-1}] at m + 2
-  // (+ pass 1's group rows, one per kGsGroup CTAs)
-  lz->part.alloc((size_t)(std::max(g1, g2) + g1 / kGsGroup + 1) * 2 * (m + 2) + 8);
+  lz->part.alloc((size_t)std::max(g1, g2) * 2 * (m + 2) + 8);
   lz->rankp.alloc(2 * (m + 2));
   lz->allp.alloc(2 * (m + 2) * ctx->world);
   const size_t smem1_max = (size_t)kWarps * (2 * m + 2) * sizeof(double);
@@ -1148,7 +1132,7 @@ void lanczos_alloc(dho2g_lanczos* lz, dho2g_ctx* ctx, size_t n, size_t m) {
     DHO2G_CUDA(cudaFuncSetAttribute(gs_pass1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1_max));
     DHO2G_CUDA(cudaFuncSetAttribute(gs_pass1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1_max));
   }
-  lz->ticket.alloc(2 + (size_t)g1 / kGsGroup + 1);  // [0] pass 1 final, [1 + g] pass 1 group g; pass 2 at the end
+  lz->ticket.alloc(2);
   // SlotMeter names of dist_lanczos.cpp:41-84 (logical slots; the basis is stored padded to ldd rows)
   ctx->meter("D_shard", (int64_t)(lz->rows * (m + 1)));
   ctx->meter("B", (int64_t)(2 * m + 1));
@@ -1219,7 +1203,7 @@ static void lanczos_enqueue(dho2g_lanczos* lz, dho2g_op* op, uint64_t s0, const 
       if (world > 1) ctx->allgather_f64(lz->rankp.p, lz->allp.p, stride, "all_reduce");
       ks = pass == 0 ? ctx->kt_begin() : -1;
       gs_pass2_kernel<<<g2, kThreads, smem2, st>>>(lz->D.p, lz->ldd, hsrc, Dn, active, ngroups, allp, world, stride,
-                                                    lz->part.p, lz->rankp.p, lz->ticket.p + lz->ticket.n - 1, lz->st.p, (int)i, pass,
+                                                    lz->part.p, lz->rankp.p, lz->ticket.p + 1, lz->st.p, (int)i, pass,
                                                     gram, goff);
       DHO2G_LAUNCH();
       ctx->kt_end(ks, "gs_pass2", gsb + 4.0 * (double)lz->rows);
