@@ -137,6 +137,7 @@ int dho2g_ctx_set_option(dho2g_ctx* ctx, const char* key, double value) {
     else if (k == "gemm_splits") ctx->gemm_splits = (int)value;
     else if (k == "gemm_cta") ctx->gemm_cta = (int)value;
     else if (k == "gemm_dp") ctx->gemm_dp = (int)value;
+    else if (k == "gemm_group") ctx->gemm_group = (int)value;
     else if (k == "gemm_min_kb") ctx->gemm_min_kb = (int)value;
     else if (k == "gemm_mm_tc1") ctx->gemm_mm_tc1 = (int)value;
     else if (k == "bwd_overlap") ctx->bwd_overlap = (int)value;

@@ -937,12 +937,23 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) 
 // A rows (a working set that fits L2; measured 9x operand re-reads from HBM on the gradient GEMMs with
 // stream-K over the whole space); the remaining tiles (about one wave) are stream-K: the
 // (tile, k-block) space is cut into W equal contiguous ranges.
+// Group mode (grp = mt > 1, no data-parallel part): the workers form workers / grp groups of grp pairs; a
+// group's pairs walk the same contiguous range of the (n-tile, k-block) space, pair `sub` of the group on
+// m-tile `sub`. The grp pairs that need a B slab (n, k) load it at about the same time, so it comes from
+// DRAM once and from L2 for the others (plain stream-K over (tile, k) puts the m-tiles of one column at
+// unrelated k offsets: the R-GEMMs re-read B ~4x from DRAM). A segment boundary splits tile (sub, n)
+// between groups g and g + 1, whose pair `sub` does the fix-up as in plain stream-K.
 struct Work {
   int mt, nt, nkb, workers, N, kseg, nround;  // nround: MMA N granularity (16; 128 for an MN-major B)
   int dp;                                      // data-parallel tiles
   int chunk;  // k-blocks per TMEM accumulation chunk (drained into an fp32 running sum); >= nkb: off
-  __device__ __forceinline__ long long sk_total() const { return (long long)(mt * nt - dp) * nkb; }
-  __device__ __forceinline__ long long begin(int /*phase*/, int w) const { return sk_total() * w / workers; }
+  int grp;    // pairs per group (1: plain stream-K)
+  __device__ __forceinline__ int groups() const { return workers / grp; }
+  __device__ __forceinline__ long long sk_total() const {
+    return grp > 1 ? (long long)nt * nkb : (long long)(mt * nt - dp) * nkb;
+  }
+  // start of group (plain: worker) g's stream-K range
+  __device__ __forceinline__ long long begin(int /*phase*/, int g) const { return sk_total() * g / groups(); }
 };
 struct Seg {
   int phase, tile, k0, k1;  // phase 0: data-parallel (tile = global index); 1: stream-K (tile = index after dp)
@@ -950,14 +961,15 @@ struct Seg {
 };
 // Iterates one worker's segments: its data-parallel tiles, then its stream-K range.
 struct Cursor {
-  int p, w, t;
+  int p, w, t, sub;
   long long a, end;
   __device__ __forceinline__ void init(const Work& wk, int worker) {
     w = worker;
     p = 0;
     t = worker;
-    a = wk.begin(1, w);
-    end = wk.begin(1, w + 1);
+    sub = worker % wk.grp;
+    a = wk.begin(1, worker / wk.grp);
+    end = wk.begin(1, worker / wk.grp + 1);
   }
   __device__ __forceinline__ bool next(const Work& wk, Seg& s) {
     int g;
@@ -975,6 +987,11 @@ struct Cursor {
       s.k0 = (int)(a - (long long)s.tile * wk.nkb);
       s.k1 = (int)((long long)s.k0 + (end - a) < wk.nkb ? s.k0 + (end - a) : wk.nkb);
       a += s.k1 - s.k0;
+      if (wk.grp > 1) {  // group mode: s.tile is the n-tile, the m-tile is this pair's place in its group
+        s.mtile = sub;
+        s.ntile = s.tile;
+        return true;
+      }
       g = wk.dp + s.tile;
     }
     s.mtile = g / wk.nt;
@@ -1193,22 +1210,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (threadIdx.x == 128) st_release(flags + (sg.phase * wk.workers + worker) * 2 + rank, ready);
       } else {
         // head segment: later segments of this tile are the first segments of workers worker+1, ...
+        // (group mode: the groups after this one, their pair of the same m-tile: worker + grp, + 2 grp, ...)
         const long long tile_end = (long long)(sg.tile + 1) * wk.nkb;
         const int sbase = sg.phase * wk.workers;
-        int wlast = worker;
+        const int gw = worker / wk.grp;
+        int glast = gw;
         if (sg.k1 < wk.nkb) {
-          while (wlast + 1 < wk.workers && wk.begin(sg.phase, wlast + 1) < tile_end) ++wlast;
+          while (glast + 1 < wk.groups() && wk.begin(sg.phase, glast + 1) < tile_end) ++glast;
           if (threadIdx.x == 128)
-            for (int w2 = worker + 1; w2 <= wlast; ++w2)
-              while (ld_acquire(flags + (sbase + w2) * 2 + rank) != ready) __nanosleep(64);
+            for (int g2 = gw + 1; g2 <= glast; ++g2)
+              while (ld_acquire(flags + (sbase + worker + (g2 - gw) * wk.grp) * 2 + rank) != ready) __nanosleep(64);
           epi_bar();
         }
+        const int wlast = worker + (glast - gw) * wk.grp;
 #pragma unroll 1
         for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
           if (c0 >= ncols) break;
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
-          for (int w2 = worker + 1; w2 <= wlast; ++w2) {
+          for (int w2 = worker + wk.grp; w2 <= wlast; w2 += wk.grp) {
             const float* q = ws + ((size_t)(sbase + w2) * 2 + rank) * PART_FLOATS + slot_off +
                              (size_t)((c0 - chalf * (NT / 2)) / 16) * (4 * 32 * 4);
 #pragma unroll
@@ -1271,6 +1291,12 @@ int launch(dho2g_ctx* ctx, const CUtensorMap* maps, Work wk, const OpOff& oa, co
   // turns the data-parallel part off)
   const long long waves = tiles / wk.workers;
   wk.dp = (ctx->gemm_dp && waves >= 2) ? (int)((waves - 1) * wk.workers) : 0;
+  wk.grp = 1;
+  if (ctx->gemm_group && waves < 2 && wk.mt > 1 && 2 * wk.mt <= wk.workers) {  // few m-tiles: group mode
+    wk.grp = wk.mt;
+    wk.workers -= wk.workers % wk.mt;
+    wk.dp = 0;
+  }
   // stream-K partial slots (2 schedule parts x workers x 2 CTAs)
   ctx->gemm_ws.ensure_g((size_t)2 * wk.workers * 2 * PART_MAX);
   ctx->gemm_flags.ensure_g((size_t)2 * wk.workers * 2 + 16);

@@ -46,6 +46,8 @@ struct dho2g_ctx {
   int gemm_splits = 0;   // 0 = automatic split-K for small-M GEMMs (single-CTA kernel)
   int gemm_cta = 0;      // tcgen05 kernel: 0 auto, 1 single-CTA 128x128 tiles, 2 CTA-pair 256x256 tiles
   int gemm_dp = 1;       // pair kernel: data-parallel waves before the stream-K remainder (0: all stream-K)
+  int gemm_group = 1;    // pair kernel, few m-tiles (the HVP's M = 1024): m-tile groups of pairs walk the same
+                         // (n, k) ranges, so each B slab is read from DRAM once (0: plain stream-K)
   int gemm_mm_tc1 = 0;   // auto: short-K MN-major x MN-major GEMMs on the single-CTA kernel (off: measured slower since the
                          // compile-time epilogues)
   int gemm_min_kb = 4;   // pair kernel: minimum k-blocks per CTA pair (caps the worker count of small GEMMs)
