@@ -1430,16 +1430,18 @@ int dho2g_test_collectives_graph(dho2g_ctx* ctx, double* max_err) {
 int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_t n_ctas) {
   return guard([&] {
     check_ctx(ctx);
-    // on: 1 arms the pair kernel's trace (4 stamps per CTA), 2 the single-CTA kernel's (8 stamps per CTA);
-    // 0 disarms both and copies the buffer out
+    // on: 1 arms the pair kernel's trace (8 stamps per CTA: [0] start, [1] last MMA issued, [2] last segment's
+    // accumulator ready, [3] end, [4] head fix-up wait done, [5] head epilogue done), 3 / 4 the same for
+    // R-forward / R-backward launches only; 2 the single-CTA kernel's (8 stamps per CTA); 0 disarms all and
+    // copies the buffer out
     static DevBuf<unsigned long long> buf;
     if (on) {
-      buf.alloc(n_ctas * (on == 2 ? 8 : 4));
+      buf.alloc(n_ctas * 8);
       if (on == 2) gemm_trace1_set(buf.p);
-      else gemm_trace_set(buf.p);
+      else gemm_trace_set(buf.p, on >= 3 ? on - 2 : 0);
     } else {
       DHO2G_CUDA(cudaStreamSynchronize(ctx->stream));
-      gemm_trace_set(nullptr);
+      gemm_trace_set(nullptr, 0);
       gemm_trace1_set(nullptr);
       if (out && buf.p)
         DHO2G_CUDA(cudaMemcpy(out, buf.p, std::min(n_ctas * 8, buf.n) * sizeof(unsigned long long),

@@ -193,8 +193,55 @@ __device__ __forceinline__ float epi_elem_t(const Epi& e, int row, int col, floa
 // the layer epilogues restage the block through shared memory (sm: 32 x 17 floats) so that their
 // row-major inputs / outputs / bf16 pairs are coalesced, and write the transposed pair from the
 // lane = row layout.
+// The layer epilogues' inputs of a 32 x 16 block (lane: rows row0 + 2 it + lane / 16, column col0 + lane % 16),
+// loaded apart from the math so a caller can have them in flight with its accumulator reads.
+template <int MODE>
+__device__ __forceinline__ void epi_load_block(const Epi& e, int row0, int col0, EpiIn (&in)[16]) {
+  if (MODE == EPI_STORE) return;
+  const int lane = threadIdx.x & 31;
+  const int col = col0 + (lane & 15);
+#pragma unroll
+  for (int it = 0; it < 16; ++it) {
+    const int row = row0 + 2 * it + (lane >> 4);
+    if (row < e.M && col < e.N) in[it] = epi_load_t<MODE>(e, row, col);
+  }
+}
+// L2 prefetch of one lane's row of a 32 x 128 epilogue block's inputs (4 lines of 128 bytes per array)
+template <int MODE>
+__device__ __forceinline__ void epi_prefetch_row(const Epi& e, int row, int col0) {
+  if (MODE == EPI_STORE || row >= e.M) return;
+  auto pf = [&](const float* base) {
+    if (!base) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (col0 + 32 * q < e.N)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)row * e.N + col0 + 32 * q));
+  };
+  if (MODE == EPI_FWD) {
+    if (!e.do0) pf(e.a_in);
+  } else if (MODE == EPI_BWD) {
+    pf(e.a_in);
+    if (e.do1) {
+      pf(e.u_in);
+      if (!e.relu) pf(e.ra_in);
+    }
+  }
+}
+
+// mx_out: the lane's max |x| is folded into *mx_out instead of a per-block atomicMax on e.amax (the caller
+// publishes one max per CTA: ~10^4 same-address atomics per launch serialised at the end of the R-GEMMs)
+template <int MODE>
+__device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc_in)[16], float* sm,
+                                             const EpiIn (&in)[16], float* mx_out = nullptr);
 template <int MODE>
 __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc_in)[16], float* sm) {
+  EpiIn in[16];
+  if (MODE != EPI_STORE) epi_load_block<MODE>(e, row0, col0, in);
+  epi_warp16_t<MODE>(e, row0, col0, acc_in, sm, in);
+}
+template <int MODE>
+__device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, const float (&acc_in)[16], float* sm,
+                                             const EpiIn (&in)[16], float* mx_out) {
   const int lane = threadIdx.x & 31;
   float acc[16];
   const float inv = acc_unscale(e);
@@ -244,13 +291,6 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
   __syncwarp();
   const int rr = lane >> 4, cc = lane & 15;
   const int col = col0 + cc;
-  // all loads of the 32x16 block first (one memory latency per block, not one per row pair)
-  EpiIn in[16];
-#pragma unroll
-  for (int it = 0; it < 16; ++it) {
-    const int row = row0 + 2 * it + rr;
-    if (row < e.M && col < e.N) in[it] = epi_load_t<MODE>(e, row, col);
-  }
   float mx = 0.f;
 #pragma unroll
   for (int it = 0; it < 16; ++it) {
@@ -261,7 +301,10 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
     sm[rl * 17 + cc] = x;
     mx = fmaxf(mx, fabsf(x));
   }
-  if (e.amax) amax_warp(e, mx);
+  if (e.amax) {
+    if (mx_out) *mx_out = fmaxf(*mx_out, mx);
+    else amax_warp(e, mx);
+  }
   __syncwarp();
   if (e.csum && row0 < e.M && lane < 16 && col0 + lane < e.N) {  // column sums of this 32-row block (rows >= M hold 0)
     float t = 0.f;
@@ -885,6 +928,8 @@ namespace tc2 {
 // ns at [0] start of work (after the prologue), [1] last MMA issued (leader), [2] start of the last
 // segment's epilogue work, [3] end, per CTA slot blockIdx.x.
 __device__ unsigned long long* g_gemm_trace = nullptr;
+// which launches write it: 0 all, 1 R-forward (EPI_FWD, R half), 2 R-backward (EPI_BWD, R half)
+__device__ int g_gemm_trace_filter = 0;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1013,6 +1058,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                      OpOff oa, OpOff ob, const __grid_constant__ Epi e, float* __restrict__ ws,
                      unsigned* __restrict__ flags, unsigned ready) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ float s_mx[8];  // epilogue warps' max |x| (one e.amax update per CTA and tile)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -1058,7 +1104,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // may overlap the previous kernel's tail; no global memory is touched before the previous grid has
   // completed and flushed (a no-op when launched without the attribute).
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  unsigned long long* trace = g_gemm_trace ? g_gemm_trace + (size_t)blockIdx.x * 4 : nullptr;
+  const int tf = g_gemm_trace_filter;
+  const bool traced = tf == 0 || (tf == 1 && MODE == EPI_FWD && e.do1) || (tf == 2 && MODE == EPI_BWD && e.do1);
+  unsigned long long* trace = (g_gemm_trace && traced) ? g_gemm_trace + (size_t)blockIdx.x * 8 : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -1146,6 +1194,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       // (round-to-nearest fp32), then free the accumulator for the MMAs of the chunk after next. Columns
       // past the MMA's N hold unused values.
       const int nchunks = (sg.k1 - sg.k0 + wk.chunk - 1) / wk.chunk;
+      // a head segment runs the layer epilogue: its inputs into L2 while the last chunk's MMAs run
+      const bool head = sg.k0 == 0;
+      if (head && nchunks == 1) epi_prefetch_row<MODE>(e, m0 + ew * 32 + lane, n0 + cbase);
       if (nchunks > 1) {
         float rs[NT / 2];
 #pragma unroll
@@ -1168,6 +1219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (lane == 0) arrive_leader(&tempty[ab]);
         }
         // fold the running sum into the last chunk's accumulator: acc = last + sum
+        if (head) epi_prefetch_row<MODE>(e, m0 + ew * 32 + lane, n0 + cbase);
         const uint32_t ab = uc % nacc;
         mbar_wait(&tfull[ab], (uc / nacc) & 1);
         fence_after();
@@ -1222,10 +1274,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               while (ld_acquire(flags + (sbase + worker + (g2 - gw) * wk.grp) * 2 + rank) != ready) __nanosleep(64);
           epi_bar();
         }
+        if (trace && threadIdx.x == 128) trace[4] = gtimer();
         const int wlast = worker + (glast - gw) * wk.grp;
+        float wmx = 0.f;  // this lane's max |x| over the tile (e.amax)
 #pragma unroll 1
         for (int c0 = chalf * (NT / 2); c0 < (chalf + 1) * (NT / 2); c0 += 16) {
           if (c0 >= ncols) break;
+          // the block's epilogue inputs in flight together with the accumulator and partial reads
+          EpiIn in[16];
+          epi_load_block<MODE>(e, m0 + ew * 32, n0 + c0, in);
           float v[16];
           tmem_ld16(tbase + (uint32_t)c0, v);
           for (int w2 = worker + wk.grp; w2 <= wlast; w2 += wk.grp) {
@@ -1237,8 +1294,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               v[4 * j] += t.x; v[4 * j + 1] += t.y; v[4 * j + 2] += t.z; v[4 * j + 3] += t.w;
             }
           }
-          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
+          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm, in, &wmx);
         }
+        if (MODE != EPI_STORE && e.amax) {  // one atomicMax per CTA and tile
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) wmx = fmaxf(wmx, __shfl_xor_sync(0xffffffffu, wmx, o));
+          if (lane == 0) s_mx[warp - 4] = wmx;
+          epi_bar();
+          if (threadIdx.x == 128) {
+            float m = s_mx[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) m = fmaxf(m, s_mx[q]);
+            if (m > 0.f) atomicMax(e.amax, __float_as_uint(m));
+          }
+          epi_bar();  // s_mx is rewritten by the next tile's epilogue
+        }
+        if (trace && threadIdx.x == 128) trace[5] = gtimer();
         fence_before();
         __syncwarp();
         if (lane == 0) arrive_leader(&tempty[ab]);
@@ -1427,8 +1498,9 @@ void gemm3_store(dho2g_ctx* ctx, int M, int N, int K, const bf16* Ahi, const bf1
 // Test hook (option gemm_trace): route the next pair-GEMM launches' per-CTA timelines into buf (4 u64 per
 // CTA slot); buf = nullptr switches tracing off.
 namespace dho2g {
-void gemm_trace_set(unsigned long long* buf) {
+void gemm_trace_set(unsigned long long* buf, int filter) {
   DHO2G_CUDA(cudaMemcpyToSymbol(tc2::g_gemm_trace, &buf, sizeof(buf)));
+  DHO2G_CUDA(cudaMemcpyToSymbol(tc2::g_gemm_trace_filter, &filter, sizeof(filter)));
 }
 void gemm_trace1_set(unsigned long long* buf) {
   DHO2G_CUDA(cudaMemcpyToSymbol(tc1::g_tc1_trace, &buf, sizeof(buf)));

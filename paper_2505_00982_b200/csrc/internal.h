@@ -487,7 +487,7 @@ void lanczos_run_into(dho2g_lanczos* lz, dho2g_op* op, uint64_t seed);
 void wait_stream(dho2g_ctx* ctx, cudaStream_t s);
 void nccl_call(dho2g_ctx* ctx, ncclResult_t r, const char* what);
 void nccl_settle(dho2g_ctx* ctx, const char* what);
-void gemm_trace_set(unsigned long long* buf);  // test hook (gemm.cu)
+void gemm_trace_set(unsigned long long* buf, int filter);  // test hook (gemm.cu)
 void gemm_trace1_set(unsigned long long* buf);  // the same for the single-CTA kernel (8 stamps per CTA)
 // out[0] = scale * <a, b> over rows (single CTA, deterministic)
 void dot_dev(cudaStream_t st, const float* a, const float* b, size_t rows, double scale, double* out);
