@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* tempty = tfull + ACC;    // [ACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + ACC);
   __shared__ int s_last;
+  __shared__ float s_mx1[8];  // epilogue warps' max |x| (one e.amax update per CTA)
   unsigned long long* trace = g_tc1_trace ? g_tc1_trace + (size_t)blockIdx.x * 8 : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = gtimer1();
 
@@ -707,6 +708,7 @@ __global__ void __launch_bounds__(384, 1)
     const int chalf = (warp - 4) >> 2;
     float* esm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256) + (warp - 4) * (32 * 17);
     uint32_t uc = 0;
+    float wmx = 0.f;  // this lane's max |x| over all its units (one e.amax update per CTA, at the end)
     const uint32_t tsum = tmem + ((uint32_t)(ew * 32) << 16) + SUM_COL;  // chunk running sum (TMEM)
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++uc) {
       int m0, n0, split, tile, kb0, kb1;
@@ -745,7 +747,9 @@ __global__ void __launch_bounds__(384, 1)
         for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 16) {
           float v[16];
           acc16(c0, v);
-          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
+          EpiIn in[16];
+          epi_load_block<MODE>(e, m0 + ew * 32, n0 + c0, in);
+          epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm, in, &wmx);
         }
         fence_before();
         __syncwarp();
@@ -803,9 +807,23 @@ __global__ void __launch_bounds__(384, 1)
             v[4 * q] += t.x; v[4 * q + 1] += t.y; v[4 * q + 2] += t.z; v[4 * q + 3] += t.w;
           }
         }
-        epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm);
+        EpiIn in[16];
+        epi_load_block<MODE>(e, m0 + ew * 32, n0 + c0, in);
+        epi_warp16_t<MODE>(e, m0 + ew * 32, n0 + c0, v, esm, in, &wmx);
       }
       if (threadIdx.x == 128) flags[tile] = 0u;  // ticket back to zero for the next launch
+    }
+    if (MODE != EPI_STORE && e.amax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wmx = fmaxf(wmx, __shfl_xor_sync(0xffffffffu, wmx, o));
+      if (lane == 0) s_mx1[warp - 4] = wmx;
+      epi_bar();
+      if (threadIdx.x == 128) {
+        float m = s_mx1[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) m = fmaxf(m, s_mx1[q]);
+        if (m > 0.f) atomicMax(e.amax, __float_as_uint(m));
+      }
     }
     if (trace && threadIdx.x == 128) trace[5] = gtimer1();
   }
