@@ -1472,12 +1472,12 @@ void gemm3x(dho2g_ctx* ctx, int M, int N, int K, int kseg, const GOp& A, const G
     gemm3_simt(ctx, M, N, K, kseg, A, B, e);
   } else {
     if (!ctx->encode_fn) fail(DHO2G_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    // CTA pairs (256-row tiles) for the big shapes; M <= 512 or K < 1024 run as 128 x 128 single-CTA tiles:
+    // CTA pairs (256-row tiles) for the big shapes; M <= 512 or K <= 1024 run as 128 x 128 single-CTA tiles:
     // with few 256 x 256 tiles per pair each pair ends on an exposed full-tile epilogue (C3, M = 512: fwdR 72 ->
     // 51 us, the weight blocks at K = 512 46 -> 38 us, 102 -> 118 steps/s; C4 keeps the pairs: 10.5 vs 9.3).
     // Short-K weight blocks with both operands MN-major can also take the single-CTA kernel (gemm_mm_tc1).
     const bool short_mm = A.mn_major && B.mn_major && K <= 2048 && ctx->gemm_mm_tc1;
-    pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 512 && K >= 1024 && !short_mm);
+    pair = ctx->gemm_cta == 2 || (ctx->gemm_cta == 0 && M > 512 && K > 1024 && !short_mm);
     splits = pair ? tc2::run(ctx, M, N, K, kseg, A, B, e) : tc1::run(ctx, M, N, K, kseg, A, B, e);
     pair_nt = pair ? tc2::NT : 0;
   }
