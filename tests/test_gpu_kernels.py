@@ -94,6 +94,29 @@ def test_gemm3_pair_dp_stream_k(ctx, M, N, K, dp):
     assert np.max(np.abs(c1 - exact) / scale) < 2e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 3584, 2048), (512, 2048, 4096), (768, 1000, 3000), (1000, 2500, 1536)])
+@pytest.mark.parametrize("group", [0, 1])
+def test_gemm3_pair_groups(ctx, M, N, K, group):
+    """CTA-pair kernel with few m-tiles: m-tile groups of pairs walking the same (n, k) ranges (group = 1,
+    one pair per m-tile, stream-K fix-up between groups) against plain stream-K (group = 0). Exact to
+    2e-5 of sum |a||b| and bitwise repeatable (ragged M and N included)."""
+    rng = np.random.default_rng(M + 3 * N + 7 * K + group)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    exact = A.astype(np.float64) @ B.astype(np.float64).T
+    scale = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64).T
+    ctx.set_option("gemm_cta", 2)
+    ctx.set_option("gemm_group", group)
+    try:
+        c1 = run_gemm(ctx, A, B, 0)
+        c2 = run_gemm(ctx, A, B, 0)
+    finally:
+        ctx.set_option("gemm_cta", 0)
+        ctx.set_option("gemm_group", 1)
+    assert (c1 == c2).all()
+    assert np.max(np.abs(c1 - exact) / scale) < 2e-5
+
+
 @pytest.mark.parametrize("M,N,K0,K1", [(256, 384, 130, 0), (300, 200, 100, 70), (700, 260, 64, 200),
                                        (1024, 512, 1024, 1024)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
