@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(128) split_pair_kernel(int B, int s, int P, co
                                                          const unsigned* __restrict__ mxr, float* __restrict__ sout,
                                                          float* sx, unsigned* ticket, bf16* __restrict__ Rh,
                                                          bf16* __restrict__ Rl) {
+  // launched as a programmatic dependent of the producing GEMM: nothing is read or written before that grid
+  // has completed (a no-op without the launch attribute)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   float mx = 0.f;
   if (mxx) mx = fmaxf(mx, __uint_as_float(*mxx));
   if (mxr) mx = fmaxf(mx, __uint_as_float(*mxr));
@@ -501,8 +504,19 @@ static void split_pair(dho2g_mlp* m, int B, int s, int P, const float* X, const 
   // one wave of resident blocks (12 of 128 threads per SM at this kernel's register count), rows strided
   const int gy = (int)std::max<size_t>(1, std::min<size_t>((size_t)B, std::max<size_t>(1, (size_t)ctx->sm_count * 12 / gx)));
   const size_t bi = (size_t)(sout - m->scl.p);  // this buffer's x-half scale and ticket
-  split_pair_kernel<<<dim3(gx, gy), 128, 0, ctx->stream>>>(B, s, P, X, idx, ldX, x32, rx32, mxx, mxr, sout,
-                                                          m->sclx.p + bi, m->sticket.p + bi, Rh, Rl);
+  // programmatic dependent launch (option gemm_pdl): the launch and block scheduling overlap the producing
+  // GEMM's tail; the kernel waits for that grid before touching memory
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(gx, gy);
+  cfg.blockDim = dim3(128);
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = ctx->gemm_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  DHO2G_CUDA(cudaLaunchKernelEx(&cfg, split_pair_kernel, B, s, P, X, idx, ldX, x32, rx32, mxx, mxr, sout,
+                                m->sclx.p + bi, m->sticket.p + bi, Rh, Rl));
   DHO2G_LAUNCH();
   // algorithmic bytes: rx always, x when this call may rewrite it (counted as written: an upper bound)
   ctx->kt_end(slot, "split_pair", (double)B * s * 8.0 * ((rx32 ? 1.0 : 0.0) + ((X || x32) && !rx32 ? 1.0 : 0.0)));
