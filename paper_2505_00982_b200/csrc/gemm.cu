@@ -196,7 +196,8 @@ __device__ __forceinline__ float epi_elem_t(const Epi& e, int row, int col, floa
 // Forward epilogues without a transposed or pair-split output: lane = row, its 16 consecutive columns with
 // vector loads and stores (64 contiguous bytes per row), no restage through shared memory.
 // (Measured: R-forward 146 -> 137 us at C4. The backward epilogues read three arrays and write column sums:
-// there lanes = rows cost 4x the L1 wavefronts of the restaged 2-row pattern and measured 5-23 % slower.)
+// there lanes = rows cost 4x the L1 wavefronts of the restaged 2-row pattern and measured 5-23 % slower; they
+// use 8-row x 16-byte vectors after the restage instead: R-backward 157-162 -> 147 us.)
 template <int MODE>
 __device__ __forceinline__ bool epi_lane_rows(const Epi& e, int col0) {
   return MODE == EPI_FWD && !e.Rh && !e.Th && !e.csum && col0 + 16 <= e.N && (e.N & 3) == 0;
@@ -207,6 +208,7 @@ __device__ __forceinline__ bool epi_lane_rows(const Epi& e, int col0) {
 template <int MODE>
 __device__ __forceinline__ void epi_load_block(const Epi& e, int row0, int col0, EpiIn (&in)[16]) {
   if (MODE == EPI_STORE || epi_lane_rows<MODE>(e, col0)) return;
+  if (MODE == EPI_BWD && !e.Rh && !e.Th && col0 + 16 <= e.N && (e.N & 3) == 0) return;  // (vector path)
   const int lane = threadIdx.x & 31;
   const int col = col0 + (lane & 15);
 #pragma unroll
@@ -256,6 +258,67 @@ __device__ __forceinline__ void epi_warp16_t(const Epi& e, int row0, int col0, c
   const float inv = acc_unscale(e);
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = acc_in[j] * inv;
+  if (MODE == EPI_BWD && !e.Rh && !e.Th && col0 + 16 <= e.N && (e.N & 3) == 0) {
+    // Backward: restage the accumulator block through shared memory, then lane = (row 8 q + lane / 4,
+    // columns 4 (lane % 4) .. + 3): 16-byte loads / stores of 8 rows x 64 bytes per instruction (4x fewer
+    // memory instructions than the scalar 2-row pattern, the same lines). Same per-element arithmetic as
+    // epi_elem_t.
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm[lane * 17 + j] = acc[j];
+    __syncwarp();
+    const int c4 = (lane & 3) * 4;
+    float mx = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rl = 8 * q + (lane >> 2), row = row0 + rl;
+      float xo[4] = {0.f, 0.f, 0.f, 0.f};
+      if (row < e.M) {
+        const size_t ei = (size_t)row * e.N + col0 + c4;
+        const float4 a4 = __ldg(reinterpret_cast<const float4*>(e.a_in + ei));
+        const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+        float ac[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ac[j] = sm[rl * 17 + c4 + j];
+        if (e.do0) {  // d = u act'(a)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) xo[j] = ac[j] * act_prime(e.relu, a[j]);
+          if (e.f0) *reinterpret_cast<float4*>(e.f0 + ei) = make_float4(xo[0], xo[1], xo[2], xo[3]);
+          if (e.u_out) *reinterpret_cast<float4*>(e.u_out + ei) = make_float4(ac[0], ac[1], ac[2], ac[3]);
+        } else {  // rd = ru act'(a) + u (-2 a ra) (tanh)
+          const float4 u4 = __ldg(reinterpret_cast<const float4*>(e.u_in + ei));
+          const float4 r4 = e.relu ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(reinterpret_cast<const float4*>(e.ra_in + ei));
+          const float u[4] = {u4.x, u4.y, u4.z, u4.w}, ra[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float ap = act_prime(e.relu, a[j]);
+            const float rap = (!e.relu && ap != 0.f) ? -2.f * a[j] * ra[j] : 0.f;
+            xo[j] = ac[j] * ap + u[j] * rap;
+          }
+          if (e.f1) *reinterpret_cast<float4*>(e.f1 + ei) = make_float4(xo[0], xo[1], xo[2], xo[3]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mx = fmaxf(mx, fabsf(xo[j]));
+      }
+      if (e.csum) {
+        __syncwarp();  // (every lane has read its accumulators of row rl before they are overwritten)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sm[rl * 17 + c4 + j] = xo[j];
+      }
+    }
+    if (e.amax) {
+      if (mx_out) *mx_out = fmaxf(*mx_out, mx);
+      else amax_warp(e, mx);
+    }
+    __syncwarp();
+    if (e.csum && row0 < e.M && lane < 16) {  // column sums of this 32-row block (rows >= M hold 0)
+      float t = 0.f;
+#pragma unroll 8
+      for (int rl = 0; rl < 32; ++rl) t += sm[rl * 17 + lane];
+      e.csum[(size_t)(row0 >> 5) * e.N + col0 + lane] = t;
+    }
+    __syncwarp();
+    return;
+  }
   if (MODE == EPI_FWD && epi_lane_rows<MODE>(e, col0)) {  // (the same per-element arithmetic as epi_elem_t)
     const int row = row0 + lane;
     float mx = 0.f;
