@@ -1431,9 +1431,9 @@ int dho2g_test_gemm_trace(dho2g_ctx* ctx, int on, unsigned long long* out, size_
   return guard([&] {
     check_ctx(ctx);
     // on: 1 arms the pair kernel's trace (8 stamps per CTA: [0] start, [1] last MMA issued, [2] last segment's
-    // accumulator ready, [3] end, [4] head fix-up wait done, [5] head epilogue done), 3 / 4 the same for
-    // R-forward / R-backward launches only; 2 the single-CTA kernel's (8 stamps per CTA); 0 disarms all and
-    // copies the buffer out
+    // accumulator ready, [3] end, [4] head fix-up wait done, [5] head epilogue done), 3 / 4 / 5 the same for
+    // R-forward / R-backward / store-epilogue launches only; 2 the single-CTA kernel's (8 stamps per CTA); 0
+    // disarms all and copies the buffer out
     static DevBuf<unsigned long long> buf;
     if (on) {
       buf.alloc(n_ctas * 8);

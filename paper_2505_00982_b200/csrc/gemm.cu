@@ -1061,7 +1061,7 @@ namespace tc2 {
 // ns at [0] start of work (after the prologue), [1] last MMA issued (leader), [2] start of the last
 // segment's epilogue work, [3] end, per CTA slot blockIdx.x.
 __device__ unsigned long long* g_gemm_trace = nullptr;
-// which launches write it: 0 all, 1 R-forward (EPI_FWD, R half), 2 R-backward (EPI_BWD, R half)
+// which launches write it: 0 all, 1 R-forward (EPI_FWD, R half), 2 R-backward (EPI_BWD, R half), 3 EPI_STORE
 __device__ int g_gemm_trace_filter = 0;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -1238,7 +1238,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   // completed and flushed (a no-op when launched without the attribute).
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tf = g_gemm_trace_filter;
-  const bool traced = tf == 0 || (tf == 1 && MODE == EPI_FWD && e.do1) || (tf == 2 && MODE == EPI_BWD && e.do1);
+  const bool traced = tf == 0 || (tf == 1 && MODE == EPI_FWD && e.do1) || (tf == 2 && MODE == EPI_BWD && e.do1) ||
+                      (tf == 3 && MODE == EPI_STORE);
   unsigned long long* trace = (g_gemm_trace && traced) ? g_gemm_trace + (size_t)blockIdx.x * 8 : nullptr;
   if (trace && threadIdx.x == 0) trace[0] = gtimer();
 

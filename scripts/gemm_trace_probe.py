@@ -1,7 +1,7 @@
 """Per-CTA timeline of one R-forward (or R-backward) pair-GEMM launch inside a C4 refresh (test hook
 dho2g_test_gemm_trace; %globaltimer). Investigation only.
 
-    python scripts/gemm_trace_probe.py [fwd|bwd]"""
+    python scripts/gemm_trace_probe.py [fwd|bwd|store]"""
 import ctypes as C
 import os
 import sys
@@ -25,7 +25,7 @@ d.lanczos_distributed(ctx, 2, op, mlp.dim(), 7).close()
 n = 148
 buf = (C.c_uint64 * (n * 8))()
 for rep in range(2):
-    _lib.lib.dho2g_test_gemm_trace(ctx.h, 3 if which == "fwd" else 4, None, n)
+    _lib.lib.dho2g_test_gemm_trace(ctx.h, {"fwd": 3, "bwd": 4, "store": 5}[which], None, n)
     d.lanczos_distributed(ctx, 2, op, mlp.dim(), 7).close()
     _lib.lib.dho2g_test_gemm_trace(ctx.h, 0, buf, n)
     t = np.array(buf[:], dtype=np.float64).reshape(n, 8)
